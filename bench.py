@@ -1,0 +1,359 @@
+"""Benchmark of the BASELINE.json metric on B200.
+
+Metric: "LSTM fwd+bwd target tokens/sec (6xBLSTM n=1000, T=60) at 1/2/4/8 B200
+vs CPU" (BASELINE.json).  One step = forward + backward (BPTT) of the
+Listing-1 encoder — 6 bidirectional LSTM layers, H = 1000, D0 = 620 (the
+embedding width, models.hpp:14), T = 60 — over one batch of synthetic
+sequences, plus, at N > 1, the data-parallel NCCL gradient all-reduce
+overlapped with BPTT.  tokens = valid (sequence, time) positions.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LSTM fwd+bwd target tokens/sec (6×BLSTM n=1000, T=60) at 1/2/4/8 B200 vs CPU"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("SL_BENCH_PREC", "fp32"))
+    ap.add_argument("--batch", type=int, default=256, help="sequences per GPU (weak scaling)")
+    ap.add_argument("--layers", type=int, default=6)
+    ap.add_argument("--hidden", type=int, default=1000)
+    ap.add_argument("--input", type=int, default=620)
+    ap.add_argument("--time", type=int, default=60)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def flops_per_token(L, D0, H):
+    """Algorithmic GEMM flops per token, fwd+bwd, both directions:
+    24 H (D + H) per layer-direction."""
+    return sum(2 * 24 * H * ((D0 if l == 0 else 2 * H) + H) for l in range(L))
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(args, steps=1):
+    """Time the reference's own CPU implementation of the path on this host.
+
+    oracle/_ref/libseqloom_ref32.so = the reference's tensor/tape/layers.cpp
+    compiled unmodified, driven through its public lstm_sequence + Tape::backward
+    (kind "reference"); if absent, the C restatement (kind "port").  Threads =
+    host cores (<= 64), each with its own Tape on a one-sequence batch shard (the
+    reference's data-parallel model); OpenBLAS at 1 thread per tape
+    (EIGEN_DONT_PARALLELIZE, reference core/CMakeLists.txt:31).
+
+    Bounded sample: the reference runs layers one after another, so one
+    sequence through the full 6xBLSTM stack costs 2 t(D0) + 2(L-1) t(2H), where
+    t(D) is one layer-direction fwd+bwd with input width D.  Each step times
+    one layer-direction of each distinct shape per thread (~10 s) and reports
+    threads * T / (2 t(D0) + 2 (L-1) t(2H)).
+    """
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    import oracle
+    L, H, D0, T = args.layers, args.hidden, args.input, args.time
+    try:
+        ref = oracle.Reference(32)
+        kind = "reference"
+    except FileNotFoundError:
+        ref = oracle.Restatement()
+        kind = "port"
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    rng = np.random.default_rng(0)
+    s = 1 / np.sqrt(H)
+    shapes = [D0, 2 * H]
+    params = {D: tuple(rng.uniform(-s, s, shp) for shp in ((D, 4 * H), (H, 4 * H), (4 * H,)))
+              for D in shapes}
+    xs = {D: rng.uniform(-1, 1, (1, T, D)) for D in shapes}
+    lens = np.full(1, T, np.int32)
+    dy = rng.uniform(-1, 1, (1, T, H))
+    times = []
+
+    def one(out):
+        tt = {}
+        for D in shapes:
+            W, R, b = params[D]
+            t0 = time.perf_counter()
+            if kind == "reference":
+                ref.sequence(xs[D], lens, W, R, b, 1, dy)
+            else:
+                ref.sequence_bwd(xs[D], lens, W, R, b, 1, dy)
+            tt[D] = time.perf_counter() - t0
+        out.append(tt)
+
+    rates = []
+    for _ in range(steps):
+        res = []
+        ths = [threading.Thread(target=one, args=(res,)) for _ in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] for r in res]
+        rates.append(threads * T / max(per_seq))
+    value = statistics.median(rates)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{threads} threads x 1 sequence (T={T}); per thread one fwd+bwd layer-direction "
+                      f"of each shape (D={D0}, D={2 * H}; H={H}) of the {L}xBLSTM stack, stack time = "
+                      f"2 t(D0) + {2 * (L - 1)} t(2H) (layers run sequentially in the reference); fp32 "
+                      f"reference build + scipy OpenBLAS 1 thread/tape; median of {steps}",
+            "seconds_per_step": max(per_seq)}
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1805_05225_b200 import lstm
+    from paper_1805_05225_b200.encoder import BLSTMEncoder
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
+    enc = BLSTMEncoder(L, B, T, D0, H, args.precision, dev)
+    enc.init_uniform(seed=1)
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1
+    lens = torch.full((B,), T, dtype=torch.int32, device=dev)
+    dy = torch.rand(B, T, 2 * H, device=dev, generator=g) * 2 - 1
+    lib = lstm.lib()
+    lib.sl_profile_enable.argtypes = [ctypes.c_int]
+    lib.sl_launch_count.restype = ctypes.c_ulonglong
+
+    class Entry(ctypes.Structure):
+        _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_int32), ("ms", ctypes.c_double),
+                    ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+    handles = []
+
+    def on_grads(l, bucket):
+        if world > 1:
+            handles.append(dist.all_reduce(bucket, async_op=True))
+
+    def step(xin):
+        enc.forward(xin, lens)
+        enc.backward(dy, on_layer_grads=on_grads)
+        while handles:
+            handles.pop().wait()
+
+    for _ in range(args.warmup):
+        step(x)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib.sl_profile_read(None, 0, 1)
+    lib.sl_profile_enable(1)
+    n0 = lib.sl_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step(x)
+        e1.record()
+        torch.cuda.synchronize()
+    lib.sl_profile_enable(0)
+    launches = (lib.sl_launch_count() - n0)
+    ms = e0.elapsed_time(e1)
+    entries = (Entry * 32)()
+    n = lib.sl_profile_read(entries, 32, 1)
+    phases = {e.name.decode(): {"calls": e.calls, "ms": e.ms, "flops": e.flops}
+              for e in entries[:n]}
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- end to end: host buffers through the public API, copies timed
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        lh = lens.cpu().pin_memory()
+        xd = torch.empty_like(x)
+        ld = torch.empty_like(lens)
+        loss_h = torch.empty((), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            ld.copy_(lh, non_blocking=True)
+            y = enc.forward(xd, ld)
+            loss = (y * dy).sum()  # L = sum(y . dy), so dL/dy = dy
+            loss_h.copy_(loss, non_blocking=True)
+            enc.backward(dy, on_layer_grads=on_grads)
+            while handles:
+                handles.pop().wait()
+            torch.cuda.current_stream().synchronize()  # the host reads the step's loss
+            return float(loss_h)
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * T * args.steps / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": xh.numel() * 4 + lh.numel() * 4, "d2h_bytes_per_step": 4,
+               "timing": "host wall clock, max over ranks"}
+    return dict(ms=ms_max, phases=phases, launches=int(launches), clocks=clocks.summary(),
+                e2e=e2e)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
+    cfg = {"workload": f"config4-encoder: {L}xBLSTM H={H} D0={D0} T={T} fwd+bwd (+DP grad "
+                       f"all-reduce at N>1)", "global_batch": B * world, "batch_per_gpu": B,
+           "seq_len": T, "hidden": H, "input_dim": D0, "layers": L, "directions": 2,
+           "parallelism": f"dp{world}", "seq_lens": "all = T",
+           "l2": "working set (weights 590 MB fp32 + activations) far exceeds the 126 MB L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu = cpu_reference(args, steps=max(1, args.steps))
+        print(json.dumps({"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f32", "data": "synthetic", "config": cfg, "impl": "reference",
+                          "cpu_baseline": {k: cpu[k] for k in ("kind", "cores", "sample", "value", "unit")},
+                          "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_ours(args, rank, world, local_rank)
+    tokens = world * B * T * args.steps
+    value = tokens / (r["ms"] / 1e3)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    # dominant kernel phase -> roofline
+    ph = r["phases"]
+    top = max(ph.items(), key=lambda kv: kv[1]["ms"]) if ph else (None, None)
+    roof = None
+    if top[0]:
+        name, e = top
+        per_launch_ms = e["ms"] / max(e["calls"], 1)
+        achieved = e["flops"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"
+                if peaks else "fallback 1400",
+                "share_of_step": e["ms"] / r["ms"],
+                "phases": {k: {"calls": v["calls"], "ms_per_call": v["ms"] / max(v["calls"], 1),
+                               "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+                           for k, v in ph.items()}}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
+           "data": "synthetic (x ~ U(-1,1), params ~ U(+-1/sqrt(H)), dy ~ U(-1,1))",
+           "config": cfg, "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
+           "roofline": roof,
+           "algorithmic_tflops": flops_per_token(L, D0, H) * B * world / (r["ms"] / args.steps / 1e3) / 1e12}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            out["cpu_baseline"] = cpu_reference(args, steps=1)
+        except Exception as exc:  # the baseline must never sink the GPU line
+            out["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

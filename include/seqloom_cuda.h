@@ -1,0 +1,136 @@
+/* seqloom_cuda.h — C ABI of the B200-native fused LSTM layer.
+ *
+ * This is the drop-in boundary for the reference's LSTM hot path:
+ *   seqloom::lstm_sequence(Tape&, W, R, b, xs, direction)   reference layers.hpp:17 / layers.cpp:8-37
+ *   Tape::lstm_step(W, R, b, x, h_prev, c_prev)              reference tape.hpp:123-129 / tape.cpp:1074-1222
+ * plus the fused bidirectional variant eval_layer builds for the Listing-1
+ * encoder (reference compiler.cpp:600-608: two lstm_sequence calls whose
+ * outputs feed concat_feature, tape.cpp:709-783).
+ *
+ * Conventions (all match the reference's layouts so no caller-side reshuffle
+ * is needed, reference tensor.hpp:21 canonical order, row-major):
+ *   x   [B, T, D]          fp32, batch-major, padded positions t >= len[b] ignored
+ *   y   [B, T, ndir*H]     fp32; direction d writes columns [d*H, (d+1)*H) — the
+ *                          concat_feature([fw, bw]) layout; padded positions are 0
+ *   W   [D, 4H]  R [H, 4H]  b [4H]   fp32, gate blocks (i | f | g | o)
+ *   seq_lens [B]           int32 in (0, T] (reference tensor.cpp:121-138)
+ *   h_last/c_last [ndir, B, H]  state after step len[b]-1 in processing order
+ * All data pointers are DEVICE pointers owned by the caller; pointer arrays
+ * (W[d], ...) are host arrays of device pointers, one per direction.
+ * Every call is asynchronous on `stream`.  No exception crosses the ABI: each
+ * entry point returns SL_OK or an error code, with a message retrievable by
+ * sl_last_error() (thread-local).  Gradient outputs follow the tape's
+ * GradBuffer::accumulate contract (reference tape.cpp:76-89) when
+ * `accumulate` != 0 (+=), else they are overwritten.
+ */
+#ifndef SEQLOOM_CUDA_H_
+#define SEQLOOM_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sl_stream_t; /* == cudaStream_t */
+
+enum sl_status {
+  SL_OK = 0,
+  SL_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument (layers.cpp:14-16) */
+  SL_ERR_SHAPE = 2,            /* reference: seqloom::ShapeError (tape.cpp:1092-1094) */
+  SL_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
+  SL_ERR_WORKSPACE = 4,        /* reserve / workspace too small */
+  SL_ERR_UNSUPPORTED = 5       /* e.g. not running on an sm_100 device */
+};
+
+enum sl_precision {
+  SL_PREC_FP32 = 0, /* fp32 semantics: rel. parity 1e-4 vs the fp32 reference */
+  SL_PREC_BF16 = 1  /* bf16 tensor-core operands, fp32 accumulate / cell state; rel. 2e-2 */
+};
+
+/* One LSTM layer, one or two directions over the same input. */
+typedef struct sl_lstm_layer {
+  int32_t batch;     /* B  */
+  int32_t time;      /* T  (max length; seq_lens[b] <= T) */
+  int32_t input_dim; /* D  */
+  int32_t hidden;    /* H  */
+  int32_t num_dirs;  /* 1, or 2 = bidirectional: dir 0 forward, dir 1 backward, run concurrently */
+  int32_t direction; /* num_dirs == 1: +1 or -1 (reference layers.cpp:14) */
+  int32_t precision; /* enum sl_precision */
+  int32_t flags;     /* reserved, must be 0 */
+} sl_lstm_layer;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sl_version(void);
+/* Last error message of the calling thread ("" when none). */
+const char* sl_last_error(void);
+
+/* Validate a descriptor: SL_OK, or the error (and message) fwd/bwd would raise. */
+int sl_lstm_layer_check(const sl_lstm_layer* layer);
+
+/* Bytes of the caller-owned buffer that carries saved activations from
+ * sl_lstm_layer_fwd to sl_lstm_layer_bwd (cuDNN "reserve space" semantics;
+ * pass NULL / 0 to fwd for inference: nothing is saved). */
+size_t sl_lstm_reserve_size(const sl_lstm_layer* layer);
+/* Bytes of per-call scratch needed by fwd and by bwd. */
+size_t sl_lstm_workspace_size(const sl_lstm_layer* layer);
+
+/* Forward of lstm_sequence over all directions (layers.cpp:8-37).
+ * h_last / c_last may be NULL. */
+int sl_lstm_layer_fwd(const sl_lstm_layer* layer, const float* x, const int32_t* seq_lens,
+                      const float* const* W, const float* const* R, const float* const* b,
+                      float* y, float* h_last, float* c_last, void* reserve,
+                      size_t reserve_bytes, void* workspace, size_t workspace_bytes,
+                      sl_stream_t stream);
+
+/* Backward (BPTT) of lstm_sequence: the adjoint of every tape record the
+ * reference's forward emits (tape.cpp:1142-1219 per step, plus the
+ * slice/stack/mask/reverse adjoints).  dy is [B, T, ndir*H]; dh_last and
+ * dc_last ([ndir, B, H]) may be NULL.  dx, dW[d], dR[d], db[d] may be NULL
+ * (not needed).  `reserve` must come from the matching fwd call. */
+int sl_lstm_layer_bwd(const sl_lstm_layer* layer, const float* x, const int32_t* seq_lens,
+                      const float* const* W, const float* const* R, const float* dy,
+                      const float* dh_last, const float* dc_last, float* dx, float* const* dW,
+                      float* const* dR, float* const* db, int accumulate, const void* reserve,
+                      size_t reserve_bytes, void* workspace, size_t workspace_bytes,
+                      sl_stream_t stream);
+
+/* Single step, Tape::lstm_step (tape.cpp:1074-1141): x [B, D], h0/c0 [B, H]
+ * -> h, c [B, H].  `saved` [B, 5H] fp32 (i, f, g, o, tanh c) may be NULL
+ * when no backward follows. */
+int sl_lstm_cell_fwd(int32_t batch, int32_t input_dim, int32_t hidden, int32_t precision,
+                     const float* x, const float* h0, const float* c0, const float* W,
+                     const float* R, const float* b, float* h, float* c, float* saved,
+                     sl_stream_t stream);
+
+/* Backward closure of lstm_step (tape.cpp:1142-1219).  gh / gc may be NULL
+ * (zero); any output may be NULL. */
+int sl_lstm_cell_bwd(int32_t batch, int32_t input_dim, int32_t hidden, int32_t precision,
+                     const float* x, const float* h0, const float* c0, const float* W,
+                     const float* R, const float* saved, const float* gh, const float* gc,
+                     float* dx, float* dh0, float* dc0, float* dW, float* dR, float* db,
+                     int accumulate, sl_stream_t stream);
+
+/* ---- measurement hooks (used by bench.py; off by default) -------------------
+ * When enabled, every internal kernel phase is bracketed by CUDA events on the
+ * stream it is launched on; sl_profile_read folds them into per-phase totals
+ * (name, calls, device ms, algorithmic flops / bytes).  Phase names:
+ *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
+ *   k5_cell_fwd, k5_cell_bwd */
+typedef struct sl_profile_entry {
+  char name[32];
+  int32_t calls;
+  double ms;
+  double flops;
+  double bytes;
+} sl_profile_entry;
+int sl_profile_enable(int enable);
+int sl_profile_read(sl_profile_entry* out, int max_entries, int reset);
+/* Number of this library's kernels launched so far (process-wide). */
+unsigned long long sl_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEQLOOM_CUDA_H_ */

@@ -1,0 +1,205 @@
+"""ORACLE — test infrastructure only.
+
+Loaders for the two CPU checkers of the LSTM hot path:
+
+* ``restatement()`` — ``_build/liblstm_oracle.so``: the plain-C fp64
+  restatement in ``lstm_oracle.c`` (each function cites the reference
+  file:line it follows).
+* ``reference(bits)`` — ``_ref/libseqloom_ref{32,64}.so``: the REFERENCE's own
+  ``tensor.cpp tape.cpp layers.cpp gradcheck.cpp`` compiled unmodified from
+  /root/reference plus ``ref_bridge.cpp`` (built by ``make -C oracle``; the
+  .so travels to the GPU box with the snapshot, /root/reference does not).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package.  The
+product (``paper_1805_05225_b200``) never does: it has no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_P = ctypes.POINTER
+_d = _P(ctypes.c_double)
+_i = _P(ctypes.c_int)
+
+
+def build(force: bool = False) -> None:
+    """Compile the restatement and, when /root/reference exists, the reference."""
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj"):
+        targets += ["ref", "ref-tests"]
+    subprocess.run(["make", "-C", HERE, "-j8"] + (["-B"] if force else []) + targets,
+                   check=True, stdout=subprocess.DEVNULL)
+
+
+def _ptr(a, typ=_d):
+    return None if a is None else a.ctypes.data_as(typ)
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Restatement:
+    """fp64 C restatement (oracle/lstm_oracle.c)."""
+
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "_build", "liblstm_oracle.so")
+        if not os.path.exists(path):
+            build()
+        self.lib = ctypes.CDLL(path)
+        L = self.lib
+        L.orc_lstm_sequence_fwd.argtypes = [ctypes.c_int] * 5 + [_d, _i, _d, _d, _d, _d, _d, _d]
+        L.orc_lstm_sequence_bwd.argtypes = [ctypes.c_int] * 5 + [_d, _i, _d, _d, _d, _d, _d, _d,
+                                                                 _d, _d, _d, _d]
+        L.orc_lstm_step_fwd.argtypes = [ctypes.c_int] * 3 + [_d] * 9
+        L.orc_lstm_step_bwd.argtypes = [ctypes.c_int] * 3 + [_d] * 14
+
+    def sequence_fwd(self, x, lens, W, R, b, direction):
+        B, T, D = x.shape
+        H = R.shape[0]
+        x, W, R, b = map(_f64, (x, W, R, b))
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        y = np.zeros((B, T, H))
+        hl = np.zeros((B, H))
+        cl = np.zeros((B, H))
+        self.lib.orc_lstm_sequence_fwd(B, T, D, H, direction, _ptr(x), _ptr(lens, _i), _ptr(W),
+                                       _ptr(R), _ptr(b), _ptr(y), _ptr(hl), _ptr(cl))
+        return y, hl, cl
+
+    def sequence_bwd(self, x, lens, W, R, b, direction, dy, dh_last=None, dc_last=None):
+        B, T, D = x.shape
+        H = R.shape[0]
+        x, W, R, b, dy, dh_last, dc_last = map(_f64, (x, W, R, b, dy, dh_last, dc_last))
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        dx = np.zeros((B, T, D))
+        dW = np.zeros((D, 4 * H))
+        dR = np.zeros((H, 4 * H))
+        db = np.zeros((4 * H,))
+        self.lib.orc_lstm_sequence_bwd(B, T, D, H, direction, _ptr(x), _ptr(lens, _i), _ptr(W),
+                                       _ptr(R), _ptr(b), _ptr(dy), _ptr(dh_last), _ptr(dc_last),
+                                       _ptr(dx), _ptr(dW), _ptr(dR), _ptr(db))
+        return dx, dW, dR, db
+
+    def step_fwd(self, x, h0, c0, W, R, b):
+        B, D = x.shape
+        H = R.shape[0]
+        x, h0, c0, W, R, b = map(_f64, (x, h0, c0, W, R, b))
+        h = np.zeros((B, H))
+        c = np.zeros((B, H))
+        sv = np.zeros((B, 5 * H))
+        self.lib.orc_lstm_step_fwd(B, D, H, _ptr(x), _ptr(h0), _ptr(c0), _ptr(W), _ptr(R),
+                                   _ptr(b), _ptr(h), _ptr(c), _ptr(sv))
+        return h, c, sv
+
+    def step_bwd(self, x, h0, c0, W, R, b, gh=None, gc=None):
+        B, D = x.shape
+        H = R.shape[0]
+        _, _, sv = self.step_fwd(x, h0, c0, W, R, b)
+        x, h0, c0, W, R, gh, gc = map(_f64, (x, h0, c0, W, R, gh, gc))
+        out = [np.zeros((B, D)), np.zeros((B, H)), np.zeros((B, H)), np.zeros((D, 4 * H)),
+               np.zeros((H, 4 * H)), np.zeros((4 * H,))]
+        self.lib.orc_lstm_step_bwd(B, D, H, _ptr(x), _ptr(h0), _ptr(c0), _ptr(W), _ptr(R),
+                                   _ptr(sv), _ptr(gh), _ptr(gc), *[_ptr(o) for o in out])
+        return tuple(out)  # dx, dh0, dc0, dW, dR, db
+
+
+class Reference:
+    """The reference implementation itself (oracle/_ref/libseqloom_ref{32,64}.so)."""
+
+    def __init__(self, bits: int = 64, path: str | None = None):
+        path = path or os.path.join(HERE, "_ref", f"libseqloom_ref{bits}.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} missing: build it with `make -C oracle ref` where /root/reference exists")
+        self.lib = ctypes.CDLL(path, mode=ctypes.RTLD_LOCAL)
+        L = self.lib
+        c = ctypes.c_char_p
+        L.ref_real_bytes.restype = ctypes.c_int
+        L.ref_lstm_sequence.argtypes = [ctypes.c_int] * 5 + [_d, _i] + [_d] * 9 + [c, ctypes.c_int]
+        L.ref_lstm_step.argtypes = [ctypes.c_int] * 3 + [_d] * 16 + [c, ctypes.c_int]
+        L.ref_blstm_stack.argtypes = ([ctypes.c_int] * 5 + [_d, _i, _P(_d), _d, _d, _d, _P(_d)] +
+                                      [c, ctypes.c_int])
+        self.bits = 8 * L.ref_real_bytes()
+
+    @staticmethod
+    def _check(rc, err):
+        if rc != 0:
+            raise RuntimeError(err.value.decode())
+
+    def sequence(self, x, lens, W, R, b, direction, dy=None):
+        """Returns y, and (dx, dW, dR, db) when dy is given (else None)."""
+        B, T, D = x.shape
+        H = R.shape[0]
+        x, W, R, b, dy = map(_f64, (x, W, R, b, dy))
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        y = np.zeros((B, T, H))
+        g = None
+        if dy is not None:
+            g = (np.zeros((B, T, D)), np.zeros((D, 4 * H)), np.zeros((H, 4 * H)), np.zeros(4 * H))
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_lstm_sequence(B, T, D, H, direction, _ptr(x), _ptr(lens, _i), _ptr(W),
+                                        _ptr(R), _ptr(b), _ptr(dy), _ptr(y),
+                                        *([_ptr(a) for a in g] if g else [None] * 4), err, 512)
+        self._check(rc, err)
+        return y, g
+
+    def step(self, x, h0, c0, W, R, b, gh=None, gc=None):
+        B, D = x.shape
+        H = R.shape[0]
+        x, h0, c0, W, R, b, gh, gc = map(_f64, (x, h0, c0, W, R, b, gh, gc))
+        h = np.zeros((B, H))
+        c = np.zeros((B, H))
+        grad = gh is not None or gc is not None
+        g = [np.zeros((B, D)), np.zeros((B, H)), np.zeros((B, H)), np.zeros((D, 4 * H)),
+             np.zeros((H, 4 * H)), np.zeros(4 * H)] if grad else None
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_lstm_step(B, D, H, _ptr(x), _ptr(h0), _ptr(c0), _ptr(W), _ptr(R),
+                                    _ptr(b), _ptr(gh), _ptr(gc), _ptr(h), _ptr(c),
+                                    *([_ptr(a) for a in g] if g else [None] * 6), err, 512)
+        self._check(rc, err)
+        return h, c, (tuple(g) if g else None)
+
+    def blstm_stack(self, x, lens, params, dy=None):
+        """params: list over layers of (W_fw, R_fw, b_fw, W_bw, R_bw, b_bw)."""
+        B, T, D0 = x.shape
+        L = len(params)
+        H = params[0][1].shape[0]
+        flat = [_f64(p) for layer in params for p in layer]
+        parr = (_d * len(flat))(*[_ptr(p) for p in flat])
+        x, dy = _f64(x), _f64(dy)
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        y = np.zeros((B, T, 2 * H))
+        dx = np.zeros_like(x) if dy is not None else None
+        grads = [np.zeros_like(p) for p in flat] if dy is not None else None
+        garr = (_d * len(flat))(*[_ptr(g) for g in grads]) if grads else None
+        err = ctypes.create_string_buffer(512)
+        rc = self.lib.ref_blstm_stack(L, B, T, D0, H, _ptr(x), _ptr(lens, _i), parr, _ptr(dy),
+                                      _ptr(y), _ptr(dx), garr, err, 512)
+        self._check(rc, err)
+        if grads is not None:
+            grads = [tuple(grads[l * 6:(l + 1) * 6]) for l in range(L)]
+        return y, dx, grads
+
+
+def seeded_case(seed: int, B: int, T: int, D: int, H: int, ragged: bool = True,
+                wscale: float | None = None):
+    """Synthetic inputs as SURVEY §8(d): x ~ U(-1,1); W, R, b ~ U(+-1/sqrt(H));
+    ragged lens ~ U[ceil(T/2), T] with at least one full-length row."""
+    rng = np.random.default_rng(seed)
+    s = wscale if wscale is not None else 1.0 / np.sqrt(H)
+    x = rng.uniform(-1, 1, (B, T, D))
+    W = rng.uniform(-s, s, (D, 4 * H))
+    R = rng.uniform(-s, s, (H, 4 * H))
+    b = rng.uniform(-s, s, (4 * H,))
+    if ragged:
+        lens = rng.integers((T + 1) // 2, T + 1, size=B).astype(np.int32)
+        lens[0] = T
+    else:
+        lens = np.full(B, T, dtype=np.int32)
+    return x, lens, W, R, b

@@ -1,0 +1,91 @@
+"""The caller of the boundary for the BASELINE workload: an L-layer BLSTM encoder.
+
+Mirrors how the reference's executor drives the LSTM path for the Listing-1
+encoder: for every `rec` layer enc{l}_{fw,bw}, eval_layer's Rec branch
+concatenates the inputs (concat_feature) and calls lstm_sequence with the
+layer's `{q}/W, {q}/R, {q}/b` params (compiler.cpp:600-608, param names and
+shapes compiler.cpp:485-494, topology models.cpp).  Here each layer is ONE
+bidirectional sl_lstm_layer call (both directions concurrent) writing the
+[fw ‖ bw] concat in place, and all parameters / gradients live in flat device
+buffers so the data-parallel gradient all-reduce can run per layer bucket,
+overlapped with the BPTT of the layers below.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import lstm
+
+
+class BLSTMEncoder:
+    def __init__(self, num_layers: int, batch: int, time: int, input_dim: int, hidden: int,
+                 precision: str = "bf16", device=None):
+        self.L, self.B, self.T, self.D0, self.H = num_layers, batch, time, input_dim, hidden
+        self.precision = precision
+        self.device = torch.device(device or "cuda")
+        H = hidden
+        self.in_dims = [input_dim if l == 0 else 2 * H for l in range(num_layers)]
+        # flat parameter / gradient storage, one contiguous bucket per layer
+        self.layer_numel = [2 * (D * 4 * H + H * 4 * H + 4 * H) for D in self.in_dims]
+        total = sum(self.layer_numel)
+        self.params = torch.empty(total, dtype=torch.float32, device=self.device)
+        self.grads = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self.p_views, self.g_views, self.buckets = [], [], []
+        off = 0
+        for l, D in enumerate(self.in_dims):
+            n = self.layer_numel[l]
+            self.buckets.append(self.grads[off:off + n])
+            pv, gv = [], []
+            for _ in range(2):  # fw, bw
+                for shape in ((D, 4 * H), (H, 4 * H), (4 * H,)):
+                    k = 1
+                    for s in shape:
+                        k *= s
+                    pv.append(self.params[off:off + k].view(shape))
+                    gv.append(self.grads[off:off + k].view(shape))
+                    off += k
+            self.p_views.append(pv)
+            self.g_views.append(gv)
+        self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device)
+                       for D in self.in_dims]
+        self.acts = [torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
+                     for _ in range(num_layers)]
+        self.dxs = [torch.empty(batch, time, D, dtype=torch.float32, device=self.device)
+                    for D in self.in_dims]
+
+    def param_names(self):
+        """Reference naming (compiler.cpp:488-492): enc{l}_{fw,bw}/{W,R,b}."""
+        return [f"enc{l}_{d}/{n}" for l in range(self.L) for d in ("fw", "bw")
+                for n in ("W", "R", "b")]
+
+    def init_uniform(self, seed: int = 0):
+        """W, R, b ~ U(+-1/sqrt(H)) (SURVEY §8(d) synthetic inputs)."""
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        s = 1.0 / self.H ** 0.5
+        self.params.uniform_(-s, s, generator=g)
+
+    def _wrb(self, l):
+        v = self.p_views[l]
+        return [v[0], v[3]], [v[1], v[4]], [v[2], v[5]]
+
+    def forward(self, x, seq_lens, train: bool = True):
+        inp = x
+        for l in range(self.L):
+            W, R, b = self._wrb(l)
+            self.layers[l].forward(inp, seq_lens, W, R, b, y=self.acts[l], train=train)
+            inp = self.acts[l]
+        return inp
+
+    def backward(self, dy, on_layer_grads=None):
+        """BPTT from the top layer down; on_layer_grads(l, bucket) fires as soon
+        as layer l's gradients are complete (used to start its all-reduce)."""
+        g = dy
+        for l in reversed(range(self.L)):
+            gv = self.g_views[l]
+            dx, _, _, _ = self.layers[l].backward(
+                g, dx=self.dxs[l], dW=[gv[0], gv[3]], dR=[gv[1], gv[4]], db=[gv[2], gv[5]],
+                need_dx=True)
+            if on_layer_grads is not None:
+                on_layer_grads(l, self.buckets[l])
+            g = dx
+        return g

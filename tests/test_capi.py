@@ -1,0 +1,92 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol the public
+header declares, and validates descriptors with the reference's error
+behaviour — no compute calls (there is no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1805_05225_b200 import lstm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADERS = [os.path.join(ROOT, "include", "seqloom_cuda.h")]
+
+
+def declared_symbols():
+    names = set()
+    for h in HEADERS:
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*[A-Za-z_][\w\s\*]*?\b(sl_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ("sl_lstm_layer_fwd", "sl_lstm_layer_bwd", "sl_lstm_cell_fwd", "sl_lstm_cell_bwd",
+              "sl_lstm_reserve_size", "sl_lstm_workspace_size", "sl_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = lstm.lib()
+    for s in declared_symbols():
+        assert hasattr(L, s), f"{s} declared in include/ but not exported"
+
+
+def test_library_is_sm100a_only():
+    # the product library carries sm_100a SASS only (no PTX / other-arch fallback)
+    import subprocess
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lstm.LIB_PATH],
+                       capture_output=True, text=True)
+    assert r.returncode == 0
+    archs = set(re.findall(r"sm_(\d+a?)", r.stdout))
+    assert archs == {"100a"}, archs
+
+
+def desc(**kw):
+    d = dict(batch=4, time=5, input_dim=3, hidden=8, num_dirs=1, direction=1, precision=0,
+             flags=0)
+    d.update(kw)
+    return lstm._Layer(*[d[n] for n, _ in lstm._Layer._fields_])
+
+
+def test_valid_descriptor_and_sizes():
+    L = lstm.lib()
+    d = desc()
+    assert L.sl_lstm_layer_check(ctypes.byref(d)) == 0
+    r1 = L.sl_lstm_reserve_size(ctypes.byref(d))
+    w1 = L.sl_lstm_workspace_size(ctypes.byref(d))
+    assert r1 > 0 and w1 > 0
+    d2 = desc(num_dirs=2)
+    assert L.sl_lstm_reserve_size(ctypes.byref(d2)) >= 2 * r1 - 4096
+
+
+@pytest.mark.parametrize("kw,code,needle", [
+    (dict(direction=0), lstm.SL_ERR_INVALID_ARGUMENT, "direction must be +1 or -1"),
+    (dict(direction=2), lstm.SL_ERR_INVALID_ARGUMENT, "direction must be +1 or -1"),
+    (dict(time=0), lstm.SL_ERR_SHAPE, "Batch and Time"),
+    (dict(batch=-1), lstm.SL_ERR_SHAPE, "Batch and Time"),
+    (dict(num_dirs=3), lstm.SL_ERR_INVALID_ARGUMENT, "num_dirs"),
+    (dict(precision=7), lstm.SL_ERR_UNSUPPORTED, "precision"),
+])
+def test_descriptor_errors_match_reference(kw, code, needle):
+    # reference layers.cpp:10-16: ShapeError for missing axes, invalid_argument for direction
+    L = lstm.lib()
+    rc = L.sl_lstm_layer_check(ctypes.byref(desc(**kw)))
+    assert rc == code
+    assert needle in L.sl_last_error().decode()
+    assert L.sl_lstm_reserve_size(ctypes.byref(desc(**kw))) == 0
+
+
+def test_python_mirror_raises_like_reference():
+    import torch
+    x = torch.zeros(2, 3, 4)
+    with pytest.raises(ValueError, match="direction must be"):
+        lstm.lstm_sequence(x, torch.ones(2, dtype=torch.int32), torch.zeros(4, 8),
+                           torch.zeros(2, 8), torch.zeros(8), direction=0)
+    with pytest.raises(lstm.ShapeError):
+        lstm.lstm_sequence(torch.zeros(3, 4), torch.ones(2, dtype=torch.int32),
+                           torch.zeros(4, 8), torch.zeros(2, 8), torch.zeros(8), direction=1)

@@ -1,0 +1,240 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Tolerances (norm-wise max|gpu-ref| / max|ref| per tensor):
+  SL_PREC_FP32 : 1e-4   (north_star: "relative 1e-4 for the FP32/TF32 path")
+  SL_PREC_BF16 : 2e-2   (north_star: "a separately stated looser bound for BF16")
+References: the golden fixtures produced by the reference build
+(tests/golden/, make_golden.py) at small sizes; the fp64 torch restatement
+(oracle/torch_ref.py, pinned to the C restatement by tests/test_oracle.py) at
+BASELINE sizes; plus size-independent properties.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import torch_ref
+import oracle
+from paper_1805_05225_b200 import lstm
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+PRECS = ["fp32"]
+
+
+def rel(a, b):
+    a = torch.as_tensor(a).double().cpu()
+    b = torch.as_tensor(b).double().cpu()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def cu(a, dtype=torch.float32):
+    return torch.as_tensor(np.asarray(a)).to("cuda", dtype).contiguous()
+
+
+def run_layer(x, lens, params, nd, direction, prec, dy, dh=None, dc=None, accumulate_twice=False):
+    B, T, D = x.shape
+    H = params[0][1].shape[0]
+    layer = lstm.LSTMLayer(B, T, D, H, nd, direction, prec)
+    W = [p[0] for p in params]
+    R = [p[1] for p in params]
+    b = [p[2] for p in params]
+    y, hl, cl = layer.forward(x, lens, W, R, b)
+    dx, dW, dR, db = layer.backward(dy, dh, dc)
+    if accumulate_twice:
+        layer.backward(dy, dh, dc, dx=dx, dW=dW, dR=dR, db=db, accumulate=True)
+    torch.cuda.synchronize()
+    return dict(y=y, h_last=hl, c_last=cl, dx=dx, dW=dW, dR=dR, db=db)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name", ["config1_fw", "config1_bw", "t1_bw", "lens35_fw", "odd_bw"])
+def test_golden_sequence(cuda, name, prec):
+    f = np.load(os.path.join(GOLD, name + ".npz"))
+    d = int(f["direction"])
+    out = run_layer(cu(f["x"]), cu(f["lens"], torch.int32), [(cu(f["W"]), cu(f["R"]), cu(f["b"]))],
+                    1, d, prec, cu(f["dy"]))
+    tol = TOL[prec]
+    assert rel(out["y"], f["y_ref64"]) < tol
+    assert rel(out["dx"], f["dx_ref64"]) < tol
+    assert rel(out["dW"][0], f["dW_ref64"]) < tol
+    assert rel(out["dR"][0], f["dR_ref64"]) < tol
+    assert rel(out["db"][0], f["db_ref64"]) < tol
+    # padded outputs are exactly zero (tape.cpp:797-798)
+    lens = f["lens"]
+    y = out["y"].cpu().numpy()
+    for r, L in enumerate(lens):
+        assert np.all(y[r, L:] == 0.0)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_golden_bidirectional_stack(cuda, prec):
+    f = np.load(os.path.join(GOLD, "blstm2.npz"))
+    L = int(f["L"])
+    lens = cu(f["lens"], torch.int32)
+    x = cu(f["x"])
+    layers, inputs = [], [x]
+    for l in range(L):
+        B, T, D = inputs[-1].shape
+        H = f[f"R_fw_{l}"].shape[0]
+        layer = lstm.LSTMLayer(B, T, D, H, 2, 1, prec)
+        P = [[cu(f[f"{n}_{k}_{l}"]) for k in ("fw", "bw")] for n in ("W", "R", "b")]
+        y, _, _ = layer.forward(inputs[-1], lens, *P)
+        layers.append((layer, P))
+        inputs.append(y)
+    assert rel(inputs[-1], f["y_ref64"]) < TOL[prec]
+    g = cu(f["dy"])
+    for l in reversed(range(L)):
+        layer, P = layers[l]
+        dx, dW, dR, db = layer.backward(g)
+        for k, n in enumerate(("fw", "bw")):
+            assert rel(dW[k], f[f"dW_{n}_{l}_ref64"]) < TOL[prec]
+            assert rel(dR[k], f[f"dR_{n}_{l}_ref64"]) < TOL[prec]
+            assert rel(db[k], f[f"db_{n}_{l}_ref64"]) < TOL[prec]
+        g = dx
+    assert rel(g, f["dx_ref64"]) < TOL[prec]
+
+
+def _seeded(seed, B, T, D, H, ragged=True):
+    x, lens, W, R, b = oracle.seeded_case(seed, B, T, D, H, ragged=ragged)
+    return cu(x), cu(lens, torch.int32), cu(W), cu(R), cu(b)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("direction", [1, -1])
+def test_config2_full_size_vs_fp64(cuda, prec, direction):
+    # BASELINE configs[1]: H = D = 1024, B = 128, T = 60 (ragged lengths)
+    x, lens, W, R, b = _seeded(100 + direction, 128, 60, 1024, 1024)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    dy = torch.rand(128, 60, 1024, device="cuda", generator=g) * 2 - 1
+    dh = torch.rand(1, 128, 1024, device="cuda", generator=g) * 2 - 1
+    dc = torch.rand(1, 128, 1024, device="cuda", generator=g) * 2 - 1
+    out = run_layer(x, lens, [(W, R, b)], 1, direction, prec, dy, dh, dc)
+    ref = torch_ref.sequence(x, lens, W, R, b, direction, dy, dh[0], dc[0])
+    tol = TOL[prec]
+    assert rel(out["y"], ref["y"]) < tol
+    assert rel(out["h_last"][0], ref["h_last"]) < tol
+    assert rel(out["c_last"][0], ref["c_last"]) < tol
+    assert rel(out["dx"], ref["dx"]) < tol
+    assert rel(out["dW"][0], ref["dW"]) < tol
+    assert rel(out["dR"][0], ref["dR"]) < tol
+    assert rel(out["db"][0], ref["db"]) < tol
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_config3_layer_bidirectional_vs_fp64(cuda, prec):
+    # BASELINE configs[2] layer shapes: H = 1000, D0 = 620, both directions concurrent
+    B, T, D, H = 64, 60, 620, 1000
+    x, lens, _, _, _ = _seeded(7, B, T, D, H)
+    params = [_seeded(8 + k, 1, 1, D, H)[2:] for k in range(2)]
+    dy = torch.rand(B, T, 2 * H, device="cuda") * 2 - 1
+    out = run_layer(x, lens, params, 2, 1, prec, dy)
+    dx = 0
+    for k, d in enumerate((1, -1)):
+        W, R, b = params[k]
+        ref = torch_ref.sequence(x, lens, W, R, b, d, dy[:, :, k * H:(k + 1) * H])
+        assert rel(out["y"][:, :, k * H:(k + 1) * H], ref["y"]) < TOL[prec]
+        assert rel(out["dW"][k], ref["dW"]) < TOL[prec]
+        assert rel(out["dR"][k], ref["dR"]) < TOL[prec]
+        assert rel(out["db"][k], ref["db"]) < TOL[prec]
+        dx = dx + ref["dx"]
+    assert rel(out["dx"], dx) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_masked_inputs_cannot_leak(cuda, prec):
+    # tape_test.cpp:535-566 / SPEC.md:106: perturbing padded positions changes
+    # neither valid outputs nor gradients (bitwise)
+    x, lens, W, R, b = _seeded(9, 16, 24, 40, 48)
+    dy = torch.rand(16, 24, 2 * 48, device="cuda")
+    a = run_layer(x, lens, [(W, R, b)] * 2, 2, 1, prec, dy)
+    x2 = x.clone()
+    for r, L in enumerate(lens.tolist()):
+        x2[r, L:] = 123.5
+    dy2 = dy.clone()
+    for r, L in enumerate(lens.tolist()):
+        dy2[r, L:] = -7.0
+    c = run_layer(x2, lens, [(W, R, b)] * 2, 2, 1, prec, dy2)
+    assert torch.equal(a["y"], c["y"])
+    for k in ("dW", "dR", "db"):
+        for u, v in zip(a[k], c[k]):
+            assert torch.equal(u, v), k
+    valid = (torch.arange(24, device="cuda")[None] < lens[:, None])[..., None]
+    assert torch.equal(a["dx"] * valid, c["dx"] * valid)
+    assert torch.all(c["dx"][~valid.expand_as(c["dx"])] == 0)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_deterministic_bitwise(cuda, prec):
+    # tape_test.cpp:513-533: repeated runs are bitwise identical
+    x, lens, W, R, b = _seeded(10, 32, 20, 64, 96)
+    dy = torch.rand(32, 20, 96, device="cuda")
+    a = run_layer(x, lens, [(W, R, b)], 1, -1, prec, dy)
+    c = run_layer(x, lens, [(W, R, b)], 1, -1, prec, dy)
+    for k in ("y", "dx", "h_last", "c_last"):
+        assert torch.equal(a[k], c[k]), k
+    for k in ("dW", "dR", "db"):
+        assert torch.equal(a[k][0], c[k][0]), k
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_time1_both_directions_equal(cuda, prec):
+    # SPEC.md:316
+    x, lens, W, R, b = _seeded(11, 8, 1, 16, 32, ragged=False)
+    dy = torch.rand(8, 1, 32, device="cuda")
+    a = run_layer(x, lens, [(W, R, b)], 1, 1, prec, dy)
+    c = run_layer(x, lens, [(W, R, b)], 1, -1, prec, dy)
+    assert torch.equal(a["y"], c["y"])
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_backward_direction_is_rev_forward_rev(cuda, prec):
+    # dir -1 == reverse_per_seq . dir +1 . reverse_per_seq
+    x, lens, W, R, b = _seeded(12, 24, 33, 48, 64)
+    def rev(t):
+        out = t.clone()
+        for r, L in enumerate(lens.tolist()):
+            out[r, :L] = t[r, :L].flip(0)
+        return out
+    dy = torch.rand(24, 33, 64, device="cuda")
+    a = run_layer(x, lens, [(W, R, b)], 1, -1, prec, dy)
+    c = run_layer(rev(x), lens, [(W, R, b)], 1, 1, prec, rev(dy))
+    assert rel(a["y"], rev(c["y"])) < 1e-6
+    assert rel(a["dW"][0], c["dW"][0]) < 1e-5
+    assert rel(a["dx"], rev(c["dx"])) < 1e-5
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_accumulate_contract(cuda, prec):
+    # GradBuffer::accumulate (tape.cpp:76-89): accumulate=1 adds into existing grads
+    x, lens, W, R, b = _seeded(13, 8, 10, 12, 16)
+    dy = torch.rand(8, 10, 16, device="cuda")
+    once = run_layer(x, lens, [(W, R, b)], 1, 1, prec, dy)
+    twice = run_layer(x, lens, [(W, R, b)], 1, 1, prec, dy, accumulate_twice=True)
+    assert rel(twice["dx"], 2 * once["dx"]) < 1e-6
+    for k in ("dW", "dR", "db"):
+        assert rel(twice[k][0], 2 * once[k][0]) < 1e-6
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_lstm_step_golden(cuda, prec):
+    f = np.load(os.path.join(GOLD, "lstm_step.npz"))
+    z = lambda *s: torch.zeros(*s, device="cuda")
+    h, c, _ = lstm.lstm_step(z(1, 2), z(1, 3), torch.full((1, 3), 2.0, device="cuda"), z(2, 12),
+                             z(3, 12), z(12), prec)
+    assert rel(c, f["hand_c2_c"]) < 1e-6 and rel(h, f["hand_c2_h"]) < 1e-6
+    args = [cu(f["rand_" + k]) for k in ("x", "h0", "c0", "W", "R", "b")]
+    h, c, saved = lstm.lstm_step(*args, precision=prec)
+    assert rel(h, f["rand_h"]) < TOL[prec] and rel(c, f["rand_c"]) < TOL[prec]
+    g = lstm.lstm_step_backward(*args[:5], saved, cu(f["rand_gh"]), cu(f["rand_gc"]), prec)
+    for k, v in zip(("dx", "dh0", "dc0", "dW", "dR", "db"), g):
+        assert rel(v, f["rand_" + k]) < TOL[prec], k
+
+
+def test_lstm_sequence_functional_matches_layer(cuda):
+    x, lens, W, R, b = _seeded(14, 4, 6, 5, 7)
+    y = lstm.lstm_sequence(x, lens, W, R, b, -1)
+    ref = torch_ref.sequence(x, lens, W, R, b, -1)
+    assert rel(y, ref["y"]) < 1e-4
