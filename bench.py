@@ -343,7 +343,7 @@ def main():
            "data": "synthetic (x ~ U(-1,1), params ~ U(+-1/sqrt(H)), dy ~ U(-1,1))",
            "config": cfg, "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
            "roofline": roof,
-           "algorithmic_tflops": flops_per_token(L, D0, H) * B * world / (r["ms"] / args.steps / 1e3) / 1e12}
+           "algorithmic_tflops": flops_per_token(L, D0, H) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             out["cpu_baseline"] = cpu_reference(args, steps=1)
