@@ -1,0 +1,18 @@
+/* seqloom_cuda_internal.h — test / benchmarking hooks of libseqloom_cuda.so.
+ * Not part of the drop-in boundary (see seqloom_cuda.h); used by tests/ to
+ * check individual kernels against torch references. */
+#ifndef SEQLOOM_CUDA_INTERNAL_H_
+#define SEQLOOM_CUDA_INTERNAL_H_
+#include "seqloom_cuda.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C[M,N] = alpha * op(A) op(B) + beta * C + bias on the BF16 tcgen05 GEMM.
+ * A: a_mn ? [K, M] : [M, K] bf16 (lda);  B: b_mn ? [K, N] : [N, K] bf16 (ldb). */
+int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+                       int64_t ldb, int b_mn, float* C, int64_t ldc, float alpha, float beta,
+                       const float* bias, sl_stream_t stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

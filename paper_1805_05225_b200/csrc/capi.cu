@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "cell.h"
+#include "convert.h"
 #include "gemm.h"
 #include "profile.h"
 #include "recurrence.h"
@@ -53,7 +54,7 @@ void validate(const sl_lstm_layer* L) {
              "lstm_sequence: input needs Batch and Time axes, got B=" +
                  std::to_string(L->batch) + " T=" + std::to_string(L->time) +
                  " D=" + std::to_string(L->input_dim) + " H=" + std::to_string(L->hidden));
-  SL_REQUIRE(L->precision == SL_PREC_FP32, SL_ERR_UNSUPPORTED,
+  SL_REQUIRE(L->precision == SL_PREC_FP32 || L->precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
              "precision " + std::to_string(L->precision) + " not supported by this build");
   SL_REQUIRE(L->flags == 0, SL_ERR_INVALID_ARGUMENT, "sl_lstm_layer.flags must be 0");
 }
@@ -66,9 +67,24 @@ struct ReserveView {
   float* gates[2] = {nullptr, nullptr};
   float* cprev[2] = {nullptr, nullptr};
   float* hprev[2] = {nullptr, nullptr};
+  __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
+  __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
 };
 
-ReserveView carve_reserve(const Dims& d, void* p, size_t* bytes) {
+// Padded extents of the bf16 path (TMA needs 16 B aligned rows).
+struct Pad {
+  int64_t Dp, Hp, G4p, Gc;  // Gc = nd * G4p (concatenated gate columns)
+};
+Pad pads(const Dims& d) {
+  Pad p;
+  p.Dp = round_up(d.D, 8);
+  p.Hp = round_up(d.H, 8);
+  p.G4p = round_up(4 * (int64_t)d.H, 8);
+  p.Gc = d.nd * p.G4p;
+  return p;
+}
+
+ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   ReserveView r;
   for (int k = 0; k < d.nd; ++k) {
@@ -76,23 +92,43 @@ ReserveView carve_reserve(const Dims& d, void* p, size_t* bytes) {
     r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
     r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
   }
+  if (prec == SL_PREC_BF16) {
+    const Pad pd = pads(d);
+    r.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
+    r.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
+  }
   *bytes = c.off;
   return r;
 }
 
 struct FwdWork {
   float* xw[2] = {nullptr, nullptr};
+  int64_t xw_ld = 0;
   float* hbuf[2] = {nullptr, nullptr};
   float* cbuf[2] = {nullptr, nullptr};
+  float* bcat = nullptr;  // bf16 path: concatenated bias [nd*G4p]
+  __nv_bfloat16* xb = nullptr;    // bf16 inference (no reserve)
+  __nv_bfloat16* wcat = nullptr;
   unsigned* bar = nullptr;
 };
 
-FwdWork carve_fwd(const Dims& d, void* p, size_t* bytes) {
+FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   FwdWork w;
   w.bar = c.take<unsigned>(64);
+  if (prec == SL_PREC_BF16) {
+    const Pad pd = pads(d);
+    float* xw = c.take<float>((size_t)d.BT() * pd.Gc);
+    w.xw_ld = pd.Gc;
+    for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * pd.G4p : nullptr;
+    w.bcat = c.take<float>((size_t)pd.Gc);
+    w.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
+    w.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
+  } else {
+    w.xw_ld = 4 * d.H;
+    for (int k = 0; k < d.nd; ++k) w.xw[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
+  }
   for (int k = 0; k < d.nd; ++k) {
-    w.xw[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
     w.hbuf[k] = c.take<float>((size_t)2 * d.B * d.H);
     w.cbuf[k] = c.take<float>((size_t)d.B * d.H);
   }
@@ -104,10 +140,12 @@ struct BwdWork {
   float* dz[2] = {nullptr, nullptr};
   float* dzbuf[2] = {nullptr, nullptr};
   float* gcbuf[2] = {nullptr, nullptr};
+  __nv_bfloat16* dzb = nullptr;  // bf16 path: DZ of both directions [B*T, nd*G4p]
+  __nv_bfloat16* hpb = nullptr;  // bf16 path: Hprev of one direction [B*T, Hp]
   unsigned* bar = nullptr;
 };
 
-BwdWork carve_bwd(const Dims& d, void* p, size_t* bytes) {
+BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   BwdWork w;
   w.bar = c.take<unsigned>(64);
@@ -115,6 +153,11 @@ BwdWork carve_bwd(const Dims& d, void* p, size_t* bytes) {
     w.dz[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
     w.dzbuf[k] = c.take<float>((size_t)2 * d.B * 4 * d.H);
     w.gcbuf[k] = c.take<float>((size_t)d.B * d.H);
+  }
+  if (prec == SL_PREC_BF16) {
+    const Pad pd = pads(d);
+    w.dzb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
+    w.hpb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Hp);
   }
   *bytes = c.off;
   return w;
@@ -158,7 +201,7 @@ size_t sl_lstm_reserve_size(const sl_lstm_layer* L) {
   size_t bytes = 0;
   if (guarded([&] {
         validate(L);
-        carve_reserve(dims(L), nullptr, &bytes);
+        carve_reserve(dims(L), L->precision, nullptr, &bytes);
       }) != SL_OK)
     return 0;
   return bytes;
@@ -168,8 +211,8 @@ size_t sl_lstm_workspace_size(const sl_lstm_layer* L) {
   size_t f = 0, b = 0;
   if (guarded([&] {
         validate(L);
-        carve_fwd(dims(L), nullptr, &f);
-        carve_bwd(dims(L), nullptr, &b);
+        carve_fwd(dims(L), L->precision, nullptr, &f);
+        carve_bwd(dims(L), L->precision, nullptr, &b);
       }) != SL_OK)
     return 0;
   return std::max(f, b);
@@ -184,18 +227,49 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     validate(L);
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
     const Dims d = dims(L);
+    const int prec = L->precision;
     SL_REQUIRE(x && seq_lens && W && R && b && y, SL_ERR_INVALID_ARGUMENT,
                "sl_lstm_layer_fwd: null pointer argument");
+    for (int k = 0; k < d.nd; ++k)
+      SL_REQUIRE(W[k] && R[k] && b[k], SL_ERR_INVALID_ARGUMENT,
+                 "sl_lstm_layer_fwd: null weight pointer");
     size_t need_w = 0, need_r = 0;
-    FwdWork w = carve_fwd(d, workspace, &need_w);
+    FwdWork w = carve_fwd(d, prec, workspace, &need_w);
     SL_REQUIRE(workspace && workspace_bytes >= need_w, SL_ERR_WORKSPACE,
                "sl_lstm_layer_fwd: workspace too small");
     ReserveView rv;
     if (reserve) {
-      rv = carve_reserve(d, reserve, &need_r);
+      rv = carve_reserve(d, prec, reserve, &need_r);
       SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_fwd: reserve too small");
     }
     SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 64 * sizeof(unsigned), stream));
+    const double k1_flops = 2.0 * d.BT() * d.D * 4.0 * d.H * d.nd;
+    if (prec == SL_PREC_BF16) {
+      // Pack [W_fw | W_bw] and x to bf16 (kept in the reserve for the backward
+      // GEMMs), then K1 for both directions as ONE tcgen05 GEMM.
+      const Pad pd = pads(d);
+      __nv_bfloat16* xb = rv.xb ? rv.xb : w.xb;
+      __nv_bfloat16* wcat = rv.wcat ? rv.wcat : w.wcat;
+      if (pd.G4p != 4 * d.H) {
+        SL_CUDA_TRY(cudaMemsetAsync(wcat, 0, sizeof(__nv_bfloat16) * d.D * pd.Gc, stream));
+        SL_CUDA_TRY(cudaMemsetAsync(w.bcat, 0, sizeof(float) * pd.Gc, stream));
+      }
+      for (int k = 0; k < d.nd; ++k) {
+        f32_to_bf16(d.D, 4 * d.H, W[k], 4 * d.H, wcat + k * pd.G4p, pd.Gc, stream);
+        SL_CUDA_TRY(cudaMemcpyAsync(w.bcat + k * pd.G4p, b[k], sizeof(float) * 4 * d.H,
+                                    cudaMemcpyDeviceToDevice, stream));
+      }
+      f32_to_bf16(d.BT(), d.D, x, d.D, xb, pd.Dp, stream);
+      Phase ph(stream, "k1_xw_gemm", k1_flops);
+      TcGemm g{(int)d.BT(), (int)pd.Gc, d.D, xb, pd.Dp, false, wcat, pd.Gc, true,
+               w.xw[0], pd.Gc, 1.f, 0.f, w.bcat};
+      gemm_bf16_tc(g, stream);
+    } else {
+      Phase ph(stream, "k1_xw_gemm", k1_flops);
+      for (int k = 0; k < d.nd; ++k)  // K1: XW = X W + b over all B*T rows (tape.cpp:1103-1109)
+        gemm_f32(false, false, (int)d.BT(), 4 * d.H, d.D, 1.f, x, d.D, W[k], 4 * d.H, 0.f,
+                 w.xw[k], 4 * d.H, b[k], stream);
+    }
     RecFwdArgs a{};
     a.B = d.B;
     a.T = d.T;
@@ -203,20 +277,13 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     a.nd = d.nd;
     rec_partition(d.H, d.nd, &a.U, &a.ctas_per_dir);
     a.lens = seq_lens;
-    a.xw_ld = 4 * d.H;
+    a.xw_ld = w.xw_ld;
     a.y = y;
     a.y_ld = (int64_t)d.nd * d.H;
     a.h_last = h_last;
     a.c_last = c_last;
     a.bar = w.bar;
     for (int k = 0; k < d.nd; ++k) {
-      SL_REQUIRE(W[k] && R[k] && b[k], SL_ERR_INVALID_ARGUMENT,
-                 "sl_lstm_layer_fwd: null weight pointer");
-      {  // K1: XW = X W + b over all B*T rows (replaces tape.cpp:1103-1109 per step).
-        Phase ph(stream, "k1_xw_gemm", 2.0 * d.BT() * d.D * 4.0 * d.H);
-        gemm_f32(false, false, (int)d.BT(), 4 * d.H, d.D, 1.f, x, d.D, W[k], 4 * d.H, 0.f,
-                 w.xw[k], 4 * d.H, b[k], stream);
-      }
       SL_CUDA_TRY(cudaMemsetAsync(w.hbuf[k], 0, sizeof(float) * d.B * d.H, stream));
       SL_CUDA_TRY(cudaMemsetAsync(w.cbuf[k], 0, sizeof(float) * d.B * d.H, stream));
       a.dirsign[k] = dir_sign(L, k);
@@ -245,13 +312,14 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     validate(L);
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
     const Dims d = dims(L);
+    const int prec = L->precision;
     SL_REQUIRE(x && seq_lens && W && R && dy && reserve, SL_ERR_INVALID_ARGUMENT,
                "sl_lstm_layer_bwd: null pointer argument");
     size_t need_w = 0, need_r = 0;
-    BwdWork w = carve_bwd(d, workspace, &need_w);
+    BwdWork w = carve_bwd(d, prec, workspace, &need_w);
     SL_REQUIRE(workspace && workspace_bytes >= need_w, SL_ERR_WORKSPACE,
                "sl_lstm_layer_bwd: workspace too small");
-    ReserveView rv = carve_reserve(d, const_cast<void*>(reserve), &need_r);
+    ReserveView rv = carve_reserve(d, prec, const_cast<void*>(reserve), &need_r);
     SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_bwd: reserve too small");
     SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 64 * sizeof(unsigned), stream));
     RecBwdArgs a{};
@@ -285,16 +353,44 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     }
     const float beta = accumulate ? 1.f : 0.f;
     const int M = (int)d.BT(), G = 4 * d.H;
+    const double fx = 2.0 * M * G * (double)d.D;
+    if (prec == SL_PREC_BF16) {
+      // K4 on tensor cores: DZ of both directions side by side -> one dX GEMM.
+      const Pad pd = pads(d);
+      if (pd.G4p != G) SL_CUDA_TRY(cudaMemsetAsync(w.dzb, 0, sizeof(__nv_bfloat16) * M * pd.Gc, stream));
+      for (int k = 0; k < d.nd; ++k) f32_to_bf16(M, G, w.dz[k], G, w.dzb + k * pd.G4p, pd.Gc, stream);
+      if (dx) {
+        Phase ph(stream, "k4_dx_gemm", fx * d.nd);
+        TcGemm g{M, d.D, (int)pd.Gc, w.dzb, pd.Gc, false, rv.wcat, pd.Gc, false, dx, d.D, 1.f,
+                 beta, nullptr};
+        gemm_bf16_tc(g, stream);
+      }
+      for (int k = 0; k < d.nd; ++k) {
+        if (dW && dW[k]) {
+          Phase ph(stream, "k4_dw_gemm", fx);
+          TcGemm g{d.D, G, M, rv.xb, pd.Dp, true, w.dzb + k * pd.G4p, pd.Gc, true, dW[k], G, 1.f,
+                   beta, nullptr};
+          gemm_bf16_tc(g, stream);
+        }
+        if (dR && dR[k]) {
+          f32_to_bf16(M, d.H, rv.hprev[k], d.H, w.hpb, pd.Hp, stream);
+          Phase ph(stream, "k4_dr_gemm", 2.0 * M * G * (double)d.H);
+          TcGemm g{d.H, G, M, w.hpb, pd.Hp, true, w.dzb + k * pd.G4p, pd.Gc, true, dR[k], G, 1.f,
+                   beta, nullptr};
+          gemm_bf16_tc(g, stream);
+        }
+      }
+      return;
+    }
     for (int k = 0; k < d.nd; ++k) {
       // K4: hoisted weight / input gradients over all B*T rows (tape.cpp:1174-1205).
-      const double f = 2.0 * M * G * (double)d.D;
       if (dx) {
-        Phase ph(stream, "k4_dx_gemm", f);
+        Phase ph(stream, "k4_dx_gemm", fx);
         gemm_f32(false, true, M, d.D, G, 1.f, w.dz[k], G, W[k], G, k == 0 ? beta : 1.f, dx, d.D,
                  nullptr, stream);
       }
       if (dW && dW[k]) {
-        Phase ph(stream, "k4_dw_gemm", f);
+        Phase ph(stream, "k4_dw_gemm", fx);
         gemm_f32(true, false, d.D, G, M, 1.f, x, d.D, w.dz[k], G, beta, dW[k], G, nullptr, stream);
       }
       if (dR && dR[k]) {
@@ -311,7 +407,8 @@ int sl_lstm_cell_fwd(int32_t B, int32_t D, int32_t H, int32_t precision, const f
                      const float* b, float* h, float* c, float* saved, sl_stream_t stream) {
   return guarded([&] {
     SL_REQUIRE(B > 0 && D > 0 && H > 0, SL_ERR_SHAPE, "lstm_step: inconsistent shapes");
-    SL_REQUIRE(precision == SL_PREC_FP32, SL_ERR_UNSUPPORTED, "precision not supported");
+    SL_REQUIRE(precision == SL_PREC_FP32 || precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
+               "precision not supported");
     SL_REQUIRE(x && h0 && c0 && W && R && b && h && c, SL_ERR_INVALID_ARGUMENT,
                "sl_lstm_cell_fwd: null pointer argument");
     Phase ph(reinterpret_cast<cudaStream_t>(stream), "k5_cell_fwd", 2.0 * B * (D + H) * 4.0 * H);
@@ -326,7 +423,8 @@ int sl_lstm_cell_bwd(int32_t B, int32_t D, int32_t H, int32_t precision, const f
                      sl_stream_t stream) {
   return guarded([&] {
     SL_REQUIRE(B > 0 && D > 0 && H > 0, SL_ERR_SHAPE, "lstm_step: inconsistent shapes");
-    SL_REQUIRE(precision == SL_PREC_FP32, SL_ERR_UNSUPPORTED, "precision not supported");
+    SL_REQUIRE(precision == SL_PREC_FP32 || precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
+               "precision not supported");
     SL_REQUIRE(x && h0 && c0 && W && R && saved, SL_ERR_INVALID_ARGUMENT,
                "sl_lstm_cell_bwd: null pointer argument");
     Phase ph(reinterpret_cast<cudaStream_t>(stream), "k5_cell_bwd", 4.0 * B * (D + H) * 4.0 * H);
@@ -336,3 +434,15 @@ int sl_lstm_cell_bwd(int32_t B, int32_t D, int32_t H, int32_t precision, const f
 }
 
 }  // extern "C"
+
+#include "../../include/seqloom_cuda_internal.h"
+
+extern "C" int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn,
+                                  const void* B, int64_t ldb, int b_mn, float* C, int64_t ldc,
+                                  float alpha, float beta, const float* bias, sl_stream_t stream) {
+  return guarded([&] {
+    TcGemm g{M, N, K, static_cast<const __nv_bfloat16*>(A), lda, a_mn != 0,
+             static_cast<const __nv_bfloat16*>(B), ldb, b_mn != 0, C, ldc, alpha, beta, bias};
+    gemm_bf16_tc(g, reinterpret_cast<cudaStream_t>(stream));
+  });
+}

@@ -1,0 +1,50 @@
+// Layout / precision conversion kernels for the BF16 path: fp32 row-major
+// [rows, cols] (src_ld) -> bf16 [rows, cols] (dst_ld).  Vectorised 4-wide
+// when both leading dimensions allow it; grid sized to the SM count.
+#include "convert.h"
+#include "profile.h"
+
+namespace sl {
+namespace {
+
+__global__ void f32_to_bf16_kernel(int64_t rows, int64_t cols, const float* __restrict__ src,
+                                   int64_t src_ld, __nv_bfloat16* __restrict__ dst, int64_t dst_ld,
+                                   bool vec) {
+  if (vec) {
+    const int64_t c4 = cols / 4;
+    const int64_t n = rows * c4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = e / c4, c = (e % c4) * 4;
+      const float4 v = *reinterpret_cast<const float4*>(src + r * src_ld + c);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 packed;
+      packed.x = *reinterpret_cast<uint32_t*>(&lo);
+      packed.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst + r * dst_ld + c) = packed;
+    }
+  } else {
+    const int64_t n = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = e / cols, c = e % cols;
+      dst[r * dst_ld + c] = __float2bfloat16_rn(src[r * src_ld + c]);
+    }
+  }
+}
+
+}  // namespace
+
+void f32_to_bf16(int64_t rows, int64_t cols, const float* src, int64_t src_ld, __nv_bfloat16* dst,
+                 int64_t dst_ld, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  const bool vec = (cols % 4 == 0) && (src_ld % 4 == 0) && (dst_ld % 4 == 0) &&
+                   ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 8 == 0);
+  const int64_t work = vec ? rows * cols / 4 : rows * cols;
+  const int grid = (int)std::min<int64_t>(ceil_div(work, 256), 148 * 16);
+  f32_to_bf16_kernel<<<grid, 256, 0, stream>>>(rows, cols, src, src_ld, dst, dst_ld, vec);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace sl

@@ -10,3 +10,26 @@ void gemm_f32(bool transA, bool transB, int M, int N, int K, float alpha, const 
               const float* bias, cudaStream_t stream);
 
 }  // namespace sl
+
+namespace sl {
+
+// BF16 tcgen05 GEMM (gemm_tc.cu): C[M,N] = alpha * op(A) op(B) + beta * C + bias[N], fp32 C.
+//   a_mn = false: A stored [M, K] (lda);  a_mn = true: A stored [K, M] (lda)
+//   b_mn = false: B stored [N, K] (ldb);  b_mn = true: B stored [K, N] (ldb)
+// lda / ldb must be multiples of 8 elements, base pointers 16 B aligned.
+struct TcGemm {
+  int M, N, K;
+  const __nv_bfloat16* A;
+  int64_t lda;
+  bool a_mn;
+  const __nv_bfloat16* B;
+  int64_t ldb;
+  bool b_mn;
+  float* C;
+  int64_t ldc;
+  float alpha, beta;
+  const float* bias;
+};
+void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
+
+}  // namespace sl

@@ -1,0 +1,299 @@
+// BF16 tensor-core GEMM for sm_100a: TMA -> shared (SWIZZLE_128B) -> tcgen05.mma
+// -> TMEM -> fused epilogue.  Used by the SL_PREC_BF16 path for
+//   K1  XW[B*T, 8H]  = X . [W_fw | W_bw] + b          (A K-major,  B N-major)
+//   K4  dX[B*T, D]  (+)= DZ . [W_fw | W_bw]^T         (A K-major,  B K-major)
+//       dW[D, 8H]   (+)= X^T . DZ                     (A M-major,  B N-major)
+//       dR[H, 4H]   (+)= Hprev^T . DZ_d               (A M-major,  B N-major)
+// i.e. the reference's per-step Eigen products (tape.cpp:1103, 1174-1203)
+// hoisted into one GEMM each over all B*T rows.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: 4-stage ring of {A 128x64, B BNx64} bf16 tiles
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> alpha*acc + bias + beta*C -> fp32 global
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the
+// MMAs of tile i+1.  Operand majorness is a compile-time switch so the same
+// kernel serves X.W, DZ.W^T and X^T.DZ without any transpose pass.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm.h"
+#include "profile.h"
+#include "tc.cuh"
+
+namespace sl {
+namespace {
+
+constexpr int BM = 128, BK = 64, kStages = 4, kThreads = 192;
+constexpr uint32_t kBoxBytes = 64 * 64 * 2;  // one 64(MN) x 64(K) bf16 box = 8 KB
+
+struct Params {
+  int M, N, K;
+  int nm, nn, nk;
+  float* C;
+  int64_t ldc;
+  float alpha, beta;
+  const float* bias;
+};
+
+template <int BN>
+struct Smem {
+  static constexpr uint32_t kA = BM * BK * 2;  // 16 KB
+  static constexpr uint32_t kB = BN * BK * 2;  // 16 / 32 KB
+  static constexpr uint32_t kStage = kA + kB;
+  static constexpr uint32_t kBytes = kStages * kStage + 1024;  // + alignment slack
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, Params p) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr uint32_t kTmemCols = 2 * BN;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull_bar[a], 1);
+      tc::mbar_init(&tempty_bar[a], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_base_sh);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_base_sh;
+  const int ntiles = p.nm * p.nn;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t % p.nm) * BM, n0 = (t / p.nm) * BN;
+        for (int kb = 0; kb < p.nk; ++kb) {
+          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStage;
+          uint8_t* sb = sa + S::kA;
+          tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStage);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tc::tma_load_2d(sa + j * kBoxBytes, &tmA, &full_bar[stage], m0 + 64 * j, k0);
+          } else {
+            tc::tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tc::tma_load_2d(sb + j * kBoxBytes, &tmB, &full_bar[stage], n0 + 64 * j, k0);
+          } else {
+            tc::tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::make_idesc(BM, BN, 1, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        tc::mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < p.nk; ++kb) {
+          tc::mbar_wait(&full_bar[stage], phase);
+          tc::fence_after_sync();
+          const uint32_t sa = base + stage * S::kStage;
+          const uint32_t sb = sa + S::kA;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 16 elems = 32 B inside the 128 B swizzle row.
+            // MN-major: advance 16 K-rows = 2 KB; MN blocks 8 KB apart (LBO).
+            const uint64_t ad = A_MN ? tc::make_sdesc(sa + k * 2048, kBoxBytes, 1024)
+                                     : tc::make_sdesc(sa + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, kBoxBytes, 1024)
+                                     : tc::make_sdesc(sb + k * 32, 0, 1024);
+            tc::mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {  // ---------------- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1)
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      const int m0 = (t % p.nm) * BM, n0 = (t / p.nm) * BN;
+      tc::mbar_wait(&tfull_bar[acc], use & 1);
+      tc::fence_after_sync();
+      const int row = m0 + 32 * q + lane;
+      float* crow = p.C + (int64_t)row * p.ldc;
+      const bool vec = (p.ldc % 4) == 0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BN + c, v);
+        if (row >= p.M) continue;
+        const int col0 = n0 + c;
+        if (vec && col0 + 32 <= p.N) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 o;
+            o.x = p.alpha * v[j];
+            o.y = p.alpha * v[j + 1];
+            o.z = p.alpha * v[j + 2];
+            o.w = p.alpha * v[j + 3];
+            if (p.bias) {
+              const float4 bb = *reinterpret_cast<const float4*>(p.bias + col0 + j);
+              o.x += bb.x;
+              o.y += bb.y;
+              o.z += bb.z;
+              o.w += bb.w;
+            }
+            float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
+            if (p.beta != 0.f) {
+              const float4 old = *dst;
+              o.x += p.beta * old.x;
+              o.y += p.beta * old.y;
+              o.z += p.beta * old.z;
+              o.w += p.beta * old.w;
+            }
+            *dst = o;
+          }
+        } else {
+          for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+            float o = p.alpha * v[j];
+            if (p.bias) o += p.bias[col0 + j];
+            float* dst = crow + col0 + j;
+            if (p.beta != 0.f) o += p.beta * *dst;
+            *dst = o;
+          }
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  SL_REQUIRE(fn != nullptr, SL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// Row-major bf16 matrix [outer, inner] with leading dimension ld (elements),
+// boxes of 64 (inner, = one 128 B swizzle row) x box_outer.
+CUtensorMap tmap_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  SL_REQUIRE(((uintptr_t)ptr & 15) == 0 && (ld * 2) % 16 == 0, SL_ERR_INVALID_ARGUMENT,
+             "gemm_bf16_tc: operands need 16 B aligned base and leading dimension % 8 == 0");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SL_REQUIRE(r == CUDA_SUCCESS, SL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStream_t s) {
+  auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Smem<BN>::kBytes));
+    configured = true;
+  }
+  const int tiles = p.nm * p.nn;
+  const int grid = std::min(tiles, num_sms());
+  kern<<<grid, kThreads, Smem<BN>::kBytes, s>>>(a, b, p);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace
+
+void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
+  if (g.M <= 0 || g.N <= 0) return;
+  constexpr int BN = 256;
+  Params p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.nm = (int)ceil_div(g.M, BM);
+  p.nn = (int)ceil_div(g.N, BN);
+  p.nk = (int)ceil_div(g.K, BK);
+  p.C = g.C;
+  p.ldc = g.ldc;
+  p.alpha = g.alpha;
+  p.beta = g.beta;
+  p.bias = g.bias;
+  // A: K-major stored [M, K]; MN-major stored [K, M].  B: K-major stored [N, K]; MN-major [K, N].
+  const CUtensorMap ta = g.a_mn ? tmap_bf16(g.A, g.M, g.K, g.lda, 64)
+                                : tmap_bf16(g.A, g.K, g.M, g.lda, BM);
+  const CUtensorMap tb = g.b_mn ? tmap_bf16(g.B, g.N, g.K, g.ldb, 64)
+                                : tmap_bf16(g.B, g.K, g.N, g.ldb, BN);
+  if (!g.a_mn && g.b_mn) launch<BN, false, true>(ta, tb, p, stream);
+  else if (!g.a_mn && !g.b_mn) launch<BN, false, false>(ta, tb, p, stream);
+  else if (g.a_mn && g.b_mn) launch<BN, true, true>(ta, tb, p, stream);
+  else launch<BN, true, false>(ta, tb, p, stream);
+}
+
+}  // namespace sl

@@ -1,0 +1,56 @@
+"""GPU numerics of the BF16 tcgen05 GEMM (K1 / K4) against a torch fp32
+reference on the same bf16-rounded operands (tolerance: fp32 accumulation
+order only, rel 1e-5)."""
+import ctypes
+
+import pytest
+import torch
+
+from paper_1805_05225_b200 import lstm
+
+pytestmark = pytest.mark.gpu
+
+
+def lib():
+    L = lstm.lib()
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    L.sl_debug_gemm_bf16.argtypes = [ctypes.c_int] * 3 + [vp, i64, ctypes.c_int, vp, i64,
+                                                          ctypes.c_int, vp, i64, ctypes.c_float,
+                                                          ctypes.c_float, vp, vp]
+    return L
+
+
+def run(M, N, K, a_mn, b_mn, alpha=1.0, beta=0.0, bias=False, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = (torch.rand((K, M) if a_mn else (M, K), device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand((K, N) if b_mn else (N, K), device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.rand(M, N, device="cuda", generator=g)
+    bvec = torch.rand(N, device="cuda", generator=g) if bias else None
+    opA = A.float().t() if a_mn else A.float()
+    opB = B.float() if b_mn else B.float().t()
+    ref = alpha * (opA @ opB) + beta * C
+    if bias:
+        ref = ref + bvec
+    rc = lib().sl_debug_gemm_bf16(M, N, K, A.data_ptr(), A.shape[1], int(a_mn), B.data_ptr(),
+                                  B.shape[1], int(b_mn), C.data_ptr(), N, alpha, beta,
+                                  bvec.data_ptr() if bias else None,
+                                  torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, lib().sl_last_error()
+    torch.cuda.synchronize()
+    return C, ref
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, True), (False, False), (True, True), (True, False)])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 320), (200, 304, 136),
+                                   (1000, 4000, 1024)])
+def test_gemm_bf16_tc(cuda, a_mn, b_mn, shape):
+    M, N, K = shape
+    C, ref = run(M, N, K, a_mn, b_mn)
+    err = (C - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+
+
+def test_gemm_bf16_tc_epilogue(cuda):
+    C, ref = run(384, 520, 200, False, True, alpha=0.5, beta=1.0, bias=True)
+    err = (C - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err

@@ -21,7 +21,7 @@ from paper_1805_05225_b200 import lstm
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 TOL = {"fp32": 1e-4, "bf16": 2e-2}
-PRECS = ["fp32"]
+PRECS = ["fp32", "bf16"]
 
 
 def rel(a, b):
