@@ -14,11 +14,14 @@
 #include "convert.h"
 #include "gemm.h"
 #include "profile.h"
+#include "rec_tc.h"
 #include "recurrence.h"
 
 namespace sl {
 
 static thread_local std::string g_last_error;
+static unsigned long long* g_rec_trace = nullptr;  // debug: sl_debug_set_trace
+static int g_rec_trace_cta = 0;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 namespace {
@@ -69,7 +72,20 @@ struct ReserveView {
   float* hprev[2] = {nullptr, nullptr};
   __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
   __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
+  __nv_bfloat16* hprevb[2] = {nullptr, nullptr};  // bf16 path: h_{s-1} [B*T, Hp]
+  __nv_bfloat16* rt[2] = {nullptr, nullptr};      // bf16 path: packed R^T slices
 };
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;  // sizing only (no device yet): B200
+  }
+  return n;
+}
 
 // Padded extents of the bf16 path (TMA needs 16 B aligned rows).
 struct Pad {
@@ -77,7 +93,7 @@ struct Pad {
 };
 Pad pads(const Dims& d) {
   Pad p;
-  p.Dp = round_up(d.D, 8);
+  p.Dp = round_up(d.D + 1, 8);  // + a ones column (db from the dW GEMM)
   p.Hp = round_up(d.H, 8);
   p.G4p = round_up(4 * (int64_t)d.H, 8);
   p.Gc = d.nd * p.G4p;
@@ -90,12 +106,18 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
   for (int k = 0; k < d.nd; ++k) {
     r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
     r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
-    r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
+    if (prec != SL_PREC_BF16) r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
   }
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
+    const int U = tc_rec_units(d.H, d.nd, sm_count());
+    SL_REQUIRE(U > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     r.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
     r.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
+    for (int k = 0; k < d.nd; ++k) {
+      r.hprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Hp);
+      r.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(d.H, U));
+    }
   }
   *bytes = c.off;
   return r;
@@ -109,6 +131,8 @@ struct FwdWork {
   float* bcat = nullptr;  // bf16 path: concatenated bias [nd*G4p]
   __nv_bfloat16* xb = nullptr;    // bf16 inference (no reserve)
   __nv_bfloat16* wcat = nullptr;
+  __nv_bfloat16* rt[2] = {nullptr, nullptr};
+  __nv_bfloat16* hbufb[2] = {nullptr, nullptr};  // bf16 path: h ring [2][B][Kp]
   unsigned* bar = nullptr;
 };
 
@@ -124,24 +148,31 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
     w.bcat = c.take<float>((size_t)pd.Gc);
     w.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
     w.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
+    const int U = tc_rec_units(d.H, d.nd, sm_count());
+    SL_REQUIRE(U > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
+    for (int k = 0; k < d.nd; ++k) {
+      w.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(d.H, U));
+      w.hbufb[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * round_up(d.H, 64));
+    }
   } else {
     w.xw_ld = 4 * d.H;
-    for (int k = 0; k < d.nd; ++k) w.xw[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
-  }
-  for (int k = 0; k < d.nd; ++k) {
-    w.hbuf[k] = c.take<float>((size_t)2 * d.B * d.H);
-    w.cbuf[k] = c.take<float>((size_t)d.B * d.H);
+    for (int k = 0; k < d.nd; ++k) {
+      w.xw[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
+      w.hbuf[k] = c.take<float>((size_t)2 * d.B * d.H);
+      w.cbuf[k] = c.take<float>((size_t)d.B * d.H);
+    }
   }
   *bytes = c.off;
   return w;
 }
 
 struct BwdWork {
-  float* dz[2] = {nullptr, nullptr};
-  float* dzbuf[2] = {nullptr, nullptr};
-  float* gcbuf[2] = {nullptr, nullptr};
-  __nv_bfloat16* dzb = nullptr;  // bf16 path: DZ of both directions [B*T, nd*G4p]
-  __nv_bfloat16* hpb = nullptr;  // bf16 path: Hprev of one direction [B*T, Hp]
+  float* dz[2] = {nullptr, nullptr};      // fp32 path
+  float* dzbuf[2] = {nullptr, nullptr};   // fp32 path
+  float* gcbuf[2] = {nullptr, nullptr};   // fp32 path
+  __nv_bfloat16* dzb = nullptr;           // bf16 path: DZ of both directions [B*T, nd*G4p]
+  __nv_bfloat16* dzring[2] = {nullptr, nullptr};  // bf16 path: DZ ring [2][B][Kz]
+  __nv_bfloat16* rb[2] = {nullptr, nullptr};      // bf16 path: packed R row slices
   unsigned* bar = nullptr;
 };
 
@@ -149,15 +180,22 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   BwdWork w;
   w.bar = c.take<unsigned>(64);
-  for (int k = 0; k < d.nd; ++k) {
-    w.dz[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
-    w.dzbuf[k] = c.take<float>((size_t)2 * d.B * 4 * d.H);
-    w.gcbuf[k] = c.take<float>((size_t)d.B * d.H);
-  }
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
+    const int U = tc_rec_units(d.H, d.nd, sm_count());
+    SL_REQUIRE(U > 0 && tc_rec_bwd_fits(d.H, U), SL_ERR_UNSUPPORTED,
+               "bf16 recurrence: hidden size too large for one launch");
     w.dzb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
-    w.hpb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Hp);
+    for (int k = 0; k < d.nd; ++k) {
+      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * round_up(4 * (int64_t)d.H, 64));
+      w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(d.H, U));
+    }
+  } else {
+    for (int k = 0; k < d.nd; ++k) {
+      w.dz[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
+      w.dzbuf[k] = c.take<float>((size_t)2 * d.B * 4 * d.H);
+      w.gcbuf[k] = c.take<float>((size_t)d.B * d.H);
+    }
   }
   *bytes = c.off;
   return w;
@@ -260,6 +298,7 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
                                     cudaMemcpyDeviceToDevice, stream));
       }
       f32_to_bf16(d.BT(), d.D, x, d.D, xb, pd.Dp, stream);
+      fill_col_bf16(d.BT(), d.D, xb, pd.Dp, 1.f, stream);
       Phase ph(stream, "k1_xw_gemm", k1_flops);
       TcGemm g{(int)d.BT(), (int)pd.Gc, d.D, xb, pd.Dp, false, wcat, pd.Gc, true,
                w.xw[0], pd.Gc, 1.f, 0.f, w.bcat};
@@ -269,6 +308,42 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       for (int k = 0; k < d.nd; ++k)  // K1: XW = X W + b over all B*T rows (tape.cpp:1103-1109)
         gemm_f32(false, false, (int)d.BT(), 4 * d.H, d.D, 1.f, x, d.D, W[k], 4 * d.H, 0.f,
                  w.xw[k], 4 * d.H, b[k], stream);
+    }
+    if (prec == SL_PREC_BF16) {
+      const Pad pd = pads(d);
+      TcRecFwdArgs a{};
+      a.B = d.B;
+      a.T = d.T;
+      a.H = d.H;
+      a.nd = d.nd;
+      a.U = tc_rec_units(d.H, d.nd, sm_count());
+      a.P = (int)ceil_div(d.H, a.U);
+      a.Kp = (int)round_up(d.H, 64);
+      a.lens = seq_lens;
+      a.xw_ld = w.xw_ld;
+      a.y = y;
+      a.y_ld = (int64_t)d.nd * d.H;
+      a.h_last = h_last;
+      a.c_last = c_last;
+      a.hprev_ld = pd.Hp;
+      a.bar = w.bar;
+      __nv_bfloat16* rt[2] = {nullptr, nullptr};
+      for (int k = 0; k < d.nd; ++k) {
+        rt[k] = rv.rt[k] ? rv.rt[k] : w.rt[k];
+        tc_rec_pack(R[k], d.H, a.U, rt[k], stream);
+        SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kp, stream));
+        a.dirsign[k] = dir_sign(L, k);
+        a.xw[k] = w.xw[k];
+        a.hbuf[k] = w.hbufb[k];
+        a.gates[k] = rv.gates[k];
+        a.cprev[k] = rv.cprev[k];
+        a.hprev[k] = rv.hprevb[k];
+      }
+      a.trace = g_rec_trace;
+      a.trace_cta = g_rec_trace_cta;
+      Phase ph(stream, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd);
+      rec_fwd_tc(a, rt, stream);
+      return;
     }
     RecFwdArgs a{};
     a.B = d.B;
@@ -322,6 +397,73 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     ReserveView rv = carve_reserve(d, prec, const_cast<void*>(reserve), &need_r);
     SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_bwd: reserve too small");
     SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 64 * sizeof(unsigned), stream));
+    const float beta = accumulate ? 1.f : 0.f;
+    const int M = (int)d.BT(), G = 4 * d.H;
+    const double fx = 2.0 * M * G * (double)d.D;
+    const double rec_flops = 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd;
+    if (prec == SL_PREC_BF16) {
+      const Pad pd = pads(d);
+      TcRecBwdArgs a{};
+      a.B = d.B;
+      a.T = d.T;
+      a.H = d.H;
+      a.nd = d.nd;
+      a.U = tc_rec_units(d.H, d.nd, sm_count());
+      a.P = (int)ceil_div(d.H, a.U);
+      a.Kz = (int)round_up(4 * (int64_t)d.H, 64);
+      a.lens = seq_lens;
+      a.dy = dy;
+      a.dy_ld = (int64_t)d.nd * d.H;
+      a.dh_last = dh_last;
+      a.dc_last = dc_last;
+      a.dzcat = w.dzb;
+      a.dzcat_ld = pd.Gc;
+      a.dz_dir_off = pd.G4p;
+      a.bar = w.bar;
+      a.trace = g_rec_trace;
+      a.trace_cta = g_rec_trace_cta;
+      if (pd.G4p != G) SL_CUDA_TRY(cudaMemsetAsync(w.dzb, 0, sizeof(__nv_bfloat16) * M * pd.Gc, stream));
+      for (int k = 0; k < d.nd; ++k) {
+        tc_rec_bwd_pack(R[k], d.H, a.U, w.rb[k], stream);
+        SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kz, stream));
+        a.dirsign[k] = dir_sign(L, k);
+        a.gates[k] = rv.gates[k];
+        a.cprev[k] = rv.cprev[k];
+        a.dzring[k] = w.dzring[k];
+      }
+      {
+        Phase ph(stream, "k3_rec_bwd", rec_flops);
+        rec_bwd_tc(a, w.rb, stream);
+      }
+      // K4 on tensor cores: DZ of both directions side by side -> one dX GEMM;
+      // dW and db from ONE GEMM over [X | 1] (the ones column yields colsum(DZ)).
+      if (dx) {
+        Phase ph(stream, "k4_dx_gemm", fx * d.nd);
+        TcGemm g{M, d.D, (int)pd.Gc, w.dzb, pd.Gc, false, rv.wcat, pd.Gc, false, dx, d.D, 1.f,
+                 beta, nullptr};
+        gemm_bf16_tc(g, stream);
+      }
+      for (int k = 0; k < d.nd; ++k) {
+        float* dbk = db ? db[k] : nullptr;
+        if ((dW && dW[k]) || dbk) {
+          Phase ph(stream, "k4_dw_gemm", fx);
+          TcGemm g{d.D + 1, G, M, rv.xb, pd.Dp, true, w.dzb + k * pd.G4p, pd.Gc, true,
+                   dW ? dW[k] : nullptr, G, 1.f, beta, nullptr};
+          g.m_split = d.D;
+          g.C2 = dbk;
+          g.ldc2 = G;
+          if (!dbk) g.M = d.D;
+          gemm_bf16_tc(g, stream);
+        }
+        if (dR && dR[k]) {
+          Phase ph(stream, "k4_dr_gemm", 2.0 * M * G * (double)d.H);
+          TcGemm g{d.H, G, M, rv.hprevb[k], pd.Hp, true, w.dzb + k * pd.G4p, pd.Gc, true, dR[k],
+                   G, 1.f, beta, nullptr};
+          gemm_bf16_tc(g, stream);
+        }
+      }
+      return;
+    }
     RecBwdArgs a{};
     a.B = d.B;
     a.T = d.T;
@@ -348,39 +490,8 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       SL_CUDA_TRY(cudaMemsetAsync(w.gcbuf[k], 0, sizeof(float) * d.B * d.H, stream));
     }
     {
-      Phase ph(stream, "k3_rec_bwd", 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd);
+      Phase ph(stream, "k3_rec_bwd", rec_flops);
       rec_bwd_f32(a, stream);
-    }
-    const float beta = accumulate ? 1.f : 0.f;
-    const int M = (int)d.BT(), G = 4 * d.H;
-    const double fx = 2.0 * M * G * (double)d.D;
-    if (prec == SL_PREC_BF16) {
-      // K4 on tensor cores: DZ of both directions side by side -> one dX GEMM.
-      const Pad pd = pads(d);
-      if (pd.G4p != G) SL_CUDA_TRY(cudaMemsetAsync(w.dzb, 0, sizeof(__nv_bfloat16) * M * pd.Gc, stream));
-      for (int k = 0; k < d.nd; ++k) f32_to_bf16(M, G, w.dz[k], G, w.dzb + k * pd.G4p, pd.Gc, stream);
-      if (dx) {
-        Phase ph(stream, "k4_dx_gemm", fx * d.nd);
-        TcGemm g{M, d.D, (int)pd.Gc, w.dzb, pd.Gc, false, rv.wcat, pd.Gc, false, dx, d.D, 1.f,
-                 beta, nullptr};
-        gemm_bf16_tc(g, stream);
-      }
-      for (int k = 0; k < d.nd; ++k) {
-        if (dW && dW[k]) {
-          Phase ph(stream, "k4_dw_gemm", fx);
-          TcGemm g{d.D, G, M, rv.xb, pd.Dp, true, w.dzb + k * pd.G4p, pd.Gc, true, dW[k], G, 1.f,
-                   beta, nullptr};
-          gemm_bf16_tc(g, stream);
-        }
-        if (dR && dR[k]) {
-          f32_to_bf16(M, d.H, rv.hprev[k], d.H, w.hpb, pd.Hp, stream);
-          Phase ph(stream, "k4_dr_gemm", 2.0 * M * G * (double)d.H);
-          TcGemm g{d.H, G, M, w.hpb, pd.Hp, true, w.dzb + k * pd.G4p, pd.Gc, true, dR[k], G, 1.f,
-                   beta, nullptr};
-          gemm_bf16_tc(g, stream);
-        }
-      }
-      return;
     }
     for (int k = 0; k < d.nd; ++k) {
       // K4: hoisted weight / input gradients over all B*T rows (tape.cpp:1174-1205).
@@ -445,4 +556,10 @@ extern "C" int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t ld
              static_cast<const __nv_bfloat16*>(B), ldb, b_mn != 0, C, ldc, alpha, beta, bias};
     gemm_bf16_tc(g, reinterpret_cast<cudaStream_t>(stream));
   });
+}
+
+extern "C" int sl_debug_set_trace(unsigned long long* dev_buf, int cta) {
+  g_rec_trace = dev_buf;
+  g_rec_trace_cta = cta;
+  return 0;
 }

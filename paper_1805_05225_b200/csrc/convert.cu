@@ -33,7 +33,23 @@ __global__ void f32_to_bf16_kernel(int64_t rows, int64_t cols, const float* __re
   }
 }
 
+__global__ void fill_col_bf16_kernel(int64_t rows, int64_t col, __nv_bfloat16* dst, int64_t ld,
+                                     __nv_bfloat16 v) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    dst[r * ld + col] = v;
+}
+
 }  // namespace
+
+void fill_col_bf16(int64_t rows, int64_t col, __nv_bfloat16* dst, int64_t ld, float value,
+                   cudaStream_t stream) {
+  if (rows <= 0) return;
+  fill_col_bf16_kernel<<<(int)std::min<int64_t>(ceil_div(rows, 256), 148 * 4), 256, 0, stream>>>(
+      rows, col, dst, ld, __float2bfloat16_rn(value));
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
 
 void f32_to_bf16(int64_t rows, int64_t cols, const float* src, int64_t src_ld, __nv_bfloat16* dst,
                  int64_t dst_ld, cudaStream_t stream) {

@@ -29,6 +29,11 @@ struct TcGemm {
   int64_t ldc;
   float alpha, beta;
   const float* bias;
+  // optional: rows >= m_split are written to C2 (row - m_split) instead of C
+  // (used to emit db = colsum(DZ) from the ones-column of [X | 1]^T . DZ)
+  int m_split = 1 << 30;
+  float* C2 = nullptr;
+  int64_t ldc2 = 0;
 };
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 

@@ -35,6 +35,9 @@ struct Params {
   int64_t ldc;
   float alpha, beta;
   const float* bias;
+  int m_split;
+  float* C2;
+  int64_t ldc2;
 };
 
 template <int BN>
@@ -158,13 +161,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&tfull_bar[acc], use & 1);
       tc::fence_after_sync();
       const int row = m0 + 32 * q + lane;
-      float* crow = p.C + (int64_t)row * p.ldc;
-      const bool vec = (p.ldc % 4) == 0;
+      const bool second = row >= p.m_split;
+      float* crow = second ? p.C2 + (int64_t)(row - p.m_split) * p.ldc2 : p.C + (int64_t)row * p.ldc;
+      const bool vec = second ? (p.ldc2 % 4) == 0 && ((uintptr_t)p.C2 & 15) == 0
+                              : (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BN + c, v);
-        if (row >= p.M) continue;
+        if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
         const int col0 = n0 + c;
         if (vec && col0 + 32 <= p.N) {
 #pragma unroll
@@ -285,6 +290,9 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.bias = g.bias;
+  p.m_split = g.m_split;
+  p.C2 = g.C2;
+  p.ldc2 = g.ldc2;
   // A: K-major stored [M, K]; MN-major stored [K, M].  B: K-major stored [N, K]; MN-major [K, N].
   const CUtensorMap ta = g.a_mn ? tmap_bf16(g.A, g.M, g.K, g.lda, 64)
                                 : tmap_bf16(g.A, g.K, g.M, g.lda, BM);

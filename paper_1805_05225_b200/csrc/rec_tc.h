@@ -1,0 +1,66 @@
+// Tensor-core persistent recurrence (rec_tc.cu) — arguments and entry points.
+#pragma once
+#include "common.cuh"
+
+namespace sl {
+
+struct TcRecFwdArgs {
+  int B, T, H, nd, U, P;  // P = CTAs per direction (= ceil(H / U))
+  int b0;                 // first batch row of this launch (set internally)
+  int Kp;                 // K padded to 64 (= round_up(H, 64))
+  int stages;             // h-tile ring depth
+  const int32_t* lens;
+  int dirsign[2];
+  const float* xw[2];  // hoisted x W + b, fp32 [B*T, xw_ld], dir d's gate blocks at col 0
+  int64_t xw_ld;
+  float* y;  // fp32 [B*T, y_ld] (dir d at col d*H) or null
+  int64_t y_ld;
+  __nv_bfloat16* ybf;  // bf16 copy of y (next layer's K1 operand) or null
+  int64_t ybf_ld;
+  float* h_last;  // [nd, B, H] or null
+  float* c_last;
+  float* gates[2];            // saved (i,f,g,o) fp32 [B*T, 4H] (null = inference)
+  float* cprev[2];            // saved c_{s-1} fp32 [B*T, H]
+  __nv_bfloat16* hprev[2];    // saved h_{s-1} bf16 [B*T, hprev_ld] (dR GEMM operand)
+  int64_t hprev_ld;
+  __nv_bfloat16* hbuf[2];     // ring [2][B][Kp] bf16, zeroed
+  unsigned* bar;              // zeroed step counters, 2 per batch chunk
+  unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
+  int trace_cta;
+};
+
+struct TcRecBwdArgs {
+  int B, T, H, nd, U, P;
+  int b0;      // first batch row of this launch (set internally)
+  int Kz;      // K of the per-step dh GEMM = gate columns padded to 64 (round_up(4H, 64))
+  int stages;  // set internally
+  const int32_t* lens;
+  int dirsign[2];
+  const float* gates[2];  // saved by K2: (i,f,g,o) fp32 [B*T, 4H]
+  const float* cprev[2];  // saved by K2: c_{s-1} fp32 [B*T, H]
+  const float* dy;        // [B*T, dy_ld], dir d at col d*H
+  int64_t dy_ld;
+  const float* dh_last;  // [nd, B, H] or null
+  const float* dc_last;
+  __nv_bfloat16* dzring[2];  // [2][B][Kz] bf16, zeroed
+  __nv_bfloat16* dzcat;      // out: DZ bf16 [B*T, dzcat_ld], dir d at col d*dz_dir_off
+  int64_t dzcat_ld, dz_dir_off;
+  unsigned* bar;  // zeroed step counters
+  unsigned long long* trace;
+  int trace_cta;
+};
+
+size_t tc_rec_bwd_pack_elems(int H, int U);
+void tc_rec_bwd_pack(const float* R, int H, int U, __nv_bfloat16* RB, cudaStream_t stream);
+bool tc_rec_bwd_fits(int H, int U);
+void rec_bwd_tc(const TcRecBwdArgs& a, __nv_bfloat16* const* RB, cudaStream_t stream);
+
+// Units per CTA for the tensor-core recurrence (0 = shape unsupported).
+int tc_rec_units(int H, int nd, int sms);
+// Elements of the packed R^T slice buffer for one direction.
+size_t tc_rec_pack_elems(int H, int U);
+// Pack R [H, 4H] fp32 into the per-CTA K-major bf16 slices the kernel loads.
+void tc_rec_pack(const float* R, int H, int U, __nv_bfloat16* RT, cudaStream_t stream);
+void rec_fwd_tc(const TcRecFwdArgs& a, __nv_bfloat16* const* RT, cudaStream_t stream);
+
+}  // namespace sl

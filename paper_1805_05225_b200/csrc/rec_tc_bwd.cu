@@ -1,0 +1,339 @@
+// K3 — persistent tensor-core BPTT (SL_PREC_BF16 path): the mirror of K2.
+//
+// One launch runs all T steps of both directions backwards.  CTA c of
+// direction d owns hidden units [c*U, c*U+U): it keeps R[units, :] (the rows
+// of R feeding those units' h, all 4H gate columns, bf16, K-major) resident in
+// shared memory, and per step s (descending):
+//   warp 0      waits for every CTA of the direction to publish DZ_{s+1}, then
+//               TMA-streams DZ_{s+1} [128-row batch tile x 64 gate cols] bf16
+//               from the L2-resident ring buffer;
+//   warp 1      tcgen05.mma: dh_rec[:, units] = DZ_{s+1} . R[units, :]^T
+//               (tape.cpp:1182-1189, the per-step GEMM GH = DZ R^T);
+//   warps 2..   one/two threads per batch row: gh = dy + dh_rec, the cell-gate
+//               adjoint of tape.cpp:1157-1170 with the carried dc, writing
+//               DZ_s to the ring (for the next step) and to the [B*T, 8H]
+//               DZ matrix the hoisted K4 GEMMs consume; db is reduced on the fly.
+// As in K2 the two 128-row batch tiles are independent recurrences with their
+// own step counters, so one tile's epilogue overlaps the other's MMAs.
+#include "profile.h"
+#include "rec_tc.h"
+#include "rec_tc_common.cuh"
+
+namespace sl {
+namespace {
+using namespace rtc;
+
+constexpr int kStages = 6;
+constexpr uint32_t kTile = 128 * 64 * 2;  // 16 KB A tile
+constexpr uint32_t kSmemMax = 227 * 1024;
+
+uint32_t bwd_smem(int NB, int Kz, int stages) { return (uint32_t)NB * Kz * 2 + stages * kTile + 1024; }
+
+template <int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
+__global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
+    rec_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
+                      const __grid_constant__ CUtensorMap tmR1,
+                      const __grid_constant__ CUtensorMap tmZ0,
+                      const __grid_constant__ CUtensorMap tmZ1, TcRecBwdArgs a) {
+  constexpr int NB = U < 16 ? 16 : U;  // MMA N (M = 128 needs N % 16 == 0)
+  constexpr int kEpi = 128 * MT * SPLIT;
+  constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : 64;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t r_bar, tfull_bar[MT], tempty_bar[MT];
+  __shared__ uint32_t tmem_sh;
+  __shared__ int tmax_sh;
+
+  const int d = blockIdx.x / a.P;
+  const int cta = blockIdx.x % a.P;
+  const int u0 = cta * U;
+  const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
+  const CUtensorMap* tmZ = d == 0 ? &tmZ0 : &tmZ1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
+  const uint32_t r_bytes = (uint32_t)NB * a.Kz * 2;
+  uint8_t* sR = smem;
+  uint8_t* sA = smem + r_bytes;
+  const int nkc = a.Kz / 64;
+
+  if (threadIdx.x == 0) {
+    tmax_sh = 0;
+    tc::prefetch_tmap(tmR);
+    tc::prefetch_tmap(tmZ);
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    tc::mbar_init(&r_bar, 1);
+    for (int m = 0; m < MT; ++m) {
+      tc::mbar_init(&tfull_bar[m], 1);
+      tc::mbar_init(&tempty_bar[m], kEpi / MT);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  {
+    int m = 0;
+    for (int i = threadIdx.x; i < a.B; i += blockDim.x) m = max(m, (int)a.lens[i]);
+    atomicMax(&tmax_sh, m);
+  }
+  __syncthreads();
+  const int Tmax = tmax_sh;
+  const uint32_t tmem = tmem_sh;
+  unsigned* ctr = a.bar + d * 2;
+  const int kc_off = cta % nkc;
+
+  if (warp == 0) {
+    if (lane == 0) {  // -------------------------------------------- producer
+      tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
+      for (int kc = 0; kc < nkc; ++kc)
+        tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
+      int st = 0;
+      uint32_t ph = 0;
+      const int nst = a.stages;
+      for (int s = 0; s < Tmax; ++s) {  // s = iteration (processing step Tmax-1-s)
+        const int slot = s & 1;          // ring slot holding DZ of the previous iteration
+        for (int mt = 0; mt < MT; ++mt) {
+          if (s > 0) {
+            const unsigned target = (unsigned)a.P * (unsigned)s;
+            while (ld_acquire(ctr + mt) < target) {
+            }
+            tc::fence_proxy_async_global();
+          }
+          if (mt == 0) SL_TRACE(0);
+          for (int kq = 0; kq < nkc; ++kq) {
+            const int kc = (kq + kc_off) % nkc;
+            tc::mbar_wait(&empty_bar[st], ph ^ 1);
+            tc::mbar_arrive_expect_tx(&full_bar[st], kTile);
+            tma_load_3d(sA + st * kTile, tmZ, &full_bar[st], kc * 64, a.b0 + mt * 128, slot);
+            if (++st == nst) {
+              st = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // -------------------------------------------- MMA issuer
+      constexpr uint32_t idesc = tc::make_idesc(128, NB, 1, false, false);
+      tc::mbar_wait(&r_bar, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      const int nst = a.stages;
+      for (int s = 0; s < Tmax; ++s) {
+        for (int mt = 0; mt < MT; ++mt) {
+          tc::mbar_wait(&tempty_bar[mt], (s & 1) ^ 1);
+          tc::fence_after_sync();
+          for (int kq = 0; kq < nkc; ++kq) {
+            const int kc = (kq + kc_off) % nkc;
+            tc::mbar_wait(&full_bar[st], ph);
+            tc::fence_after_sync();
+            if (mt == 0 && kq == 0) SL_TRACE(1);
+            const uint32_t sa = base + r_bytes + st * kTile;
+            const uint32_t sb = base + (uint32_t)kc * NB * 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc::mma_f16(tmem + mt * NB, tc::make_sdesc(sa + k * 32, 0, 1024),
+                          tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | k) != 0);
+            tc::mma_commit(&empty_bar[st]);
+            if (++st == nst) {
+              st = 0;
+              ph ^= 1;
+            }
+          }
+          if (mt == MT - 1) SL_TRACE(2);
+          tc::mma_commit(&tfull_bar[mt]);
+        }
+      }
+    }
+  } else {  // ------------------------------------------------------ epilogue
+    const int e = warp - 2;
+    const int mt = e / (4 * SPLIT);
+    const int half = (e / 4) % SPLIT;
+    const int q = warp & 3;
+    const int row = a.b0 + mt * 128 + q * 32 + lane;
+    const bool valid_row = row < a.B;
+    const int len = valid_row ? a.lens[row] : 0;
+    const int dir = a.dirsign[d];
+    const int H = a.H, T = a.T;
+    const int lo = half * UT;
+    const int ut0 = u0 + lo;
+    const int nu = max(0, min(UT, H - ut0));
+    __nv_bfloat16* zr = a.dzring[d];
+    const float* gates = a.gates[d];
+    const float* cprev = a.cprev[d];
+    float gcar[UT];
+#pragma unroll
+    for (int u = 0; u < UT; ++u) gcar[u] = 0.f;
+
+    for (int it = 0; it < Tmax; ++it) {
+      const int s = Tmax - 1 - it;  // processing step
+      const bool active = valid_row && s < len;
+      const int t = active ? src_time(s, len, dir) : s;
+      const size_t pos = (size_t)row * T + t;
+      float gv[4 * UT], cp[UT], dyv[UT];
+      if (active) {  // prefetch this step's saved activations and upstream grad
+        const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) load_f32<UT>(gates + pos * 4 * H + g * H + ut0, gv + g * UT, nu, vec);
+        load_f32<UT>(cprev + pos * H + ut0, cp, nu, vec);
+        load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)d * H + ut0, dyv, nu,
+                     vec && (a.dy_ld % 4) == 0);
+      }
+      float dh[UT];
+      tc::mbar_wait(&tfull_bar[mt], it & 1);
+      tc::fence_after_sync();
+      tmem_ld_cols<UT>(tmem + ((uint32_t)(q * 32) << 16) + mt * NB + lo, dh);
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty_bar[mt]);
+
+      if (valid_row) {
+        __nv_bfloat16* zn = zr + ((size_t)((it + 1) & 1) * a.B + row) * a.Kz + ut0;
+        __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+        float* dz = gv;  // DZ overwrites the gate values in place (unit by unit)
+        if (active) {
+          const bool last = (s == len - 1);
+#pragma unroll
+          for (int u = 0; u < UT; ++u) {
+            float gh = dh[u] + dyv[u];
+            float gc = gcar[u];
+            if (last && a.dh_last) gh += a.dh_last[((size_t)d * a.B + row) * H + ut0 + u];
+            if (last && a.dc_last) gc += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
+            const float gi = gv[u], gf = gv[UT + u], gg = gv[2 * UT + u], go = gv[3 * UT + u];
+            const float tcv = tc::tanh_approx(fmaf(gf, cp[u], gi * gg));
+            const float d_o = gh * tcv;                               // tape.cpp:1161
+            const float dcn = gc + gh * go * (1.f - tcv * tcv);       // tape.cpp:1162
+            gcar[u] = dcn * gf;                                       // tape.cpp:1166
+            dz[u] = dcn * gg * gi * (1.f - gi);                       // tape.cpp:1167
+            dz[UT + u] = dcn * cp[u] * gf * (1.f - gf);               // tape.cpp:1168
+            dz[2 * UT + u] = dcn * gi * (1.f - gg * gg);              // tape.cpp:1169
+            dz[3 * UT + u] = d_o * go * (1.f - go);                   // tape.cpp:1170
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4 * UT; ++j) dz[j] = 0.f;
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          store_bf16<UT>(zn + g * H, dz + g * UT, nu);
+          store_bf16<UT>(zc + g * H, dz + g * UT, nu);
+        }
+      }
+      named_sync(1 + mt, kEpi / MT);
+      if ((e % (4 * SPLIT)) == 0 && lane == 0) {
+        tc::fence_proxy_async_global();
+        red_release_gpu(ctr + mt, 1u);
+      }
+    }
+    if (valid_row) {  // DZ rows of positions beyond the longest sequence
+      float zero[UT];
+#pragma unroll
+      for (int u = 0; u < UT; ++u) zero[u] = 0.f;
+      for (int s = Tmax; s < T; ++s) {
+        __nv_bfloat16* zc =
+            a.dzcat + ((size_t)row * T + s) * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) store_bf16<UT>(zc + g * H, zero, nu);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+// RB[c*NB + u][j] = R[c*U + u][j] (bf16; zero rows for u >= U or unit >= H, zero cols j >= 4H)
+__global__ void pack_rb_kernel(const float* __restrict__ R, int H, int U, int NB, int P, int Kz,
+                               __nv_bfloat16* __restrict__ RB) {
+  const int64_t n = (int64_t)P * NB * Kz;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % Kz);
+    const int r = (int)(e / Kz);
+    const int c = r / NB, u = r % NB;
+    const int unit = c * U + u;
+    float v = 0.f;
+    if (u < U && unit < H && j < 4 * H) v = R[(int64_t)unit * 4 * H + j];
+    RB[e] = __float2bfloat16_rn(v);
+  }
+}
+
+template <int U, int MT>
+void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs& a,
+                cudaStream_t stream) {
+  auto kern = rec_bwd_tc_kernel<U, MT>;
+  constexpr int NB = U < 16 ? 16 : U;
+  const uint32_t smem = bwd_smem(NB, a.Kz, a.stages);
+  SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  TcRecBwdArgs copy = a;
+  CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[a.nd > 1 ? 1 : 0];
+  void* params[] = {&r0, &r1, &z0, &z1, &copy};
+  constexpr int kSplit = U >= 8 ? 2 : 1;
+  SL_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(a.P * a.nd),
+                                          dim3(64 + 128 * MT * kSplit), params, smem, stream));
+  count_launch();
+}
+
+}  // namespace
+
+size_t tc_rec_bwd_pack_elems(int H, int U) {
+  const int NB = U < 16 ? 16 : U;
+  return (size_t)ceil_div(H, U) * NB * round_up(4 * (int64_t)H, 64);
+}
+
+void tc_rec_bwd_pack(const float* R, int H, int U, __nv_bfloat16* RB, cudaStream_t stream) {
+  const int NB = U < 16 ? 16 : U;
+  const int P = (int)ceil_div(H, U);
+  const int Kz = (int)round_up(4 * (int64_t)H, 64);
+  const int64_t n = (int64_t)P * NB * Kz;
+  pack_rb_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, stream>>>(
+      R, H, U, NB, P, Kz, RB);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
+
+bool tc_rec_bwd_fits(int H, int U) {
+  const int NB = U < 16 ? 16 : U;
+  return bwd_smem(NB, (int)round_up(4 * (int64_t)H, 64), 2) <= kSmemMax;
+}
+
+void rec_bwd_tc(const TcRecBwdArgs& a0, __nv_bfloat16* const* RB, cudaStream_t stream) {
+  TcRecBwdArgs a = a0;
+  const int NB = a.U < 16 ? 16 : a.U;
+  CUtensorMap tr[2], tz[2];
+  for (int k = 0; k < a.nd; ++k) {
+    cuuint64_t rd[2] = {(cuuint64_t)a.Kz, (cuuint64_t)a.P * NB};
+    cuuint64_t rs[1] = {(cuuint64_t)a.Kz * 2};
+    cuuint32_t rb[2] = {64, (cuuint32_t)NB};
+    tr[k] = tmap(RB[k], 2, rd, rs, rb);
+    cuuint64_t zd[3] = {(cuuint64_t)a.Kz, (cuuint64_t)a.B, 2};
+    cuuint64_t zs[2] = {(cuuint64_t)a.Kz * 2, (cuuint64_t)a.Kz * 2 * a.B};
+    cuuint32_t zb[3] = {64, 128, 1};
+    tz[k] = tmap(a.dzring[k], 3, zd, zs, zb);
+  }
+  a.stages = 0;
+  for (int st = kStages; st >= 2 && !a.stages; --st)
+    if (bwd_smem(NB, a.Kz, st) <= kSmemMax) a.stages = st;
+  SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
+  unsigned* bar0 = a.bar;
+  for (int b0 = 0; b0 < a.B; b0 += 256) {
+    a.b0 = b0;
+    a.bar = bar0 + 4 * (b0 / 256);
+    const int MT = (a.B - b0) > 128 ? 2 : 1;
+    switch (a.U * 10 + MT) {
+      case 41: launch_bwd<4, 1>(tr, tz, a, stream); break;
+      case 42: launch_bwd<4, 2>(tr, tz, a, stream); break;
+      case 81: launch_bwd<8, 1>(tr, tz, a, stream); break;
+      case 82: launch_bwd<8, 2>(tr, tz, a, stream); break;
+      case 161: launch_bwd<16, 1>(tr, tz, a, stream); break;
+      case 162: launch_bwd<16, 2>(tr, tz, a, stream); break;
+      default: throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_tc: unsupported units per CTA"};
+    }
+  }
+}
+
+}  // namespace sl

@@ -1,0 +1,142 @@
+// Helpers shared by the tensor-core recurrence kernels (rec_tc.cu, rec_tc_bwd.cu).
+#pragma once
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace sl {
+namespace rtc {
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(tc::smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SL_TRACE(k)                                                          \
+  do {                                                                       \
+    if (a.trace && blockIdx.x == a.trace_cta) a.trace[s * 8 + (k)] = gtimer(); \
+  } while (0)
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Row-segment stores: 16 B vectors when the destination is aligned and the
+// CTA's unit slice is full, scalar otherwise (odd H / last CTA).
+template <int U>
+__device__ __forceinline__ void store_f32(float* dst, const float* v, int nu) {
+  if (nu == U && (U % 4) == 0 && ((uintptr_t)dst & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 4)
+      *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  } else {
+    for (int i = 0; i < nu; ++i) dst[i] = v[i];
+  }
+}
+template <int U>
+__device__ __forceinline__ void store_bf16(__nv_bfloat16* dst, const float* v, int nu) {
+  if (nu == U && (U % 8) == 0 && ((uintptr_t)dst & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 8) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
+      __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+      uint4 w;
+      w.x = *reinterpret_cast<uint32_t*>(&p0);
+      w.y = *reinterpret_cast<uint32_t*>(&p1);
+      w.z = *reinterpret_cast<uint32_t*>(&p2);
+      w.w = *reinterpret_cast<uint32_t*>(&p3);
+      *reinterpret_cast<uint4*>(dst + i) = w;
+    }
+  } else if (nu == U && (U % 4) == 0 && ((uintptr_t)dst & 7) == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 4) {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+      __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&p0);
+      w.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(dst + i) = w;
+    }
+  } else {
+    for (int i = 0; i < nu; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+template <int U>
+__device__ __forceinline__ void load_f32(const float* src, float* v, int nu, bool vec) {
+  if (vec && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
+      v[i] = x.x;
+      v[i + 1] = x.y;
+      v[i + 2] = x.z;
+      v[i + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < U; ++i) v[i] = (i < nu) ? __ldg(src + i) : 0.f;
+  }
+}
+
+template <int n>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[n]) {
+  if constexpr (n == 8) {
+    tc::tmem_ld_32x32b_x8(taddr, v);
+  } else if constexpr (n == 4) {
+    tc::tmem_ld_32x32b_x4(taddr, v);
+  } else if constexpr (n == 16) {
+    tc::tmem_ld_32x32b_x16(taddr, v);
+  } else {
+    static_assert(n == 2, "unsupported tmem load width");
+    tc::tmem_ld_32x32b_x2(taddr, v);
+  }
+}
+
+
+// ---- host: TMA descriptors (bf16, SWIZZLE_128B unless stated)
+inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    SL_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    SL_REQUIRE(q == cudaDriverEntryPointSuccess && f, SL_ERR_CUDA, "cuTensorMapEncodeTiled missing");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+inline CUtensorMap tmap(const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                 const cuuint32_t* box) {
+  CUtensorMap m;
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SL_REQUIRE(r == CUDA_SUCCESS, SL_ERR_CUDA, "cuTensorMapEncodeTiled failed (recurrence)");
+  return m;
+}
+
+
+}  // namespace rtc
+}  // namespace sl
