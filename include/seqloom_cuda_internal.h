@@ -15,6 +15,9 @@ int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn
 /* Debug: record per-step globaltimer stamps of CTA `cta` of the recurrence
  * kernels into dev_buf[T][8] (NULL disables). */
 int sl_debug_set_trace(unsigned long long* dev_buf, int cta);
+/* Experiments only (results become wrong): 1 = skip the recurrence MMAs,
+ * 2 = skip the recurrence epilogue math/stores. */
+int sl_debug_set_flags(int flags);
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@ namespace sl {
 static thread_local std::string g_last_error;
 static unsigned long long* g_rec_trace = nullptr;  // debug: sl_debug_set_trace
 static int g_rec_trace_cta = 0;
+static int g_rec_debug_flags = 0;  // experiments only (sl_debug_set_flags)
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 namespace {
@@ -152,7 +153,7 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
     SL_REQUIRE(U > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     for (int k = 0; k < d.nd; ++k) {
       w.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(d.H, U));
-      w.hbufb[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * round_up(d.H, 64));
+      w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, d.H));
     }
   } else {
     w.xw_ld = 4 * d.H;
@@ -182,13 +183,12 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
   w.bar = c.take<unsigned>(64);
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
-    const int U = tc_rec_units(d.H, d.nd, sm_count());
-    SL_REQUIRE(U > 0 && tc_rec_bwd_fits(d.H, U), SL_ERR_UNSUPPORTED,
-               "bf16 recurrence: hidden size too large for one launch");
+    const TcBwdShape sh = tc_rec_bwd_shape(d.H, d.nd, sm_count());
+    SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     w.dzb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
     for (int k = 0; k < d.nd; ++k) {
-      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * round_up(4 * (int64_t)d.H, 64));
-      w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(d.H, U));
+      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * sh.Kz);
+      w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(sh));
     }
   } else {
     for (int k = 0; k < d.nd; ++k) {
@@ -331,7 +331,8 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       for (int k = 0; k < d.nd; ++k) {
         rt[k] = rv.rt[k] ? rv.rt[k] : w.rt[k];
         tc_rec_pack(R[k], d.H, a.U, rt[k], stream);
-        SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kp, stream));
+        SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, d.H),
+                                    stream));
         a.dirsign[k] = dir_sign(L, k);
         a.xw[k] = w.xw[k];
         a.hbuf[k] = w.hbufb[k];
@@ -341,6 +342,7 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       }
       a.trace = g_rec_trace;
       a.trace_cta = g_rec_trace_cta;
+      a.debug_flags = g_rec_debug_flags;
       Phase ph(stream, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd);
       rec_fwd_tc(a, rt, stream);
       return;
@@ -408,9 +410,10 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       a.T = d.T;
       a.H = d.H;
       a.nd = d.nd;
-      a.U = tc_rec_units(d.H, d.nd, sm_count());
-      a.P = (int)ceil_div(d.H, a.U);
-      a.Kz = (int)round_up(4 * (int64_t)d.H, 64);
+      const TcBwdShape sh = tc_rec_bwd_shape(d.H, d.nd, sm_count());
+      a.U = sh.U;
+      a.P = sh.P;
+      a.Kz = sh.Kz;
       a.lens = seq_lens;
       a.dy = dy;
       a.dy_ld = (int64_t)d.nd * d.H;
@@ -424,7 +427,7 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       a.trace_cta = g_rec_trace_cta;
       if (pd.G4p != G) SL_CUDA_TRY(cudaMemsetAsync(w.dzb, 0, sizeof(__nv_bfloat16) * M * pd.Gc, stream));
       for (int k = 0; k < d.nd; ++k) {
-        tc_rec_bwd_pack(R[k], d.H, a.U, w.rb[k], stream);
+        tc_rec_bwd_pack(R[k], d.H, sh, w.rb[k], stream);
         SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kz, stream));
         a.dirsign[k] = dir_sign(L, k);
         a.gates[k] = rv.gates[k];
@@ -433,7 +436,7 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       }
       {
         Phase ph(stream, "k3_rec_bwd", rec_flops);
-        rec_bwd_tc(a, w.rb, stream);
+        rec_bwd_tc(a, sh, w.rb, stream);
       }
       // K4 on tensor cores: DZ of both directions side by side -> one dX GEMM;
       // dW and db from ONE GEMM over [X | 1] (the ones column yields colsum(DZ)).
@@ -561,5 +564,10 @@ extern "C" int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t ld
 extern "C" int sl_debug_set_trace(unsigned long long* dev_buf, int cta) {
   g_rec_trace = dev_buf;
   g_rec_trace_cta = cta;
+  return 0;
+}
+
+extern "C" int sl_debug_set_flags(int flags) {
+  g_rec_debug_flags = flags;
   return 0;
 }

@@ -30,6 +30,9 @@ namespace {
 using namespace rtc;
 
 constexpr int kStages = 6;  // max h-tile ring depth
+// h_s is written to kHCopies replicas of the ring and CTA c reads replica
+// c % kHCopies: ~P/kHCopies CTAs (not all P) request each L2 line per step.
+constexpr int kHCopies = 4;
 constexpr uint32_t kHTileBytes = 128 * 64 * 2;  // 128 rows x 64 K bf16 = 16 KB
 constexpr uint32_t kSmemMax = 227 * 1024;
 
@@ -119,12 +122,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             }
             tc::fence_proxy_async_global();
           }
-          if (mt == 0) SL_TRACE(0);
+          SL_TRACE(mt == 0 ? 0 : 3);
           for (int kq = 0; kq < nkc; ++kq) {
             const int kc = (kq + kc_off) % nkc;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             tc::mbar_arrive_expect_tx(&full_bar[st], kHTileBytes);
-            tma_load_3d(sH + st * kHTileBytes, tmH, &full_bar[st], kc * 64, a.b0 + mt * 128, slot);
+            tma_load_3d(sH + st * kHTileBytes, tmH, &full_bar[st], kc * 64, a.b0 + mt * 128,
+                        (cta % kHCopies) * 2 + slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -148,9 +152,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kc = (kq + kc_off) % nkc;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            if (mt == 0 && kq == 0) SL_TRACE(1);
+            if (kq == 0) SL_TRACE(mt == 0 ? 1 : 4);
+            if (kq == nkc - 1) SL_TRACE(mt == 0 ? 2 : 5);
             const uint32_t sa = base + r_bytes + st * kHTileBytes;
             const uint32_t sb = base + (uint32_t)kc * N * 128;
+            if (!(a.debug_flags & 1))
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc::mma_f16(tmem + mt * N, tc::make_sdesc(sa + k * 32, 0, 1024),
@@ -161,7 +167,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               ph ^= 1;
             }
           }
-          if (mt == MT - 1) SL_TRACE(2);
           tc::mma_commit(&tfull_bar[mt]);
         }
       }
@@ -216,7 +221,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       float z[4 * UT];
       tc::mbar_wait(&tfull_bar[mt], s & 1);
       tc::fence_after_sync();
-      if (e == 0 && lane == 0) SL_TRACE(3);
       {
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * N + lo;
 #pragma unroll
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
 
-      if (valid_row) {
+      if (valid_row && !(a.debug_flags & 2)) {
         __nv_bfloat16* hn = hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0;
         if (active) {
           if (save) {  // c_{s-1}, h_{s-1} before the update
@@ -266,15 +270,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
           if (save) store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
         }
-        store_bf16<UT>(hn, hst, nu);
+#pragma unroll
+        for (int cp = 0; cp < kHCopies; ++cp) store_bf16<UT>(hn + (size_t)cp * 2 * a.B * a.Kp, hst, nu);
       }
-      if (e == 0 && lane == 0) SL_TRACE(4);
       named_sync(1 + mt, kEpi / MT);  // the tile's epilogue threads only
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
-        if (e == 0) SL_TRACE(5);
         tc::fence_proxy_async_global();
         red_release_gpu(ctr + mt, 1u);
-        if (e == 0) SL_TRACE(6);
+        SL_TRACE(6 + mt);
       }
     }
     // positions beyond the longest sequence, final states
@@ -341,6 +344,8 @@ int tc_rec_units(int H, int nd, int sms) {
   return 0;
 }
 
+size_t tc_rec_hbuf_elems(int B, int H) { return (size_t)kHCopies * 2 * B * round_up(H, 64); }
+
 size_t tc_rec_pack_elems(int H, int U) {
   const int P = (int)ceil_div(H, U);
   return (size_t)P * 4 * U * round_up(H, 64);
@@ -365,7 +370,7 @@ void rec_fwd_tc(const TcRecFwdArgs& a0, __nv_bfloat16* const* RT, cudaStream_t s
     cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)N};
     tr[k] = tmap(RT[k], 2, rd, rs, rb);
-    cuuint64_t hd[3] = {(cuuint64_t)a.Kp, (cuuint64_t)a.B, 2};
+    cuuint64_t hd[3] = {(cuuint64_t)a.Kp, (cuuint64_t)a.B, (cuuint64_t)2 * kHCopies};
     cuuint64_t hs[2] = {(cuuint64_t)a.Kp * 2, (cuuint64_t)a.Kp * 2 * a.B};
     cuuint32_t hbx[3] = {64, 128, 1};
     th[k] = tmap(a.hbuf[k], 3, hd, hs, hbx);

@@ -23,10 +23,11 @@ struct TcRecFwdArgs {
   float* cprev[2];            // saved c_{s-1} fp32 [B*T, H]
   __nv_bfloat16* hprev[2];    // saved h_{s-1} bf16 [B*T, hprev_ld] (dR GEMM operand)
   int64_t hprev_ld;
-  __nv_bfloat16* hbuf[2];     // ring [2][B][Kp] bf16, zeroed
+  __nv_bfloat16* hbuf[2];     // ring [kHCopies][2][B][Kp] bf16, zeroed (tc_rec_hbuf_elems)
   unsigned* bar;              // zeroed step counters, 2 per batch chunk
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;
+  int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores (wrong results)
 };
 
 struct TcRecBwdArgs {
@@ -50,10 +51,20 @@ struct TcRecBwdArgs {
   int trace_cta;
 };
 
-size_t tc_rec_bwd_pack_elems(int H, int U);
-void tc_rec_bwd_pack(const float* R, int H, int U, __nv_bfloat16* RB, cudaStream_t stream);
-bool tc_rec_bwd_fits(int H, int U);
-void rec_bwd_tc(const TcRecBwdArgs& a, __nv_bfloat16* const* RB, cudaStream_t stream);
+// K-split partition of the BPTT kernel: clusters of C CTAs, each finalizing U
+// units, P CTAs per direction, Kz = gate columns padded to 64*C.
+struct TcBwdShape {
+  int C, U, P, Kz;
+};
+TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms);  // C == 0: unsupported
+size_t tc_rec_bwd_pack_elems(const TcBwdShape& sh);
+void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB,
+                     cudaStream_t stream);
+void rec_bwd_tc(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* const* RB,
+                cudaStream_t stream);
+
+// Elements of one direction's h ring (all replicas).
+size_t tc_rec_hbuf_elems(int B, int H);
 
 // Units per CTA for the tensor-core recurrence (0 = shape unsupported).
 int tc_rec_units(int H, int nd, int sms);

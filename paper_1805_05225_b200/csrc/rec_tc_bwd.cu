@@ -27,35 +27,48 @@ constexpr int kStages = 6;
 constexpr uint32_t kTile = 128 * 64 * 2;  // 16 KB A tile
 constexpr uint32_t kSmemMax = 227 * 1024;
 
-uint32_t bwd_smem(int NB, int Kz, int stages) { return (uint32_t)NB * Kz * 2 + stages * kTile + 1024; }
+__host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
-template <int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
+uint32_t bwd_smem(int C, int U, int Kc, int stages) {
+  const uint32_t recv = C > 1 ? (uint32_t)C * U * 128 * 4 : 0;
+  return (uint32_t)nb_of(C, U) * Kc * 2 + stages * kTile + recv + 1024;
+}
+
+// C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
+// U   hidden units each CTA finalizes (the cluster owns C*U units)
+// MT  128-row batch tiles per launch
+template <int C, int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
 __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     rec_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
                       const __grid_constant__ CUtensorMap tmR1,
                       const __grid_constant__ CUtensorMap tmZ0,
                       const __grid_constant__ CUtensorMap tmZ1, TcRecBwdArgs a) {
-  constexpr int NB = U < 16 ? 16 : U;  // MMA N (M = 128 needs N % 16 == 0)
-  constexpr int kEpi = 128 * MT * SPLIT;
-  constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : 64;
+  constexpr int NB = nb_of(C, U);  // MMA N: the cluster's units
+  constexpr int kEpiTile = 128 * SPLIT;
+  constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : (MT * NB <= 64) ? 64 : (MT * NB <= 128) ? 128 : 256;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar[MT], tempty_bar[MT];
+  __shared__ __align__(8) uint64_t recv_full, free_bar[C];
   __shared__ uint32_t tmem_sh;
   __shared__ int tmax_sh;
 
   const int d = blockIdx.x / a.P;
-  const int cta = blockIdx.x % a.P;
-  const int u0 = cta * U;
+  const int cta = blockIdx.x % a.P;        // CTA index within the direction
+  const int r = C > 1 ? (int)cluster_rank() : 0;  // K-slice of this CTA
+  const int cl = cta / C;                  // cluster index within the direction
+  const int u0 = cl * C * U + r * U;       // first unit this CTA finalizes
+  const int Kc = a.Kz / C;
   const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
   const CUtensorMap* tmZ = d == 0 ? &tmZ0 : &tmZ1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
-  const uint32_t r_bytes = (uint32_t)NB * a.Kz * 2;
+  const uint32_t r_bytes = (uint32_t)NB * Kc * 2;
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
-  const int nkc = a.Kz / 64;
+  float* recv = reinterpret_cast<float*>(sA + a.stages * kTile);  // [C][U][128] partials from peers
+  const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
@@ -68,13 +81,16 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     tc::mbar_init(&r_bar, 1);
     for (int m = 0; m < MT; ++m) {
       tc::mbar_init(&tfull_bar[m], 1);
-      tc::mbar_init(&tempty_bar[m], kEpi / MT);
+      tc::mbar_init(&tempty_bar[m], kEpiTile);
     }
+    tc::mbar_init(&recv_full, (C - 1) * kEpiTile);
+    for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[p], kEpiTile);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
   tc::fence_before_sync();
   __syncthreads();
+  if constexpr (C > 1) cluster_sync();  // peers' barriers are initialized before any remote arrive
   tc::fence_after_sync();
   {
     int m = 0;
@@ -104,12 +120,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             }
             tc::fence_proxy_async_global();
           }
-          if (mt == 0) SL_TRACE(0);
+          SL_TRACE(mt == 0 ? 0 : 3);
           for (int kq = 0; kq < nkc; ++kq) {
             const int kc = (kq + kc_off) % nkc;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             tc::mbar_arrive_expect_tx(&full_bar[st], kTile);
-            tma_load_3d(sA + st * kTile, tmZ, &full_bar[st], kc * 64, a.b0 + mt * 128, slot);
+            tma_load_3d(sA + st * kTile, tmZ, &full_bar[st], r * Kc + kc * 64, a.b0 + mt * 128, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -133,7 +149,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kc = (kq + kc_off) % nkc;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            if (mt == 0 && kq == 0) SL_TRACE(1);
+            if (kq == 0) SL_TRACE(mt == 0 ? 1 : 4);
+            if (kq == nkc - 1) SL_TRACE(mt == 0 ? 2 : 5);
             const uint32_t sa = base + r_bytes + st * kTile;
             const uint32_t sb = base + (uint32_t)kc * NB * 128;
 #pragma unroll
@@ -146,7 +163,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               ph ^= 1;
             }
           }
-          if (mt == MT - 1) SL_TRACE(2);
           tc::mma_commit(&tfull_bar[mt]);
         }
       }
@@ -156,7 +172,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     const int mt = e / (4 * SPLIT);
     const int half = (e / 4) % SPLIT;
     const int q = warp & 3;
-    const int row = a.b0 + mt * 128 + q * 32 + lane;
+    const int rl = q * 32 + lane;  // row within the tile
+    const int row = a.b0 + mt * 128 + rl;
     const bool valid_row = row < a.B;
     const int len = valid_row ? a.lens[row] : 0;
     const int dir = a.dirsign[d];
@@ -167,12 +184,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     __nv_bfloat16* zr = a.dzring[d];
     const float* gates = a.gates[d];
     const float* cprev = a.cprev[d];
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * NB;
     float gcar[UT];
 #pragma unroll
     for (int u = 0; u < UT; ++u) gcar[u] = 0.f;
 
     for (int it = 0; it < Tmax; ++it) {
       const int s = Tmax - 1 - it;  // processing step
+      const int use = it * MT + mt;  // index of this tile's use of the shared exchange buffer
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
@@ -186,11 +205,48 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                      vec && (a.dy_ld % 4) == 0);
       }
       float dh[UT];
+      const bool tr0 = a.trace && blockIdx.x == a.trace_cta && e == 0 && lane == 0;
+      if (tr0) a.trace[it * 16 + 12] = gtimer();
       tc::mbar_wait(&tfull_bar[mt], it & 1);
       tc::fence_after_sync();
-      tmem_ld_cols<UT>(tmem + ((uint32_t)(q * 32) << 16) + mt * NB + lo, dh);
+      if (tr0) a.trace[it * 16 + 8] = gtimer();
+      if constexpr (C > 1) {
+        // reduce-scatter of the K-split partials: send each peer the columns of
+        // the units it finalizes (coalesced: a warp writes 32 consecutive rows)
+#pragma unroll 1
+        for (int pi = 1; pi < C; ++pi) {
+          const int p = (r + pi) % C;
+          if (use > 0) mbar_wait_cluster(&free_bar[p], (use - 1) & 1);
+          float v[UT];
+          tmem_ld_cols<UT>(tbase + p * U + lo, v);
+          const uint32_t dst = mapa(tc::smem_u32(recv + ((size_t)r * U + lo) * 128 + rl), p);
+#pragma unroll
+          for (int u = 0; u < UT; ++u) st_cluster_f32(dst + u * 128 * 4, v[u]);
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int pi = 1; pi < C; ++pi)
+            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full), (r + pi) % C), 32);
+      }
+      if (tr0) a.trace[it * 16 + 9] = gtimer();
+      tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
+      if constexpr (C > 1) {
+        mbar_wait_cluster(&recv_full, use & 1);
+        if (tr0) a.trace[it * 16 + 10] = gtimer();
+#pragma unroll 1
+        for (int pi = 1; pi < C; ++pi) {
+          const int p = (r + pi) % C;
+          const float* src = recv + ((size_t)p * U + lo) * 128 + rl;
+#pragma unroll
+          for (int u = 0; u < UT; ++u) dh[u] += src[u * 128];
+        }
+        __syncwarp();
+        if (lane == 0)  // tell every sender its slot in my buffer is free again
+          for (int pi = 1; pi < C; ++pi)
+            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[r]), (r + pi) % C), 32);
+      }
 
       if (valid_row) {
         __nv_bfloat16* zn = zr + ((size_t)((it + 1) & 1) * a.B + row) * a.Kz + ut0;
@@ -206,13 +262,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             if (last && a.dc_last) gc += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
             const float gi = gv[u], gf = gv[UT + u], gg = gv[2 * UT + u], go = gv[3 * UT + u];
             const float tcv = tc::tanh_approx(fmaf(gf, cp[u], gi * gg));
-            const float d_o = gh * tcv;                               // tape.cpp:1161
-            const float dcn = gc + gh * go * (1.f - tcv * tcv);       // tape.cpp:1162
-            gcar[u] = dcn * gf;                                       // tape.cpp:1166
-            dz[u] = dcn * gg * gi * (1.f - gi);                       // tape.cpp:1167
-            dz[UT + u] = dcn * cp[u] * gf * (1.f - gf);               // tape.cpp:1168
-            dz[2 * UT + u] = dcn * gi * (1.f - gg * gg);              // tape.cpp:1169
-            dz[3 * UT + u] = d_o * go * (1.f - go);                   // tape.cpp:1170
+            const float d_o = gh * tcv;                          // tape.cpp:1161
+            const float dcn = gc + gh * go * (1.f - tcv * tcv);  // tape.cpp:1162
+            gcar[u] = dcn * gf;                                  // tape.cpp:1166
+            dz[u] = dcn * gg * gi * (1.f - gi);                  // tape.cpp:1167
+            dz[UT + u] = dcn * cp[u] * gf * (1.f - gf);          // tape.cpp:1168
+            dz[2 * UT + u] = dcn * gi * (1.f - gg * gg);         // tape.cpp:1169
+            dz[3 * UT + u] = d_o * go * (1.f - go);              // tape.cpp:1170
           }
         } else {
 #pragma unroll
@@ -224,10 +280,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           store_bf16<UT>(zc + g * H, dz + g * UT, nu);
         }
       }
-      named_sync(1 + mt, kEpi / MT);
+      if (tr0) a.trace[it * 16 + 11] = gtimer();
+      named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
         red_release_gpu(ctr + mt, 1u);
+        if (a.trace && blockIdx.x == a.trace_cta) a.trace[it * 16 + 6 + mt] = gtimer();
       }
     }
     if (valid_row) {  // DZ rows of positions beyond the longest sequence
@@ -243,71 +301,101 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     }
   }
   __syncthreads();
+  if constexpr (C > 1) cluster_sync();  // no CTA leaves while a peer may still touch its smem
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
-// RB[c*NB + u][j] = R[c*U + u][j] (bf16; zero rows for u >= U or unit >= H, zero cols j >= 4H)
-__global__ void pack_rb_kernel(const float* __restrict__ R, int H, int U, int NB, int P, int Kz,
-                               __nv_bfloat16* __restrict__ RB) {
-  const int64_t n = (int64_t)P * NB * Kz;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+// RB[(cl*C + r)*NB + n][kk] = R[cl*C*U + n][r*Kc + kk]  (bf16; zero outside the layer)
+__global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U, int NB, int P,
+                               int Kc, __nv_bfloat16* __restrict__ RB) {
+  const int64_t n_el = (int64_t)P * NB * Kc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(e % Kz);
-    const int r = (int)(e / Kz);
-    const int c = r / NB, u = r % NB;
-    const int unit = c * U + u;
+    const int kk = (int)(e % Kc);
+    const int rowi = (int)(e / Kc);
+    const int cta = rowi / NB, n = rowi % NB;
+    const int cl = cta / C, r = cta % C;
+    const int unit = cl * C * U + n;
+    const int j = r * Kc + kk;
     float v = 0.f;
-    if (u < U && unit < H && j < 4 * H) v = R[(int64_t)unit * 4 * H + j];
+    if (n < C * U && unit < H && j < 4 * H) v = R[(int64_t)unit * 4 * H + j];
     RB[e] = __float2bfloat16_rn(v);
   }
 }
 
-template <int U, int MT>
+template <int C, int U, int MT>
 void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs& a,
                 cudaStream_t stream) {
-  auto kern = rec_bwd_tc_kernel<U, MT>;
-  constexpr int NB = U < 16 ? 16 : U;
-  const uint32_t smem = bwd_smem(NB, a.Kz, a.stages);
+  auto kern = rec_bwd_tc_kernel<C, U, MT>;
+  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.stages);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (C > 1)
+    SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   TcRecBwdArgs copy = a;
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[a.nd > 1 ? 1 : 0];
-  void* params[] = {&r0, &r1, &z0, &z1, &copy};
   constexpr int kSplit = U >= 8 ? 2 : 1;
-  SL_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(a.P * a.nd),
-                                          dim3(64 + 128 * MT * kSplit), params, smem, stream));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.P * a.nd);
+  cfg.blockDim = dim3(64 + 128 * MT * kSplit);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+  attrs[0].val.cooperative = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = C;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, z0, z1, copy));
   count_launch();
 }
 
 }  // namespace
 
-size_t tc_rec_bwd_pack_elems(int H, int U) {
-  const int NB = U < 16 ? 16 : U;
-  return (size_t)ceil_div(H, U) * NB * round_up(4 * (int64_t)H, 64);
+TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms) {
+  // Prefer 4-CTA clusters (4x less DZ per CTA); most CTAs that fit a cluster
+  // grid (~128 SMs usable by 4-CTA clusters on 148 SMs) and shared memory.
+  for (int C : {4, 2, 1}) {
+    const int usable = C == 4 ? std::min(sms, 128) : sms;
+    for (int U : {4, 8, 16}) {
+      const int P = (int)ceil_div(H, (int64_t)C * U) * C;
+      const int Kz = (int)round_up(4 * (int64_t)H, 64 * C);
+      if ((int64_t)P * nd <= usable && bwd_smem(C, U, Kz / C, 2) <= kSmemMax)
+        return TcBwdShape{C, U, P, Kz};
+    }
+  }
+  return TcBwdShape{0, 0, 0, 0};
 }
 
-void tc_rec_bwd_pack(const float* R, int H, int U, __nv_bfloat16* RB, cudaStream_t stream) {
-  const int NB = U < 16 ? 16 : U;
-  const int P = (int)ceil_div(H, U);
-  const int Kz = (int)round_up(4 * (int64_t)H, 64);
-  const int64_t n = (int64_t)P * NB * Kz;
+size_t tc_rec_bwd_pack_elems(const TcBwdShape& sh) {
+  return (size_t)sh.P * nb_of(sh.C, sh.U) * (sh.Kz / sh.C);
+}
+
+void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB,
+                     cudaStream_t stream) {
+  const int NB = nb_of(sh.C, sh.U);
+  const int Kc = sh.Kz / sh.C;
+  const int64_t n = (int64_t)sh.P * NB * Kc;
   pack_rb_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, stream>>>(
-      R, H, U, NB, P, Kz, RB);
+      R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
 
-bool tc_rec_bwd_fits(int H, int U) {
-  const int NB = U < 16 ? 16 : U;
-  return bwd_smem(NB, (int)round_up(4 * (int64_t)H, 64), 2) <= kSmemMax;
-}
-
-void rec_bwd_tc(const TcRecBwdArgs& a0, __nv_bfloat16* const* RB, cudaStream_t stream) {
+void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* const* RB,
+                cudaStream_t stream) {
   TcRecBwdArgs a = a0;
-  const int NB = a.U < 16 ? 16 : a.U;
+  a.U = sh.U;
+  a.P = sh.P;
+  a.Kz = sh.Kz;
+  const int NB = nb_of(sh.C, sh.U);
+  const int Kc = sh.Kz / sh.C;
   CUtensorMap tr[2], tz[2];
   for (int k = 0; k < a.nd; ++k) {
-    cuuint64_t rd[2] = {(cuuint64_t)a.Kz, (cuuint64_t)a.P * NB};
-    cuuint64_t rs[1] = {(cuuint64_t)a.Kz * 2};
+    cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)a.P * NB};
+    cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
     tr[k] = tmap(RB[k], 2, rd, rs, rb);
     cuuint64_t zd[3] = {(cuuint64_t)a.Kz, (cuuint64_t)a.B, 2};
@@ -317,21 +405,24 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, __nv_bfloat16* const* RB, cudaStream_t s
   }
   a.stages = 0;
   for (int st = kStages; st >= 2 && !a.stages; --st)
-    if (bwd_smem(NB, a.Kz, st) <= kSmemMax) a.stages = st;
+    if (bwd_smem(sh.C, sh.U, Kc, st) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
     a.bar = bar0 + 4 * (b0 / 256);
     const int MT = (a.B - b0) > 128 ? 2 : 1;
-    switch (a.U * 10 + MT) {
-      case 41: launch_bwd<4, 1>(tr, tz, a, stream); break;
-      case 42: launch_bwd<4, 2>(tr, tz, a, stream); break;
-      case 81: launch_bwd<8, 1>(tr, tz, a, stream); break;
-      case 82: launch_bwd<8, 2>(tr, tz, a, stream); break;
-      case 161: launch_bwd<16, 1>(tr, tz, a, stream); break;
-      case 162: launch_bwd<16, 2>(tr, tz, a, stream); break;
-      default: throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_tc: unsupported units per CTA"};
+    const int key = sh.C * 1000 + sh.U * 10 + MT;
+    switch (key) {
+#define SL_BWD_CASE(C_, U_, MT_) \
+  case C_ * 1000 + U_ * 10 + MT_: launch_bwd<C_, U_, MT_>(tr, tz, a, stream); break;
+      SL_BWD_CASE(4, 4, 1) SL_BWD_CASE(4, 4, 2) SL_BWD_CASE(4, 8, 1) SL_BWD_CASE(4, 8, 2)
+      SL_BWD_CASE(4, 16, 1) SL_BWD_CASE(4, 16, 2) SL_BWD_CASE(2, 4, 1) SL_BWD_CASE(2, 4, 2)
+      SL_BWD_CASE(2, 8, 1) SL_BWD_CASE(2, 8, 2) SL_BWD_CASE(2, 16, 1) SL_BWD_CASE(2, 16, 2)
+      SL_BWD_CASE(1, 4, 1) SL_BWD_CASE(1, 4, 2) SL_BWD_CASE(1, 8, 1) SL_BWD_CASE(1, 8, 2)
+      SL_BWD_CASE(1, 16, 1) SL_BWD_CASE(1, 16, 2)
+#undef SL_BWD_CASE
+      default: throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_tc: unsupported partition"};
     }
   }
 }

@@ -30,7 +30,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define SL_TRACE(k)                                                          \
   do {                                                                       \
-    if (a.trace && blockIdx.x == a.trace_cta) a.trace[s * 8 + (k)] = gtimer(); \
+    if (a.trace && blockIdx.x == a.trace_cta) a.trace[s * 16 + (k)] = gtimer(); \
   } while (0)
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
@@ -137,6 +137,48 @@ inline CUtensorMap tmap(const void* ptr, int rank, const cuuint64_t* dims, const
   return m;
 }
 
+
+}  // namespace rtc
+}  // namespace sl
+
+namespace sl {
+namespace rtc {
+
+// ---- thread-block-cluster / DSMEM primitives
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cta address -> the same variable's shared::cluster address in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// arrive (release, cluster scope) on an mbarrier of another CTA of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr, uint32_t count) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(count)
+               : "memory");
+}
+// wait with cluster-scope acquire (sees DSMEM writes released by peers)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(tc::smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 }  // namespace rtc
 }  // namespace sl

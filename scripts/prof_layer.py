@@ -5,6 +5,7 @@
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from paper_1805_05225_b200 import lstm
 
 ap = argparse.ArgumentParser()
@@ -16,6 +17,7 @@ ap.add_argument("--H", type=int, default=1000)
 ap.add_argument("--nd", type=int, default=2)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--fwd-only", action="store_true")
+ap.add_argument("--infer", action="store_true")
 a = ap.parse_args()
 B, T, D, H, nd = a.B, a.T, a.D, a.H, a.nd
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -38,24 +40,30 @@ layer.forward(x, lens, W, R, b)
 e1.record()
 torch.cuda.synchronize()
 print(f"fwd layer ms {e0.elapsed_time(e1):.3f}")
+from trace_report import report
 if os.environ.get("SL_TRACE"):
     import ctypes
     L = lstm.lib()
+    L.sl_debug_set_flags(int(os.environ.get("SL_FLAGS", "0")))
     for cta in [int(c) for c in os.environ["SL_TRACE"].split(",")]:
-        buf = torch.zeros(T * 8, dtype=torch.int64, device="cuda")
+        buf = torch.zeros(T * 16, dtype=torch.int64, device="cuda")
         L.sl_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta)
-        layer.forward(x, lens, W, R, b)
+        layer.forward(x, lens, W, R, b, train=not a.infer)
         torch.cuda.synchronize()
         L.sl_debug_set_trace(None, 0)
-        t = buf.view(T, 8).cpu().double()
-        t0 = t[0, 1].item()
-        rel = (t - t0) / 1000.0
-        print(f"cta {cta}: per-step us [wait_done, first_tile, last_mma_issued, mma_done(epi), epi_done, synced, published]")
-        for s_ in [1, 2, 30, 59]:
-            print(s_, [round(v, 2) for v in rel[s_, :7].tolist()])
-        steps = rel[2:, 0] - rel[1:-1, 0]
-        print("step period us (median):", steps.median().item())
-        print("phases median us: load", (rel[:, 1] - rel[:, 0])[1:].median().item(), "mma", (rel[:, 2] - rel[:, 1]).median().item(),
-              "to_epi", (rel[:, 3] - rel[:, 2]).median().item(), "epi", (rel[:, 4] - rel[:, 3]).median().item(),
-              "sync", (rel[:, 5] - rel[:, 4]).median().item(), "publish", (rel[:, 6] - rel[:, 5]).median().item(),
-              "wait_next", (rel[2:, 0] - rel[1:-1, 6]).median().item())
+        report(buf, T, f"fwd cta {cta}{' (inference)' if a.infer else ''}")
+if os.environ.get("SL_TRACE_BWD"):
+    import ctypes
+    L = lstm.lib()
+    for cta in [int(c) for c in os.environ["SL_TRACE_BWD"].split(",")]:
+        buf = torch.zeros(T * 16, dtype=torch.int64, device="cuda")
+        layer.forward(x, lens, W, R, b)
+        L.sl_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta)
+        layer.backward(dy)
+        torch.cuda.synchronize()
+        L.sl_debug_set_trace(None, 0)
+        report(buf, T, f"bwd cta {cta}")
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    layer.forward(x, lens, W, R, b)
+    e0.record(); layer.backward(dy); e1.record(); torch.cuda.synchronize()
+    print(f"bwd layer ms {e0.elapsed_time(e1):.3f}")
