@@ -32,7 +32,7 @@ def build(force: bool = False) -> None:
     """Compile the restatement and, when /root/reference exists, the reference."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj"):
-        targets += ["ref", "ref-tests"]
+        targets += ["ref", "ref-tests", "dropin"]
     subprocess.run(["make", "-C", HERE, "-j8"] + (["-B"] if force else []) + targets,
                    check=True, stdout=subprocess.DEVNULL)
 
