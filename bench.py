@@ -204,17 +204,13 @@ def run_ours(args, rank, world, local_rank):
         _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_int32), ("ms", ctypes.c_double),
                     ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
-    handles = []
-
-    def on_grads(l, bucket):
-        if world > 1:
-            handles.append(dist.all_reduce(bucket, async_op=True))
+    from paper_1805_05225_b200.dp import BucketAllReducer
+    red = BucketAllReducer()  # layer-bucketed NCCL all-reduce, overlapped with BPTT
 
     def step(xin):
         enc.forward(xin, lens)
-        enc.backward(dy, on_layer_grads=on_grads)
-        while handles:
-            handles.pop().wait()
+        enc.backward(dy, on_layer_grads=red)
+        red.wait()
 
     for _ in range(args.warmup):
         step(x)
@@ -259,9 +255,8 @@ def run_ours(args, rank, world, local_rank):
             y = enc.forward(xd, ld)
             loss = (y * dy).sum()  # L = sum(y . dy), so dL/dy = dy
             loss_h.copy_(loss, non_blocking=True)
-            enc.backward(dy, on_layer_grads=on_grads)
-            while handles:
-                handles.pop().wait()
+            enc.backward(dy, on_layer_grads=red)
+            red.wait()
             torch.cuda.current_stream().synchronize()  # the host reads the step's loss
             return float(loss_h)
 
