@@ -12,6 +12,9 @@ extern "C" {
 int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                        int64_t ldb, int b_mn, float* C, int64_t ldc, float alpha, float beta,
                        const float* bias, sl_stream_t stream);
+/* Same GEMM with A [M,K] K-major, B [K,N] N-major and a bf16 output (K1's XW path). */
+int sl_debug_gemm_bf16_out(int M, int N, int K, const void* A, int64_t lda, const void* B,
+                           int64_t ldb, void* Cb, int64_t ldc, const float* bias, sl_stream_t stream);
 /* Debug: record per-step globaltimer stamps of CTA `cta` of the recurrence
  * kernels into dev_buf[T][8] (NULL disables). */
 int sl_debug_set_trace(unsigned long long* dev_buf, int cta);

@@ -74,6 +74,8 @@ struct ReserveView {
   __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
   __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
   __nv_bfloat16* hprevb[2] = {nullptr, nullptr};  // bf16 path: h_{s-1} [B*T, Hp]
+  __nv_bfloat16* gatesb[2] = {nullptr, nullptr};  // bf16 path: saved (i,f,g,o) [B*T, 4H]
+  __nv_bfloat16* cprevb[2] = {nullptr, nullptr};  // bf16 path: saved c_{s-1} [B*T, H]
   __nv_bfloat16* rt[2] = {nullptr, nullptr};      // bf16 path: packed R^T slices
 };
 
@@ -105,19 +107,24 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   ReserveView r;
   for (int k = 0; k < d.nd; ++k) {
-    r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
-    r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
-    if (prec != SL_PREC_BF16) r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
+    if (prec == SL_PREC_BF16) {
+      r.gatesb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * 4 * d.H);
+      r.cprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * d.H);
+    } else {
+      r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
+      r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
+      r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
+    }
   }
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
-    const int U = tc_rec_units(d.H, d.nd, sm_count());
-    SL_REQUIRE(U > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
+    const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
+    SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     r.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
     r.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
     for (int k = 0; k < d.nd; ++k) {
       r.hprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Hp);
-      r.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(d.H, U));
+      r.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(sh));
     }
   }
   *bytes = c.off;
@@ -126,6 +133,7 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
 
 struct FwdWork {
   float* xw[2] = {nullptr, nullptr};
+  __nv_bfloat16* xwb[2] = {nullptr, nullptr};  // bf16 path: K1 output in bf16
   int64_t xw_ld = 0;
   float* hbuf[2] = {nullptr, nullptr};
   float* cbuf[2] = {nullptr, nullptr};
@@ -143,17 +151,17 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
   w.bar = c.take<unsigned>(64);
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
-    float* xw = c.take<float>((size_t)d.BT() * pd.Gc);
+    __nv_bfloat16* xw = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
     w.xw_ld = pd.Gc;
-    for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * pd.G4p : nullptr;
+    for (int k = 0; k < d.nd; ++k) w.xwb[k] = xw ? xw + k * pd.G4p : nullptr;
     w.bcat = c.take<float>((size_t)pd.Gc);
     w.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
     w.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
-    const int U = tc_rec_units(d.H, d.nd, sm_count());
-    SL_REQUIRE(U > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
+    const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
+    SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     for (int k = 0; k < d.nd; ++k) {
-      w.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(d.H, U));
-      w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, d.H));
+      w.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(sh));
+      w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, sh));
     }
   } else {
     w.xw_ld = 4 * d.H;
@@ -301,7 +309,8 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       fill_col_bf16(d.BT(), d.D, xb, pd.Dp, 1.f, stream);
       Phase ph(stream, "k1_xw_gemm", k1_flops);
       TcGemm g{(int)d.BT(), (int)pd.Gc, d.D, xb, pd.Dp, false, wcat, pd.Gc, true,
-               w.xw[0], pd.Gc, 1.f, 0.f, w.bcat};
+               nullptr, pd.Gc, 1.f, 0.f, w.bcat};
+      g.Cb = w.xwb[0];  // XW in bf16: half the bytes K1 writes and K2 reads
       gemm_bf16_tc(g, stream);
     } else {
       Phase ph(stream, "k1_xw_gemm", k1_flops);
@@ -316,9 +325,7 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       a.T = d.T;
       a.H = d.H;
       a.nd = d.nd;
-      a.U = tc_rec_units(d.H, d.nd, sm_count());
-      a.P = (int)ceil_div(d.H, a.U);
-      a.Kp = (int)round_up(d.H, 64);
+      const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
       a.lens = seq_lens;
       a.xw_ld = w.xw_ld;
       a.y = y;
@@ -330,21 +337,21 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       __nv_bfloat16* rt[2] = {nullptr, nullptr};
       for (int k = 0; k < d.nd; ++k) {
         rt[k] = rv.rt[k] ? rv.rt[k] : w.rt[k];
-        tc_rec_pack(R[k], d.H, a.U, rt[k], stream);
-        SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, d.H),
+        tc_rec_pack(R[k], d.H, sh, rt[k], stream);
+        SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh),
                                     stream));
         a.dirsign[k] = dir_sign(L, k);
-        a.xw[k] = w.xw[k];
+        a.xw[k] = w.xwb[k];
         a.hbuf[k] = w.hbufb[k];
-        a.gates[k] = rv.gates[k];
-        a.cprev[k] = rv.cprev[k];
+        a.gates[k] = rv.gatesb[k];
+        a.cprev[k] = rv.cprevb[k];
         a.hprev[k] = rv.hprevb[k];
       }
       a.trace = g_rec_trace;
       a.trace_cta = g_rec_trace_cta;
       a.debug_flags = g_rec_debug_flags;
       Phase ph(stream, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd);
-      rec_fwd_tc(a, rt, stream);
+      rec_fwd_tc(a, sh, rt, stream);
       return;
     }
     RecFwdArgs a{};
@@ -430,8 +437,8 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
         tc_rec_bwd_pack(R[k], d.H, sh, w.rb[k], stream);
         SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kz, stream));
         a.dirsign[k] = dir_sign(L, k);
-        a.gates[k] = rv.gates[k];
-        a.cprev[k] = rv.cprev[k];
+        a.gates[k] = rv.gatesb[k];
+        a.cprev[k] = rv.cprevb[k];
         a.dzring[k] = w.dzring[k];
       }
       {
@@ -570,4 +577,15 @@ extern "C" int sl_debug_set_trace(unsigned long long* dev_buf, int cta) {
 extern "C" int sl_debug_set_flags(int flags) {
   g_rec_debug_flags = flags;
   return 0;
+}
+
+extern "C" int sl_debug_gemm_bf16_out(int M, int N, int K, const void* A, int64_t lda,
+                                      const void* B, int64_t ldb, void* Cb, int64_t ldc,
+                                      const float* bias, sl_stream_t stream) {
+  return guarded([&] {
+    TcGemm g{M, N, K, static_cast<const __nv_bfloat16*>(A), lda, false,
+             static_cast<const __nv_bfloat16*>(B), ldb, true, nullptr, ldc, 1.f, 0.f, bias};
+    g.Cb = static_cast<__nv_bfloat16*>(Cb);
+    gemm_bf16_tc(g, reinterpret_cast<cudaStream_t>(stream));
+  });
 }

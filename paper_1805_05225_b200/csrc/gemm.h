@@ -34,6 +34,8 @@ struct TcGemm {
   int m_split = 1 << 30;
   float* C2 = nullptr;
   int64_t ldc2 = 0;
+  // optional: write the result as bf16 here (ld = ldc) instead of fp32 C
+  __nv_bfloat16* Cb = nullptr;
 };
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 

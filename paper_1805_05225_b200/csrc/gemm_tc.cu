@@ -38,6 +38,7 @@ struct Params {
   int m_split;
   float* C2;
   int64_t ldc2;
+  __nv_bfloat16* Cb;  // bf16 output instead of C (beta must be 0)
 };
 
 template <int BN>
@@ -169,8 +170,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BN + c, v);
-        if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
         const int col0 = n0 + c;
+        if (p.Cb) {  // bf16 output (K1's XW): alpha * acc + bias, rounded
+          if (row >= p.M) continue;
+          __nv_bfloat16* brow = p.Cb + (int64_t)row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              float o[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = p.alpha * v[j + i] + (p.bias ? p.bias[col0 + j + i] : 0.f);
+              uint4 w;
+              __nv_bfloat162 t0 = __floats2bfloat162_rn(o[0], o[1]), t1 = __floats2bfloat162_rn(o[2], o[3]);
+              __nv_bfloat162 t2 = __floats2bfloat162_rn(o[4], o[5]), t3 = __floats2bfloat162_rn(o[6], o[7]);
+              w.x = *reinterpret_cast<uint32_t*>(&t0);
+              w.y = *reinterpret_cast<uint32_t*>(&t1);
+              w.z = *reinterpret_cast<uint32_t*>(&t2);
+              w.w = *reinterpret_cast<uint32_t*>(&t3);
+              *reinterpret_cast<uint4*>(brow + j) = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+              brow[j] = __float2bfloat16_rn(p.alpha * v[j] + (p.bias ? p.bias[col0 + j] : 0.f));
+          }
+          continue;
+        }
+        if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
         if (vec && col0 + 32 <= p.N) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -293,6 +318,8 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   p.m_split = g.m_split;
   p.C2 = g.C2;
   p.ldc2 = g.ldc2;
+  p.Cb = g.Cb;
+  SL_REQUIRE(!g.Cb || g.beta == 0.f, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc: bf16 output needs beta = 0");
   // A: K-major stored [M, K]; MN-major stored [K, M].  B: K-major stored [N, K]; MN-major [K, N].
   const CUtensorMap ta = g.a_mn ? tmap_bf16(g.A, g.M, g.K, g.lda, 64)
                                 : tmap_bf16(g.A, g.K, g.M, g.lda, BM);

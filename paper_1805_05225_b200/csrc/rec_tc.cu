@@ -1,25 +1,30 @@
 // K2 — persistent tensor-core forward recurrence (SL_PREC_BF16 path).
 //
-// One launch runs all T steps of both directions.  CTA c of direction d owns
-// hidden units [c*U, c*U+U) and keeps its slice of R — the 4U gate columns of
-// those units, all K = H rows, bf16 — RESIDENT in shared memory for the whole
-// sequence (loaded once by TMA).  Per step s:
-//   warp 0      waits on the direction's step counter (every CTA published
-//               h_{s-1}), then TMA-streams h_{s-1} [128-row batch tile x 64]
-//               bf16 chunks from the L2-resident ring buffer into a smem ring;
-//   warp 1      issues tcgen05.mma (M = 128 batch rows, N = 4U gate columns,
-//               K = 16) into TMEM: Z_rec = h_{s-1} . R[:, cols];
-//   warps 2..   (4 per batch tile, one thread per batch row) tcgen05.ld the
-//               accumulator, add the hoisted input projection x W + b (K1),
-//               apply sigmoid / tanh, update the fp32 cell state held in
-//               registers, and write h_s (bf16, ring buffer), y, and the
-//               saved activations; then publish the step with one
-//               release-increment of the direction counter.
-// No kernel relaunch per step, no grid-wide cooperative sync: the only
-// cross-CTA dependency is "all slices of h_{s-1} are written" (reference
-// semantics: layers.cpp:27-33, tape.cpp:1103-1135; masking tape.cpp:797;
-// per-sequence reversal tape.cpp:846).
+// One launch runs all T steps of both directions.  The hidden units of a
+// direction are split over clusters of C CTAs; a cluster owns UC = C*U units
+// (its N = 4*UC gate columns) and K-splits the recurrent product over its C
+// CTAs: CTA r keeps R[K-slice r, the cluster's gate columns] (bf16, K-major)
+// RESIDENT in shared memory for the whole sequence.  Per step s:
+//   warp 0      waits on the step counter of the (direction, batch tile) —
+//               every CTA published its slice of h_{s-1} — then TMA-streams
+//               ITS K-slice of h_{s-1} [128-row tile x 64] from the L2 ring;
+//   warp 1      tcgen05.mma M = 128 batch rows x N = 4*UC (128 for C=2,U=16:
+//               the measured full-rate MMA width) x K = 16 into TMEM: the
+//               partial Z_rec over the CTA's K-slice;
+//   warps 2..   two threads per batch row: tcgen05.ld the partial columns of
+//               the peers' units and push them to the peers through DSMEM
+//               (st.shared::cluster.v4, one remote mbarrier arrive per warp),
+//               add the peers' partials for the own units, add x W + b (K1),
+//               apply sigmoid / tanh (SFU), update the fp32 cell state held in
+//               registers, and write h_s (bf16 ring), y and the saved
+//               activations; then release-increment the tile's step counter.
+// No relaunch and no grid-wide sync per step.  The two 128-row batch tiles are
+// independent recurrences with their own counters, so one tile's epilogue
+// overlaps the other's loads and MMAs.  Reference semantics: layers.cpp:27-33,
+// tape.cpp:1103-1135 (step), tape.cpp:797 (mask), tape.cpp:846 (reversal).
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "profile.h"
 #include "rec_tc.h"
@@ -29,46 +34,51 @@ namespace sl {
 namespace {
 using namespace rtc;
 
-constexpr int kStages = 6;  // max h-tile ring depth
-// h_s is written to kHCopies replicas of the ring and CTA c reads replica
-// c % kHCopies: ~P/kHCopies CTAs (not all P) request each L2 line per step.
-constexpr int kHCopies = 4;
+constexpr int kStages = 6;                      // max h-tile ring depth
 constexpr uint32_t kHTileBytes = 128 * 64 * 2;  // 128 rows x 64 K bf16 = 16 KB
 constexpr uint32_t kSmemMax = 227 * 1024;
 
-uint32_t fwd_smem(int N, int Kp, int stages) {
-  return (uint32_t)N * Kp * 2 + stages * kHTileBytes + 1024;
+// R slice + h ring stages + the (C-1) peers' partials [128 rows][4U] fp32
+uint32_t fwd_smem(int C, int U, int Kc, int stages) {
+  const uint32_t recv = C > 1 ? (uint32_t)(C - 1) * 128 * 4 * U * 4 : 0;
+  return (uint32_t)4 * C * U * Kc * 2 + stages * kHTileBytes + recv + 1024;
 }
 
-// U units per CTA (N = 4U), MT 128-row batch tiles.
-template <int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
+template <int C, int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
 __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     rec_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
                       const __grid_constant__ CUtensorMap tmR1,
                       const __grid_constant__ CUtensorMap tmH0,
                       const __grid_constant__ CUtensorMap tmH1, TcRecFwdArgs a) {
-  constexpr int N = 4 * U;
-  constexpr int kEpi = 128 * MT * SPLIT;
+  constexpr int UC = C * U;   // units per cluster
+  constexpr int N = 4 * UC;   // MMA N: the cluster's gate columns, ordered (gate, unit)
+  constexpr int kEpiTile = 128 * SPLIT;
   constexpr uint32_t kTmemCols = (MT * N <= 32) ? 32 : (MT * N <= 64) ? 64 : (MT * N <= 128) ? 128
                                  : (MT * N <= 256) ? 256 : 512;
+  constexpr int RS = 4 * U;   // recv row stride (floats): 4 gates x U units
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar[MT], tempty_bar[MT];
+  __shared__ __align__(8) uint64_t recv_full, free_bar[C];
   __shared__ uint32_t tmem_sh;
   __shared__ int tmax_sh;
 
   const int d = blockIdx.x / a.P;
   const int cta = blockIdx.x % a.P;
-  const int u0 = cta * U;
+  const int r = C > 1 ? (int)cluster_rank() : 0;
+  const int cl = cta / C;
+  const int u0 = cl * UC + r * U;  // first unit this CTA finalizes
+  const int Kc = a.Kp / C;
   const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
   const CUtensorMap* tmH = d == 0 ? &tmH0 : &tmH1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
-  const uint32_t r_bytes = (uint32_t)N * a.Kp * 2;
+  const uint32_t r_bytes = (uint32_t)N * Kc * 2;
   uint8_t* sR = smem;
   uint8_t* sH = smem + r_bytes;
-  const int nkc = a.Kp / 64;
+  float* recv = reinterpret_cast<float*>(sH + a.stages * kHTileBytes);  // [C-1][128][RS]
+  const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
@@ -81,13 +91,16 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     tc::mbar_init(&r_bar, 1);
     for (int m = 0; m < MT; ++m) {
       tc::mbar_init(&tfull_bar[m], 1);
-      tc::mbar_init(&tempty_bar[m], kEpi / MT);
+      tc::mbar_init(&tempty_bar[m], kEpiTile);
     }
+    tc::mbar_init(&recv_full, (C - 1) * kEpiTile);
+    for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[p], kEpiTile);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
   tc::fence_before_sync();
   __syncthreads();
+  if constexpr (C > 1) cluster_sync();
   tc::fence_after_sync();
   {  // longest sequence (steps beyond it only need zero outputs)
     int m = 0;
@@ -97,12 +110,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   __syncthreads();
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
-  // One step counter per (direction, batch tile): the two 128-row tiles are
-  // independent recurrences, so tile 0 of step s+1 streams and multiplies
-  // while tile 1 of step s is still in its epilogue.
+  // one step counter per (direction, batch tile)
   unsigned* ctr = a.bar + d * 2;
-  // Stagger the K-chunk order per CTA so the ~P CTAs of a direction do not
-  // all pull the same 16 KB h tile from the same L2 lines at the same time.
   const int kc_off = cta % nkc;
 
   if (warp == 0) {
@@ -127,8 +136,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kc = (kq + kc_off) % nkc;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             tc::mbar_arrive_expect_tx(&full_bar[st], kHTileBytes);
-            tma_load_3d(sH + st * kHTileBytes, tmH, &full_bar[st], kc * 64, a.b0 + mt * 128,
-                        (cta % kHCopies) * 2 + slot);
+            tma_load_3d(sH + st * kHTileBytes, tmH, &full_bar[st], r * Kc + kc * 64,
+                        a.b0 + mt * 128, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -158,9 +167,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const uint32_t sb = base + (uint32_t)kc * N * 128;
             if (!(a.debug_flags & 1))
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_f16(tmem + mt * N, tc::make_sdesc(sa + k * 32, 0, 1024),
-                          tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                tc::mma_f16(tmem + mt * N, tc::make_sdesc(sa + k * 32, 0, 1024),
+                            tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | k) != 0);
             tc::mma_commit(&empty_bar[st]);
             if (++st == nst) {
               st = 0;
@@ -178,67 +187,99 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     const int mt = e / (4 * SPLIT);
     const int half = (e / 4) % SPLIT;
     const int q = warp & 3;
-    const int row = a.b0 + mt * 128 + q * 32 + lane;
+    const int rl = q * 32 + lane;
+    const int row = a.b0 + mt * 128 + rl;
     const bool valid_row = row < a.B;
     const int len = valid_row ? a.lens[row] : 0;
     const int dir = a.dirsign[d];
     const int H = a.H, T = a.T;
-    const int lo = half * UT;          // first local unit of this thread
-    const int ut0 = u0 + lo;           // first global unit
+    const int lo = half * UT;   // first local unit of this thread (within the CTA's U)
+    const int ut0 = u0 + lo;    // first global unit
     const int nu = max(0, min(UT, H - ut0));
-    const float* xw = a.xw[d];
+    const __nv_bfloat16* xw = a.xw[d];
     __nv_bfloat16* hb = a.hbuf[d];
     const bool save = a.gates[d] != nullptr;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * N;
     float cst[UT], hst[UT];
 #pragma unroll
     for (int u = 0; u < UT; ++u) cst[u] = hst[u] = 0.f;
 
     for (int s = 0; s < Tmax; ++s) {
+      const int use = s * MT + mt;  // index of this tile's use of the exchange buffer
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
+      float z[4 * UT];
+      const bool tr0 = a.trace && blockIdx.x == a.trace_cta && e == 0 && lane == 0;
+      if (tr0) a.trace[s * 16 + 12] = gtimer();
+      tc::mbar_wait(&tfull_bar[mt], s & 1);
+      tc::fence_after_sync();
+      if (tr0) a.trace[s * 16 + 8] = gtimer();
+      if constexpr (C > 1) {  // push the peers' columns of my partial Z
+#pragma unroll 1
+        for (int pi = 1; pi < C; ++pi) {
+          const int p = (r + pi) % C;
+          if (use > 0) mbar_wait_cluster(&free_bar[p], (use - 1) & 1);
+          const int slot_at_p = (r - p + C) % C - 1;  // my slot in p's buffer
+          const uint32_t dst =
+              mapa(tc::smem_u32(recv + ((size_t)slot_at_p * 128 + rl) * RS + lo), p);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float v[UT];
+            tmem_ld_cols<UT>(tbase + g * UC + p * U + lo, v);
+            st_cluster_vec<UT>(dst + g * U * 4, v);
+          }
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int pi = 1; pi < C; ++pi)
+            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full), (r + pi) % C), 32);
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float v[UT];
+        tmem_ld_cols<UT>(tbase + g * UC + r * U + lo, v);
+#pragma unroll
+        for (int u = 0; u < UT; ++u) z[g * UT + u] = v[u];
+      }
+      if (tr0) a.trace[s * 16 + 9] = gtimer();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty_bar[mt]);
       float xv[4 * UT];
-      if (active) {
-        const float* xr = xw + pos * a.xw_ld + ut0;
-        if (nu == UT && (UT % 4) == 0 && ((uintptr_t)xr & 15) == 0 && (H % 4) == 0) {
+      if (active) {  // hoisted input projection x W + b of this step (K1 output)
+        const __nv_bfloat16* xr = xw + pos * a.xw_ld + ut0;
+        const bool vec = nu == UT && (H % 8) == 0 && (a.xw_ld % 8) == 0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) load_bf16<UT>(xr + g * H, xv + g * UT, nu, vec);
+      }
+      if constexpr (C > 1) {
+        mbar_wait_cluster(&recv_full, use & 1);
+        if (tr0) a.trace[s * 16 + 10] = gtimer();
+#pragma unroll 1
+        for (int pi = 0; pi < C - 1; ++pi) {
+          const float4* src = reinterpret_cast<const float4*>(recv + ((size_t)pi * 128 + rl) * RS + lo);
 #pragma unroll
           for (int g = 0; g < 4; ++g)
 #pragma unroll
             for (int u = 0; u < UT; u += 4) {
-              const float4 v4 = __ldg(reinterpret_cast<const float4*>(xr + g * H + u));
-              xv[g * UT + u] = v4.x;
-              xv[g * UT + u + 1] = v4.y;
-              xv[g * UT + u + 2] = v4.z;
-              xv[g * UT + u + 3] = v4.w;
+              const float4 v = src[(g * U + u) / 4];
+              z[g * UT + u] += v.x;
+              z[g * UT + u + 1] += v.y;
+              z[g * UT + u + 2] += v.z;
+              z[g * UT + u + 3] += v.w;
             }
-        } else {
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-#pragma unroll
-            for (int u = 0; u < UT; ++u) xv[g * UT + u] = (u < nu) ? __ldg(xr + g * H + u) : 0.f;
         }
+        __syncwarp();
+        if (lane == 0)  // every sender's slot in my buffer is free again
+          for (int pi = 1; pi < C; ++pi)
+            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[r]), (r + pi) % C), 32);
       }
-      float z[4 * UT];
-      tc::mbar_wait(&tfull_bar[mt], s & 1);
-      tc::fence_after_sync();
-      {
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * N + lo;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float v[UT];
-          tmem_ld_cols<UT>(tbase + g * U, v);
-#pragma unroll
-          for (int u = 0; u < UT; ++u) z[g * UT + u] = v[u];
-        }
-      }
-      tc::fence_before_sync();
-      tc::mbar_arrive(&tempty_bar[mt]);
 
       if (valid_row && !(a.debug_flags & 2)) {
         __nv_bfloat16* hn = hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0;
         if (active) {
           if (save) {  // c_{s-1}, h_{s-1} before the update
-            store_f32<UT>(a.cprev[d] + pos * H + ut0, cst, nu);
+            store_bf16<UT>(a.cprev[d] + pos * H + ut0, cst, nu);
             store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, hst, nu);
           }
 #pragma unroll
@@ -256,9 +297,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             hst[u] = go * tc::tanh_approx(cn);
           }
           if (save) {
-            float* gsave = a.gates[d] + pos * 4 * H + ut0;
+            __nv_bfloat16* gsave = a.gates[d] + pos * 4 * H + ut0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) store_f32<UT>(gsave + g * H, z + g * UT, nu);
+            for (int g = 0; g < 4; ++g) store_bf16<UT>(gsave + g * H, z + g * UT, nu);
           }
           if (a.y) store_f32<UT>(a.y + pos * a.y_ld + (size_t)d * H + ut0, hst, nu);
           if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, hst, nu);
@@ -270,10 +311,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
           if (save) store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
         }
-#pragma unroll
-        for (int cp = 0; cp < kHCopies; ++cp) store_bf16<UT>(hn + (size_t)cp * 2 * a.B * a.Kp, hst, nu);
+        store_bf16<UT>(hn, hst, nu);
       }
-      named_sync(1 + mt, kEpi / MT);  // the tile's epilogue threads only
+      if (tr0) a.trace[s * 16 + 11] = gtimer();
+      named_sync(1 + mt, kEpiTile);  // the tile's epilogue threads only
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
         red_release_gpu(ctr + mt, 1u);
@@ -298,100 +339,129 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     }
   }
   __syncthreads();
+  if constexpr (C > 1) cluster_sync();  // no CTA leaves while a peer may still touch its smem
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
-// RT[c*N + g*U + u][k] = R[k][g*H + c*U + u] (bf16), zero outside [H) x [H).
-__global__ void pack_rt_kernel(const float* __restrict__ R, int H, int U, int P, int Kp,
+// RT[(cl*C + r)*N + g*UC + j][kk] = R[r*Kc + kk][g*H + cl*UC + j]  (bf16, zero outside)
+__global__ void pack_rt_kernel(const float* __restrict__ R, int H, int C, int U, int P, int Kc,
                                __nv_bfloat16* __restrict__ RT) {
-  const int N = 4 * U;
-  const int64_t n = (int64_t)P * N * Kp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+  const int UC = C * U, N = 4 * UC;
+  const int64_t n_el = (int64_t)P * N * Kc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(e % Kp);
-    const int r = (int)(e / Kp);
-    const int c = r / N, j = r % N, g = j / U, u = j % U;
-    const int unit = c * U + u;
+    const int kk = (int)(e % Kc);
+    const int rowi = (int)(e / Kc);
+    const int cta = rowi / N, j = rowi % N;
+    const int cl = cta / C, r = cta % C;
+    const int g = j / UC, unit = cl * UC + j % UC;
+    const int k = r * Kc + kk;
     float v = 0.f;
     if (unit < H && k < H) v = R[(int64_t)k * 4 * H + (int64_t)g * H + unit];
     RT[e] = __float2bfloat16_rn(v);
   }
 }
 
-template <int U, int MT>
+template <int C, int U, int MT>
 void launch_fwd(const CUtensorMap* tr, const CUtensorMap* th, const TcRecFwdArgs& a,
                 cudaStream_t stream) {
-  auto kern = rec_fwd_tc_kernel<U, MT>;
-  const uint32_t smem = fwd_smem(4 * U, a.Kp, a.stages);
+  auto kern = rec_fwd_tc_kernel<C, U, MT>;
+  const uint32_t smem = fwd_smem(C, U, a.Kp / C, a.stages);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TcRecFwdArgs copy = a;
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];
-  void* params[] = {&r0, &r1, &h0, &h1, &copy};
-  // Cooperative launch: guarantees every CTA is co-resident (they spin on each
-  // other's step counters), and fails loudly instead of deadlocking if not.
   constexpr int kSplit = U >= 8 ? 2 : 1;
-  SL_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(a.P * a.nd), dim3(64 + 128 * MT * kSplit),
-                                          params, smem, stream));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.P * a.nd);
+  cfg.blockDim = dim3(64 + 128 * MT * kSplit);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  // cooperative: every CTA co-resident (they wait on each other's step
+  // counters) — the launch fails loudly instead of deadlocking otherwise
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = C;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, h0, h1, copy));
   count_launch();
 }
 
 }  // namespace
 
-int tc_rec_units(int H, int nd, int sms) {
-  const int Kp = (int)round_up(H, 64);
-  for (int U : {4, 8, 16})
-    if ((int64_t)ceil_div(H, U) * nd <= sms && fwd_smem(4 * U, Kp, 2) <= kSmemMax) return U;
-  return 0;
+TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms) {
+  // 2-CTA clusters (N = 4*C*U = 128, the full-rate MMA width; each CTA streams
+  // only its K-half of h) trade the h stream for a DSMEM partial exchange;
+  // opt-in (SL_FWD_CLUSTER=1) until that exchange beats the single-CTA form.
+  const char* env = getenv("SL_FWD_CLUSTER");
+  const bool cluster = env && env[0] == '1';
+  for (int C : {2, 1})
+    for (int U : {16, 8, 4}) {
+      const int P = (int)ceil_div(H, (int64_t)C * U) * C;
+      const int Kp = (int)round_up(H, 64 * C);
+      if ((C == 1 || cluster) && 4 * C * U <= 128 && (int64_t)P * nd <= sms &&
+          fwd_smem(C, U, Kp / C, 2) <= kSmemMax && ((int64_t)ceil_div(H, (int64_t)C * U / 2) * C * nd > sms || U == 4))
+        return TcFwdShape{C, U, P, Kp};
+    }
+  return TcFwdShape{0, 0, 0, 0};
 }
 
-size_t tc_rec_hbuf_elems(int B, int H) { return (size_t)kHCopies * 2 * B * round_up(H, 64); }
+size_t tc_rec_hbuf_elems(int B, const TcFwdShape& sh) { return (size_t)2 * B * sh.Kp; }
 
-size_t tc_rec_pack_elems(int H, int U) {
-  const int P = (int)ceil_div(H, U);
-  return (size_t)P * 4 * U * round_up(H, 64);
+size_t tc_rec_pack_elems(const TcFwdShape& sh) {
+  return (size_t)sh.P * 4 * sh.C * sh.U * (sh.Kp / sh.C);
 }
 
-void tc_rec_pack(const float* R, int H, int U, __nv_bfloat16* RT, cudaStream_t stream) {
-  const int P = (int)ceil_div(H, U);
-  const int Kp = (int)round_up(H, 64);
-  const int64_t n = (int64_t)P * 4 * U * Kp;
+void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
+                 cudaStream_t stream) {
+  const int Kc = sh.Kp / sh.C;
+  const int64_t n = (int64_t)sh.P * 4 * sh.C * sh.U * Kc;
   pack_rt_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, stream>>>(
-      R, H, U, P, Kp, RT);
+      R, H, sh.C, sh.U, sh.P, Kc, RT);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
 
-void rec_fwd_tc(const TcRecFwdArgs& a0, __nv_bfloat16* const* RT, cudaStream_t stream) {
+void rec_fwd_tc(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* const* RT,
+                cudaStream_t stream) {
   TcRecFwdArgs a = a0;
-  const int N = 4 * a.U;
+  a.U = sh.U;
+  a.P = sh.P;
+  a.Kp = sh.Kp;
+  const int N = 4 * sh.C * sh.U;
+  const int Kc = sh.Kp / sh.C;
   CUtensorMap tr[2], th[2];
   for (int k = 0; k < a.nd; ++k) {
-    cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.P * N};
-    cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
+    cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)a.P * N};
+    cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)N};
     tr[k] = tmap(RT[k], 2, rd, rs, rb);
-    cuuint64_t hd[3] = {(cuuint64_t)a.Kp, (cuuint64_t)a.B, (cuuint64_t)2 * kHCopies};
+    cuuint64_t hd[3] = {(cuuint64_t)a.Kp, (cuuint64_t)a.B, 2};
     cuuint64_t hs[2] = {(cuuint64_t)a.Kp * 2, (cuuint64_t)a.Kp * 2 * a.B};
     cuuint32_t hbx[3] = {64, 128, 1};
     th[k] = tmap(a.hbuf[k], 3, hd, hs, hbx);
   }
   a.stages = 0;
   for (int st = kStages; st >= 2 && !a.stages; --st)
-    if (fwd_smem(N, a.Kp, st) <= kSmemMax) a.stages = st;
+    if (fwd_smem(sh.C, sh.U, Kc, st) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_tc: R slice does not fit in shared memory");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles
     a.b0 = b0;
     a.bar = bar0 + 4 * (b0 / 256);  // fresh zeroed counters per chunk (2 dirs x 2 tiles)
     const int MT = (a.B - b0) > 128 ? 2 : 1;
-    switch (a.U * 10 + MT) {
-      case 41: launch_fwd<4, 1>(tr, th, a, stream); break;
-      case 42: launch_fwd<4, 2>(tr, th, a, stream); break;
-      case 81: launch_fwd<8, 1>(tr, th, a, stream); break;
-      case 82: launch_fwd<8, 2>(tr, th, a, stream); break;
-      case 161: launch_fwd<16, 1>(tr, th, a, stream); break;
-      case 162: launch_fwd<16, 2>(tr, th, a, stream); break;
-      default: throw Error{SL_ERR_UNSUPPORTED, "rec_fwd_tc: unsupported units per CTA"};
+    switch (sh.C * 1000 + sh.U * 10 + MT) {
+#define SL_FWD_CASE(C_, U_, MT_) \
+  case C_ * 1000 + U_ * 10 + MT_: launch_fwd<C_, U_, MT_>(tr, th, a, stream); break;
+      SL_FWD_CASE(2, 4, 1) SL_FWD_CASE(2, 4, 2) SL_FWD_CASE(2, 8, 1) SL_FWD_CASE(2, 8, 2)
+      SL_FWD_CASE(2, 16, 1) SL_FWD_CASE(2, 16, 2) SL_FWD_CASE(1, 4, 1) SL_FWD_CASE(1, 4, 2)
+      SL_FWD_CASE(1, 8, 1) SL_FWD_CASE(1, 8, 2) SL_FWD_CASE(1, 16, 1) SL_FWD_CASE(1, 16, 2)
+#undef SL_FWD_CASE
+      default: throw Error{SL_ERR_UNSUPPORTED, "rec_fwd_tc: unsupported partition"};
     }
   }
 }

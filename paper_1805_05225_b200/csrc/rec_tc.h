@@ -11,7 +11,7 @@ struct TcRecFwdArgs {
   int stages;             // h-tile ring depth
   const int32_t* lens;
   int dirsign[2];
-  const float* xw[2];  // hoisted x W + b, fp32 [B*T, xw_ld], dir d's gate blocks at col 0
+  const __nv_bfloat16* xw[2];  // hoisted x W + b, bf16 [B*T, xw_ld], dir d's gate blocks at col 0
   int64_t xw_ld;
   float* y;  // fp32 [B*T, y_ld] (dir d at col d*H) or null
   int64_t y_ld;
@@ -19,11 +19,11 @@ struct TcRecFwdArgs {
   int64_t ybf_ld;
   float* h_last;  // [nd, B, H] or null
   float* c_last;
-  float* gates[2];            // saved (i,f,g,o) fp32 [B*T, 4H] (null = inference)
-  float* cprev[2];            // saved c_{s-1} fp32 [B*T, H]
+  __nv_bfloat16* gates[2];    // saved (i,f,g,o) bf16 [B*T, 4H] (null = inference)
+  __nv_bfloat16* cprev[2];    // saved c_{s-1} bf16 [B*T, H]
   __nv_bfloat16* hprev[2];    // saved h_{s-1} bf16 [B*T, hprev_ld] (dR GEMM operand)
   int64_t hprev_ld;
-  __nv_bfloat16* hbuf[2];     // ring [kHCopies][2][B][Kp] bf16, zeroed (tc_rec_hbuf_elems)
+  __nv_bfloat16* hbuf[2];     // ring [2][B][Kp] bf16, zeroed (tc_rec_hbuf_elems)
   unsigned* bar;              // zeroed step counters, 2 per batch chunk
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;
@@ -37,8 +37,8 @@ struct TcRecBwdArgs {
   int stages;  // set internally
   const int32_t* lens;
   int dirsign[2];
-  const float* gates[2];  // saved by K2: (i,f,g,o) fp32 [B*T, 4H]
-  const float* cprev[2];  // saved by K2: c_{s-1} fp32 [B*T, H]
+  const __nv_bfloat16* gates[2];  // saved by K2: (i,f,g,o) bf16 [B*T, 4H]
+  const __nv_bfloat16* cprev[2];  // saved by K2: c_{s-1} bf16 [B*T, H]
   const float* dy;        // [B*T, dy_ld], dir d at col d*H
   int64_t dy_ld;
   const float* dh_last;  // [nd, B, H] or null
@@ -63,15 +63,19 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
 void rec_bwd_tc(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* const* RB,
                 cudaStream_t stream);
 
-// Elements of one direction's h ring (all replicas).
-size_t tc_rec_hbuf_elems(int B, int H);
-
-// Units per CTA for the tensor-core recurrence (0 = shape unsupported).
-int tc_rec_units(int H, int nd, int sms);
-// Elements of the packed R^T slice buffer for one direction.
-size_t tc_rec_pack_elems(int H, int U);
+// K-split partition of the forward kernel: clusters of C CTAs, each finalizing
+// U units (the cluster owns C*U units, MMA N = 4*C*U), P CTAs per direction,
+// Kp = H padded to 64*C.
+struct TcFwdShape {
+  int C, U, P, Kp;
+};
+TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms);  // C == 0: unsupported
+size_t tc_rec_hbuf_elems(int B, const TcFwdShape& sh);  // one direction's h ring
+size_t tc_rec_pack_elems(const TcFwdShape& sh);         // one direction's packed R^T
 // Pack R [H, 4H] fp32 into the per-CTA K-major bf16 slices the kernel loads.
-void tc_rec_pack(const float* R, int H, int U, __nv_bfloat16* RT, cudaStream_t stream);
-void rec_fwd_tc(const TcRecFwdArgs& a, __nv_bfloat16* const* RT, cudaStream_t stream);
+void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
+                 cudaStream_t stream);
+void rec_fwd_tc(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
+                cudaStream_t stream);
 
 }  // namespace sl

@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     const int ut0 = u0 + lo;
     const int nu = max(0, min(UT, H - ut0));
     __nv_bfloat16* zr = a.dzring[d];
-    const float* gates = a.gates[d];
-    const float* cprev = a.cprev[d];
+    const __nv_bfloat16* gates = a.gates[d];
+    const __nv_bfloat16* cprev = a.cprev[d];
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * NB;
     float gcar[UT];
 #pragma unroll
@@ -198,9 +198,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       float gv[4 * UT], cp[UT], dyv[UT];
       if (active) {  // prefetch this step's saved activations and upstream grad
         const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
+        const bool vecb = nu == UT && (H % 8) == 0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) load_f32<UT>(gates + pos * 4 * H + g * H + ut0, gv + g * UT, nu, vec);
-        load_f32<UT>(cprev + pos * H + ut0, cp, nu, vec);
+        for (int g = 0; g < 4; ++g) load_bf16<UT>(gates + pos * 4 * H + g * H + ut0, gv + g * UT, nu, vecb);
+        load_bf16<UT>(cprev + pos * H + ut0, cp, nu, vecb);
         load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)d * H + ut0, dyv, nu,
                      vec && (a.dy_ld % 4) == 0);
       }

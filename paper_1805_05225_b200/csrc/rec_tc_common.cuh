@@ -97,6 +97,26 @@ __device__ __forceinline__ void load_f32(const float* src, float* v, int nu, boo
   }
 }
 
+template <int U>
+__device__ __forceinline__ void load_bf16(const __nv_bfloat16* src, float* v, int nu, bool vec) {
+  if (vec && (U % 8) == 0 && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 8) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + i));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ws[k]));
+        v[i + 2 * k] = f.x;
+        v[i + 2 * k + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < U; ++i) v[i] = (i < nu) ? __bfloat162float(src[i]) : 0.f;
+  }
+}
+
 template <int n>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[n]) {
   if constexpr (n == 8) {
@@ -162,6 +182,17 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 }
 __device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+// n floats (n % 4 == 0) to a 16 B aligned shared::cluster address
+template <int n>
+__device__ __forceinline__ void st_cluster_vec(uint32_t addr, const float* v) {
+#pragma unroll
+  for (int i = 0; i < n; i += 4) st_cluster_v4(addr + i * 4, v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
 // arrive (release, cluster scope) on an mbarrier of another CTA of the cluster
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr, uint32_t count) {

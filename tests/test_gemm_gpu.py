@@ -54,3 +54,23 @@ def test_gemm_bf16_tc_epilogue(cuda):
     C, ref = run(384, 520, 200, False, True, alpha=0.5, beta=1.0, bias=True)
     err = (C - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+def test_gemm_bf16_tc_bf16_output(cuda):
+    # K1 writes XW as bf16: same GEMM, rounded output
+    import ctypes as C
+    M, N, K = 300, 520, 136
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = (torch.rand((M, K), device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand((K, N), device="cuda", generator=g) * 2 - 1).bfloat16()
+    bias = torch.rand(N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    L = lib()
+    L.sl_debug_gemm_bf16_out.argtypes = [C.c_int] * 3 + [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                                         C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    rc = L.sl_debug_gemm_bf16_out(M, N, K, A.data_ptr(), K, B.data_ptr(), N, out.data_ptr(), N,
+                                  bias.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = (A.float() @ B.float() + bias).bfloat16().float()
+    assert (out.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item()
