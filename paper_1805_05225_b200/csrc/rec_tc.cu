@@ -41,7 +41,7 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 // R slice + h ring stages + the (C-1) peers' partials [128 rows][4U] fp32
 uint32_t fwd_smem(int C, int U, int Kc, int stages) {
   const uint32_t recv = C > 1 ? (uint32_t)(C - 1) * 128 * 4 * U * 4 : 0;
-  return (uint32_t)4 * C * U * Kc * 2 + stages * kHTileBytes + recv + 1024;
+  return (uint32_t)4 * C * U * Kc * 2 + stages * kHTileBytes * 2 + recv + 1024;
 }
 
 template <int C, int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const uint32_t r_bytes = (uint32_t)N * Kc * 2;
   uint8_t* sR = smem;
   uint8_t* sH = smem + r_bytes;
-  float* recv = reinterpret_cast<float*>(sH + a.stages * kHTileBytes);  // [C-1][128][RS]
+  const uint32_t stage_bytes = kHTileBytes * a.kb;  // a.kb 64-wide K chunks per TMA box
+  float* recv = reinterpret_cast<float*>(sH + a.stages * stage_bytes);  // [C-1][128][RS]
   const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
@@ -112,7 +113,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const uint32_t tmem = tmem_sh;
   // one step counter per (direction, batch tile)
   unsigned* ctr = a.bar + d * 2;
-  const int kc_off = cta % nkc;
+  const int ngrp = nkc / a.kb;  // TMA boxes per tile
+  const int kc_off = cta % ngrp;
 
   if (warp == 0) {
     if (lane == 0) {  // -------------------------------------------- producer
@@ -132,12 +134,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             tc::fence_proxy_async_global();
           }
           SL_TRACE(mt == 0 ? 0 : 3);
-          for (int kq = 0; kq < nkc; ++kq) {
-            const int kc = (kq + kc_off) % nkc;
+          for (int kq = 0; kq < ngrp; ++kq) {
+            const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
-            tc::mbar_arrive_expect_tx(&full_bar[st], kHTileBytes);
-            tma_load_3d(sH + st * kHTileBytes, tmH, &full_bar[st], r * Kc + kc * 64,
-                        a.b0 + mt * 128, slot);
+            tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
+            tma_load_4d(sH + st * stage_bytes, tmH, &full_bar[st], 0, a.b0 + mt * 128,
+                        r * (Kc / 64) + kg * a.kb, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -157,19 +159,22 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         for (int mt = 0; mt < MT; ++mt) {
           tc::mbar_wait(&tempty_bar[mt], (s & 1) ^ 1);
           tc::fence_after_sync();
-          for (int kq = 0; kq < nkc; ++kq) {
-            const int kc = (kq + kc_off) % nkc;
+          for (int kq = 0; kq < ngrp; ++kq) {
+            const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
             if (kq == 0) SL_TRACE(mt == 0 ? 1 : 4);
-            if (kq == nkc - 1) SL_TRACE(mt == 0 ? 2 : 5);
-            const uint32_t sa = base + r_bytes + st * kHTileBytes;
+            if (kq == ngrp - 1) SL_TRACE(mt == 0 ? 2 : 5);
+            for (int j = 0; j < a.kb; ++j) {
+            const int kc = kg * a.kb + j;
+            const uint32_t sa = base + r_bytes + st * stage_bytes + j * kHTileBytes;
             const uint32_t sb = base + (uint32_t)kc * N * 128;
             if (!(a.debug_flags & 1))
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 tc::mma_f16(tmem + mt * N, tc::make_sdesc(sa + k * 32, 0, 1024),
-                            tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | k) != 0);
+                            tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | j | k) != 0);
+            }
             tc::mma_commit(&empty_bar[st]);
             if (++st == nst) {
               st = 0;
@@ -209,6 +214,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
+      float xv[4 * UT];
+      if (active) {  // prefetch (before the MMA wait): hoisted input projection x W + b of this step (K1 output)
+        const __nv_bfloat16* xr = xw + pos * a.xw_ld + ut0;
+        const bool vec = nu == UT && (H % 8) == 0 && (a.xw_ld % 8) == 0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) load_bf16<UT>(xr + g * H, xv + g * UT, nu, vec);
+      }
       float z[4 * UT];
       const bool tr0 = a.trace && blockIdx.x == a.trace_cta && e == 0 && lane == 0;
       if (tr0) a.trace[s * 16 + 12] = gtimer();
@@ -245,13 +257,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       if (tr0) a.trace[s * 16 + 9] = gtimer();
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
-      float xv[4 * UT];
-      if (active) {  // hoisted input projection x W + b of this step (K1 output)
-        const __nv_bfloat16* xr = xw + pos * a.xw_ld + ut0;
-        const bool vec = nu == UT && (H % 8) == 0 && (a.xw_ld % 8) == 0;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) load_bf16<UT>(xr + g * H, xv + g * UT, nu, vec);
-      }
       if constexpr (C > 1) {
         mbar_wait_cluster(&recv_full, use & 1);
         if (tr0) a.trace[s * 16 + 10] = gtimer();
@@ -366,7 +371,7 @@ template <int C, int U, int MT>
 void launch_fwd(const CUtensorMap* tr, const CUtensorMap* th, const TcRecFwdArgs& a,
                 cudaStream_t stream) {
   auto kern = rec_fwd_tc_kernel<C, U, MT>;
-  const uint32_t smem = fwd_smem(C, U, a.Kp / C, a.stages);
+  const uint32_t smem = fwd_smem(C, U, a.Kp / C, a.kb == 2 ? a.stages : (a.stages + 1) / 2);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TcRecFwdArgs copy = a;
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];
@@ -440,14 +445,16 @@ void rec_fwd_tc(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* con
     cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)N};
     tr[k] = tmap(RT[k], 2, rd, rs, rb);
-    cuuint64_t hd[3] = {(cuuint64_t)a.Kp, (cuuint64_t)a.B, 2};
-    cuuint64_t hs[2] = {(cuuint64_t)a.Kp * 2, (cuuint64_t)a.Kp * 2 * a.B};
-    cuuint32_t hbx[3] = {64, 128, 1};
-    th[k] = tmap(a.hbuf[k], 3, hd, hs, hbx);
+    // {k_in 64, rows, k_chunk, slot}: one TMA box = kb consecutive 64-wide chunks
+    a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
+    cuuint64_t hd[4] = {64, (cuuint64_t)a.B, (cuuint64_t)a.Kp / 64, 2};
+    cuuint64_t hs[3] = {(cuuint64_t)a.Kp * 2, 128, (cuuint64_t)a.Kp * 2 * a.B};
+    cuuint32_t hbx[4] = {64, 128, (cuuint32_t)a.kb, 1};
+    th[k] = tmap(a.hbuf[k], 4, hd, hs, hbx);
   }
-  a.stages = 0;
+  a.stages = 0;  // stages of a.kb chunks (fwd_smem counts two chunks per stage)
   for (int st = kStages; st >= 2 && !a.stages; --st)
-    if (fwd_smem(sh.C, sh.U, Kc, st) <= kSmemMax) a.stages = st;
+    if (fwd_smem(sh.C, sh.U, Kc, a.kb == 2 ? st : (st + 1) / 2) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_tc: R slice does not fit in shared memory");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles

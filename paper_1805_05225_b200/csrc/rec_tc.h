@@ -8,7 +8,8 @@ struct TcRecFwdArgs {
   int B, T, H, nd, U, P;  // P = CTAs per direction (= ceil(H / U))
   int b0;                 // first batch row of this launch (set internally)
   int Kp;                 // K padded to 64 (= round_up(H, 64))
-  int stages;             // h-tile ring depth
+  int stages;             // h-tile ring depth (set internally)
+  int kb;                 // 64-wide K chunks per TMA box (set internally)
   const int32_t* lens;
   int dirsign[2];
   const __nv_bfloat16* xw[2];  // hoisted x W + b, bf16 [B*T, xw_ld], dir d's gate blocks at col 0
@@ -35,6 +36,7 @@ struct TcRecBwdArgs {
   int b0;      // first batch row of this launch (set internally)
   int Kz;      // K of the per-step dh GEMM = gate columns padded to 64 (round_up(4H, 64))
   int stages;  // set internally
+  int kb;      // 64-wide K chunks per TMA box (set internally)
   const int32_t* lens;
   int dirsign[2];
   const __nv_bfloat16* gates[2];  // saved by K2: (i,f,g,o) bf16 [B*T, 4H]

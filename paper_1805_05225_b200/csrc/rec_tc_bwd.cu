@@ -29,9 +29,9 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 
 __host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
-uint32_t bwd_smem(int C, int U, int Kc, int stages) {
+uint32_t bwd_smem(int C, int U, int Kc, int stages) {  // stages of two 16 KB chunks
   const uint32_t recv = C > 1 ? (uint32_t)C * U * 128 * 4 : 0;
-  return (uint32_t)nb_of(C, U) * Kc * 2 + stages * kTile + recv + 1024;
+  return (uint32_t)nb_of(C, U) * Kc * 2 + stages * kTile * 2 + recv + 1024;
 }
 
 // C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const uint32_t r_bytes = (uint32_t)NB * Kc * 2;
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
-  float* recv = reinterpret_cast<float*>(sA + a.stages * kTile);  // [C][U][128] partials from peers
+  const uint32_t stage_bytes = kTile * a.kb;  // a.kb 64-wide K chunks per TMA box
+  float* recv = reinterpret_cast<float*>(sA + a.stages * stage_bytes);  // [C][U][128] partials from peers
   const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
@@ -101,7 +102,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
   unsigned* ctr = a.bar + d * 2;
-  const int kc_off = cta % nkc;
+  const int ngrp = nkc / a.kb;  // TMA boxes per tile
+  const int kc_off = cta % ngrp;
 
   if (warp == 0) {
     if (lane == 0) {  // -------------------------------------------- producer
@@ -121,11 +123,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             tc::fence_proxy_async_global();
           }
           SL_TRACE(mt == 0 ? 0 : 3);
-          for (int kq = 0; kq < nkc; ++kq) {
-            const int kc = (kq + kc_off) % nkc;
+          for (int kq = 0; kq < ngrp; ++kq) {
+            const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
-            tc::mbar_arrive_expect_tx(&full_bar[st], kTile);
-            tma_load_3d(sA + st * kTile, tmZ, &full_bar[st], r * Kc + kc * 64, a.b0 + mt * 128, slot);
+            tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
+            tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, a.b0 + mt * 128,
+                        r * (Kc / 64) + kg * a.kb, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -145,18 +148,21 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         for (int mt = 0; mt < MT; ++mt) {
           tc::mbar_wait(&tempty_bar[mt], (s & 1) ^ 1);
           tc::fence_after_sync();
-          for (int kq = 0; kq < nkc; ++kq) {
-            const int kc = (kq + kc_off) % nkc;
+          for (int kq = 0; kq < ngrp; ++kq) {
+            const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
             if (kq == 0) SL_TRACE(mt == 0 ? 1 : 4);
-            if (kq == nkc - 1) SL_TRACE(mt == 0 ? 2 : 5);
-            const uint32_t sa = base + r_bytes + st * kTile;
+            if (kq == ngrp - 1) SL_TRACE(mt == 0 ? 2 : 5);
+            for (int j = 0; j < a.kb; ++j) {
+            const int kc = kg * a.kb + j;
+            const uint32_t sa = base + r_bytes + st * stage_bytes + j * kTile;
             const uint32_t sb = base + (uint32_t)kc * NB * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc::mma_f16(tmem + mt * NB, tc::make_sdesc(sa + k * 32, 0, 1024),
-                          tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | k) != 0);
+                          tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | j | k) != 0);
+            }
             tc::mma_commit(&empty_bar[st]);
             if (++st == nst) {
               st = 0;
@@ -328,7 +334,7 @@ template <int C, int U, int MT>
 void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs& a,
                 cudaStream_t stream) {
   auto kern = rec_bwd_tc_kernel<C, U, MT>;
-  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.stages);
+  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.kb == 2 ? a.stages : (a.stages + 1) / 2);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (C > 1)
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -399,14 +405,15 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
     cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
     tr[k] = tmap(RB[k], 2, rd, rs, rb);
-    cuuint64_t zd[3] = {(cuuint64_t)a.Kz, (cuuint64_t)a.B, 2};
-    cuuint64_t zs[2] = {(cuuint64_t)a.Kz * 2, (cuuint64_t)a.Kz * 2 * a.B};
-    cuuint32_t zb[3] = {64, 128, 1};
-    tz[k] = tmap(a.dzring[k], 3, zd, zs, zb);
+    a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
+    cuuint64_t zd[4] = {64, (cuuint64_t)a.B, (cuuint64_t)a.Kz / 64, 2};
+    cuuint64_t zs[3] = {(cuuint64_t)a.Kz * 2, 128, (cuuint64_t)a.Kz * 2 * a.B};
+    cuuint32_t zb[4] = {64, 128, (cuuint32_t)a.kb, 1};
+    tz[k] = tmap(a.dzring[k], 4, zd, zs, zb);
   }
   a.stages = 0;
   for (int st = kStages; st >= 2 && !a.stages; --st)
-    if (bwd_smem(sh.C, sh.U, Kc, st) <= kSmemMax) a.stages = st;
+    if (bwd_smem(sh.C, sh.U, Kc, a.kb == 2 ? st : (st + 1) / 2) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {
