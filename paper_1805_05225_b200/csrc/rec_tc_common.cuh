@@ -48,84 +48,104 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Row-segment stores: 16 B vectors when the destination is aligned and the
-// CTA's unit slice is full, scalar otherwise (odd H / last CTA).
+// Row-segment loads/stores of a CTA's unit slice: 16 B vectors for every full
+// chunk (partial slices too: the last CTA of a layer whose H is not a
+// multiple of U must not fall off the fast path — it would straggle every
+// step), scalar only for the ragged tail.  `vec` = the row pitch allows
+// vector access at all (the base alignment is checked here).
+__device__ __forceinline__ uint4 pack8_bf16(const float* v) {
+  uint4 w;
+  __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+  __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
+  w.x = *reinterpret_cast<uint32_t*>(&p0);
+  w.y = *reinterpret_cast<uint32_t*>(&p1);
+  w.z = *reinterpret_cast<uint32_t*>(&p2);
+  w.w = *reinterpret_cast<uint32_t*>(&p3);
+  return w;
+}
+__device__ __forceinline__ void unpack8_bf16(uint4 w, float* v) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ws[k]));
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+
 template <int U>
 __device__ __forceinline__ void store_f32(float* dst, const float* v, int nu) {
-  if (nu == U && (U % 4) == 0 && ((uintptr_t)dst & 15) == 0) {
+  int done = 0;
+  if ((U % 4) == 0 && ((uintptr_t)dst & 15) == 0) {
 #pragma unroll
     for (int i = 0; i < U; i += 4)
-      *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-  } else {
-    for (int i = 0; i < nu; ++i) dst[i] = v[i];
+      if (i + 4 <= nu) {
+        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        done = i + 4;
+      }
   }
+  for (int i = done; i < nu; ++i) dst[i] = v[i];
 }
 template <int U>
 __device__ __forceinline__ void store_bf16(__nv_bfloat16* dst, const float* v, int nu) {
-  if (nu == U && (U % 8) == 0 && ((uintptr_t)dst & 15) == 0) {
+  int done = 0;
+  if ((U % 8) == 0 && ((uintptr_t)dst & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < U; i += 8) {
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-      __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-      __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
-      __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-      uint4 w;
-      w.x = *reinterpret_cast<uint32_t*>(&p0);
-      w.y = *reinterpret_cast<uint32_t*>(&p1);
-      w.z = *reinterpret_cast<uint32_t*>(&p2);
-      w.w = *reinterpret_cast<uint32_t*>(&p3);
-      *reinterpret_cast<uint4*>(dst + i) = w;
-    }
-  } else if (nu == U && (U % 4) == 0 && ((uintptr_t)dst & 7) == 0) {
+    for (int i = 0; i < U; i += 8)
+      if (i + 8 <= nu) {
+        *reinterpret_cast<uint4*>(dst + i) = pack8_bf16(v + i);
+        done = i + 8;
+      }
+  } else if ((U % 4) == 0 && ((uintptr_t)dst & 7) == 0) {
 #pragma unroll
-    for (int i = 0; i < U; i += 4) {
-      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-      __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&p0);
-      w.y = *reinterpret_cast<uint32_t*>(&p1);
-      *reinterpret_cast<uint2*>(dst + i) = w;
-    }
-  } else {
-    for (int i = 0; i < nu; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+    for (int i = 0; i < U; i += 4)
+      if (i + 4 <= nu) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&p0);
+        w.y = *reinterpret_cast<uint32_t*>(&p1);
+        *reinterpret_cast<uint2*>(dst + i) = w;
+        done = i + 4;
+      }
   }
+  for (int i = done; i < nu; ++i) dst[i] = __float2bfloat16_rn(v[i]);
 }
 
 template <int U>
 __device__ __forceinline__ void load_f32(const float* src, float* v, int nu, bool vec) {
-  if (vec && ((uintptr_t)src & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < U; i += 4) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
-      v[i] = x.x;
-      v[i + 1] = x.y;
-      v[i + 2] = x.z;
-      v[i + 3] = x.w;
-    }
-  } else {
+  for (int i = 0; i < U; ++i) v[i] = 0.f;
+  int done = 0;
+  if (vec && (U % 4) == 0 && ((uintptr_t)src & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < U; ++i) v[i] = (i < nu) ? __ldg(src + i) : 0.f;
+    for (int i = 0; i < U; i += 4)
+      if (i + 4 <= nu) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
+        v[i] = x.x;
+        v[i + 1] = x.y;
+        v[i + 2] = x.z;
+        v[i + 3] = x.w;
+        done = i + 4;
+      }
   }
+  for (int i = done; i < nu; ++i) v[i] = __ldg(src + i);
 }
 
 template <int U>
 __device__ __forceinline__ void load_bf16(const __nv_bfloat16* src, float* v, int nu, bool vec) {
+#pragma unroll
+  for (int i = 0; i < U; ++i) v[i] = 0.f;
+  int done = 0;
   if (vec && (U % 8) == 0 && ((uintptr_t)src & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < U; i += 8) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + i));
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ws[k]));
-        v[i + 2 * k] = f.x;
-        v[i + 2 * k + 1] = f.y;
+    for (int i = 0; i < U; i += 8)
+      if (i + 8 <= nu) {
+        unpack8_bf16(__ldg(reinterpret_cast<const uint4*>(src + i)), v + i);
+        done = i + 8;
       }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < U; ++i) v[i] = (i < nu) ? __bfloat162float(src[i]) : 0.f;
   }
+  for (int i = done; i < nu; ++i) v[i] = __bfloat162float(src[i]);
 }
 
 template <int n>
