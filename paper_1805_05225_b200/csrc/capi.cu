@@ -96,9 +96,11 @@ struct Pad {
 };
 Pad pads(const Dims& d) {
   Pad p;
-  p.Dp = round_up(d.D + 1, 8);  // + a ones column (db from the dW GEMM)
-  p.Hp = round_up(d.H, 8);
-  p.G4p = round_up(4 * (int64_t)d.H, 8);
+  // 64-element multiples: the GEMM reads MN-major operands in whole 64-wide
+  // blocks (one 3-D TMA box per stage), and every row stays 16 B aligned
+  p.Dp = round_up(d.D + 1, 64);  // + a ones column (db from the dW GEMM)
+  p.Hp = round_up(d.H, 64);
+  p.G4p = round_up(4 * (int64_t)d.H, 64);
   p.Gc = d.nd * p.G4p;
   return p;
 }

@@ -39,7 +39,17 @@ struct Params {
   float* C2;
   int64_t ldc2;
   __nv_bfloat16* Cb;  // bf16 output instead of C (beta must be 0)
+  int a_blk3d, b_blk3d;  // MN-major operand loaded as ONE 3-D box per stage
 };
+
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                     int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(tc::smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
 
 template <int BN>
 struct Smem {
@@ -96,16 +106,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStage);
           const int k0 = kb * BK;
           if (A_MN) {
+            if (p.a_blk3d) {  // {mn_in 64, k rows 64, mn blocks}: the whole stage in one op
+              tma3(sa, &tmA, &full_bar[stage], 0, k0, m0 / 64);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tc::tma_load_2d(sa + j * kBoxBytes, &tmA, &full_bar[stage], m0 + 64 * j, k0);
+              for (int j = 0; j < BM / 64; ++j)
+                tc::tma_load_2d(sa + j * kBoxBytes, &tmA, &full_bar[stage], m0 + 64 * j, k0);
+            }
           } else {
             tc::tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
           }
           if (B_MN) {
+            if (p.b_blk3d) {
+              tma3(sb, &tmB, &full_bar[stage], 0, k0, n0 / 64);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tc::tma_load_2d(sb + j * kBoxBytes, &tmB, &full_bar[stage], n0 + 64 * j, k0);
+              for (int j = 0; j < BN / 64; ++j)
+                tc::tma_load_2d(sb + j * kBoxBytes, &tmB, &full_bar[stage], n0 + 64 * j, k0);
+            }
           } else {
             tc::tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
           }
@@ -272,6 +290,26 @@ CUtensorMap tmap_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld,
   return m;
 }
 
+// MN-major operand stored [K, MN] (ld) as a 3-D map {64 (mn within block),
+// K rows, MN blocks of 64}: one box = `nblk` 64x64 blocks laid out block after
+// block (8 KB apart = the UMMA descriptor's LBO).  Reads whole 64-wide blocks,
+// so the caller must guarantee round_up(MN, 64) readable elements per row.
+CUtensorMap tmap_bf16_mn3(const void* ptr, int64_t mn, int64_t k, int64_t ld, int nblk) {
+  SL_REQUIRE(((uintptr_t)ptr & 15) == 0 && (ld * 2) % 16 == 0, SL_ERR_INVALID_ARGUMENT,
+             "gemm_bf16_tc: operands need 16 B aligned base and leading dimension % 8 == 0");
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64, (cuuint64_t)k, (cuuint64_t)ceil_div(mn, 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), 128};
+  cuuint32_t box[3] = {64, 64, (cuuint32_t)nblk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SL_REQUIRE(r == CUDA_SUCCESS, SL_ERR_CUDA, "cuTensorMapEncodeTiled failed (mn3)");
+  return m;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -321,9 +359,16 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   p.Cb = g.Cb;
   SL_REQUIRE(!g.Cb || g.beta == 0.f, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc: bf16 output needs beta = 0");
   // A: K-major stored [M, K]; MN-major stored [K, M].  B: K-major stored [N, K]; MN-major [K, N].
-  const CUtensorMap ta = g.a_mn ? tmap_bf16(g.A, g.M, g.K, g.lda, 64)
+  // one 3-D box per stage for MN-major operands when whole 64-blocks are readable
+  // (the LSTM's buffers are padded so; callers offsetting into a row, like
+  // DZ's per-direction column blocks, keep offset + round_up(MN, 64) <= ld)
+  p.a_blk3d = g.a_mn && g.lda >= round_up(g.M, 64);
+  p.b_blk3d = g.b_mn && g.ldb >= round_up(g.N, 64);
+  const CUtensorMap ta = g.a_mn ? (p.a_blk3d ? tmap_bf16_mn3(g.A, g.M, g.K, g.lda, BM / 64)
+                                             : tmap_bf16(g.A, g.M, g.K, g.lda, 64))
                                 : tmap_bf16(g.A, g.K, g.M, g.lda, BM);
-  const CUtensorMap tb = g.b_mn ? tmap_bf16(g.B, g.N, g.K, g.ldb, 64)
+  const CUtensorMap tb = g.b_mn ? (p.b_blk3d ? tmap_bf16_mn3(g.B, g.N, g.K, g.ldb, BN / 64)
+                                             : tmap_bf16(g.B, g.N, g.K, g.ldb, 64))
                                 : tmap_bf16(g.B, g.K, g.N, g.ldb, BN);
   if (!g.a_mn && g.b_mn) launch<BN, false, true>(ta, tb, p, stream);
   else if (!g.a_mn && !g.b_mn) launch<BN, false, false>(ta, tb, p, stream);

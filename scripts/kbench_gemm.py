@@ -11,8 +11,10 @@ res = []
 for (name, M, N, K, a_mn, b_mn) in [("k1_xw", 15360, 8000, 2000, 0, 1), ("k4_dx", 15360, 2000, 8000, 0, 0),
                                     ("k4_dw", 2000, 8000, 15360, 1, 1), ("k4_dr", 1000, 4000, 15360, 1, 1),
                                     ("sq8192", 8192, 8192, 8192, 0, 0)]:
-    A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
-    B = torch.randn((K, N) if b_mn else (N, K), device="cuda").bfloat16()
+    # MN-major operands padded to 64-multiples like the layer's buffers
+    pad = lambda n: (n + 63) // 64 * 64
+    A = torch.randn((K, pad(M)) if a_mn else (M, K), device="cuda").bfloat16()
+    B = torch.randn((K, pad(N)) if b_mn else (N, K), device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     f = lambda: L.sl_debug_gemm_bf16(M, N, K, A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn, C.data_ptr(), N, 1.0, 0.0, None, s)
@@ -25,8 +27,8 @@ for (name, M, N, K, a_mn, b_mn) in [("k1_xw", 15360, 8000, 2000, 0, 1), ("k4_dx"
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     # torch/cuBLAS on the same shape for context
-    opA = A.t() if a_mn else A
-    opB = B if b_mn else B.t()
+    opA = A[:, :M].t() if a_mn else A
+    opB = B[:, :N] if b_mn else B.t()
     for _ in range(3): torch.matmul(opA, opB)
     torch.cuda.synchronize()
     e0.record()
