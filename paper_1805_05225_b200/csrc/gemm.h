@@ -38,5 +38,9 @@ struct TcGemm {
   __nv_bfloat16* Cb = nullptr;
 };
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
+// CTA-pair variant (gemm_tc2.cu, M = 256 tiles); gemm_bf16_tc dispatches to it
+// when the operands allow (gemm_bf16_tc2_ok) unless SL_GEMM_1CTA is set.
+bool gemm_bf16_tc2_ok(const TcGemm& g);
+void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream);
 
 }  // namespace sl

@@ -16,6 +16,7 @@
 // kernel serves X.W, DZ.W^T and X^T.DZ without any transpose pass.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.h"
@@ -340,6 +341,12 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStr
 
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   if (g.M <= 0 || g.N <= 0) return;
+  static const bool one_cta = getenv("SL_GEMM_1CTA") != nullptr;
+  if (!one_cta && gemm_bf16_tc2_ok(g)) {
+    SL_REQUIRE(!g.Cb || g.beta == 0.f, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc: bf16 output needs beta = 0");
+    gemm_bf16_tc2(g, stream);
+    return;
+  }
   constexpr int BN = 256;
   Params p{};
   p.M = g.M;

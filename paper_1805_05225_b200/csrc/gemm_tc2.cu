@@ -1,0 +1,374 @@
+// 2-CTA (CTA-pair) BF16 tensor-core GEMM: tcgen05.mma.cta_group::2, M = 256.
+//
+// The same operation as gemm_tc.cu (C = alpha op(A) op(B) + beta C + bias,
+// K-/MN-major operands, fp32 / bf16 / split-C epilogues) with the Blackwell
+// CTA-pair datapath: a cluster of two CTAs on one TPC computes a 256 x 256
+// tile; each CTA TMA-loads its 128 rows of A and its 128 columns of B per
+// K-block (32 KB per stage instead of 48 KB for a 128 x 256 single-CTA tile),
+// the leader issues one M=256 N=256 K=16 MMA for both, and each CTA's TMEM
+// receives its 128 rows of the accumulator.  Both CTAs' TMA loads complete on
+// the LEADER's full barrier (.cta_group::2), MMA completion is multicast to
+// both CTAs' empty / tmem-full barriers, and both epilogues release the
+// accumulator on the leader's tmem-empty barrier.
+#include <cudaTypedefs.h>
+
+#include "gemm.h"
+#include "profile.h"
+#include "tc.cuh"
+
+namespace sl {
+namespace {
+
+constexpr int BMP = 256, BNP = 256, BK = 64, kStages = 6, kThreads = 192;
+constexpr uint32_t kHalf = 128 * 64 * 2;  // 16 KB: 128 rows (or cols) x 64 K of bf16
+constexpr uint32_t kStage = 2 * kHalf;    // A half + B half per CTA
+constexpr uint32_t kSmem = kStages * kStage + 1024;
+
+struct P2 {
+  int M, N, K, nm, nn, nk;
+  float* C;
+  int64_t ldc;
+  float alpha, beta;
+  const float* bias;
+  int m_split;
+  float* C2;
+  int64_t ldc2;
+  __nv_bfloat16* Cb;
+};
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// TMA into this CTA's smem, completing on the (possibly peer) barrier `bar_cl`
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* m, uint32_t bar_cl, int c0,
+                                          int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(bar_cl)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d_pair(uint32_t dst, const CUtensorMap* m, uint32_t bar_cl, int c0,
+                                          int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cl)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on the barrier at this smem offset in BOTH CTAs of the pair when the
+// issuing thread's prior MMAs complete
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(tc::smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t bar_cl, uint32_t count) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cl),
+               "r"(count)
+               : "memory");
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, P2 p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_sh;
+  const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t r = cta_rank();
+  const bool leader = r == 0;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull_bar[a], 1);
+      tc::mbar_init(&tempty_bar[a], 2 * 128);  // both CTAs' epilogue threads (leader's copy used)
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {  // same warp id in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tmem_sh)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  cluster_sync_all();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_sh;
+  const int ntiles = p.nm * p.nn;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        const int m0 = (t % p.nm) * BMP + r * 128, n0 = (t / p.nm) * BNP + r * 128;
+        for (int kb = 0; kb < p.nk; ++kb) {
+          tc::mbar_wait(&empty_bar[st], ph ^ 1);
+          const uint32_t sa = base + st * kStage, sb = sa + kHalf;
+          const uint32_t fb = mapa_u32(tc::smem_u32(&full_bar[st]), 0);  // leader's barrier
+          if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * kStage);
+          const int k0 = kb * BK;
+          if (A_MN) tma3d_pair(sa, &tmA, fb, 0, k0, m0 / 64);
+          else tma2d_pair(sa, &tmA, fb, k0, m0);
+          if (B_MN) tma3d_pair(sb, &tmB, fb, 0, k0, n0 / 64);
+          else tma2d_pair(sb, &tmB, fb, k0, n0);
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = tc::make_idesc(BMP, BNP, 1, A_MN, B_MN);
+      int st = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        for (int kb = 0; kb < p.nk; ++kb) {
+          tc::mbar_wait(&full_bar[st], ph);
+          tc::fence_after_sync();
+          const uint32_t sa = base + st * kStage, sb = sa + kHalf;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? tc::make_sdesc(sa + k * 2048, 8192, 1024)
+                                     : tc::make_sdesc(sa + k * 32, 0, 1024);
+            const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, 8192, 1024)
+                                     : tc::make_sdesc(sb + k * 32, 0, 1024);
+            mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb | k) != 0);
+          }
+          commit_pair(&empty_bar[st]);  // frees the slot in both CTAs
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        commit_pair(&tfull_bar[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1)
+    const int q = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa_u32(tc::smem_u32(&tempty_bar[0]), 0),
+                                       mapa_u32(tc::smem_u32(&tempty_bar[1]), 0)};
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int acc = it & 1;
+      const int m0 = (t % p.nm) * BMP + r * 128, n0 = (t / p.nm) * BNP;
+      tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc::fence_after_sync();
+      const int row = m0 + 32 * q + lane;
+      const bool second = row >= p.m_split;
+      float* crow = second ? p.C2 + (int64_t)(row - p.m_split) * p.ldc2 : p.C + (int64_t)row * p.ldc;
+      const bool vec = second ? (p.ldc2 % 4) == 0 && ((uintptr_t)p.C2 & 15) == 0
+                              : (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0;
+#pragma unroll 1
+      for (int c = 0; c < BNP; c += 32) {
+        float v[32];
+        tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + c, v);
+        const int col0 = n0 + c;
+        if (p.Cb) {
+          if (row >= p.M) continue;
+          __nv_bfloat16* brow = p.Cb + (int64_t)row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              float o[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = p.alpha * v[j + i] + (p.bias ? p.bias[col0 + j + i] : 0.f);
+              uint4 w;
+              __nv_bfloat162 t0 = __floats2bfloat162_rn(o[0], o[1]), t1 = __floats2bfloat162_rn(o[2], o[3]);
+              __nv_bfloat162 t2 = __floats2bfloat162_rn(o[4], o[5]), t3 = __floats2bfloat162_rn(o[6], o[7]);
+              w.x = *reinterpret_cast<uint32_t*>(&t0);
+              w.y = *reinterpret_cast<uint32_t*>(&t1);
+              w.z = *reinterpret_cast<uint32_t*>(&t2);
+              w.w = *reinterpret_cast<uint32_t*>(&t3);
+              *reinterpret_cast<uint4*>(brow + j) = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+              brow[j] = __float2bfloat16_rn(p.alpha * v[j] + (p.bias ? p.bias[col0 + j] : 0.f));
+          }
+          continue;
+        }
+        if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
+        if (vec && col0 + 32 <= p.N) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 o = make_float4(p.alpha * v[j], p.alpha * v[j + 1], p.alpha * v[j + 2],
+                                   p.alpha * v[j + 3]);
+            if (p.bias) {
+              const float4 bb = *reinterpret_cast<const float4*>(p.bias + col0 + j);
+              o.x += bb.x;
+              o.y += bb.y;
+              o.z += bb.z;
+              o.w += bb.w;
+            }
+            float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
+            if (p.beta != 0.f) {
+              const float4 old = *dst;
+              o.x += p.beta * old.x;
+              o.y += p.beta * old.y;
+              o.z += p.beta * old.z;
+              o.w += p.beta * old.w;
+            }
+            *dst = o;
+          }
+        } else {
+          for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+            float o = p.alpha * v[j];
+            if (p.bias) o += p.bias[col0 + j];
+            float* dst = crow + col0 + j;
+            if (p.beta != 0.f) o += p.beta * *dst;
+            *dst = o;
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) arrive_remote(tempty_leader[acc], 32);  // release the accumulator (leader's barrier)
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM goes away
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 enc2() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    SL_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+CUtensorMap tm2d(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  SL_REQUIRE(enc2()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS,
+             SL_ERR_CUDA, "cuTensorMapEncodeTiled failed (gemm2 2d)");
+  return m;
+}
+CUtensorMap tm3d_mn(const void* ptr, int64_t mn, int64_t k, int64_t ld) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64, (cuuint64_t)k, (cuuint64_t)ceil_div(mn, 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), 128};
+  cuuint32_t box[3] = {64, 64, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  SL_REQUIRE(enc2()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS,
+             SL_ERR_CUDA, "cuTensorMapEncodeTiled failed (gemm2 3d)");
+  return m;
+}
+
+int sms2() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <bool A_MN, bool B_MN>
+void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream_t s) {
+  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    configured = true;
+  }
+  const int tiles = p.nm * p.nn;
+  const int pairs = std::min(tiles, sms2() / 2);
+  kern<<<2 * pairs, kThreads, kSmem, s>>>(a, b, p);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace
+
+bool gemm_bf16_tc2_ok(const TcGemm& g) {
+  // MN-major operands must be loadable as whole 64-wide blocks (3-D boxes)
+  return (!g.a_mn || g.lda >= round_up(g.M, 64)) && (!g.b_mn || g.ldb >= round_up(g.N, 64));
+}
+
+void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
+  P2 p{};
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.nm = (int)ceil_div(g.M, BMP);
+  p.nn = (int)ceil_div(g.N, BNP);
+  p.nk = (int)ceil_div(g.K, BK);
+  p.C = g.C;
+  p.ldc = g.ldc;
+  p.alpha = g.alpha;
+  p.beta = g.beta;
+  p.bias = g.bias;
+  p.m_split = g.m_split;
+  p.C2 = g.C2;
+  p.ldc2 = g.ldc2;
+  p.Cb = g.Cb;
+  SL_REQUIRE(((uintptr_t)g.A & 15) == 0 && ((uintptr_t)g.B & 15) == 0 && (g.lda * 2) % 16 == 0 &&
+                 (g.ldb * 2) % 16 == 0,
+             SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: operands need 16 B alignment");
+  const CUtensorMap ta = g.a_mn ? tm3d_mn(g.A, g.M, g.K, g.lda) : tm2d(g.A, g.K, g.M, g.lda, 128);
+  const CUtensorMap tb = g.b_mn ? tm3d_mn(g.B, g.N, g.K, g.ldb) : tm2d(g.B, g.K, g.N, g.ldb, 128);
+  if (!g.a_mn && g.b_mn) launch2<false, true>(ta, tb, p, stream);
+  else if (!g.a_mn && !g.b_mn) launch2<false, false>(ta, tb, p, stream);
+  else if (g.a_mn && g.b_mn) launch2<true, true>(ta, tb, p, stream);
+  else launch2<true, false>(ta, tb, p, stream);
+}
+
+}  // namespace sl
