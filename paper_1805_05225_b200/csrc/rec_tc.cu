@@ -281,7 +281,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       }
 
       if (valid_row && !(a.debug_flags & 2)) {
-        __nv_bfloat16* hn = hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0;
         if (active) {
           if (save) {  // c_{s-1}, h_{s-1} before the update
             store_bf16<UT>(a.cprev[d] + pos * H + ut0, cst, nu);
@@ -301,6 +300,20 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             cst[u] = cn;
             hst[u] = go * tc::tanh_approx(cn);
           }
+        }
+        // only h_s is on the cross-CTA critical path: write it, publish, and
+        // store everything else (saves, y) afterwards
+        store_bf16<UT>(hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0, hst, nu);
+      }
+      if (tr0) a.trace[s * 16 + 11] = gtimer();
+      named_sync(1 + mt, kEpiTile);  // the tile's epilogue threads only
+      if ((e % (4 * SPLIT)) == 0 && lane == 0) {
+        tc::fence_proxy_async_global();
+        red_release_gpu(ctr + mt, 1u);
+        SL_TRACE(6 + mt);
+      }
+      if (valid_row && !(a.debug_flags & 2)) {
+        if (active) {
           if (save) {
             __nv_bfloat16* gsave = a.gates[d] + pos * 4 * H + ut0;
 #pragma unroll
@@ -316,14 +329,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
           if (save) store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
         }
-        store_bf16<UT>(hn, hst, nu);
-      }
-      if (tr0) a.trace[s * 16 + 11] = gtimer();
-      named_sync(1 + mt, kEpiTile);  // the tile's epilogue threads only
-      if ((e % (4 * SPLIT)) == 0 && lane == 0) {
-        tc::fence_proxy_async_global();
-        red_release_gpu(ctr + mt, 1u);
-        SL_TRACE(6 + mt);
       }
     }
     // positions beyond the longest sequence, final states

@@ -257,7 +257,6 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 
       if (valid_row) {
         __nv_bfloat16* zn = zr + ((size_t)((it + 1) & 1) * a.B + row) * a.Kz + ut0;
-        __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
         float* dz = gv;  // DZ overwrites the gate values in place (unit by unit)
         if (active) {
           const bool last = (s == len - 1);
@@ -282,10 +281,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           for (int j = 0; j < 4 * UT; ++j) dz[j] = 0.f;
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          store_bf16<UT>(zn + g * H, dz + g * UT, nu);
-          store_bf16<UT>(zc + g * H, dz + g * UT, nu);
-        }
+        for (int g = 0; g < 4; ++g) store_bf16<UT>(zn + g * H, dz + g * UT, nu);
       }
       if (tr0) a.trace[it * 16 + 11] = gtimer();
       named_sync(1 + mt, kEpiTile);
@@ -293,6 +289,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         tc::fence_proxy_async_global();
         red_release_gpu(ctr + mt, 1u);
         if (a.trace && blockIdx.x == a.trace_cta) a.trace[it * 16 + 6 + mt] = gtimer();
+      }
+      if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
+        __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) store_bf16<UT>(zc + g * H, gv + g * UT, nu);
       }
     }
     if (valid_row) {  // DZ rows of positions beyond the longest sequence
