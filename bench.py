@@ -324,8 +324,14 @@ def main():
         per_launch_ms = e["ms"] / max(e["calls"], 1)
         achieved = e["flops"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e12
         peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        traffic = None
+        try:  # DRAM bytes per launch of this kernel from the committed ncu capture
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(name)
+        except Exception:
+            pass
         roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"
                 if peaks else "fallback 1400",
                 "share_of_step": e["ms"] / r["ms"],

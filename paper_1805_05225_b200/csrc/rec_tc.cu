@@ -397,6 +397,13 @@ void launch_fwd(const CUtensorMap* tr, const CUtensorMap* th, const TcRecFwdArgs
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
+  // SL_NO_COOP=1 (profiling only): ncu cannot launch cooperative cluster
+  // kernels; the grid (<= #SMs, 1 CTA/SM) is still co-resident in practice.
+  static const bool no_coop = getenv("SL_NO_COOP") != nullptr;
+  if (no_coop) {
+    cfg.attrs = attrs + 1;
+    cfg.numAttrs = 1;
+  }
   SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, h0, h1, copy));
   count_launch();
 }

@@ -15,6 +15,8 @@
 //               DZ matrix the hoisted K4 GEMMs consume; db is reduced on the fly.
 // As in K2 the two 128-row batch tiles are independent recurrences with their
 // own step counters, so one tile's epilogue overlaps the other's MMAs.
+#include <cstdlib>
+
 #include "profile.h"
 #include "rec_tc.h"
 #include "rec_tc_common.cuh"
@@ -356,6 +358,13 @@ void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
+  // SL_NO_COOP=1 (profiling only): ncu cannot launch cooperative cluster
+  // kernels; the grid (<= #SMs, 1 CTA/SM) is still co-resident in practice.
+  static const bool no_coop = getenv("SL_NO_COOP") != nullptr;
+  if (no_coop) {
+    cfg.attrs = attrs + 1;
+    cfg.numAttrs = 1;
+  }
   SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, z0, z1, copy));
   count_launch();
 }
