@@ -32,7 +32,8 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 __host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
 uint32_t bwd_smem(int C, int U, int Kc, int stages) {  // stages of two 16 KB chunks
-  const uint32_t recv = C > 1 ? (uint32_t)C * U * 128 * 4 : 0;
+  // per batch tile: [C-1 slots][128 rows][U] bf16 partials from the peers
+  const uint32_t recv = C > 1 ? (uint32_t)2 * (C - 1) * U * 128 * 2 : 0;
   return (uint32_t)nb_of(C, U) * Kc * 2 + stages * kTile * 2 + recv + 1024;
 }
 
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar[MT], tempty_bar[MT];
-  __shared__ __align__(8) uint64_t recv_full, free_bar[C];
+  __shared__ __align__(8) uint64_t recv_full[MT], free_bar[MT][C];
   __shared__ uint32_t tmem_sh;
   __shared__ int tmax_sh;
 
@@ -70,7 +71,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
   const uint32_t stage_bytes = kTile * a.kb;  // a.kb 64-wide K chunks per TMA box
-  float* recv = reinterpret_cast<float*>(sA + a.stages * stage_bytes);  // [C][U][128] partials from peers
+  // [MT][C-1 slots][128 rows][U] bf16 partials from the peers: one buffer per
+  // batch tile (a shared buffer would couple the two tiles' recurrences through
+  // its free/full handshake) and row-major, so each sender thread writes its
+  // row's slice with 16 B DSMEM stores
+  __nv_bfloat16* recv = reinterpret_cast<__nv_bfloat16*>(sA + a.stages * stage_bytes);
   const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
@@ -86,8 +91,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::mbar_init(&tfull_bar[m], 1);
       tc::mbar_init(&tempty_bar[m], kEpiTile);
     }
-    tc::mbar_init(&recv_full, (C - 1) * kEpiTile);
-    for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[p], kEpiTile);
+    for (int m = 0; m < MT; ++m) {
+      tc::mbar_init(&recv_full[m], (C - 1) * kEpiTile);
+      for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[m][p], kEpiTile);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 
     for (int it = 0; it < Tmax; ++it) {
       const int s = Tmax - 1 - it;  // processing step
-      const int use = it * MT + mt;  // index of this tile's use of the shared exchange buffer
+      const int use = it;  // this tile's exchange buffer is used once per step
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
@@ -225,36 +232,66 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 #pragma unroll 1
         for (int pi = 1; pi < C; ++pi) {
           const int p = (r + pi) % C;
-          if (use > 0) mbar_wait_cluster(&free_bar[p], (use - 1) & 1);
+          if (use > 0) {  // one cluster-scope acquire per warp, then warp-ordered
+            if (lane == 0) mbar_wait_cluster(&free_bar[mt][p], (use - 1) & 1);
+            __syncwarp();
+          }
           float v[UT];
           tmem_ld_cols<UT>(tbase + p * U + lo, v);
-          const uint32_t dst = mapa(tc::smem_u32(recv + ((size_t)r * U + lo) * 128 + rl), p);
+          const int slot_at_p = (r - p + C) % C - 1;  // my slot in p's buffer
+          const uint32_t dst = mapa(
+              tc::smem_u32(recv + (((size_t)mt * (C - 1) + slot_at_p) * 128 + rl) * U + lo), p);
+          if constexpr (UT % 8 == 0) {
 #pragma unroll
-          for (int u = 0; u < UT; ++u) st_cluster_f32(dst + u * 128 * 4, v[u]);
+            for (int u = 0; u < UT; u += 8) {  // 8 bf16 = one 16 B DSMEM store
+              const uint4 w = pack8_bf16(v + u);
+              asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + u * 2),
+                           "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                           : "memory");
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < UT; ++u) {
+              const __nv_bfloat16 hv = __float2bfloat16_rn(v[u]);
+              asm volatile("st.shared::cluster.b16 [%0], %1;" ::"r"(dst + u * 2),
+                           "h"(*reinterpret_cast<const unsigned short*>(&hv))
+                           : "memory");
+            }
+          }
         }
         __syncwarp();
         if (lane == 0)
           for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full), (r + pi) % C), 32);
+            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full[mt]), (r + pi) % C), 32);
       }
       if (tr0) a.trace[it * 16 + 9] = gtimer();
       tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
       if constexpr (C > 1) {
-        mbar_wait_cluster(&recv_full, use & 1);
+        if (lane == 0) mbar_wait_cluster(&recv_full[mt], use & 1);
+        __syncwarp();
         if (tr0) a.trace[it * 16 + 10] = gtimer();
 #pragma unroll 1
-        for (int pi = 1; pi < C; ++pi) {
-          const int p = (r + pi) % C;
-          const float* src = recv + ((size_t)p * U + lo) * 128 + rl;
+        for (int sl = 0; sl < C - 1; ++sl) {
+          const __nv_bfloat16* src = recv + (((size_t)mt * (C - 1) + sl) * 128 + rl) * U + lo;
+          if constexpr (UT % 8 == 0) {
 #pragma unroll
-          for (int u = 0; u < UT; ++u) dh[u] += src[u * 128];
+            for (int u = 0; u < UT; u += 8) {
+              float f[8];
+              unpack8_bf16(*reinterpret_cast<const uint4*>(src + u), f);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) dh[u + k] += f[k];
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < UT; ++u) dh[u] += __bfloat162float(src[u]);
+          }
         }
         __syncwarp();
         if (lane == 0)  // tell every sender its slot in my buffer is free again
           for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[r]), (r + pi) % C), 32);
+            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
       }
 
       if (valid_row) {

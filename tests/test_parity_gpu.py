@@ -238,3 +238,49 @@ def test_lstm_sequence_functional_matches_layer(cuda):
     y = lstm.lstm_sequence(x, lens, W, R, b, -1)
     ref = torch_ref.sequence(x, lens, W, R, b, -1)
     assert rel(y, ref["y"]) < 1e-4
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_batch_chunks_beyond_256(cuda, prec):
+    # B > 256: the tensor-core recurrences run as several 256-row batch launches
+    B, T, D, H = 300, 12, 24, 40
+    x, lens, W, R, b = _seeded(21, B, T, D, H)
+    dy = torch.rand(B, T, 2 * H, device="cuda") * 2 - 1
+    params = [(W, R, b), _seeded(22, 1, 1, D, H)[2:]]
+    out = run_layer(x, lens, params, 2, 1, prec, dy)
+    dx = 0
+    for k, d in enumerate((1, -1)):
+        Wk, Rk, bk = params[k]
+        ref = torch_ref.sequence(x, lens, Wk, Rk, bk, d, dy[:, :, k * H:(k + 1) * H])
+        assert rel(out["y"][:, :, k * H:(k + 1) * H], ref["y"]) < TOL[prec]
+        assert rel(out["h_last"][k], ref["h_last"]) < TOL[prec]
+        for g in ("dW", "dR", "db"):
+            assert rel(out[g][k], ref[g]) < TOL[prec], g
+        dx = dx + ref["dx"]
+    assert rel(out["dx"], dx) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("shape", [(1, 7, 5, 3), (3, 4, 9, 13), (5, 17, 33, 100)])
+def test_small_and_odd_shapes(cuda, prec, shape):
+    # B = 1, H not a multiple of 8 / 16 (partial unit slices), D not aligned
+    B, T, D, H = shape
+    x, lens, W, R, b = _seeded(23, B, T, D, H)
+    dy = torch.rand(B, T, H, device="cuda") * 2 - 1
+    out = run_layer(x, lens, [(W, R, b)], 1, -1, prec, dy)
+    ref = torch_ref.sequence(x, lens, W, R, b, -1, dy)
+    for k in ("y", "dx"):
+        assert rel(out[k], ref[k]) < TOL[prec], k
+    for k in ("dW", "dR", "db"):
+        assert rel(out[k][0], ref[k]) < TOL[prec], k
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_inference_mode_matches_training_forward(cuda, prec):
+    # forward without a reserve (inference: nothing saved) gives the same y / final states
+    x, lens, W, R, b = _seeded(24, 16, 20, 32, 48)
+    layer = lstm.LSTMLayer(16, 20, 32, 48, 2, 1, prec)
+    y1, h1, c1 = layer.forward(x, lens, [W, W], [R, R], [b, b], train=True)
+    y2, h2, c2 = layer.forward(x, lens, [W, W], [R, R], [b, b], train=False)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(h1, h2) and torch.equal(c1, c2)
