@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("SL_BENCH_PREC", "fp32"))
+    ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("SL_BENCH_PREC", "bf16"))
     ap.add_argument("--batch", type=int, default=256, help="sequences per GPU (weak scaling)")
     ap.add_argument("--layers", type=int, default=6)
     ap.add_argument("--hidden", type=int, default=1000)

@@ -9,8 +9,10 @@
  *
  * Conventions (all match the reference's layouts so no caller-side reshuffle
  * is needed, reference tensor.hpp:21 canonical order, row-major):
- *   x   [B, T, D]          fp32, batch-major, padded positions t >= len[b] ignored
- *   y   [B, T, ndir*H]     fp32; direction d writes columns [d*H, (d+1)*H) — the
+ *   x   [B, T, D]          fp32 (bf16 padded with SL_LAYER_X_BF16), batch-major, padded
+ *                          positions t >= len[b] ignored
+ *   y   [B, T, ndir*H]     fp32 (bf16 padded with SL_LAYER_Y_BF16); direction d writes
+ *                          columns [d*H, (d+1)*H) — the
  *                          concat_feature([fw, bw]) layout; padded positions are 0
  *   W   [D, 4H]  R [H, 4H]  b [4H]   fp32, gate blocks (i | f | g | o)
  *   seq_lens [B]           int32 in (0, T] (reference tensor.cpp:121-138)
@@ -49,6 +51,20 @@ enum sl_precision {
   SL_PREC_BF16 = 1  /* bf16 tensor-core operands, fp32 accumulate / cell state; rel. 2e-2 */
 };
 
+/* sl_lstm_layer.flags (SL_PREC_BF16 only): bf16 activations between stacked
+ * layers, so a layer's output feeds the next layer's input GEMM with no fp32
+ * round trip and no conversion pass.  The bf16 tensors are row-padded to
+ * sl_lstm_bf16_pitch(features) columns with 1.0 in column `features` (the
+ * layer's own bias/db column) and FINITE (e.g. zero-initialised) padding. */
+enum sl_layer_flags {
+  SL_LAYER_X_BF16 = 1, /* x is bf16 [B, T, sl_lstm_bf16_pitch(D)], 1.0 at column D; kept
+                          unchanged by the caller until the matching bwd */
+  SL_LAYER_Y_BF16 = 2  /* y is written as bf16 [B, T, sl_lstm_bf16_pitch(ndir*H)] with 1.0 at
+                          column ndir*H: directly the next layer's SL_LAYER_X_BF16 input */
+};
+/* Row pitch (elements) of the padded bf16 activation layout: round_up(features + 1, 64). */
+int64_t sl_lstm_bf16_pitch(int32_t features);
+
 /* One LSTM layer, one or two directions over the same input. */
 typedef struct sl_lstm_layer {
   int32_t batch;     /* B  */
@@ -58,7 +74,7 @@ typedef struct sl_lstm_layer {
   int32_t num_dirs;  /* 1, or 2 = bidirectional: dir 0 forward, dir 1 backward, run concurrently */
   int32_t direction; /* num_dirs == 1: +1 or -1 (reference layers.cpp:14) */
   int32_t precision; /* enum sl_precision */
-  int32_t flags;     /* reserved, must be 0 */
+  int32_t flags;     /* enum sl_layer_flags (0 = fp32 x / y) */
 } sl_lstm_layer;
 
 /* Library version (major*10000 + minor*100 + patch). */

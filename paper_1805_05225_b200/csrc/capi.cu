@@ -45,7 +45,10 @@ struct Carve {
 
 struct Dims {
   int B, T, D, H, nd;
+  int flags = 0;
   int64_t BT() const { return (int64_t)B * T; }
+  bool x_bf16() const { return flags & SL_LAYER_X_BF16; }
+  bool y_bf16() const { return flags & SL_LAYER_Y_BF16; }
 };
 
 void validate(const sl_lstm_layer* L) {
@@ -60,11 +63,14 @@ void validate(const sl_lstm_layer* L) {
                  " D=" + std::to_string(L->input_dim) + " H=" + std::to_string(L->hidden));
   SL_REQUIRE(L->precision == SL_PREC_FP32 || L->precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
              "precision " + std::to_string(L->precision) + " not supported by this build");
-  SL_REQUIRE(L->flags == 0, SL_ERR_INVALID_ARGUMENT, "sl_lstm_layer.flags must be 0");
+  SL_REQUIRE((L->flags & ~(SL_LAYER_X_BF16 | SL_LAYER_Y_BF16)) == 0, SL_ERR_INVALID_ARGUMENT,
+             "sl_lstm_layer.flags: unknown bits " + std::to_string(L->flags));
+  SL_REQUIRE(L->flags == 0 || L->precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
+             "sl_lstm_layer.flags: bf16 activations need precision SL_PREC_BF16");
 }
 
 Dims dims(const sl_lstm_layer* L) {
-  return Dims{L->batch, L->time, L->input_dim, L->hidden, L->num_dirs};
+  return Dims{L->batch, L->time, L->input_dim, L->hidden, L->num_dirs, L->flags};
 }
 
 struct ReserveView {
@@ -74,8 +80,8 @@ struct ReserveView {
   __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
   __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
   __nv_bfloat16* hprevb[2] = {nullptr, nullptr};  // bf16 path: h_{s-1} [B*T, Hp]
-  __nv_bfloat16* gatesb[2] = {nullptr, nullptr};  // bf16 path: saved (i,f,g,o) [B*T, 4H]
-  __nv_bfloat16* cprevb[2] = {nullptr, nullptr};  // bf16 path: saved c_{s-1} [B*T, H]
+  __nv_bfloat16* gatesb[2] = {nullptr, nullptr};  // bf16 path: saved (i,f,g,o), step-major (rec_tc.h)
+  __nv_bfloat16* cprevb[2] = {nullptr, nullptr};  // bf16 path: saved c_{s-1}, step-major
   __nv_bfloat16* rt[2] = {nullptr, nullptr};      // bf16 path: packed R^T slices
 };
 
@@ -110,8 +116,8 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
   ReserveView r;
   for (int k = 0; k < d.nd; ++k) {
     if (prec == SL_PREC_BF16) {
-      r.gatesb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * 4 * d.H);
-      r.cprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * d.H);
+      r.gatesb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * 4 * save_hq(d.H));  // step-major, rec_tc.h
+      r.cprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * save_hq(d.H));
     } else {
       r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
       r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
@@ -122,7 +128,7 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
     const Pad pd = pads(d);
     const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
     SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
-    r.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
+    if (!d.x_bf16()) r.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);  // else the caller's x
     r.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
     for (int k = 0; k < d.nd; ++k) {
       r.hprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Hp);
@@ -157,7 +163,7 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
     w.xw_ld = pd.Gc;
     for (int k = 0; k < d.nd; ++k) w.xwb[k] = xw ? xw + k * pd.G4p : nullptr;
     w.bcat = c.take<float>((size_t)pd.Gc);
-    w.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
+    if (!d.x_bf16()) w.xb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Dp);
     w.wcat = c.take<__nv_bfloat16>((size_t)d.D * pd.Gc);
     const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
     SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
@@ -239,6 +245,8 @@ extern "C" {
 
 int sl_version(void) { return 100; }
 
+int64_t sl_lstm_bf16_pitch(int32_t features) { return round_up((int64_t)features + 1, 64); }
+
 const char* sl_last_error(void) { return g_last_error.c_str(); }
 
 int sl_lstm_layer_check(const sl_lstm_layer* L) {
@@ -296,7 +304,8 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       // Pack [W_fw | W_bw] and x to bf16 (kept in the reserve for the backward
       // GEMMs), then K1 for both directions as ONE tcgen05 GEMM.
       const Pad pd = pads(d);
-      __nv_bfloat16* xb = rv.xb ? rv.xb : w.xb;
+      __nv_bfloat16* xb = d.x_bf16() ? reinterpret_cast<__nv_bfloat16*>(const_cast<float*>(x))
+                                     : (rv.xb ? rv.xb : w.xb);
       __nv_bfloat16* wcat = rv.wcat ? rv.wcat : w.wcat;
       if (pd.G4p != 4 * d.H) {
         SL_CUDA_TRY(cudaMemsetAsync(wcat, 0, sizeof(__nv_bfloat16) * d.D * pd.Gc, stream));
@@ -307,8 +316,10 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
         SL_CUDA_TRY(cudaMemcpyAsync(w.bcat + k * pd.G4p, b[k], sizeof(float) * 4 * d.H,
                                     cudaMemcpyDeviceToDevice, stream));
       }
-      f32_to_bf16(d.BT(), d.D, x, d.D, xb, pd.Dp, stream);
-      fill_col_bf16(d.BT(), d.D, xb, pd.Dp, 1.f, stream);
+      if (!d.x_bf16()) {
+        f32_to_bf16(d.BT(), d.D, x, d.D, xb, pd.Dp, stream);
+        fill_col_bf16(d.BT(), d.D, xb, pd.Dp, 1.f, stream);
+      }
       Phase ph(stream, "k1_xw_gemm", k1_flops);
       TcGemm g{(int)d.BT(), (int)pd.Gc, d.D, xb, pd.Dp, false, wcat, pd.Gc, true,
                nullptr, pd.Gc, 1.f, 0.f, w.bcat};
@@ -330,8 +341,14 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
       a.lens = seq_lens;
       a.xw_ld = w.xw_ld;
-      a.y = y;
-      a.y_ld = (int64_t)d.nd * d.H;
+      if (d.y_bf16()) {  // the next layer's padded bf16 input, with its ones column
+        a.ybf = reinterpret_cast<__nv_bfloat16*>(y);
+        a.ybf_ld = round_up((int64_t)d.nd * d.H + 1, 64);
+        fill_col_bf16(d.BT(), d.nd * d.H, a.ybf, a.ybf_ld, 1.f, stream);
+      } else {
+        a.y = y;
+        a.y_ld = (int64_t)d.nd * d.H;
+      }
       a.h_last = h_last;
       a.c_last = c_last;
       a.hprev_ld = pd.Hp;
@@ -459,7 +476,9 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
         float* dbk = db ? db[k] : nullptr;
         if ((dW && dW[k]) || dbk) {
           Phase ph(stream, "k4_dw_gemm", fx);
-          TcGemm g{d.D + 1, G, M, rv.xb, pd.Dp, true, w.dzb + k * pd.G4p, pd.Gc, true,
+          const __nv_bfloat16* xb =
+              d.x_bf16() ? reinterpret_cast<const __nv_bfloat16*>(x) : rv.xb;
+          TcGemm g{d.D + 1, G, M, xb, pd.Dp, true, w.dzb + k * pd.G4p, pd.Gc, true,
                    dW ? dW[k] : nullptr, G, 1.f, beta, nullptr};
           g.m_split = d.D;
           g.C2 = dbk;

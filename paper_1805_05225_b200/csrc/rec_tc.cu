@@ -38,9 +38,9 @@ constexpr int kStages = 6;                      // max h-tile ring depth
 constexpr uint32_t kHTileBytes = 128 * 64 * 2;  // 128 rows x 64 K bf16 = 16 KB
 constexpr uint32_t kSmemMax = 227 * 1024;
 
-// R slice + h ring stages + the (C-1) peers' partials [128 rows][4U] fp32
+// R slice + h ring stages + per batch tile the (C-1) peers' partials [128 rows][4U] bf16
 uint32_t fwd_smem(int C, int U, int Kc, int stages) {
-  const uint32_t recv = C > 1 ? (uint32_t)(C - 1) * 128 * 4 * U * 4 : 0;
+  const uint32_t recv = C > 1 ? (uint32_t)2 * (C - 1) * 128 * 4 * U * 2 : 0;
   return (uint32_t)4 * C * U * Kc * 2 + stages * kHTileBytes * 2 + recv + 1024;
 }
 
@@ -55,11 +55,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   constexpr int kEpiTile = 128 * SPLIT;
   constexpr uint32_t kTmemCols = (MT * N <= 32) ? 32 : (MT * N <= 64) ? 64 : (MT * N <= 128) ? 128
                                  : (MT * N <= 256) ? 256 : 512;
-  constexpr int RS = 4 * U;   // recv row stride (floats): 4 gates x U units
+  constexpr int RS = 4 * U;   // recv row stride (bf16): 4 gates x U units
+  constexpr uint32_t kRecvBytes = (uint32_t)(C - 1) * 128 * RS * 2;  // per tile and step
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar[MT], tempty_bar[MT];
-  __shared__ __align__(8) uint64_t recv_full, free_bar[C];
+  __shared__ __align__(8) uint64_t recv_full[MT], free_bar[MT][C];
   __shared__ uint32_t tmem_sh;
   __shared__ int tmax_sh;
 
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   uint8_t* sR = smem;
   uint8_t* sH = smem + r_bytes;
   const uint32_t stage_bytes = kHTileBytes * a.kb;  // a.kb 64-wide K chunks per TMA box
-  float* recv = reinterpret_cast<float*>(sH + a.stages * stage_bytes);  // [C-1][128][RS]
+  // [MT][C-1][128][RS] bf16: one buffer per batch tile so the tiles stay independent
+  __nv_bfloat16* recv = reinterpret_cast<__nv_bfloat16*>(sH + a.stages * stage_bytes);
   const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
@@ -94,9 +96,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::mbar_init(&tfull_bar[m], 1);
       tc::mbar_init(&tempty_bar[m], kEpiTile);
     }
-    tc::mbar_init(&recv_full, (C - 1) * kEpiTile);
-    for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[p], kEpiTile);
+    for (int m = 0; m < MT; ++m) {
+      tc::mbar_init(&recv_full[m], 1);  // armed once per step; the peers' st.async complete it
+      for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[m][p], kEpiTile);
+    }
     tc::fence_barrier_init();
+    if (C > 1)
+      for (int m = 0; m < MT; ++m) tc::mbar_arrive_expect_tx(&recv_full[m], kRecvBytes);
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
   tc::fence_before_sync();
@@ -210,16 +216,16 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     for (int u = 0; u < UT; ++u) cst[u] = hst[u] = 0.f;
 
     for (int s = 0; s < Tmax; ++s) {
-      const int use = s * MT + mt;  // index of this tile's use of the exchange buffer
+      const int use = s;  // this tile's exchange buffer is used once per step
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
-      float xv[4 * UT];
+      Bf16Vec<UT> xv[4];
       if (active) {  // prefetch (before the MMA wait): hoisted input projection x W + b of this step (K1 output)
         const __nv_bfloat16* xr = xw + pos * a.xw_ld + ut0;
-        const bool vec = nu == UT && (H % 8) == 0 && (a.xw_ld % 8) == 0;
+        const bool vec = (H % 8) == 0 && (a.xw_ld % 8) == 0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) load_bf16<UT>(xr + g * H, xv + g * UT, nu, vec);
+        for (int g = 0; g < 4; ++g) xv[g].load(xr + g * H, nu, vec);
       }
       float z[4 * UT];
       const bool tr0 = a.trace && blockIdx.x == a.trace_cta && e == 0 && lane == 0;
@@ -231,21 +237,30 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 #pragma unroll 1
         for (int pi = 1; pi < C; ++pi) {
           const int p = (r + pi) % C;
-          if (use > 0) mbar_wait_cluster(&free_bar[p], (use - 1) & 1);
+          if (use > 0) mbar_wait_cluster(&free_bar[mt][p], (use - 1) & 1);
           const int slot_at_p = (r - p + C) % C - 1;  // my slot in p's buffer
           const uint32_t dst =
-              mapa(tc::smem_u32(recv + ((size_t)slot_at_p * 128 + rl) * RS + lo), p);
+              mapa(tc::smem_u32(recv + (((size_t)mt * (C - 1) + slot_at_p) * 128 + rl) * RS + lo), p);
+          const uint32_t rbar = mapa(tc::smem_u32(&recv_full[mt]), p);
+          static_assert(UT % 4 == 0, "partial sends move 4 or 8 bf16 per store");
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             float v[UT];
             tmem_ld_cols<UT>(tbase + g * UC + p * U + lo, v);
-            st_cluster_vec<UT>(dst + g * U * 4, v);
+            Bf16Vec<UT> w;
+            w.pack(v);
+            const uint32_t dg = dst + g * U * 2;
+            if constexpr (UT % 8 == 0) {
+#pragma unroll
+              for (int u = 0; u < UT; u += 8)
+                st_async_v4(dg + u * 2, make_uint4(w.w[u / 2], w.w[u / 2 + 1], w.w[u / 2 + 2], w.w[u / 2 + 3]),
+                            rbar);
+            } else {
+#pragma unroll
+              for (int u = 0; u < UT; u += 4) st_async_v2(dg + u * 2, make_uint2(w.w[u / 2], w.w[u / 2 + 1]), rbar);
+            }
           }
         }
-        __syncwarp();
-        if (lane == 0)
-          for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full), (r + pi) % C), 32);
       }
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -258,40 +273,35 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
       if constexpr (C > 1) {
-        mbar_wait_cluster(&recv_full, use & 1);
+        mbar_wait_cluster(&recv_full[mt], use & 1);
+        if ((e % (4 * SPLIT)) == 0 && lane == 0)  // step `use` is complete: arm the next one
+          tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
         if (tr0) a.trace[s * 16 + 10] = gtimer();
 #pragma unroll 1
         for (int pi = 0; pi < C - 1; ++pi) {
-          const float4* src = reinterpret_cast<const float4*>(recv + ((size_t)pi * 128 + rl) * RS + lo);
+          const __nv_bfloat16* src = recv + (((size_t)mt * (C - 1) + pi) * 128 + rl) * RS + lo;
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
+          for (int g = 0; g < 4; ++g) {
+            Bf16Vec<UT> v;
+            v.load_shared(src + g * U);
 #pragma unroll
-            for (int u = 0; u < UT; u += 4) {
-              const float4 v = src[(g * U + u) / 4];
-              z[g * UT + u] += v.x;
-              z[g * UT + u + 1] += v.y;
-              z[g * UT + u + 2] += v.z;
-              z[g * UT + u + 3] += v.w;
-            }
+            for (int u = 0; u < UT; ++u) z[g * UT + u] += v[u];
+          }
         }
         __syncwarp();
         if (lane == 0)  // every sender's slot in my buffer is free again
           for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[r]), (r + pi) % C), 32);
+            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
       }
 
       if (valid_row && !(a.debug_flags & 2)) {
         if (active) {
-          if (save) {  // c_{s-1}, h_{s-1} before the update
-            store_bf16<UT>(a.cprev[d] + pos * H + ut0, cst, nu);
-            store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, hst, nu);
-          }
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
-            const float gi = tc::sigmoid_approx(z[u] + xv[u]);
-            const float gf = tc::sigmoid_approx(z[UT + u] + xv[UT + u]);
-            const float gg = tc::tanh_approx(z[2 * UT + u] + xv[2 * UT + u]);
-            const float go = tc::sigmoid_approx(z[3 * UT + u] + xv[3 * UT + u]);
+            const float gi = tc::sigmoid_approx(z[u] + xv[0][u]);
+            const float gf = tc::sigmoid_approx(z[UT + u] + xv[1][u]);
+            const float gg = tc::tanh_approx(z[2 * UT + u] + xv[2][u]);
+            const float go = tc::sigmoid_approx(z[3 * UT + u] + xv[3][u]);
             z[u] = gi;
             z[UT + u] = gf;
             z[2 * UT + u] = gg;
@@ -315,12 +325,26 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       if (valid_row && !(a.debug_flags & 2)) {
         if (active) {
           if (save) {
-            __nv_bfloat16* gsave = a.gates[d] + pos * 4 * H + ut0;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) store_bf16<UT>(gsave + g * H, z + g * UT, nu);
+            for (int g = 0; g < 4; ++g)
+              store_bf16<UT>(a.gates[d] + gate_save_off(s, g, row, a.B, H, ut0), z + g * UT, nu);
           }
           if (a.y) store_f32<UT>(a.y + pos * a.y_ld + (size_t)d * H + ut0, hst, nu);
           if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, hst, nu);
+          if (save) {  // saved (c, h)_{prev}: zeros at step 0, (c_s, h_s) at step s + 1's position
+            if (s == 0) {
+              float zero[UT];
+#pragma unroll
+              for (int u = 0; u < UT; ++u) zero[u] = 0.f;
+              store_bf16<UT>(a.cprev[d] + cprev_save_off(0, row, a.B, H, ut0), zero, nu);
+              store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
+            }
+            if (s + 1 < len) {
+              const size_t pn = (size_t)row * T + src_time(s + 1, len, dir);
+              store_bf16<UT>(a.cprev[d] + cprev_save_off(s + 1, row, a.B, H, ut0), cst, nu);
+              store_bf16<UT>(a.hprev[d] + pn * a.hprev_ld + ut0, hst, nu);
+            }
+          }
         } else {  // padded position t == s: zero output (tape.cpp:797), frozen state
           float zero[UT];
 #pragma unroll
@@ -342,7 +366,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         if (a.ybf) store_bf16<UT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
         if (save) store_bf16<UT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
       }
-      for (int u = 0; u < nu; ++u) {
+#pragma unroll
+      for (int u = 0; u < UT; ++u) {
+        if (u >= nu) continue;
         if (a.h_last) a.h_last[((size_t)d * a.B + row) * H + ut0 + u] = hst[u];
         if (a.c_last) a.c_last[((size_t)d * a.B + row) * H + ut0 + u] = cst[u];
       }
@@ -354,21 +380,36 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 }
 
 // RT[(cl*C + r)*N + g*UC + j][kk] = R[r*Kc + kk][g*H + cl*UC + j]  (bf16, zero outside)
+// A 32x32 shared-memory transpose: coalesced reads along R's gate columns,
+// coalesced writes along RT's K; grid = (ceil(P*N/32), ceil(Kp/32)) tiles over
+// (packed row, k), 32-bit index math only.
 __global__ void pack_rt_kernel(const float* __restrict__ R, int H, int C, int U, int P, int Kc,
                                __nv_bfloat16* __restrict__ RT) {
+  __shared__ float tile[32][33];
   const int UC = C * U, N = 4 * UC;
-  const int64_t n_el = (int64_t)P * N * Kc;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int kk = (int)(e % Kc);
-    const int rowi = (int)(e / Kc);
-    const int cta = rowi / N, j = rowi % N;
-    const int cl = cta / C, r = cta % C;
-    const int g = j / UC, unit = cl * UC + j % UC;
-    const int k = r * Kc + kk;
+  const int Kp = Kc * C;
+  const int row0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
+  // read: rows (packed) x k from R[k][col(row)], threads along the packed row
+  for (int i = ty; i < 32; i += 8) {
+    const int k = k0 + i, rowi = row0 + tx;
     float v = 0.f;
-    if (unit < H && k < H) v = R[(int64_t)k * 4 * H + (int64_t)g * H + unit];
-    RT[e] = __float2bfloat16_rn(v);
+    if (rowi < P * N && k < H) {
+      const int cta = rowi / N, j = rowi % N;
+      const int cl = cta / C, r = cta % C;
+      const int g = j / UC, unit = cl * UC + j % UC;
+      if (unit < H && k / Kc == r) v = R[(size_t)k * 4 * H + (size_t)g * H + unit];
+    }
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  // write: RT[rowi][kk] with kk along threads; the CTA's K-slice is r
+  for (int i = ty; i < 32; i += 8) {
+    const int rowi = row0 + i, k = k0 + tx;
+    if (rowi >= P * N || k >= Kp) continue;
+    const int r = (rowi / N) % C;
+    if (k / Kc != r) continue;
+    RT[(size_t)rowi * Kc + (k - r * Kc)] = __float2bfloat16_rn(tile[tx][i]);
   }
 }
 
@@ -416,6 +457,13 @@ TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms) {
   // opt-in (SL_FWD_CLUSTER=1) until that exchange beats the single-CTA form.
   const char* env = getenv("SL_FWD_CLUSTER");
   const bool cluster = env && env[0] == '1';
+  // CTA-pair kernel (M = 256 x N = 128 MMAs, 32 units per pair) unless disabled
+  const char* penv = getenv("SL_FWD_PAIR");
+  if (!(penv && penv[0] == '0') && !cluster && tc_rec_fwd_pair_fits(H, nd, sms)) {
+    TcFwdShape sh{1, 32, (int)ceil_div(H, 32), (int)round_up(H, 64)};
+    sh.pair = 1;
+    return sh;
+  }
   for (int C : {2, 1})
     for (int U : {16, 8, 4}) {
       const int P = (int)ceil_div(H, (int64_t)C * U) * C;
@@ -436,15 +484,18 @@ size_t tc_rec_pack_elems(const TcFwdShape& sh) {
 void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
                  cudaStream_t stream) {
   const int Kc = sh.Kp / sh.C;
-  const int64_t n = (int64_t)sh.P * 4 * sh.C * sh.U * Kc;
-  pack_rt_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, stream>>>(
-      R, H, sh.C, sh.U, sh.P, Kc, RT);
+  const dim3 grid((unsigned)ceil_div((int64_t)sh.P * 4 * sh.C * sh.U, 32), (unsigned)ceil_div(sh.Kp, 32));
+  pack_rt_kernel<<<grid, 256, 0, stream>>>(R, H, sh.C, sh.U, sh.P, Kc, RT);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
 
 void rec_fwd_tc(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                 cudaStream_t stream) {
+  if (sh.pair) {
+    rec_fwd_pair(a0, sh, RT, stream);
+    return;
+  }
   TcRecFwdArgs a = a0;
   a.U = sh.U;
   a.P = sh.P;

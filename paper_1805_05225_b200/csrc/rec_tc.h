@@ -4,6 +4,23 @@
 
 namespace sl {
 
+// Saved activations of the bf16 path (written by K2, read only by K3), laid
+// out step-major and batch-row-interleaved in 16-unit chunks:
+//   gates (i,f,g,o)  [T][4][NC][B][16],   c_{s-1}  [T][NC][B][16],
+// NC = ceil(H / 16), indexed by processing step s (not by time: the reversed
+// direction and ragged lengths map steps to times per row).  The epilogue
+// threads of both kernels own one batch row each (TMEM lane = row), so a warp
+// touching a 16-unit chunk of 32 consecutive rows hits 1 KB of contiguous
+// memory instead of 32 rows 8 KB apart.  A thread's unit slice must not cross
+// a 16-unit chunk.
+__host__ __device__ inline int save_hq(int H) { return (H + 15) / 16 * 16; }
+__host__ __device__ inline size_t gate_save_off(int s, int g, int row, int B, int H, int u) {
+  return ((((size_t)s * 4 + g) * (save_hq(H) / 16) + u / 16) * B + row) * 16 + u % 16;
+}
+__host__ __device__ inline size_t cprev_save_off(int s, int row, int B, int H, int u) {
+  return (((size_t)s * (save_hq(H) / 16) + u / 16) * B + row) * 16 + u % 16;
+}
+
 struct TcRecFwdArgs {
   int B, T, H, nd, U, P;  // P = CTAs per direction (= ceil(H / U))
   int b0;                 // first batch row of this launch (set internally)
@@ -20,15 +37,16 @@ struct TcRecFwdArgs {
   int64_t ybf_ld;
   float* h_last;  // [nd, B, H] or null
   float* c_last;
-  __nv_bfloat16* gates[2];    // saved (i,f,g,o) bf16 [B*T, 4H] (null = inference)
-  __nv_bfloat16* cprev[2];    // saved c_{s-1} bf16 [B*T, H]
+  __nv_bfloat16* gates[2];    // saved (i,f,g,o), step-major (gate_save_off; null = inference)
+  __nv_bfloat16* cprev[2];    // saved c_{s-1}, step-major (cprev_save_off)
   __nv_bfloat16* hprev[2];    // saved h_{s-1} bf16 [B*T, hprev_ld] (dR GEMM operand)
   int64_t hprev_ld;
   __nv_bfloat16* hbuf[2];     // ring [2][B][Kp] bf16, zeroed (tc_rec_hbuf_elems)
   unsigned* bar;              // zeroed step counters, 2 per batch chunk
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;
-  int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores (wrong results)
+  int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores,
+                    // 4 = no step-counter waits (wrong results)
 };
 
 struct TcRecBwdArgs {
@@ -39,8 +57,8 @@ struct TcRecBwdArgs {
   int kb;      // 64-wide K chunks per TMA box (set internally)
   const int32_t* lens;
   int dirsign[2];
-  const __nv_bfloat16* gates[2];  // saved by K2: (i,f,g,o) bf16 [B*T, 4H]
-  const __nv_bfloat16* cprev[2];  // saved by K2: c_{s-1} bf16 [B*T, H]
+  const __nv_bfloat16* gates[2];  // saved by K2: (i,f,g,o), step-major (gate_save_off)
+  const __nv_bfloat16* cprev[2];  // saved by K2: c_{s-1}, step-major (cprev_save_off)
   const float* dy;        // [B*T, dy_ld], dir d at col d*H
   int64_t dy_ld;
   const float* dh_last;  // [nd, B, H] or null
@@ -70,6 +88,7 @@ void rec_bwd_tc(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* cons
 // Kp = H padded to 64*C.
 struct TcFwdShape {
   int C, U, P, Kp;
+  int pair = 0;  // 1: CTA-pair kernel (rec_tc_pair.cu): U = units per pair, P = pairs per direction
 };
 TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms);  // C == 0: unsupported
 size_t tc_rec_hbuf_elems(int B, const TcFwdShape& sh);  // one direction's h ring
@@ -79,5 +98,8 @@ void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
                  cudaStream_t stream);
 void rec_fwd_tc(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                 cudaStream_t stream);
+bool tc_rec_fwd_pair_fits(int H, int nd, int sms);
+void rec_fwd_pair(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
+                  cudaStream_t stream);
 
 }  // namespace sl

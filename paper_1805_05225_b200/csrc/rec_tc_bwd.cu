@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                       const __grid_constant__ CUtensorMap tmZ1, TcRecBwdArgs a) {
   constexpr int NB = nb_of(C, U);  // MMA N: the cluster's units
   constexpr int kEpiTile = 128 * SPLIT;
+  constexpr uint32_t kRecvBytes = (uint32_t)(C - 1) * 128 * U * 2;  // per tile and use
   constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : (MT * NB <= 64) ? 64 : (MT * NB <= 128) ? 128 : 256;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
@@ -92,10 +93,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::mbar_init(&tempty_bar[m], kEpiTile);
     }
     for (int m = 0; m < MT; ++m) {
-      tc::mbar_init(&recv_full[m], (C - 1) * kEpiTile);
+      // one arming arrive per use; the peers' st.async stores complete the bytes
+      tc::mbar_init(&recv_full[m], 1);
       for (int p = 0; p < C; ++p) tc::mbar_init(&free_bar[m][p], kEpiTile);
     }
     tc::fence_barrier_init();
+    if (C > 1)
+      for (int m = 0; m < MT; ++m) tc::mbar_arrive_expect_tx(&recv_full[m], kRecvBytes);
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(&tmem_sh);
   tc::fence_before_sync();
@@ -210,13 +214,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
-      float gv[4 * UT], cp[UT], dyv[UT];
+      Bf16Vec<UT> gv[4], cp;
+      float dyv[UT];
       if (active) {  // prefetch this step's saved activations and upstream grad
         const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
-        const bool vecb = nu == UT && (H % 8) == 0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) load_bf16<UT>(gates + pos * 4 * H + g * H + ut0, gv + g * UT, nu, vecb);
-        load_bf16<UT>(cprev + pos * H + ut0, cp, nu, vecb);
+        for (int g = 0; g < 4; ++g) gv[g].load(gates + gate_save_off(s, g, row, a.B, H, ut0), nu, true);
+        cp.load(cprev + cprev_save_off(s, row, a.B, H, ut0), nu, true);
         load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)d * H + ut0, dyv, nu,
                      vec && (a.dy_ld % 4) == 0);
       }
@@ -241,36 +245,32 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           const int slot_at_p = (r - p + C) % C - 1;  // my slot in p's buffer
           const uint32_t dst = mapa(
               tc::smem_u32(recv + (((size_t)mt * (C - 1) + slot_at_p) * 128 + rl) * U + lo), p);
+          const uint32_t rbar = mapa(tc::smem_u32(&recv_full[mt]), p);
+          static_assert(UT % 4 == 0, "DSMEM partial sends move 4 or 8 bf16 per store");
+          Bf16Vec<UT> w;
+          w.pack(v);
+          // st.async: each store completes its bytes on p's receive barrier, so
+          // no release fence (which would wait for this thread's pending global
+          // stores) sits on the exchange path
           if constexpr (UT % 8 == 0) {
 #pragma unroll
-            for (int u = 0; u < UT; u += 8) {  // 8 bf16 = one 16 B DSMEM store
-              const uint4 w = pack8_bf16(v + u);
-              asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + u * 2),
-                           "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
-                           : "memory");
-            }
+            for (int u = 0; u < UT; u += 8)
+              st_async_v4(dst + u * 2, make_uint4(w.w[u / 2], w.w[u / 2 + 1], w.w[u / 2 + 2], w.w[u / 2 + 3]),
+                          rbar);
           } else {
 #pragma unroll
-            for (int u = 0; u < UT; ++u) {
-              const __nv_bfloat16 hv = __float2bfloat16_rn(v[u]);
-              asm volatile("st.shared::cluster.b16 [%0], %1;" ::"r"(dst + u * 2),
-                           "h"(*reinterpret_cast<const unsigned short*>(&hv))
-                           : "memory");
-            }
+            for (int u = 0; u < UT; u += 4) st_async_v2(dst + u * 2, make_uint2(w.w[u / 2], w.w[u / 2 + 1]), rbar);
           }
         }
-        __syncwarp();
-        if (lane == 0)
-          for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&recv_full[mt]), (r + pi) % C), 32);
       }
       if (tr0) a.trace[it * 16 + 9] = gtimer();
       tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
       if constexpr (C > 1) {
-        if (lane == 0) mbar_wait_cluster(&recv_full[mt], use & 1);
-        __syncwarp();
+        mbar_wait_cluster(&recv_full[mt], use & 1);
+        if ((e % (4 * SPLIT)) == 0 && lane == 0)  // phase `use` is complete: arm the next use
+          tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
         if (tr0) a.trace[it * 16 + 10] = gtimer();
 #pragma unroll 1
         for (int sl = 0; sl < C - 1; ++sl) {
@@ -291,13 +291,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         __syncwarp();
         if (lane == 0)  // tell every sender its slot in my buffer is free again
           for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
+            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
       }
 
+      Bf16Vec<UT> dzp[4];  // DZ_s packed: the ring copy now, the K4 copy after publishing
       if (valid_row) {
         __nv_bfloat16* zn = zr + ((size_t)((it + 1) & 1) * a.B + row) * a.Kz + ut0;
-        float* dz = gv;  // DZ overwrites the gate values in place (unit by unit)
         if (active) {
+          float dz[4 * UT];
           const bool last = (s == len - 1);
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
@@ -305,22 +306,25 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             float gc = gcar[u];
             if (last && a.dh_last) gh += a.dh_last[((size_t)d * a.B + row) * H + ut0 + u];
             if (last && a.dc_last) gc += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
-            const float gi = gv[u], gf = gv[UT + u], gg = gv[2 * UT + u], go = gv[3 * UT + u];
-            const float tcv = tc::tanh_approx(fmaf(gf, cp[u], gi * gg));
+            const float gi = gv[0][u], gf = gv[1][u], gg = gv[2][u], go = gv[3][u];
+            const float cpu = cp[u];
+            const float tcv = tc::tanh_approx(fmaf(gf, cpu, gi * gg));
             const float d_o = gh * tcv;                          // tape.cpp:1161
             const float dcn = gc + gh * go * (1.f - tcv * tcv);  // tape.cpp:1162
             gcar[u] = dcn * gf;                                  // tape.cpp:1166
             dz[u] = dcn * gg * gi * (1.f - gi);                  // tape.cpp:1167
-            dz[UT + u] = dcn * cp[u] * gf * (1.f - gf);          // tape.cpp:1168
+            dz[UT + u] = dcn * cpu * gf * (1.f - gf);            // tape.cpp:1168
             dz[2 * UT + u] = dcn * gi * (1.f - gg * gg);         // tape.cpp:1169
             dz[3 * UT + u] = d_o * go * (1.f - go);              // tape.cpp:1170
           }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) dzp[g].pack(dz + g * UT);
         } else {
 #pragma unroll
-          for (int j = 0; j < 4 * UT; ++j) dz[j] = 0.f;
+          for (int g = 0; g < 4; ++g) dzp[g].zero();
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) store_bf16<UT>(zn + g * H, dz + g * UT, nu);
+        for (int g = 0; g < 4; ++g) dzp[g].store(zn + g * H, nu);
       }
       if (tr0) a.trace[it * 16 + 11] = gtimer();
       named_sync(1 + mt, kEpiTile);
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
         __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) store_bf16<UT>(zc + g * H, gv + g * UT, nu);
+        for (int g = 0; g < 4; ++g) dzp[g].store(zc + g * H, nu);
       }
     }
     if (valid_row) {  // DZ rows of positions beyond the longest sequence
@@ -353,20 +357,19 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 }
 
 // RB[(cl*C + r)*NB + n][kk] = R[cl*C*U + n][r*Kc + kk]  (bf16; zero outside the layer)
+// One CTA per packed row; threads along kk (coalesced on both sides), 32-bit math.
 __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U, int NB, int P,
                                int Kc, __nv_bfloat16* __restrict__ RB) {
-  const int64_t n_el = (int64_t)P * NB * Kc;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int kk = (int)(e % Kc);
-    const int rowi = (int)(e / Kc);
-    const int cta = rowi / NB, n = rowi % NB;
-    const int cl = cta / C, r = cta % C;
-    const int unit = cl * C * U + n;
-    const int j = r * Kc + kk;
-    float v = 0.f;
-    if (n < C * U && unit < H && j < 4 * H) v = R[(int64_t)unit * 4 * H + j];
-    RB[e] = __float2bfloat16_rn(v);
+  const int rowi = blockIdx.x;
+  const int cta = rowi / NB, n = rowi % NB;
+  const int cl = cta / C, r = cta % C;
+  const int unit = cl * C * U + n;
+  const bool live = n < C * U && unit < H;
+  const float* src = R + (size_t)unit * 4 * H + (size_t)r * Kc;
+  __nv_bfloat16* dst = RB + (size_t)rowi * Kc;
+  for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
+    const float v = (live && r * Kc + kk < 4 * H) ? __ldg(src + kk) : 0.f;
+    dst[kk] = __float2bfloat16_rn(v);
   }
 }
 
@@ -431,9 +434,7 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
                      cudaStream_t stream) {
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  const int64_t n = (int64_t)sh.P * NB * Kc;
-  pack_rb_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, stream>>>(
-      R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  pack_rb_kernel<<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }

@@ -73,63 +73,119 @@ __device__ __forceinline__ void unpack8_bf16(uint4 w, float* v) {
   }
 }
 
+// 256-bit global accesses (sm_100: one request per 32 B; the recurrence
+// epilogues are request-rate bound, not byte bound)
+__device__ __forceinline__ void st256(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+__device__ __forceinline__ void ld256_nc(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256(const void* p, uint4& a, uint4& b) {  // coherent (data of this kernel)
+  asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p)
+               : "memory");
+}
+
+// Row-segment loads / stores of a thread's unit slice [0, nu) of U values.
+// Granule cascade: 32 B accesses where aligned, then 16 B, 8 B, scalar for the
+// ragged remainder — a partial slice (the last CTA of a layer whose H is not a
+// multiple of the slice) must stay on wide accesses or it straggles every
+// step.  All register indexing is static (no local-memory arrays).
+__device__ __forceinline__ bool aligned_to(const void* p, int bytes) {
+  return ((uintptr_t)p & (uintptr_t)(bytes - 1)) == 0;
+}
+
 template <int U>
 __device__ __forceinline__ void store_f32(float* dst, const float* v, int nu) {
   int done = 0;
-  if ((U % 4) == 0 && ((uintptr_t)dst & 15) == 0) {
+  if constexpr (U % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 8)
+      if (i == done && i + 8 <= nu && aligned_to(dst + i, 32)) {
+        st256(dst + i, make_uint4(__float_as_uint(v[i]), __float_as_uint(v[i + 1]), __float_as_uint(v[i + 2]),
+                                  __float_as_uint(v[i + 3])),
+              make_uint4(__float_as_uint(v[i + 4]), __float_as_uint(v[i + 5]), __float_as_uint(v[i + 6]),
+                         __float_as_uint(v[i + 7])));
+        done = i + 8;
+      }
+  }
+  if constexpr (U % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < U; i += 4)
-      if (i + 4 <= nu) {
+      if (i == done && i + 4 <= nu && aligned_to(dst + i, 16)) {
         *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         done = i + 4;
       }
   }
-  for (int i = done; i < nu; ++i) dst[i] = v[i];
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    if (i >= done && i < nu) dst[i] = v[i];
 }
+
 template <int U>
 __device__ __forceinline__ void store_bf16(__nv_bfloat16* dst, const float* v, int nu) {
   int done = 0;
-  if ((U % 8) == 0 && ((uintptr_t)dst & 15) == 0) {
+  if constexpr (U % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < U; i += 16)
+      if (i == done && i + 16 <= nu && aligned_to(dst + i, 32)) {
+        st256(dst + i, pack8_bf16(v + i), pack8_bf16(v + i + 8));
+        done = i + 16;
+      }
+  }
+  if constexpr (U % 8 == 0) {
 #pragma unroll
     for (int i = 0; i < U; i += 8)
-      if (i + 8 <= nu) {
+      if (i == done && i + 8 <= nu && aligned_to(dst + i, 16)) {
         *reinterpret_cast<uint4*>(dst + i) = pack8_bf16(v + i);
         done = i + 8;
       }
-  } else if ((U % 4) == 0 && ((uintptr_t)dst & 7) == 0) {
+  }
+  if constexpr (U % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < U; i += 4)
-      if (i + 4 <= nu) {
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-        uint2 w;
-        w.x = *reinterpret_cast<uint32_t*>(&p0);
-        w.y = *reinterpret_cast<uint32_t*>(&p1);
-        *reinterpret_cast<uint2*>(dst + i) = w;
+      if (i == done && i + 4 <= nu && aligned_to(dst + i, 8)) {
+        const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+        const __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+        *reinterpret_cast<uint2*>(dst + i) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
         done = i + 4;
       }
   }
-  for (int i = done; i < nu; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    if (i >= done && i < nu) dst[i] = __float2bfloat16_rn(v[i]);
 }
 
+// zero-filled beyond nu; vec = the row pitch allows vector access at all
 template <int U>
 __device__ __forceinline__ void load_f32(const float* src, float* v, int nu, bool vec) {
 #pragma unroll
   for (int i = 0; i < U; ++i) v[i] = 0.f;
   int done = 0;
-  if (vec && (U % 4) == 0 && ((uintptr_t)src & 15) == 0) {
+  if constexpr (U % 4 == 0) {
+    if (vec) {
 #pragma unroll
-    for (int i = 0; i < U; i += 4)
-      if (i + 4 <= nu) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
-        v[i] = x.x;
-        v[i + 1] = x.y;
-        v[i + 2] = x.z;
-        v[i + 3] = x.w;
-        done = i + 4;
-      }
+      for (int i = 0; i < U; i += 4)
+        if (i == done && i + 4 <= nu && aligned_to(src + i, 16)) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
+          v[i] = x.x;
+          v[i + 1] = x.y;
+          v[i + 2] = x.z;
+          v[i + 3] = x.w;
+          done = i + 4;
+        }
+    }
   }
-  for (int i = done; i < nu; ++i) v[i] = __ldg(src + i);
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    if (i >= done && i < nu) v[i] = __ldg(src + i);
 }
 
 template <int U>
@@ -137,16 +193,141 @@ __device__ __forceinline__ void load_bf16(const __nv_bfloat16* src, float* v, in
 #pragma unroll
   for (int i = 0; i < U; ++i) v[i] = 0.f;
   int done = 0;
-  if (vec && (U % 8) == 0 && ((uintptr_t)src & 15) == 0) {
+  if constexpr (U % 8 == 0) {
+    if (vec) {
 #pragma unroll
-    for (int i = 0; i < U; i += 8)
-      if (i + 8 <= nu) {
-        unpack8_bf16(__ldg(reinterpret_cast<const uint4*>(src + i)), v + i);
-        done = i + 8;
-      }
+      for (int i = 0; i < U; i += 8)
+        if (i == done && i + 8 <= nu && aligned_to(src + i, 16)) {
+          unpack8_bf16(__ldg(reinterpret_cast<const uint4*>(src + i)), v + i);
+          done = i + 8;
+        }
+    }
   }
-  for (int i = done; i < nu; ++i) v[i] = __bfloat162float(src[i]);
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    if (i >= done && i < nu) v[i] = __bfloat162float(src[i]);
 }
+
+// U bf16 values kept packed in registers (U/2 words): halves the register
+// cost of operands prefetched a whole step ahead.  All indexing is static.
+template <int U>
+struct Bf16Vec {
+  static_assert(U % 4 == 0, "Bf16Vec: multiple of 4");
+  uint32_t w[U / 2];
+  __device__ __forceinline__ float operator[](int i) const {
+    const uint32_t x = w[i / 2];
+    return __uint_as_float((i & 1) ? (x & 0xffff0000u) : (x << 16));
+  }
+  __device__ __forceinline__ void pack(const float* v) {
+#pragma unroll
+    for (int i = 0; i < U; i += 2) {
+      const __nv_bfloat162 p = __floats2bfloat162_rn(v[i], v[i + 1]);
+      w[i / 2] = *reinterpret_cast<const uint32_t*>(&p);
+    }
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < U / 2; ++i) w[i] = 0u;
+  }
+  __device__ __forceinline__ void store(__nv_bfloat16* dst, int nu) const {
+    int done = 0;
+    if constexpr (U % 16 == 0) {
+#pragma unroll
+      for (int i = 0; i < U; i += 16)
+        if (i == done && i + 16 <= nu && aligned_to(dst + i, 32)) {
+          st256(dst + i, make_uint4(w[i / 2], w[i / 2 + 1], w[i / 2 + 2], w[i / 2 + 3]),
+                make_uint4(w[i / 2 + 4], w[i / 2 + 5], w[i / 2 + 6], w[i / 2 + 7]));
+          done = i + 16;
+        }
+    }
+    if constexpr (U % 8 == 0) {
+#pragma unroll
+      for (int i = 0; i < U; i += 8)
+        if (i == done && i + 8 <= nu && aligned_to(dst + i, 16)) {
+          *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[i / 2], w[i / 2 + 1], w[i / 2 + 2], w[i / 2 + 3]);
+          done = i + 8;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < U; i += 4)
+      if (i == done && i + 4 <= nu && aligned_to(dst + i, 8)) {
+        *reinterpret_cast<uint2*>(dst + i) = make_uint2(w[i / 2], w[i / 2 + 1]);
+        done = i + 4;
+      }
+    unsigned short* d16 = reinterpret_cast<unsigned short*>(dst);
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+      if (i >= done && i < nu) d16[i] = (unsigned short)((i & 1) ? (w[i / 2] >> 16) : (w[i / 2] & 0xffffu));
+  }
+  // full slice from shared memory (generic loads; 8 B / 16 B aligned)
+  __device__ __forceinline__ void load_shared(const __nv_bfloat16* src) {
+    if constexpr (U % 8 == 0) {
+#pragma unroll
+      for (int i = 0; i < U; i += 8) {
+        const uint4 q = *reinterpret_cast<const uint4*>(src + i);
+        w[i / 2] = q.x;
+        w[i / 2 + 1] = q.y;
+        w[i / 2 + 2] = q.z;
+        w[i / 2 + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < U; i += 4) {
+        const uint2 q = *reinterpret_cast<const uint2*>(src + i);
+        w[i / 2] = q.x;
+        w[i / 2 + 1] = q.y;
+      }
+    }
+  }
+  // zero-filled beyond nu; vec = the row pitch allows vector access at all
+  __device__ __forceinline__ void load(const __nv_bfloat16* src, int nu, bool vec) {
+    zero();
+    int done = 0;
+    if (vec) {
+      if constexpr (U % 16 == 0) {
+#pragma unroll
+        for (int i = 0; i < U; i += 16)
+          if (i == done && i + 16 <= nu && aligned_to(src + i, 32)) {
+            uint4 q0, q1;
+            ld256_nc(src + i, q0, q1);
+            w[i / 2] = q0.x;
+            w[i / 2 + 1] = q0.y;
+            w[i / 2 + 2] = q0.z;
+            w[i / 2 + 3] = q0.w;
+            w[i / 2 + 4] = q1.x;
+            w[i / 2 + 5] = q1.y;
+            w[i / 2 + 6] = q1.z;
+            w[i / 2 + 7] = q1.w;
+            done = i + 16;
+          }
+      }
+      if constexpr (U % 8 == 0) {
+#pragma unroll
+        for (int i = 0; i < U; i += 8)
+          if (i == done && i + 8 <= nu && aligned_to(src + i, 16)) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + i));
+            w[i / 2] = q.x;
+            w[i / 2 + 1] = q.y;
+            w[i / 2 + 2] = q.z;
+            w[i / 2 + 3] = q.w;
+            done = i + 8;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < U; i += 4)
+        if (i == done && i + 4 <= nu && aligned_to(src + i, 8)) {
+          const uint2 q = __ldg(reinterpret_cast<const uint2*>(src + i));
+          w[i / 2] = q.x;
+          w[i / 2 + 1] = q.y;
+          done = i + 4;
+        }
+    }
+    const unsigned short* s16 = reinterpret_cast<const unsigned short*>(src);
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+      if (i >= done && i < nu) w[i / 2] |= (uint32_t)__ldg(s16 + i) << ((i & 1) * 16);
+  }
+};
 
 template <int n>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[n]) {
@@ -231,6 +412,27 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr, uint32
                "r"(count)
                : "memory");
 }
+// relaxed remote arrive: pure signalling (e.g. "I have read the accumulator" /
+// "your slot in my buffer is free"), no wait for this thread's earlier global
+// stores to drain the way a .release arrive must
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr, uint32_t count) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(count)
+               : "memory");
+}
+// DSMEM store that completes `bytes` of transaction count on the DESTINATION
+// CTA's mbarrier (the receiver arms it with expect_tx): no release fence
+__device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar_cl) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   addr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar_cl)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t addr, uint2 v, uint32_t bar_cl) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "r"(v.x), "r"(v.y), "r"(bar_cl)
+               : "memory");
+}
 // wait with cluster-scope acquire (sees DSMEM writes released by peers)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -240,6 +442,58 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "@!p bra WAITC_%=;\n\t}" ::"r"(tc::smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+
+// ---- CTA-pair (cta_group::2) primitives
+// TMA into this CTA's smem whose completion is signalled on the barrier at
+// shared::cluster address `bar_cl` (the pair leader's)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(tc::smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(bar_cl)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl, int c0,
+                                                 int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(tc::smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cl)
+      : "memory");
+}
+// D[tmem] (+)= A . B for the pair: M = 256 (128 rows of A per CTA), N split
+// over the two CTAs' B halves; issued by the leader only
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                             bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)acc)
+      : "memory");
+}
+// arrive once on the barrier at this smem offset in BOTH CTAs of the pair when
+// the issuing thread's prior MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(tc::smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {  // whole warp, both CTAs
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   tc::smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
 }
 
 }  // namespace rtc

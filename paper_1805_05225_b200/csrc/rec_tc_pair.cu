@@ -1,0 +1,384 @@
+// K2, CTA-pair form — persistent tensor-core forward recurrence on the
+// Blackwell CTA-pair datapath (tcgen05 .cta_group::2).
+//
+// Why a pair: the per-step product h_{s-1} [B x H] . R [H x 4H] is a skinny
+// GEMM that must be spread over ~128 SMs, so each SM can only keep a 64-column
+// slice of R (128 KB bf16) resident.  A single-CTA M = 128 x N = 64 MMA runs at
+// half the tensor-core rate (it costs as much as N = 128), and each CTA must
+// stream all B rows of h_{s-1} through its shared memory.  A CTA pair instead
+// issues M = 256 (the two 128-row batch tiles, one per CTA) x N = 128 (both
+// CTAs' R slices) MMAs: full rate, and each CTA streams only its own 128 rows.
+//
+// Pair (leader rank 0, peer rank 1) = 32 hidden units of one direction; CTA r
+// holds R^T rows [r*64, r*64+64) of the pair's 128 gate columns (ordered
+// gate-major: column g*32 + j = gate g of unit j) and finalizes batch tile r
+// (rows b0 + 128 r ...) for all 32 units.  Per step s:
+//   warp 0 (both)   waits on the step counter of ITS batch tile (every pair
+//                   published its units of h_{s-1} for that tile), then
+//                   TMA-streams its 128 rows of h_{s-1} from the L2 ring into
+//                   its own smem, completing on the LEADER's stage barrier;
+//   warp 1 (leader) issues the M=256 x N=128 x K=16 MMAs; commits multicast to
+//                   both CTAs' stage-free and accumulator-full barriers;
+//   warps 2..17     4 threads per batch row x 8 units: tcgen05.ld the row's
+//                   gate pre-activations, add x W + b (K1), sigmoid / tanh,
+//                   update the fp32 cell in registers, write h_s to the ring,
+//                   publish, then write y and the saved activations.
+// Semantics as rec_tc.cu: layers.cpp:27-33, tape.cpp:1103-1135 (step),
+// tape.cpp:797 (mask), tape.cpp:846 (reversal).
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "profile.h"
+#include "rec_tc.h"
+#include "rec_tc_common.cuh"
+
+namespace sl {
+namespace {
+using namespace rtc;
+
+constexpr int kPairUnits = 32;              // hidden units per pair
+constexpr int kN = 4 * kPairUnits;          // MMA N (both CTAs' R slices)
+constexpr int kNHalf = kN / 2;              // R^T rows held per CTA
+constexpr int kSplit = 2;                   // epilogue threads per batch row
+constexpr int kUT = kPairUnits / kSplit;    // units per epilogue thread
+constexpr int kEpi = 128 * kSplit;          // epilogue threads
+constexpr int kThreads = 64 + kEpi;
+constexpr int kMaxStages = 8;
+constexpr uint32_t kChunk = 128 * 64 * 2;   // 128 rows x 64 K bf16
+constexpr uint32_t kSmemMax = 227 * 1024;
+
+uint32_t pair_smem(int Kp, int stages, int kb) {
+  return (uint32_t)kNHalf * Kp * 2 + stages * kChunk * kb + 1024;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    rec_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmR0, const __grid_constant__ CUtensorMap tmR1,
+                        const __grid_constant__ CUtensorMap tmH0, const __grid_constant__ CUtensorMap tmH1,
+                        TcRecFwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t r_bar, tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_sh;
+  __shared__ int tmax_sh;
+
+  const int pr = blockIdx.x / 2;        // pair index over both directions
+  const int d = pr / a.P;               // a.P = pairs per direction
+  const int pair = pr % a.P;
+  const int r = (int)cluster_rank();    // 0 = leader; also the batch tile
+  const bool leader = r == 0;
+  const int u0 = pair * kPairUnits;
+  const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
+  const CUtensorMap* tmH = d == 0 ? &tmH0 : &tmH1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
+  const int nkc = a.Kp / 64;
+  const uint32_t r_bytes = (uint32_t)kNHalf * a.Kp * 2;
+  uint8_t* sR = smem;
+  uint8_t* sH = smem + r_bytes;
+  const uint32_t stage_bytes = kChunk * a.kb;
+
+  if (threadIdx.x == 0) {
+    tmax_sh = 0;
+    tc::prefetch_tmap(tmR);
+    tc::prefetch_tmap(tmH);
+    for (int s = 0; s < a.stages; ++s) {
+      tc::mbar_init(&full_bar[s], 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    tc::mbar_init(&r_bar, 1);
+    tc::mbar_init(&tfull_bar, 1);
+    tc::mbar_init(&tempty_bar, 2 * kEpi);  // both CTAs' epilogue threads (leader's copy used)
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<kN>(&tmem_sh);
+  tc::fence_before_sync();
+  __syncthreads();
+  cluster_sync();
+  tc::fence_after_sync();
+  {
+    int m = 0;
+    for (int i = threadIdx.x; i < a.B; i += blockDim.x) m = max(m, (int)a.lens[i]);
+    atomicMax(&tmax_sh, m);
+  }
+  __syncthreads();
+  const int Tmax = tmax_sh;
+  const uint32_t tmem = tmem_sh;
+  // debug trace: one CTA (trace_cta >= 0) or every CTA (trace_cta < 0, buffer [grid][T][16])
+  const bool trace_on = a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta);
+  unsigned long long* trace = trace_on ? a.trace + (a.trace_cta < 0 ? (size_t)blockIdx.x * a.T * 16 : 0) : nullptr;
+#define TR(k)                                          \
+  do {                                                 \
+    if (trace) trace[s * 16 + (k)] = gtimer();         \
+  } while (0)
+  unsigned* ctr = a.bar + d * 2 + r;  // step counter of (direction, my batch tile)
+  const int ngrp = nkc / a.kb;
+  const int kc_off = pair % ngrp;
+
+  if (warp == 0) {
+    if (lane == 0) {  // -------------------------------------------- producer (both CTAs)
+      const uint32_t r_bar_l = mapa(tc::smem_u32(&r_bar), 0);
+      if (leader) tc::mbar_arrive_expect_tx(&r_bar, 2 * r_bytes);
+      for (int kc = 0; kc < nkc; ++kc)
+        tma_load_2d_pair(sR + (size_t)kc * kNHalf * 128, tmR, r_bar_l, kc * 64, pair * kN + r * kNHalf);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int s = 0; s < Tmax; ++s) {
+        if (s > 0 && !(a.debug_flags & 4)) {
+          const unsigned target = (unsigned)a.P * (unsigned)s;
+          TR(13);
+          unsigned polls = 0;
+          while (ld_acquire(ctr) < target) ++polls;
+          if (trace) trace[s * 16 + 14] = polls;
+          tc::fence_proxy_async_global();
+        }
+        TR(0);
+        for (int kq = 0; kq < ngrp; ++kq) {
+          const int kg = (kq + kc_off) % ngrp;
+          tc::mbar_wait(&empty_bar[st], ph ^ 1);
+          if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
+          tma_load_4d_pair(sH + st * stage_bytes, tmH, mapa(tc::smem_u32(&full_bar[st]), 0), 0,
+                           a.b0 + r * 128, kg * a.kb, s & 1);
+          if (++st == a.stages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ------------------------------------ MMA issuer (leader)
+      constexpr uint32_t idesc = tc::make_idesc(256, kN, 1, false, false);
+      tc::mbar_wait(&r_bar, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int s = 0; s < Tmax; ++s) {
+        tc::mbar_wait(&tempty_bar, (s & 1) ^ 1);
+        tc::fence_after_sync();
+        for (int kq = 0; kq < ngrp; ++kq) {
+          const int kg = (kq + kc_off) % ngrp;
+          tc::mbar_wait(&full_bar[st], ph);
+          tc::fence_after_sync();
+          if (kq == 0) TR(1);
+          if (kq == ngrp - 1) TR(2);
+          for (int j = 0; j < a.kb; ++j) {
+            const int kc = kg * a.kb + j;
+            const uint32_t sa = base + r_bytes + st * stage_bytes + j * kChunk;
+            const uint32_t sb = base + (uint32_t)kc * kNHalf * 128;
+            if (!(a.debug_flags & 1))
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_f16_pair(tmem, tc::make_sdesc(sa + k * 32, 0, 1024), tc::make_sdesc(sb + k * 32, 0, 1024),
+                             idesc, (kq | j | k) != 0);
+          }
+          mma_commit_pair(&empty_bar[st]);
+          if (++st == a.stages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull_bar);
+      }
+    }
+  } else {  // ------------------------------------------------------ epilogue (both CTAs)
+    const int e = warp - 2;
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int part = e / 4;          // which 8-unit slice of the pair's 32 units
+    const int rl = q * 32 + lane;
+    const int row = a.b0 + r * 128 + rl;
+    const bool valid_row = row < a.B;
+    const int len = valid_row ? a.lens[row] : 0;
+    const int dir = a.dirsign[d];
+    const int H = a.H, T = a.T;
+    const int lo = part * kUT;
+    const int ut0 = u0 + lo;
+    const int nu = max(0, min(kUT, H - ut0));
+    const __nv_bfloat16* xw = a.xw[d];
+    __nv_bfloat16* hb = a.hbuf[d];
+    const bool save = a.gates[d] != nullptr;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + lo;
+    const uint32_t tempty_l = mapa(tc::smem_u32(&tempty_bar), 0);
+    const bool vec = (H % 8) == 0 && (a.xw_ld % 8) == 0;
+    float cst[kUT], hst[kUT];
+#pragma unroll
+    for (int u = 0; u < kUT; ++u) cst[u] = hst[u] = 0.f;
+
+    // x W + b (K1 output) of a step, prefetched one step ahead
+    auto load_xw = [&](int st, Bf16Vec<kUT>* xv) {
+      if (valid_row && st < len && !(a.debug_flags & 16)) {
+        const __nv_bfloat16* xr = xw + ((size_t)row * T + src_time(st, len, dir)) * a.xw_ld + ut0;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) xv[g].load(xr + g * H, nu, vec);
+      }
+    };
+    Bf16Vec<kUT> xv[4];
+    load_xw(0, xv);
+    for (int s = 0; s < Tmax; ++s) {
+      const bool active = valid_row && s < len;
+      const int t = active ? src_time(s, len, dir) : s;
+      const size_t pos = (size_t)row * T + t;
+      const bool tr0 = trace && e == 0 && lane == 0;
+      if (tr0) trace[s * 16 + 12] = gtimer();
+      if (lane == 0) tc::mbar_wait_sleep(&tfull_bar, s & 1);  // one poller per warp
+      __syncwarp();
+      tc::fence_after_sync();
+      if (tr0) trace[s * 16 + 8] = gtimer();
+      float z[4 * kUT];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float v[kUT];
+        tmem_ld_cols<kUT>(tbase + g * kPairUnits, v);
+#pragma unroll
+        for (int u = 0; u < kUT; ++u) z[g * kUT + u] = v[u];
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote_relaxed(tempty_l, 32);  // accumulator may be overwritten
+      if (tr0) trace[s * 16 + 9] = gtimer();
+
+      if (valid_row && !(a.debug_flags & 2)) {
+        if (active) {
+#pragma unroll
+          for (int u = 0; u < kUT; ++u) {
+            const float gi = tc::sigmoid_approx(z[u] + xv[0][u]);
+            const float gf = tc::sigmoid_approx(z[kUT + u] + xv[1][u]);
+            const float gg = tc::tanh_approx(z[2 * kUT + u] + xv[2][u]);
+            const float go = tc::sigmoid_approx(z[3 * kUT + u] + xv[3][u]);
+            z[u] = gi;
+            z[kUT + u] = gf;
+            z[2 * kUT + u] = gg;
+            z[3 * kUT + u] = go;
+            const float cn = fmaf(gf, cst[u], gi * gg);
+            cst[u] = cn;
+            hst[u] = go * tc::tanh_approx(cn);
+          }
+        }
+        // only h_s is on the cross-CTA critical path
+        store_bf16<kUT>(hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0, hst, nu);
+      }
+      if (tr0) trace[s * 16 + 11] = gtimer();
+      named_sync(1, kEpi);
+      if (e == 0 && lane == 0) {
+        tc::fence_proxy_async_global();
+        red_release_gpu(ctr, 1u);
+        TR(6);
+      }
+      if (valid_row && !(a.debug_flags & 10)) {
+        if (active) {
+          if (save) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              store_bf16<kUT>(a.gates[d] + gate_save_off(s, g, row, a.B, H, ut0), z + g * kUT, nu);
+          }
+          if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)d * H + ut0, hst, nu);
+          if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, hst, nu);
+          if (save) {  // the saved (c, h)_{prev} of each step, written off the critical path:
+            // zeros at the first step, (c_s, h_s) at the position of step s + 1
+            if (s == 0) {
+              float zero[kUT];
+#pragma unroll
+              for (int u = 0; u < kUT; ++u) zero[u] = 0.f;
+              store_bf16<kUT>(a.cprev[d] + cprev_save_off(0, row, a.B, H, ut0), zero, nu);
+              store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
+            }
+            if (s + 1 < len) {
+              const size_t pn = (size_t)row * T + src_time(s + 1, len, dir);
+              store_bf16<kUT>(a.cprev[d] + cprev_save_off(s + 1, row, a.B, H, ut0), cst, nu);
+              store_bf16<kUT>(a.hprev[d] + pn * a.hprev_ld + ut0, hst, nu);
+            }
+          }
+        } else {  // padded position t == s: zero output (tape.cpp:797), frozen state
+          float zero[kUT];
+#pragma unroll
+          for (int u = 0; u < kUT; ++u) zero[u] = 0.f;
+          if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)d * H + ut0, zero, nu);
+          if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
+          if (save) store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
+        }
+      }
+      if (s + 1 < Tmax) load_xw(s + 1, xv);
+    }
+    if (valid_row) {  // positions beyond the longest sequence, final states
+      float zero[kUT];
+#pragma unroll
+      for (int u = 0; u < kUT; ++u) zero[u] = 0.f;
+      for (int s = Tmax; s < T; ++s) {
+        const size_t pos = (size_t)row * T + s;
+        if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)d * H + ut0, zero, nu);
+        if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
+        if (save) store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
+      }
+#pragma unroll
+      for (int u = 0; u < kUT; ++u) {
+        if (u >= nu) continue;
+        if (a.h_last) a.h_last[((size_t)d * a.B + row) * H + ut0 + u] = hst[u];
+        if (a.c_last) a.c_last[((size_t)d * a.B + row) * H + ut0 + u] = cst[u];
+      }
+    }
+  }
+#undef TR
+  tc::fence_before_sync();
+  __syncthreads();
+  cluster_sync();  // the peer's MMAs / arrivals are done before TMEM and smem go away
+  if (warp == 1) tmem_dealloc_pair<kN>(tmem);
+}
+
+}  // namespace
+
+bool tc_rec_fwd_pair_fits(int H, int nd, int sms) {
+  const int P = (int)ceil_div(H, kPairUnits);
+  const int Kp = (int)round_up(H, 64);
+  return (int64_t)2 * P * nd <= sms && pair_smem(Kp, 2, 2) <= kSmemMax;
+}
+
+void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* const* RT,
+                  cudaStream_t stream) {
+  TcRecFwdArgs a = a0;
+  a.U = kPairUnits;
+  a.P = sh.P;
+  a.Kp = sh.Kp;
+  CUtensorMap tr[2], th[2];
+  a.kb = (a.Kp / 64) % 2 == 0 ? 2 : 1;
+  for (int k = 0; k < a.nd; ++k) {
+    cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.P * kN};
+    cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
+    cuuint32_t rb[2] = {64, (cuuint32_t)kNHalf};
+    tr[k] = tmap(RT[k], 2, rd, rs, rb);
+    cuuint64_t hd[4] = {64, (cuuint64_t)a.B, (cuuint64_t)a.Kp / 64, 2};
+    cuuint64_t hs[3] = {(cuuint64_t)a.Kp * 2, 128, (cuuint64_t)a.Kp * 2 * a.B};
+    cuuint32_t hbx[4] = {64, 128, (cuuint32_t)a.kb, 1};
+    th[k] = tmap(a.hbuf[k], 4, hd, hs, hbx);
+  }
+  a.stages = 0;
+  for (int st = kMaxStages; st >= 2 && !a.stages; --st)
+    if (pair_smem(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
+  SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_pair: R slice does not fit in shared memory");
+  const uint32_t smem = pair_smem(a.Kp, a.stages, a.kb);
+  SL_CUDA_TRY(cudaFuncSetAttribute(rec_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];
+  unsigned* bar0 = a.bar;
+  for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles
+    a.b0 = b0;
+    a.bar = bar0 + 4 * (b0 / 256);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * a.P * a.nd);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident, or fail loudly
+    attrs[1].val.cooperative = 1;
+    cfg.attrs = attrs;
+    static const bool no_coop = getenv("SL_NO_COOP") != nullptr;  // ncu only (see rec_tc.cu)
+    cfg.numAttrs = no_coop ? 1 : 2;
+    SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, rec_fwd_pair_kernel, r0, r1, h0, h1, a));
+    count_launch();
+  }
+}
+
+}  // namespace sl

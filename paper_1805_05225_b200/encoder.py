@@ -46,10 +46,18 @@ class BLSTMEncoder:
                     off += k
             self.p_views.append(pv)
             self.g_views.append(gv)
-        self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device)
-                       for D in self.in_dims]
-        self.acts = [torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
-                     for _ in range(num_layers)]
+        # bf16: the activations between layers stay in the padded bf16 layout the
+        # next layer's input GEMM reads (SL_LAYER_Y_BF16 -> SL_LAYER_X_BF16); only
+        # the top layer's output is fp32
+        chain = precision == "bf16"
+        last = num_layers - 1
+        self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device,
+                                      x_bf16=chain and l > 0, y_bf16=chain and l < last)
+                       for l, D in enumerate(self.in_dims)]
+        self.acts = [torch.zeros(batch, time, lstm.bf16_pitch(2 * H), dtype=torch.bfloat16,
+                                 device=self.device) if chain and l < last else
+                     torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
+                     for l in range(num_layers)]
         self.dxs = [torch.empty(batch, time, D, dtype=torch.float32, device=self.device)
                     for D in self.in_dims]
 

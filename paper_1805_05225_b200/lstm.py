@@ -28,6 +28,12 @@ LIB_PATH = os.path.join(_PKG, "lib", "libseqloom_cuda.so")
 
 SL_OK, SL_ERR_INVALID_ARGUMENT, SL_ERR_SHAPE, SL_ERR_CUDA, SL_ERR_WORKSPACE, SL_ERR_UNSUPPORTED = range(6)
 PRECISIONS = {"fp32": 0, "bf16": 1}
+SL_LAYER_X_BF16, SL_LAYER_Y_BF16 = 1, 2
+
+
+def bf16_pitch(features: int) -> int:
+    """Row pitch of the padded bf16 activation layout (seqloom_cuda.h sl_lstm_bf16_pitch)."""
+    return (features + 1 + 63) // 64 * 64
 
 
 class ShapeError(RuntimeError):
@@ -63,6 +69,8 @@ def lib() -> ctypes.CDLL:
                                         vp, sz, vp]
         L.sl_lstm_layer_bwd.argtypes = [P(_Layer), vp, vp, P(vp), P(vp), vp, vp, vp, vp, P(vp),
                                         P(vp), P(vp), ctypes.c_int, vp, sz, vp, sz, vp]
+        L.sl_lstm_bf16_pitch.restype = ctypes.c_int64
+        L.sl_lstm_bf16_pitch.argtypes = [i32]
         L.sl_lstm_cell_fwd.argtypes = [i32, i32, i32, i32] + [vp] * 9 + [vp]
         L.sl_lstm_cell_bwd.argtypes = [i32, i32, i32, i32] + [vp] * 14 + [ctypes.c_int, vp]
         _lib = L
@@ -110,9 +118,14 @@ class LSTMLayer:
     """
 
     def __init__(self, batch: int, time: int, input_dim: int, hidden: int, num_dirs: int = 1,
-                 direction: int = 1, precision: str = "fp32", device=None):
+                 direction: int = 1, precision: str = "fp32", device=None, x_bf16: bool = False,
+                 y_bf16: bool = False):
+        # x_bf16 / y_bf16: padded bf16 activations between stacked layers
+        # (SL_LAYER_X_BF16 / SL_LAYER_Y_BF16, bf16 precision only)
+        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
+        self.x_bf16, self.y_bf16 = x_bf16, y_bf16
         self.desc = _Layer(batch, time, input_dim, hidden, num_dirs, direction,
-                           PRECISIONS[precision], 0)
+                           PRECISIONS[precision], flags)
         self.device = torch.device(device or "cuda")
         L = lib()
         _check(L.sl_lstm_layer_check(ctypes.byref(self.desc)))
@@ -130,14 +143,21 @@ class LSTMLayer:
     def forward(self, x, seq_lens, W: Sequence, R: Sequence, b: Sequence, y=None, h_last=None,
                 c_last=None, train: bool = True):
         B, T, D, H, nd = self.shape
-        _need(x, (B, T, D), "x")
+        if self.x_bf16:
+            _need(x, (B, T, bf16_pitch(D)), "x", torch.bfloat16)
+        else:
+            _need(x, (B, T, D), "x")
         _need(seq_lens, (B,), "seq_lens", torch.int32)
         for k in range(nd):
             _need(W[k], (D, 4 * H), f"W[{k}]")
             _need(R[k], (H, 4 * H), f"R[{k}]")
             _need(b[k], (4 * H,), f"b[{k}]")
-        if y is None:
+        if y is None and self.y_bf16:
+            y = torch.zeros((B, T, bf16_pitch(nd * H)), dtype=torch.bfloat16, device=self.device)
+        elif y is None:
             y = torch.empty((B, T, nd * H), dtype=torch.float32, device=self.device)
+        elif self.y_bf16:
+            _need(y, (B, T, bf16_pitch(nd * H)), "y", torch.bfloat16)
         if h_last is None:
             h_last = torch.empty((nd, B, H), dtype=torch.float32, device=self.device)
         if c_last is None:

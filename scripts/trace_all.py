@@ -1,0 +1,80 @@
+"""Whole-grid step trace of the CTA-pair forward recurrence (rec_tc_pair.cu).
+
+    python scripts/trace_all.py [--D 2000] [--B 256] [--H 1000]
+
+Every CTA records its per-step phase timestamps (slots as in trace_report.py);
+this prints, per step, when the last CTA of each batch tile published, how
+long the consumers took to see it, and which CTAs straggle and why.
+"""
+import argparse, ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1805_05225_b200 import lstm
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=256)
+ap.add_argument("--T", type=int, default=60)
+ap.add_argument("--D", type=int, default=2000)
+ap.add_argument("--H", type=int, default=1000)
+ap.add_argument("--nd", type=int, default=2)
+a = ap.parse_args()
+B, T, D, H, nd = a.B, a.T, a.D, a.H, a.nd
+g = torch.Generator(device="cuda").manual_seed(0)
+x = torch.rand(B, T, D, device="cuda", generator=g) * 2 - 1
+lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
+s = H ** -0.5
+W = [(torch.rand(D, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
+R = [(torch.rand(H, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
+b = [(torch.rand(4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
+layer = lstm.LSTMLayer(B, T, D, H, nd, 1, "bf16")
+for _ in range(2):
+    layer.forward(x, lens, W, R, b)
+torch.cuda.synchronize()
+grid = 2 * ((H + 31) // 32) * nd
+L = lstm.lib()
+buf = torch.zeros(grid * T * 16, dtype=torch.int64, device="cuda")
+L.sl_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), -1)
+layer.forward(x, lens, W, R, b)
+torch.cuda.synchronize()
+L.sl_debug_set_trace(None, 0)
+t = buf.view(grid, T, 16).cpu().double() / 1000.0  # us
+t0 = t[:, 1, 0].min()
+t = t - t0
+tile = torch.arange(grid) % 2
+steps = range(3, T - 3)
+rows = []
+for st in steps:
+    for r in (0, 1):
+        m = tile == r
+        pub = t[m, st, 6]
+        nxt = t[m, st + 1, 0]  # producers saw the counter for step st+1
+        last = pub.max().item()
+        rows.append((last - pub.min().item(), (nxt - last).median().item(), (nxt - last).max().item(),
+                     int(torch.nonzero(m)[pub.argmax()].item())))
+rows_t = torch.tensor([r[:3] for r in rows])
+print(f"grid {grid}: per step and tile (median over steps) | publish spread {rows_t[:,0].median():.2f} us | "
+      f"last publish -> consumer start: median {rows_t[:,1].median():.2f} max {rows_t[:,2].median():.2f} us")
+period = (t[:, T - 4, 6] - t[:, 4, 6]) / (T - 8)
+print(f"period (all CTAs) median {period.median():.2f} us")
+from collections import Counter
+c = Counter(r[3] for r in rows)
+print("most frequent last publishers (cta: count):", c.most_common(8))
+# phase durations per CTA, median over steps (leader CTAs hold the MMA slots 1, 2)
+sl = slice(3, T - 3)
+w2f = (t[:, sl, 1] - t[:, sl, 0]).median(dim=1).values
+stream = (t[:, sl, 2] - t[:, sl, 1]).median(dim=1).values
+m2p = (t[:, sl, 6] - t[:, sl, 8]).median(dim=1).values
+tfw = (t[:, sl, 8] - t[:, sl, 12]).median(dim=1).values
+lead = tile == 0
+print(f"leaders: wait->first median {w2f[lead].median():.2f} max {w2f[lead].max():.2f} | "
+      f"stream median {stream[lead].median():.2f} max {stream[lead].max():.2f} (cta {int(stream[lead].argmax())*2})")
+print(f"all: tfull->publish median {m2p.median():.2f} max {m2p.max():.2f} (cta {int(m2p.argmax())})")
+raw = buf.view(grid, T, 16).cpu().double()
+polls = raw[:, sl, 14]
+spin = (raw[:, sl, 0] - raw[:, sl, 13]) / 1000.0
+rtt = spin.sum() / polls.clamp(min=1).sum()
+print(f"counter spin: median {spin.median():.2f} us, {polls.median():.0f} polls; mean poll round trip {rtt:.3f} us")
+for cta in [cc for cc, _ in c.most_common(3)]:
+    p = cta - cta % 2
+    print(f"  cta {cta}: start {t[cta, sl, 0].mean() - t[:, sl, 0].mean(dim=0).mean():+.2f} vs mean; "
+          f"pair leader stream {stream[p]:.2f}, wait->first {w2f[p]:.2f}; tfull->pub {m2p[cta]:.2f}")

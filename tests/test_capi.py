@@ -90,3 +90,20 @@ def test_python_mirror_raises_like_reference():
     with pytest.raises(lstm.ShapeError):
         lstm.lstm_sequence(torch.zeros(3, 4), torch.ones(2, dtype=torch.int32),
                            torch.zeros(4, 8), torch.zeros(2, 8), torch.zeros(8), direction=1)
+
+
+def test_bf16_activation_flags():
+    # SL_LAYER_X_BF16 / SL_LAYER_Y_BF16: bf16 precision only, known bits only;
+    # with a bf16 input the reserve no longer carries a converted copy of x
+    L = lstm.lib()
+    both = lstm.SL_LAYER_X_BF16 | lstm.SL_LAYER_Y_BF16
+    assert L.sl_lstm_layer_check(ctypes.byref(desc(precision=1, flags=both))) == 0
+    assert L.sl_lstm_layer_check(ctypes.byref(desc(precision=0, flags=1))) == lstm.SL_ERR_UNSUPPORTED
+    assert "precision" in L.sl_last_error().decode()
+    assert L.sl_lstm_layer_check(ctypes.byref(desc(precision=1, flags=8))) == lstm.SL_ERR_INVALID_ARGUMENT
+    kw = dict(batch=64, time=30, input_dim=200, hidden=64, precision=1)
+    r0 = L.sl_lstm_reserve_size(ctypes.byref(desc(**kw)))
+    r1 = L.sl_lstm_reserve_size(ctypes.byref(desc(flags=lstm.SL_LAYER_X_BF16, **kw)))
+    assert 0 < r1 <= r0 - 64 * 30 * 256 * 2
+    for f in (1, 7, 64, 199, 2000):
+        assert L.sl_lstm_bf16_pitch(f) == lstm.bf16_pitch(f) == (f + 64) // 64 * 64

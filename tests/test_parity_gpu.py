@@ -284,3 +284,70 @@ def test_inference_mode_matches_training_forward(cuda, prec):
     y2, h2, c2 = layer.forward(x, lens, [W, W], [R, R], [b, b], train=False)
     torch.cuda.synchronize()
     assert torch.equal(y1, y2) and torch.equal(h1, h2) and torch.equal(c1, c2)
+
+
+def test_bf16_activation_io_matches_fp32_io(cuda):
+    # SL_LAYER_X_BF16 / SL_LAYER_Y_BF16 only change the I/O format: fed the same
+    # bf16-rounded x, the layer computes exactly what the fp32-I/O layer computes
+    B, T, D, H = 37, 11, 70, 48
+    x, lens, W, R, b = _seeded(31, B, T, D, H)
+    x = x.bfloat16().float()
+    W2, R2, b2 = _seeded(32, 1, 1, D, H)[2:]
+    dy = torch.rand(B, T, 2 * H, device="cuda") * 2 - 1
+    ref = lstm.LSTMLayer(B, T, D, H, 2, 1, "bf16")
+    y0, h0, c0 = ref.forward(x, lens, [W, W2], [R, R2], [b, b2])
+    g0 = ref.backward(dy)
+    xp = torch.zeros(B, T, lstm.bf16_pitch(D), dtype=torch.bfloat16, device="cuda")
+    xp[:, :, :D] = x.bfloat16()
+    xp[:, :, D] = 1.0
+    lay = lstm.LSTMLayer(B, T, D, H, 2, 1, "bf16", x_bf16=True, y_bf16=True)
+    y1, h1, c1 = lay.forward(xp, lens, [W, W2], [R, R2], [b, b2])
+    g1 = lay.backward(dy)
+    torch.cuda.synchronize()
+    assert y1.shape == (B, T, lstm.bf16_pitch(2 * H)) and y1.dtype == torch.bfloat16
+    assert torch.equal(y1[:, :, :2 * H], y0.bfloat16())
+    assert torch.equal(y1[:, :, 2 * H], torch.ones(B, T, dtype=torch.bfloat16, device="cuda"))
+    assert torch.equal(h1, h0) and torch.equal(c1, c0)
+    assert torch.equal(g1[0], g0[0])
+    for k in (1, 2, 3):
+        for d in range(2):
+            assert torch.equal(g1[k][d], g0[k][d])
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_encoder_stack_matches_fp64(cuda, prec):
+    # the BASELINE caller (3-layer BLSTM, bf16 activations chained between
+    # layers on the bf16 path) against a layer-by-layer fp64 restatement
+    from paper_1805_05225_b200.encoder import BLSTMEncoder
+    Lyr, B, T, D0, H = 3, 20, 9, 24, 32
+    enc = BLSTMEncoder(Lyr, B, T, D0, H, prec)
+    enc.init_uniform(5)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.rand(B, T, D0, device="cuda", generator=g) * 2 - 1
+    lens = torch.randint(T // 2, T + 1, (B,), device="cuda", generator=g).int()
+    dy = torch.rand(B, T, 2 * H, device="cuda", generator=g) * 2 - 1
+    y = enc.forward(x, lens)
+    dx = enc.backward(dy)
+    torch.cuda.synchronize()
+    # fp64 reference: forward through the stack, then backward layer by layer
+    inp, saved = x.double(), []
+    for l in range(Lyr):
+        W, R, bb = enc._wrb(l)
+        outs = [torch_ref.sequence(inp, lens, W[k], R[k], bb[k], (1, -1)[k]) for k in range(2)]
+        saved.append(inp)
+        inp = torch.cat([o["y"] for o in outs], dim=2)
+    assert rel(y, inp) < TOL[prec] * 2
+    gy = dy.double()
+    for l in reversed(range(Lyr)):
+        W, R, bb = enc._wrb(l)
+        gx = 0
+        for k in range(2):
+            ref = torch_ref.sequence(saved[l], lens, W[k], R[k], bb[k], (1, -1)[k],
+                                     gy[:, :, k * H:(k + 1) * H])
+            gv = enc.g_views[l]
+            assert rel(gv[3 * k + 0], ref["dW"]) < TOL[prec] * 2, (l, k, "dW")
+            assert rel(gv[3 * k + 1], ref["dR"]) < TOL[prec] * 2, (l, k, "dR")
+            assert rel(gv[3 * k + 2], ref["db"]) < TOL[prec] * 2, (l, k, "db")
+            gx = gx + ref["dx"]
+        gy = gx
+    assert rel(dx, gy) < TOL[prec] * 2
