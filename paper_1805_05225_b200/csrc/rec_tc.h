@@ -45,6 +45,7 @@ struct TcRecFwdArgs {
   unsigned* bar;              // zeroed step counters, 2 per batch chunk
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;
+  int xw_tma;       // pair kernel: x W tiles may be TMA-loaded (set internally)
   int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores,
                     // 4 = no step-counter waits (wrong results)
 };

@@ -46,6 +46,7 @@ constexpr int kEpi = 128 * kSplit;          // epilogue threads
 constexpr int kThreads = 64 + kEpi;
 constexpr int kMaxStages = 8;
 constexpr uint32_t kChunk = 128 * 64 * 2;   // 128 rows x 64 K bf16
+constexpr uint32_t kXwGate = 128 * 32 * 2;  // x W tile of one gate: 128 rows x 32 units bf16
 constexpr uint32_t kSmemMax = 227 * 1024;
 
 uint32_t pair_smem(int Kp, int stages, int kb) {
@@ -55,12 +56,14 @@ uint32_t pair_smem(int Kp, int stages, int kb) {
 __global__ void __launch_bounds__(kThreads, 1)
     rec_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmR0, const __grid_constant__ CUtensorMap tmR1,
                         const __grid_constant__ CUtensorMap tmH0, const __grid_constant__ CUtensorMap tmH1,
+                        const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                         TcRecFwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar, tempty_bar;
+  __shared__ __align__(8) uint64_t xw_full[kMaxStages];  // ring slots carrying an x W tile
   __shared__ uint32_t tmem_sh;
-  __shared__ int tmax_sh;
+  __shared__ int tmax_sh, tmin_sh;
 
   const int pr = blockIdx.x / 2;        // pair index over both directions
   const int d = pr / a.P;               // a.P = pairs per direction
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int u0 = pair * kPairUnits;
   const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
   const CUtensorMap* tmH = d == 0 ? &tmH0 : &tmH1;
+  const CUtensorMap* tmX = d == 0 ? &tmX0 : &tmX1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
@@ -81,11 +85,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
+    tmin_sh = 1 << 30;
     tc::prefetch_tmap(tmR);
     tc::prefetch_tmap(tmH);
+    if (a.xw_tma) tc::prefetch_tmap(tmX);
     for (int s = 0; s < a.stages; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
+      tc::mbar_init(&xw_full[s], 1);
     }
     tc::mbar_init(&r_bar, 1);
     tc::mbar_init(&tfull_bar, 1);
@@ -98,12 +105,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc::fence_after_sync();
   {
-    int m = 0;
-    for (int i = threadIdx.x; i < a.B; i += blockDim.x) m = max(m, (int)a.lens[i]);
+    int m = 0, mn = 1 << 30;
+    for (int i = threadIdx.x; i < a.B; i += blockDim.x) {
+      m = max(m, (int)a.lens[i]);
+      mn = min(mn, (int)a.lens[i]);
+    }
     atomicMax(&tmax_sh, m);
+    atomicMin(&tmin_sh, mn);
   }
   __syncthreads();
   const int Tmax = tmax_sh;
+  // Equal lengths: step s is the same time index for every row, so a step's
+  // x W rows form one TMA box per gate; it rides the h ring as one extra slot
+  // per step (loaded before the step counter is even polled, consumed by the
+  // epilogue) instead of 4 x 128 scattered 32 B loads.
+  const bool xw_tma = a.xw_tma && tmin_sh == Tmax;
+  const int dir = a.dirsign[d];
   const uint32_t tmem = tmem_sh;
   // debug trace: one CTA (trace_cta >= 0) or every CTA (trace_cta < 0, buffer [grid][T][16])
   const bool trace_on = a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta);
@@ -125,6 +142,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       int st = 0;
       uint32_t ph = 0;
       for (int s = 0; s < Tmax; ++s) {
+        if (xw_tma) {  // this step's x W tile: 4 gate boxes [128 rows x 32 units]
+          tc::mbar_wait(&empty_bar[st], ph ^ 1);
+          // the slot's stage-full barrier (the leader's) must still complete one
+          // phase per ring pass, or the MMA issuer's parity drifts
+          if (leader) tc::mbar_arrive(&full_bar[st]);
+          tc::mbar_arrive_expect_tx(&xw_full[st], 4 * kXwGate);
+          const int t = src_time(s, Tmax, dir);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            tma_load_3d(sH + st * stage_bytes + g * kXwGate, tmX, &xw_full[st], g * a.H + u0, t,
+                        a.b0 + r * 128);
+          if (++st == a.stages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
         if (s > 0 && !(a.debug_flags & 4)) {
           const unsigned target = (unsigned)a.P * (unsigned)s;
           TR(13);
@@ -154,6 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int st = 0;
       uint32_t ph = 0;
       for (int s = 0; s < Tmax; ++s) {
+        if (xw_tma && ++st == a.stages) {  // the x W slot belongs to the epilogue
+          st = 0;
+          ph ^= 1;
+        }
         tc::mbar_wait(&tempty_bar, (s & 1) ^ 1);
         tc::fence_after_sync();
         for (int kq = 0; kq < ngrp; ++kq) {
@@ -189,7 +226,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = a.b0 + r * 128 + rl;
     const bool valid_row = row < a.B;
     const int len = valid_row ? a.lens[row] : 0;
-    const int dir = a.dirsign[d];
     const int H = a.H, T = a.T;
     const int lo = part * kUT;
     const int ut0 = u0 + lo;
@@ -205,7 +241,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = 0; u < kUT; ++u) cst[u] = hst[u] = 0.f;
 
     // x W + b (K1 output) of a step, prefetched one step ahead
+    uint32_t xw_par = 0;  // per ring slot: parity of its next x W use
     auto load_xw = [&](int st, Bf16Vec<kUT>* xv) {
+      if (xw_tma) {
+        const int slot = (int)(((int64_t)st * (ngrp + 1)) % a.stages);
+        tc::mbar_wait(&xw_full[slot], (xw_par >> slot) & 1);
+        xw_par ^= 1u << slot;
+        const uint8_t* tile = sH + slot * stage_bytes + rl * 64;
+        const uint32_t sw = (rl >> 1) & 3;  // SWIZZLE_64B: 16 B chunk ^= address bits [7:8]
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint4 q0 = *reinterpret_cast<const uint4*>(tile + g * kXwGate + ((2 * part) ^ sw) * 16);
+          const uint4 q1 = *reinterpret_cast<const uint4*>(tile + g * kXwGate + ((2 * part + 1) ^ sw) * 16);
+          xv[g].w[0] = q0.x, xv[g].w[1] = q0.y, xv[g].w[2] = q0.z, xv[g].w[3] = q0.w;
+          xv[g].w[4] = q1.x, xv[g].w[5] = q1.y, xv[g].w[6] = q1.z, xv[g].w[7] = q1.w;
+        }
+        named_sync(2, kEpi);  // every epilogue thread has its slice: the slot is free
+        if (e == 0 && lane == 0) tc::mbar_arrive(&empty_bar[slot]);
+        return;
+      }
       if (valid_row && st < len && !(a.debug_flags & 16)) {
         const __nv_bfloat16* xr = xw + ((size_t)row * T + src_time(st, len, dir)) * a.xw_ld + ut0;
 #pragma unroll
@@ -338,8 +392,24 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   a.U = kPairUnits;
   a.P = sh.P;
   a.Kp = sh.Kp;
-  CUtensorMap tr[2], th[2];
+  CUtensorMap tr[2], th[2], tx[2];
   a.kb = (a.Kp / 64) % 2 == 0 ? 2 : 1;
+  // x W tiles by TMA: 3-D view {columns, T, B} of the bf16 K1 output, one box
+  // per gate of [128 rows x 32 units], 64 B swizzle (conflict-free epilogue reads)
+  a.xw_tma = kChunk * a.kb >= 4 * kXwGate && (a.xw_ld * 2) % 16 == 0 && !(a.debug_flags & 64);
+  for (int k = 0; k < a.nd; ++k) {
+    a.xw_tma = a.xw_tma && ((uintptr_t)a.xw[k] & 15) == 0;
+  }
+  for (int k = 0; k < a.nd; ++k) {
+    if (a.xw_tma) {
+      cuuint64_t xd[3] = {(cuuint64_t)a.xw_ld, (cuuint64_t)a.T, (cuuint64_t)a.B};
+      cuuint64_t xs[2] = {(cuuint64_t)a.xw_ld * 2, (cuuint64_t)a.xw_ld * 2 * a.T};
+      cuuint32_t xb[3] = {32, 1, 128};
+      tx[k] = tmap(a.xw[k], 3, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_64B);
+    } else {
+      tx[k] = CUtensorMap{};
+    }
+  }
   for (int k = 0; k < a.nd; ++k) {
     cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.P * kN};
     cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
@@ -357,6 +427,7 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   const uint32_t smem = pair_smem(a.Kp, a.stages, a.kb);
   SL_CUDA_TRY(cudaFuncSetAttribute(rec_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];
+  CUtensorMap x0 = tx[0], x1 = tx[a.nd > 1 ? 1 : 0];
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles
     a.b0 = b0;
@@ -376,7 +447,7 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
     cfg.attrs = attrs;
     static const bool no_coop = getenv("SL_NO_COOP") != nullptr;  // ncu only (see rec_tc.cu)
     cfg.numAttrs = no_coop ? 1 : 2;
-    SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, rec_fwd_pair_kernel, r0, r1, h0, h1, a));
+    SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, rec_fwd_pair_kernel, r0, r1, h0, h1, x0, x1, a));
     count_launch();
   }
 }

@@ -351,3 +351,31 @@ def test_encoder_stack_matches_fp64(cuda, prec):
             gx = gx + ref["dx"]
         gy = gx
     assert rel(dx, gy) < TOL[prec] * 2
+
+
+@pytest.mark.parametrize("L", [60, 41])
+def test_equal_lengths_tma_paths_match(cuda, L):
+    # equal sequence lengths (the throughput workload: every row at the same
+    # time index per step) switch the bf16 forward to TMA-loaded x W tiles;
+    # results must equal the per-row load path bit for bit and the fp64 oracle
+    B, T, D, H = 200, 60, 96, 1000
+    x, _, W, R, b = _seeded(41, B, T, D, H)
+    lens = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    W2, R2, b2 = _seeded(42, 1, 1, D, H)[2:]
+    dy = torch.rand(B, T, 2 * H, device="cuda") * 2 - 1
+    outs = []
+    for flags in (0, 64):  # 64: experiments switch that disables the TMA x W path
+        lstm.lib().sl_debug_set_flags(flags)
+        try:
+            outs.append(run_layer(x, lens, [(W, R, b), (W2, R2, b2)], 2, 1, "bf16", dy))
+        finally:
+            lstm.lib().sl_debug_set_flags(0)
+    for k in ("y", "h_last", "c_last", "dx"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    for k in ("dW", "dR", "db"):
+        for d in range(2):
+            assert torch.equal(outs[0][k][d], outs[1][k][d]), k
+    for k, (Wk, Rk, bk, d) in enumerate(((W, R, b, 1), (W2, R2, b2, -1))):
+        ref = torch_ref.sequence(x, lens, Wk, Rk, bk, d, dy[:, :, k * H:(k + 1) * H])
+        assert rel(outs[0]["y"][:, :, k * H:(k + 1) * H], ref["y"]) < TOL["bf16"]
+        assert rel(outs[0]["dR"][k], ref["dR"]) < TOL["bf16"]
