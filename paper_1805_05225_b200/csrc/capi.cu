@@ -156,7 +156,7 @@ struct FwdWork {
 FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   FwdWork w;
-  w.bar = c.take<unsigned>(64);
+  w.bar = c.take<unsigned>(rec_bar_count(d.B));
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
     __nv_bfloat16* xw = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
@@ -196,7 +196,7 @@ struct BwdWork {
 BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
   Carve c(p);
   BwdWork w;
-  w.bar = c.take<unsigned>(64);
+  w.bar = c.take<unsigned>(rec_bar_count(d.B));
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
     const TcBwdShape sh = tc_rec_bwd_shape(d.H, d.nd, sm_count());
@@ -298,7 +298,7 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       rv = carve_reserve(d, prec, reserve, &need_r);
       SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_fwd: reserve too small");
     }
-    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 64 * sizeof(unsigned), stream));
+    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), stream));
     const double k1_flops = 2.0 * d.BT() * d.D * 4.0 * d.H * d.nd;
     if (prec == SL_PREC_BF16) {
       // Pack [W_fw | W_bw] and x to bf16 (kept in the reserve for the backward
@@ -424,7 +424,7 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
                "sl_lstm_layer_bwd: workspace too small");
     ReserveView rv = carve_reserve(d, prec, const_cast<void*>(reserve), &need_r);
     SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_bwd: reserve too small");
-    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 64 * sizeof(unsigned), stream));
+    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), stream));
     const float beta = accumulate ? 1.f : 0.f;
     const int M = (int)d.BT(), G = 4 * d.H;
     const double fx = 2.0 * M * G * (double)d.D;

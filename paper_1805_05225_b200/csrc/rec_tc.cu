@@ -522,7 +522,7 @@ void rec_fwd_tc(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* con
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles
     a.b0 = b0;
-    a.bar = bar0 + 4 * (b0 / 256);  // fresh zeroed counters per chunk (2 dirs x 2 tiles)
+    a.bar = bar0 + kBarPerChunk * (b0 / 256);  // fresh zeroed counters per chunk
     const int MT = (a.B - b0) > 128 ? 2 : 1;
     switch (sh.C * 1000 + sh.U * 10 + MT) {
 #define SL_FWD_CASE(C_, U_, MT_) \

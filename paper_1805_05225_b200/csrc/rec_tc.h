@@ -21,6 +21,11 @@ __host__ __device__ inline size_t cprev_save_off(int s, int row, int B, int H, i
   return (((size_t)s * (save_hq(H) / 16) + u / 16) * B + row) * 16 + u % 16;
 }
 
+// Step counters of the persistent recurrences: kBarPerChunk zeroed unsigned
+// per 256-row batch chunk (one launch each), rec_bar_count(B) in total.
+constexpr int kBarPerChunk = 64;
+inline size_t rec_bar_count(int B) { return (size_t)kBarPerChunk * ((B + 255) / 256); }
+
 struct TcRecFwdArgs {
   int B, T, H, nd, U, P;  // P = CTAs per direction (= ceil(H / U))
   int b0;                 // first batch row of this launch (set internally)

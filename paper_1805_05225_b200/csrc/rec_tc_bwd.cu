@@ -466,7 +466,7 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
-    a.bar = bar0 + 4 * (b0 / 256);
+    a.bar = bar0 + kBarPerChunk * (b0 / 256);
     const int MT = (a.B - b0) > 128 ? 2 : 1;
     const int key = sh.C * 1000 + sh.U * 10 + MT;
     switch (key) {

@@ -124,25 +124,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_sh;
   // debug trace: one CTA (trace_cta >= 0) or every CTA (trace_cta < 0, buffer [grid][T][16])
   const bool trace_on = a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta);
-  unsigned long long* trace = trace_on ? a.trace + (a.trace_cta < 0 ? (size_t)blockIdx.x * a.T * 16 : 0) : nullptr;
+  // all-CTA mode uses 48 slots per step: [0,16) phases, [16,32) per-group TMA
+  // issue times, [32,48) per-group stage-full times at the MMA issuer
+  const int tstride = a.trace_cta < 0 ? 48 : 16;
+  unsigned long long* trace =
+      trace_on ? a.trace + (a.trace_cta < 0 ? (size_t)blockIdx.x * a.T * tstride : 0) : nullptr;
 #define TR(k)                                          \
   do {                                                 \
-    if (trace) trace[s * 16 + (k)] = gtimer();         \
+    if (trace) trace[s * tstride + (k)] = gtimer();    \
   } while (0)
-  unsigned* ctr = a.bar + d * 2 + r;  // step counter of (direction, my batch tile)
+  // Step counters per (direction, batch tile, K group of kb*64 hidden units):
+  // a pair publishes its 32 units of h_s to its group's counter, and a
+  // consumer streams each K group as soon as THAT group is complete — the
+  // stream overlaps the stragglers instead of waiting for the slowest pair.
   const int ngrp = nkc / a.kb;
-  const int kc_off = pair % ngrp;
+  const int gunits = a.kb * 64;
+  const int kc_off = (a.debug_flags & 128) ? (u0 / gunits) % ngrp
+                     : (a.debug_flags & 256) ? (u0 / gunits + ngrp / 2) % ngrp : pair % ngrp;
+  unsigned* ctr = a.bar + (d * 2 + r) * 16;
+  auto group_pairs = [&](int g) {  // pairs publishing into K group g
+    return max(0, min(gunits / kPairUnits, a.P - g * (gunits / kPairUnits)));
+  };
 
-  if (warp == 0) {
-    if (lane == 0) {  // -------------------------------------------- producer (both CTAs)
+  if (warp == 0) {  // ------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
       const uint32_t r_bar_l = mapa(tc::smem_u32(&r_bar), 0);
       if (leader) tc::mbar_arrive_expect_tx(&r_bar, 2 * r_bytes);
       for (int kc = 0; kc < nkc; ++kc)
         tma_load_2d_pair(sR + (size_t)kc * kNHalf * 128, tmR, r_bar_l, kc * 64, pair * kN + r * kNHalf);
-      int st = 0;
-      uint32_t ph = 0;
-      for (int s = 0; s < Tmax; ++s) {
-        if (xw_tma) {  // this step's x W tile: 4 gate boxes [128 rows x 32 units]
+    }
+    int st = 0;  // ring position, tracked by every lane (only lane 0 issues)
+    uint32_t ph = 0;
+    auto advance = [&]() {
+      if (++st == a.stages) {
+        st = 0;
+        ph ^= 1;
+      }
+    };
+    const int kg_lane = (lane + kc_off) % ngrp;  // lane k polls the k-th group in issue order
+    for (int s = 0; s < Tmax; ++s) {
+      if (xw_tma) {  // this step's x W tile: 4 gate boxes [128 rows x 32 units]
+        if (lane == 0) {
           tc::mbar_wait(&empty_bar[st], ph ^ 1);
           // the slot's stage-full barrier (the leader's) must still complete one
           // phase per ring pass, or the MMA issuer's parity drifts
@@ -153,30 +175,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int g = 0; g < 4; ++g)
             tma_load_3d(sH + st * stage_bytes + g * kXwGate, tmX, &xw_full[st], g * a.H + u0, t,
                         a.b0 + r * 128);
-          if (++st == a.stages) {
-            st = 0;
-            ph ^= 1;
-          }
         }
-        if (s > 0 && !(a.debug_flags & 4)) {
-          const unsigned target = (unsigned)a.P * (unsigned)s;
-          TR(13);
-          unsigned polls = 0;
-          while (ld_acquire(ctr) < target) ++polls;
-          if (trace) trace[s * 16 + 14] = polls;
-          tc::fence_proxy_async_global();
-        }
-        TR(0);
-        for (int kq = 0; kq < ngrp; ++kq) {
-          const int kg = (kq + kc_off) % ngrp;
-          tc::mbar_wait(&empty_bar[st], ph ^ 1);
-          if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
-          tma_load_4d_pair(sH + st * stage_bytes, tmH, mapa(tc::smem_u32(&full_bar[st]), 0), 0,
-                           a.b0 + r * 128, kg * a.kb, s & 1);
-          if (++st == a.stages) {
-            st = 0;
-            ph ^= 1;
+        advance();
+      }
+      const unsigned target = (unsigned)group_pairs(kg_lane) * (unsigned)s;
+      bool rdy = lane >= ngrp || s == 0 || (a.debug_flags & 4);
+      if (lane == 0) TR(13);
+      int done = 0;
+      while (done < ngrp) {
+        if (!rdy) rdy = ld_acquire(ctr + kg_lane) >= target;
+        const unsigned m = __ballot_sync(0xffffffffu, rdy);
+        while (done < ngrp && ((m >> done) & 1u)) {
+          if (lane == 0) {
+            if (done == 0) TR(0);
+            if (tstride == 48) TR(16 + done);
+            const int kg = (done + kc_off) % ngrp;
+            tc::fence_proxy_async_global();  // the group's h (generic-proxy stores) -> TMA reads
+            tc::mbar_wait(&empty_bar[st], ph ^ 1);
+            if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
+            tma_load_4d_pair(sH + st * stage_bytes, tmH, mapa(tc::smem_u32(&full_bar[st]), 0), 0,
+                             a.b0 + r * 128, kg * a.kb, s & 1);
           }
+          advance();
+          ++done;
         }
       }
     }
@@ -199,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::fence_after_sync();
           if (kq == 0) TR(1);
           if (kq == ngrp - 1) TR(2);
+          if (tstride == 48) TR(32 + kq);
           for (int j = 0; j < a.kb; ++j) {
             const int kc = kg * a.kb + j;
             const uint32_t sa = base + r_bytes + st * stage_bytes + j * kChunk;
@@ -273,11 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
       const bool tr0 = trace && e == 0 && lane == 0;
-      if (tr0) trace[s * 16 + 12] = gtimer();
+      if (tr0) trace[s * tstride + 12] = gtimer();
       if (lane == 0) tc::mbar_wait_sleep(&tfull_bar, s & 1);  // one poller per warp
       __syncwarp();
       tc::fence_after_sync();
-      if (tr0) trace[s * 16 + 8] = gtimer();
+      if (tr0) trace[s * tstride + 8] = gtimer();
       float z[4 * kUT];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote_relaxed(tempty_l, 32);  // accumulator may be overwritten
-      if (tr0) trace[s * 16 + 9] = gtimer();
+      if (tr0) trace[s * tstride + 9] = gtimer();
 
       if (valid_row && !(a.debug_flags & 2)) {
         if (active) {
@@ -311,11 +333,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // only h_s is on the cross-CTA critical path
         store_bf16<kUT>(hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0, hst, nu);
       }
-      if (tr0) trace[s * 16 + 11] = gtimer();
+      if (tr0) trace[s * tstride + 11] = gtimer();
       named_sync(1, kEpi);
       if (e == 0 && lane == 0) {
         tc::fence_proxy_async_global();
-        red_release_gpu(ctr, 1u);
+        red_release_gpu(ctr + u0 / gunits, 1u);  // my K group's counter
         TR(6);
       }
       if (valid_row && !(a.debug_flags & 10)) {
@@ -394,6 +416,7 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   a.Kp = sh.Kp;
   CUtensorMap tr[2], th[2], tx[2];
   a.kb = (a.Kp / 64) % 2 == 0 ? 2 : 1;
+  if (const char* kb = getenv("SL_FWD_KB")) a.kb = kb[0] == '1' ? 1 : a.kb;  // experiments
   // x W tiles by TMA: 3-D view {columns, T, B} of the bf16 K1 output, one box
   // per gate of [128 rows x 32 units], 64 B swizzle (conflict-free epilogue reads)
   a.xw_tma = kChunk * a.kb >= 4 * kXwGate && (a.xw_ld * 2) % 16 == 0 && !(a.debug_flags & 64);
@@ -431,7 +454,7 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {  // batch chunks of up to two 128-row tiles
     a.b0 = b0;
-    a.bar = bar0 + 4 * (b0 / 256);
+    a.bar = bar0 + kBarPerChunk * (b0 / 256);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * a.P * a.nd);
     cfg.blockDim = dim3(kThreads);

@@ -32,12 +32,14 @@ for _ in range(2):
 torch.cuda.synchronize()
 grid = 2 * ((H + 31) // 32) * nd
 L = lstm.lib()
-buf = torch.zeros(grid * T * 16, dtype=torch.int64, device="cuda")
+L.sl_debug_set_flags(int(os.environ.get("SL_FLAGS", "0")))
+buf = torch.zeros(grid * T * 48, dtype=torch.int64, device="cuda")
 L.sl_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), -1)
 layer.forward(x, lens, W, R, b)
 torch.cuda.synchronize()
 L.sl_debug_set_trace(None, 0)
-t = buf.view(grid, T, 16).cpu().double() / 1000.0  # us
+L.sl_debug_set_flags(0)
+t = buf.view(grid, T, 48).cpu().double() / 1000.0  # us
 t0 = t[:, 1, 0].min()
 t = t - t0
 tile = torch.arange(grid) % 2
@@ -69,7 +71,7 @@ lead = tile == 0
 print(f"leaders: wait->first median {w2f[lead].median():.2f} max {w2f[lead].max():.2f} | "
       f"stream median {stream[lead].median():.2f} max {stream[lead].max():.2f} (cta {int(stream[lead].argmax())*2})")
 print(f"all: tfull->publish median {m2p.median():.2f} max {m2p.max():.2f} (cta {int(m2p.argmax())})")
-raw = buf.view(grid, T, 16).cpu().double()
+raw = buf.view(grid, T, 48).cpu().double()
 polls = raw[:, sl, 14]
 spin = (raw[:, sl, 0] - raw[:, sl, 13]) / 1000.0
 rtt = spin.sum() / polls.clamp(min=1).sum()
@@ -78,3 +80,42 @@ for cta in [cc for cc, _ in c.most_common(3)]:
     p = cta - cta % 2
     print(f"  cta {cta}: start {t[cta, sl, 0].mean() - t[:, sl, 0].mean(dim=0).mean():+.2f} vs mean; "
           f"pair leader stream {stream[p]:.2f}, wait->first {w2f[p]:.2f}; tfull->pub {m2p[cta]:.2f}")
+qs = torch.tensor([0.0, 0.1, 0.5, 0.9, 1.0], dtype=torch.float64)
+print("leader stream quantiles (0,10,50,90,100%):", [round(v, 2) for v in torch.quantile(stream[lead], qs).tolist()])
+slow = torch.argsort(stream[lead], descending=True)[:6] * 2
+print("slowest leaders:", slow.tolist(), [round(stream[i].item(), 2) for i in slow])
+st0 = 20
+for cta in slow[:3].tolist() + [0]:
+    row = t[cta, st0]
+    print(f"  cta {cta} step {st0}: first-issue {row[0]:.2f} first-full {row[1]:.2f} last-full {row[2]:.2f} "
+          f"tfull {row[8]:.2f} publish {row[6]:.2f} | peer publish {t[cta + 1, st0, 6]:.2f}")
+
+# per-group readiness vs issue: does a consumer wait for publishers or for ring slots?
+P = (H + 31) // 32
+ngrp = 8 if ((H + 63) // 64) % 2 == 0 else (H + 63) // 64
+gunits = ((H + 63) // 64 // ngrp) * 64
+cta_pair = (torch.arange(grid) // 2) % P
+cta_dir = (torch.arange(grid) // 2) // P
+cta_grp = cta_pair * 32 // gunits
+slk, lag_full = [], []
+for st_ in range(4, T - 4):
+    for c in range(0, grid):
+        r, d = c % 2, int(cta_dir[c])
+        same = (tile == r) & (cta_dir == d)
+        koff = int(cta_pair[c]) % ngrp
+        for kq in range(ngrp):
+            kg = (kq + koff) % ngrp
+            pubs = t[same & (cta_grp == kg), st_ - 1, 6]
+            ready = pubs.max().item()
+            slk.append(t[c, st_, 16 + kq].item() - ready)
+            if r == 0:
+                lag_full.append(t[c, st_, 32 + kq].item() - t[c, st_, 16 + kq].item())
+slk = torch.tensor(slk, dtype=torch.float64)
+lag_full = torch.tensor(lag_full, dtype=torch.float64)
+print(f"group issue - group ready: quantiles {[round(v,2) for v in torch.quantile(slk, qs).tolist()]}")
+print(f"group issue -> stage full at MMA (leaders): quantiles {[round(v,2) for v in torch.quantile(lag_full, qs).tolist()]}")
+c = 0
+st_ = 20
+print("cta 0 step 20 issue times:", [round(t[c, st_, 16 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)])
+print("cta 0 step 20 full  times:", [round(t[c, st_, 32 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)])
+print("cta 0 step 20 tfull/publish:", round(t[c, st_, 8].item() - t[c, st_, 16].item(), 2), round(t[c, st_, 6].item() - t[c, st_, 16].item(), 2))
