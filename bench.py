@@ -1,11 +1,16 @@
 """Benchmark of the BASELINE.json metric on B200.
 
 Metric: "LSTM fwd+bwd target tokens/sec (6xBLSTM n=1000, T=60) at 1/2/4/8 B200
-vs CPU" (BASELINE.json).  One step = forward + backward (BPTT) of the
-Listing-1 encoder — 6 bidirectional LSTM layers, H = 1000, D0 = 620 (the
-embedding width, models.hpp:14), T = 60 — over one batch of synthetic
-sequences, plus, at N > 1, the data-parallel NCCL gradient all-reduce
-overlapped with BPTT.  tokens = valid (sequence, time) positions.
+vs CPU" (BASELINE.json), on configs[3] — the Listing-1 training step — as far
+as it is built: one step = forward + backward (BPTT) of the 6-layer
+bidirectional LSTM encoder (H = 1000, D0 = 620, the embedding width,
+models.hpp:14) and the 1-layer LSTM decoder (H = 1000, input [620-wide target
+embedding ‖ 2000-wide context], models.cpp:161), T_src = T_tgt = 60, then the
+fused global-norm clip + Adam step over all LSTM parameters, plus at N > 1 the
+data-parallel NCCL gradient all-reduce overlapped with BPTT.  Not built
+(SURVEY §8 f1/f2): the MLP attention and the output softmax — the decoder's
+context input is the encoder output at the same position (model.py).
+tokens = target (sequence, time) positions.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -48,9 +53,11 @@ def parse():
 
 
 def flops_per_token(L, D0, H):
-    """Algorithmic GEMM flops per token, fwd+bwd, both directions:
-    24 H (D + H) per layer-direction."""
-    return sum(2 * 24 * H * ((D0 if l == 0 else 2 * H) + H) for l in range(L))
+    """Algorithmic GEMM flops per target token, fwd+bwd: 24 H (D + H)
+    per layer-direction — the encoder's 2L layer-directions plus the decoder
+    layer (D = D0 + 2H); T_src = T_tgt."""
+    enc = sum(2 * 24 * H * ((D0 if l == 0 else 2 * H) + H) for l in range(L))
+    return enc + 24 * H * (D0 + 2 * H + H)
 
 
 # ---------------------------------------------------------------- clocks
@@ -141,13 +148,28 @@ def cpu_reference(args, steps=1):
     threads = max(1, min(os.cpu_count() or 1, 64))
     rng = np.random.default_rng(0)
     s = 1 / np.sqrt(H)
-    shapes = [D0, 2 * H]
+    shapes = [D0, 2 * H, D0 + 2 * H]  # encoder layer 0, encoder layers 1.., decoder
     params = {D: tuple(rng.uniform(-s, s, shp) for shp in ((D, 4 * H), (H, 4 * H), (4 * H,)))
               for D in shapes}
     xs = {D: rng.uniform(-1, 1, (1, T, D)) for D in shapes}
     lens = np.full(1, T, np.int32)
     dy = rng.uniform(-1, 1, (1, T, H))
     times = []
+    # optimizer step on the host: all LSTM parameters, timed on a slice
+    n_par = sum(2 * (D * 4 * H + H * 4 * H + 4 * H) for D in [D0] + [2 * H] * (L - 1))
+    n_par += (D0 + 2 * H) * 4 * H + H * 4 * H + 4 * H
+    k = 4_000_000
+    pa, ga = rng.standard_normal(k).astype(np.float32), rng.standard_normal(k).astype(np.float32)
+    ma, va = np.zeros(k, np.float32), np.zeros(k, np.float32)
+    t0 = time.perf_counter()
+    nrm = np.sqrt(np.dot(ga, ga))
+    ga *= min(1.0, 5.0 / nrm)
+    ma *= 0.9
+    ma += 0.1 * ga
+    va *= 0.999
+    va += 0.001 * ga * ga
+    pa -= 1e-3 * (ma / 0.1) / (np.sqrt(va / 0.001) + 1e-8)
+    adam_s = (time.perf_counter() - t0) * n_par / k
 
     def one(out):
         tt = {}
@@ -169,15 +191,17 @@ def cpu_reference(args, steps=1):
             t.start()
         for t in ths:
             t.join()
-        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] for r in res]
-        rates.append(threads * T / max(per_seq))
+        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] for r in res]
+        rates.append(threads * T / (max(per_seq) + adam_s))
     value = statistics.median(rates)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{threads} threads x 1 sequence (T={T}); per thread one fwd+bwd layer-direction "
-                      f"of each shape (D={D0}, D={2 * H}; H={H}) of the {L}xBLSTM stack, stack time = "
-                      f"2 t(D0) + {2 * (L - 1)} t(2H) (layers run sequentially in the reference); fp32 "
-                      f"reference build + scipy OpenBLAS 1 thread/tape; median of {steps}",
-            "seconds_per_step": max(per_seq)}
+                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}), step time = "
+                      f"2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) (layers run sequentially in the reference) "
+                      f"+ one clip+Adam step over {n_par / 1e6:.1f}M params ({adam_s:.2f} s, fp32 numpy "
+                      f"restatement timed on a 4M-element slice and scaled: the reference has no optimizer "
+                      f"code); fp32 reference build + scipy OpenBLAS 1 thread/tape; median of {steps}",
+            "seconds_per_step": max(per_seq) + adam_s}
 
 
 # ---------------------------------------------------------------- ours
@@ -185,17 +209,19 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_1805_05225_b200 import lstm
-    from paper_1805_05225_b200.encoder import BLSTMEncoder
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
-    enc = BLSTMEncoder(L, B, T, D0, H, args.precision, dev)
-    enc.init_uniform(seed=1)
+    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev)
+    model.init_uniform(seed=1)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
-    x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1
+    x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1      # source embeddings
+    emb = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1    # target embeddings
     lens = torch.full((B,), T, dtype=torch.int32, device=dev)
-    dy = torch.rand(B, T, 2 * H, device=dev, generator=g) * 2 - 1
+    dy = torch.rand(B, T, H, device=dev, generator=g) * 2 - 1      # dL/d(decoder output)
+    model.set_target_embeddings(emb)
     lib = lstm.lib()
     lib.sl_profile_enable.argtypes = [ctypes.c_int]
     lib.sl_launch_count.restype = ctypes.c_ulonglong
@@ -208,9 +234,7 @@ def run_ours(args, rank, world, local_rank):
     red = BucketAllReducer()  # layer-bucketed NCCL all-reduce, overlapped with BPTT
 
     def step(xin):
-        enc.forward(xin, lens)
-        enc.backward(dy, on_layer_grads=red)
-        red.wait()
+        model.step(xin, lens, dy, reducer=red, grad_scale=1.0 / world)
 
     for _ in range(args.warmup):
         step(x)
@@ -244,19 +268,23 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
+        eh = emb.cpu().pin_memory()
         lh = lens.cpu().pin_memory()
-        xd = torch.empty_like(x)
+        xd, ed = torch.empty_like(x), torch.empty_like(emb)
         ld = torch.empty_like(lens)
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
 
         def e2e_step():
             xd.copy_(xh, non_blocking=True)
+            ed.copy_(eh, non_blocking=True)
             ld.copy_(lh, non_blocking=True)
-            y = enc.forward(xd, ld)
+            model.set_target_embeddings(ed)
+            y = model.forward(xd, ld)
             loss = (y * dy).sum()  # L = sum(y . dy), so dL/dy = dy
             loss_h.copy_(loss, non_blocking=True)
-            enc.backward(dy, on_layer_grads=red)
+            model.backward(dy, on_grads=red)
             red.wait()
+            model.opt.step(model.grads, grad_scale=1.0 / world)
             torch.cuda.current_stream().synchronize()  # the host reads the step's loss
             return float(loss_h)
 
@@ -272,7 +300,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * B * T * args.steps / float(tt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": xh.numel() * 4 + lh.numel() * 4, "d2h_bytes_per_step": 4,
+               "h2d_bytes_per_step": (xh.numel() + eh.numel() + lh.numel()) * 4, "d2h_bytes_per_step": 4,
                "timing": "host wall clock, max over ranks"}
     return dict(ms=ms_max, phases=phases, launches=int(launches), clocks=clocks.summary(),
                 e2e=e2e)
@@ -284,8 +312,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
-    cfg = {"workload": f"config4-encoder: {L}xBLSTM H={H} D0={D0} T={T} fwd+bwd (+DP grad "
-                       f"all-reduce at N>1)", "global_batch": B * world, "batch_per_gpu": B,
+    cfg = {"workload": f"config4 LSTM training step: {L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
+                       f"H={H} (input {D0}+{2 * H}), T_src=T_tgt={T}, fwd+bwd + fused clip(5.0)+Adam "
+                       f"(+DP grad all-reduce at N>1); attention/softmax not built (SURVEY 8 f1/f2)",
+           "global_batch": B * world, "batch_per_gpu": B,
            "seq_len": T, "hidden": H, "input_dim": D0, "layers": L, "directions": 2,
            "parallelism": f"dp{world}", "seq_lens": "all = T",
            "l2": "working set (weights 590 MB fp32 + activations) far exceeds the 126 MB L2"}

@@ -128,12 +128,28 @@ int sl_lstm_cell_bwd(int32_t batch, int32_t input_dim, int32_t hidden, int32_t p
                      float* dx, float* dh0, float* dc0, float* dW, float* dR, float* db,
                      int accumulate, sl_stream_t stream);
 
+/* ---- optimizer (the training step around the hot path) --------
+ * One fused step over a flat fp32 parameter buffer of n elements:
+ *   g' = grad_scale * g;  clip: g' *= min(1, clip_norm / ||g'||_2)  (clip_norm <= 0: off)
+ *   m = b1 m + (1-b1) g';  v = b2 v + (1-b2) g'^2;
+ *   p -= lr * (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps)
+ * (reference SPEC.md:429-437 adam_step, global-norm clip 5.0 before Adam
+ * SPEC.md:484).  step >= 1 counts calls.  A non-finite gradient leaves p, m, v
+ * untouched and sets *nonfinite_out (device int32, may be NULL); *grad_norm_out
+ * (device float, may be NULL) receives ||grad_scale * g||_2 before clipping.
+ * `scratch` is a device buffer of sl_adam_scratch_size() bytes.  All buffers
+ * 16 B aligned, device-resident, asynchronous on `stream`. */
+size_t sl_adam_scratch_size(void);
+int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* v, int32_t step,
+                 float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,
+                 void* scratch, float* grad_norm_out, int32_t* nonfinite_out, sl_stream_t stream);
+
 /* ---- measurement hooks (used by bench.py; off by default) -------------------
  * When enabled, every internal kernel phase is bracketed by CUDA events on the
  * stream it is launched on; sl_profile_read folds them into per-phase totals
  * (name, calls, device ms, algorithmic flops / bytes).  Phase names:
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
- *   k5_cell_fwd, k5_cell_bwd */
+ *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam */
 typedef struct sl_profile_entry {
   char name[32];
   int32_t calls;

@@ -7,9 +7,11 @@
 // replacing the reference's per-step Eigen GEMMs and per-step GradBuffer
 // temporaries (tape.cpp:1103-1104, 1174-1215, 76-89).
 #include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
+#include "adam.h"
 #include "cell.h"
 #include "convert.h"
 #include "gemm.h"
@@ -246,6 +248,23 @@ extern "C" {
 int sl_version(void) { return 100; }
 
 int64_t sl_lstm_bf16_pitch(int32_t features) { return round_up((int64_t)features + 1, 64); }
+
+size_t sl_adam_scratch_size(void) { return sizeof(AdamScratch); }
+
+int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* v, int32_t step,
+                 float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,
+                 void* scratch, float* grad_norm_out, int32_t* nonfinite_out, sl_stream_t stream) {
+  return guarded([&] {
+    SL_REQUIRE(step >= 1, SL_ERR_INVALID_ARGUMENT, "adam_step: step counts from 1");
+    SL_REQUIRE(lr > 0.f && beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f,
+               SL_ERR_INVALID_ARGUMENT, "adam_step: hyperparameters out of range");
+    AdamHyper h{lr, beta1, beta2, eps, grad_scale, clip_norm,
+                (float)(1.0 / (1.0 - std::pow((double)beta1, step))),
+                (float)(1.0 / (1.0 - std::pow((double)beta2, step)))};
+    adam_step(n, params, grads, m, v, h, static_cast<AdamScratch*>(scratch), grad_norm_out, nonfinite_out,
+              reinterpret_cast<cudaStream_t>(stream));
+  });
+}
 
 const char* sl_last_error(void) { return g_last_error.c_str(); }
 

@@ -18,8 +18,16 @@ from . import lstm
 
 
 class BLSTMEncoder:
+    @staticmethod
+    def numel(num_layers: int, input_dim: int, hidden: int) -> int:
+        H = hidden
+        return sum(2 * (D * 4 * H + H * 4 * H + 4 * H)
+                   for D in [input_dim] + [2 * H] * (num_layers - 1))
+
     def __init__(self, num_layers: int, batch: int, time: int, input_dim: int, hidden: int,
-                 precision: str = "bf16", device=None):
+                 precision: str = "bf16", device=None, params=None, grads=None):
+        """params / grads: optional flat fp32 views (numel() elements) to live in,
+        e.g. slices of a whole model's buffers; by default the encoder owns them."""
         self.L, self.B, self.T, self.D0, self.H = num_layers, batch, time, input_dim, hidden
         self.precision = precision
         self.device = torch.device(device or "cuda")
@@ -28,8 +36,11 @@ class BLSTMEncoder:
         # flat parameter / gradient storage, one contiguous bucket per layer
         self.layer_numel = [2 * (D * 4 * H + H * 4 * H + 4 * H) for D in self.in_dims]
         total = sum(self.layer_numel)
-        self.params = torch.empty(total, dtype=torch.float32, device=self.device)
-        self.grads = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self.params = params if params is not None else torch.empty(total, dtype=torch.float32,
+                                                                     device=self.device)
+        self.grads = grads if grads is not None else torch.zeros(total, dtype=torch.float32,
+                                                                  device=self.device)
+        assert self.params.numel() == total and self.grads.numel() == total
         self.p_views, self.g_views, self.buckets = [], [], []
         off = 0
         for l, D in enumerate(self.in_dims):
@@ -65,6 +76,16 @@ class BLSTMEncoder:
         """Reference naming (compiler.cpp:488-492): enc{l}_{fw,bw}/{W,R,b}."""
         return [f"enc{l}_{d}/{n}" for l in range(self.L) for d in ("fw", "bw")
                 for n in ("W", "R", "b")]
+
+    def param_slices(self):
+        """(name, offset, numel) of every parameter inside the flat buffer."""
+        out, off = [], 0
+        for l, D in enumerate(self.in_dims):
+            for d in ("fw", "bw"):
+                for n, k in (("W", D * 4 * self.H), ("R", self.H * 4 * self.H), ("b", 4 * self.H)):
+                    out.append((f"enc{l}_{d}/{n}", off, k))
+                    off += k
+        return out
 
     def init_uniform(self, seed: int = 0):
         """W, R, b ~ U(+-1/sqrt(H)) (SURVEY §8(d) synthetic inputs)."""

@@ -1,0 +1,95 @@
+"""The config-4 training step around the LSTM hot path (BASELINE configs[3]):
+6-layer BLSTM encoder + 1-layer LSTM decoder, fwd + bwd, data-parallel
+gradient all-reduce, fused clip + Adam — the parts of the reference's
+Listing-1 step (models.cpp:17-184, compiler.cpp eval_layer / RnnCell) that are
+LSTM layers or the optimizer.  What is NOT built ("next"):
+the MLP attention and the output projection + softmax; the decoder input is
+[target embedding ‖ context] with the context stand-in c_t = encoder output at
+t (an identity alignment, T_src = T_tgt), so encoder gradients still flow
+through the decoder as they do through attention in the reference.  The
+decoder is run as one unidirectional LSTM layer over the teacher-forced
+inputs (the decoder cell has no recurrent input feeding without attention).
+
+All parameters (encoder then decoder) and their gradients live in ONE flat
+fp32 buffer each: the gradient all-reduce buckets are slices of it and the
+optimizer is one fused kernel over it.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import lstm
+from .encoder import BLSTMEncoder
+from .optim import Adam
+
+
+class Seq2SeqLSTM:
+    def __init__(self, enc_layers: int, batch: int, time: int, emb: int, hidden: int,
+                 precision: str = "bf16", device=None, lr: float = 1e-3, clip_norm: float = 5.0):
+        self.L, self.B, self.T, self.E, self.H = enc_layers, batch, time, emb, hidden
+        self.device = torch.device(device or "cuda")
+        H = hidden
+        self.Dd = emb + 2 * H  # decoder input [embedding ‖ context] (models.cpp:161: 620 + 2000)
+        n_enc = BLSTMEncoder.numel(enc_layers, emb, H)
+        n_dec = self.Dd * 4 * H + H * 4 * H + 4 * H
+        self.params = torch.empty(n_enc + n_dec, dtype=torch.float32, device=self.device)
+        self.grads = torch.zeros_like(self.params)
+        self.enc = BLSTMEncoder(enc_layers, batch, time, emb, H, precision, self.device,
+                                params=self.params[:n_enc], grads=self.grads[:n_enc])
+        off = n_enc
+        self.dec_p, self.dec_g = [], []
+        for shape in ((self.Dd, 4 * H), (H, 4 * H), (4 * H,)):
+            k = 1
+            for s in shape:
+                k *= s
+            self.dec_p.append(self.params[off:off + k].view(shape))
+            self.dec_g.append(self.grads[off:off + k].view(shape))
+            off += k
+        self.dec_bucket = self.grads[n_enc:]
+        bf16 = precision == "bf16"
+        self.dec = lstm.LSTMLayer(batch, time, self.Dd, H, 1, 1, precision, self.device, x_bf16=bf16)
+        if bf16:  # padded bf16 decoder input, ones column at Dd (seqloom_cuda.h SL_LAYER_X_BF16)
+            self.dec_in = torch.zeros(batch, time, lstm.bf16_pitch(self.Dd), dtype=torch.bfloat16,
+                                      device=self.device)
+            self.dec_in[:, :, self.Dd] = 1.0
+        else:
+            self.dec_in = torch.zeros(batch, time, self.Dd, dtype=torch.float32, device=self.device)
+        self.dec_y = torch.empty(batch, time, H, dtype=torch.float32, device=self.device)
+        self.dec_dx = torch.empty(batch, time, self.Dd, dtype=torch.float32, device=self.device)
+        self.enc_dy = torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
+        names = self.enc.param_slices() + [
+            (f"dec/{n}", n_enc + o, k) for n, o, k in
+            (("W", 0, self.Dd * 4 * H), ("R", self.Dd * 4 * H, H * 4 * H),
+             ("b", self.Dd * 4 * H + H * 4 * H, 4 * H))]
+        self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
+
+    def init_uniform(self, seed: int = 0):
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        s = 1.0 / self.H ** 0.5
+        self.params.uniform_(-s, s, generator=g)
+
+    def set_target_embeddings(self, emb: torch.Tensor):
+        """emb [B, T, E]: the teacher-forced target-side embeddings."""
+        self.dec_in[:, :, :self.E] = emb.to(self.dec_in.dtype)
+
+    def forward(self, x, seq_lens):
+        y = self.enc.forward(x, seq_lens)
+        self.dec_in[:, :, self.E:self.Dd] = y.to(self.dec_in.dtype)  # context stand-in c_t = enc_t
+        W, R, b = self.dec_p
+        self.dec.forward(self.dec_in, seq_lens, [W], [R], [b], y=self.dec_y)
+        return self.dec_y
+
+    def backward(self, dy_dec, on_grads=None):
+        W, R, b = self.dec_g
+        self.dec.backward(dy_dec, dx=self.dec_dx, dW=[W], dR=[R], db=[b])
+        if on_grads is not None:
+            on_grads(-1, self.dec_bucket)
+        self.enc_dy.copy_(self.dec_dx[:, :, self.E:])
+        return self.enc.backward(self.enc_dy, on_layer_grads=on_grads)
+
+    def step(self, x, seq_lens, dy_dec, reducer=None, grad_scale: float = 1.0):
+        self.forward(x, seq_lens)
+        self.backward(dy_dec, on_grads=reducer)
+        if reducer is not None:
+            reducer.wait()
+        self.opt.step(self.grads, grad_scale=grad_scale)

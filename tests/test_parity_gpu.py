@@ -379,3 +379,63 @@ def test_equal_lengths_tma_paths_match(cuda, L):
         ref = torch_ref.sequence(x, lens, Wk, Rk, bk, d, dy[:, :, k * H:(k + 1) * H])
         assert rel(outs[0]["y"][:, :, k * H:(k + 1) * H], ref["y"]) < TOL["bf16"]
         assert rel(outs[0]["dR"][k], ref["dR"]) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_seq2seq_training_step_matches_fp64(cuda, prec):
+    # the bench's config-4 step (model.py): encoder + decoder over
+    # [target embedding ‖ encoder output], gradients through both, then Adam
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    from oracle import adam_ref
+    Lyr, B, T, E, H = 2, 12, 7, 20, 24
+    m = Seq2SeqLSTM(Lyr, B, T, E, H, prec, lr=1e-2, clip_norm=5.0)
+    m.init_uniform(3)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1
+    emb = (torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1)
+    if prec == "bf16":
+        emb = emb.bfloat16().float()  # the decoder's bf16 input carries it exactly
+    lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
+    dy = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    m.set_target_embeddings(emb)
+    p0 = m.params.clone()
+    # fp64 reference of the same composition (with the pre-step parameters)
+    inp, saved = x.double(), []
+    for l in range(Lyr):
+        W, R, bb = [[v.double() for v in vs] for vs in m.enc._wrb(l)]
+        outs = [torch_ref.sequence(inp, lens, W[k], R[k], bb[k], (1, -1)[k]) for k in range(2)]
+        saved.append((inp, W, R, bb))
+        inp = torch.cat([o["y"] for o in outs], dim=2)
+    enc_out = inp
+    if prec == "bf16":  # the decoder input is stored in bf16 (both parts)
+        enc_out = enc_out.bfloat16().double()
+    dec_in = torch.cat([emb.double(), enc_out], dim=2)
+    Wd, Rd, bd = [t.double() for t in m.dec_p]
+    dref = torch_ref.sequence(dec_in, lens, Wd, Rd, bd, 1, dy.double())
+    m.step(x, lens, dy)
+    torch.cuda.synchronize()
+    m.opt.check_finite(m.grads)
+    tol = TOL[prec] * 2
+    assert rel(m.dec_y, dref["y"]) < tol
+    grads_ref = [dref["dW"], dref["dR"], dref["db"]]
+    gy = dref["dx"][:, :, E:]
+    enc_grads = []
+    for l in reversed(range(Lyr)):
+        inp_l, W, R, bb = saved[l]
+        gx, gl = 0, []
+        for k in range(2):
+            ref = torch_ref.sequence(inp_l, lens, W[k], R[k], bb[k], (1, -1)[k], gy[:, :, k * H:(k + 1) * H])
+            gl += [ref["dW"], ref["dR"], ref["db"]]
+            gx = gx + ref["dx"]
+        enc_grads = gl + enc_grads
+        gy = gx
+    flat_ref = torch.cat([t.reshape(-1) for t in enc_grads + grads_ref])
+    for (name, off, k) in m.opt.names:
+        assert rel(m.grads[off:off + k], flat_ref[off:off + k]) < tol, name
+    # and the optimizer applied clip + Adam to exactly these gradients
+    pr, _, _, _ = adam_ref.adam_step(p0.double().cpu().numpy(), m.grads.double().cpu().numpy(),
+                                     np.zeros(p0.numel()), np.zeros(p0.numel()), 1, lr=float(np.float32(1e-2)),
+                                     beta1=float(np.float32(0.9)), beta2=float(np.float32(0.999)),
+                                     eps=float(np.float32(1e-8)), clip_norm=5.0)
+    assert np.abs(m.params.double().cpu().numpy() - pr).max() < 1e-6
+
