@@ -368,6 +368,20 @@ def main():
                 "phases": {k: {"calls": v["calls"], "ms_per_call": v["ms"] / max(v["calls"], 1),
                                "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
                            for k, v in ph.items()}}
+    # recurrence phases: per-step latency against the W_h-from-SMEM bound the
+    # north star names (bytes of W_h resident across the SMs / (SMs x 128 B/clk x f_SM))
+    if roof is not None:
+        f_sm = (r["clocks"].get("sm_mhz") or 1965.0) * 1e6
+        rec = {}
+        for name, nd_, hid in (("k2_rec_fwd", 2, H), ("k3_rec_bwd", 2, H)):
+            e = ph.get(name)
+            if not e:
+                continue
+            us = e["ms"] / max(e["calls"], 1) * 1e3 / T
+            wh_bytes = nd_ * 4 * hid * hid * (2 if args.precision == "bf16" else 4)
+            bound = wh_bytes / (148 * 128 * f_sm) * 1e6
+            rec[name] = {"us_per_step": us, "wh_smem_bound_us": bound, "ratio_to_bound": us / bound}
+        roof["recurrence_per_step"] = rec
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),

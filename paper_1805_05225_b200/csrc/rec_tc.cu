@@ -380,9 +380,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 }
 
 // RT[(cl*C + r)*N + g*UC + j][kk] = R[r*Kc + kk][g*H + cl*UC + j]  (bf16, zero outside)
-// A 32x32 shared-memory transpose: coalesced reads along R's gate columns,
-// coalesced writes along RT's K; grid = (ceil(P*N/32), ceil(Kp/32)) tiles over
-// (packed row, k), 32-bit index math only.
+// Generic (K-split) form: a 32x32 shared-memory transpose over (packed row, k).
 __global__ void pack_rt_kernel(const float* __restrict__ R, int H, int C, int U, int P, int Kc,
                                __nv_bfloat16* __restrict__ RT) {
   __shared__ float tile[32][33];
@@ -390,7 +388,6 @@ __global__ void pack_rt_kernel(const float* __restrict__ R, int H, int C, int U,
   const int Kp = Kc * C;
   const int row0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
-  // read: rows (packed) x k from R[k][col(row)], threads along the packed row
   for (int i = ty; i < 32; i += 8) {
     const int k = k0 + i, rowi = row0 + tx;
     float v = 0.f;
@@ -403,13 +400,55 @@ __global__ void pack_rt_kernel(const float* __restrict__ R, int H, int C, int U,
     tile[i][tx] = v;
   }
   __syncthreads();
-  // write: RT[rowi][kk] with kk along threads; the CTA's K-slice is r
   for (int i = ty; i < 32; i += 8) {
     const int rowi = row0 + i, k = k0 + tx;
     if (rowi >= P * N || k >= Kp) continue;
     const int r = (rowi / N) % C;
     if (k / Kc != r) continue;
     RT[(size_t)rowi * Kc + (k - r * Kc)] = __float2bfloat16_rn(tile[tx][i]);
+  }
+}
+
+// No K split (C = 1): the rows (cta, g, j) of one (cta, gate) are UC consecutive
+// columns of R, so each block transposes a [64 k x UC columns] tile: float4
+// loads along the columns, 16 B bf16 stores along k.  grid = (P * 4, Kp / 64).
+template <int UC>
+__global__ void __launch_bounds__(256) pack_rt_c1_kernel(const float* __restrict__ R, int H, int Kp,
+                                                         __nv_bfloat16* __restrict__ RT) {
+  __shared__ float tile[64][UC + 1];
+  const int cg = blockIdx.x;            // (cta, gate)
+  const int cta = cg / 4, g = cg % 4;
+  const int k0 = blockIdx.y * 64;
+  const int c0 = g * H + cta * UC;      // first R column of the tile
+  const int units_here = min(UC, H - cta * UC);
+  const bool vec = (H % 4) == 0 && units_here == UC;
+  constexpr int CV = UC / 4;            // float4 per tile row
+  for (int e = threadIdx.x; e < 64 * CV; e += 256) {
+    const int i = e / CV, cq = (e % CV) * 4;
+    const int k = k0 + i;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (k < H) {
+      const float* src = R + (size_t)k * 4 * H + c0 + cq;
+      if (vec) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+        v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (cq + u < units_here) v[u] = __ldg(src + u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tile[i][cq + u] = v[u];
+  }
+  __syncthreads();
+  // 8 k per thread-store: UC rows x 8 chunks of 8 bf16
+  for (int e = threadIdx.x; e < UC * 8; e += 256) {
+    const int j = e / 8, kq = (e % 8) * 8;
+    float f[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) f[u] = tile[kq + u][j];
+    *reinterpret_cast<uint4*>(RT + ((size_t)cta * 4 * UC + g * UC + j) * Kp + k0 + kq) = pack8_bf16(f);
   }
 }
 
@@ -484,8 +523,14 @@ size_t tc_rec_pack_elems(const TcFwdShape& sh) {
 void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
                  cudaStream_t stream) {
   const int Kc = sh.Kp / sh.C;
-  const dim3 grid((unsigned)ceil_div((int64_t)sh.P * 4 * sh.C * sh.U, 32), (unsigned)ceil_div(sh.Kp, 32));
-  pack_rt_kernel<<<grid, 256, 0, stream>>>(R, H, sh.C, sh.U, sh.P, Kc, RT);
+  if (sh.C == 1 && (sh.U == 16 || sh.U == 32) && sh.Kp % 64 == 0) {
+    const dim3 grid((unsigned)sh.P * 4, (unsigned)(sh.Kp / 64));
+    if (sh.U == 32) pack_rt_c1_kernel<32><<<grid, 256, 0, stream>>>(R, H, sh.Kp, RT);
+    else pack_rt_c1_kernel<16><<<grid, 256, 0, stream>>>(R, H, sh.Kp, RT);
+  } else {
+    const dim3 grid((unsigned)ceil_div((int64_t)sh.P * 4 * sh.C * sh.U, 32), (unsigned)ceil_div(sh.Kp, 32));
+    pack_rt_kernel<<<grid, 256, 0, stream>>>(R, H, sh.C, sh.U, sh.P, Kc, RT);
+  }
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }

@@ -367,9 +367,25 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   const bool live = n < C * U && unit < H;
   const float* src = R + (size_t)unit * 4 * H + (size_t)r * Kc;
   __nv_bfloat16* dst = RB + (size_t)rowi * Kc;
-  for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
-    const float v = (live && r * Kc + kk < 4 * H) ? __ldg(src + kk) : 0.f;
-    dst[kk] = __float2bfloat16_rn(v);
+  const int valid = live ? max(0, min(Kc, 4 * H - r * Kc)) : 0;
+  // 4 columns per thread: float4 loads when the row start is 16 B aligned, 8 B bf16 stores
+  const bool vec = (((uintptr_t)src) & 15) == 0 && (Kc % 4) == 0;
+  for (int kk = threadIdx.x * 4; kk < Kc; kk += blockDim.x * 4) {
+    float v[4];
+    if (vec && kk + 4 <= valid) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(src + kk));
+      v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = kk + u < valid ? __ldg(src + kk + u) : 0.f;
+    }
+    if (kk + 4 <= Kc) {
+      const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+      *reinterpret_cast<uint2*>(dst + kk) =
+          make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
+    } else {
+      for (int u = 0; u < 4 && kk + u < Kc; ++u) dst[kk + u] = __float2bfloat16_rn(v[u]);
+    }
   }
 }
 
