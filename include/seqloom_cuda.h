@@ -134,7 +134,10 @@ int sl_lstm_cell_bwd(int32_t batch, int32_t input_dim, int32_t hidden, int32_t p
  *   m = b1 m + (1-b1) g';  v = b2 v + (1-b2) g'^2;
  *   p -= lr * (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps)
  * (reference SPEC.md:429-437 adam_step, global-norm clip 5.0 before Adam
- * SPEC.md:484).  step >= 1 counts calls.  A non-finite gradient leaves p, m, v
+ * SPEC.md:484).  step >= 1 is the step number; step == 0 uses the counter kept
+ * in `scratch` (+1 per successful step) so a captured CUDA graph replays real
+ * Adam steps.  `scratch` must be zero-filled once before its first use.  A
+ * non-finite gradient leaves p, m, v
  * untouched and sets *nonfinite_out (device int32, may be NULL); *grad_norm_out
  * (device float, may be NULL) receives ||grad_scale * g||_2 before clipping.
  * `scratch` is a device buffer of sl_adam_scratch_size() bytes.  All buffers

@@ -10,6 +10,8 @@
 // (already all-reduced) gradient, (2) the element-wise update, which reads
 // the clip scale computed from (1) on the device — no host round trip.
 // Bytes per parameter: 4 (pass 1) + 16 read + 12 written (pass 2).
+#include <cstddef>
+
 #include "adam.h"
 #include "profile.h"
 
@@ -65,7 +67,11 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, c
     if (norm > h.clip_norm) scale *= h.clip_norm / norm;
   }
   const float b1 = h.beta1, b2 = h.beta2, c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
-  const float inv_bc1 = h.inv_bc1, inv_bc2 = h.inv_bc2, lr = h.lr, eps = h.eps;
+  // the step number lives on the device so a captured CUDA graph replays real steps
+  const int t = h.step > 0 ? h.step : sc->t + 1;
+  const float inv_bc1 = (float)(1.0 / (1.0 - pow((double)h.beta1, (double)t)));
+  const float inv_bc2 = (float)(1.0 / (1.0 - pow((double)h.beta2, (double)t)));
+  const float lr = h.lr, eps = h.eps;
   auto upd = [&](float& pp, float gg, float& mm, float& vv) {
     gg *= scale;
     mm = fmaf(b1, mm, c1 * gg);
@@ -90,9 +96,12 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, c
     upd(p[i], g[i], m[i], v[i]);
 }
 
-__global__ void adam_report_kernel(const AdamScratch* sc, float grad_scale, float* norm_out, int32_t* bad_out) {
+// after the update (stream order): report, and advance the device step counter
+__global__ void adam_report_kernel(AdamScratch* sc, int32_t step, float grad_scale, float* norm_out,
+                                   int32_t* bad_out) {
   if (norm_out) *norm_out = (float)sqrt(sc->sumsq) * grad_scale;
   if (bad_out) *bad_out = (int32_t)sc->nonfinite;
+  if (!sc->nonfinite) sc->t = step > 0 ? step : sc->t + 1;
 }
 
 int sms() {
@@ -113,7 +122,7 @@ void adam_step(int64_t n, float* params, const float* grads, float* m, float* v,
              "adam_step: null buffer");
   SL_REQUIRE(((uintptr_t)params | (uintptr_t)grads | (uintptr_t)m | (uintptr_t)v) % 16 == 0,
              SL_ERR_INVALID_ARGUMENT, "adam_step: buffers need 16 B alignment");
-  SL_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(AdamScratch), stream));
+  SL_CUDA_TRY(cudaMemsetAsync(scratch, 0, offsetof(AdamScratch, t), stream));  // keep the step counter
   const int64_t n4 = (n + 3) / 4;
   const int grid = (int)std::min<int64_t>(std::max<int64_t>(1, (n4 + kThreads - 1) / kThreads), 4LL * sms());
   {
@@ -128,11 +137,9 @@ void adam_step(int64_t n, float* params, const float* grads, float* m, float* v,
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
   }
-  if (norm_out || nonfinite_out) {
-    adam_report_kernel<<<1, 1, 0, stream>>>(scratch, h.grad_scale, norm_out, nonfinite_out);
-    SL_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
+  adam_report_kernel<<<1, 1, 0, stream>>>(scratch, h.step, h.grad_scale, norm_out, nonfinite_out);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace sl

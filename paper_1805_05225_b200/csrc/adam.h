@@ -8,13 +8,13 @@ struct AdamHyper {
   float lr, beta1, beta2, eps;
   float grad_scale;  // applied to the gradient first (e.g. 1/N after a sum all-reduce)
   float clip_norm;   // <= 0: no clipping
-  float inv_bc1, inv_bc2;  // 1 / (1 - beta^t), computed in double on the host
+  int32_t step;      // > 0: this step number; 0: the device counter in the scratch + 1
 };
 
-struct AdamScratch {  // device scratch, zeroed per step
-  double sumsq;
-  unsigned nonfinite;
-  unsigned pad;
+struct AdamScratch {  // device scratch
+  double sumsq;        // zeroed per step
+  unsigned nonfinite;  // zeroed per step
+  int32_t t;           // persistent step counter (zero when the scratch is created)
 };
 
 void adam_step(int64_t n, float* params, const float* grads, float* m, float* v, const AdamHyper& h,

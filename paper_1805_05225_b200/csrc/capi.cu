@@ -255,12 +255,10 @@ int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* 
                  float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,
                  void* scratch, float* grad_norm_out, int32_t* nonfinite_out, sl_stream_t stream) {
   return guarded([&] {
-    SL_REQUIRE(step >= 1, SL_ERR_INVALID_ARGUMENT, "adam_step: step counts from 1");
+    SL_REQUIRE(step >= 0, SL_ERR_INVALID_ARGUMENT, "adam_step: step counts from 1 (0 = device counter)");
     SL_REQUIRE(lr > 0.f && beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f,
                SL_ERR_INVALID_ARGUMENT, "adam_step: hyperparameters out of range");
-    AdamHyper h{lr, beta1, beta2, eps, grad_scale, clip_norm,
-                (float)(1.0 / (1.0 - std::pow((double)beta1, step))),
-                (float)(1.0 / (1.0 - std::pow((double)beta2, step)))};
+    AdamHyper h{lr, beta1, beta2, eps, grad_scale, clip_norm, step};
     adam_step(n, params, grads, m, v, h, static_cast<AdamScratch*>(scratch), grad_norm_out, nonfinite_out,
               reinterpret_cast<cudaStream_t>(stream));
   });

@@ -26,7 +26,9 @@ class Adam:
         self.t = 0
         L = lstm.lib()
         L.sl_adam_scratch_size.restype = ctypes.c_size_t
-        self.scratch = torch.empty(L.sl_adam_scratch_size(), dtype=torch.uint8, device=params.device)
+        # the scratch also carries the device-side step counter (step == 0 below),
+        # so the step can be captured in a CUDA graph and replayed
+        self.scratch = torch.zeros(L.sl_adam_scratch_size(), dtype=torch.uint8, device=params.device)
         self.grad_norm = torch.zeros(1, dtype=torch.float32, device=params.device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=params.device)
 
@@ -39,7 +41,7 @@ class Adam:
         L.sl_adam_step.argtypes = [ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int32, f, f, f, f, f, f, vp, vp,
                                    vp, vp]
         lstm._check(L.sl_adam_step(self.params.numel(), lstm._p(self.params), lstm._p(grads), lstm._p(self.m),
-                                   lstm._p(self.v), self.t, self.lr if lr is None else lr, self.betas[0],
+                                   lstm._p(self.v), 0, self.lr if lr is None else lr, self.betas[0],
                                    self.betas[1], self.eps, grad_scale, self.clip_norm, lstm._p(self.scratch),
                                    lstm._p(self.grad_norm), lstm._p(self.nonfinite), lstm._stream()))
 

@@ -439,3 +439,37 @@ def test_seq2seq_training_step_matches_fp64(cuda, prec):
                                      eps=float(np.float32(1e-8)), clip_norm=5.0)
     assert np.abs(m.params.double().cpu().numpy() - pr).max() < 1e-6
 
+
+
+def test_cuda_graph_replay_matches_eager_steps(cuda):
+    # the bench times the training step captured as a CUDA graph: replays must
+    # reproduce eager steps bit for bit (incl. Adam's device-side step counter)
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    Lyr, B, T, E, H = 2, 40, 9, 24, 64
+
+    def make():
+        m = Seq2SeqLSTM(Lyr, B, T, E, H, "bf16", lr=1e-2)
+        m.init_uniform(8)
+        return m
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1
+    emb = torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1
+    lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
+    dy = torch.rand(B, T, H, device="cuda", generator=g) * 2 - 1
+    a, b = make(), make()
+    for m in (a, b):
+        m.set_target_embeddings(emb)
+    for _ in range(3):
+        a.step(x, lens, dy)
+    b.step(x, lens, dy)  # warm-up outside the capture (allocations, attributes)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        b.step(x, lens, dy)
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params)
+    assert torch.equal(a.opt.m, b.opt.m) and torch.equal(a.opt.v, b.opt.v)
