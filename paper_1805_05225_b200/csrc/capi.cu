@@ -190,7 +190,7 @@ struct BwdWork {
   float* dzbuf[2] = {nullptr, nullptr};   // fp32 path
   float* gcbuf[2] = {nullptr, nullptr};   // fp32 path
   __nv_bfloat16* dzb = nullptr;           // bf16 path: DZ of both directions [B*T, nd*G4p]
-  __nv_bfloat16* dzring[2] = {nullptr, nullptr};  // bf16 path: DZ ring [2][B][Kz]
+  __nv_bfloat16* dzring[2] = {nullptr, nullptr};  // bf16 path: DZ ring (rec_tc.h dz_ring_off)
   __nv_bfloat16* rb[2] = {nullptr, nullptr};      // bf16 path: packed R row slices
   unsigned* bar = nullptr;
 };
@@ -205,7 +205,7 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
     SL_REQUIRE(sh.C > 0, SL_ERR_UNSUPPORTED, "bf16 recurrence: hidden size too large for one launch");
     w.dzb = c.take<__nv_bfloat16>((size_t)d.BT() * pd.Gc);
     for (int k = 0; k < d.nd; ++k) {
-      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * d.B * sh.Kz);
+      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
       w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(sh));
     }
   } else {
@@ -468,10 +468,12 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
       a.bar = w.bar;
       a.trace = g_rec_trace;
       a.trace_cta = g_rec_trace_cta;
+      a.debug_flags = g_rec_debug_flags;
       if (pd.G4p != G) SL_CUDA_TRY(cudaMemsetAsync(w.dzb, 0, sizeof(__nv_bfloat16) * M * pd.Gc, stream));
       for (int k = 0; k < d.nd; ++k) {
         tc_rec_bwd_pack(R[k], d.H, sh, w.rb[k], stream);
-        SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * d.B * a.Kz, stream));
+        SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * a.Kz,
+                                    stream));
         a.dirsign[k] = dir_sign(L, k);
         a.gates[k] = rv.gatesb[k];
         a.cprev[k] = rv.cprevb[k];

@@ -55,6 +55,17 @@ struct TcRecFwdArgs {
                     // 4 = no step-counter waits (wrong results)
 };
 
+// DZ ring of the BPTT kernel (written by its epilogues, TMA-read as the MMA A
+// operand): [2 slots][Kz / 8][Bp][8] bf16, Bp = round_up(B, 8) — 16 B K-chunks
+// of all rows back to back (the SWIZZLE_NONE K-major core-matrix layout), so a
+// warp's 32 rows of one 8-unit slice are 512 contiguous bytes.  Gate g of unit
+// u is column g * dz_ring_hq(H) + u.
+__host__ __device__ inline int dz_ring_hq(int H) { return (H + 7) / 8 * 8; }
+__host__ __device__ inline int dz_ring_bp(int B) { return (B + 7) / 8 * 8; }
+__host__ __device__ inline size_t dz_ring_off(int slot, int row, int col, int Bp, int Kz) {
+  return (((size_t)slot * (Kz / 8) + col / 8) * Bp + row) * 8 + col % 8;
+}
+
 struct TcRecBwdArgs {
   int B, T, H, nd, U, P;
   int b0;      // first batch row of this launch (set internally)
@@ -69,12 +80,14 @@ struct TcRecBwdArgs {
   int64_t dy_ld;
   const float* dh_last;  // [nd, B, H] or null
   const float* dc_last;
-  __nv_bfloat16* dzring[2];  // [2][B][Kz] bf16, zeroed
+  __nv_bfloat16* dzring[2];  // dz_ring_off layout, 2 * dz_ring_bp(B) * Kz bf16, zeroed
   __nv_bfloat16* dzcat;      // out: DZ bf16 [B*T, dzcat_ld], dir d at col d*dz_dir_off
   int64_t dzcat_ld, dz_dir_off;
   unsigned* bar;  // zeroed step counters
   unsigned long long* trace;
   int trace_cta;
+  int debug_flags;  // experiments only: 8 = skip the DZ copy for K4, 16 = skip dy / saved-activation
+                    // loads (wrong results)
 };
 
 // K-split partition of the BPTT kernel: clusters of C CTAs, each finalizing U

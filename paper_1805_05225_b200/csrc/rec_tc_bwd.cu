@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
-            tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, a.b0 + mt * 128,
-                        r * (Kc / 64) + kg * a.kb, slot);
+            tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
+                        (r * (Kc / 64) + kg * a.kb) * 8, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
@@ -169,11 +169,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             if (kq == ngrp - 1) SL_TRACE(mt == 0 ? 2 : 5);
             for (int j = 0; j < a.kb; ++j) {
             const int kc = kg * a.kb + j;
+            // A: the stage holds [kb * 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk
             const uint32_t sa = base + r_bytes + st * stage_bytes + j * kTile;
             const uint32_t sb = base + (uint32_t)kc * NB * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              tc::mma_f16(tmem + mt * NB, tc::make_sdesc(sa + k * 32, 0, 1024),
+              tc::mma_f16(tmem + mt * NB, tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128),
                           tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | j | k) != 0);
             }
             tc::mma_commit(&empty_bar[st]);
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       const size_t pos = (size_t)row * T + t;
       Bf16Vec<UT> gv[4], cp;
       float dyv[UT];
-      if (active) {  // prefetch this step's saved activations and upstream grad
+      if (active && !(a.debug_flags & 16)) {  // prefetch this step's saved activations and upstream grad
         const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
 #pragma unroll
         for (int g = 0; g < 4; ++g) gv[g].load(gates + gate_save_off(s, g, row, a.B, H, ut0), nu, true);
@@ -288,15 +289,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             for (int u = 0; u < UT; ++u) dh[u] += __bfloat162float(src[u]);
           }
         }
-        __syncwarp();
-        if (lane == 0)  // tell every sender its slot in my buffer is free again
-          for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
+        // the senders learn that their slots are free from ONE arrive per peer
+        // after the tile's publish barrier below (every reader is done by then)
       }
+      if (tr0) a.trace[it * 16 + 13] = gtimer();
 
       Bf16Vec<UT> dzp[4];  // DZ_s packed: the ring copy now, the K4 copy after publishing
       if (valid_row) {
-        __nv_bfloat16* zn = zr + ((size_t)((it + 1) & 1) * a.B + row) * a.Kz + ut0;
+        const int hq8 = dz_ring_hq(H);
         if (active) {
           float dz[4 * UT];
           const bool last = (s == len - 1);
@@ -319,21 +319,26 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           }
 #pragma unroll
           for (int g = 0; g < 4; ++g) dzp[g].pack(dz + g * UT);
+          if (tr0) a.trace[it * 16 + 14] = gtimer();
         } else {
 #pragma unroll
           for (int g = 0; g < 4; ++g) dzp[g].zero();
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) dzp[g].store(zn + g * H, nu);
+        for (int g = 0; g < 4; ++g)
+          dzp[g].store(zr + dz_ring_off((it + 1) & 1, row, g * hq8 + ut0, dz_ring_bp(a.B), a.Kz), nu);
       }
       if (tr0) a.trace[it * 16 + 11] = gtimer();
       named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
         red_release_gpu(ctr + mt, 1u);
+        if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
+          for (int pi = 1; pi < C; ++pi)
+            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), kEpiTile);
         if (a.trace && blockIdx.x == a.trace_cta) a.trace[it * 16 + 6 + mt] = gtimer();
       }
-      if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
+      if (valid_row && !(a.debug_flags & 8)) {  // the K4 operand copy is off the cross-CTA critical path
         __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
 #pragma unroll
         for (int g = 0; g < 4; ++g) dzp[g].store(zc + g * H, nu);
@@ -365,8 +370,17 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   const int cl = cta / C, r = cta % C;
   const int unit = cl * C * U + n;
   const bool live = n < C * U && unit < H;
-  const float* src = R + (size_t)unit * 4 * H + (size_t)r * Kc;
   __nv_bfloat16* dst = RB + (size_t)rowi * Kc;
+  const int hq8 = dz_ring_hq(H);
+  if (hq8 != H) {  // gate blocks padded to a multiple of 8 columns in the DZ ring
+    for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
+      const int col = r * Kc + kk, g = col / hq8, u = col % hq8;
+      const float v = (live && g < 4 && u < H) ? __ldg(R + (size_t)unit * 4 * H + (size_t)g * H + u) : 0.f;
+      dst[kk] = __float2bfloat16_rn(v);
+    }
+    return;
+  }
+  const float* src = R + (size_t)unit * 4 * H + (size_t)r * Kc;
   const int valid = live ? max(0, min(Kc, 4 * H - r * Kc)) : 0;
   // 4 columns per thread: float4 loads when the row start is 16 B aligned, 8 B bf16 stores
   const bool vec = (((uintptr_t)src) & 15) == 0 && (Kc % 4) == 0;
@@ -434,7 +448,7 @@ TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms) {
     const int usable = C == 4 ? std::min(sms, 128) : sms;
     for (int U : {4, 8, 16}) {
       const int P = (int)ceil_div(H, (int64_t)C * U) * C;
-      const int Kz = (int)round_up(4 * (int64_t)H, 64 * C);
+      const int Kz = (int)round_up(4 * (int64_t)dz_ring_hq(H), 64 * C);
       if ((int64_t)P * nd <= usable && bwd_smem(C, U, Kz / C, 2) <= kSmemMax)
         return TcBwdShape{C, U, P, Kz};
     }
@@ -470,10 +484,13 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
     tr[k] = tmap(RB[k], 2, rd, rs, rb);
     a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
-    cuuint64_t zd[4] = {64, (cuuint64_t)a.B, (cuuint64_t)a.Kz / 64, 2};
-    cuuint64_t zs[3] = {(cuuint64_t)a.Kz * 2, 128, (cuuint64_t)a.Kz * 2 * a.B};
-    cuuint32_t zb[4] = {64, 128, (cuuint32_t)a.kb, 1};
-    tz[k] = tmap(a.dzring[k], 4, zd, zs, zb);
+    // the DZ ring in its interleaved layout, as {8 rows x 8 k (128 contiguous B),
+    // 8-row groups, K-chunks, slot}: 128 B TMA rows, box = 128 rows x kb*64 K
+    const int Bp = dz_ring_bp(a.B);
+    cuuint64_t zd[4] = {64, (cuuint64_t)Bp / 8, (cuuint64_t)a.Kz / 8, 2};
+    cuuint64_t zs[3] = {128, (cuuint64_t)Bp * 16, (cuuint64_t)a.Kz / 8 * Bp * 16};
+    cuuint32_t zb[4] = {64, 16, (cuuint32_t)a.kb * 8, 1};
+    tz[k] = tmap(a.dzring[k], 4, zd, zs, zb, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   a.stages = 0;
   for (int st = kStages; st >= 2 && !a.stages; --st)

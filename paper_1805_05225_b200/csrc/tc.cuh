@@ -206,6 +206,19 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_byte
   return d;
 }
 
+// Shared-memory matrix descriptor, SWIZZLE_NONE K-major ("interleaved") layout:
+// 8-row x 16 B core matrices stored contiguously (128 B); LBO = byte distance
+// between core matrices adjacent along K, SBO = along M/N.
+__device__ __forceinline__ uint64_t make_sdesc_noswz(uint32_t saddr, uint32_t lbo_bytes,
+                                                     uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo_bytes & 0x3FFFF) >> 4) << 16;
+  d |= (uint64_t)((sbo_bytes & 0x3FFFF) >> 4) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor for kind::f16 / kind::tf32 with fp32 accumulate.
 // ab_fmt: 1 = BF16, 2 = TF32.  a_mn / b_mn: operand is MN-major.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int ab_fmt, bool a_mn, bool b_mn) {

@@ -55,6 +55,7 @@ if os.environ.get("SL_TRACE"):
 if os.environ.get("SL_TRACE_BWD"):
     import ctypes
     L = lstm.lib()
+    L.sl_debug_set_flags(int(os.environ.get("SL_FLAGS", "0")))
     for cta in [int(c) for c in os.environ["SL_TRACE_BWD"].split(",")]:
         buf = torch.zeros(T * 16, dtype=torch.int64, device="cuda")
         layer.forward(x, lens, W, R, b)

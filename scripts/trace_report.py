@@ -15,3 +15,6 @@ def report(buf, T, name):
               f"{med(rel[:,8]-rel[:,2]):.2f}) sends {med(rel[:,9]-rel[:,8]):.2f} "
               f"recv-wait {med(rel[:,10]-rel[:,9]):.2f} math+stores {med(rel[:,11]-rel[:,10]):.2f} "
               f"sync+pub {med(rel[:,6]-rel[:,11]):.2f}")
+    if t[2:-1, 13].min() > 0 and t[2:-1, 14].min() > 0:
+        print(f"   math detail: recv-read {med(rel[:,13]-rel[:,10]):.2f} compute {med(rel[:,14]-rel[:,13]):.2f} "
+              f"ring-store {med(rel[:,11]-rel[:,14]):.2f}")
