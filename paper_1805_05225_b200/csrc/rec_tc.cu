@@ -514,7 +514,7 @@ TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms) {
   return TcFwdShape{0, 0, 0, 0};
 }
 
-size_t tc_rec_hbuf_elems(int B, const TcFwdShape& sh) { return (size_t)2 * B * sh.Kp; }
+size_t tc_rec_hbuf_elems(int B, const TcFwdShape& sh) { return (size_t)2 * dz_ring_bp(B) * sh.Kp; }
 
 size_t tc_rec_pack_elems(const TcFwdShape& sh) {
   return (size_t)sh.P * 4 * sh.C * sh.U * (sh.Kp / sh.C);

@@ -46,7 +46,8 @@ struct TcRecFwdArgs {
   __nv_bfloat16* cprev[2];    // saved c_{s-1}, step-major (cprev_save_off)
   __nv_bfloat16* hprev[2];    // saved h_{s-1} bf16 [B*T, hprev_ld] (dR GEMM operand)
   int64_t hprev_ld;
-  __nv_bfloat16* hbuf[2];     // ring [2][B][Kp] bf16, zeroed (tc_rec_hbuf_elems)
+  __nv_bfloat16* hbuf[2];     // h ring, zeroed (tc_rec_hbuf_elems): [2][B][Kp] (rec_tc.cu kernels) or
+                              // the interleaved dz_ring_off layout with K = Kp (pair kernel)
   unsigned* bar;              // zeroed step counters, 2 per batch chunk
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
             tma_load_4d_pair(sH + st * stage_bytes, tmH, mapa(tc::smem_u32(&full_bar[st]), 0), 0,
-                             a.b0 + r * 128, kg * a.kb, s & 1);
+                             (a.b0 + r * 128) / 8, kg * a.kb * 8, s & 1);
           }
           advance();
           ++done;
@@ -228,8 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!(a.debug_flags & 1))
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_f16_pair(tmem, tc::make_sdesc(sa + k * 32, 0, 1024), tc::make_sdesc(sb + k * 32, 0, 1024),
-                             idesc, (kq | j | k) != 0);
+                mma_f16_pair(tmem, tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128),
+                             tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | j | k) != 0);
           }
           mma_commit_pair(&empty_bar[st]);
           if (++st == a.stages) {
@@ -331,7 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // only h_s is on the cross-CTA critical path
-        store_bf16<kUT>(hb + ((size_t)((s + 1) & 1) * a.B + row) * a.Kp + ut0, hst, nu);
+        // h ring in the interleaved layout (rec_tc.h dz_ring_off): 8-unit chunks of
+        // consecutive rows are contiguous, so each warp store covers 512 B
+#pragma unroll
+        for (int c = 0; c < kUT; c += 8)
+          store_bf16<8>(hb + dz_ring_off((s + 1) & 1, row, ut0 + c, dz_ring_bp(a.B), a.Kp), hst + c,
+                        max(0, min(8, nu - c)));
       }
       if (tr0) trace[s * tstride + 11] = gtimer();
       named_sync(1, kEpi);
@@ -340,6 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         red_release_gpu(ctr + u0 / gunits, 1u);  // my K group's counter
         TR(6);
       }
+      // take the next step's x W tile out of its ring slot now (before the
+      // saves): a slot held through the saves starves this CTA's next h
+      // stream of a stage, and a late CTA would fall further behind each step
+      if (s + 1 < Tmax) load_xw(s + 1, xv);
       if (valid_row && !(a.debug_flags & 10)) {
         if (active) {
           if (save) {
@@ -373,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (save) store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
         }
       }
-      if (s + 1 < Tmax) load_xw(s + 1, xv);
     }
     if (valid_row) {  // positions beyond the longest sequence, final states
       float zero[kUT];
@@ -438,10 +446,13 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
     cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)kNHalf};
     tr[k] = tmap(RT[k], 2, rd, rs, rb);
-    cuuint64_t hd[4] = {64, (cuuint64_t)a.B, (cuuint64_t)a.Kp / 64, 2};
-    cuuint64_t hs[3] = {(cuuint64_t)a.Kp * 2, 128, (cuuint64_t)a.Kp * 2 * a.B};
-    cuuint32_t hbx[4] = {64, 128, (cuuint32_t)a.kb, 1};
-    th[k] = tmap(a.hbuf[k], 4, hd, hs, hbx);
+    // interleaved h ring {8 rows x 8 k, 8-row groups, K chunks of 8, slot}: 128 B
+    // TMA rows; a box is 128 rows x kb*64 K in the SWIZZLE_NONE core-matrix layout
+    const int Bp = dz_ring_bp(a.B);
+    cuuint64_t hd[4] = {64, (cuuint64_t)Bp / 8, (cuuint64_t)a.Kp / 8, 2};
+    cuuint64_t hs[3] = {128, (cuuint64_t)Bp * 16, (cuuint64_t)a.Kp / 8 * Bp * 16};
+    cuuint32_t hbx[4] = {64, 16, (cuuint32_t)a.kb * 8, 1};
+    th[k] = tmap(a.hbuf[k], 4, hd, hs, hbx, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   a.stages = 0;
   for (int st = kMaxStages; st >= 2 && !a.stages; --st)

@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 #include "rec_tc_common.cuh"
@@ -97,7 +98,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64, 1)
   tc::fence_before_sync();
   __syncthreads();
   cluster_sync();
-  if (threadIdx.x == 0) out[blockIdx.x] = gtimer() - t0;
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    out[blockIdx.x] = ((gtimer() - t0) << 8) | smid;  // time << 8 | SM id
+  }
   if (warp == 1) tmem_dealloc_pair<128>(tmem_sh);
 }
 
@@ -125,9 +130,20 @@ int main() {
       }
       std::vector<unsigned long long> h(ctas);
       cudaMemcpy(h.data(), out, ctas * 8, cudaMemcpyDeviceToHost);
-      unsigned long long worst = 0;
-      for (auto v : h) worst = v > worst ? v : worst;
+      unsigned long long worst = 0, best = ~0ull;
+      std::vector<std::pair<unsigned long long, int>> per;
+      for (auto v : h) {
+        const unsigned long long tt = v >> 8;
+        worst = tt > worst ? tt : worst;
+        best = tt < best ? tt : best;
+        per.push_back({tt, (int)(v & 255)});
+      }
+      std::sort(per.begin(), per.end());
       const double us_step = worst / 1e3 / steps;
+      printf("   per-CTA us/step: min %.2f median %.2f max %.2f; slowest SMs:", best / 1e3 / steps,
+             per[per.size() / 2].first / 1e3 / steps, us_step);
+      for (int i = (int)per.size() - 1; i >= (int)per.size() - 6; --i) printf(" %d", per[i].second);
+      printf("\n");
       printf("%s release=%s%s : %.2f us per 256 KB step, %.1f GB/s per CTA\n", pair_mode ? "pair" : "solo",
              commit ? "tcgen05.commit" : "mbarrier.arrive", do_mma ? (variant == 4 ? " +MMA(nonzero)" : " +MMA") : "",
              us_step, 256.0 * 1024 / us_step / 1e3);

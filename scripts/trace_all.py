@@ -119,3 +119,8 @@ st_ = 20
 print("cta 0 step 20 issue times:", [round(t[c, st_, 16 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)])
 print("cta 0 step 20 full  times:", [round(t[c, st_, 32 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)])
 print("cta 0 step 20 tfull/publish:", round(t[c, st_, 8].item() - t[c, st_, 16].item(), 2), round(t[c, st_, 6].item() - t[c, st_, 16].item(), 2))
+sl_ = int(slow[0])
+for c in (sl_, sl_ + 1, 0, 1):
+    print(f"cta {c} step 20 issue:", [round(t[c, st_, 16 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)],
+          "| full:", [round(t[c, st_, 32 + k].item() - t[c, st_, 16].item(), 2) for k in range(ngrp)] if c % 2 == 0 else "")
+    print(f"   first issue at {t[c, st_, 16].item() - t[0, st_, 16].item():+.2f} vs cta 0; tfull {t[c, st_, 8].item() - t[c, st_, 16].item():.2f} publish {t[c, st_, 6].item() - t[c, st_, 16].item():.2f}")
