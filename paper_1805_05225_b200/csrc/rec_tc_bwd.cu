@@ -40,7 +40,12 @@ uint32_t bwd_smem(int C, int U, int Kc, int stages) {  // stages of two 16 KB ch
 // C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
 // U   hidden units each CTA finalizes (the cluster owns C*U units)
 // MT  128-row batch tiles per launch
-template <int C, int U, int MT, int SPLIT = (U >= 8 ? 2 : 1), int UT = U / SPLIT>
+// SPLIT epilogue threads per batch row (UT = U / SPLIT units each).  (One
+// thread per row for U = 16 — 32 B segments, half the requests — measured
+// slower: the per-thread math and stores then sit on the critical path.)
+constexpr int bwd_split(int U) { return U >= 8 ? 2 : 1; }
+
+template <int C, int U, int MT, int SPLIT = bwd_split(U), int UT = U / SPLIT>
 __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     rec_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
                       const __grid_constant__ CUtensorMap tmR1,
@@ -115,6 +120,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
   unsigned* ctr = a.bar + d * 2;
+  // debug trace: one CTA (trace_cta >= 0, [T][16]) or every CTA (trace_cta < 0, [grid][T][16])
+  unsigned long long* trace =
+      (a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta))
+          ? a.trace + (a.trace_cta < 0 ? (size_t)blockIdx.x * a.T * 16 : 0) : nullptr;
   const int ngrp = nkc / a.kb;  // TMA boxes per tile
   const int kc_off = cta % ngrp;
 
@@ -126,8 +135,20 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       int st = 0;
       uint32_t ph = 0;
       const int nst = a.stages;
+      // the saved activations the epilogue reads this iteration: this CTA's
+      // 16-unit chunk of the 4 gates and of c_{s-1}, all rows of the launch
+      const int pf_u = (u0 / 16) * 16;
+      const int pf_rows = min(a.B - a.b0, MT * 128);
+      const bool pf = a.gates[d] != nullptr && u0 < a.H && !(a.debug_flags & 32);
       for (int s = 0; s < Tmax; ++s) {  // s = iteration (processing step Tmax-1-s)
         const int slot = s & 1;          // ring slot holding DZ of the previous iteration
+        if (pf) {
+          const int ps = Tmax - 1 - s;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            prefetch_l2(a.gates[d] + gate_save_off(ps, g, a.b0, a.B, a.H, pf_u), pf_rows * 32);
+          prefetch_l2(a.cprev[d] + cprev_save_off(ps, a.b0, a.B, a.H, pf_u), pf_rows * 32);
+        }
         for (int mt = 0; mt < MT; ++mt) {
           if (s > 0) {
             const unsigned target = (unsigned)a.P * (unsigned)s;
@@ -135,7 +156,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             }
             tc::fence_proxy_async_global();
           }
-          SL_TRACE(mt == 0 ? 0 : 3);
+          if (trace) trace[s * 16 + (mt == 0 ? 0 : 3)] = gtimer();
           for (int kq = 0; kq < ngrp; ++kq) {
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
@@ -165,8 +186,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            if (kq == 0) SL_TRACE(mt == 0 ? 1 : 4);
-            if (kq == ngrp - 1) SL_TRACE(mt == 0 ? 2 : 5);
+            if (kq == 0 && trace) trace[s * 16 + (mt == 0 ? 1 : 4)] = gtimer();
+            if (kq == ngrp - 1 && trace) trace[s * 16 + (mt == 0 ? 2 : 5)] = gtimer();
             for (int j = 0; j < a.kb; ++j) {
             const int kc = kg * a.kb + j;
             // A: the stage holds [kb * 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk
@@ -226,11 +247,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                      vec && (a.dy_ld % 4) == 0);
       }
       float dh[UT];
-      const bool tr0 = a.trace && blockIdx.x == a.trace_cta && e == 0 && lane == 0;
-      if (tr0) a.trace[it * 16 + 12] = gtimer();
+      const bool tr0 = trace && e == 0 && lane == 0;
+      if (tr0) trace[it * 16 + 12] = gtimer();
       tc::mbar_wait(&tfull_bar[mt], it & 1);
       tc::fence_after_sync();
-      if (tr0) a.trace[it * 16 + 8] = gtimer();
+      if (tr0) trace[it * 16 + 8] = gtimer();
       if constexpr (C > 1) {
         // reduce-scatter of the K-split partials: send each peer the columns of
         // the units it finalizes (coalesced: a warp writes 32 consecutive rows)
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           }
         }
       }
-      if (tr0) a.trace[it * 16 + 9] = gtimer();
+      if (tr0) trace[it * 16 + 9] = gtimer();
       tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         mbar_wait_cluster(&recv_full[mt], use & 1);
         if ((e % (4 * SPLIT)) == 0 && lane == 0)  // phase `use` is complete: arm the next use
           tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
-        if (tr0) a.trace[it * 16 + 10] = gtimer();
+        if (tr0) trace[it * 16 + 10] = gtimer();
 #pragma unroll 1
         for (int sl = 0; sl < C - 1; ++sl) {
           const __nv_bfloat16* src = recv + (((size_t)mt * (C - 1) + sl) * 128 + rl) * U + lo;
@@ -292,7 +313,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         // the senders learn that their slots are free from ONE arrive per peer
         // after the tile's publish barrier below (every reader is done by then)
       }
-      if (tr0) a.trace[it * 16 + 13] = gtimer();
+      if (tr0) trace[it * 16 + 13] = gtimer();
 
       Bf16Vec<UT> dzp[4];  // DZ_s packed: the ring copy now, the K4 copy after publishing
       if (valid_row) {
@@ -300,35 +321,54 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         if (active) {
           float dz[4 * UT];
           const bool last = (s == len - 1);
+          if (last && (a.dh_last || a.dc_last)) {  // the final-state adjoints enter at s = len - 1
 #pragma unroll
-          for (int u = 0; u < UT; ++u) {
-            float gh = dh[u] + dyv[u];
-            float gc = gcar[u];
-            if (last && a.dh_last) gh += a.dh_last[((size_t)d * a.B + row) * H + ut0 + u];
-            if (last && a.dc_last) gc += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
-            const float gi = gv[0][u], gf = gv[1][u], gg = gv[2][u], go = gv[3][u];
-            const float cpu = cp[u];
-            const float tcv = tc::tanh_approx(fmaf(gf, cpu, gi * gg));
-            const float d_o = gh * tcv;                          // tape.cpp:1161
-            const float dcn = gc + gh * go * (1.f - tcv * tcv);  // tape.cpp:1162
-            gcar[u] = dcn * gf;                                  // tape.cpp:1166
-            dz[u] = dcn * gg * gi * (1.f - gi);                  // tape.cpp:1167
-            dz[UT + u] = dcn * cpu * gf * (1.f - gf);            // tape.cpp:1168
-            dz[2 * UT + u] = dcn * gi * (1.f - gg * gg);         // tape.cpp:1169
-            dz[3 * UT + u] = d_o * go * (1.f - go);              // tape.cpp:1170
+            for (int u = 0; u < UT; ++u) {
+              if (a.dh_last) dh[u] += a.dh_last[((size_t)d * a.B + row) * H + ut0 + u];
+              if (a.dc_last) gcar[u] += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
+            }
+          }
+          const float2 one = f2s(1.f), mone = f2s(-1.f);
+#pragma unroll
+          for (int u = 0; u < UT; u += 2) {  // two units per paired-fp32 instruction
+            const float2 gh = add2(f2(dh[u], dh[u + 1]), f2(dyv[u], dyv[u + 1]));
+            const float2 gc = f2(gcar[u], gcar[u + 1]);
+            const float2 gi = bf16x2_f2(gv[0].w[u / 2]), gf = bf16x2_f2(gv[1].w[u / 2]);
+            const float2 gg = bf16x2_f2(gv[2].w[u / 2]), go = bf16x2_f2(gv[3].w[u / 2]);
+            const float2 cpu = bf16x2_f2(cp.w[u / 2]);
+            const float2 tcv = tanh2(fma2(gf, cpu, mul2(gi, gg)));
+            const float2 d_o = mul2(gh, tcv);                                      // tape.cpp:1161
+            const float2 dcn = fma2(mul2(gh, go), fma2(mul2(mone, tcv), tcv, one), gc);  // tape.cpp:1162
+            const float2 cg = mul2(dcn, gf);                                       // tape.cpp:1166
+            gcar[u] = cg.x, gcar[u + 1] = cg.y;
+            const float2 zi = mul2(mul2(dcn, gg), mul2(gi, fma2(mone, gi, one)));    // tape.cpp:1167
+            const float2 zf = mul2(mul2(dcn, cpu), mul2(gf, fma2(mone, gf, one)));   // tape.cpp:1168
+            const float2 zg = mul2(mul2(dcn, gi), fma2(mul2(mone, gg), gg, one));    // tape.cpp:1169
+            const float2 zo = mul2(mul2(d_o, go), fma2(mone, go, one));              // tape.cpp:1170
+            dz[u] = zi.x, dz[u + 1] = zi.y;
+            dz[UT + u] = zf.x, dz[UT + u + 1] = zf.y;
+            dz[2 * UT + u] = zg.x, dz[2 * UT + u + 1] = zg.y;
+            dz[3 * UT + u] = zo.x, dz[3 * UT + u + 1] = zo.y;
           }
 #pragma unroll
           for (int g = 0; g < 4; ++g) dzp[g].pack(dz + g * UT);
-          if (tr0) a.trace[it * 16 + 14] = gtimer();
+          if (tr0) trace[it * 16 + 14] = gtimer();
         } else {
 #pragma unroll
           for (int g = 0; g < 4; ++g) dzp[g].zero();
         }
 #pragma unroll
         for (int g = 0; g < 4; ++g)
-          dzp[g].store(zr + dz_ring_off((it + 1) & 1, row, g * hq8 + ut0, dz_ring_bp(a.B), a.Kz), nu);
+#pragma unroll
+          for (int c = 0; c < UT; c += 8) {  // the ring's 8-unit chunks are Bp * 16 B apart
+            Bf16Vec<(UT < 8 ? UT : 8)> part;
+#pragma unroll
+            for (int w = 0; w < (UT < 8 ? UT : 8) / 2; ++w) part.w[w] = dzp[g].w[c / 2 + w];
+            part.store(zr + dz_ring_off((it + 1) & 1, row, g * hq8 + ut0 + c, dz_ring_bp(a.B), a.Kz),
+                       max(0, min(UT < 8 ? UT : 8, nu - c)));
+          }
       }
-      if (tr0) a.trace[it * 16 + 11] = gtimer();
+      if (tr0) trace[it * 16 + 11] = gtimer();
       named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
@@ -336,7 +376,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
           for (int pi = 1; pi < C; ++pi)
             mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), kEpiTile);
-        if (a.trace && blockIdx.x == a.trace_cta) a.trace[it * 16 + 6 + mt] = gtimer();
+        if (trace) trace[it * 16 + 6 + mt] = gtimer();
       }
       if (valid_row && !(a.debug_flags & 8)) {  // the K4 operand copy is off the cross-CTA critical path
         __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
@@ -413,7 +453,7 @@ void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   TcRecBwdArgs copy = a;
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[a.nd > 1 ? 1 : 0];
-  constexpr int kSplit = U >= 8 ? 2 : 1;
+  constexpr int kSplit = bwd_split(U);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.P * a.nd);
   cfg.blockDim = dim3(64 + 128 * MT * kSplit);

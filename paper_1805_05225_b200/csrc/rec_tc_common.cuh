@@ -444,6 +444,30 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 
 
+// ---- paired fp32 math (sm_100 FFMA2 / FMUL2 / FADD2: two lanes per instruction)
+// The recurrence epilogues are instruction-issue bound (16 warps on 4
+// schedulers do the per-unit gate math at once), so units are processed in pairs.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 tanh2(float2 x) { return f2(tc::tanh_approx(x.x), tc::tanh_approx(x.y)); }
+// sigmoid(x) = 0.5 tanh(x / 2) + 0.5
+__device__ __forceinline__ float2 sigmoid2(float2 x) {
+  return fma2(f2s(0.5f), tanh2(mul2(f2s(0.5f), x)), f2s(0.5f));
+}
+// the two bf16 of one packed word as (low, high) floats
+__device__ __forceinline__ float2 bf16x2_f2(uint32_t w) {
+  return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+// Bulk L2 prefetch by the TMA engine (no registers, no LSU requests): pulls a
+// contiguous range into L2 ahead of the epilogue's loads.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ---- CTA-pair (cta_group::2) primitives
 // TMA into this CTA's smem whose completion is signalled on the barrier at
 // shared::cluster address `bar_cl` (the pair leader's)

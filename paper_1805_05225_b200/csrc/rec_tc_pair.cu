@@ -316,18 +316,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (valid_row && !(a.debug_flags & 2)) {
         if (active) {
 #pragma unroll
-          for (int u = 0; u < kUT; ++u) {
-            const float gi = tc::sigmoid_approx(z[u] + xv[0][u]);
-            const float gf = tc::sigmoid_approx(z[kUT + u] + xv[1][u]);
-            const float gg = tc::tanh_approx(z[2 * kUT + u] + xv[2][u]);
-            const float go = tc::sigmoid_approx(z[3 * kUT + u] + xv[3][u]);
-            z[u] = gi;
-            z[kUT + u] = gf;
-            z[2 * kUT + u] = gg;
-            z[3 * kUT + u] = go;
-            const float cn = fmaf(gf, cst[u], gi * gg);
-            cst[u] = cn;
-            hst[u] = go * tc::tanh_approx(cn);
+          for (int u = 0; u < kUT; u += 2) {  // two units per paired-fp32 instruction
+            const float2 gi = sigmoid2(add2(f2(z[u], z[u + 1]), bf16x2_f2(xv[0].w[u / 2])));
+            const float2 gf = sigmoid2(add2(f2(z[kUT + u], z[kUT + u + 1]), bf16x2_f2(xv[1].w[u / 2])));
+            const float2 gg = tanh2(add2(f2(z[2 * kUT + u], z[2 * kUT + u + 1]), bf16x2_f2(xv[2].w[u / 2])));
+            const float2 go = sigmoid2(add2(f2(z[3 * kUT + u], z[3 * kUT + u + 1]), bf16x2_f2(xv[3].w[u / 2])));
+            z[u] = gi.x, z[u + 1] = gi.y;
+            z[kUT + u] = gf.x, z[kUT + u + 1] = gf.y;
+            z[2 * kUT + u] = gg.x, z[2 * kUT + u + 1] = gg.y;
+            z[3 * kUT + u] = go.x, z[3 * kUT + u + 1] = go.y;
+            const float2 cn = fma2(gf, f2(cst[u], cst[u + 1]), mul2(gi, gg));  // c = f c + i g
+            cst[u] = cn.x, cst[u + 1] = cn.y;
+            const float2 h = mul2(go, tanh2(cn));                             // h = o tanh(c)
+            hst[u] = h.x, hst[u + 1] = h.y;
           }
         }
         // only h_s is on the cross-CTA critical path
