@@ -95,6 +95,7 @@ struct TcRecBwdArgs {
 // units, P CTAs per direction, Kz = gate columns padded to 64*C.
 struct TcBwdShape {
   int C, U, P, Kz;
+  int pair = 0;  // 1: CTA-pair kernel (rec_tc_bwd_pair.cu), clusters of 8 = 4 pairs x 128 units
 };
 TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms);  // C == 0: unsupported
 size_t tc_rec_bwd_pack_elems(const TcBwdShape& sh);
@@ -102,6 +103,10 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
                      cudaStream_t stream);
 void rec_bwd_tc(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* const* RB,
                 cudaStream_t stream);
+bool tc_rec_bwd_pair_fits(int H, int nd, int sms, int B, TcBwdShape* out);
+size_t tc_rec_bwd_pair_pack_elems(const TcBwdShape& sh);
+void tc_rec_bwd_pair_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream);
+void rec_bwd_pair(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* const* RB, cudaStream_t stream);
 
 // K-split partition of the forward kernel: clusters of C CTAs, each finalizing
 // U units (the cluster owns C*U units, MMA N = 4*C*U), P CTAs per direction,

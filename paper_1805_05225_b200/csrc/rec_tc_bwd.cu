@@ -482,6 +482,8 @@ void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs
 }  // namespace
 
 TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms) {
+  TcBwdShape pair_shape;
+  if (tc_rec_bwd_pair_fits(H, nd, sms, 0, &pair_shape)) return pair_shape;
   // Prefer 4-CTA clusters (4x less DZ per CTA); most CTAs that fit a cluster
   // grid (~128 SMs usable by 4-CTA clusters on 148 SMs) and shared memory.
   for (int C : {4, 2, 1}) {
@@ -497,11 +499,16 @@ TcBwdShape tc_rec_bwd_shape(int H, int nd, int sms) {
 }
 
 size_t tc_rec_bwd_pack_elems(const TcBwdShape& sh) {
+  if (sh.pair) return tc_rec_bwd_pair_pack_elems(sh);
   return (size_t)sh.P * nb_of(sh.C, sh.U) * (sh.Kz / sh.C);
 }
 
 void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB,
                      cudaStream_t stream) {
+  if (sh.pair) {
+    tc_rec_bwd_pair_pack(R, H, sh, RB, stream);
+    return;
+  }
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
   pack_rb_kernel<<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
@@ -511,6 +518,10 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
 
 void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* const* RB,
                 cudaStream_t stream) {
+  if (sh.pair) {
+    rec_bwd_pair(a0, sh, RB, stream);
+    return;
+  }
   TcRecBwdArgs a = a0;
   a.U = sh.U;
   a.P = sh.P;

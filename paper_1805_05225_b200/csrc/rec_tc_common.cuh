@@ -500,11 +500,12 @@ __device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t a, uint64
 }
 // arrive once on the barrier at this smem offset in BOTH CTAs of the pair when
 // the issuing thread's prior MMAs complete
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+// (mask = the pair's two cluster ranks; 0x3 for a 2-CTA cluster)
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask = 0x3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
       "[%0], %1;" ::"r"(tc::smem_u32(bar)),
-      "h"((uint16_t)0x3)
+      "h"(mask)
       : "memory");
 }
 template <uint32_t kCols>
