@@ -47,18 +47,19 @@ def parse():
     ap.add_argument("--hidden", type=int, default=1000)
     ap.add_argument("--input", type=int, default=620)
     ap.add_argument("--time", type=int, default=60)
+    ap.add_argument("--vocab", type=int, default=20000, help="target vocabulary (output softmax); 0 = none")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     return ap.parse_args()
 
 
-def flops_per_token(L, D0, H):
+def flops_per_token(L, D0, H, V=0):
     """Algorithmic GEMM flops per target token, fwd+bwd: 24 H (D + H)
     per layer-direction — the encoder's 2L layer-directions plus the decoder
-    layer (D = D0 + 2H); T_src = T_tgt."""
+    layer (D = D0 + 2H); T_src = T_tgt — plus 6 H V for the output layer."""
     enc = sum(2 * 24 * H * ((D0 if l == 0 else 2 * H) + H) for l in range(L))
-    return enc + 24 * H * (D0 + 2 * H + H)
+    return enc + 24 * H * (D0 + 2 * H + H) + 6 * H * V
 
 
 # ---------------------------------------------------------------- clocks
@@ -159,6 +160,7 @@ def cpu_reference(args, steps=1):
     # optimizer step on the host: all LSTM parameters, timed on a slice
     n_par = sum(2 * (D * 4 * H + H * 4 * H + 4 * H) for D in [D0] + [2 * H] * (L - 1))
     n_par += (D0 + 2 * H) * 4 * H + H * 4 * H + 4 * H
+    n_par += H * args.vocab + args.vocab  # output softmax layer
     k = 4_000_000
     pa, ga = rng.standard_normal(k).astype(np.float32), rng.standard_normal(k).astype(np.float32)
     ma, va = np.zeros(k, np.float32), np.zeros(k, np.float32)
@@ -172,8 +174,19 @@ def cpu_reference(args, steps=1):
     pa -= 1e-3 * (ma / 0.1) / (np.sqrt(va / 0.001) + 1e-8)
     adam_s = (time.perf_counter() - t0) * n_par / k
 
+    V = args.vocab
+    if V and kind == "reference":
+        Wo = rng.uniform(-s, s, (H, V))
+        bo = rng.uniform(-s, s, V)
+        xo = rng.uniform(-1, 1, (1, T, H))
+        tgo = rng.integers(0, V, (1, T)).astype(np.int32)
+
     def one(out):
         tt = {}
+        if V and kind == "reference":  # the output softmax layer + CE, fwd + bwd
+            t0 = time.perf_counter()
+            ref.output_ce(xo, lens, tgo, Wo, bo, 0.1)
+            tt["out"] = time.perf_counter() - t0
         for D in shapes:
             W, R, b = params[D]
             t0 = time.perf_counter()
@@ -192,13 +205,14 @@ def cpu_reference(args, steps=1):
             t.start()
         for t in ths:
             t.join()
-        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] for r in res]
+        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] + r.get("out", 0.0) for r in res]
         rates.append(threads * T / (max(per_seq) + adam_s))
     value = statistics.median(rates)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{threads} threads x 1 sequence (T={T}); per thread one fwd+bwd layer-direction "
-                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}), step time = "
-                      f"2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) (layers run sequentially in the reference) "
+                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}) and the output "
+                      f"softmax + CE (V={V}), step time = 2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) + t(out) "
+                      f"(layers run sequentially in the reference) "
                       f"+ one clip+Adam step over {n_par / 1e6:.1f}M params ({adam_s:.2f} s, fp32 numpy "
                       f"restatement timed on a 4M-element slice and scaled: the reference has no optimizer "
                       f"code); fp32 reference build + scipy OpenBLAS 1 thread/tape; median of {steps}",
@@ -215,13 +229,16 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
-    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev)
+    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev, vocab=args.vocab)
     model.init_uniform(seed=1)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
     x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1      # source embeddings
     emb = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1    # target embeddings
     lens = torch.full((B,), T, dtype=torch.int32, device=dev)
-    dy = torch.rand(B, T, H, device=dev, generator=g) * 2 - 1      # dL/d(decoder output)
+    if args.vocab:  # target ids for the output layer's CE loss
+        dy = torch.randint(0, args.vocab, (B, T), device=dev, generator=g, dtype=torch.int32)
+    else:
+        dy = torch.rand(B, T, H, device=dev, generator=g) * 2 - 1  # dL/d(decoder output)
     model.set_target_embeddings(emb)
     lib = lstm.lib()
     lib.sl_profile_enable.argtypes = [ctypes.c_int]
@@ -309,12 +326,16 @@ def run_ours(args, rank, world, local_rank):
             ed.copy_(eh, non_blocking=True)
             ld.copy_(lh, non_blocking=True)
             model.set_target_embeddings(ed)
-            y = model.forward(xd, ld)
-            loss = (y * dy).sum()  # L = sum(y . dy), so dL/dy = dy
-            loss_h.copy_(loss, non_blocking=True)
-            model.backward(dy, on_grads=red)
-            red.wait()
-            model.opt.step(model.grads, grad_scale=1.0 / world)
+            if args.vocab:  # the real loss: output softmax + label-smoothed CE
+                loss = model.step(xd, ld, dy, reducer=red, grad_scale=1.0 / world)
+                loss_h.copy_(loss, non_blocking=True)
+            else:
+                y = model.forward(xd, ld)
+                loss = (y * dy).sum()  # L = sum(y . dy), so dL/dy = dy
+                loss_h.copy_(loss, non_blocking=True)
+                model.backward(dy, on_grads=red)
+                red.wait()
+                model.opt.step(model.grads, grad_scale=1.0 / world)
             torch.cuda.current_stream().synchronize()  # the host reads the step's loss
             return float(loss_h)
 
@@ -331,6 +352,7 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * B * T * args.steps / float(tt.item()), "unit": UNIT,
                "h2d_bytes_per_step": (xh.numel() + eh.numel() + lh.numel()) * 4, "d2h_bytes_per_step": 4,
+               "note": "x, target embeddings and lens copied in; the scalar loss copied out",
                "timing": "host wall clock, max over ranks"}
     return dict(ms=ms_max, phases=phases, launches=int(launches), clocks=clocks.summary(),
                 e2e=e2e, eager_ms=eager_ms / args.steps, graph=graph is not None)
@@ -342,9 +364,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
-    cfg = {"workload": f"config4 LSTM training step: {L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
-                       f"H={H} (input {D0}+{2 * H}), T_src=T_tgt={T}, fwd+bwd + fused clip(5.0)+Adam "
-                       f"(+DP grad all-reduce at N>1); attention/softmax not built (SURVEY 8 f1/f2)",
+    out_s = (f" + output softmax V={args.vocab} with label-smoothed CE (eps 0.1)" if args.vocab else "")
+    cfg = {"workload": f"config4 training step: {L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
+                       f"H={H} (input {D0}+{2 * H}){out_s}, T_src=T_tgt={T}, fwd+bwd + fused "
+                       f"clip(5.0)+Adam (+DP grad all-reduce at N>1); MLP attention not built (SURVEY 8 f1)",
+           "vocab": args.vocab,
            "global_batch": B * world, "batch_per_gpu": B,
            "seq_len": T, "hidden": H, "input_dim": D0, "layers": L, "directions": 2,
            "parallelism": f"dp{world}", "seq_lens": "all = T",
@@ -419,7 +443,7 @@ def main():
            "config": dict(cfg, cuda_graph=r["graph"], eager_ms_per_step=r["eager_ms"]),
            "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
            "roofline": roof,
-           "algorithmic_tflops": flops_per_token(L, D0, H) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}
+           "algorithmic_tflops": flops_per_token(L, D0, H, args.vocab) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             out["cpu_baseline"] = cpu_reference(args, steps=1)

@@ -147,12 +147,30 @@ int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* 
                  float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,
                  void* scratch, float* grad_norm_out, int32_t* nonfinite_out, sl_stream_t stream);
 
+/* ---- output layer + loss ---------------------------------------
+ * The decoder's Softmax layer and its training loss in one call: logits =
+ * x W + b (reference compiler.cpp:651-663), log_softmax (tape.cpp:879-924),
+ * ce_label_smoothing with `epsilon` averaged over the valid (t < seq_lens[b])
+ * positions (tape.cpp:1224-1298), and the gradients of that mean loss:
+ *   x [B, T, D] fp32, targets [B, T] int32 in [0, V), W [D, V], b [V];
+ *   *loss (device float); dx [B, T, D], dW [D, V], db [V] may be NULL;
+ *   *bad_target (device int32) is set when a valid position's id is out of
+ *   range (the reference raises IndexError naming the layer).
+ * bf16 tensor-core GEMMs with fp32 accumulation; the fp32 logits are never
+ * written to HBM (bf16 logits + fused online-softmax statistics). */
+size_t sl_output_ce_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab);
+int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, const float* x,
+                 const int32_t* targets, const int32_t* seq_lens, const float* W, const float* b,
+                 float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
+                 void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream);
+
 /* ---- measurement hooks (used by bench.py; off by default) -------------------
  * When enabled, every internal kernel phase is bracketed by CUDA events on the
  * stream it is launched on; sl_profile_read folds them into per-phase totals
  * (name, calls, device ms, algorithmic flops / bytes).  Phase names:
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
- *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam */
+ *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam, k7_logits_gemm, k7_softmax_ce,
+ *   k7_dx_gemm, k7_dw_gemm */
 typedef struct sl_profile_entry {
   char name[32];
   int32_t calls;

@@ -125,6 +125,9 @@ class Reference:
         L.ref_lstm_step.argtypes = [ctypes.c_int] * 3 + [_d] * 16 + [c, ctypes.c_int]
         L.ref_blstm_stack.argtypes = ([ctypes.c_int] * 5 + [_d, _i, _P(_d), _d, _d, _d, _P(_d)] +
                                       [c, ctypes.c_int])
+        if hasattr(L, "ref_output_ce"):
+            L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
+                                        [c, ctypes.c_int])
         self.bits = 8 * L.ref_real_bytes()
 
     @staticmethod
@@ -185,6 +188,47 @@ class Reference:
         if grads is not None:
             grads = [tuple(grads[l * 6:(l + 1) * 6]) for l in range(L)]
         return y, dx, grads
+
+
+def _output_ce(self, x, lens, targets, W, b, eps):
+    """The reference's Softmax layer + ce_label_smoothing: (loss, dx, dW, db)."""
+    B, T, D = x.shape
+    V = W.shape[1]
+    x, W, b = map(_f64, (x, W, b))
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    targets = np.ascontiguousarray(targets, dtype=np.int32)
+    loss = np.zeros(1)
+    dx, dW, db = np.zeros((B, T, D)), np.zeros((D, V)), np.zeros(V)
+    err = ctypes.create_string_buffer(512)
+    rc = self.lib.ref_output_ce(B, T, D, V, _ptr(x), _ptr(lens, _i), _ptr(targets, _i), _ptr(W), _ptr(b),
+                                float(eps), _ptr(loss), _ptr(dx), _ptr(dW), _ptr(db), err, 512)
+    self._check(rc, err)
+    return float(loss[0]), dx, dW, db
+
+
+Reference.output_ce = _output_ce
+
+
+def output_ce_np(x, lens, targets, W, b, eps):
+    """fp64 numpy restatement of the same (compiler.cpp:651-663, tape.cpp:879-924,
+    1224-1298): loss = mean over valid rows of lse - (1-eps) z_y - eps/V sum_j z_j."""
+    x, W, b = (np.asarray(a, np.float64) for a in (x, W, b))
+    B, T, D = x.shape
+    V = W.shape[1]
+    z = x.reshape(B * T, D) @ W + b                     # matmul + add (tape.cpp:327-356)
+    m = z.max(axis=1, keepdims=True)
+    lse = m + np.log(np.exp(z - m).sum(axis=1, keepdims=True))
+    lp = z - lse                                        # log_softmax (tape.cpp:889-897)
+    valid = (np.arange(T)[None, :] < np.asarray(lens)[:, None]).reshape(-1)
+    y = np.asarray(targets).reshape(-1)
+    n = int(valid.sum())
+    rows = np.nonzero(valid)[0]
+    loss = (-(1 - eps) * lp[rows, y[rows]] - eps / V * lp[rows].sum(axis=1)).sum() / n  # tape.cpp:1270-1278
+    g = np.zeros_like(z)                                # adjoints (tape.cpp:1285-1293, 907-917)
+    g[rows] = np.exp(lp[rows]) - eps / V
+    g[rows, y[rows]] -= 1 - eps
+    g /= n
+    return loss, (g @ W.T).reshape(B, T, D), x.reshape(B * T, D).T @ g, g.sum(axis=0)
 
 
 def seeded_case(seed: int, B: int, T: int, D: int, H: int, ragged: bool = True,

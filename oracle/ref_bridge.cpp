@@ -130,6 +130,38 @@ int ref_lstm_step(int B, int D, int H, const double* x, const double* h0, const 
   }
 }
 
+// The decoder output layer + loss exactly as the reference builds it:
+// ce_label_smoothing(log_softmax(add(matmul(x, W), b)), targets, eps)
+// (compiler.cpp:651-663, tape.cpp:879-924, 1224-1298), gradients by
+// Tape::backward.  x [B, T, D], targets [B, T] (seq_lens mask), W [D, V].
+int ref_output_ce(int B, int T, int D, int V, const double* x, const int* lens, const int* targets,
+                  const double* W, const double* b, double eps, double* loss, double* dx, double* dW,
+                  double* db, char* err, int errlen) {
+  try {
+    Tape t(true);
+    std::vector<std::int32_t> lv(lens, lens + B);
+    Tensor xt = make({{Axis::Batch, B}, {Axis::Time, T}, {Axis::Feature, D}}, x);
+    xt.set_seq_lens(lv);
+    NodeId xn = t.param("x", xt);
+    NodeId Wn = t.param("W", make({{Axis::Feature, D}, {Axis::Other, V}}, W));
+    NodeId bn = t.param("b", make({{Axis::Feature, V}}, b));
+    IdTensor ids = IdTensor::from_data({{Axis::Batch, B}, {Axis::Time, T}},
+                                       std::vector<std::int32_t>(targets, targets + B * T));
+    ids.set_seq_lens(lv);
+    NodeId lp = t.log_softmax(t.add(t.matmul(xn, Wn), bn));
+    NodeId ln = t.ce_label_smoothing(lp, ids, static_cast<Real>(eps), "output_prob");
+    *loss = static_cast<double>(t.value(ln).scalar_value());
+    GradBuffer g = t.backward(ln);
+    auto grads = t.param_gradients(g);
+    put(grads.at("x"), dx);
+    put(grads.at("W"), dW);
+    put(grads.at("b"), db);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 // An L-layer bidirectional LSTM stack, each layer's input the feature concat
 // [fw ‖ bw] of the previous layer (compiler.cpp:600-608 with the Listing-1
 // enc{i}_fw / enc{i}_bw topology, models.cpp).  params[l*6 + {0..5}] =

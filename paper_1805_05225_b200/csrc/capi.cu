@@ -17,6 +17,7 @@
 #include "gemm.h"
 #include "profile.h"
 #include "rec_tc.h"
+#include "softmax_ce.h"
 #include "recurrence.h"
 
 namespace sl {
@@ -250,6 +251,29 @@ int sl_version(void) { return 100; }
 int64_t sl_lstm_bf16_pitch(int32_t features) { return round_up((int64_t)features + 1, 64); }
 
 size_t sl_adam_scratch_size(void) { return sizeof(AdamScratch); }
+
+size_t sl_output_ce_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab) {
+  if (batch <= 0 || time <= 0 || input_dim <= 0 || vocab <= 0) return 0;
+  return output_ce_workspace_bytes(batch, time, input_dim, vocab);
+}
+
+int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, const float* x,
+                 const int32_t* targets, const int32_t* seq_lens, const float* W, const float* b,
+                 float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
+                 void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream) {
+  return guarded([&] {
+    SL_REQUIRE(epsilon >= 0.f && epsilon < 1.f, SL_ERR_INVALID_ARGUMENT,
+               "label smoothing epsilon must be in [0, 1)");  // reference tape.cpp:1226-1228
+    SL_REQUIRE(batch > 0 && time > 0 && input_dim > 0 && vocab > 0, SL_ERR_SHAPE,
+               "output_ce: log_probs must end in Feature axis (B, T, D, V > 0)");
+    SL_REQUIRE(x && targets && seq_lens && W && b && loss && bad_target, SL_ERR_INVALID_ARGUMENT,
+               "output_ce: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= output_ce_workspace_bytes(batch, time, input_dim, vocab),
+               SL_ERR_WORKSPACE, "output_ce: workspace too small");
+    output_ce(batch, time, input_dim, vocab, x, targets, seq_lens, W, b, epsilon, loss, dx, dW, db,
+              accumulate != 0, workspace, bad_target, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
 
 int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* v, int32_t step,
                  float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,

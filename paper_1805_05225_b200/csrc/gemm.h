@@ -36,6 +36,13 @@ struct TcGemm {
   int64_t ldc2 = 0;
   // optional: write the result as bf16 here (ld = ldc) instead of fp32 C
   __nv_bfloat16* Cb = nullptr;
+  // optional (with Cb, pair GEMM only): per row and 128-column block, the online
+  // softmax statistics of the (bf16-rounded) outputs — float4 {max, sum exp(z -
+  // max), sum z, z[target] if the block holds the row's target else 0} at
+  // sm_part[row * sm_ld + col / 128] (softmax_ce.cu)
+  float4* sm_part = nullptr;
+  int sm_ld = 0;
+  const int32_t* sm_targets = nullptr;
 };
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 // CTA-pair variant (gemm_tc2.cu, M = 256 tiles); gemm_bf16_tc dispatches to it

@@ -342,7 +342,9 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStr
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   if (g.M <= 0 || g.N <= 0) return;
   static const bool one_cta = getenv("SL_GEMM_1CTA") != nullptr;
-  if (!one_cta && gemm_bf16_tc2_ok(g)) {
+  SL_REQUIRE(!g.sm_part || gemm_bf16_tc2_ok(g), SL_ERR_UNSUPPORTED,
+             "gemm_bf16_tc: softmax partials need the CTA-pair GEMM");
+  if ((!one_cta || g.sm_part) && gemm_bf16_tc2_ok(g)) {
     SL_REQUIRE(!g.Cb || g.beta == 0.f, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc: bf16 output needs beta = 0");
     gemm_bf16_tc2(g, stream);
     return;

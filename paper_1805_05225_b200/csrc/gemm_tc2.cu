@@ -41,6 +41,9 @@ struct P2 {
   int64_t ldc2;
   __nv_bfloat16* Cb;
   int skip_epi;  // experiments only: load the accumulator but store nothing (wrong results)
+  float4* sm_part;  // softmax partials (gemm.h TcGemm::sm_part)
+  int sm_ld;
+  const int32_t* sm_targets;
 };
 
 
@@ -210,6 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       const bool vec = second ? (p.ldc2 % 4) == 0 && ((uintptr_t)p.C2 & 15) == 0
                               : (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0;
       constexpr int kColsPerWarp = BNP / (kEpiWarps / 4);
+      static_assert(kColsPerWarp == 128, "softmax partials are per 128-column block");
+      // online softmax statistics of this row over the warp's 128 columns
+      float sm_m = -INFINITY, sm_s = 0.f, sm_t = 0.f, sm_y = 0.f;
+      const int sm_tgt = (p.sm_part && row < p.M) ? p.sm_targets[row] : -1;
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
@@ -245,11 +252,41 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               w.z = *reinterpret_cast<uint32_t*>(&t2);
               w.w = *reinterpret_cast<uint32_t*>(&t3);
               *reinterpret_cast<uint4*>(brow + j) = w;
+              if (p.sm_part) {  // statistics of the stored (bf16) values
+                const float zb[8] = {__low2float(t0), __high2float(t0), __low2float(t1), __high2float(t1),
+                                     __low2float(t2), __high2float(t2), __low2float(t3), __high2float(t3)};
+                float cm = zb[0];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) cm = fmaxf(cm, zb[i]);
+                const float mn = fmaxf(sm_m, cm);
+                float acc = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  acc += exp2f((zb[i] - mn) * 1.4426950408889634f);
+                  sm_t += zb[i];
+                  if (col0 + j + i == sm_tgt) sm_y = zb[i];
+                }
+                sm_m = mn;
+                sm_s = acc;
+              }
             }
           } else {
-            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
-              brow[j] = __float2bfloat16_rn(p.alpha * v[j] + (p.bias ? p.bias[col0 + j] : 0.f));
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
+              const __nv_bfloat16 zb = __float2bfloat16_rn(p.alpha * v[j] + (p.bias ? p.bias[col0 + j] : 0.f));
+              brow[j] = zb;
+              if (p.sm_part) {
+                const float z = __bfloat162float(zb);
+                const float mn = fmaxf(sm_m, z);
+                sm_s = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f) + exp2f((z - mn) * 1.4426950408889634f);
+                sm_m = mn;
+                sm_t += z;
+                if (col0 + j == sm_tgt) sm_y = z;
+              }
+            }
           }
+          if (p.sm_part && c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
+            p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] =
+                make_float4(sm_m, sm_s, sm_t, sm_y);
           continue;
         }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
@@ -391,6 +428,11 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   // bulk-tensor output stores when the output is written (not accumulated) and
   // its rows are 16 B aligned; the per-row path stays for beta != 0
   p.skip_epi = getenv("SL_GEMM_SKIP_EPI") != nullptr;
+  p.sm_part = g.sm_part;
+  p.sm_ld = g.sm_ld;
+  p.sm_targets = g.sm_targets;
+  SL_REQUIRE(!g.sm_part || (g.Cb && g.sm_targets), SL_ERR_INVALID_ARGUMENT,
+             "gemm: softmax partials need the bf16 output and the targets");
   if (!g.a_mn && g.b_mn) launch2<false, true>(ta, tb, p, stream);
   else if (!g.a_mn && !g.b_mn) launch2<false, false>(ta, tb, p, stream);
   else if (g.a_mn && g.b_mn) launch2<true, true>(ta, tb, p, stream);

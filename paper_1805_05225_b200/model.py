@@ -1,14 +1,15 @@
 """The config-4 training step around the LSTM hot path (BASELINE configs[3]):
-6-layer BLSTM encoder + 1-layer LSTM decoder, fwd + bwd, data-parallel
-gradient all-reduce, fused clip + Adam — the parts of the reference's
-Listing-1 step (models.cpp:17-184, compiler.cpp eval_layer / RnnCell) that are
-LSTM layers or the optimizer.  What is NOT built ("next"):
-the MLP attention and the output projection + softmax; the decoder input is
-[target embedding ‖ context] with the context stand-in c_t = encoder output at
-t (an identity alignment, T_src = T_tgt), so encoder gradients still flow
-through the decoder as they do through attention in the reference.  The
-decoder is run as one unidirectional LSTM layer over the teacher-forced
-inputs (the decoder cell has no recurrent input feeding without attention).
+6-layer BLSTM encoder + 1-layer LSTM decoder + the output softmax layer with
+the label-smoothed CE loss, fwd + bwd, data-parallel gradient all-reduce,
+fused clip + Adam — the Listing-1 step (models.cpp:17-184, compiler.cpp
+eval_layer / RnnCell / Softmax) minus the MLP attention (not
+built) and the readout layer: the decoder input is [target embedding ‖
+context] with the context stand-in c_t = encoder output at t (an identity
+alignment, T_src = T_tgt), so encoder gradients still flow through the
+decoder as they do through attention in the reference, and the output layer
+reads the decoder state directly.  The decoder runs as one unidirectional
+LSTM layer over the teacher-forced inputs (no recurrent input feeding
+without attention).
 
 All parameters (encoder then decoder) and their gradients live in ONE flat
 fp32 buffer each: the gradient all-reduce buckets are slices of it and the
@@ -21,18 +22,24 @@ import torch
 from . import lstm
 from .encoder import BLSTMEncoder
 from .optim import Adam
+from .output import OutputCE
 
 
 class Seq2SeqLSTM:
     def __init__(self, enc_layers: int, batch: int, time: int, emb: int, hidden: int,
-                 precision: str = "bf16", device=None, lr: float = 1e-3, clip_norm: float = 5.0):
+                 precision: str = "bf16", device=None, lr: float = 1e-3, clip_norm: float = 5.0,
+                 vocab: int = 0, label_smoothing: float = 0.1):
+        """vocab > 0 adds the output softmax layer [hidden, vocab] and the CE loss
+        (step() then takes target ids instead of an upstream gradient)."""
         self.L, self.B, self.T, self.E, self.H = enc_layers, batch, time, emb, hidden
         self.device = torch.device(device or "cuda")
         H = hidden
         self.Dd = emb + 2 * H  # decoder input [embedding ‖ context] (models.cpp:161: 620 + 2000)
         n_enc = BLSTMEncoder.numel(enc_layers, emb, H)
         n_dec = self.Dd * 4 * H + H * 4 * H + 4 * H
-        self.params = torch.empty(n_enc + n_dec, dtype=torch.float32, device=self.device)
+        self.V = vocab
+        n_out = H * vocab + vocab if vocab else 0
+        self.params = torch.empty(n_enc + n_dec + n_out, dtype=torch.float32, device=self.device)
         self.grads = torch.zeros_like(self.params)
         self.enc = BLSTMEncoder(enc_layers, batch, time, emb, H, precision, self.device,
                                 params=self.params[:n_enc], grads=self.grads[:n_enc])
@@ -45,7 +52,15 @@ class Seq2SeqLSTM:
             self.dec_p.append(self.params[off:off + k].view(shape))
             self.dec_g.append(self.grads[off:off + k].view(shape))
             off += k
-        self.dec_bucket = self.grads[n_enc:]
+        self.dec_bucket = self.grads[n_enc:n_enc + n_dec]
+        if vocab:  # output softmax layer (compiler.cpp:651-663): W [H, V], b [V]
+            self.out_p = [self.params[off:off + H * vocab].view(H, vocab),
+                          self.params[off + H * vocab:off + n_out]]
+            self.out_g = [self.grads[off:off + H * vocab].view(H, vocab),
+                          self.grads[off + H * vocab:off + n_out]]
+            self.out_bucket = self.grads[off:off + n_out]
+            self.out = OutputCE(batch, time, H, vocab, label_smoothing, device=self.device)
+            self.dec_dy = torch.empty(batch, time, H, dtype=torch.float32, device=self.device)
         bf16 = precision == "bf16"
         self.dec = lstm.LSTMLayer(batch, time, self.Dd, H, 1, 1, precision, self.device, x_bf16=bf16)
         if bf16:  # padded bf16 decoder input, ones column at Dd (seqloom_cuda.h SL_LAYER_X_BF16)
@@ -61,6 +76,8 @@ class Seq2SeqLSTM:
             (f"dec/{n}", n_enc + o, k) for n, o, k in
             (("W", 0, self.Dd * 4 * H), ("R", self.Dd * 4 * H, H * 4 * H),
              ("b", self.Dd * 4 * H + H * 4 * H, 4 * H))]
+        if vocab:
+            names += [("output_prob/W", n_enc + n_dec, H * vocab), ("output_prob/b", n_enc + n_dec + H * vocab, vocab)]
         self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
 
     def init_uniform(self, seed: int = 0):
@@ -87,9 +104,28 @@ class Seq2SeqLSTM:
         self.enc_dy.copy_(self.dec_dx[:, :, self.E:])
         return self.enc.backward(self.enc_dy, on_layer_grads=on_grads)
 
-    def step(self, x, seq_lens, dy_dec, reducer=None, grad_scale: float = 1.0):
+    def loss_and_output_grads(self, targets, seq_lens, on_grads=None):
+        """Output layer + label-smoothed CE on the decoder states: returns the
+        (device) loss; dL/d(decoder output) lands in self.dec_dy."""
+        W, b = self.out_p
+        loss, _, _, _ = self.out.forward_backward(self.dec_y, targets, seq_lens, W, b, dx=self.dec_dy,
+                                                  dW=self.out_g[0], db=self.out_g[1])
+        if on_grads is not None:
+            on_grads(-2, self.out_bucket)
+        return loss
+
+    def step(self, x, seq_lens, dy_or_targets, reducer=None, grad_scale: float = 1.0):
+        """One training step.  With the output layer (vocab > 0) the last
+        argument is the target ids [B, T] and the step returns the device loss;
+        without it, the upstream gradient of the decoder output."""
         self.forward(x, seq_lens)
-        self.backward(dy_dec, on_grads=reducer)
+        loss = None
+        if self.V:
+            loss = self.loss_and_output_grads(dy_or_targets, seq_lens, on_grads=reducer)
+            self.backward(self.dec_dy, on_grads=reducer)
+        else:
+            self.backward(dy_or_targets, on_grads=reducer)
         if reducer is not None:
             reducer.wait()
         self.opt.step(self.grads, grad_scale=grad_scale)
+        return loss

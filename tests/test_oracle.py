@@ -223,3 +223,34 @@ def test_reference_own_unit_tests_pass():
                            env={**os.environ, "OPENBLAS_NUM_THREADS": "1"})
         assert r.returncode == 0, r.stdout + r.stderr
         assert "failed: 0" in r.stdout
+
+
+def test_output_ce_restatement_pinned_to_reference():
+    # the decoder output layer + loss: numpy restatement vs the
+    # reference's own Tape ops (matmul, add, log_softmax, ce_label_smoothing)
+    import oracle
+    ref = oracle.Reference(64)
+    rng = np.random.default_rng(3)
+    B, T, D, V = 4, 6, 9, 23
+    x = rng.uniform(-1, 1, (B, T, D))
+    W = rng.uniform(-0.4, 0.4, (D, V))
+    b = rng.uniform(-0.4, 0.4, V)
+    lens = np.array([6, 2, 5, 1], np.int32)
+    tg = rng.integers(0, V, (B, T)).astype(np.int32)
+    for eps in (0.0, 0.1, 0.5):
+        a = ref.output_ce(x, lens, tg, W, b, eps)
+        n = oracle.output_ce_np(x, lens, tg, W, b, eps)
+        assert abs(a[0] - n[0]) < 1e-12
+        for p, q in zip(a[1:], n[1:]):
+            assert np.abs(p - q).max() < 1e-12
+    # uniform logits: every lp = -log V, so the loss is log V for any eps
+    loss = oracle.output_ce_np(np.zeros((1, 2, 3)), [2], np.zeros((1, 2), np.int32), np.zeros((3, 7)),
+                               np.zeros(7), 0.3)[0]
+    assert abs(loss - np.log(7)) < 1e-12
+    # the reference's argument errors
+    with pytest.raises(RuntimeError, match=r"epsilon must be in \[0, 1\)"):
+        ref.output_ce(x, lens, tg, W, b, 1.0)
+    bad = tg.copy()
+    bad[0, 0] = V
+    with pytest.raises(RuntimeError, match="out of range"):
+        ref.output_ce(x, lens, bad, W, b, 0.1)

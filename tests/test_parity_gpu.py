@@ -492,3 +492,36 @@ def test_bwd_pair_kernel_opt_in(cuda, monkeypatch, nd, H):
             assert rel(out[g][k], ref[g]) < TOL["bf16"], g
         dx = dx + ref["dx"]
     assert rel(out["dx"], dx) < TOL["bf16"]
+
+
+def test_seq2seq_with_output_layer_matches_fp64(cuda):
+    # the full bench step incl. the output softmax + label-smoothed CE: the
+    # decoder receives dL/dy from the output layer (not a synthetic gradient)
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    Lyr, B, T, E, H, V = 1, 12, 6, 16, 32, 300
+    m = Seq2SeqLSTM(Lyr, B, T, E, H, "fp32", vocab=V, label_smoothing=0.1)
+    m.init_uniform(5)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1
+    emb = torch.rand(B, T, E, device="cuda", generator=g) * 2 - 1
+    lens = torch.randint(T // 2, T + 1, (B,), device="cuda", generator=g).int()
+    tg = torch.randint(0, V, (B, T), device="cuda", generator=g).int()
+    m.set_target_embeddings(emb)
+    # fp64 reference of the composition, pre-step parameters
+    inp = x.double()
+    W, R, bb = [[v.double() for v in vs] for vs in m.enc._wrb(0)]
+    enc_out = torch.cat([torch_ref.sequence(inp, lens, W[k], R[k], bb[k], (1, -1)[k])["y"] for k in range(2)], 2)
+    dec_in = torch.cat([emb.double(), enc_out], dim=2)
+    Wd, Rd, bd = [t.double() for t in m.dec_p]
+    dec_y = torch_ref.sequence(dec_in, lens, Wd, Rd, bd, 1)["y"]
+    loss, ddy, dWo, dbo = oracle.output_ce_np(dec_y.cpu().numpy(), lens.cpu().numpy(), tg.cpu().numpy(),
+                                              m.out_p[0].double().cpu().numpy(), m.out_p[1].double().cpu().numpy(),
+                                              0.1)
+    dref = torch_ref.sequence(dec_in, lens, Wd, Rd, bd, 1, torch.as_tensor(ddy, device="cuda"))
+    l = m.step(x, lens, tg)
+    torch.cuda.synchronize()
+    # the output layer runs on bf16 tensor cores even in the fp32 LSTM mode
+    assert abs(float(l) - loss) < 2e-3 * max(1.0, abs(loss))
+    assert rel(m.out_g[0], dWo) < 2e-2 and rel(m.out_g[1], dbo) < 2e-2
+    for t_, r_ in zip(m.dec_g, (dref["dW"], dref["dR"], dref["db"])):
+        assert rel(t_, r_) < 3e-2
