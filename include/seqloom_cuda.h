@@ -147,6 +147,39 @@ int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* 
                  float lr, float beta1, float beta2, float eps, float grad_scale, float clip_norm,
                  void* scratch, float* grad_norm_out, int32_t* nonfinite_out, sl_stream_t stream);
 
+/* ---- decoder MLP attention step --------------------------------
+ * One step of the Listing-1 decoder's attention subnet (reference
+ * models.cpp:107-154, compiler.cpp:616-639), fp32:
+ *   s_tr = s W_s + b_s;  e = tanh(enc_ctx + accum W_fb + b_fb + s_tr) v + b_v;
+ *   a = softmax over the valid source positions (tape.cpp:926-985);
+ *   accum_out = accum + a;  att = sum_j a_j enc_j (tape.cpp:987-1072).
+ * Shapes: enc_ctx [B, Ts, K], enc [B, Ts, E], s [B, H], accum / a / accum_out
+ * [B, Ts], W_s [H, K], b_s [K], W_fb [1, K], b_fb [K], v [K, 1], b_v [1] (a
+ * device scalar), att [B, E]; src_lens [B].  The backward takes the forward's
+ * `a`, the upstream d_att and d_accum_out (may be NULL), and writes (or, with
+ * accumulate, adds) every input gradient; any gradient output may be NULL
+ * except d_enc_ctx, d_enc, d_accum, d_W_fb, d_b_fb, d_v, d_b_v. */
+typedef struct sl_attention {
+  int32_t batch;     /* B  */
+  int32_t src_time;  /* Ts */
+  int32_t key_dim;   /* K  */
+  int32_t enc_dim;   /* E  */
+  int32_t state_dim; /* H  */
+} sl_attention;
+size_t sl_attention_workspace_size(const sl_attention* att);
+int sl_attention_step_fwd(const sl_attention* att, const int32_t* src_lens, const float* enc_ctx,
+                          const float* enc, const float* s, const float* accum, const float* W_s,
+                          const float* b_s, const float* W_fb, const float* b_fb, const float* v,
+                          const float* b_v, float* att_out, float* a, float* accum_out, void* workspace,
+                          size_t workspace_bytes, sl_stream_t stream);
+int sl_attention_step_bwd(const sl_attention* att, const int32_t* src_lens, const float* enc_ctx,
+                          const float* enc, const float* s, const float* accum, const float* W_s,
+                          const float* b_s, const float* W_fb, const float* b_fb, const float* v,
+                          const float* a, const float* d_att, const float* d_accum_out, float* d_enc_ctx,
+                          float* d_enc, float* d_s, float* d_accum, float* d_W_s, float* d_b_s, float* d_W_fb,
+                          float* d_b_fb, float* d_v, float* d_b_v, int accumulate, void* workspace,
+                          size_t workspace_bytes, sl_stream_t stream);
+
 /* ---- output layer + loss ---------------------------------------
  * The decoder's Softmax layer and its training loss in one call: logits =
  * x W + b (reference compiler.cpp:651-663), log_softmax (tape.cpp:879-924),
@@ -170,7 +203,7 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
  * (name, calls, device ms, algorithmic flops / bytes).  Phase names:
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
  *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam, k7_logits_gemm, k7_softmax_ce,
- *   k7_dx_gemm, k7_dw_gemm */
+ *   k7_dx_gemm, k7_dw_gemm, k8_attention_fwd, k8_attention_bwd */
 typedef struct sl_profile_entry {
   char name[32];
   int32_t calls;

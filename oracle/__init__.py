@@ -125,6 +125,9 @@ class Reference:
         L.ref_lstm_step.argtypes = [ctypes.c_int] * 3 + [_d] * 16 + [c, ctypes.c_int]
         L.ref_blstm_stack.argtypes = ([ctypes.c_int] * 5 + [_d, _i, _P(_d), _d, _d, _d, _P(_d)] +
                                       [c, ctypes.c_int])
+        if hasattr(L, "ref_attention_step"):
+            L.ref_attention_step.argtypes = ([ctypes.c_int] * 5 + [_i] + [_d] * 9 + [ctypes.c_double] +
+                                             [_d] * 15 + [c, ctypes.c_int])
         if hasattr(L, "ref_output_ce"):
             L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
                                         [c, ctypes.c_int])
@@ -207,6 +210,66 @@ def _output_ce(self, x, lens, targets, W, b, eps):
 
 
 Reference.output_ce = _output_ce
+
+
+def _attention_step(self, lens, enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v, bv, d_att=None, d_accum=None):
+    """The reference's attention subnet step: (att, a, accum', grads dict or None)."""
+    B, Ts, K = enc_ctx.shape
+    E = enc.shape[2]
+    H = s.shape[1]
+    ins = [_f64(a) for a in (enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v)]
+    d_att, d_accum = _f64(d_att), _f64(d_accum)
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    att, a, acc2 = np.zeros((B, E)), np.zeros((B, Ts)), np.zeros((B, Ts))
+    names = ["enc_ctx", "enc", "s", "accum", "Ws", "bs", "Wfb", "bfb", "v", "bv"]
+    shapes = [(B, Ts, K), (B, Ts, E), (B, H), (B, Ts), (H, K), (K,), (1, K), (K,), (K, 1), (1,)]
+    g = [np.zeros(sh) for sh in shapes] if d_att is not None else None
+    err = ctypes.create_string_buffer(512)
+    rc = self.lib.ref_attention_step(B, Ts, K, E, H, _ptr(lens, _i), *[_ptr(x) for x in ins], float(bv),
+                                     _ptr(d_att), _ptr(d_accum), _ptr(att), _ptr(a), _ptr(acc2),
+                                     *([_ptr(x) for x in g] if g else [None] * 10), err, 512)
+    self._check(rc, err)
+    return att, a, acc2, (dict(zip(names, g)) if g else None)
+
+
+Reference.attention_step = _attention_step
+
+
+def attention_step_np(lens, enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v, bv, d_att=None, d_accum=None):
+    """fp64 numpy restatement of the same step (models.cpp:107-154 wiring; ops
+    tape.cpp:327-356 matmul, 134-174 broadcast add, 926-985 softmax_over_spatial,
+    987-1072 generic_attention).  Returns (att, a, accum', grads or None)."""
+    enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v = (np.asarray(x, np.float64) for x in
+                                                   (enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v))
+    B, Ts, K = enc_ctx.shape
+    valid = np.arange(Ts)[None, :] < np.asarray(lens)[:, None]           # [B, Ts]
+    s_tr = s @ Ws + bs                                                   # [B, K]
+    e_in = enc_ctx + accum[:, :, None] * Wfb[0][None, None, :] + bfb + s_tr[:, None, :]
+    u = np.tanh(e_in)
+    e = u @ v[:, 0] + bv                                                 # [B, Ts]
+    em = np.where(valid, e, -np.inf)
+    m = em.max(axis=1, keepdims=True)
+    ex = np.where(valid, np.exp(em - m), 0.0)
+    a = ex / ex.sum(axis=1, keepdims=True)                               # tape.cpp:952-960
+    acc2 = accum + a
+    att = np.einsum("bj,bje->be", a, enc)                                # tape.cpp:1005-1014
+    if d_att is None:
+        return att, a, acc2, None
+    d_att = np.asarray(d_att, np.float64)
+    # the upstream gradient of accum' is masked at padded source positions like
+    # every time-masked tape value (the reference's mul / reduce_sum respect seq_lens)
+    d_acc2 = np.zeros((B, Ts)) if d_accum is None else np.where(valid, np.asarray(d_accum, np.float64), 0.0)
+    d_a = np.einsum("be,bje->bj", d_att, enc) + d_acc2                   # tape.cpp:1031-1041
+    g_enc = a[:, :, None] * d_att[:, None, :]                            # tape.cpp:1047-1058
+    dot = (d_a * a).sum(axis=1, keepdims=True)
+    d_e = np.where(valid, a * (d_a - dot), 0.0)                          # tape.cpp:966-978
+    d_u = d_e[:, :, None] * v[:, 0][None, None, :]
+    d_ein = d_u * (1 - u * u)
+    g = {"enc_ctx": d_ein, "enc": g_enc, "s": d_ein.sum(axis=1) @ Ws.T, "accum": d_acc2 + d_ein @ Wfb[0],
+         "Ws": s.T @ d_ein.sum(axis=1), "bs": d_ein.sum(axis=(0, 1)),
+         "Wfb": (accum[:, :, None] * d_ein).sum(axis=(0, 1))[None, :], "bfb": d_ein.sum(axis=(0, 1)),
+         "v": np.einsum("bjk,bj->k", u, d_e)[:, None], "bv": np.array([d_e.sum()])}
+    return att, a, acc2, g
 
 
 def output_ce_np(x, lens, targets, W, b, eps):

@@ -162,6 +162,75 @@ int ref_output_ce(int B, int T, int D, int V, const double* x, const int* lens, 
   }
 }
 
+// One MLP-attention step of the Listing-1 decoder subnet, built from the
+// reference's own layer ops exactly as eval_layer wires it (models.cpp:107-154,
+// compiler.cpp:616-639): s_tr = s W_s + b_s; weight_feedback = accum W_fb +
+// b_fb; e = tanh(enc_ctx + weight_feedback + s_tr) v + b_v; a =
+// softmax_over_spatial(e) (tape.cpp:926-985); accum' = accum + a; att =
+// generic_attention(a, enc) (tape.cpp:987-1072).  The upstream gradients
+// d_att [B, E] and d_accum [B, Ts] enter through L = sum(att d_att) +
+// sum(accum' d_accum).  Outputs (optional): att, a, accum' and the gradients.
+int ref_attention_step(int B, int Ts, int K, int E, int H, const int* lens, const double* enc_ctx,
+                       const double* enc, const double* s, const double* accum, const double* Ws,
+                       const double* bs, const double* Wfb, const double* bfb, const double* v, double bv,
+                       const double* d_att, const double* d_accum, double* att, double* a, double* accum2,
+                       double* g_enc_ctx, double* g_enc, double* g_s, double* g_accum, double* g_Ws,
+                       double* g_bs, double* g_Wfb, double* g_bfb, double* g_v, double* g_bv, char* err,
+                       int errlen) {
+  try {
+    const bool grad = d_att != nullptr;
+    Tape t(grad);
+    std::vector<std::int32_t> lv(lens, lens + B);
+    auto leaf = [&](const char* name, Tensor x) { return grad ? t.param(name, x) : t.constant(x); };
+    Tensor tc_ = make({{Axis::Batch, B}, {Axis::Time, Ts}, {Axis::Feature, K}}, enc_ctx);
+    tc_.set_seq_lens(lv);
+    Tensor te = make({{Axis::Batch, B}, {Axis::Time, Ts}, {Axis::Feature, E}}, enc);
+    te.set_seq_lens(lv);
+    Tensor ta = make({{Axis::Batch, B}, {Axis::Time, Ts}, {Axis::Feature, 1}}, accum);
+    ta.set_seq_lens(lv);
+    NodeId ctxn = leaf("enc_ctx", tc_), encn = leaf("enc", te), accn = leaf("accum", ta);
+    NodeId sn = leaf("s", make({{Axis::Batch, B}, {Axis::Feature, H}}, s));
+    NodeId Wsn = leaf("Ws", make({{Axis::Feature, H}, {Axis::Other, K}}, Ws));
+    NodeId bsn = leaf("bs", make({{Axis::Feature, K}}, bs));
+    NodeId Wfbn = leaf("Wfb", make({{Axis::Feature, 1}, {Axis::Other, K}}, Wfb));
+    NodeId bfbn = leaf("bfb", make({{Axis::Feature, K}}, bfb));
+    NodeId vn = leaf("v", make({{Axis::Feature, K}, {Axis::Other, 1}}, v));
+    NodeId bvn = leaf("bv", make({{Axis::Feature, 1}}, &bv));
+    NodeId s_tr = t.add(t.matmul(sn, Wsn), bsn);
+    NodeId fb = t.add(t.matmul(accn, Wfbn), bfbn);
+    NodeId e_in = t.add(t.add(ctxn, fb), s_tr);
+    NodeId e = t.add(t.matmul(t.tanh(e_in), vn), bvn);
+    NodeId an = t.softmax_over_spatial(e);
+    NodeId acc2 = t.add(accn, an);
+    NodeId attn = t.generic_attention(an, encn);
+    put(t.value(attn), att);
+    put(t.value(an), a);
+    put(t.value(acc2), accum2);
+    if (!grad) return 0;
+    NodeId loss = sum_all(t, t.mul(attn, t.constant(make({{Axis::Batch, B}, {Axis::Feature, E}}, d_att))));
+    if (d_accum) {
+      Tensor tda = make({{Axis::Batch, B}, {Axis::Time, Ts}, {Axis::Feature, 1}}, d_accum);
+      tda.set_seq_lens(lv);
+      loss = t.add(loss, sum_all(t, t.mul(acc2, t.constant(tda))));
+    }
+    GradBuffer g = t.backward(loss);
+    auto grads = t.param_gradients(g);
+    put(grads.at("enc_ctx"), g_enc_ctx);
+    put(grads.at("enc"), g_enc);
+    put(grads.at("s"), g_s);
+    put(grads.at("accum"), g_accum);
+    put(grads.at("Ws"), g_Ws);
+    put(grads.at("bs"), g_bs);
+    put(grads.at("Wfb"), g_Wfb);
+    put(grads.at("bfb"), g_bfb);
+    put(grads.at("v"), g_v);
+    put(grads.at("bv"), g_bv);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 // An L-layer bidirectional LSTM stack, each layer's input the feature concat
 // [fw ‖ bw] of the previous layer (compiler.cpp:600-608 with the Listing-1
 // enc{i}_fw / enc{i}_bw topology, models.cpp).  params[l*6 + {0..5}] =

@@ -1,0 +1,42 @@
+// The decoder's MLP attention step (attention.cu).
+#pragma once
+#include "common.cuh"
+
+namespace sl {
+
+struct AttnArgs {
+  int B, Ts, K, E, H;
+  const int32_t* lens;     // source lengths [B]
+  const float* enc_ctx;    // [B, Ts, K]
+  const float* enc;        // [B, Ts, E]
+  const float* accum;      // [B, Ts]
+  const float* W_fb;       // [1, K]
+  const float* b_fb;       // [K]
+  const float* v;          // [K, 1]
+  const float* b_v;        // [1] (device)
+  float* s_tr;             // workspace [B, K]
+  // forward outputs
+  float* att;              // [B, E]
+  float* a;                // [B, Ts]
+  float* accum_out;        // [B, Ts]
+  // backward
+  const float* a_saved;    // [B, Ts] from the forward
+  const float* d_att;      // [B, E]
+  const float* d_accum_out;  // [B, Ts] or null
+  float* d_s_tr;           // workspace [B, K]
+  float* d_enc_ctx;        // [B, Ts, K]
+  float* d_enc;            // [B, Ts, E]
+  float* d_accum;          // [B, Ts]
+  float* d_W_fb;           // [K]
+  float* d_b_fb;           // [K]
+  float* d_v;              // [K]
+  float* d_b_v;            // [1]
+  int accumulate;
+};
+
+size_t attention_workspace_bytes(int B, int K);
+void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st);
+void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, float* d_s, float* d_W_s,
+                   float* d_b_s, void* ws, cudaStream_t st);
+
+}  // namespace sl

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "adam.h"
+#include "attention.h"
 #include "cell.h"
 #include "convert.h"
 #include "gemm.h"
@@ -251,6 +252,86 @@ int sl_version(void) { return 100; }
 int64_t sl_lstm_bf16_pitch(int32_t features) { return round_up((int64_t)features + 1, 64); }
 
 size_t sl_adam_scratch_size(void) { return sizeof(AdamScratch); }
+
+static void check_attention(const sl_attention* at) {
+  SL_REQUIRE(at != nullptr, SL_ERR_INVALID_ARGUMENT, "attention: null descriptor");
+  SL_REQUIRE(at->batch > 0 && at->src_time > 0 && at->key_dim > 0 && at->enc_dim > 0 && at->state_dim > 0,
+             SL_ERR_SHAPE, "softmax_over_spatial: needs Batch and Time axes (all extents > 0)");
+}
+
+size_t sl_attention_workspace_size(const sl_attention* at) {
+  if (!at || at->batch <= 0 || at->key_dim <= 0) return 0;
+  return attention_workspace_bytes(at->batch, at->key_dim);
+}
+
+static AttnArgs attn_args(const sl_attention* at, const int32_t* lens, const float* enc_ctx, const float* enc,
+                          const float* accum, const float* W_fb, const float* b_fb, const float* v) {
+  AttnArgs p{};
+  p.B = at->batch;
+  p.Ts = at->src_time;
+  p.K = at->key_dim;
+  p.E = at->enc_dim;
+  p.H = at->state_dim;
+  p.lens = lens;
+  p.enc_ctx = enc_ctx;
+  p.enc = enc;
+  p.accum = accum;
+  p.W_fb = W_fb;
+  p.b_fb = b_fb;
+  p.v = v;
+  return p;
+}
+
+int sl_attention_step_fwd(const sl_attention* at, const int32_t* src_lens, const float* enc_ctx,
+                          const float* enc, const float* s, const float* accum, const float* W_s,
+                          const float* b_s, const float* W_fb, const float* b_fb, const float* v,
+                          const float* b_v, float* att_out, float* a, float* accum_out, void* workspace,
+                          size_t workspace_bytes, sl_stream_t stream) {
+  return guarded([&] {
+    check_attention(at);
+    SL_REQUIRE(src_lens && enc_ctx && enc && s && accum && W_s && b_s && W_fb && b_fb && v && b_v && att_out &&
+                   a && accum_out,
+               SL_ERR_INVALID_ARGUMENT, "attention fwd: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim),
+               SL_ERR_WORKSPACE, "attention: workspace too small");
+    AttnArgs p = attn_args(at, src_lens, enc_ctx, enc, accum, W_fb, b_fb, v);
+    p.b_v = b_v;
+    p.att = att_out;
+    p.a = a;
+    p.accum_out = accum_out;
+    attention_fwd(p, s, W_s, b_s, workspace, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int sl_attention_step_bwd(const sl_attention* at, const int32_t* src_lens, const float* enc_ctx,
+                          const float* enc, const float* s, const float* accum, const float* W_s,
+                          const float* b_s, const float* W_fb, const float* b_fb, const float* v,
+                          const float* a, const float* d_att, const float* d_accum_out, float* d_enc_ctx,
+                          float* d_enc, float* d_s, float* d_accum, float* d_W_s, float* d_b_s, float* d_W_fb,
+                          float* d_b_fb, float* d_v, float* d_b_v, int accumulate, void* workspace,
+                          size_t workspace_bytes, sl_stream_t stream) {
+  return guarded([&] {
+    check_attention(at);
+    SL_REQUIRE(src_lens && enc_ctx && enc && s && accum && W_s && b_s && W_fb && b_fb && v && a && d_att &&
+                   d_enc_ctx && d_enc && d_accum && d_W_fb && d_b_fb && d_v && d_b_v,
+               SL_ERR_INVALID_ARGUMENT, "attention bwd: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim),
+               SL_ERR_WORKSPACE, "attention: workspace too small");
+    AttnArgs p = attn_args(at, src_lens, enc_ctx, enc, accum, W_fb, b_fb, v);
+    p.a_saved = a;
+    p.d_att = d_att;
+    p.d_accum_out = d_accum_out;
+    p.d_enc_ctx = d_enc_ctx;
+    p.d_enc = d_enc;
+    p.d_accum = d_accum;
+    p.d_W_fb = d_W_fb;
+    p.d_b_fb = d_b_fb;
+    p.d_v = d_v;
+    p.d_b_v = d_b_v;
+    p.accumulate = accumulate != 0;
+    attention_bwd(p, s, W_s, b_s, d_s, d_W_s, d_b_s, workspace, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
 
 size_t sl_output_ce_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab) {
   if (batch <= 0 || time <= 0 || input_dim <= 0 || vocab <= 0) return 0;

@@ -254,3 +254,26 @@ def test_output_ce_restatement_pinned_to_reference():
     bad[0, 0] = V
     with pytest.raises(RuntimeError, match="out of range"):
         ref.output_ce(x, lens, bad, W, b, 0.1)
+
+
+def test_attention_step_restatement_pinned_to_reference():
+    # the decoder's MLP attention step: numpy restatement vs the
+    # reference's own layer ops (matmul/add/tanh/softmax_over_spatial/generic_attention)
+    import oracle
+    ref = oracle.Reference(64)
+    rng = np.random.default_rng(11)
+    B, Ts, K, E, H = 3, 6, 9, 8, 5
+    lens = np.array([6, 2, 4], np.int32)
+    args = dict(enc_ctx=rng.uniform(-1, 1, (B, Ts, K)), enc=rng.uniform(-1, 1, (B, Ts, E)),
+                s=rng.uniform(-1, 1, (B, H)), accum=rng.uniform(0, 1, (B, Ts)), Ws=rng.uniform(-.5, .5, (H, K)),
+                bs=rng.uniform(-.5, .5, K), Wfb=rng.uniform(-.5, .5, (1, K)), bfb=rng.uniform(-.5, .5, K),
+                v=rng.uniform(-.5, .5, (K, 1)), bv=0.3)
+    d_att, d_acc = rng.uniform(-1, 1, (B, E)), rng.uniform(-1, 1, (B, Ts))
+    r = ref.attention_step(lens, **args, d_att=d_att, d_accum=d_acc)
+    n = oracle.attention_step_np(lens, **args, d_att=d_att, d_accum=d_acc)
+    for i in range(3):
+        assert np.abs(r[i] - n[i]).max() < 1e-12
+    for k in r[3]:
+        assert np.abs(r[3][k].reshape(n[3][k].shape) - n[3][k]).max() < 1e-12, k
+    # padded source positions get no attention weight
+    assert np.all(n[1][1, 2:] == 0) and abs(n[1][1].sum() - 1) < 1e-12
