@@ -6,11 +6,13 @@
 //   a     = softmax over the valid source positions       (tape.cpp:926-985)
 //   accum'= accum + a
 //   att   = sum_j a_j enc_j                               (tape.cpp:987-1072)
-// One CTA per batch row streams its [Ts, K] energy inputs and [Ts, E] encoder
-// states once per step (both L2-resident across the decoder's steps at the
-// config-4 shape), with the tanh / softmax / weighted sum fused; the small
-// projections (s_tr and its gradients) are fp32 GEMMs.  fp32 throughout: the
-// step is bandwidth-bound, not tensor-bound.
+// The step streams its [Ts, K] energy inputs and [Ts, E] encoder states once
+// (forward) / twice with their gradients (backward), with the tanh / softmax /
+// weighted sum fused into those passes; the small projections (s_tr and its
+// gradients) run on the tensor cores as fp32-accurate split-bf16 GEMMs
+// (gemm_f32x3.cu).  fp32 data: the step is bandwidth-bound, not tensor-bound.
+#include <algorithm>
+
 #include "attention.h"
 #include "gemm.h"
 #include "profile.h"
@@ -32,136 +34,369 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// dynamic smem: c[K] (= b_fb + s_tr[b]), wfb[K], v[K], e[Ts] (+ bwd: 4 [K] accumulators)
-__global__ void __launch_bounds__(kThreads) attn_fwd_kernel(AttnArgs p) {
-  extern __shared__ float sm[];
-  const int b = blockIdx.x, K = p.K, Ts = p.Ts, E = p.E;
-  float* c = sm;
-  float* wfb = c + K;
-  float* v = wfb + K;
-  float* e = v + K;
-  for (int k = threadIdx.x; k < K; k += kThreads) {
-    c[k] = p.b_fb[k] + p.s_tr[(size_t)b * K + k];
-    wfb[k] = p.W_fb[k];
-    v[k] = p.v[k];
+// Decomposition: every kernel runs one CTA per (batch row, chunk of kJC source
+// positions) or (batch row, slice of encoder columns) — ~1000 CTAs, so loads of
+// one CTA overlap the tanh / reduction work of the others on the same SM (one
+// CTA per batch row left 256 CTAs on 148 SMs, half of them alone, at ~25% of
+// HBM).  Inside a CTA every thread owns VK key columns (VE encoder columns) and
+// walks the chunk's positions with per-position partial sums in registers, so
+// every load is an independent coalesced 16 B vector; the per-position dot
+// products finish in one block reduction.  VK = 4 / VE = 8 when K % 4 == 0 /
+// E % 8 == 0 and the rows stay 16 B aligned, else scalar columns.
+constexpr int kJC = 16;        // source positions per CTA (d_a pass)
+constexpr int kJE = 8;         // source positions per CTA (tanh passes: more CTAs resident per SM)
+constexpr int kCtxThreads = 64;  // context kernel: 64 threads x VE columns per CTA ...
+constexpr int kCtxGroups = 4;    // ... times 4 groups splitting the source positions
+
+__device__ __forceinline__ int round_up_dev(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int W>
+struct Vec {
+  float f[W];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < W; ++i) f[i] = 0.f;
   }
-  __syncthreads();
-  const int len = min(max(p.lens[b], 0), Ts);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const float bv = *p.b_v;
-  for (int j = warp; j < len; j += kWarps) {  // energies e_j (tape.cpp ops: add, tanh, matmul v)
-    const float* ctx = p.enc_ctx + ((size_t)b * Ts + j) * K;
-    const float acc_j = p.accum[(size_t)b * Ts + j];
-    float s = 0.f;
-    for (int k = lane; k < K; k += 32) s += v[k] * tanhf(ctx[k] + acc_j * wfb[k] + c[k]);
-    s = warp_sum(s);
-    if (lane == 0) e[j] = s + bv;
-  }
-  __syncthreads();
-  if (warp == 0) {  // masked softmax over the source positions (tape.cpp:952-960)
-    float m = -INFINITY;
-    for (int j = lane; j < len; j += 32) m = fmaxf(m, e[j]);
-    m = warp_max(m);
-    float z = 0.f;
-    for (int j = lane; j < len; j += 32) z += expf(e[j] - m);
-    z = warp_sum(z);
-    for (int j = lane; j < Ts; j += 32) {
-      const float a = j < len ? expf(e[j] - m) / z : 0.f;
-      e[j] = a;
-      p.a[(size_t)b * Ts + j] = a;
-      p.accum_out[(size_t)b * Ts + j] = p.accum[(size_t)b * Ts + j] + a;
+  __device__ __forceinline__ void load(const float* p) {  // read-only data
+    if constexpr (W % 8 == 0) {  // 256-bit loads (32 B aligned rows): half the load instructions
+#pragma unroll
+      for (int i = 0; i < W; i += 8)
+        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(f[i]), "=f"(f[i + 1]), "=f"(f[i + 2]), "=f"(f[i + 3]), "=f"(f[i + 4]), "=f"(f[i + 5]),
+                       "=f"(f[i + 6]), "=f"(f[i + 7])
+                     : "l"(p + i));
+    } else if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W; i += 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i / 4);
+        f[i] = q.x, f[i + 1] = q.y, f[i + 2] = q.z, f[i + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; ++i) f[i] = __ldg(p + i);
     }
   }
+  __device__ __forceinline__ void load_plain(const float* p) {  // data this kernel also writes
+    if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W; i += 4) {
+        const float4 q = reinterpret_cast<const float4*>(p)[i / 4];
+        f[i] = q.x, f[i + 1] = q.y, f[i + 2] = q.z, f[i + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; ++i) f[i] = p[i];
+    }
+  }
+  __device__ __forceinline__ void store(float* p) const {
+    if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W; i += 4)
+        reinterpret_cast<float4*>(p)[i / 4] = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; ++i) p[i] = f[i];
+    }
+  }
+  __device__ __forceinline__ void atomic_add(float* p) const {
+    if constexpr (W % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < W; i += 4)
+        atomicAdd(reinterpret_cast<float4*>(p) + i / 4, make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; ++i) atomicAdd(p + i, f[i]);
+    }
+  }
+};
+
+// tanh(x) = 1 - 2 / (1 + e^{2x}): two MUFU ops, absolute error ~1e-7 (the
+// energies and their adjoint only see tanh through sums, so an absolute bound
+// is the one that matters); clamped so e^{2x} stays finite
+__device__ __forceinline__ float tanh_fast(float x) {
+  x = fminf(fmaxf(x, -15.f), 15.f);
+  return 1.f - __fdividef(2.f, 1.f + __expf(2.f * x));
+}
+
+// sum over the block of per-thread partials part[0..n): result to out[0..n)
+template <int kJC>
+__device__ __forceinline__ void block_reduce_chunk(const float (&part)[kJC], int n, float* red /*[kWarps][kJC]*/,
+                                                   float* out) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // transpose-reduce: after each round a lane holds sums over twice the lanes for half the positions
+  float v[kJC];
+#pragma unroll
+  for (int j = 0; j < kJC; ++j) v[j] = part[j];
+#pragma unroll
+  for (int w = kJC / 2, o = 16; w >= 1; w /= 2, o /= 2) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      const float send = upper ? v[j] : v[j + w];
+      const float keep = upper ? v[j + w] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  float t = v[0];
+#pragma unroll
+  for (int o = 32 / kJC / 2; o >= 1; o /= 2) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane % (32 / kJC) == 0) {  // the position index is spelled by the lane's high bits
+    int j = 0;
+#pragma unroll
+    for (int w = kJC / 2, o = 16; w >= 1; w /= 2, o /= 2)
+      if (lane & o) j += w;
+    red[warp * kJC + j] = t;
+  }
   __syncthreads();
-  // context att[b] = sum_j a_j enc[b, j] (tape.cpp:1005-1014)
-  for (int x = threadIdx.x; x < E; x += kThreads) {
+  if (threadIdx.x < n) {
     float s = 0.f;
-    for (int j = 0; j < len; ++j) s += e[j] * p.enc[((size_t)b * Ts + j) * E + x];
-    p.att[(size_t)b * E + x] = s;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[w * kJC + threadIdx.x];
+    out[threadIdx.x] = s;
   }
 }
 
-__global__ void __launch_bounds__(kThreads) attn_bwd_kernel(AttnArgs p) {
-  extern __shared__ float sm[];
-  const int b = blockIdx.x, K = p.K, Ts = p.Ts, E = p.E;
-  float* c = sm;
-  float* wfb = c + K;
-  float* v = wfb + K;
-  float* ds = v + K;    // d s_tr[b]
-  float* dwf = ds + K;  // d W_fb partial
-  float* dbf = dwf + K; // d b_fb partial
-  float* dv = dbf + K;  // d v partial
-  float* de = dv + K;   // d_a -> d_e [Ts]
-  float* aa = de + Ts;  // a [Ts]
-  for (int k = threadIdx.x; k < K; k += kThreads) {
-    c[k] = p.b_fb[k] + p.s_tr[(size_t)b * K + k];
-    wfb[k] = p.W_fb[k];
-    v[k] = p.v[k];
-    ds[k] = dwf[k] = dbf[k] = dv[k] = 0.f;
-  }
+template <int VK>
+__device__ __forceinline__ void load_cols(const AttnArgs& p, int b, int k, Vec<VK>& c, Vec<VK>& w, Vec<VK>& v) {
+  Vec<VK> bf;
+  c.load(p.s_tr + (size_t)b * p.K + k);
+  bf.load(p.b_fb + k);
+#pragma unroll
+  for (int i = 0; i < VK; ++i) c.f[i] += bf.f[i];
+  w.load(p.W_fb + k);
+  v.load(p.v + k);
+}
+
+// e[b, j] (without b_v) for the CTA's chunk of valid positions:
+// e_j = <v, tanh(enc_ctx_j + accum_j W_fb + b_fb + s_tr)>  (compiler.cpp:616-639)
+template <int VK>
+__global__ void __launch_bounds__(kThreads, 3) attn_energy_kernel(AttnArgs p, float* __restrict__ e_out) {
+  __shared__ float red[kWarps * kJE];
+  const int b = blockIdx.y, j0 = blockIdx.x * kJE, K = p.K, Ts = p.Ts;
   const int len = min(max(p.lens[b], 0), Ts);
-  for (int j = threadIdx.x; j < Ts; j += kThreads) aa[j] = p.a_saved[(size_t)b * Ts + j];
-  __syncthreads();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const float* dattb = p.d_att + (size_t)b * E;
-  // d_a_j = <d_att, enc_j> + d_accum'_j (masked, tape.cpp:1031-1041); d enc_j = a_j d_att
-  for (int j = warp; j < Ts; j += kWarps) {
-    const float* encj = p.enc + ((size_t)b * Ts + j) * E;
-    float* genc = p.d_enc + ((size_t)b * Ts + j) * E;
-    const float aj = aa[j];
-    float s = 0.f;
-    for (int x = lane; x < E; x += 32) {
-      const float g = dattb[x];
-      s += g * encj[x];
-      genc[x] = (p.accumulate ? genc[x] : 0.f) + aj * g;
-    }
-    s = warp_sum(s);
-    if (lane == 0) de[j] = j < len ? s + (p.d_accum_out ? p.d_accum_out[(size_t)b * Ts + j] : 0.f) : 0.f;
+  const int n = min(kJE, len - j0);
+  if (n <= 0) return;
+  float part[kJE], acc[kJE];
+#pragma unroll
+  for (int j = 0; j < kJE; ++j) {
+    part[j] = 0.f;
+    acc[j] = j < n ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
   }
-  __syncthreads();
-  if (warp == 0) {  // softmax adjoint (tape.cpp:966-978)
-    float dot = 0.f;
-    for (int j = lane; j < len; j += 32) dot += de[j] * aa[j];
-    dot = warp_sum(dot);
-    for (int j = lane; j < Ts; j += 32) de[j] = j < len ? aa[j] * (de[j] - dot) : 0.f;
-  }
-  __syncthreads();
-  // through tanh and the adds: d e_in[j, k] = d_e_j v_k (1 - u^2)
-  float dbv = 0.f;
-  for (int j = warp; j < Ts; j += kWarps) {
-    const float dej = de[j];
-    const float* ctx = p.enc_ctx + ((size_t)b * Ts + j) * K;
-    float* gctx = p.d_enc_ctx + ((size_t)b * Ts + j) * K;
-    const float acc_j = p.accum[(size_t)b * Ts + j];
-    float dacc = 0.f;
-    for (int k = lane; k < K; k += 32) {
-      float g = 0.f;
-      if (j < len) {
-        const float u = tanhf(ctx[k] + acc_j * wfb[k] + c[k]);
-        g = dej * v[k] * (1.f - u * u);
-        atomicAdd(&dv[k], u * dej);
-        atomicAdd(&ds[k], g);
-        atomicAdd(&dwf[k], acc_j * g);
-        atomicAdd(&dbf[k], g);
-        dacc += g * wfb[k];
+  for (int k = threadIdx.x * VK; k < K; k += kThreads * VK) {
+    Vec<VK> c, w, v;
+    load_cols(p, b, k, c, w, v);
+    Vec<VK> x[kJE];
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < n) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j) {
+      if (j < n) {
+#pragma unroll
+        for (int i = 0; i < VK; ++i) part[j] += v.f[i] * tanh_fast(x[j].f[i] + acc[j] * w.f[i] + c.f[i]);
       }
-      gctx[k] = (p.accumulate ? gctx[k] : 0.f) + g;
-    }
-    dacc = warp_sum(dacc);
-    if (lane == 0) {
-      const float up = (j < len && p.d_accum_out) ? p.d_accum_out[(size_t)b * Ts + j] : 0.f;
-      float* ga = p.d_accum + (size_t)b * Ts + j;
-      *ga = (p.accumulate ? *ga : 0.f) + up + dacc;
-      dbv += dej;
     }
   }
-  if (lane == 0 && dbv != 0.f) atomicAdd(p.d_b_v, dbv);
+  block_reduce_chunk(part, n, red, e_out + (size_t)b * Ts + j0);
+}
+
+// masked softmax of row b (tape.cpp:952-960) into a_sh[0..Ts) — warp 0
+__device__ __forceinline__ void row_softmax(const AttnArgs& p, const float* e, int b, int len, float* a_sh) {
+  const int lane = threadIdx.x % 32, Ts = p.Ts;
+  const float bv = *p.b_v;
+  float m = -INFINITY;
+  for (int j = lane; j < len; j += 32) m = fmaxf(m, e[(size_t)b * Ts + j] + bv);
+  m = warp_max(m);
+  float z = 0.f;
+  for (int j = lane; j < len; j += 32) z += expf(e[(size_t)b * Ts + j] + bv - m);
+  z = warp_sum(z);
+  for (int j = lane; j < Ts; j += 32) a_sh[j] = j < len ? expf(e[(size_t)b * Ts + j] + bv - m) / z : 0.f;
+}
+
+// softmax (recomputed per CTA from the Ts energies) and the context slice
+// att[b, x0:x1) = sum_j a_j enc[b, j, x0:x1)  (tape.cpp:1005-1014); CTA 0 of
+// the row also writes a and accum'.  kCtxGroups thread groups split the
+// positions (interleaved) for more loads in flight per SM and add their
+// partial sums in a fixed order through shared memory (deterministic).
+template <int VE>
+__global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(AttnArgs p, const float* __restrict__ e) {
+  extern __shared__ float a_sh[];  // [Ts] then [kCtxGroups - 1][kCtxThreads * VE] partials
+  const int b = blockIdx.y, Ts = p.Ts, E = p.E;
+  const int len = min(max(p.lens[b], 0), Ts);
+  if (threadIdx.x < 32) row_softmax(p, e, b, len, a_sh);
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += kThreads) {
-    p.d_s_tr[(size_t)b * K + k] = ds[k];
-    atomicAdd(&p.d_W_fb[k], dwf[k]);
-    atomicAdd(&p.d_b_fb[k], dbf[k]);
-    atomicAdd(&p.d_v[k], dv[k]);
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < Ts; j += kCtxThreads * kCtxGroups) {
+      p.a[(size_t)b * Ts + j] = a_sh[j];
+      p.accum_out[(size_t)b * Ts + j] = p.accum[(size_t)b * Ts + j] + a_sh[j];
+    }
+  const int ct = threadIdx.x % kCtxThreads, grp = threadIdx.x / kCtxThreads;
+  const int x = (blockIdx.x * kCtxThreads + ct) * VE;
+  float* part = a_sh + round_up_dev(Ts, 8);
+  Vec<VE> s;
+  s.zero();
+  if (x < E) {
+    int j = grp;
+    constexpr int G = kCtxGroups;
+    for (; j + 3 * G < len; j += 4 * G) {  // 4 independent loads in flight per thread
+      Vec<VE> q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i].load(p.enc + ((size_t)b * Ts + j + i * G) * E + x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float aj = a_sh[j + i * G];
+#pragma unroll
+        for (int w = 0; w < VE; ++w) s.f[w] += aj * q[i].f[w];
+      }
+    }
+    for (; j < len; j += G) {
+      Vec<VE> q;
+      q.load(p.enc + ((size_t)b * Ts + j) * E + x);
+      const float aj = a_sh[j];
+#pragma unroll
+      for (int w = 0; w < VE; ++w) s.f[w] += aj * q.f[w];
+    }
+    if (grp > 0) s.store(part + ((grp - 1) * kCtxThreads + ct) * VE);
+  }
+  __syncthreads();
+  if (grp == 0 && x < E) {
+#pragma unroll
+    for (int g = 1; g < kCtxGroups; ++g) {
+      Vec<VE> o;
+      o.load_plain(part + ((g - 1) * kCtxThreads + ct) * VE);
+#pragma unroll
+      for (int w = 0; w < VE; ++w) s.f[w] += o.f[w];
+    }
+    s.store(p.att + (size_t)b * E + x);
+  }
+}
+
+// backward 1: d_a[b, j] = <d_att_b, enc_bj> (valid j; tape.cpp:1031-1041) and
+// d enc_bj = a_j d_att_b (every j of the chunk: zero at padded positions)
+template <int VE>
+__global__ void __launch_bounds__(kThreads, 3) attn_bwd_da_kernel(AttnArgs p, float* __restrict__ d_a) {
+  __shared__ float red[kWarps * kJC];
+  const int b = blockIdx.y, j0 = blockIdx.x * kJC, Ts = p.Ts, E = p.E;
+  const int len = min(max(p.lens[b], 0), Ts);
+  const int n = min(kJC, Ts - j0);
+  float part[kJC], aj[kJC];
+#pragma unroll
+  for (int j = 0; j < kJC; ++j) {
+    part[j] = 0.f;
+    aj[j] = j < n ? __ldg(p.a_saved + (size_t)b * Ts + j0 + j) : 0.f;
+  }
+  for (int x = threadIdx.x * VE; x < E; x += kThreads * VE) {
+    Vec<VE> g;
+    g.load(p.d_att + (size_t)b * E + x);
+#pragma unroll
+    for (int j = 0; j < kJC; ++j) {
+      if (j < n) {
+        const size_t off = ((size_t)b * Ts + j0 + j) * E + x;
+        Vec<VE> o;
+        if (p.accumulate) o.load_plain(p.d_enc + off);
+        else o.zero();
+#pragma unroll
+        for (int w = 0; w < VE; ++w) o.f[w] += aj[j] * g.f[w];
+        o.store(p.d_enc + off);
+        if (j0 + j < len) {
+          Vec<VE> q;
+          q.load(p.enc + off);
+#pragma unroll
+          for (int w = 0; w < VE; ++w) part[j] += g.f[w] * q.f[w];
+        }
+      }
+    }
+  }
+  block_reduce_chunk(part, n, red, d_a + (size_t)b * Ts + j0);
+}
+
+// backward 2: softmax adjoint of the row (tape.cpp:966-978; + d accum', masked),
+// then through tanh for the chunk: d e_in[j, k] = d_e_j v_k (1 - u^2) -> d enc_ctx,
+// d accum_j = d accum'_j + <d e_in[j], W_fb>, and the column sums d s_tr[b] /
+// d b_fb / d W_fb / d v (per-thread over the chunk, then vector atomics)
+template <int VK>
+__global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, const float* __restrict__ d_a) {
+  __shared__ float red[kWarps * kJE];
+  __shared__ float de_sh[kJE], sum_sh[kJE];
+  const int b = blockIdx.y, j0 = blockIdx.x * kJE, Ts = p.Ts, K = p.K;
+  const int len = min(max(p.lens[b], 0), Ts);
+  const int n = min(kJE, Ts - j0);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float* da_b = d_a + (size_t)b * Ts;
+  const float* a_b = p.a_saved + (size_t)b * Ts;
+  const float* up_b = p.d_accum_out ? p.d_accum_out + (size_t)b * Ts : nullptr;
+  if (warp == 0) {
+    float dot = 0.f;
+    for (int j = lane; j < len; j += 32) dot += (da_b[j] + (up_b ? up_b[j] : 0.f)) * a_b[j];
+    dot = warp_sum(dot);
+    float dbv = 0.f;
+    if (lane < kJE) {
+      const int jj = j0 + lane;
+      const float d = (lane < n && jj < len) ? a_b[jj] * (da_b[jj] + (up_b ? up_b[jj] : 0.f) - dot) : 0.f;
+      de_sh[lane] = d;
+      dbv = d;
+    }
+    dbv = warp_sum(dbv);
+    if (lane == 0 && dbv != 0.f) atomicAdd(p.d_b_v, dbv);
+  }
+  __syncthreads();
+  float part[kJE], de[kJE], acc[kJE];
+#pragma unroll
+  for (int j = 0; j < kJE; ++j) {
+    part[j] = 0.f;
+    de[j] = de_sh[j];
+    acc[j] = (j < n && j0 + j < len) ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
+  }
+  const int nv = max(0, min(n, len - j0));  // valid positions of the chunk
+  for (int k = threadIdx.x * VK; k < K; k += kThreads * VK) {
+    Vec<VK> c, w, v, ds, dwf, dv;
+    load_cols(p, b, k, c, w, v);
+    ds.zero(), dwf.zero(), dv.zero();
+    Vec<VK> x[kJE];
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < nv) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j) {
+      if (j < n) {
+        const size_t off = ((size_t)b * Ts + j0 + j) * K + k;
+        Vec<VK> gk;
+        if (j < nv) {
+#pragma unroll
+          for (int i = 0; i < VK; ++i) {
+            const float u = tanh_fast(x[j].f[i] + acc[j] * w.f[i] + c.f[i]);
+            gk.f[i] = de[j] * v.f[i] * (1.f - u * u);
+            ds.f[i] += gk.f[i];
+            dwf.f[i] += acc[j] * gk.f[i];
+            dv.f[i] += u * de[j];
+            part[j] += gk.f[i] * w.f[i];
+          }
+        } else {
+          gk.zero();
+        }
+        if (p.accumulate) {
+          Vec<VK> o;
+          o.load_plain(p.d_enc_ctx + off);
+#pragma unroll
+          for (int i = 0; i < VK; ++i) gk.f[i] += o.f[i];
+        }
+        gk.store(p.d_enc_ctx + off);
+      }
+    }
+    if (nv > 0) {
+      ds.atomic_add(p.d_s_tr + (size_t)b * K + k);
+      ds.atomic_add(p.d_b_fb + k);
+      dwf.atomic_add(p.d_W_fb + k);
+      dv.atomic_add(p.d_v + k);
+    }
+  }
+  block_reduce_chunk(part, n, red, sum_sh);
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int jj = j0 + threadIdx.x;
+    const float up = (jj < len && up_b) ? up_b[jj] : 0.f;
+    float* ga = p.d_accum + (size_t)b * Ts + jj;
+    *ga = (p.accumulate ? *ga : 0.f) + up + (jj < len ? sum_sh[threadIdx.x] : 0.f);
   }
 }
 
@@ -176,50 +411,88 @@ __global__ void colsum_kernel(const float* x, int rows, int cols, float* out) {
 
 }  // namespace
 
-size_t attention_workspace_bytes(int B, int K) { return (size_t)2 * B * K * sizeof(float) + 256; }
+// workspace: s_tr [B, K] | d_s_tr [B, K] | e / d_a [B, Ts] | split-bf16 operands of the projection GEMMs
+static size_t x3_bytes(int B, int K, int H) {
+  return std::max({gemm_f32x3_workspace_bytes(false, false, B, K, H, false),   // s_tr = s W_s
+                   gemm_f32x3_workspace_bytes(false, true, B, H, K, false),    // d s = d s_tr W_s^T
+                   gemm_f32x3_workspace_bytes(true, false, H, K, B, true)});   // [d W_s; d b_s]
+}
+static size_t ws_head(int B, int K, int Ts) {
+  return (size_t)round_up((int64_t)2 * B * K * sizeof(float), 256) + (size_t)round_up((int64_t)B * Ts * 4, 256);
+}
+size_t attention_workspace_bytes(int B, int K, int H, int Ts) { return ws_head(B, K, Ts) + x3_bytes(B, K, H) + 256; }
+static float* row_buf(const AttnArgs& p, void* ws) {  // e (forward) / d_a (backward) [B, Ts]
+  return reinterpret_cast<float*>(static_cast<char*>(ws) + round_up((int64_t)2 * p.B * p.K * sizeof(float), 256));
+}
+static void* x3_ws(const AttnArgs& p, void* ws) { return static_cast<char*>(ws) + ws_head(p.B, p.K, p.Ts); }
 
-static size_t fwd_smem(const AttnArgs& p) { return (size_t)(3 * p.K + p.Ts) * sizeof(float); }
-static size_t bwd_smem(const AttnArgs& p) { return (size_t)(7 * p.K + 2 * p.Ts) * sizeof(float); }
+static bool al16(const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+static bool al32(const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 31) == 0; }
+// vector widths: 4 key / 8 encoder columns per thread when every row stays 16 B aligned
+static int vec_k(const AttnArgs& p) {
+  return (p.K % 4 == 0 && al16(p.enc_ctx) && al16(p.d_enc_ctx) && al16(p.s_tr) && al16(p.d_s_tr) && al16(p.b_fb) &&
+          al16(p.W_fb) && al16(p.v) && al16(p.d_W_fb) && al16(p.d_b_fb) && al16(p.d_v))
+             ? 4
+             : 1;
+}
+static int vec_e(const AttnArgs& p) {
+  return (p.E % 8 == 0 && al32(p.enc) && al32(p.d_enc) && al32(p.d_att) && al32(p.att)) ? 8 : 1;
+}
 
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {
   p.s_tr = static_cast<float*>(ws);
-  gemm_f32(false, false, p.B, p.K, p.H, 1.f, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, st);  // s_tr = s W_s + b_s
-  const size_t smem = fwd_smem(p);
-  SL_REQUIRE(smem <= 227 * 1024, SL_ERR_UNSUPPORTED, "attention: key_dim / src_time too large");
-  SL_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws),
+             st);  // s_tr = s W_s + b_s
+  float* e = row_buf(p, ws);
   Phase ph(st, "k8_attention_fwd", 0.0, 4.0 * p.B * p.Ts * (double)(p.K + p.E));
-  attn_fwd_kernel<<<p.B, kThreads, smem, st>>>(p);
+  const dim3 g1((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
+  if (vec_k(p) == 4) attn_energy_kernel<4><<<g1, kThreads, 0, st>>>(p, e);
+  else attn_energy_kernel<1><<<g1, kThreads, 0, st>>>(p, e);
   SL_CUDA_TRY(cudaGetLastError());
-  count_launch();
+  const int ve = vec_e(p);
+  const dim3 g2((unsigned)ceil_div(p.E, kCtxThreads * ve), (unsigned)p.B);
+  const size_t smem = (size_t)(round_up(p.Ts, 8) + (kCtxGroups - 1) * kCtxThreads * ve) * sizeof(float);
+  SL_REQUIRE(smem <= 48 * 1024, SL_ERR_UNSUPPORTED, "attention: src_time too large");
+  if (ve == 8) attn_context_kernel<8><<<g2, kCtxThreads * kCtxGroups, smem, st>>>(p, e);
+  else attn_context_kernel<1><<<g2, kCtxThreads * kCtxGroups, smem, st>>>(p, e);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch(2);
 }
 
 void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, float* d_s, float* d_W_s,
                    float* d_b_s, void* ws, cudaStream_t st) {
   p.s_tr = static_cast<float*>(ws);
   p.d_s_tr = p.s_tr + (size_t)p.B * p.K;
-  gemm_f32(false, false, p.B, p.K, p.H, 1.f, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, st);  // recompute s_tr
+  gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws),
+             st);  // recompute s_tr
   if (!p.accumulate) {
     SL_CUDA_TRY(cudaMemsetAsync(p.d_W_fb, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_b_fb, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_v, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_b_v, 0, sizeof(float), st));
-    if (d_b_s) SL_CUDA_TRY(cudaMemsetAsync(d_b_s, 0, sizeof(float) * p.K, st));
+    if (d_b_s && !d_W_s) SL_CUDA_TRY(cudaMemsetAsync(d_b_s, 0, sizeof(float) * p.K, st));
   }
-  const size_t smem = bwd_smem(p);
-  SL_REQUIRE(smem <= 227 * 1024, SL_ERR_UNSUPPORTED, "attention: key_dim / src_time too large");
-  SL_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SL_CUDA_TRY(cudaMemsetAsync(p.d_s_tr, 0, sizeof(float) * p.B * p.K, st));
+  float* d_a = row_buf(p, ws);
   {
     Phase ph(st, "k8_attention_bwd", 0.0, 4.0 * p.B * p.Ts * (double)(2 * p.K + 2 * p.E));
-    attn_bwd_kernel<<<p.B, kThreads, smem, st>>>(p);
+    const dim3 g((unsigned)ceil_div(p.Ts, kJC), (unsigned)p.B), ge((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
+    if (vec_e(p) == 8) attn_bwd_da_kernel<8><<<g, kThreads, 0, st>>>(p, d_a);
+    else attn_bwd_da_kernel<1><<<g, kThreads, 0, st>>>(p, d_a);
     SL_CUDA_TRY(cudaGetLastError());
-    count_launch();
+    if (vec_k(p) == 4) attn_bwd_de_kernel<4><<<ge, kThreads, 0, st>>>(p, d_a);
+    else attn_bwd_de_kernel<1><<<ge, kThreads, 0, st>>>(p, d_a);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch(2);
   }
   const float beta = p.accumulate ? 1.f : 0.f;
   if (d_s)  // d s = d s_tr W_s^T
-    gemm_f32(false, true, p.B, p.H, p.K, 1.f, p.d_s_tr, p.K, W_s, p.K, beta, d_s, p.H, nullptr, st);
-  if (d_W_s)  // d W_s = s^T d s_tr
-    gemm_f32(true, false, p.H, p.K, p.B, 1.f, s, p.H, p.d_s_tr, p.K, beta, d_W_s, p.K, nullptr, st);
-  if (d_b_s) {
+    gemm_f32x3(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, W_s, p.K, beta, d_s, p.H, nullptr, nullptr, 0,
+               x3_ws(p, ws), st);
+  if (d_W_s)  // [d W_s; d b_s] = [s | 1]^T d s_tr
+    gemm_f32x3(true, false, p.H, p.K, p.B, s, p.H, p.d_s_tr, p.K, beta, d_W_s, p.K, nullptr, d_b_s, p.K,
+               x3_ws(p, ws), st);
+  else if (d_b_s) {
     colsum_kernel<<<(unsigned)ceil_div(p.K, 256), 256, 0, st>>>(p.d_s_tr, p.B, p.K, d_b_s);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();

@@ -34,7 +34,7 @@ struct AttnArgs {
   int accumulate;
 };
 
-size_t attention_workspace_bytes(int B, int K);
+size_t attention_workspace_bytes(int B, int K, int H, int Ts);
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st);
 void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, float* d_s, float* d_W_s,
                    float* d_b_s, void* ws, cudaStream_t st);

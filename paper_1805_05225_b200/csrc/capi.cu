@@ -260,8 +260,8 @@ static void check_attention(const sl_attention* at) {
 }
 
 size_t sl_attention_workspace_size(const sl_attention* at) {
-  if (!at || at->batch <= 0 || at->key_dim <= 0) return 0;
-  return attention_workspace_bytes(at->batch, at->key_dim);
+  if (!at || at->batch <= 0 || at->key_dim <= 0 || at->state_dim <= 0) return 0;
+  return attention_workspace_bytes(at->batch, at->key_dim, at->state_dim, at->src_time);
 }
 
 static AttnArgs attn_args(const sl_attention* at, const int32_t* lens, const float* enc_ctx, const float* enc,
@@ -292,7 +292,7 @@ int sl_attention_step_fwd(const sl_attention* at, const int32_t* src_lens, const
     SL_REQUIRE(src_lens && enc_ctx && enc && s && accum && W_s && b_s && W_fb && b_fb && v && b_v && att_out &&
                    a && accum_out,
                SL_ERR_INVALID_ARGUMENT, "attention fwd: null pointer argument");
-    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim),
+    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim, at->state_dim, at->src_time),
                SL_ERR_WORKSPACE, "attention: workspace too small");
     AttnArgs p = attn_args(at, src_lens, enc_ctx, enc, accum, W_fb, b_fb, v);
     p.b_v = b_v;
@@ -315,7 +315,7 @@ int sl_attention_step_bwd(const sl_attention* at, const int32_t* src_lens, const
     SL_REQUIRE(src_lens && enc_ctx && enc && s && accum && W_s && b_s && W_fb && b_fb && v && a && d_att &&
                    d_enc_ctx && d_enc && d_accum && d_W_fb && d_b_fb && d_v && d_b_v,
                SL_ERR_INVALID_ARGUMENT, "attention bwd: null pointer argument");
-    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim),
+    SL_REQUIRE(workspace && workspace_bytes >= attention_workspace_bytes(at->batch, at->key_dim, at->state_dim, at->src_time),
                SL_ERR_WORKSPACE, "attention: workspace too small");
     AttnArgs p = attn_args(at, src_lens, enc_ctx, enc, accum, W_fb, b_fb, v);
     p.a_saved = a;

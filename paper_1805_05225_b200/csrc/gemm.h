@@ -9,6 +9,15 @@ void gemm_f32(bool transA, bool transB, int M, int N, int K, float alpha, const 
               int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
               const float* bias, cudaStream_t stream);
 
+// fp32-accurate GEMM on the bf16 tensor cores via split-bf16 operands
+// (gemm_f32x3.cu): C = op(A) op(B) + beta C + bias.  With ones_row_out, A must be
+// stored [K, M] (transA) and the column sums of op(B) (= ones^T op(B)) are also
+// written to ones_row_out (+ beta * previous) — the bias gradient for free.
+size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K, bool a_ones);
+void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
+                int64_t ld_ones, void* ws, cudaStream_t st);
+
 }  // namespace sl
 
 namespace sl {
@@ -43,7 +52,13 @@ struct TcGemm {
   float4* sm_part = nullptr;
   int sm_ld = 0;
   const int32_t* sm_targets = nullptr;
+  // optional (pair GEMM only): split K into ksplit ranges; range z writes its plain
+  // fp32 partial product (alpha = 1, no bias / beta / C2) to C + z * split_stride
+  int ksplit = 1;
+  int64_t split_stride = 0;
 };
+// number of K splits the pair GEMM would use to fill the SMs for this shape
+int gemm_tc2_ksplit(int M, int N, int K);
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 // CTA-pair variant (gemm_tc2.cu, M = 256 tiles); gemm_bf16_tc dispatches to it
 // when the operands allow (gemm_bf16_tc2_ok) unless SL_GEMM_1CTA is set.

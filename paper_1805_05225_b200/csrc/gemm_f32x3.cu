@@ -1,0 +1,155 @@
+// fp32-accurate GEMM on the bf16 tensor cores (split-bf16, "3 x bf16"):
+//   x = x_hi + x_lo with x_hi = bf16(x), x_lo = bf16(x - x_hi)  (|x_lo| <= 2^-9 |x|)
+//   A B ~= A_hi B_hi + A_lo B_hi + A_hi B_lo          (dropped A_lo B_lo ~ 2^-18)
+// computed as ONE tcgen05 GEMM over a K dimension tripled by concatenation,
+//   [A_hi | A_lo | A_hi] . [B_hi ; B_hi ; B_lo]
+// with fp32 accumulation in TMEM — relative error ~1e-5, i.e. fp32-class for
+// the tolerances the reference's fp32 CPU path is held to, at tensor-core
+// speed.  Used where a small fp32 GEMM would otherwise leave most SMs idle on
+// the SIMT path (the attention step's s W_s projections: M = batch).
+#include "convert.h"
+#include "gemm.h"
+#include "profile.h"
+
+namespace sl {
+namespace {
+
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// S [rows, cols] (ld) -> three copies along the K dimension (k_cols: K = cols, else K = rows),
+// each copy padded to Kp with zeros; copy i holds hi unless lo_mask bit i is set.
+// ones_col >= 0 (K = rows only): that column is 1 (hi) / 0 (lo) for k < K.
+// One CTA row per (extended) source row, two contiguous columns per thread.
+__global__ void split3_kernel(const float* __restrict__ S, int64_t ld, int rows, int cols, bool k_cols, int Kp,
+                              int lo_mask, int ones_col, __nv_bfloat16* __restrict__ D, int64_t dld) {
+  const int r = blockIdx.y;
+  const int cols_ext = k_cols ? Kp : cols + (ones_col >= 0 ? 1 : 0);
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c >= cols_ext) return;
+  float x[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int cc = c + i;
+    x[i] = 0.f;
+    if (r < rows && cc < cols) x[i] = S[(int64_t)r * ld + cc];
+    else if (r < rows && cc == ones_col) x[i] = 1.f;
+  }
+  __nv_bfloat16 hi[2], lo[2];
+  split_bf16(x[0], hi[0], lo[0]);
+  split_bf16(x[1], hi[1], lo[1]);
+  const bool pair = c + 1 < cols_ext;
+#pragma unroll
+  for (int copy = 0; copy < 3; ++copy) {
+    const bool use_lo = (lo_mask >> copy) & 1;
+    __nv_bfloat16* dst = k_cols ? D + (int64_t)r * dld + copy * Kp + c : D + (int64_t)(copy * Kp + r) * dld + c;
+    if (pair) {
+      __nv_bfloat162 v;
+      v.x = use_lo ? lo[0] : hi[0];
+      v.y = use_lo ? lo[1] : hi[1];
+      *reinterpret_cast<__nv_bfloat162*>(dst) = v;
+    } else {
+      *dst = use_lo ? lo[0] : hi[0];
+    }
+  }
+}
+
+// C[m, n] = sum_z P[z][m, n] (fixed order: deterministic) + bias[n] + beta C[m, n]; rows >= m_split -> C2
+__global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t pstride, int64_t pld, int N,
+                                     float beta, float* C, int64_t ldc, const float* __restrict__ bias, int m_split,
+                                     float* C2, int64_t ldc2) {
+  const int m = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const float* src = P + (int64_t)m * pld + n;
+  float s = 0.f;
+#pragma unroll 4
+  for (int z = 0; z < S; ++z) s += __ldg(src + z * pstride);
+  if (bias) s += bias[n];
+  float* dst = m >= m_split ? C2 + (int64_t)(m - m_split) * ldc2 + n : C + (int64_t)m * ldc + n;
+  if (beta != 0.f) s += beta * *dst;
+  *dst = s;
+}
+
+struct X3Dims {
+  int Kp;
+  int64_t a_rows, a_ld, b_rows, b_ld;  // stored bf16 operands
+  int ksplit;
+  int64_t p_ld, p_stride;  // split-K partials [ksplit][M (+1)][p_ld] fp32
+};
+
+X3Dims x3_dims(bool transA, bool transB, int M, int N, int K, bool a_ones) {
+  X3Dims d;
+  d.Kp = (int)round_up(K, 8);
+  // A: op(A) = A [M, K] -> K along columns; op(A) = A^T (A stored [K, M]) -> K along rows
+  if (!transA) d.a_rows = M, d.a_ld = 3 * (int64_t)d.Kp;
+  else d.a_rows = 3 * (int64_t)d.Kp, d.a_ld = round_up(M + (a_ones ? 1 : 0), 64);
+  // B: op(B) = B stored [K, N] -> K along rows; op(B) = B^T (B stored [N, K]) -> K along columns
+  if (!transB) d.b_rows = 3 * (int64_t)d.Kp, d.b_ld = round_up(N, 64);
+  else d.b_rows = N, d.b_ld = 3 * (int64_t)d.Kp;
+  const int Mt = M + (a_ones ? 1 : 0);
+  d.ksplit = gemm_tc2_ksplit(Mt, N, 3 * d.Kp);
+  d.p_ld = round_up(N, 4);
+  d.p_stride = round_up((int64_t)Mt * d.p_ld, 64);
+  return d;
+}
+
+void split3(const float* S, int64_t ld, int rows, int cols, bool k_cols, int Kp, int lo_mask, int ones_col,
+            __nv_bfloat16* D, int64_t dld, cudaStream_t st) {
+  const int rows_ext = k_cols ? rows : Kp;
+  const int cols_ext = k_cols ? Kp : cols + (ones_col >= 0 ? 1 : 0);
+  const dim3 grid((unsigned)ceil_div(cols_ext, 256), (unsigned)rows_ext);
+  split3_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace
+
+size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K, bool a_ones) {
+  const X3Dims d = x3_dims(transA, transB, M, N, K, a_ones);
+  return (size_t)round_up(d.a_rows * d.a_ld * 2, 256) + (size_t)round_up(d.b_rows * d.b_ld * 2, 256) +
+         (d.ksplit > 1 ? (size_t)d.ksplit * d.p_stride * 4 : 0);
+}
+
+void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
+                int64_t ld_ones, void* ws, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  const bool a_ones = ones_row_out != nullptr;
+  SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
+  const X3Dims d = x3_dims(transA, transB, M, N, K, a_ones);
+  auto* a3 = static_cast<__nv_bfloat16*>(ws);
+  auto* b3 = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ws) + round_up(d.a_rows * d.a_ld * 2, 256));
+  // A copies: hi, lo, hi (lo_mask 0b010); B copies: hi, hi, lo (0b100)
+  if (!transA) split3(A, lda, M, K, true, d.Kp, 0b010, -1, a3, d.a_ld, st);
+  else split3(A, lda, K, M, false, d.Kp, 0b010, a_ones ? M : -1, a3, d.a_ld, st);
+  if (!transB) split3(B, ldb, K, N, false, d.Kp, 0b100, -1, b3, d.b_ld, st);
+  else split3(B, ldb, N, K, true, d.Kp, 0b100, -1, b3, d.b_ld, st);
+  TcGemm g{M + (a_ones ? 1 : 0), N, 3 * d.Kp, a3, d.a_ld, transA, b3, d.b_ld, !transB, C, ldc, 1.f, beta, bias};
+  if (d.ksplit > 1) {  // small output: split K over the idle SMs, then a fixed-order reduction
+    float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(b3) + round_up(d.b_rows * d.b_ld * 2, 256));
+    g.C = part;
+    g.ldc = d.p_ld;
+    g.beta = 0.f;
+    g.bias = nullptr;
+    g.ksplit = d.ksplit;  // gemm_tc2_ksplit already returns a count without empty units
+    g.split_stride = d.p_stride;
+    gemm_bf16_tc(g, st);
+    const int Mt = M + (a_ones ? 1 : 0);
+    splitk_reduce_kernel<<<dim3((unsigned)ceil_div(N, 256), (unsigned)Mt), 256, 0, st>>>(
+        part, d.ksplit, d.p_stride, d.p_ld, N, beta, C, ldc, bias, a_ones ? M : (1 << 30), ones_row_out, ld_ones);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    return;
+  }
+  if (a_ones) {
+    g.m_split = M;
+    g.C2 = ones_row_out;
+    g.ldc2 = ld_ones;
+  }
+  gemm_bf16_tc(g, st);
+}
+
+}  // namespace sl

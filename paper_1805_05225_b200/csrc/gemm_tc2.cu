@@ -44,7 +44,18 @@ struct P2 {
   float4* sm_part;  // softmax partials (gemm.h TcGemm::sm_part)
   int sm_ld;
   const int32_t* sm_targets;
+  int ksplit, kb_per;    // split-K: work unit t -> tile t % tiles, K blocks [z kb_per, (z + 1) kb_per), z = t / tiles
+  int64_t split_stride;  // ... written to C + z * split_stride
 };
+
+// K-block range of work unit t (split-K; ksplit == 1: the whole K)
+__device__ __forceinline__ void unit_kb(const P2& p, int t, int& tile, int& kb0, int& kb1, int& z) {
+  const int tiles = p.nm * p.nn;
+  tile = t % tiles;
+  z = t / tiles;
+  kb0 = z * p.kb_per;
+  kb1 = min(p.nk, kb0 + p.kb_per);
+}
 
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -140,15 +151,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   cluster_sync_all();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_sh;
-  const int ntiles = p.nm * p.nn;
+  const int ntiles = p.nm * p.nn * p.ksplit;  // work units
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int st = 0;
       uint32_t ph = 0;
       for (int t = pair; t < ntiles; t += npairs) {
-        const int m0 = (t % p.nm) * BMP + r * 128, n0 = (t / p.nm) * BNP + r * 128;
-        for (int kb = 0; kb < p.nk; ++kb) {
+        int tile, kb0, kb1, z;
+        unit_kb(p, t, tile, kb0, kb1, z);
+        const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP + r * 128;
+        for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty_bar[st], ph ^ 1);
           const uint32_t sa = base + st * kStage, sb = sa + kHalf;
           const uint32_t fb = mapa_u32(tc::smem_u32(&full_bar[st]), 0);  // leader's barrier
@@ -175,7 +188,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         const int acc = it & 1;
         tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after_sync();
-        for (int kb = 0; kb < p.nk; ++kb) {
+        int tile, kb0, kb1, z;
+        unit_kb(p, t, tile, kb0, kb1, z);
+        for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full_bar[st], ph);
           tc::fence_after_sync();
           const uint32_t sa = base + st * kStage, sb = sa + kHalf;
@@ -185,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                                      : tc::make_sdesc(sa + k * 32, 0, 1024);
             const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, 8192, 1024)
                                      : tc::make_sdesc(sb + k * 32, 0, 1024);
-            mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb | k) != 0);
+            mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           commit_pair(&empty_bar[st]);  // frees the slot in both CTAs
           if (++st == kStages) {
@@ -204,12 +219,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     int it = 0;
     for (int t = pair; t < ntiles; t += npairs, ++it) {
       const int acc = it & 1;
-      const int m0 = (t % p.nm) * BMP + r * 128, n0 = (t / p.nm) * BNP;
+      int tile, kb0, kb1, z;
+      unit_kb(p, t, tile, kb0, kb1, z);
+      const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP;
       tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc::fence_after_sync();
       const int row = m0 + 32 * q + lane;
       const bool second = row >= p.m_split;
-      float* crow = second ? p.C2 + (int64_t)(row - p.m_split) * p.ldc2 : p.C + (int64_t)row * p.ldc;
+      float* crow = second ? p.C2 + (int64_t)(row - p.m_split) * p.ldc2
+                           : p.C + z * p.split_stride + (int64_t)row * p.ldc;
       const bool vec = second ? (p.ldc2 % 4) == 0 && ((uintptr_t)p.C2 & 15) == 0
                               : (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0;
       constexpr int kColsPerWarp = BNP / (kEpiWarps / 4);
@@ -389,7 +407,7 @@ void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     configured = true;
   }
-  const int tiles = p.nm * p.nn;
+  const int tiles = p.nm * p.nn * p.ksplit;
   const int pairs = std::min(tiles, sms2() / 2);
   kern<<<2 * pairs, kThreads, kSmem, s>>>(a, b, p);
   SL_CUDA_TRY(cudaGetLastError());
@@ -397,6 +415,17 @@ void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream
 }
 
 }  // namespace
+
+int gemm_tc2_ksplit(int M, int N, int K) {
+  const int tiles = (int)(ceil_div(M, BMP) * ceil_div(N, BNP));
+  const int nk = (int)ceil_div(K, BK);
+  // fill the SM pairs, keeping >= 4 K blocks per unit so the 6-stage pipeline still streams;
+  // only for a handful of output tiles — beyond that the partials' extra HBM round trip and
+  // the reduction cost more than the idle SMs
+  if (tiles > 8) return 1;
+  const int want = std::max(1, std::min(sms2() / 2 / tiles, nk / 4));
+  return (int)ceil_div(nk, ceil_div(nk, want));  // the count gemm_bf16_tc2 actually runs (no empty units)
+}
 
 bool gemm_bf16_tc2_ok(const TcGemm& g) {
   // MN-major operands must be loadable as whole 64-wide blocks (3-D boxes)
@@ -420,6 +449,18 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   p.C2 = g.C2;
   p.ldc2 = g.ldc2;
   p.Cb = g.Cb;
+  p.ksplit = 1;
+  p.kb_per = p.nk;
+  p.split_stride = 0;
+  if (g.ksplit > 1) {  // fp32 partial products only (the caller reduces them)
+    SL_REQUIRE(!g.Cb && !g.bias && g.beta == 0.f && g.m_split >= g.M, SL_ERR_INVALID_ARGUMENT,
+               "gemm_bf16_tc2: split-K writes plain fp32 partials");
+    p.kb_per = (int)ceil_div(p.nk, g.ksplit);
+    p.ksplit = (int)ceil_div(p.nk, p.kb_per);  // no empty units
+    SL_REQUIRE(p.ksplit == g.ksplit, SL_ERR_INVALID_ARGUMENT,
+               "gemm_bf16_tc2: split count must be one gemm_tc2_ksplit returns (every partial written)");
+    p.split_stride = g.split_stride;
+  }
   SL_REQUIRE(((uintptr_t)g.A & 15) == 0 && ((uintptr_t)g.B & 15) == 0 && (g.lda * 2) % 16 == 0 &&
                  (g.ldb * 2) % 16 == 0,
              SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: operands need 16 B alignment");
