@@ -25,9 +25,11 @@ class BLSTMEncoder:
                    for D in [input_dim] + [2 * H] * (num_layers - 1))
 
     def __init__(self, num_layers: int, batch: int, time: int, input_dim: int, hidden: int,
-                 precision: str = "bf16", device=None, params=None, grads=None):
+                 precision: str = "bf16", device=None, params=None, grads=None, train: bool = True):
         """params / grads: optional flat fp32 views (numel() elements) to live in,
-        e.g. slices of a whole model's buffers; by default the encoder owns them."""
+        e.g. slices of a whole model's buffers; by default the encoder owns them.
+        train=False: inference only (no reserves, no gradients, one workspace
+        shared by all layers — BASELINE config 5)."""
         self.L, self.B, self.T, self.D0, self.H = num_layers, batch, time, input_dim, hidden
         self.precision = precision
         self.device = torch.device(device or "cuda")
@@ -38,14 +40,17 @@ class BLSTMEncoder:
         total = sum(self.layer_numel)
         self.params = params if params is not None else torch.empty(total, dtype=torch.float32,
                                                                      device=self.device)
-        self.grads = grads if grads is not None else torch.zeros(total, dtype=torch.float32,
-                                                                  device=self.device)
-        assert self.params.numel() == total and self.grads.numel() == total
+        if grads is None:
+            grads = torch.zeros(total if train else 0, dtype=torch.float32, device=self.device)
+        self.grads = grads
+        self.train = train
+        assert self.params.numel() == total and (self.grads.numel() == total or not train)
         self.p_views, self.g_views, self.buckets = [], [], []
         off = 0
         for l, D in enumerate(self.in_dims):
             n = self.layer_numel[l]
-            self.buckets.append(self.grads[off:off + n])
+            if train:
+                self.buckets.append(self.grads[off:off + n])
             pv, gv = [], []
             for _ in range(2):  # fw, bw
                 for shape in ((D, 4 * H), (H, 4 * H), (4 * H,)):
@@ -53,7 +58,8 @@ class BLSTMEncoder:
                     for s in shape:
                         k *= s
                     pv.append(self.params[off:off + k].view(shape))
-                    gv.append(self.grads[off:off + k].view(shape))
+                    if train:
+                        gv.append(self.grads[off:off + k].view(shape))
                     off += k
             self.p_views.append(pv)
             self.g_views.append(gv)
@@ -62,15 +68,27 @@ class BLSTMEncoder:
         # the top layer's output is fp32
         chain = precision == "bf16"
         last = num_layers - 1
+        shared = None
+        if not train:  # the layers run one after another: one workspace serves all of them
+            need = max(lstm.LSTMLayer.workspace_size(batch, time, D, H, 2, 1, precision,
+                                                     x_bf16=chain and l > 0, y_bf16=chain and l < last)
+                       for l, D in enumerate(self.in_dims))
+            shared = torch.empty(need, dtype=torch.uint8, device=self.device)
         self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device,
-                                      x_bf16=chain and l > 0, y_bf16=chain and l < last)
+                                      x_bf16=chain and l > 0, y_bf16=chain and l < last,
+                                      train=train, workspace=shared)
                        for l, D in enumerate(self.in_dims)]
-        self.acts = [torch.zeros(batch, time, lstm.bf16_pitch(2 * H), dtype=torch.bfloat16,
-                                 device=self.device) if chain and l < last else
-                     torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
-                     for l in range(num_layers)]
+        def act(l):  # layer l's output buffer
+            if chain and l < last:
+                return torch.zeros(batch, time, lstm.bf16_pitch(2 * H), dtype=torch.bfloat16, device=self.device)
+            return torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
+        if train:
+            self.acts = [act(l) for l in range(num_layers)]
+        else:  # inference keeps nothing for a backward: the inner layers ping-pong two buffers
+            inner = [act(l) for l in range(min(2, last))]
+            self.acts = [inner[l % 2] for l in range(last)] + [act(last)]
         self.dxs = [torch.empty(batch, time, D, dtype=torch.float32, device=self.device)
-                    for D in self.in_dims]
+                    for D in self.in_dims] if train else []
 
     def param_names(self):
         """Reference naming (compiler.cpp:488-492): enc{l}_{fw,bw}/{W,R,b}."""
@@ -97,7 +115,8 @@ class BLSTMEncoder:
         v = self.p_views[l]
         return [v[0], v[3]], [v[1], v[4]], [v[2], v[5]]
 
-    def forward(self, x, seq_lens, train: bool = True):
+    def forward(self, x, seq_lens, train: bool = None):
+        train = self.train if train is None else train
         inp = x
         for l in range(self.L):
             W, R, b = self._wrb(l)

@@ -119,9 +119,13 @@ class LSTMLayer:
 
     def __init__(self, batch: int, time: int, input_dim: int, hidden: int, num_dirs: int = 1,
                  direction: int = 1, precision: str = "fp32", device=None, x_bf16: bool = False,
-                 y_bf16: bool = False):
+                 y_bf16: bool = False, train: bool = True, workspace=None):
         # x_bf16 / y_bf16: padded bf16 activations between stacked layers
-        # (SL_LAYER_X_BF16 / SL_LAYER_Y_BF16, bf16 precision only)
+        # (SL_LAYER_X_BF16 / SL_LAYER_Y_BF16, bf16 precision only).
+        # train=False: an inference-only layer (the reference's grad-disabled
+        # Tape(false), tape.cpp:103) — no reserve is allocated and forward()
+        # saves nothing.  workspace: an optional caller-owned uint8 buffer of at
+        # least workspace_size() bytes (stacked inference layers can share one).
         flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
         self.x_bf16, self.y_bf16 = x_bf16, y_bf16
         self.desc = _Layer(batch, time, input_dim, hidden, num_dirs, direction,
@@ -131,9 +135,24 @@ class LSTMLayer:
         _check(L.sl_lstm_layer_check(ctypes.byref(self.desc)))
         self.reserve_bytes = L.sl_lstm_reserve_size(ctypes.byref(self.desc))
         self.workspace_bytes = L.sl_lstm_workspace_size(ctypes.byref(self.desc))
-        self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
-        self.reserve = torch.empty(self.reserve_bytes, dtype=torch.uint8, device=self.device)
+        if workspace is not None:
+            if workspace.dtype != torch.uint8 or workspace.numel() < self.workspace_bytes:
+                raise ValueError(f"workspace: need >= {self.workspace_bytes} uint8 bytes")
+            self.workspace = workspace
+        else:
+            self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self.train = train
+        if not train:
+            self.reserve_bytes = 0
+        self.reserve = torch.empty(self.reserve_bytes, dtype=torch.uint8, device=self.device) if train else None
         self._saved = None
+
+    @staticmethod
+    def workspace_size(batch, time, input_dim, hidden, num_dirs=1, direction=1, precision="fp32",
+                       x_bf16=False, y_bf16=False) -> int:
+        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
+        d = _Layer(batch, time, input_dim, hidden, num_dirs, direction, PRECISIONS[precision], flags)
+        return lib().sl_lstm_workspace_size(ctypes.byref(d))
 
     @property
     def shape(self):
@@ -143,6 +162,8 @@ class LSTMLayer:
     def forward(self, x, seq_lens, W: Sequence, R: Sequence, b: Sequence, y=None, h_last=None,
                 c_last=None, train: bool = True):
         B, T, D, H, nd = self.shape
+        if train and not self.train:
+            raise RuntimeError("forward(train=True) on an inference-only layer (constructed with train=False)")
         if self.x_bf16:
             _need(x, (B, T, bf16_pitch(D)), "x", torch.bfloat16)
         else:

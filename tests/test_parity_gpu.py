@@ -525,3 +525,25 @@ def test_seq2seq_with_output_layer_matches_fp64(cuda):
     assert rel(m.out_g[0], dWo) < 2e-2 and rel(m.out_g[1], dbo) < 2e-2
     for t_, r_ in zip(m.dec_g, (dref["dW"], dref["dR"], dref["db"])):
         assert rel(t_, r_) < 3e-2
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_inference_encoder_matches_training_forward(cuda, prec):
+    # BASELINE config 5 path: an inference-only encoder (no reserves, shared
+    # workspace, ping-pong activations) gives bit-identical outputs to the
+    # training encoder's forward on the same parameters and ragged lengths
+    from paper_1805_05225_b200.encoder import BLSTMEncoder
+    L, B, T, D, H = 3, 5, 9, 7, 24
+    tr = BLSTMEncoder(L, B, T, D, H, precision=prec)
+    tr.init_uniform(3)
+    inf = BLSTMEncoder(L, B, T, D, H, precision=prec, params=tr.params.clone(), train=False)
+    assert all(layer.reserve is None for layer in inf.layers)
+    g = torch.Generator().manual_seed(5)
+    x = (torch.rand(B, T, D, generator=g) * 2 - 1).cuda()
+    lens = torch.tensor([9, 5, 1, 7, 9], dtype=torch.int32).cuda()
+    y_tr = tr.forward(x, lens).clone()
+    y_inf = inf.forward(x, lens)
+    torch.cuda.synchronize()
+    assert torch.equal(y_tr, y_inf)
+    with pytest.raises(RuntimeError):
+        inf.layers[0].forward(x, lens, *inf._wrb(0), train=True)
