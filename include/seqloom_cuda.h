@@ -197,13 +197,39 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
                  float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
                  void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream);
 
+/* ---- embedding lookup -------------------------------------------
+ * The reference's Linear layer on ids = gather_rows(table, ids) (compiler.cpp:
+ * 584-589, tape.cpp:448-492): row r of out (row stride out_ld) = table[ids[r]],
+ * table [vocab, dim] fp32.  An id outside [0, vocab) is the reference's
+ * IndexError naming the layer: the row is zero-filled and *bad_row (device
+ * int32) receives the first offending row (INT32_MAX when every id is valid) —
+ * the host raises after synchronising.  Flags:
+ *   SL_EMB_ONES_COLUMN   (bf16 only) also write 1.0 at column dim and zeros up
+ *                        to out_ld: the padded layer-0 LSTM input of a layer
+ *                        flagged SL_LAYER_X_BF16 (out_ld = sl_lstm_bf16_pitch(dim))
+ *   SL_EMB_NEGATIVE_ZERO ids < 0 give zero rows without an error (the decoder's
+ *                        previous-target embedding at t = 0: initial_output 0)
+ * The backward scatter-adds the d_out rows (stride d_out_ld) into d_table in
+ * the reference's order (ascending row per id) — bit-exact, deterministic;
+ * without accumulate the untouched rows are zeroed; negative ids add nothing. */
+enum sl_embedding_flags { SL_EMB_ONES_COLUMN = 1, SL_EMB_NEGATIVE_ZERO = 2 };
+size_t sl_embedding_workspace_size(int64_t n_ids, int32_t vocab);
+int sl_embedding_fwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* table,
+                     float* out, int64_t out_ld, int flags, int32_t* bad_row, sl_stream_t stream);
+int sl_embedding_fwd_bf16(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* table,
+                          void* out_bf16, int64_t out_ld, int flags, int32_t* bad_row, sl_stream_t stream);
+int sl_embedding_bwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* d_out,
+                     int64_t d_out_ld, float* d_table, int accumulate, void* workspace, size_t workspace_bytes,
+                     sl_stream_t stream);
+
 /* ---- measurement hooks (used by bench.py; off by default) -------------------
  * When enabled, every internal kernel phase is bracketed by CUDA events on the
  * stream it is launched on; sl_profile_read folds them into per-phase totals
  * (name, calls, device ms, algorithmic flops / bytes).  Phase names:
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
  *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam, k7_logits_gemm, k7_softmax_ce,
- *   k7_dx_gemm, k7_dw_gemm, k8_attention_fwd, k8_attention_bwd */
+ *   k7_dx_gemm, k7_dw_gemm, k8_attention_fwd, k8_attention_bwd, k9_embedding_fwd,
+ *   k9_embedding_bwd */
 typedef struct sl_profile_entry {
   char name[32];
   int32_t calls;

@@ -128,6 +128,8 @@ class Reference:
         if hasattr(L, "ref_attention_step"):
             L.ref_attention_step.argtypes = ([ctypes.c_int] * 5 + [_i] + [_d] * 9 + [ctypes.c_double] +
                                              [_d] * 15 + [c, ctypes.c_int])
+        if hasattr(L, "ref_gather_rows"):
+            L.ref_gather_rows.argtypes = [ctypes.c_int] * 4 + [_d, _i, _d, _d, _d, c, ctypes.c_int]
         if hasattr(L, "ref_output_ce"):
             L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
                                         [c, ctypes.c_int])
@@ -210,6 +212,48 @@ def _output_ce(self, x, lens, targets, W, b, eps):
 
 
 Reference.output_ce = _output_ce
+
+
+def _gather_rows(self, table, ids, d_out=None):
+    """The reference's gather_rows over ids [B, T]: (out [B, T, D], d_table or None).
+    An out-of-range id raises IndexError with the reference's message."""
+    V, D = table.shape
+    B, T = ids.shape
+    table, d_out = _f64(table), _f64(d_out)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    out = np.zeros((B, T, D))
+    dt = np.zeros((V, D)) if d_out is not None else None
+    err = ctypes.create_string_buffer(512)
+    rc = self.lib.ref_gather_rows(B, T, V, D, _ptr(table), _ptr(ids, _i), _ptr(d_out), _ptr(out), _ptr(dt),
+                                  err, 512)
+    if rc != 0 and "out of range" in err.value.decode():
+        raise IndexError(err.value.decode())
+    self._check(rc, err)
+    return out, dt
+
+
+Reference.gather_rows = _gather_rows
+
+
+def gather_rows_np(table, ids, d_out=None, layer="emb"):
+    """Restatement of Tape::gather_rows (tape.cpp:448-492) in the table's dtype:
+    out[r] = table[ids[r]]; the adjoint adds the d_out rows into a zero table
+    gradient one row at a time in ascending r (tape.cpp:478-486) — the exact
+    float summation order of the reference's fp32 build."""
+    table = np.asarray(table)
+    V, D = table.shape
+    flat = np.asarray(ids, dtype=np.int64).reshape(-1)
+    for v in flat:
+        if v < 0 or v >= V:
+            raise IndexError(f"id {int(v)} out of range [0, {V}) in layer '{layer}'")
+    out = table[flat].reshape(tuple(np.shape(ids)) + (D,))
+    if d_out is None:
+        return out, None
+    g = np.asarray(d_out, dtype=table.dtype).reshape(-1, D)
+    dt = np.zeros((V, D), dtype=table.dtype)
+    for r, v in enumerate(flat):
+        dt[v] += g[r]
+    return out, dt
 
 
 def _attention_step(self, lens, enc_ctx, enc, s, accum, Ws, bs, Wfb, bfb, v, bv, d_att=None, d_accum=None):

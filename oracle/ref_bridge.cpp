@@ -162,6 +162,30 @@ int ref_output_ce(int B, int T, int D, int V, const double* x, const int* lens, 
   }
 }
 
+// The reference's embedding lookup, Tape::gather_rows(table, ids, layer)
+// (tape.cpp:448-492), over ids [B, T]; with d_out, the table gradient through
+// L = sum(out * d_out), so dL/d(out) == d_out.  An out-of-range id is the
+// reference's IndexError (message names the layer) → returned as an error.
+int ref_gather_rows(int B, int T, int V, int D, const double* table, const int* ids, const double* d_out,
+                    double* out, double* d_table, char* err, int errlen) {
+  try {
+    Tape t(d_out != nullptr);
+    NodeId tb = t.param("emb/W", make({{Axis::Feature, V}, {Axis::Other, D}}, table));
+    IdTensor it = IdTensor::from_data({{Axis::Batch, B}, {Axis::Time, T}},
+                                      std::vector<std::int32_t>(ids, ids + (std::size_t)B * T));
+    NodeId on = t.gather_rows(tb, it, "emb");
+    put(t.value(on), out);
+    if (!d_out) return 0;
+    NodeId gy = t.constant(make({{Axis::Batch, B}, {Axis::Time, T}, {Axis::Feature, D}}, d_out));
+    NodeId loss = sum_all(t, t.mul(on, gy));
+    GradBuffer g = t.backward(loss);
+    put(t.param_gradients(g).at("emb/W"), d_table);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 // One MLP-attention step of the Listing-1 decoder subnet, built from the
 // reference's own layer ops exactly as eval_layer wires it (models.cpp:107-154,
 // compiler.cpp:616-639): s_tr = s W_s + b_s; weight_feedback = accum W_fb +

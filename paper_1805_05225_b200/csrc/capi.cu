@@ -13,6 +13,7 @@
 
 #include "adam.h"
 #include "attention.h"
+#include "embedding.h"
 #include "cell.h"
 #include "convert.h"
 #include "gemm.h"
@@ -353,6 +354,58 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
                SL_ERR_WORKSPACE, "output_ce: workspace too small");
     output_ce(batch, time, input_dim, vocab, x, targets, seq_lens, W, b, epsilon, loss, dx, dW, db,
               accumulate != 0, workspace, bad_target, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+size_t sl_embedding_workspace_size(int64_t n_ids, int32_t vocab) {
+  if (n_ids < 0 || vocab <= 0) return 0;
+  return embedding_workspace_bytes(n_ids, vocab);
+}
+
+static void check_embedding(int64_t n, int32_t vocab, int32_t dim) {
+  SL_REQUIRE(vocab > 0 && dim > 0 && n >= 0 && n < INT32_MAX, SL_ERR_SHAPE,
+             "gather_rows: table must be [Feature=V, Other=D] (V, D > 0)");  // tape.cpp:451-453
+}
+
+int sl_embedding_fwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* table,
+                     float* out, int64_t out_ld, int flags, int32_t* bad_row, sl_stream_t stream) {
+  return guarded([&] {
+    check_embedding(n_ids, vocab, dim);
+    SL_REQUIRE((ids && table && out) || n_ids == 0, SL_ERR_INVALID_ARGUMENT, "embedding: null pointer argument");
+    SL_REQUIRE(bad_row, SL_ERR_INVALID_ARGUMENT, "embedding: null bad_row");
+    SL_REQUIRE(out_ld >= dim && (flags & ~SL_EMB_NEGATIVE_ZERO) == 0, SL_ERR_INVALID_ARGUMENT,
+               "embedding: out_ld < dim or unsupported flags");
+    embedding_fwd(n_ids, ids, vocab, dim, table, out, out_ld, flags, bad_row, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int sl_embedding_fwd_bf16(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* table,
+                          void* out_bf16, int64_t out_ld, int flags, int32_t* bad_row, sl_stream_t stream) {
+  return guarded([&] {
+    check_embedding(n_ids, vocab, dim);
+    SL_REQUIRE((ids && table && out_bf16) || n_ids == 0, SL_ERR_INVALID_ARGUMENT,
+               "embedding: null pointer argument");
+    SL_REQUIRE(bad_row, SL_ERR_INVALID_ARGUMENT, "embedding: null bad_row");
+    SL_REQUIRE(out_ld >= dim + ((flags & SL_EMB_ONES_COLUMN) ? 1 : 0) &&
+                   (flags & ~(SL_EMB_ONES_COLUMN | SL_EMB_NEGATIVE_ZERO)) == 0,
+               SL_ERR_INVALID_ARGUMENT, "embedding: out_ld too small (ones column) or unsupported flags");
+    embedding_fwd_bf16(n_ids, ids, vocab, dim, table, static_cast<__nv_bfloat16*>(out_bf16), out_ld, flags,
+                       bad_row, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int sl_embedding_bwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t dim, const float* d_out,
+                     int64_t d_out_ld, float* d_table, int accumulate, void* workspace, size_t workspace_bytes,
+                     sl_stream_t stream) {
+  return guarded([&] {
+    check_embedding(n_ids, vocab, dim);
+    SL_REQUIRE(d_table && ((ids && d_out) || n_ids == 0), SL_ERR_INVALID_ARGUMENT,
+               "embedding: null pointer argument");
+    SL_REQUIRE(d_out_ld >= dim, SL_ERR_INVALID_ARGUMENT, "embedding: d_out_ld < dim");
+    SL_REQUIRE(workspace && workspace_bytes >= embedding_workspace_bytes(n_ids, vocab), SL_ERR_WORKSPACE,
+               "embedding: workspace too small");
+    embedding_bwd(n_ids, ids, vocab, dim, d_out, d_out_ld, d_table, accumulate != 0, workspace,
+                  reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

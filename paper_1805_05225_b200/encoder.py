@@ -25,11 +25,13 @@ class BLSTMEncoder:
                    for D in [input_dim] + [2 * H] * (num_layers - 1))
 
     def __init__(self, num_layers: int, batch: int, time: int, input_dim: int, hidden: int,
-                 precision: str = "bf16", device=None, params=None, grads=None, train: bool = True):
+                 precision: str = "bf16", device=None, params=None, grads=None, train: bool = True,
+                 x0_bf16: bool = False):
         """params / grads: optional flat fp32 views (numel() elements) to live in,
         e.g. slices of a whole model's buffers; by default the encoder owns them.
         train=False: inference only (no reserves, no gradients, one workspace
-        shared by all layers — BASELINE config 5)."""
+        shared by all layers — BASELINE config 5).  x0_bf16 (bf16): layer 0 takes
+        the padded bf16 input directly (e.g. written by the embedding lookup)."""
         self.L, self.B, self.T, self.D0, self.H = num_layers, batch, time, input_dim, hidden
         self.precision = precision
         self.device = torch.device(device or "cuda")
@@ -71,11 +73,12 @@ class BLSTMEncoder:
         shared = None
         if not train:  # the layers run one after another: one workspace serves all of them
             need = max(lstm.LSTMLayer.workspace_size(batch, time, D, H, 2, 1, precision,
-                                                     x_bf16=chain and l > 0, y_bf16=chain and l < last)
+                                                     x_bf16=chain and (l > 0 or x0_bf16),
+                                                     y_bf16=chain and l < last)
                        for l, D in enumerate(self.in_dims))
             shared = torch.empty(need, dtype=torch.uint8, device=self.device)
         self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device,
-                                      x_bf16=chain and l > 0, y_bf16=chain and l < last,
+                                      x_bf16=chain and (l > 0 or x0_bf16), y_bf16=chain and l < last,
                                       train=train, workspace=shared)
                        for l, D in enumerate(self.in_dims)]
         def act(l):  # layer l's output buffer

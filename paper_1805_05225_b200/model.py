@@ -11,6 +11,13 @@ reads the decoder state directly.  The decoder runs as one unidirectional
 LSTM layer over the teacher-forced inputs (no recurrent input feeding
 without attention).
 
+With src_vocab / trg_vocab the step starts from token ids like the
+reference: the `src` layer's embedding lookup feeds encoder layer 0 (written
+straight into its padded bf16 input), and the `trg` layer's lookup of the
+PREVIOUS target (zero at t = 0: initial_output 0, models.cpp:94-97) fills
+the embedding half of the decoder input; their backward passes scatter-add
+into the two tables (embedding.py).
+
 All parameters (encoder then decoder) and their gradients live in ONE flat
 fp32 buffer each: the gradient all-reduce buckets are slices of it and the
 optimizer is one fused kernel over it.
@@ -20,6 +27,7 @@ from __future__ import annotations
 import torch
 
 from . import lstm
+from .embedding import Embedding
 from .encoder import BLSTMEncoder
 from .optim import Adam
 from .output import OutputCE
@@ -28,9 +36,13 @@ from .output import OutputCE
 class Seq2SeqLSTM:
     def __init__(self, enc_layers: int, batch: int, time: int, emb: int, hidden: int,
                  precision: str = "bf16", device=None, lr: float = 1e-3, clip_norm: float = 5.0,
-                 vocab: int = 0, label_smoothing: float = 0.1):
+                 vocab: int = 0, label_smoothing: float = 0.1, src_vocab: int = 0, trg_vocab: int = 0):
         """vocab > 0 adds the output softmax layer [hidden, vocab] and the CE loss
-        (step() then takes target ids instead of an upstream gradient)."""
+        (step() then takes target ids instead of an upstream gradient).
+        src_vocab > 0: step() takes source token ids [B, T] (the `src` embedding
+        layer) instead of source embeddings; trg_vocab > 0 (needs vocab): the
+        decoder's target-embedding input comes from the `trg` layer's lookup of
+        the previous target id instead of set_target_embeddings()."""
         self.L, self.B, self.T, self.E, self.H = enc_layers, batch, time, emb, hidden
         self.device = torch.device(device or "cuda")
         H = hidden
@@ -39,10 +51,17 @@ class Seq2SeqLSTM:
         n_dec = self.Dd * 4 * H + H * 4 * H + 4 * H
         self.V = vocab
         n_out = H * vocab + vocab if vocab else 0
-        self.params = torch.empty(n_enc + n_dec + n_out, dtype=torch.float32, device=self.device)
+        if trg_vocab and not vocab:
+            raise ValueError("trg_vocab needs the output layer (vocab > 0): the previous target ids")
+        self.Vs, self.Vt = src_vocab, trg_vocab
+        n_src, n_trg = src_vocab * emb, trg_vocab * emb
+        self.params = torch.empty(n_enc + n_dec + n_out + n_src + n_trg, dtype=torch.float32,
+                                  device=self.device)
         self.grads = torch.zeros_like(self.params)
+        bf16 = precision == "bf16"
         self.enc = BLSTMEncoder(enc_layers, batch, time, emb, H, precision, self.device,
-                                params=self.params[:n_enc], grads=self.grads[:n_enc])
+                                params=self.params[:n_enc], grads=self.grads[:n_enc],
+                                x0_bf16=bf16 and src_vocab > 0)
         off = n_enc
         self.dec_p, self.dec_g = [], []
         for shape in ((self.Dd, 4 * H), (H, 4 * H), (4 * H,)):
@@ -61,7 +80,21 @@ class Seq2SeqLSTM:
             self.out_bucket = self.grads[off:off + n_out]
             self.out = OutputCE(batch, time, H, vocab, label_smoothing, device=self.device)
             self.dec_dy = torch.empty(batch, time, H, dtype=torch.float32, device=self.device)
-        bf16 = precision == "bf16"
+        off = n_enc + n_dec + n_out
+        if src_vocab:  # `src` layer: embedding table [Vs, E] (compiler.cpp:584-589)
+            self.src_p = self.params[off:off + n_src].view(src_vocab, emb)
+            self.src_g = self.grads[off:off + n_src].view(src_vocab, emb)
+            self.src_bucket = self.grads[off:off + n_src]
+            self.src_emb = Embedding(src_vocab, emb, batch * time, layer="src", device=self.device)
+            self.x0 = (torch.zeros(batch, time, lstm.bf16_pitch(emb), dtype=torch.bfloat16, device=self.device)
+                       if bf16 else torch.empty(batch, time, emb, dtype=torch.float32, device=self.device))
+            off += n_src
+        if trg_vocab:  # `trg` layer: embedding table [Vt, E] of the previous target
+            self.trg_p = self.params[off:off + n_trg].view(trg_vocab, emb)
+            self.trg_g = self.grads[off:off + n_trg].view(trg_vocab, emb)
+            self.trg_bucket = self.grads[off:off + n_trg]
+            self.trg_emb = Embedding(trg_vocab, emb, batch * time, layer="trg", device=self.device)
+            self.prev_ids = torch.full((batch, time), -1, dtype=torch.int32, device=self.device)
         self.dec = lstm.LSTMLayer(batch, time, self.Dd, H, 1, 1, precision, self.device, x_bf16=bf16)
         if bf16:  # padded bf16 decoder input, ones column at Dd (seqloom_cuda.h SL_LAYER_X_BF16)
             self.dec_in = torch.zeros(batch, time, lstm.bf16_pitch(self.Dd), dtype=torch.bfloat16,
@@ -78,6 +111,10 @@ class Seq2SeqLSTM:
              ("b", self.Dd * 4 * H + H * 4 * H, 4 * H))]
         if vocab:
             names += [("output_prob/W", n_enc + n_dec, H * vocab), ("output_prob/b", n_enc + n_dec + H * vocab, vocab)]
+        if src_vocab:
+            names += [("src/W", n_enc + n_dec + n_out, n_src)]
+        if trg_vocab:
+            names += [("trg/W", n_enc + n_dec + n_out + n_src, n_trg)]
         self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
 
     def init_uniform(self, seed: int = 0):
@@ -89,9 +126,23 @@ class Seq2SeqLSTM:
         """emb [B, T, E]: the teacher-forced target-side embeddings."""
         self.dec_in[:, :, :self.E] = emb.to(self.dec_in.dtype)
 
-    def forward(self, x, seq_lens):
+    def set_targets(self, targets):
+        """The `trg` layer input: previous target ids, -1 (a zero embedding) at t = 0."""
+        self.prev_ids[:, 1:].copy_(targets[:, :-1])
+
+    def forward(self, x, seq_lens, targets=None):
+        """x: source embeddings [B, T, E] — or, with src_vocab, source ids [B, T]
+        int32; targets (trg_vocab): the target ids whose predecessors feed the
+        decoder."""
+        if self.Vs:
+            self.src_ids = x
+            x = self.src_emb.forward(x, self.src_p, out=self.x0,
+                                     bf16_pitch=self.x0.shape[-1] if self.x0.dtype == torch.bfloat16 else None)
         y = self.enc.forward(x, seq_lens)
         self.dec_in[:, :, self.E:self.Dd] = y.to(self.dec_in.dtype)  # context stand-in c_t = enc_t
+        if self.Vt:
+            self.set_targets(targets)
+            self.trg_emb.forward(self.prev_ids, self.trg_p, out=self.dec_in[:, :, :self.E], negative_zero=True)
         W, R, b = self.dec_p
         self.dec.forward(self.dec_in, seq_lens, [W], [R], [b], y=self.dec_y)
         return self.dec_y
@@ -101,8 +152,26 @@ class Seq2SeqLSTM:
         self.dec.backward(dy_dec, dx=self.dec_dx, dW=[W], dR=[R], db=[b])
         if on_grads is not None:
             on_grads(-1, self.dec_bucket)
+        if self.Vt:
+            self.trg_emb.backward(self.prev_ids, self.dec_dx[:, :, :self.E], self.trg_g)
+            if on_grads is not None:
+                on_grads(-3, self.trg_bucket)
         self.enc_dy.copy_(self.dec_dx[:, :, self.E:])
-        return self.enc.backward(self.enc_dy, on_layer_grads=on_grads)
+        dx = self.enc.backward(self.enc_dy, on_layer_grads=on_grads)
+        if self.Vs:
+            self.src_emb.backward(self.src_ids, dx, self.src_g)
+            if on_grads is not None:
+                on_grads(-4, self.src_bucket)
+        return dx
+
+    def check_ids(self):
+        """Synchronise; raise the reference's IndexError for a bad source / target id."""
+        if self.Vs:
+            self.src_emb.check_ids()
+        if self.Vt:
+            self.trg_emb.check_ids()
+        if self.V:
+            self.out.check_targets()
 
     def loss_and_output_grads(self, targets, seq_lens, on_grads=None):
         """Output layer + label-smoothed CE on the decoder states: returns the
@@ -118,7 +187,7 @@ class Seq2SeqLSTM:
         """One training step.  With the output layer (vocab > 0) the last
         argument is the target ids [B, T] and the step returns the device loss;
         without it, the upstream gradient of the decoder output."""
-        self.forward(x, seq_lens)
+        self.forward(x, seq_lens, dy_or_targets if self.Vt else None)
         loss = None
         if self.V:
             loss = self.loss_and_output_grads(dy_or_targets, seq_lens, on_grads=reducer)

@@ -277,3 +277,32 @@ def test_attention_step_restatement_pinned_to_reference():
         assert np.abs(r[3][k].reshape(n[3][k].shape) - n[3][k]).max() < 1e-12, k
     # padded source positions get no attention weight
     assert np.all(n[1][1, 2:] == 0) and abs(n[1][1].sum() - 1) < 1e-12
+
+
+def test_gather_rows_oracle_pinned_to_reference_test():
+    # reference tape_test.cpp:81-104: table {1,2,3,4} [2, 2], ids {1, 0} -> {3,4,1,2};
+    # ids {0, 0} with L = sum(out) -> table grad {2, 2, 0, 0}; id 7 -> IndexError naming "emb"
+    tbl = np.array([[1, 2], [3, 4]], dtype=np.float32)
+    out, _ = oracle.gather_rows_np(tbl, np.array([1, 0]))
+    assert out.reshape(-1).tolist() == [3, 4, 1, 2]
+    _, g = oracle.gather_rows_np(tbl, np.array([0, 0]), d_out=np.ones((2, 2), np.float32))
+    assert g.reshape(-1).tolist() == [2, 2, 0, 0]
+    with pytest.raises(IndexError, match="emb"):
+        oracle.gather_rows_np(tbl, np.array([7]))
+
+
+@pytest.mark.skipif(not _ref_available(), reason="oracle/_ref not built")
+def test_gather_rows_restatement_matches_reference_bitwise():
+    rng = np.random.default_rng(11)
+    V, D, B, T = 13, 7, 5, 9
+    tbl = rng.uniform(-1, 1, (V, D)).astype(np.float32)
+    ids = rng.integers(0, V, (B, T)).astype(np.int32)
+    ids[0, :] = 3  # a long duplicate run: order of the fp32 adds matters
+    d_out = rng.uniform(-1, 1, (B, T, D)).astype(np.float32)
+    ref = oracle.Reference(32)
+    out_r, g_r = ref.gather_rows(tbl, ids, d_out)
+    out_o, g_o = oracle.gather_rows_np(tbl, ids, d_out)
+    assert np.array_equal(out_r.astype(np.float32), out_o)
+    assert np.array_equal(g_r.astype(np.float32), g_o)
+    with pytest.raises(IndexError, match="in layer 'emb'"):
+        ref.gather_rows(tbl, np.full((1, 1), V, np.int32))

@@ -547,3 +547,48 @@ def test_inference_encoder_matches_training_forward(cuda, prec):
     assert torch.equal(y_tr, y_inf)
     with pytest.raises(RuntimeError):
         inf.layers[0].forward(x, lens, *inf._wrb(0), train=True)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_seq2seq_from_token_ids_matches_supplied_embeddings(cuda, prec):
+    # the `src` / `trg` embedding layers in the config-4 step:
+    # starting from ids must give bit-identical losses / gradients to feeding the
+    # looked-up embeddings directly, and the two table gradients must be the
+    # reference-order scatter of the input gradients (oracle.gather_rows_np)
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    Lyr, B, T, E, H, V, Vs, Vt = 2, 3, 6, 16, 24, 11, 13, 17
+    m1 = Seq2SeqLSTM(Lyr, B, T, E, H, prec, vocab=V, src_vocab=Vs, trg_vocab=Vt)
+    m1.init_uniform(5)
+    m2 = Seq2SeqLSTM(Lyr, B, T, E, H, prec, vocab=V)
+    n = m2.params.numel()
+    m2.params.copy_(m1.params[:n])
+    g = torch.Generator().manual_seed(6)
+    src = torch.randint(0, Vs, (B, T), generator=g, dtype=torch.int32).cuda()
+    src[0, :4] = 2  # duplicate ids: scatter order matters
+    tgt = torch.randint(0, V, (B, T), generator=g, dtype=torch.int32).cuda()
+    tgt[1, :] = 3
+    tgt %= min(V, Vt)
+    lens = torch.tensor([6, 4, 5], dtype=torch.int32).cuda()
+    x = m1.src_p[src.long()]
+    prev = torch.cat([torch.full((B, 1), -1, dtype=torch.int32, device="cuda"), tgt[:, :-1]], dim=1)
+    emb = m1.trg_p[prev.clamp_min(0).long()] * (prev >= 0).unsqueeze(-1)
+    m2.set_target_embeddings(emb)
+    m1.forward(src, lens, tgt)
+    l1 = m1.loss_and_output_grads(tgt, lens)
+    m1.backward(m1.dec_dy)
+    m2.forward(x, lens)
+    l2 = m2.loss_and_output_grads(tgt, lens)
+    dx2 = m2.backward(m2.dec_dy)
+    torch.cuda.synchronize()
+    m1.check_ids()
+    assert float(l1) == float(l2)
+    assert torch.equal(m1.dec_y, m2.dec_y)
+    assert torch.equal(m1.grads[:n], m2.grads)
+    _, gs = oracle.gather_rows_np(m1.src_p.cpu().numpy(), src.cpu().numpy(), dx2.cpu().numpy())
+    assert np.array_equal(m1.src_g.cpu().numpy(), gs)
+    d_emb = m2.dec_dx[:, :, :E].cpu().numpy().reshape(-1, E)
+    gt = np.zeros((Vt, E), np.float32)
+    for r, v in enumerate(prev.cpu().numpy().reshape(-1)):
+        if v >= 0:
+            gt[v] += d_emb[r]
+    assert np.array_equal(m1.trg_g.cpu().numpy(), gt)
