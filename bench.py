@@ -2,15 +2,17 @@
 
 Metric: "LSTM fwd+bwd target tokens/sec (6xBLSTM n=1000, T=60) at 1/2/4/8 B200
 vs CPU" (BASELINE.json), on configs[3] — the Listing-1 training step — as far
-as it is built: one step = forward + backward (BPTT) of the 6-layer
-bidirectional LSTM encoder (H = 1000, D0 = 620, the embedding width,
-models.hpp:14) and the 1-layer LSTM decoder (H = 1000, input [620-wide target
-embedding ‖ 2000-wide context], models.cpp:161), T_src = T_tgt = 60, then the
-fused global-norm clip + Adam step over all LSTM parameters, plus at N > 1 the
-data-parallel NCCL gradient all-reduce overlapped with BPTT.  Not built
-(SURVEY §8 f1/f2): the MLP attention and the output softmax — the decoder's
-context input is the encoder output at the same position (model.py).
-tokens = target (sequence, time) positions.
+as it is wired: one step = the source / target embedding lookups (V = 20K
+each; width 620, models.hpp:14) from token ids, forward + backward
+(BPTT) of the 6-layer bidirectional LSTM encoder (H = 1000) and the 1-layer
+LSTM decoder (H = 1000, input [620-wide previous-target embedding ‖ 2000-wide
+context], models.cpp:161), the output softmax layer (V = 20K) with the
+label-smoothed CE loss, T_src = T_tgt = 60, then the fused global-norm clip +
+Adam step over all parameters, plus at N > 1 the data-parallel NCCL gradient
+all-reduce overlapped with BPTT.  The MLP attention is built
+and measured standalone (scripts/bench_attention.py) but not in this step:
+the decoder's context input is the encoder output at the same position
+(model.py).  tokens = target (sequence, time) positions.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -48,6 +50,9 @@ def parse():
     ap.add_argument("--input", type=int, default=620)
     ap.add_argument("--time", type=int, default=60)
     ap.add_argument("--vocab", type=int, default=20000, help="target vocabulary (output softmax); 0 = none")
+    ap.add_argument("--src-vocab", type=int, default=20000, help="source embedding table rows; 0 = feed embeddings")
+    ap.add_argument("--trg-vocab", type=int, default=20000,
+                    help="target embedding table rows (needs --vocab); 0 = feed embeddings")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
@@ -161,6 +166,7 @@ def cpu_reference(args, steps=1):
     n_par = sum(2 * (D * 4 * H + H * 4 * H + 4 * H) for D in [D0] + [2 * H] * (L - 1))
     n_par += (D0 + 2 * H) * 4 * H + H * 4 * H + 4 * H
     n_par += H * args.vocab + args.vocab  # output softmax layer
+    n_par += (args.src_vocab + (args.trg_vocab if args.vocab else 0)) * D0  # embedding tables
     k = 4_000_000
     pa, ga = rng.standard_normal(k).astype(np.float32), rng.standard_normal(k).astype(np.float32)
     ma, va = np.zeros(k, np.float32), np.zeros(k, np.float32)
@@ -175,6 +181,11 @@ def cpu_reference(args, steps=1):
     adam_s = (time.perf_counter() - t0) * n_par / k
 
     V = args.vocab
+    Vs, Vt = args.src_vocab, (args.trg_vocab if V else 0)
+    if (Vs or Vt) and kind == "reference":  # embedding lookups of one sequence, fwd + bwd
+        tbl = {Vv: rng.uniform(-s, s, (Vv, D0)) for Vv in {Vs, Vt} if Vv}
+        ids_e = {Vv: rng.integers(0, Vv, (1, T)).astype(np.int32) for Vv in tbl}
+        d_e = rng.uniform(-1, 1, (1, T, D0))
     if V and kind == "reference":
         Wo = rng.uniform(-s, s, (H, V))
         bo = rng.uniform(-s, s, V)
@@ -183,6 +194,11 @@ def cpu_reference(args, steps=1):
 
     def one(out):
         tt = {}
+        if (Vs or Vt) and kind == "reference":
+            t0 = time.perf_counter()
+            for Vv in [v for v in (Vs, Vt) if v]:
+                ref.gather_rows(tbl[Vv], ids_e[Vv], d_e)
+            tt["emb"] = time.perf_counter() - t0
         if V and kind == "reference":  # the output softmax layer + CE, fwd + bwd
             t0 = time.perf_counter()
             ref.output_ce(xo, lens, tgo, Wo, bo, 0.1)
@@ -205,13 +221,15 @@ def cpu_reference(args, steps=1):
             t.start()
         for t in ths:
             t.join()
-        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] + r.get("out", 0.0) for r in res]
+        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] + r.get("out", 0.0) + r.get("emb", 0.0)
+                   for r in res]
         rates.append(threads * T / (max(per_seq) + adam_s))
     value = statistics.median(rates)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{threads} threads x 1 sequence (T={T}); per thread one fwd+bwd layer-direction "
-                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}) and the output "
-                      f"softmax + CE (V={V}), step time = 2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) + t(out) "
+                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}), the output "
+                      f"softmax + CE (V={V}) and the src/trg embedding lookups (gather_rows fwd+bwd, "
+                      f"V={Vs}/{Vt}), step time = 2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) + t(out) + t(emb) "
                       f"(layers run sequentially in the reference) "
                       f"+ one clip+Adam step over {n_par / 1e6:.1f}M params ({adam_s:.2f} s, fp32 numpy "
                       f"restatement timed on a 4M-element slice and scaled: the reference has no optimizer "
@@ -229,17 +247,23 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
-    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev, vocab=args.vocab)
+    Vs, Vt = args.src_vocab, (args.trg_vocab if args.vocab else 0)
+    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev, vocab=args.vocab, src_vocab=Vs, trg_vocab=Vt)
     model.init_uniform(seed=1)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
-    x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1      # source embeddings
-    emb = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1    # target embeddings
+    if Vs:  # source token ids (the `src` embedding layer looks them up)
+        x = torch.randint(0, Vs, (B, T), device=dev, generator=g, dtype=torch.int32)
+    else:  # source embeddings
+        x = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1
+    emb = torch.rand(B, T, D0, device=dev, generator=g) * 2 - 1    # target embeddings (trg_vocab = 0)
     lens = torch.full((B,), T, dtype=torch.int32, device=dev)
-    if args.vocab:  # target ids for the output layer's CE loss
-        dy = torch.randint(0, args.vocab, (B, T), device=dev, generator=g, dtype=torch.int32)
+    if args.vocab:  # target ids for the output layer's CE loss (and the `trg` lookup)
+        dy = torch.randint(0, min(args.vocab, Vt or args.vocab), (B, T), device=dev, generator=g,
+                           dtype=torch.int32)
     else:
         dy = torch.rand(B, T, H, device=dev, generator=g) * 2 - 1  # dL/d(decoder output)
-    model.set_target_embeddings(emb)
+    if not Vt:
+        model.set_target_embeddings(emb)
     lib = lstm.lib()
     lib.sl_profile_enable.argtypes = [ctypes.c_int]
     lib.sl_launch_count.restype = ctypes.c_ulonglong
@@ -314,20 +338,23 @@ def run_ours(args, rank, world, local_rank):
     # ---- end to end: host buffers through the public API, copies timed
     e2e = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
-        eh = emb.cpu().pin_memory()
-        lh = lens.cpu().pin_memory()
-        xd, ed = torch.empty_like(x), torch.empty_like(emb)
-        ld = torch.empty_like(lens)
+        # per step in: source ids (or embeddings), target ids (or target
+        # embeddings + the upstream gradient), lengths; out: the scalar loss
+        hin = [x, lens] + ([dy] if args.vocab else []) + ([] if Vt else [emb])
+        hosts = [t.cpu().pin_memory() for t in hin]
+        devs = [torch.empty_like(t) for t in hin]
+        xd, ld = devs[0], devs[1]
+        dyd = devs[2] if args.vocab else dy
+        ed = devs[-1] if not Vt else None
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
 
         def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            ed.copy_(eh, non_blocking=True)
-            ld.copy_(lh, non_blocking=True)
-            model.set_target_embeddings(ed)
+            for d_, h_ in zip(devs, hosts):
+                d_.copy_(h_, non_blocking=True)
+            if ed is not None:
+                model.set_target_embeddings(ed)
             if args.vocab:  # the real loss: output softmax + label-smoothed CE
-                loss = model.step(xd, ld, dy, reducer=red, grad_scale=1.0 / world)
+                loss = model.step(xd, ld, dyd, reducer=red, grad_scale=1.0 / world)
                 loss_h.copy_(loss, non_blocking=True)
             else:
                 y = model.forward(xd, ld)
@@ -351,8 +378,10 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * B * T * args.steps / float(tt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": (xh.numel() + eh.numel() + lh.numel()) * 4, "d2h_bytes_per_step": 4,
-               "note": "x, target embeddings and lens copied in; the scalar loss copied out",
+               "h2d_bytes_per_step": sum(h_.numel() * h_.element_size() for h_ in hosts), "d2h_bytes_per_step": 4,
+               "note": ("source ids" if Vs else "source embeddings") + ", " +
+                       ("target ids" if Vt else "target embeddings") + " and lens copied in; the scalar "
+                       "loss copied out",
                "timing": "host wall clock, max over ranks"}
     return dict(ms=ms_max, phases=phases, launches=int(launches), clocks=clocks.summary(),
                 e2e=e2e, eager_ms=eager_ms / args.steps, graph=graph is not None)
@@ -365,14 +394,18 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
     out_s = (f" + output softmax V={args.vocab} with label-smoothed CE (eps 0.1)" if args.vocab else "")
-    cfg = {"workload": f"config4 training step: {L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
+    Vt = args.trg_vocab if args.vocab else 0
+    emb_s = (f"src/trg embedding lookups from token ids (V={args.src_vocab}/{Vt}) + " if args.src_vocab or Vt
+             else "")
+    cfg = {"workload": f"config4 training step: {emb_s}{L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
                        f"H={H} (input {D0}+{2 * H}){out_s}, T_src=T_tgt={T}, fwd+bwd + fused "
-                       f"clip(5.0)+Adam (+DP grad all-reduce at N>1); MLP attention not built (SURVEY 8 f1)",
-           "vocab": args.vocab,
+                       f"clip(5.0)+Adam (+DP grad all-reduce at N>1); MLP attention measured standalone, "
+                       f"not in this step (context = encoder output at t)",
+           "vocab": args.vocab, "src_vocab": args.src_vocab, "trg_vocab": Vt,
            "global_batch": B * world, "batch_per_gpu": B,
            "seq_len": T, "hidden": H, "input_dim": D0, "layers": L, "directions": 2,
            "parallelism": f"dp{world}", "seq_lens": "all = T",
-           "l2": "working set (weights 590 MB fp32 + activations) far exceeds the 126 MB L2"}
+           "l2": "working set (weights ~0.77 GB fp32 + Adam moments + activations) far exceeds the 126 MB L2"}
 
     if args.impl == "reference":
         if rank != 0:
