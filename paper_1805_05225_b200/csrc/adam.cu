@@ -6,7 +6,8 @@
 // theta <- theta - lr m^ / (sqrt(v^) + eps)) with the global-norm clip at 5.0
 // applied before Adam.  The reference has no code for this op.
 //
-// Two HBM-bound passes: (1) sum of squares + non-finite detection of the
+// Two HBM-bound passes: (1) sum of squares (a fixed-order, run-to-run
+// deterministic reduction) + non-finite detection of the
 // (already all-reduced) gradient, (2) the element-wise update, which reads
 // the clip scale computed from (1) on the device — no host round trip.
 // Bytes per parameter: 4 (pass 1) + 16 read + 12 written (pass 2).
@@ -54,7 +55,24 @@ __global__ void __launch_bounds__(kThreads) grad_sumsq_kernel(const float* __res
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&sc->nonfinite, 1u);
   const double s = block_sum((double)acc);
-  if (threadIdx.x == 0) atomicAdd(&sc->sumsq, s);
+  // deterministic total: every block leaves its partial, the last block to finish
+  // adds them in block order (the same bits every run, unlike float atomics)
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    sc->part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) t += *((volatile double*)&sc->part[b]);
+  t = block_sum(t);
+  if (threadIdx.x == 0) {
+    sc->sumsq = t;
+    sc->ticket = 0;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
@@ -124,7 +142,9 @@ void adam_step(int64_t n, float* params, const float* grads, float* m, float* v,
              SL_ERR_INVALID_ARGUMENT, "adam_step: buffers need 16 B alignment");
   SL_CUDA_TRY(cudaMemsetAsync(scratch, 0, offsetof(AdamScratch, t), stream));  // keep the step counter
   const int64_t n4 = (n + 3) / 4;
-  const int grid = (int)std::min<int64_t>(std::max<int64_t>(1, (n4 + kThreads - 1) / kThreads), 4LL * sms());
+  const int grid = (int)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(1, (n4 + kThreads - 1) / kThreads),
+                                                             4LL * sms()),
+                                          kAdamMaxBlocks);
   {
     Phase ph(stream, "k6_grad_norm", 0.0, 4.0 * n);
     grad_sumsq_kernel<<<grid, kThreads, 0, stream>>>(grads, n, scratch);

@@ -11,10 +11,14 @@ struct AdamHyper {
   int32_t step;      // > 0: this step number; 0: the device counter in the scratch + 1
 };
 
-struct AdamScratch {  // device scratch
-  double sumsq;        // zeroed per step
+constexpr int kAdamMaxBlocks = 2048;
+struct AdamScratch {  // device scratch (zero when created)
+  double sumsq;        // zeroed per step; the fixed-order total of part[]
   unsigned nonfinite;  // zeroed per step
-  int32_t t;           // persistent step counter (zero when the scratch is created)
+  int32_t t;           // persistent step counter (byte offset 12: optim.py reads it)
+  unsigned ticket;     // blocks done with pass 1; the last one resets it
+  unsigned pad;
+  double part[kAdamMaxBlocks];  // per-block sums of squares (deterministic reduction)
 };
 
 void adam_step(int64_t n, float* params, const float* grads, float* m, float* v, const AdamHyper& h,

@@ -116,6 +116,24 @@ class Seq2SeqLSTM:
         if trg_vocab:
             names += [("trg/W", n_enc + n_dec + n_out + n_src, n_trg)]
         self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
+        # checkpoint manifest (name, offset, shape) in the reference's layer/param naming
+        shapes = {}
+        for l, D in enumerate(self.enc.in_dims):
+            for d in ("fw", "bw"):
+                shapes.update({f"enc{l}_{d}/W": (D, 4 * H), f"enc{l}_{d}/R": (H, 4 * H), f"enc{l}_{d}/b": (4 * H,)})
+        shapes.update({"dec/W": (self.Dd, 4 * H), "dec/R": (H, 4 * H), "dec/b": (4 * H,),
+                       "output_prob/W": (H, vocab), "output_prob/b": (vocab,),
+                       "src/W": (src_vocab, emb), "trg/W": (trg_vocab, emb)})
+        self.manifest = [(n, o, shapes[n]) for n, o, _ in names]
+
+    def save(self, directory: str, **state):
+        """Checkpoint in the reference trainer's format (checkpoint.py)."""
+        from . import checkpoint
+        checkpoint.save(directory, self.params, self.manifest, optimizer=self.opt, **state)
+
+    def load(self, directory: str):
+        from . import checkpoint
+        return checkpoint.load(directory, self.params, self.manifest, optimizer=self.opt)
 
     def init_uniform(self, seed: int = 0):
         g = torch.Generator(device=self.device).manual_seed(seed)

@@ -45,6 +45,15 @@ class Adam:
                                    self.betas[1], self.eps, grad_scale, self.clip_norm, lstm._p(self.scratch),
                                    lstm._p(self.grad_norm), lstm._p(self.nonfinite), lstm._stream()))
 
+    # the device-side step counter (AdamScratch::t, csrc/adam.h: after a double
+    # and an unsigned) — read / written for checkpoints (checkpoint.py)
+    def device_step(self) -> int:
+        return int(self.scratch[12:16].view(torch.int32).item())
+
+    def set_device_step(self, t: int) -> None:
+        self.scratch[12:16].view(torch.int32).fill_(int(t))
+        self.t = int(t)
+
     def check_finite(self, grads: torch.Tensor | None = None):
         """Synchronise; raise FloatingPointError naming the first parameter whose
         gradient is non-finite (the step was skipped, parameters untouched)."""

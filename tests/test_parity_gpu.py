@@ -592,3 +592,30 @@ def test_seq2seq_from_token_ids_matches_supplied_embeddings(cuda, prec):
         if v >= 0:
             gt[v] += d_emb[r]
     assert np.array_equal(m1.trg_g.cpu().numpy(), gt)
+
+
+def test_checkpoint_resume_is_bitwise(cuda, tmp_path):
+    # SPEC invariant "save -> load -> continue == uninterrupted, bitwise": two
+    # steps straight vs one step, save, load into a fresh model, one more step
+    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    Lyr, B, T, E, H, V = 2, 3, 5, 16, 24, 11
+    mk = lambda: Seq2SeqLSTM(Lyr, B, T, E, H, "bf16", vocab=V, src_vocab=13, trg_vocab=V)
+    g = torch.Generator().manual_seed(9)
+    src = torch.randint(0, 13, (B, T), generator=g, dtype=torch.int32).cuda()
+    tgt = torch.randint(0, V, (B, T), generator=g, dtype=torch.int32).cuda()
+    lens = torch.tensor([5, 3, 4], dtype=torch.int32).cuda()
+    a = mk()
+    a.init_uniform(1)
+    b = mk()
+    b.params.copy_(a.params)
+    a.step(src, lens, tgt)
+    a.step(src, lens, tgt)
+    b.step(src, lens, tgt)
+    b.save(str(tmp_path), epoch=1)
+    c = mk()
+    meta = c.load(str(tmp_path))
+    assert meta["epoch"] == 1 and meta["params"][-1]["name"] == "trg/W"
+    assert c.opt.device_step() == 1
+    c.step(src, lens, tgt)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, c.params)
