@@ -7,9 +7,14 @@ HBM copy bandwidth (the step is bandwidth-bound).  The times include the
 step's three small projection GEMMs (fp32-accurate split-bf16 on the tensor
 cores, gemm_f32x3.cu), which the algorithmic byte count leaves out.
 
-    python scripts/bench_attention.py [--B 256] [--iters 50]
+The reference's own CPU implementation of the same step (oracle/_ref: the
+attention subnet built from its Tape ops, fwd + bwd) is timed beside it on a
+bounded sample (--cpu-rows batch rows, one thread per row up to the host's
+cores) and reported as steps/s scaled to the full batch.
+
+    python scripts/bench_attention.py [--B 256] [--iters 50] [--cpu-rows 16]
 """
-import argparse, json, os, sys
+import argparse, json, os, sys, threading, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1805_05225_b200.attention import Attention
@@ -21,6 +26,7 @@ ap.add_argument("--K", type=int, default=1000)
 ap.add_argument("--E", type=int, default=2000)
 ap.add_argument("--H", type=int, default=1000)
 ap.add_argument("--iters", type=int, default=50)
+ap.add_argument("--cpu-rows", type=int, default=16, help="batch rows in the CPU reference sample (0 = skip)")
 a = ap.parse_args()
 B, Ts, K, E, H = a.B, a.Ts, a.K, a.E, a.H
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -59,4 +65,47 @@ out = {"op": "attention_step", "B": B, "Ts": Ts, "K": K, "E": E, "H": H,
        "fwd_frac": fwd_bytes / fwd_ms / 1e6 / hbm, "bwd_frac": bwd_bytes / bwd_ms / 1e6 / hbm,
        "per_decoder_step_us": (fwd_ms + bwd_ms) * 1e3,
        "per_training_step_ms_T60": (fwd_ms + bwd_ms) * Ts}
+
+
+def cpu_reference(rows):
+    """The reference attention step (fwd + bwd through its Tape) on `rows`
+    one-row batches in parallel threads; returns full-batch steps/s."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    import oracle
+    ref = oracle.Reference(32)
+    rng = np.random.default_rng(0)
+    args = dict(enc_ctx=rng.uniform(-1, 1, (1, Ts, K)), enc=rng.uniform(-1, 1, (1, Ts, E)),
+                s=rng.uniform(-1, 1, (1, H)), accum=rng.uniform(0, 1, (1, Ts)),
+                Ws=rng.uniform(-1, 1, (H, K)) / H ** 0.5, bs=rng.uniform(-.5, .5, K),
+                Wfb=rng.uniform(-.5, .5, (1, K)), bfb=rng.uniform(-.5, .5, K),
+                v=rng.uniform(-1, 1, (K, 1)) / K ** 0.5, bv=0.0,
+                d_att=rng.uniform(-1, 1, (1, E)), d_accum=rng.uniform(-1, 1, (1, Ts)))
+    lens = np.full(1, Ts, np.int32)
+    threads = max(1, min(rows, os.cpu_count() or 1))
+    secs = []
+
+    def one():
+        t0 = time.perf_counter()
+        for _ in range(rows // threads):
+            ref.attention_step(lens, **args)
+        secs.append(time.perf_counter() - t0)
+
+    ths = [threading.Thread(target=one) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    per_row = max(secs) / (rows // threads)  # seconds per batch row per thread
+    return {"kind": "reference", "cores": threads, "value": threads / (per_row * B), "unit": "steps/s",
+            "sample": f"{threads} threads x {rows // threads} one-row steps (Ts={Ts}, K={K}, E={E}, H={H}), "
+                      f"fwd+bwd through the reference Tape (fp32 build), scaled to B={B}"}
+
+
+if a.cpu_rows:
+    try:
+        out["cpu_baseline"] = cpu_reference(a.cpu_rows)
+        out["gpu_steps_per_s"] = 1e3 / (fwd_ms + bwd_ms)
+    except FileNotFoundError as e:
+        out["cpu_baseline"] = {"unavailable": str(e)}
 print(json.dumps(out))

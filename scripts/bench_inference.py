@@ -9,14 +9,20 @@ resident in HBM, timed with CUDA events after warm-up, and reported as
 frames/s (one frame = one valid (sequence, time) position) and as the average
 per-step recurrence latency implied by the K2 phase (sl_profile_*).
 
+The reference CPU path (oracle/_ref: lstm_sequence forward, grad-disabled
+Tape) is timed beside it on a bounded sample: one sequence per thread at T=60
+through one layer-direction of each input width, scaled to the 6-layer stack.
+
     python scripts/bench_inference.py [--layers 6] [--hidden 1024] [--feat 40]
-        [--batches 1,16,64,256,1024] [--times 60,500] [--iters 3]
+        [--batches 1,16,64,256,1024] [--times 60,500] [--iters 3] [--no-cpu]
 """
 import argparse
 import ctypes
 import json
 import os
 import sys
+import threading
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -32,6 +38,7 @@ ap.add_argument("--batches", default="1,16,64,256,1024")
 ap.add_argument("--times", default="60,500")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--precision", default="bf16")
+ap.add_argument("--no-cpu", action="store_true")
 a = ap.parse_args()
 
 L = lstm.lib()
@@ -87,5 +94,46 @@ for T in [int(t) for t in a.times.split(",")]:
         print(json.dumps(row), flush=True)
         del enc, x
         torch.cuda.empty_cache()
-print(json.dumps({"config": "BASELINE configs[4]: 6xBLSTM n=%d, F=%d, inference, %s" % (H, D0, a.precision),
-                  "points": results}))
+
+
+def cpu_reference(T=60):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    import oracle
+    ref = oracle.Reference(32)
+    rng = np.random.default_rng(0)
+    s = 1 / np.sqrt(H)
+    shapes = [D0, 2 * H]
+    prm = {D: tuple(rng.uniform(-s, s, shp) for shp in ((D, 4 * H), (H, 4 * H), (4 * H,))) for D in shapes}
+    xs = {D: rng.uniform(-1, 1, (1, T, D)) for D in shapes}
+    lens = np.full(1, T, np.int32)
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    res = []
+
+    def one():
+        tt = {}
+        for D in shapes:
+            t0 = time.perf_counter()
+            ref.sequence(xs[D], lens, *prm[D], 1)
+            tt[D] = time.perf_counter() - t0
+        res.append(tt)
+
+    ths = [threading.Thread(target=one) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    per_seq = max(2 * r[D0] + 2 * (NL - 1) * r[2 * H] for r in res)
+    return {"kind": "reference", "cores": threads, "value": threads * T / per_seq, "unit": "frames/s",
+            "sample": f"{threads} threads x 1 sequence (T={T}) through one layer-direction of each input "
+                      f"width (D={D0}, D={2 * H}; H={H}), forward only, step = 2 t(D0) + {2 * (NL - 1)} t(2H)"}
+
+
+summary = {"config": "BASELINE configs[4]: 6xBLSTM n=%d, F=%d, inference, %s" % (H, D0, a.precision),
+           "points": results}
+if not a.no_cpu:
+    try:
+        summary["cpu_baseline"] = cpu_reference()
+    except FileNotFoundError as e:
+        summary["cpu_baseline"] = {"unavailable": str(e)}
+print(json.dumps(summary))
