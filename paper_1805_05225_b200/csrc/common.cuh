@@ -51,6 +51,11 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 __device__ __forceinline__ void red_release_gpu(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// several counters after ONE release fence: fence_acq_rel_gpu(); red_relaxed_gpu(...) x n
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // All threads of the CTA call this.  `target` = CTAs in the group * (episode+1).
 __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();

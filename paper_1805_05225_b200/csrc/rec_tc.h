@@ -23,7 +23,7 @@ __host__ __device__ inline size_t cprev_save_off(int s, int row, int B, int H, i
 
 // Step counters of the persistent recurrences: kBarPerChunk zeroed unsigned
 // per 256-row batch chunk (one launch each), rec_bar_count(B) in total.
-constexpr int kBarPerChunk = 64;
+constexpr int kBarPerChunk = 512;  // fwd: [dir][tile][16 K groups]; bwd: [dir][tile][128 DZ boxes]
 inline size_t rec_bar_count(int B) { return (size_t)kBarPerChunk * ((B + 255) / 256); }
 
 struct TcRecFwdArgs {

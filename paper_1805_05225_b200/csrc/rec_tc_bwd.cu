@@ -26,6 +26,7 @@ namespace {
 using namespace rtc;
 
 constexpr int kStages = 6;
+constexpr int kBoxCtrs = 128;  // step counters per (direction, batch tile): one per DZ box
 constexpr uint32_t kTile = 128 * 64 * 2;  // 16 KB A tile
 constexpr uint32_t kSmemMax = 227 * 1024;
 
@@ -119,7 +120,25 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   __syncthreads();
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
-  unsigned* ctr = a.bar + d * 2;
+  // Step counters per (direction, batch tile, DZ box of kb*64 ring columns): a
+  // CTA publishes DZ_s of its units to every box its columns fall in (<= 2 per
+  // gate), and a consumer streams each box of its K slice as soon as THAT box's
+  // producers (a handful of CTAs) published — not the slowest of all P.
+  const int bw = a.kb * 64;
+  unsigned* ctr = a.bar + d * 2 * kBoxCtrs;
+  const int hq8c = dz_ring_hq(a.H);
+  auto box_producers = [&](int gb) -> unsigned {  // CTAs whose DZ columns hit box gb
+    const int lo = gb * bw, hi = lo + bw;
+    unsigned n = 0;
+    for (int c = 0; c < a.P; ++c) {
+      const int ua = c * U, ub = min(ua + U, a.H);
+      bool hit = false;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) hit |= ua < ub && g * hq8c + ua < hi && g * hq8c + ub > lo;
+      n += hit ? 1u : 0u;
+    }
+    return n;
+  };
   // debug trace: one CTA (trace_cta >= 0, [T][16]) or every CTA (trace_cta < 0, [grid][T][16])
   unsigned long long* trace =
       (a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta))
@@ -127,46 +146,55 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int ngrp = nkc / a.kb;  // TMA boxes per tile
   const int kc_off = cta % ngrp;
 
-  if (warp == 0) {
-    if (lane == 0) {  // -------------------------------------------- producer
+  if (warp == 0) {  // ---------------------------------------------- producer
+    if (lane == 0) {
       tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
       for (int kc = 0; kc < nkc; ++kc)
         tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
-      int st = 0;
-      uint32_t ph = 0;
-      const int nst = a.stages;
-      // the saved activations the epilogue reads this iteration: this CTA's
-      // 16-unit chunk of the 4 gates and of c_{s-1}, all rows of the launch
-      const int pf_u = (u0 / 16) * 16;
-      const int pf_rows = min(a.B - a.b0, MT * 128);
-      const bool pf = a.gates[d] != nullptr && u0 < a.H && !(a.debug_flags & 32);
-      for (int s = 0; s < Tmax; ++s) {  // s = iteration (processing step Tmax-1-s)
-        const int slot = s & 1;          // ring slot holding DZ of the previous iteration
-        if (pf) {
-          const int ps = Tmax - 1 - s;
+    }
+    int st = 0;  // ring position, tracked by every lane (lane 0 issues)
+    uint32_t ph = 0;
+    const int nst = a.stages;
+    // the saved activations the epilogue reads this iteration: this CTA's
+    // 16-unit chunk of the 4 gates and of c_{s-1}, all rows of the launch
+    const int pf_u = (u0 / 16) * 16;
+    const int pf_rows = min(a.B - a.b0, MT * 128);
+    const bool pf = a.gates[d] != nullptr && u0 < a.H && !(a.debug_flags & 32);
+    // lane k polls the k-th box of this CTA's K slice in issue order
+    const int kg_lane = (lane + kc_off) % ngrp;
+    const int gb_lane = r * (Kc / bw) + kg_lane;
+    const unsigned exp_lane = lane < ngrp ? box_producers(gb_lane) : 0u;
+    for (int s = 0; s < Tmax; ++s) {  // s = iteration (processing step Tmax-1-s)
+      const int slot = s & 1;          // ring slot holding DZ of the previous iteration
+      if (pf && lane == 0) {
+        const int ps = Tmax - 1 - s;
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            prefetch_l2(a.gates[d] + gate_save_off(ps, g, a.b0, a.B, a.H, pf_u), pf_rows * 32);
-          prefetch_l2(a.cprev[d] + cprev_save_off(ps, a.b0, a.B, a.H, pf_u), pf_rows * 32);
-        }
-        for (int mt = 0; mt < MT; ++mt) {
-          if (s > 0) {
-            const unsigned target = (unsigned)a.P * (unsigned)s;
-            while (ld_acquire(ctr + mt) < target) {
+        for (int g = 0; g < 4; ++g)
+          prefetch_l2(a.gates[d] + gate_save_off(ps, g, a.b0, a.B, a.H, pf_u), pf_rows * 32);
+        prefetch_l2(a.cprev[d] + cprev_save_off(ps, a.b0, a.B, a.H, pf_u), pf_rows * 32);
+      }
+      for (int mt = 0; mt < MT; ++mt) {
+        const unsigned target = exp_lane * (unsigned)s;
+        bool rdy = lane >= ngrp || s == 0;
+        int done = 0;
+        while (done < ngrp) {
+          if (!rdy) rdy = ld_acquire(ctr + mt * kBoxCtrs + gb_lane) >= target;
+          const unsigned m = __ballot_sync(0xffffffffu, rdy);
+          while (done < ngrp && ((m >> done) & 1u)) {
+            if (lane == 0) {
+              if (done == 0 && trace) trace[s * 16 + (mt == 0 ? 0 : 3)] = gtimer();
+              const int kg = (done + kc_off) % ngrp;
+              tc::fence_proxy_async_global();  // the box's DZ (generic-proxy stores) -> TMA reads
+              tc::mbar_wait(&empty_bar[st], ph ^ 1);
+              tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
+              tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
+                          (r * (Kc / 64) + kg * a.kb) * 8, slot);
             }
-            tc::fence_proxy_async_global();
-          }
-          if (trace) trace[s * 16 + (mt == 0 ? 0 : 3)] = gtimer();
-          for (int kq = 0; kq < ngrp; ++kq) {
-            const int kg = (kq + kc_off) % ngrp;
-            tc::mbar_wait(&empty_bar[st], ph ^ 1);
-            tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
-            tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
-                        (r * (Kc / 64) + kg * a.kb) * 8, slot);
             if (++st == nst) {
               st = 0;
               ph ^= 1;
             }
+            ++done;
           }
         }
       }
@@ -372,7 +400,18 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
-        red_release_gpu(ctr + mt, 1u);
+        {  // every DZ box my columns fall in (ascending, each once), after ONE release fence
+          const int ua = u0, ub = min(u0 + U, H);
+          int prev = -1;
+          fence_acq_rel_gpu();
+#pragma unroll 1
+          for (int g = 0; g < 4 && ua < ub; ++g)
+            for (int gb = (g * hq8c + ua) / bw; gb <= (g * hq8c + ub - 1) / bw; ++gb)
+              if (gb != prev) {
+                red_relaxed_gpu(ctr + mt * kBoxCtrs + gb, 1u);
+                prev = gb;
+              }
+        }
         if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
           for (int pi = 1; pi < C; ++pi)
             mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), kEpiTile);
@@ -547,6 +586,8 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   for (int st = kStages; st >= 2 && !a.stages; --st)
     if (bwd_smem(sh.C, sh.U, Kc, a.kb == 2 ? st : (st + 1) / 2) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
+  SL_REQUIRE(a.Kz / (a.kb * 64) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
+             "rec_bwd_tc: too many DZ boxes for the step counters");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
