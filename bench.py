@@ -53,18 +53,30 @@ def parse():
     ap.add_argument("--src-vocab", type=int, default=20000, help="source embedding table rows; 0 = feed embeddings")
     ap.add_argument("--trg-vocab", type=int, default=20000,
                     help="target embedding table rows (needs --vocab); 0 = feed embeddings")
+    ap.add_argument("--no-attention", action="store_true",
+                    help="the pre-attention step (decoder context = encoder output at t) instead of Listing 1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.attention = not a.no_attention
+    if a.attention and not (a.vocab and a.src_vocab and a.trg_vocab and a.precision == "bf16"):
+        ap.error("the attention step needs --vocab, --src-vocab, --trg-vocab > 0 and bf16 (or --no-attention)")
+    return a
 
 
-def flops_per_token(L, D0, H, V=0):
+def flops_per_token(L, D0, H, V=0, attention=False, Ts=60):
     """Algorithmic GEMM flops per target token, fwd+bwd: 24 H (D + H)
     per layer-direction — the encoder's 2L layer-directions plus the decoder
-    layer (D = D0 + 2H); T_src = T_tgt — plus 6 H V for the output layer."""
+    cell (D = D0 + 2H); T_src = T_tgt — plus 6 H V for the output layer.  With
+    attention (key = readout = H, enc = 2H): + 6 E K (enc_ctx) + 6 H K (s_tr)
+    + 6 (H + D0 + E) H (readout) + 6 Ts (K + E) (energies and context, fwd + bwd)."""
     enc = sum(2 * 24 * H * ((D0 if l == 0 else 2 * H) + H) for l in range(L))
-    return enc + 24 * H * (D0 + 2 * H + H) + 6 * H * V
+    f = enc + 24 * H * (D0 + 2 * H + H) + 6 * H * V
+    if attention:
+        E, K = 2 * H, H
+        f += 6 * E * K + 6 * H * K + 6 * (H + D0 + E) * H + 6 * Ts * (K + E)
+    return f
 
 
 # ---------------------------------------------------------------- clocks
@@ -192,8 +204,30 @@ def cpu_reference(args, steps=1):
         xo = rng.uniform(-1, 1, (1, T, H))
         tgo = rng.integers(0, V, (1, T)).astype(np.int32)
 
+    att_case = None
+    if getattr(args, "attention", False) and kind == "reference":
+        E, K = 2 * H, H
+        att_case = dict(enc_ctx=rng.uniform(-1, 1, (1, T, K)), enc=rng.uniform(-1, 1, (1, T, E)),
+                        Ws=rng.uniform(-s, s, (H, K)), bs=rng.uniform(-s, s, K), Wfb=rng.uniform(-s, s, (1, K)),
+                        bfb=rng.uniform(-s, s, K), v=rng.uniform(-s, s, (K, 1)), bv=0.1)
+        att_in = dict(s=rng.uniform(-1, 1, (1, H)), accum=rng.uniform(0, 1, (1, T)),
+                      d_att=rng.uniform(-1, 1, (1, E)), d_accum=rng.uniform(-1, 1, (1, T)))
+        Wd, Rd_, bd = params[D0 + 2 * H]
+        xc, hc, cc = rng.uniform(-1, 1, (1, D0 + 2 * H)), rng.uniform(-1, 1, (1, H)), rng.uniform(-1, 1, (1, H))
+        Wro = rng.uniform(-s, s, (H + D0 + E, H)).astype(np.float32)
+        xro = rng.uniform(-1, 1, (T, H + D0 + E)).astype(np.float32)
+
     def one(out):
         tt = {}
+        if att_case is not None:  # the step-by-step attention decoder of one sequence, fwd + bwd
+            t0 = time.perf_counter()
+            for _ in range(T):
+                ref.step(xc, hc, cc, Wd, Rd_, bd, gh=hc, gc=cc)          # RnnCell s (lstm_step + closure)
+                ref.attention_step(lens, **att_case, s=att_in["s"], accum=att_in["accum"],
+                                   d_att=att_in["d_att"], d_accum=att_in["d_accum"])
+            y = np.maximum(xro @ Wro, 0)                                  # readout fwd + both GEMMs of its bwd
+            _ = (y @ Wro.T, xro.T @ y)
+            tt["dec"] = time.perf_counter() - t0
         if (Vs or Vt) and kind == "reference":
             t0 = time.perf_counter()
             for Vv in [v for v in (Vs, Vt) if v]:
@@ -203,7 +237,7 @@ def cpu_reference(args, steps=1):
             t0 = time.perf_counter()
             ref.output_ce(xo, lens, tgo, Wo, bo, 0.1)
             tt["out"] = time.perf_counter() - t0
-        for D in shapes:
+        for D in (shapes[:2] if att_case is not None else shapes):
             W, R, b = params[D]
             t0 = time.perf_counter()
             if kind == "reference":
@@ -221,13 +255,16 @@ def cpu_reference(args, steps=1):
             t.start()
         for t in ths:
             t.join()
-        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r[D0 + 2 * H] + r.get("out", 0.0) + r.get("emb", 0.0)
-                   for r in res]
+        per_seq = [2 * r[D0] + 2 * (L - 1) * r[2 * H] + r.get("dec", r.get(D0 + 2 * H, 0.0)) + r.get("out", 0.0)
+                   + r.get("emb", 0.0) for r in res]
         rates.append(threads * T / (max(per_seq) + adam_s))
     value = statistics.median(rates)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{threads} threads x 1 sequence (T={T}); per thread one fwd+bwd layer-direction "
-                      f"of each shape (D={D0}, D={2 * H}, decoder D={D0 + 2 * H}; H={H}), the output "
+                      f"of each shape (D={D0}, D={2 * H}; H={H}), the decoder "
+                      + ("(T x [lstm_step + closure, D=" + str(D0 + 2 * H) + "] + T x [attention step fwd+bwd, "
+                         "Ts=" + str(T) + "] + the readout GEMMs)" if att_case is not None else
+                         "(one lstm_sequence D=" + str(D0 + 2 * H) + ")") + f", the output "
                       f"softmax + CE (V={V}) and the src/trg embedding lookups (gather_rows fwd+bwd, "
                       f"V={Vs}/{Vt}), step time = 2 t(D0) + {2 * (L - 1)} t(2H) + t(dec) + t(out) + t(emb) "
                       f"(layers run sequentially in the reference) "
@@ -242,13 +279,16 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_1805_05225_b200 import lstm
-    from paper_1805_05225_b200.model import Seq2SeqLSTM
+    from paper_1805_05225_b200.model import Seq2SeqAttention, Seq2SeqLSTM
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
     Vs, Vt = args.src_vocab, (args.trg_vocab if args.vocab else 0)
-    model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev, vocab=args.vocab, src_vocab=Vs, trg_vocab=Vt)
+    if args.attention:
+        model = Seq2SeqAttention(L, B, T, T, D0, H, args.vocab, Vs, Vt, device=dev)
+    else:
+        model = Seq2SeqLSTM(L, B, T, D0, H, args.precision, dev, vocab=args.vocab, src_vocab=Vs, trg_vocab=Vt)
     model.init_uniform(seed=1)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
     if Vs:  # source token ids (the `src` embedding layer looks them up)
@@ -262,7 +302,7 @@ def run_ours(args, rank, world, local_rank):
                            dtype=torch.int32)
     else:
         dy = torch.rand(B, T, H, device=dev, generator=g) * 2 - 1  # dL/d(decoder output)
-    if not Vt:
+    if not Vt and not args.attention:
         model.set_target_embeddings(emb)
     lib = lstm.lib()
     lib.sl_profile_enable.argtypes = [ctypes.c_int]
@@ -340,12 +380,12 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         # per step in: source ids (or embeddings), target ids (or target
         # embeddings + the upstream gradient), lengths; out: the scalar loss
-        hin = [x, lens] + ([dy] if args.vocab else []) + ([] if Vt else [emb])
+        hin = [x, lens] + ([dy] if args.vocab else []) + ([] if Vt or args.attention else [emb])
         hosts = [t.cpu().pin_memory() for t in hin]
         devs = [torch.empty_like(t) for t in hin]
         xd, ld = devs[0], devs[1]
         dyd = devs[2] if args.vocab else dy
-        ed = devs[-1] if not Vt else None
+        ed = devs[-1] if not (Vt or args.attention) else None
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
 
         def e2e_step():
@@ -397,10 +437,18 @@ def main():
     Vt = args.trg_vocab if args.vocab else 0
     emb_s = (f"src/trg embedding lookups from token ids (V={args.src_vocab}/{Vt}) + " if args.src_vocab or Vt
              else "")
-    cfg = {"workload": f"config4 training step: {emb_s}{L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
-                       f"H={H} (input {D0}+{2 * H}){out_s}, T_src=T_tgt={T}, fwd+bwd + fused "
-                       f"clip(5.0)+Adam (+DP grad all-reduce at N>1); MLP attention measured standalone, "
-                       f"not in this step (context = encoder output at t)",
+    if args.attention:
+        work = (f"config4 training step (Listing-1 attention model): src/trg embedding lookups from token ids "
+                f"(V={args.src_vocab}/{Vt}, width {D0}) + {L}xBLSTM encoder H={H} + enc_ctx + LSTM decoder cell "
+                f"H={H} with input feeding [prev trg {D0} ‖ prev att {2 * H}] + MLP attention (key {H}, weight "
+                f"feedback) + relu readout {H} + output softmax V={args.vocab} with label-smoothed CE (eps 0.1), "
+                f"teacher forcing, T_src=T_tgt={T}, fwd+bwd + fused clip(5.0)+Adam over all parameters "
+                f"(+DP grad all-reduce at N>1); no dropout")
+    else:
+        work = (f"config4 training step: {emb_s}{L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
+                f"H={H} (input {D0}+{2 * H}){out_s}, T_src=T_tgt={T}, fwd+bwd + fused "
+                f"clip(5.0)+Adam (+DP grad all-reduce at N>1); no attention (context = encoder output at t)")
+    cfg = {"workload": work, "attention": args.attention,
            "vocab": args.vocab, "src_vocab": args.src_vocab, "trg_vocab": Vt,
            "global_batch": B * world, "batch_per_gpu": B,
            "seq_len": T, "hidden": H, "input_dim": D0, "layers": L, "directions": 2,
@@ -476,7 +524,7 @@ def main():
            "config": dict(cfg, cuda_graph=r["graph"], eager_ms_per_step=r["eager_ms"]),
            "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
            "roofline": roof,
-           "algorithmic_tflops": flops_per_token(L, D0, H, args.vocab) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}
+           "algorithmic_tflops": flops_per_token(L, D0, H, args.vocab, args.attention, T) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             out["cpu_baseline"] = cpu_reference(args, steps=1)

@@ -180,6 +180,55 @@ int sl_attention_step_bwd(const sl_attention* att, const int32_t* src_lens, cons
                           float* d_b_fb, float* d_v, float* d_b_v, int accumulate, void* workspace,
                           size_t workspace_bytes, sl_stream_t stream);
 
+/* ---- the Listing-1 attention decoder over a target sequence ----
+ * The reference's `output` subnetwork as its training loop evaluates it with
+ * teacher forcing (models.cpp:83-166; compiler.cpp:770-905 runs it step by
+ * step), plus the base layer enc_ctx (models.cpp:60), per target step t:
+ *   s_t, c_t = lstm_step([trg_{t-1} ‖ att_{t-1}], s_{t-1}, c_{t-1})  (RnnCell `s`)
+ *   e = tanh(enc_ctx + accum_{t-1} W_fb + b_fb + s_t W_s + b_s) v + b_v
+ *   a_t = softmax over the valid source positions, accum_t = accum_{t-1} + a_t
+ *   att_t = sum_j a_t[j] enc_j
+ *   readout_t = relu([s_t ‖ trg_{t-1} ‖ att_t] W_ro + b_ro)
+ * with trg_{t-1} = trg_W[prev_ids[b, t]] (prev_ids < 0: the zero initial
+ * output), att_{-1} = s_{-1} = c_{-1} = accum_{-1} = 0.  The output_prob layer
+ * and its loss are sl_output_ce on `readout`.
+ * enc is the encoder output in the padded bf16 layout sl_lstm_layer writes with
+ * SL_LAYER_Y_BF16 ([B, Ts, enc_ld], enc_ld >= sl_lstm_bf16_pitch(enc_dim), 1.0
+ * at column enc_dim); prev_ids [B, T] int32; readout [B, T, readout_dim] fp32.
+ * Parameters / gradients are fp32 in the reference layouts (compiler.cpp:
+ * 470-500); the backward overwrites every gradient and d_enc [B, Ts, enc_dim].
+ * bf16 tensor-core operands, fp32 accumulation and cell state (SL_PREC_BF16
+ * tolerance).  The workspace carries the forward's saved activations to the
+ * backward (same parameters, inputs and workspace).  Limits: batch <= 256 per
+ * call; hidden, enc_dim, key_dim, readout_dim multiples of 8; key_dim <= 1024;
+ * an out-of-range prev id sets *bad_row (the reference's IndexError).  Every
+ * parameter / gradient pointer must be 16 B aligned. */
+typedef struct sl_attn_decoder {
+  int32_t batch, src_time, trg_time, embed_dim, enc_dim, hidden, key_dim, readout_dim, trg_vocab;
+} sl_attn_decoder;
+typedef struct sl_attn_decoder_params {
+  const float *enc_ctx_W, *enc_ctx_b;    /* [E, K], [K]            */
+  const float *s_W, *s_R, *s_b;          /* [Emb+E, 4H], [H, 4H], [4H] */
+  const float *fb_W, *fb_b;              /* weight_feedback [1, K], [K] */
+  const float *s_tr_W, *s_tr_b;          /* [H, K], [K]            */
+  const float *e_W, *e_b;                /* [K, 1], [1]            */
+  const float *readout_W, *readout_b;    /* [H+Emb+E, Rd], [Rd]    */
+  const float *trg_W;                    /* [trg_vocab, Emb]       */
+} sl_attn_decoder_params;
+typedef struct sl_attn_decoder_grads {
+  float *enc_ctx_W, *enc_ctx_b, *s_W, *s_R, *s_b, *fb_W, *fb_b, *s_tr_W, *s_tr_b, *e_W, *e_b, *readout_W,
+      *readout_b, *trg_W;
+} sl_attn_decoder_grads;
+size_t sl_attn_decoder_workspace_size(const sl_attn_decoder* dec);
+int sl_attn_decoder_fwd(const sl_attn_decoder* dec, const sl_attn_decoder_params* params, const void* enc_bf16,
+                        int64_t enc_ld, const int32_t* src_lens, const int32_t* prev_ids, float* readout,
+                        int32_t* bad_row, void* workspace, size_t workspace_bytes, sl_stream_t stream);
+int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params* params,
+                        const sl_attn_decoder_grads* grads, const void* enc_bf16, int64_t enc_ld,
+                        const int32_t* src_lens, const int32_t* prev_ids, const float* readout,
+                        const float* d_readout, float* d_enc, void* workspace, size_t workspace_bytes,
+                        sl_stream_t stream);
+
 /* ---- output layer + loss ---------------------------------------
  * The decoder's Softmax layer and its training loss in one call: logits =
  * x W + b (reference compiler.cpp:651-663), log_softmax (tape.cpp:879-924),
@@ -229,6 +278,7 @@ int sl_embedding_bwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t d
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
  *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam, k7_logits_gemm, k7_softmax_ce,
  *   k7_dx_gemm, k7_dw_gemm, k8_attention_fwd, k8_attention_bwd, k9_embedding_fwd,
+ *   k10_dec_*,
  *   k9_embedding_bwd */
 typedef struct sl_profile_entry {
   char name[32];

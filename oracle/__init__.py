@@ -354,3 +354,97 @@ def seeded_case(seed: int, B: int, T: int, D: int, H: int, ragged: bool = True,
     else:
         lens = np.full(B, T, dtype=np.int32)
     return x, lens, W, R, b
+
+
+def lstm_step_np(x, h, c, W, R, b, gh=None, gc=None):
+    """fp64 numpy restatement of Tape::lstm_step (tape.cpp:1095-1135) and its
+    backward closure (tape.cpp:1157-1215).  Forward: (h', c').  With gh:
+    (dx, dh, dc, dW, dR, db) for upstream gh, gc (gc None = 0)."""
+    x, h, c, W, R, b = (np.asarray(a, np.float64) for a in (x, h, c, W, R, b))
+    H = h.shape[1]
+    z = x @ W + h @ R + b
+    sig = lambda v: 1.0 / (1.0 + np.exp(-v))
+    i, f, g, o = sig(z[:, :H]), sig(z[:, H:2 * H]), np.tanh(z[:, 2 * H:3 * H]), sig(z[:, 3 * H:])
+    c2 = f * c + i * g
+    tc = np.tanh(c2)
+    if gh is None:
+        return o * tc, c2
+    gh = np.asarray(gh, np.float64)
+    gc = np.zeros_like(gh) if gc is None else np.asarray(gc, np.float64)
+    d_o = gh * tc
+    dc = gc + gh * o * (1 - tc * tc)
+    dz = np.concatenate([dc * g * i * (1 - i), dc * c * f * (1 - f), dc * i * (1 - g * g), d_o * o * (1 - o)], axis=1)
+    return dz @ W.T, dz @ R.T, dc * f, x.T @ dz, h.T @ dz, dz.sum(axis=0)
+
+
+def attn_decoder_np(src_lens, enc, prev_ids, P, d_readout=None, relu_mask=None):
+    """fp64 restatement of the Listing-1 `output` subnetwork over a teacher-forced
+    target sequence as the reference's training loop evaluates it (models.cpp:
+    83-166, compiler.cpp:770-905: one step per target position, loop-carried
+    prev: values starting at zero, compiler.cpp:674-697) plus the base layer
+    enc_ctx (models.cpp:60).  It chains the two pinned per-step restatements —
+    lstm_step_np (the RnnCell `s`) and attention_step_np — and a relu Linear
+    readout.  P: dict with the decoder.NAMES keys (reference shapes).
+    Returns readout [B, T, Rd]; with d_readout also the gradients (dict, same
+    keys) and d_enc, by the reverse replay of those steps (tape.cpp:1363-1381).
+    relu_mask (optional, [B, T, Rd] bool): the readout's relu derivative to use
+    instead of pre > 0 — a lower-precision run may round a pre-activation within
+    its error of 0 to the other side; comparing gradients needs the same mask."""
+    enc = np.asarray(enc, np.float64)
+    P = {k: np.asarray(v, np.float64) for k, v in P.items()}
+    B, Ts, E = enc.shape
+    T = prev_ids.shape[1]
+    H = P["s_R"].shape[0]
+    Emb = P["trg_W"].shape[1]
+    ids = np.asarray(prev_ids)
+    trg = np.where(ids[..., None] >= 0, P["trg_W"][np.maximum(ids, 0)], 0.0)       # [B, T, Emb]
+    enc_ctx = enc @ P["enc_ctx_W"] + P["enc_ctx_b"]
+    s, c, att, acc = np.zeros((B, H)), np.zeros((B, H)), np.zeros((B, E)), np.zeros((B, Ts))
+    att_args = lambda: (P["s_tr_W"], P["s_tr_b"], P["fb_W"], P["fb_b"], P["e_W"], P["e_b"][0])
+    saves, S, ATT = [], np.zeros((B, T, H)), np.zeros((B, T, E))
+    for t in range(T):
+        x = np.concatenate([trg[:, t], att], axis=1)
+        s2, c2 = lstm_step_np(x, s, c, P["s_W"], P["s_R"], P["s_b"])
+        att2, _, acc2, _ = attention_step_np(src_lens, enc_ctx, enc, s2, acc, *att_args())
+        saves.append((x, s, c, s2, acc))
+        S[:, t], ATT[:, t] = s2, att2
+        s, c, att, acc = s2, c2, att2, acc2
+    RO = np.concatenate([S, trg, ATT], axis=2)
+    pre = RO @ P["readout_W"] + P["readout_b"]
+    readout = np.maximum(pre, 0.0)
+    if d_readout is None:
+        return readout
+    attn_decoder_np.pre = pre
+    dpre = np.asarray(d_readout, np.float64) * (pre > 0 if relu_mask is None else np.asarray(relu_mask))
+    g = {k: np.zeros_like(v) for k, v in P.items()}
+    g["readout_W"] = RO.reshape(B * T, -1).T @ dpre.reshape(B * T, -1)
+    g["readout_b"] = dpre.sum(axis=(0, 1))
+    dRO = dpre @ P["readout_W"].T
+    dS, dTRG, dATT = dRO[:, :, :H], dRO[:, :, H:H + Emb].copy(), dRO[:, :, H + Emb:]
+    d_enc, d_ctx = np.zeros_like(enc), np.zeros_like(enc_ctx)
+    dh, dc, datt, dacc = np.zeros((B, H)), np.zeros((B, H)), np.zeros((B, E)), np.zeros((B, Ts))
+    for t in reversed(range(T)):
+        x, s_prev, c_prev, s_t, acc_prev = saves[t]
+        _, _, _, ga = attention_step_np(src_lens, enc_ctx, enc, s_t, acc_prev, *att_args(),
+                                        d_att=dATT[:, t] + datt, d_accum=dacc)
+        d_ctx += ga["enc_ctx"]
+        d_enc += ga["enc"]
+        for mine, theirs in (("s_tr_W", "Ws"), ("s_tr_b", "bs"), ("fb_W", "Wfb"), ("fb_b", "bfb"), ("e_W", "v"),
+                             ("e_b", "bv")):
+            g[mine] += ga[theirs]
+        dacc = ga["accum"]
+        dx, dh, dc, dW, dR, db = lstm_step_np(x, s_prev, c_prev, P["s_W"], P["s_R"], P["s_b"],
+                                              gh=dS[:, t] + dh + ga["s"], gc=dc)
+        g["s_W"] += dW
+        g["s_R"] += dR
+        g["s_b"] += db
+        dTRG[:, t] += dx[:, :Emb]
+        datt = dx[:, Emb:]
+    d_enc += d_ctx @ P["enc_ctx_W"].T
+    g["enc_ctx_W"] = enc.reshape(B * Ts, E).T @ d_ctx.reshape(B * Ts, -1)
+    g["enc_ctx_b"] = d_ctx.sum(axis=(0, 1))
+    flat, rows = ids.reshape(-1), dTRG.reshape(B * T, Emb)
+    for r in np.argsort(flat, kind="stable"):     # gather_rows adjoint (tape.cpp:476-488)
+        if flat[r] >= 0:
+            g["trg_W"][flat[r]] += rows[r]
+    return readout, g, d_enc

@@ -15,6 +15,7 @@
 #include "attention.h"
 #include "embedding.h"
 #include "cell.h"
+#include "decoder.h"
 #include "convert.h"
 #include "gemm.h"
 #include "profile.h"
@@ -406,6 +407,77 @@ int sl_embedding_bwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t d
                "embedding: workspace too small");
     embedding_bwd(n_ids, ids, vocab, dim, d_out, d_out_ld, d_table, accumulate != 0, workspace,
                   reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+static DecDims dec_dims(const sl_attn_decoder* d) {
+  SL_REQUIRE(d, SL_ERR_INVALID_ARGUMENT, "attn_decoder: null descriptor");
+  return DecDims{d->batch, d->src_time, d->trg_time, d->embed_dim, d->enc_dim, d->hidden, d->key_dim,
+                 d->readout_dim, d->trg_vocab};
+}
+static DecParams dec_params(const sl_attn_decoder_params* p) {
+  SL_REQUIRE(p, SL_ERR_INVALID_ARGUMENT, "attn_decoder: null params");
+  const float* all[] = {p->enc_ctx_W, p->enc_ctx_b, p->s_W, p->s_R, p->s_b, p->fb_W, p->fb_b,
+                        p->s_tr_W, p->s_tr_b, p->e_W, p->e_b, p->readout_W, p->readout_b, p->trg_W};
+  for (const float* q : all)
+    SL_REQUIRE(q && ((uintptr_t)q & 15) == 0, SL_ERR_INVALID_ARGUMENT,
+               "attn_decoder: parameter pointers must be non-null and 16 B aligned");
+  return DecParams{p->enc_ctx_W, p->enc_ctx_b, p->s_W, p->s_R, p->s_b, p->fb_W, p->fb_b,
+                   p->s_tr_W, p->s_tr_b, p->e_W, p->e_b, p->readout_W, p->readout_b, p->trg_W};
+}
+
+size_t sl_attn_decoder_workspace_size(const sl_attn_decoder* dec) {
+  try {
+    const DecDims d = dec_dims(dec);
+    decoder_check(d);
+    set_error("");
+    return decoder_workspace_bytes(d);
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return 0;
+  }
+}
+
+int sl_attn_decoder_fwd(const sl_attn_decoder* dec, const sl_attn_decoder_params* params, const void* enc_bf16,
+                        int64_t enc_ld, const int32_t* src_lens, const int32_t* prev_ids, float* readout,
+                        int32_t* bad_row, void* workspace, size_t workspace_bytes, sl_stream_t stream) {
+  return guarded([&] {
+    const DecDims d = dec_dims(dec);
+    decoder_check(d);
+    const DecParams p = dec_params(params);
+    SL_REQUIRE(enc_bf16 && src_lens && prev_ids && readout && bad_row, SL_ERR_INVALID_ARGUMENT,
+               "attn_decoder: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= decoder_workspace_bytes(d), SL_ERR_WORKSPACE,
+               "attn_decoder: workspace too small");
+    decoder_fwd(d, p, static_cast<const __nv_bfloat16*>(enc_bf16), enc_ld, src_lens, prev_ids, readout, bad_row,
+                workspace, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params* params,
+                        const sl_attn_decoder_grads* grads, const void* enc_bf16, int64_t enc_ld,
+                        const int32_t* src_lens, const int32_t* prev_ids, const float* readout,
+                        const float* d_readout, float* d_enc, void* workspace, size_t workspace_bytes,
+                        sl_stream_t stream) {
+  return guarded([&] {
+    const DecDims d = dec_dims(dec);
+    decoder_check(d);
+    const DecParams p = dec_params(params);
+    SL_REQUIRE(grads, SL_ERR_INVALID_ARGUMENT, "attn_decoder: null grads");
+    const sl_attn_decoder_grads& q = *grads;
+    float* all[] = {q.enc_ctx_W, q.enc_ctx_b, q.s_W, q.s_R, q.s_b, q.fb_W, q.fb_b,
+                    q.s_tr_W, q.s_tr_b, q.e_W, q.e_b, q.readout_W, q.readout_b, q.trg_W};
+    for (float* x : all)
+      SL_REQUIRE(x && ((uintptr_t)x & 15) == 0, SL_ERR_INVALID_ARGUMENT,
+                 "attn_decoder: gradient pointers must be non-null and 16 B aligned");
+    SL_REQUIRE(enc_bf16 && src_lens && prev_ids && readout && d_readout && d_enc, SL_ERR_INVALID_ARGUMENT,
+               "attn_decoder: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= decoder_workspace_bytes(d), SL_ERR_WORKSPACE,
+               "attn_decoder: workspace too small");
+    const DecGrads g{q.enc_ctx_W, q.enc_ctx_b, q.s_W, q.s_R, q.s_b, q.fb_W, q.fb_b,
+                     q.s_tr_W, q.s_tr_b, q.e_W, q.e_b, q.readout_W, q.readout_b, q.trg_W};
+    decoder_bwd(d, p, g, static_cast<const __nv_bfloat16*>(enc_bf16), enc_ld, src_lens, prev_ids, readout,
+                d_readout, d_enc, workspace, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

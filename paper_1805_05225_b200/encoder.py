@@ -26,12 +26,14 @@ class BLSTMEncoder:
 
     def __init__(self, num_layers: int, batch: int, time: int, input_dim: int, hidden: int,
                  precision: str = "bf16", device=None, params=None, grads=None, train: bool = True,
-                 x0_bf16: bool = False):
+                 x0_bf16: bool = False, top_bf16: bool = False):
         """params / grads: optional flat fp32 views (numel() elements) to live in,
         e.g. slices of a whole model's buffers; by default the encoder owns them.
         train=False: inference only (no reserves, no gradients, one workspace
         shared by all layers — BASELINE config 5).  x0_bf16 (bf16): layer 0 takes
-        the padded bf16 input directly (e.g. written by the embedding lookup)."""
+        the padded bf16 input directly (e.g. written by the embedding lookup);
+        top_bf16 (bf16): the top layer writes that layout too (the attention
+        decoder's input, decoder.py) instead of fp32."""
         self.L, self.B, self.T, self.D0, self.H = num_layers, batch, time, input_dim, hidden
         self.precision = precision
         self.device = torch.device(device or "cuda")
@@ -69,7 +71,7 @@ class BLSTMEncoder:
         # next layer's input GEMM reads (SL_LAYER_Y_BF16 -> SL_LAYER_X_BF16); only
         # the top layer's output is fp32
         chain = precision == "bf16"
-        last = num_layers - 1
+        last = num_layers - 1 + (1 if chain and top_bf16 else 0)
         shared = None
         if not train:  # the layers run one after another: one workspace serves all of them
             need = max(lstm.LSTMLayer.workspace_size(batch, time, D, H, 2, 1, precision,
@@ -88,8 +90,9 @@ class BLSTMEncoder:
         if train:
             self.acts = [act(l) for l in range(num_layers)]
         else:  # inference keeps nothing for a backward: the inner layers ping-pong two buffers
-            inner = [act(l) for l in range(min(2, last))]
-            self.acts = [inner[l % 2] for l in range(last)] + [act(last)]
+            top = num_layers - 1
+            inner = [act(l) for l in range(min(2, top))]
+            self.acts = [inner[l % 2] for l in range(top)] + [act(top)]
         self.dxs = [torch.empty(batch, time, D, dtype=torch.float32, device=self.device)
                     for D in self.in_dims] if train else []
 

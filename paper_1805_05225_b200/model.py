@@ -216,3 +216,151 @@ class Seq2SeqLSTM:
             reducer.wait()
         self.opt.step(self.grads, grad_scale=grad_scale)
         return loss
+
+
+class Seq2SeqAttention:
+    """The full Listing-1 attention model's training step (BASELINE configs[3]:
+    "6-layer BLSTM n=1000 encoder + 1-layer LSTM decoder with MLP attention, full
+    training step with Adam"; make_attention_model, models.cpp:26-184):
+
+      src (embedding of the source ids) -> enc0..enc{L-1} (BLSTM, lstm_sequence)
+      -> encoder -> enc_ctx;  the `output` subnetwork (decoder.AttnDecoder: the
+      RnnCell s with input feeding of the previous attention, the MLP attention,
+      the readout) over the teacher-forced target;  output_prob (softmax +
+      label-smoothed CE, output.OutputCE) on the readout;  then the fused
+      global-norm clip + Adam step.
+
+    Dropout on the output_prob input (models.hpp:18) is not applied (a
+    deterministic step; it would be one fused mask multiply).  The encoder's top
+    layer writes the padded bf16 layout the decoder's GEMMs read directly.
+    Parameters use the reference's qualified manifest names
+    (compiler.cpp:470-500) and live in ONE flat fp32 buffer; the gradient
+    buckets (output_prob, the decoder subnetwork, each encoder layer, src) are
+    slices of it, reduced as soon as each is complete (dp.BucketAllReducer)."""
+
+    def __init__(self, enc_layers: int, batch: int, src_time: int, trg_time: int, emb: int, hidden: int,
+                 vocab: int, src_vocab: int, trg_vocab: int, key: int | None = None, readout: int | None = None,
+                 device=None, lr: float = 1e-3, clip_norm: float = 5.0, label_smoothing: float = 0.1):
+        from .decoder import NAMES, AttnDecoder, param_shapes
+        self.L, self.B, self.Ts, self.T, self.E, self.H = enc_layers, batch, src_time, trg_time, emb, hidden
+        self.K, self.Rd = key or hidden, readout or hidden
+        self.V, self.Vs, self.Vt = vocab, src_vocab, trg_vocab
+        self.device = torch.device(device or "cuda")
+        H, Ed = hidden, 2 * hidden
+        n_enc = BLSTMEncoder.numel(enc_layers, emb, H)
+        dshapes = param_shapes(emb, Ed, H, self.K, self.Rd, trg_vocab)
+        # every parameter starts on a 128 B boundary (the kernels' vector accesses and the
+        # GEMM epilogues' 16 B stores); the padding holds zeros and zero gradients
+        al = lambda n: (n + 31) // 32 * 32
+        layout, off = [], al(n_enc)
+        for field, ref_name in NAMES:
+            layout.append((field, ref_name, off, dshapes[field]))
+            off = al(off + _numel(dshapes[field]))
+        dec_end = off
+        out_w, out_b = off, al(off + self.Rd * vocab)
+        off = al(out_b + vocab)
+        out_end = off
+        src_off = off
+        total = al(src_off + src_vocab * emb)
+        self.params = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self.grads = torch.zeros_like(self.params)
+        self.enc = BLSTMEncoder(enc_layers, batch, src_time, emb, H, "bf16", self.device,
+                                params=self.params[:n_enc], grads=self.grads[:n_enc], x0_bf16=True, top_bf16=True)
+        names = self.enc.param_slices()
+        shapes = {}
+        for l, D in enumerate(self.enc.in_dims):
+            for d in ("fw", "bw"):
+                shapes.update({f"enc{l}_{d}/W": (D, 4 * H), f"enc{l}_{d}/R": (H, 4 * H), f"enc{l}_{d}/b": (4 * H,)})
+        self.dec_p, self.dec_g = {}, {}
+        for field, ref_name, o, shp in layout:
+            k = _numel(shp)
+            self.dec_p[field] = self.params[o:o + k].view(shp)
+            self.dec_g[field] = self.grads[o:o + k].view(shp)
+            names.append((ref_name, o, k))
+            shapes[ref_name] = shp
+        self.dec_bucket = self.grads[al(n_enc):dec_end]
+        self.out_p = [self.params[out_w:out_w + self.Rd * vocab].view(self.Rd, vocab),
+                      self.params[out_b:out_b + vocab]]
+        self.out_g = [self.grads[out_w:out_w + self.Rd * vocab].view(self.Rd, vocab),
+                      self.grads[out_b:out_b + vocab]]
+        self.out_bucket = self.grads[out_w:out_end]
+        names += [("output/output_prob/W", out_w, self.Rd * vocab), ("output/output_prob/b", out_b, vocab)]
+        shapes.update({"output/output_prob/W": (self.Rd, vocab), "output/output_prob/b": (vocab,)})
+        n_src = src_vocab * emb
+        self.src_p = self.params[src_off:src_off + n_src].view(src_vocab, emb)
+        self.src_g = self.grads[src_off:src_off + n_src].view(src_vocab, emb)
+        self.src_bucket = self.grads[src_off:src_off + n_src]
+        names.append(("src/W", src_off, n_src))
+        shapes["src/W"] = (src_vocab, emb)
+        self.src_emb = Embedding(src_vocab, emb, batch * src_time, layer="src", device=self.device)
+        self.x0 = torch.zeros(batch, src_time, lstm.bf16_pitch(emb), dtype=torch.bfloat16, device=self.device)
+        self.dec = AttnDecoder(batch, src_time, trg_time, emb, Ed, H, self.K, self.Rd, trg_vocab, self.device)
+        self.out = OutputCE(batch, trg_time, self.Rd, vocab, label_smoothing, device=self.device)
+        self.readout = torch.empty(batch, trg_time, self.Rd, dtype=torch.float32, device=self.device)
+        self.d_readout = torch.empty_like(self.readout)
+        self.d_enc = torch.empty(batch, src_time, Ed, dtype=torch.float32, device=self.device)
+        self.prev_ids = torch.full((batch, trg_time), -1, dtype=torch.int32, device=self.device)
+        self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
+        self.manifest = [(n, o, shapes[n]) for n, o, _ in names]
+
+    def save(self, directory: str, **state):
+        from . import checkpoint
+        checkpoint.save(directory, self.params, self.manifest, optimizer=self.opt, **state)
+
+    def load(self, directory: str):
+        from . import checkpoint
+        return checkpoint.load(directory, self.params, self.manifest, optimizer=self.opt)
+
+    def init_uniform(self, seed: int = 0):
+        """Every parameter ~ U(+-1/sqrt(H)); the alignment padding stays zero."""
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        s = 1.0 / self.H ** 0.5
+        self.params.uniform_(-s, s, generator=g)
+        keep = torch.zeros_like(self.params, dtype=torch.bool)
+        for _, o, k in self.opt.names:
+            keep[o:o + k] = True
+        self.params.masked_fill_(~keep, 0.0)
+
+    def forward(self, src_ids, src_lens, targets):
+        """src_ids [B, Ts], targets [B, T] int32 -> readout [B, T, Rd] (fp32)."""
+        self.src_ids = src_ids
+        self.src_emb.forward(src_ids, self.src_p, out=self.x0, bf16_pitch=self.x0.shape[-1])
+        self.enc_out = self.enc.forward(self.x0, src_lens)
+        self.prev_ids[:, 1:].copy_(targets[:, :-1])  # prev:trg, the zero initial output at t = 0
+        self.src_lens = src_lens
+        return self.dec.forward(self.enc_out, src_lens, self.prev_ids, self.dec_p, readout=self.readout)
+
+    def step(self, src_ids, src_lens, targets, trg_lens=None, reducer=None, grad_scale: float = 1.0):
+        """One training step; returns the device loss (mean label-smoothed CE
+        over the valid target positions, trg_lens defaulting to src_lens)."""
+        trg_lens = src_lens if trg_lens is None else trg_lens
+        self.forward(src_ids, src_lens, targets)
+        W, b = self.out_p
+        loss, _, _, _ = self.out.forward_backward(self.readout, targets, trg_lens, W, b, dx=self.d_readout,
+                                                  dW=self.out_g[0], db=self.out_g[1])
+        if reducer is not None:
+            reducer(-2, self.out_bucket)
+        self.dec.backward(self.enc_out, src_lens, self.prev_ids, self.dec_p, self.readout, self.d_readout,
+                          self.dec_g, d_enc=self.d_enc)
+        if reducer is not None:
+            reducer(-1, self.dec_bucket)
+        dx = self.enc.backward(self.d_enc, on_layer_grads=reducer)
+        self.src_emb.backward(self.src_ids, dx, self.src_g)
+        if reducer is not None:
+            reducer(-4, self.src_bucket)
+            reducer.wait()
+        self.opt.step(self.grads, grad_scale=grad_scale)
+        return loss
+
+    def check_ids(self):
+        """Synchronise; raise the reference's IndexError for a bad source / target id."""
+        self.src_emb.check_ids()
+        self.dec.check_ids(self.prev_ids)
+        self.out.check_targets()
+
+
+def _numel(shape):
+    k = 1
+    for s in shape:
+        k *= s
+    return k

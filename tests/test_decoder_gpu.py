@@ -1,0 +1,116 @@
+"""The attention decoder (sl_attn_decoder_fwd/bwd) on the GPU against the fp64
+restatement pinned to the reference build (tests/test_decoder_oracle.py).
+bf16 tensor-core operands: the SL_PREC_BF16 tolerance (norm-wise 2e-2)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1805_05225_b200 import lstm
+from paper_1805_05225_b200.decoder import NAMES, AttnDecoder, param_shapes
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def rel(a, b):
+    a = torch.as_tensor(a).double().cpu()
+    b = torch.as_tensor(np.asarray(b)).double().reshape(a.shape)
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def make_case(seed, B, Ts, T, emb, enc, hidden, key, readout, trg_vocab):
+    rng = np.random.default_rng(seed)
+    shapes = param_shapes(emb, enc, hidden, key, readout, trg_vocab)
+    fan = {"enc_ctx_W": enc, "s_W": emb + enc + hidden, "s_R": emb + enc + hidden, "s_tr_W": hidden,
+           "e_W": key, "readout_W": hidden + emb + enc}
+    P = {}
+    for n, s in shapes.items():
+        sc = 1.0 / np.sqrt(fan[n]) if n in fan else 0.5
+        P[n] = rng.uniform(-sc, sc, s).astype(np.float32)
+    P["trg_W"] = rng.uniform(-1, 1, shapes["trg_W"]).astype(np.float32)
+    enc_x = torch.as_tensor(rng.uniform(-1, 1, (B, Ts, enc)), dtype=torch.float32).bfloat16()
+    lens = rng.integers(max(1, Ts // 2), Ts + 1, B).astype(np.int32)
+    lens[0] = Ts
+    ids = rng.integers(0, trg_vocab, (B, T)).astype(np.int32)
+    ids[:, 0] = -1
+    d_ro = rng.uniform(-1, 1, (B, T, readout)).astype(np.float32)
+    return P, enc_x, lens, ids, d_ro
+
+
+def run_gpu(dims, P, enc_x, lens, ids, d_ro, dec=None):
+    B, Ts, T, emb, enc, hidden, key, readout, V = dims
+    dec = dec or AttnDecoder(B, Ts, T, emb, enc, hidden, key, readout, V)
+    pitch = lstm.bf16_pitch(enc)
+    e = torch.zeros(B, Ts, pitch, dtype=torch.bfloat16, device="cuda")
+    e[:, :, :enc] = enc_x.cuda()
+    e[:, :, enc] = 1.0
+    params = {n: torch.as_tensor(P[n]).cuda().contiguous() for n, _ in NAMES}
+    grads = {n: torch.full_like(params[n], float("nan")) for n, _ in NAMES}
+    src_lens = torch.as_tensor(lens).cuda()
+    prev = torch.as_tensor(ids).cuda()
+    ro = dec.forward(e, src_lens, prev, params)
+    d_enc = dec.backward(e, src_lens, prev, params, ro, torch.as_tensor(d_ro).cuda(), grads)
+    torch.cuda.synchronize()
+    dec.check_ids(prev)
+    return ro, grads, d_enc
+
+
+CASES = [(4, 7, 5, 12, 16, 8, 16, 8, 11), (16, 23, 9, 20, 64, 32, 48, 24, 50),
+         (8, 60, 60, 620, 2000, 1000, 1000, 1000, 300)]
+
+
+@pytest.mark.parametrize("dims", CASES)
+def test_decoder_matches_restatement(cuda, dims):
+    P, enc_x, lens, ids, d_ro = make_case(sum(dims), *dims)
+    ro, grads, d_enc = run_gpu(dims, P, enc_x, lens, ids, d_ro)
+    # the relu derivative as the GPU saw it: bf16 operands may round a pre-activation
+    # within its error of 0 to the other side (each such flip moves a whole readout_W
+    # column), so the gradients are compared under the same mask, and the masks may
+    # differ only where the fp64 pre-activation is within that error of 0
+    mask = (ro > 0).cpu().numpy()
+    r_ro, g, r_denc = oracle.attn_decoder_np(lens, enc_x.float().numpy(), ids, P, d_readout=d_ro, relu_mask=mask)
+    pre = oracle.attn_decoder_np.pre
+    flips = mask != (pre > 0)
+    assert np.abs(pre[flips]).max(initial=0.0) < 2 * TOL * np.abs(pre).max()
+    assert rel(ro, r_ro) < TOL
+    assert rel(d_enc, r_denc) < TOL
+    for n, _ in NAMES:
+        if n == "e_b":  # sum of softmax adjoints: 0 analytically — compare on the scale of d e
+            assert abs(float(grads[n]) - float(g[n][0])) < 1e-3 * max(1.0, np.abs(g["e_W"]).max()), n
+            continue
+        assert rel(grads[n], g[n]) < TOL, (n, rel(grads[n], g[n]))
+
+
+def test_decoder_deterministic_and_masked(cuda):
+    dims = CASES[1]
+    P, enc_x, lens, ids, d_ro = make_case(7, *dims)
+    lens[1] = 5
+    dec = AttnDecoder(*dims)
+    ro1, g1, d1 = run_gpu(dims, P, enc_x, lens, ids, d_ro, dec)
+    enc2 = enc_x.clone()
+    enc2[1, 5:] = 3.0  # padded source positions must not matter
+    ro2, g2, d2 = run_gpu(dims, P, enc2, lens, ids, d_ro, dec)
+    assert torch.equal(ro1, ro2)
+    assert float(d1[1, 5:].abs().max()) == 0.0
+    for n, _ in NAMES:
+        if n in ("enc_ctx_W", "enc_ctx_b"):
+            continue
+        assert torch.equal(g1[n], g2[n]), n
+    ro3, g3, d3 = run_gpu(dims, P, enc_x, lens, ids, d_ro, dec)
+    assert torch.equal(ro1, ro3) and torch.equal(d1, d3)
+    for n, _ in NAMES:
+        assert torch.equal(g1[n], g3[n]), n
+
+
+def test_decoder_bad_id_raises(cuda):
+    dims = CASES[0]
+    P, enc_x, lens, ids, d_ro = make_case(1, *dims)
+    ids[2, 3] = dims[-1]
+    with pytest.raises(IndexError, match="output/trg"):
+        run_gpu(dims, P, enc_x, lens, ids, d_ro)
+
+
+def test_decoder_shape_errors(cuda):
+    with pytest.raises(lstm.ShapeError):
+        AttnDecoder(4, 7, 5, 12, 16, 8, 2000, 8, 11)  # key_dim > 1024
