@@ -838,6 +838,18 @@ extern "C" int sl_debug_gemm_bf16(int M, int N, int K, const void* A, int64_t ld
   });
 }
 
+extern "C" int sl_debug_gemm_bf16_split(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+                                        int64_t ldb, int b_mn, float* C, int64_t ldc, int ksplit,
+                                        sl_stream_t stream) {
+  return guarded([&] {
+    TcGemm g{M, N, K, static_cast<const __nv_bfloat16*>(A), lda, a_mn != 0,
+             static_cast<const __nv_bfloat16*>(B), ldb, b_mn != 0, C, ldc, 1.f, 0.f, nullptr};
+    g.ksplit = ksplit;
+    g.split_stride = (int64_t)M * ldc;
+    gemm_bf16_tc(g, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
 extern "C" int sl_debug_set_trace(unsigned long long* dev_buf, int cta) {
   g_rec_trace = dev_buf;
   g_rec_trace_cta = cta;

@@ -32,8 +32,11 @@
 //    after the loop from small saved per-step vectors (a_t, d att_t, de_t),
 //    recomputing tanh in registers, so the loop never read-modify-writes a
 //    [B, Ts, K] accumulator.  All reductions are fixed-order (deterministic).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
+#include <memory>
 
 #include "convert.h"
 #include "decoder.h"
@@ -59,6 +62,15 @@ __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// split cluster barrier: announce this CTA has started (its shared memory exists) early,
+// wait for the peer just before the first remote shared-memory access
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// bulk L2 prefetch of a contiguous 16 B-aligned range (multiple of 16 B): one instruction
+// puts a whole row segment in flight, so a later phase's loads hit L2
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -104,9 +116,9 @@ struct CellFwd {
   const float* xw;  // [B*T, 4H]: trg_{t-1} W_trg + b (hoisted)
   float* c_all;     // [B*T, H]
   float* gates;     // [B*T, 5H]: i f g o tanh(c)
-  bf16* xa;         // [B*T, pxa]: s_t -> row (b, t+1), column E
+  bf16* xa;         // [T*B, pxa] (time-major rows t*B + b): s_t -> row (t+1, b), column E
   int64_t pxa;
-  bf16* ro;  // [B*T, pro]: s_t -> row (b, t), column 0
+  bf16* ro;  // [T*B, pro]: s_t -> row (t, b), column 0
   int64_t pro;
 };
 
@@ -115,7 +127,7 @@ __global__ void dec_cell_fwd_kernel(CellFwd a) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= a.B * qn) return;
   const int b = idx / qn, j = (idx - b * qn) * 4;
-  const int64_t row = (int64_t)b * a.T + a.t;
+  const int64_t row = (int64_t)a.t * a.B + b;  // every per-step buffer is time-major: a step is contiguous
   const int H = a.H;
   float z[4][4];
 #pragma unroll
@@ -130,7 +142,7 @@ __global__ void dec_cell_fwd_kernel(CellFwd a) {
   }
   float cp[4] = {0.f, 0.f, 0.f, 0.f};
   if (a.t > 0) {
-    const float4 v = ldf4(a.c_all + (row - 1) * H + j);
+    const float4 v = ldf4(a.c_all + (row - a.B) * H + j);
     cp[0] = v.x, cp[1] = v.y, cp[2] = v.z, cp[3] = v.w;
   }
   float gi[4], gf[4], gg[4], go[4], c[4], tc[4], h[4];
@@ -152,7 +164,7 @@ __global__ void dec_cell_fwd_kernel(CellFwd a) {
   stf4(gs + 3 * H, go);
   stf4(gs + 4 * H, tc);
   st4(a.ro + row * a.pro + j, h);
-  if (a.t + 1 < a.T) st4(a.xa + (row + 1) * a.pxa + a.E + j, h);
+  if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + a.E + j, h);
 }
 
 struct CellBwd {
@@ -178,7 +190,7 @@ __global__ void dec_cell_bwd_kernel(CellBwd a) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= a.B * qn) return;
   const int b = idx / qn, j = (idx - b * qn) * 4;
-  const int64_t row = (int64_t)b * a.T + a.t;
+  const int64_t row = (int64_t)a.t * a.B + b;
   const int H = a.H;
   float gh[4] = {0.f, 0.f, 0.f, 0.f}, gc[4] = {0.f, 0.f, 0.f, 0.f};
   addf4(gh, ldf4(a.dro + row * a.prf + j));
@@ -191,7 +203,7 @@ __global__ void dec_cell_bwd_kernel(CellBwd a) {
               go[4] = {vo.x, vo.y, vo.z, vo.w}, tc[4] = {vt.x, vt.y, vt.z, vt.w};
   float cp[4] = {0.f, 0.f, 0.f, 0.f};
   if (a.t > 0) {
-    const float4 v = ldf4(a.c_all + (row - 1) * H + j);
+    const float4 v = ldf4(a.c_all + (row - a.B) * H + j);
     cp[0] = v.x, cp[1] = v.y, cp[2] = v.z, cp[3] = v.w;
   }
   float dzi[4], dzf[4], dzg[4], dzo[4], dcp[4];
@@ -227,82 +239,158 @@ struct AttFwd {
   float* str_all;  // [T][B][K]: s_tr (with b_s)
   float* a_all;    // [T][B][Ts]
   float* acc_all;  // [T+1][B][Ts]: acc_all[t] = accum_{t-1}
-  bf16* ro;        // att_t -> row (b, t), column oa
+  bf16* ro;        // att_t -> row (t, b), column oa
   int64_t pro;
   int oa;
-  bf16* xa;  // att_t -> row (b, t+1), column 0
+  bf16* xa;  // att_t -> row (t+1, b), column 0
   int64_t pxa;
 };
 
-__global__ void __launch_bounds__(kAttThreads) dec_attn_fwd_kernel(AttFwd a) {
+// One CTA PAIR (a 2-CTA cluster) per batch row: CTA r takes the source positions
+// s = r (mod 2) for the energies and half of the encoder columns for the context;
+// the energies meet in both CTAs' shared memory over DSMEM.  Inside a CTA four
+// groups of 128 threads split the positions and every thread owns 8 key columns
+// (their s_tr, W_fb, v in registers); loads are issued four positions at a time
+// so enough bytes are in flight to stream the row's enc_ctx / enc from L2.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttThreads) dec_attn_fwd_kernel(AttFwd a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
-  const int K = a.K, Ts = a.Ts, b = blockIdx.x, tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  float* c = sm;           // s_tr + b_fb
-  float* w = c + K;        // W_fb
-  float* vv = w + K;       // v
-  float* e = vv + K;       // energies, then a
-  float* acc = e + Ts;     // accum_{t-1}
+  const int Ts = a.Ts, K = a.K, tid = threadIdx.x, lane = tid % 32;
+  const int r = (int)cl.block_rank(), b = blockIdx.x / 2;
+  float* red = sm;            // [Ts][4] per-warp partial energies
+  float* es = red + 4 * Ts;   // [Ts] energies, then a
+  float* acc = es + Ts;       // [Ts] accum_{t-1}
+  float* ctx = sm + (6 * Ts + 3) / 4 * 4;  // [256][4] context partials of the second position group (16 B aligned)
+  cluster_arrive_relaxed();
   const int len = min(max(a.lens[b], 0), Ts);
   const size_t tb = (size_t)a.t * a.B + b;
-  for (int k = tid; k < K; k += kAttThreads) {
-    float st = a.b_s[k];
-    for (int z = 0; z < a.nsplit; ++z) st += a.P[z * a.p_stride + (int64_t)b * a.p_ld + k];
-    a.str_all[tb * K + k] = st;
-    c[k] = st + a.b_fb[k];
-    w[k] = a.W_fb[k];
-    vv[k] = a.v[k];
+  if (tid < 64) {  // this CTA's enc_ctx rows (energies) and enc column half (context) into L2 now
+    for (int s = r + 2 * tid; s < len; s += 128)
+      prefetch_l2(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk, (uint32_t)K * 2);
+  } else if (tid < 128) {
+    for (int s = tid - 64; s < len; s += 64)
+      prefetch_l2(a.enc + ((int64_t)b * Ts + s) * a.ld_enc + r * (a.E / 2), (uint32_t)a.E);
   }
   for (int s = tid; s < Ts; s += kAttThreads) acc[s] = a.acc_all[tb * Ts + s];
-  __syncthreads();
-  const float bv = *a.b_v;
-  for (int s = warp; s < len; s += kAttWarps) {  // e_s = <v, tanh(e_in_s)> + b_v
-    const bf16* x = a.enc_ctx + ((int64_t)b * Ts + s) * a.pk;
-    const float as = acc[s];
-    float sum = 0.f;
-    for (int k0 = lane * 8; k0 < K; k0 += 256) {
-      float f[8];
-      ld8(x + k0, f);
+  const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
+  const bool act = k0 < K;
+  float cv[8], wv[8], vk[8];
+  if (act) {
+    float st[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sum += vv[k0 + i] * tanh_approx(f[i] + as * w[k0 + i] + c[k0 + i]);
+    for (int i = 0; i < 8; ++i) st[i] = a.b_s[k0 + i];
+    for (int z = 0; z < a.nsplit; ++z) {
+      const float* pz = a.P + z * a.p_stride + (int64_t)b * a.p_ld + k0;
+      const float4 u0 = ldf4(pz), u1 = ldf4(pz + 4);
+      st[0] += u0.x, st[1] += u0.y, st[2] += u0.z, st[3] += u0.w;
+      st[4] += u1.x, st[5] += u1.y, st[6] += u1.z, st[7] += u1.w;
     }
-    sum = warp_sum(sum);
-    if (lane == 0) e[s] = sum + bv;
+    if (r == 0 && g == 0) {
+      const float s0[4] = {st[0], st[1], st[2], st[3]}, s1[4] = {st[4], st[5], st[6], st[7]};
+      stf4(a.str_all + tb * K + k0, s0);
+      stf4(a.str_all + tb * K + k0 + 4, s1);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cv[i] = st[i] + a.b_fb[k0 + i];
+      wv[i] = a.W_fb[k0 + i];
+      vk[i] = a.v[k0 + i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cv[i] = wv[i] = vk[i] = 0.f;
   }
   __syncthreads();
-  if (warp == 0) {  // masked softmax over the valid positions (tape.cpp:952-960)
+  // energies of this CTA's positions s = r + 2 (g + 4 m), four per batch
+  for (int s0 = r + 2 * g; s0 < len; s0 += 32) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int s = s0 + 8 * u;
+      x[u] = (act && s < len) ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0)
+                              : make_uint4(0, 0, 0, 0);
+    }
+    float p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int s = s0 + 8 * u;
+      float f[8];
+      unpack8(x[u], f);
+      const float as = s < len ? acc[s] : 0.f;
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += vk[i] * tanh_approx(f[i] + as * wv[i] + cv[i]);
+      p[u] = warp_sum(act ? sum : 0.f);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (s0 + 8 * u < len) red[(s0 + 8 * u) * 4 + wig] = p[u];
+    }
+  }
+  __syncthreads();
+  cluster_wait();
+  float* peer_es = cl.map_shared_rank(es, r ^ 1);
+  const float bv = *a.b_v;
+  for (int s = r + 2 * tid; s < len; s += 2 * kAttThreads) {
+    const float e = ((red[s * 4] + red[s * 4 + 1]) + red[s * 4 + 2]) + red[s * 4 + 3] + bv;
+    es[s] = e;
+    peer_es[s] = e;
+  }
+  cl.sync();
+  if (tid < 32) {  // masked softmax over the valid positions (tape.cpp:952-960), in both CTAs
     float m = -INFINITY;
-    for (int s = lane; s < len; s += 32) m = fmaxf(m, e[s]);
+    for (int s = lane; s < len; s += 32) m = fmaxf(m, es[s]);
     m = warp_max(m);
     float sum = 0.f;
     for (int s = lane; s < len; s += 32) {
-      const float ex = expf(e[s] - m);
-      e[s] = ex;
+      const float ex = expf(es[s] - m);
+      es[s] = ex;
       sum += ex;
     }
     sum = warp_sum(sum);
     const float inv = len > 0 ? 1.f / sum : 0.f;
     __syncwarp();
     for (int s = lane; s < Ts; s += 32) {
-      const float av = s < len ? e[s] * inv : 0.f;
-      e[s] = av;
-      a.a_all[tb * Ts + s] = av;
-      a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = acc[s] + av;
+      const float av = s < len ? es[s] * inv : 0.f;
+      es[s] = av;
+      if (r == 0) {
+        a.a_all[tb * Ts + s] = av;
+        a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = acc[s] + av;
+      }
     }
   }
   __syncthreads();
-  for (int e0 = tid * 4; e0 < a.E; e0 += kAttThreads * 4) {  // att = sum_s a_s enc_s (tape.cpp:1005-1014)
+  {  // att = sum_s a_s enc_s (tape.cpp:1005-1014): this CTA's half of the columns, two position groups
+    const int gc = tid / 256, qc = tid % 256, Eh = a.E / 2, e0 = r * Eh + qc * 4;
+    const bool on = qc * 4 < Eh;
     float o[4] = {0.f, 0.f, 0.f, 0.f};
     const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + e0;
-    for (int s = 0; s < len; ++s) {
-      float f[4];
-      ld4(x + (int64_t)s * a.ld_enc, f);
-      const float as = e[s];
+    for (int s0 = gc; s0 < len; s0 += 8) {
+      float f[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] += as * f[i];
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + 2 * u;
+        if (on && s < len) ld4(x + (int64_t)s * a.ld_enc, f[u]);
+        else f[u][0] = f[u][1] = f[u][2] = f[u][3] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float as = s0 + 2 * u < len ? es[s0 + 2 * u] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] += as * f[u][i];
+      }
     }
-    const int64_t row = (int64_t)b * a.T + a.t;
-    st4(a.ro + row * a.pro + a.oa + e0, o);
-    if (a.t + 1 < a.T) st4(a.xa + (row + 1) * a.pxa + e0, o);
+    if (gc == 1 && on) stf4(ctx + qc * 4, o);
+    __syncthreads();
+    if (gc == 0 && on) {
+      const float4 o2 = ldf4(ctx + qc * 4);
+      o[0] += o2.x, o[1] += o2.y, o[2] += o2.z, o[3] += o2.w;
+      const int64_t row = (int64_t)a.t * a.B + b;
+      st4(a.ro + row * a.pro + a.oa + e0, o);
+      if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + e0, o);
+    }
   }
 }
 
@@ -324,7 +412,7 @@ struct AttBwd {
   float* dacc_out;       // d accum_{t-1}
   float* datt_all;       // [T][B][E]
   float* de_all;         // [T][B][Ts]
-  bf16* ds;              // d s_tr -> row (b, t) of [B*T, pds]
+  bf16* ds;              // d s_tr -> row (t, b) of [T*B, pds]
   int64_t pds;
   float* ds32;  // [B*T, K]
 };
@@ -332,92 +420,160 @@ struct AttBwd {
 // Adjoint of one attention step, restricted to what the recurrence needs:
 // d_a = enc d_att + d accum_t (tape.cpp:1031-1041), de = a (d_a - <a, d_a>)
 // (tape.cpp:966-978), d e_in = de v (1 - u^2) -> d s_tr = sum_s d e_in and
-// d accum_{t-1} = d accum_t + d e_in W_fb.
-__global__ void __launch_bounds__(kAttThreads) dec_attn_bwd_kernel(AttBwd a) {
+// d accum_{t-1} = d accum_t + d e_in W_fb.  One CTA pair per batch row (CTA r:
+// positions s = r mod 2); d_a meets over DSMEM, the pair's d s_tr halves are
+// summed in a fixed order by CTA 0.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttThreads) dec_attn_bwd_kernel(AttBwd a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
   extern __shared__ float sm[];
-  const int K = a.K, Ts = a.Ts, E = a.E, b = blockIdx.x, tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  float* datt = sm;            // [E]
-  float* c = datt + E;         // [K] s_tr + b_fb
-  float* w = c + K;            // [K]
-  float* vv = w + K;           // [K]
-  float* dsum = vv + K;        // [4][K]
-  float* av = dsum + 4 * K;    // [Ts]
-  float* acc = av + Ts;        // [Ts]
-  float* dacc = acc + Ts;      // [Ts] d accum_t
-  float* da = dacc + Ts;       // [Ts]
-  float* de = da + Ts;         // [Ts]
-  float* red = de + Ts;        // [Ts][4]
+  const int K = a.K, Ts = a.Ts, E = a.E, tid = threadIdx.x, lane = tid % 32;
+  const int r = (int)cl.block_rank(), b = blockIdx.x / 2;
+  float* dsum = sm;             // [4][K]
+  float* pdst = dsum + 4 * K;   // [K] this CTA's d s_tr
+  float* av = pdst + K;         // [Ts]
+  float* acc = av + Ts;         // [Ts]
+  float* dacc = acc + Ts;       // [Ts] d accum_t
+  float* da = dacc + Ts;        // [Ts]
+  float* de = da + Ts;          // [Ts]
+  float* red = de + Ts;         // [Ts][8]
+  cluster_arrive_relaxed();
   const int len = min(max(a.lens[b], 0), Ts);
   const size_t tb = (size_t)a.t * a.B + b;
-  const int64_t row = (int64_t)b * a.T + a.t;
-  for (int e0 = tid; e0 < E; e0 += kAttThreads) {
-    float d = a.dro[row * a.prf + a.oa + e0];
-    for (int z = 0; z < a.n1; ++z) d += a.P1[z * a.p1_stride + (int64_t)b * a.p1_ld + e0];
-    datt[e0] = d;
-    a.datt_all[tb * E + e0] = d;
-  }
-  for (int k = tid; k < K; k += kAttThreads) {
-    c[k] = a.str_all[tb * K + k] + a.b_fb[k];
-    w[k] = a.W_fb[k];
-    vv[k] = a.v[k];
+  const int64_t row = (int64_t)a.t * a.B + b;
+  if (tid < 64) {  // this CTA's enc rows (d_a) and enc_ctx rows (tanh adjoint) into L2 now
+    for (int s = r + 2 * tid; s < len; s += 128)
+      prefetch_l2(a.enc + ((int64_t)b * Ts + s) * a.ld_enc, (uint32_t)E * 2);
+  } else if (tid < 128) {
+    for (int s = r + 2 * (tid - 64); s < len; s += 128)
+      prefetch_l2(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk, (uint32_t)K * 2);
   }
   for (int s = tid; s < Ts; s += kAttThreads) {
     av[s] = a.a_all[tb * Ts + s];
     acc[s] = a.acc_all[tb * Ts + s];
     dacc[s] = (a.dacc_in && s < len) ? a.dacc_in[(int64_t)b * Ts + s] : 0.f;
   }
-  __syncthreads();
-  for (int s = warp; s < len; s += kAttWarps) {
-    const bf16* x = a.enc + ((int64_t)b * Ts + s) * a.ld_enc;
-    float sum = 0.f;
-    for (int e0 = lane * 8; e0 < E; e0 += 256) {
-      float f[8];
-      ld8(x + e0, f);
+  {  // d_a of this CTA's positions: two groups of 256 threads, 8 encoder columns each
+    const int gc = tid / 256, qc = tid % 256, wig = qc / 32, e0 = qc * 8;
+    const bool on = e0 < E;
+    float dv[8];
+    if (on) {
+      const float* pd = a.dro + row * a.prf + a.oa + e0;
+      const float4 u0 = ldf4(pd), u1 = ldf4(pd + 4);
+      dv[0] = u0.x, dv[1] = u0.y, dv[2] = u0.z, dv[3] = u0.w, dv[4] = u1.x, dv[5] = u1.y, dv[6] = u1.z, dv[7] = u1.w;
+      for (int z = 0; z < a.n1; ++z) {
+        const float* pz = a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + e0;
+        const float4 w0 = ldf4(pz), w1 = ldf4(pz + 4);
+        dv[0] += w0.x, dv[1] += w0.y, dv[2] += w0.z, dv[3] += w0.w;
+        dv[4] += w1.x, dv[5] += w1.y, dv[6] += w1.z, dv[7] += w1.w;
+      }
+      if (r == 0 && gc == 0) {
+        const float d0[4] = {dv[0], dv[1], dv[2], dv[3]}, d1[4] = {dv[4], dv[5], dv[6], dv[7]};
+        stf4(a.datt_all + tb * E + e0, d0);
+        stf4(a.datt_all + tb * E + e0 + 4, d1);
+      }
+    } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sum += datt[e0 + i] * f[i];
+      for (int i = 0; i < 8; ++i) dv[i] = 0.f;
     }
-    sum = warp_sum(sum);
-    if (lane == 0) da[s] = sum + dacc[s];
+    for (int s0 = r + 2 * gc; s0 < len; s0 += 16) {  // positions s0, s0+4, s0+8, s0+12
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + 4 * u;
+        x[u] = (on && s < len) ? *reinterpret_cast<const uint4*>(a.enc + ((int64_t)b * Ts + s) * a.ld_enc + e0)
+                               : make_uint4(0, 0, 0, 0);
+      }
+      float p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float f[8];
+        unpack8(x[u], f);
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sum += dv[i] * f[i];
+        p[u] = warp_sum(sum);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + 4 * u < len) red[(s0 + 4 * u) * 8 + wig] = p[u];
+      }
+    }
   }
   __syncthreads();
-  if (warp == 0) {
+  cluster_wait();
+  float* peer_da = cl.map_shared_rank(da, r ^ 1);
+  for (int s = r + 2 * tid; s < len; s += 2 * kAttThreads) {
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sum += red[s * 8 + w];
+    sum += dacc[s];
+    da[s] = sum;
+    peer_da[s] = sum;
+  }
+  cl.sync();
+  if (tid < 32) {  // softmax adjoint, in both CTAs
     float dot = 0.f;
     for (int s = lane; s < len; s += 32) dot += av[s] * da[s];
     dot = warp_sum(dot);
     for (int s = lane; s < Ts; s += 32) {
       const float d = s < len ? av[s] * (da[s] - dot) : 0.f;
       de[s] = d;
-      a.de_all[tb * Ts + s] = d;
+      if (r == 0) a.de_all[tb * Ts + s] = d;
     }
   }
   __syncthreads();
-  {  // four groups of 128 threads split the positions; a thread owns 8 key columns
-    const int g = tid / 128, q = tid % 128, wig = (tid % 128) / 32, k0 = q * 8;
+  {  // tanh adjoint over this CTA's positions: four groups of 128 threads, 8 key columns each
+    const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
     const bool act = k0 < K;
     float wv[8], cv[8], vk[8], ds[8];
+    if (act) {
+      const float* st = a.str_all + tb * K + k0;
+      const float4 s0v = ldf4(st), s1v = ldf4(st + 4);
+      const float sv[8] = {s0v.x, s0v.y, s0v.z, s0v.w, s1v.x, s1v.y, s1v.z, s1v.w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      wv[i] = act ? w[k0 + i] : 0.f;
-      cv[i] = act ? c[k0 + i] : 0.f;
-      vk[i] = act ? vv[k0 + i] : 0.f;
-      ds[i] = 0.f;
+      for (int i = 0; i < 8; ++i) {
+        wv[i] = a.W_fb[k0 + i];
+        cv[i] = sv[i] + a.b_fb[k0 + i];
+        vk[i] = a.v[k0 + i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = cv[i] = vk[i] = 0.f;
     }
-    for (int s = g; s < len; s += 4) {
-      float pa = 0.f;
-      if (act) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ds[i] = 0.f;
+    for (int s0 = r + 2 * g; s0 < len; s0 += 32) {  // positions s0 + 8u
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + 8 * u;
+        x[u] = (act && s < len) ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0)
+                                : make_uint4(0, 0, 0, 0);
+      }
+      float p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + 8 * u;
+        const float as = s < len ? acc[s] : 0.f, des = s < len ? de[s] : 0.f;
         float f[8];
-        ld8(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0, f);
-        const float as = acc[s], des = de[s];
+        unpack8(x[u], f);
+        float pa = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float u = tanh_approx(f[i] + as * wv[i] + cv[i]);
-          const float dein = des * vk[i] * (1.f - u * u);
+          const float uu = tanh_approx(f[i] + as * wv[i] + cv[i]);
+          const float dein = des * vk[i] * (1.f - uu * uu);
           ds[i] += dein;
           pa += wv[i] * dein;
         }
+        p[u] = warp_sum(act ? pa : 0.f);
       }
-      pa = warp_sum(pa);
-      if (lane == 0) red[s * 4 + wig] = pa;
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + 8 * u < len) red[(s0 + 8 * u) * 8 + wig] = p[u];  // (red reused: d_a is consumed)
+      }
     }
     if (act) {
 #pragma unroll
@@ -425,14 +581,20 @@ __global__ void __launch_bounds__(kAttThreads) dec_attn_bwd_kernel(AttBwd a) {
     }
   }
   __syncthreads();
-  for (int k = tid; k < K; k += kAttThreads) {
-    const float d = ((dsum[k] + dsum[K + k]) + dsum[2 * K + k]) + dsum[3 * K + k];
-    a.ds32[row * K + k] = d;
-    a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
-  }
-  for (int s = tid; s < Ts; s += kAttThreads)
+  for (int k = tid; k < K; k += kAttThreads) pdst[k] = ((dsum[k] + dsum[K + k]) + dsum[2 * K + k]) + dsum[3 * K + k];
+  for (int s = r + 2 * tid; s < Ts; s += 2 * kAttThreads)
     a.dacc_out[(int64_t)b * Ts + s] =
-        s < len ? dacc[s] + (((red[s * 4] + red[s * 4 + 1]) + red[s * 4 + 2]) + red[s * 4 + 3]) : 0.f;
+        s < len ? dacc[s] + (((red[s * 8] + red[s * 8 + 1]) + red[s * 8 + 2]) + red[s * 8 + 3]) : 0.f;
+  cl.sync();
+  if (r == 0) {
+    const float* peer = cl.map_shared_rank(pdst, 1);
+    for (int k = tid; k < K; k += kAttThreads) {
+      const float d = pdst[k] + peer[k];
+      a.ds32[row * K + k] = d;
+      a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
+    }
+  }
+  cl.sync();  // CTA 1's shared memory stays alive until CTA 0 has read it
 }
 
 // ---- after the loop: the accumulations over t ----------------------------------------------
@@ -535,33 +697,45 @@ __global__ void __launch_bounds__(128) dec_ctx_grad_kernel(CtxGrad a) {
   }
 }
 
-// d enc[b, s, e] = sum_t a_t[b, s] d att_t[b, e]  (the generic_attention adjoint
-// w.r.t. its base, tape.cpp:1047-1058, summed over the steps in t order)
-constexpr int kEncCols = 256, kEncPos = 32;
-__global__ void __launch_bounds__(kEncCols) dec_enc_grad_kernel(int B, int Ts, int T, int E, const float* a_all,
-                                                               const float* datt_all, float* d_enc, int64_t ld) {
-  extern __shared__ float sa[];  // [T][Ts]
-  const int b = blockIdx.y, e = blockIdx.x * kEncCols + threadIdx.x;
-  for (int i = threadIdx.x; i < T * Ts; i += kEncCols) {
-    const int t = i / Ts, s = i % Ts;
-    sa[i] = a_all[((size_t)t * B + b) * Ts + s];
+// d enc[b, s, e] += sum_t a_t[b, s] d att_t[b, e]  (the generic_attention adjoint
+// w.r.t. its base, tape.cpp:1047-1058, summed over the steps in t order).  A CTA
+// covers (b, 16 positions, 512 columns): every thread keeps a 16 x 4 register tile,
+// per step one float4 of d att and four float4 broadcasts of a from shared memory.
+constexpr int kEncCols = 512, kEncPos = 16;
+__global__ void __launch_bounds__(128) dec_enc_grad_kernel(int B, int Ts, int T, int E, const float* a_all,
+                                                          const float* datt_all, float* d_enc, int64_t ld) {
+  extern __shared__ float sa[];  // [T][kEncPos]
+  const int b = blockIdx.z, s0 = blockIdx.y * kEncPos, e = blockIdx.x * kEncCols + threadIdx.x * 4;
+  for (int i = threadIdx.x; i < T * kEncPos; i += 128) {
+    const int t = i / kEncPos, s = s0 + i % kEncPos;
+    sa[i] = s < Ts ? a_all[((size_t)t * B + b) * Ts + s] : 0.f;
   }
   __syncthreads();
   if (e >= E) return;
-  for (int s0 = 0; s0 < Ts; s0 += kEncPos) {
-    float o[kEncPos];
+  float o[kEncPos][4];
 #pragma unroll
-    for (int s = 0; s < kEncPos; ++s) o[s] = 0.f;
-    for (int t = 0; t < T; ++t) {
-      const float d = datt_all[((size_t)t * B + b) * E + e];
-      const float* at = sa + t * Ts + s0;
+  for (int s = 0; s < kEncPos; ++s) o[s][0] = o[s][1] = o[s][2] = o[s][3] = 0.f;
+  for (int t = 0; t < T; ++t) {
+    const float4 d = ldf4(datt_all + ((size_t)t * B + b) * E + e);
+    const float4* at = reinterpret_cast<const float4*>(sa + t * kEncPos);
 #pragma unroll
-      for (int s = 0; s < kEncPos; ++s)
-        if (s0 + s < Ts) o[s] += at[s] * d;
+    for (int q = 0; q < kEncPos / 4; ++q) {
+      const float4 a4 = at[q];
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        o[4 * q + u][0] += av[u] * d.x, o[4 * q + u][1] += av[u] * d.y;
+        o[4 * q + u][2] += av[u] * d.z, o[4 * q + u][3] += av[u] * d.w;
+      }
     }
+  }
 #pragma unroll
-    for (int s = 0; s < kEncPos; ++s)
-      if (s0 + s < Ts) d_enc[((int64_t)b * Ts + s0 + s) * ld + e] = o[s];
+  for (int s = 0; s < kEncPos; ++s) {
+    if (s0 + s >= Ts) break;
+    float* p = d_enc + ((int64_t)b * Ts + s0 + s) * ld + e;
+    float4 v = ldf4(p);
+    v.x += o[s][0], v.y += o[s][1], v.z += o[s][2], v.w += o[s][3];
+    *reinterpret_cast<float4*>(p) = v;
   }
 }
 
@@ -583,24 +757,46 @@ __global__ void colsum2_kernel(const float* part, int chunks, int cols, float* o
   out[c] = s;
 }
 
-__global__ void relu_kernel(float* y, int64_t n4) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 v = reinterpret_cast<float4*>(y)[i];
+// readout [b, t] = relu(pre [t*B + b]): the time-major GEMM rows to the caller's [B, T] layout
+__global__ void relu_kernel(const float* pre, float* y, int B, int T, int cols) {
+  const int q = cols / 4;
+  const int64_t n = (int64_t)B * T * q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / q;  // output row b*T + t
+    const int c = (int)(i - r * q) * 4, b = (int)(r / T), t = (int)(r - (int64_t)b * T);
+    float4 v = ldf4(pre + ((int64_t)t * B + b) * cols + c);
     v.x = fmaxf(v.x, 0.f), v.y = fmaxf(v.y, 0.f), v.z = fmaxf(v.z, 0.f), v.w = fmaxf(v.w, 0.f);
-    reinterpret_cast<float4*>(y)[i] = v;
+    *reinterpret_cast<float4*>(y + r * cols + c) = v;
   }
 }
-// d (readout pre-activation) = d readout * [readout > 0], as the bf16 GEMM operand
-__global__ void relu_grad_kernel(const float* y, const float* dy, int64_t rows, int cols, bf16* out, int64_t ld) {
+// d (readout pre-activation) = d readout * [readout > 0] ([B, T] in), as the time-major bf16 GEMM operand
+__global__ void relu_grad_kernel(const float* y, const float* dy, int B, int T, int cols, bf16* out, int64_t ld) {
   const int q = cols / 4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * q;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / q;
-    const int c = (int)(i - r * q) * 4;
-    const float4 v = ldf4(y + r * cols + c), d = ldf4(dy + r * cols + c);
+  const int64_t n = (int64_t)B * T * q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / q;  // time-major row t*B + b
+    const int c = (int)(i - r * q) * 4, t = (int)(r / B), b = (int)(r - (int64_t)t * B);
+    const int64_t src = ((int64_t)b * T + t) * cols + c;
+    const float4 v = ldf4(y + src), d = ldf4(dy + src);
     const float o[4] = {v.x > 0.f ? d.x : 0.f, v.y > 0.f ? d.y : 0.f, v.z > 0.f ? d.z : 0.f, v.w > 0.f ? d.w : 0.f};
     st4(out + r * ld + c, o);
   }
+}
+// the readout input's ones column (the [trg | 1] operand of d W_trg / d b) and the zero
+// padding after it (read by the readout GEMM's K loop)
+__global__ void ro_ones_kernel(bf16* ro, int64_t rows, int64_t pitch, int col, int n) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  bf16* p = ro + r * pitch + col;
+  p[0] = __float2bfloat16_rn(1.f);
+  for (int i = 1; i < n; ++i) p[i] = __float2bfloat16_rn(0.f);
+}
+// prev_ids [B, T] -> time-major [T, B]
+__global__ void ids_to_time_major_kernel(const int32_t* ids, int B, int T, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * T) return;
+  const int t = i / B, b = i - t * B;
+  out[i] = ids[(int64_t)b * T + t];
 }
 
 // ---- host side -----------------------------------------------------------------------------
@@ -624,11 +820,13 @@ int ksplit_for(int M, int N, int K) {
 }
 
 struct Lay {
-  int PZ, PXA, OA, PRO, PK, PR, PRF;
+  int PZ, PXA, OA, PRO, PK, PR, PRF, PDR;  // PDR: pitch of the [DZ | d readout] rows
   int ks_f, ks_s, ks_1, ks_2;
   int ctx_blocks;
-  bf16 *wd2, *wtrg, *wstr, *wctx, *wro;
+  bf16 *wd2, *wtrg, *wstr, *wctx, *wro, *wtrgcat;
   bf16 *enc_ctx, *xa, *ro, *dz, *ds, *drob, *dctx;
+  int32_t* ids_tm;
+  float *pre, *dtrg;
   float *xw, *pf, *pstr, *p1, *p2, *c_all, *gates, *str_all, *a_all, *acc_all, *de_all, *datt_all, *ds32, *dro,
       *dc, *dacc, *part, *colws, *tmp;
   void* emb_ws;
@@ -645,6 +843,7 @@ Lay layout(const DecDims& d, void* base) {
   L.PK = (int)round_up(d.K, 64);
   L.PR = (int)round_up(d.Rd, 64);
   L.PRF = L.PRO;
+  L.PDR = L.PZ + L.PR;
   L.ks_f = ksplit_for(d.B, 4 * d.H, d.E + d.H);
   L.ks_s = ksplit_for(d.B, d.K, d.H);
   L.ks_1 = ksplit_for(d.B, d.E + d.H, 4 * d.H);
@@ -666,13 +865,17 @@ Lay layout(const DecDims& d, void* base) {
   L.wstr = tb((int64_t)d.H * L.PK);
   L.wctx = tb((int64_t)d.E * L.PK);
   L.wro = tb((int64_t)(L.OA + d.E) * L.PR);
+  L.wtrgcat = tb((int64_t)d.Emb * L.PDR);
   L.enc_ctx = tb(BTs * L.PK);
   L.xa = tb(BT * L.PXA);
   L.ro = tb(BT * L.PRO);
-  L.dz = tb(BT * L.PZ);
+  L.dz = tb(BT * L.PDR);  // [DZ (4H, pad to PZ) | d readout pre-activation (Rd, pad to PR)] per row
   L.ds = tb(BT * L.PK);
-  L.drob = tb(BT * L.PR);
+  L.drob = L.dz + L.PZ;
   L.dctx = tb(BTs * L.PK);
+  L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
+  L.pre = tf(BT * d.Rd);
+  L.dtrg = tf(BT * d.Emb);
   L.xw = tf(BT * 4 * d.H);
   L.pf = tf((int64_t)L.ks_f * d.B * 4 * d.H);
   L.pstr = tf((int64_t)L.ks_s * d.B * L.PK);
@@ -717,8 +920,8 @@ void gemm_split(TcGemm g, int ks, cudaStream_t st) {
   gemm_bf16_tc(g, st);
 }
 
-size_t att_fwd_smem(const DecDims& d) { return (size_t)(3 * d.K + 2 * d.Ts) * 4; }
-size_t att_bwd_smem(const DecDims& d) { return (size_t)(d.E + 7 * d.K + 9 * d.Ts) * 4; }
+size_t att_fwd_smem(const DecDims& d) { return (size_t)(6 * d.Ts + 4 + 1024) * 4; }
+size_t att_bwd_smem(const DecDims& d) { return (size_t)(5 * d.K + 13 * d.Ts) * 4; }
 
 void configure() {  // opt in to > 48 KB dynamic shared memory once
   static bool done = false;
@@ -741,9 +944,9 @@ void decoder_check(const DecDims& d) {
              SL_ERR_SHAPE, "attn_decoder: dimensions must be positive, batch <= 256 per call");
   SL_REQUIRE(d.H % 8 == 0 && d.E % 8 == 0 && d.K % 8 == 0 && d.Rd % 8 == 0, SL_ERR_UNSUPPORTED,
              "attn_decoder: hidden, enc, key and readout dims must be multiples of 8");
-  SL_REQUIRE(d.K <= 1024 && d.E <= 8192 && d.Ts <= 1024 && d.T <= 1024 && (int64_t)d.T * d.Ts <= 48 * 1024,
+  SL_REQUIRE(d.K <= 1024 && d.E <= 2048 && d.Ts <= 1024 && d.T <= 1024 && (int64_t)d.T * d.Ts <= 48 * 1024,
              SL_ERR_UNSUPPORTED,
-             "attn_decoder: key_dim <= 1024, enc_dim <= 8192, src/trg time <= 1024, src*trg time <= 48K supported");
+             "attn_decoder: key_dim <= 1024, enc_dim <= 2048, src/trg time <= 1024, src*trg time <= 48K supported");
 }
 
 size_t decoder_workspace_bytes(const DecDims& d) { return layout(d, nullptr).bytes; }
@@ -759,9 +962,9 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
   const int64_t BT = (int64_t)B * T, BTs = (int64_t)B * d.Ts;
   const double flops = 2.0 * BTs * E * K + 2.0 * BT * d.Emb * 4 * H + 2.0 * BT * (E + H) * 4 * H +
                        2.0 * BT * H * K + 2.0 * BT * (L.OA + E) * d.Rd;
-  Phase ph(st, "k10_decoder_fwd", flops);
-  SL_CUDA_TRY(cudaMemsetAsync(L.xa, 0, (size_t)BT * L.PXA * 2, st));
-  SL_CUDA_TRY(cudaMemsetAsync(L.ro, 0, (size_t)BT * L.PRO * 2, st));
+  (void)flops;
+  std::unique_ptr<Phase> ph(new Phase(st, "k10_dec_fwd_hoisted", 2.0 * BTs * E * K + 2.0 * BT * d.Emb * 4 * H));
+  SL_CUDA_TRY(cudaMemsetAsync(L.xa, 0, (size_t)B * L.PXA * 2, st));  // step 0's [att ‖ s]_{-1} = 0
   SL_CUDA_TRY(cudaMemsetAsync(L.acc_all, 0, (size_t)BTs * 4, st));
   // packed bf16 weights (rows of the reference layouts; see the GEMMs for the majorness)
   f32_to_bf16(E, 4 * H, p.s_W + (int64_t)d.Emb * 4 * H, 4 * H, L.wd2, L.PZ, st);
@@ -772,9 +975,18 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
   f32_to_bf16(H + d.Emb, d.Rd, p.ro_W, d.Rd, L.wro, L.PR, st);
   SL_CUDA_TRY(cudaMemsetAsync(L.wro + (int64_t)(H + d.Emb) * L.PR, 0, (size_t)(L.OA - H - d.Emb) * L.PR * 2, st));
   f32_to_bf16(E, d.Rd, p.ro_W + (int64_t)(H + d.Emb) * d.Rd, d.Rd, L.wro + (int64_t)L.OA * L.PR, L.PR, st);
+  // [W_trg | W_ro(trg rows)] along K: d trg_{t-1} = [DZ | d ro] [W_trg | W_ro,trg]^T in one GEMM
+  SL_CUDA_TRY(cudaMemsetAsync(L.wtrgcat, 0, (size_t)d.Emb * L.PDR * 2, st));
+  f32_to_bf16(d.Emb, 4 * H, p.s_W, 4 * H, L.wtrgcat, L.PDR, st);
+  f32_to_bf16(d.Emb, d.Rd, p.ro_W + (int64_t)H * d.Rd, d.Rd, L.wtrgcat + L.PZ, L.PDR, st);
   // trg_{t-1} into the readout-input rows (columns H..H+Emb) + the ones column
-  embedding_fwd_bf16(BT, prev_ids, d.Vt, d.Emb, p.trg_W, L.ro + H, L.PRO, SL_EMB_NEGATIVE_ZERO, bad_row, st);
-  fill_col_bf16(BT, H + d.Emb, L.ro, L.PRO, 1.f, st);
+  ids_to_time_major_kernel<<<(unsigned)ceil_div(BT, 256), 256, 0, st>>>(prev_ids, B, T, L.ids_tm);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  embedding_fwd_bf16(BT, L.ids_tm, d.Vt, d.Emb, p.trg_W, L.ro + H, L.PRO, SL_EMB_NEGATIVE_ZERO, bad_row, st);
+  ro_ones_kernel<<<(unsigned)ceil_div(BT, 256), 256, 0, st>>>(L.ro, BT, L.PRO, H + d.Emb, L.OA - H - d.Emb);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
   {  // enc_ctx = enc W_ctx + b_ctx (bf16 out); x W_trg + b for all t
     TcGemm g = mk((int)BTs, K, E, enc, ld_enc, false, L.wctx, L.PK, true, nullptr, L.PK);
     g.bias = p.ctx_b;
@@ -784,28 +996,36 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
     x.bias = p.s_b;
     gemm_bf16_tc(x, st);
   }
+  ph.reset();
   const int cell_threads = B * (H / 4);
+  const double att_bytes = 2.0 * B * d.Ts * (K + E);
   for (int t = 0; t < T; ++t) {
-    if (t > 0)
-      gemm_split(mk(B, 4 * H, E + H, L.xa + (int64_t)t * L.PXA, (int64_t)T * L.PXA, false, L.wd2, L.PZ, true, L.pf,
-                    4 * H),
+    if (t > 0) {
+      Phase p1(st, "k10_cell_gemm", 2.0 * B * (E + H) * 4 * H);
+      gemm_split(mk(B, 4 * H, E + H, L.xa + (int64_t)t * B * L.PXA, L.PXA, false, L.wd2, L.PZ, true, L.pf, 4 * H),
                  L.ks_f, st);
+    }
+    ph.reset(new Phase(st, "k10_cell_fwd", 0.0, 4.0 * B * H * 16));
     CellFwd cf{B, T, H, E, t, t > 0 ? L.ks_f : 0, L.pf, 4 * H, (int64_t)B * 4 * H, L.xw, L.c_all, L.gates,
                L.xa, L.PXA, L.ro, L.PRO};
     dec_cell_fwd_kernel<<<(unsigned)ceil_div(cell_threads, 256), 256, 0, st>>>(cf);
-    gemm_split(mk(B, K, H, L.ro + (int64_t)t * L.PRO, (int64_t)T * L.PRO, false, L.wstr, L.PK, true, L.pstr, L.PK),
+    ph.reset(new Phase(st, "k10_str_gemm", 2.0 * B * H * K));
+    gemm_split(mk(B, K, H, L.ro + (int64_t)t * B * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr, L.PK),
                L.ks_s, st);
     AttFwd af{B, d.Ts, T, K, E, t, L.ks_s, src_lens, L.pstr, L.PK, (int64_t)B * L.PK, p.str_b, p.fb_W, p.fb_b,
               p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO, L.OA,
               L.xa, L.PXA};
-    dec_attn_fwd_kernel<<<B, kAttThreads, att_fwd_smem(d), st>>>(af);
+    ph.reset(new Phase(st, "k10_attn_fwd", 0.0, att_bytes));
+    dec_attn_fwd_kernel<<<2 * B, kAttThreads, att_fwd_smem(d), st>>>(af);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch(2);
+    ph.reset();
   }
-  TcGemm r = mk((int)BT, d.Rd, L.OA + E, L.ro, L.PRO, false, L.wro, L.PR, true, readout, d.Rd);
+  ph.reset(new Phase(st, "k10_dec_fwd_hoisted", 2.0 * BT * (L.OA + E) * d.Rd));
+  TcGemm r = mk((int)BT, d.Rd, L.OA + E, L.ro, L.PRO, false, L.wro, L.PR, true, L.pre, d.Rd);
   r.bias = p.ro_b;
   gemm_bf16_tc(r, st);
-  relu_kernel<<<sm_count() * 4, 256, 0, st>>>(readout, BT * d.Rd / 4);
+  relu_kernel<<<sm_count() * 4, 256, 0, st>>>(L.pre, readout, B, T, d.Rd);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -820,62 +1040,76 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   const int64_t BT = (int64_t)B * T, BTs = (int64_t)B * d.Ts;
   const double flops = 2.0 * (2.0 * BTs * E * K + 2.0 * BT * Emb * 4 * H + 2.0 * BT * (E + H) * 4 * H +
                               2.0 * BT * H * K + 2.0 * BT * (L.OA + E) * Rd);
-  Phase ph(st, "k10_decoder_bwd", flops);
+  (void)flops;
+  std::unique_ptr<Phase> ph(new Phase(st, "k10_dec_bwd_hoisted", 4.0 * BT * (L.OA + E) * Rd));
   // readout: relu adjoint, d [s ‖ trg ‖ att], d W_ro (three row blocks) and d b_ro (ones column)
-  relu_grad_kernel<<<sm_count() * 4, 256, 0, st>>>(readout, d_readout, BT, Rd, L.drob, L.PR);
+  // zero pads of the [DZ | d ro] rows (inside the K range of the d trg GEMM)
+  SL_CUDA_TRY(cudaMemset2DAsync(L.dz + 4 * H, (size_t)L.PDR * 2, 0, (size_t)(L.PZ - 4 * H) * 2, BT, st));
+  SL_CUDA_TRY(cudaMemset2DAsync(L.drob + Rd, (size_t)L.PDR * 2, 0, (size_t)(L.PR - Rd) * 2, BT, st));
+  relu_grad_kernel<<<sm_count() * 4, 256, 0, st>>>(readout, d_readout, B, T, Rd, L.drob, L.PDR);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
-  gemm_bf16_tc(mk((int)BT, L.OA + E, Rd, L.drob, L.PR, false, L.wro, L.PR, false, L.dro, L.PRF), st);
-  gemm_bf16_tc(mk(H, Rd, (int)BT, L.ro, L.PRO, true, L.drob, L.PR, true, g.ro_W, Rd), st);
+  gemm_bf16_tc(mk((int)BT, L.OA + E, Rd, L.drob, L.PDR, false, L.wro, L.PR, false, L.dro, L.PRF), st);
+  gemm_bf16_tc(mk(H, Rd, (int)BT, L.ro, L.PRO, true, L.drob, L.PDR, true, g.ro_W, Rd), st);
   {
-    TcGemm w = mk(Emb + 1, Rd, (int)BT, L.ro + H, L.PRO, true, L.drob, L.PR, true, g.ro_W + (int64_t)H * Rd, Rd);
+    TcGemm w = mk(Emb + 1, Rd, (int)BT, L.ro + H, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)H * Rd, Rd);
     w.m_split = Emb;
     w.C2 = g.ro_b;
     w.ldc2 = Rd;
     gemm_bf16_tc(w, st);
   }
-  gemm_bf16_tc(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
+  gemm_bf16_tc(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
                st);
+  ph.reset();
   const int cell_threads = B * (H / 4);
+  const double att_bytes = 2.0 * B * d.Ts * (K + E);
   for (int t = T - 1; t >= 0; --t) {
     const bool last = t == T - 1;
-    if (!last)
-      gemm_split(mk(B, E + H, 4 * H, L.dz + (int64_t)(t + 1) * L.PZ, (int64_t)T * L.PZ, false, L.wd2, L.PZ, false,
-                    L.p1, E + H),
+    if (!last) {
+      Phase p1(st, "k10_g1_gemm", 2.0 * B * (E + H) * 4 * H);
+      gemm_split(mk(B, E + H, 4 * H, L.dz + (int64_t)(t + 1) * B * L.PDR, L.PDR, false, L.wd2, L.PZ, false, L.p1,
+                    E + H),
                  L.ks_1, st);
+    }
+    ph.reset(new Phase(st, "k10_attn_bwd", 0.0, att_bytes));
     AttBwd ab{B, d.Ts, T, K, E, t, last ? 0 : L.ks_1, src_lens, L.p1, E + H, (int64_t)B * (E + H), L.dro, L.PRF,
               L.OA, p.fb_W, p.fb_b, p.e_W, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all,
               last ? nullptr : L.dacc + (int64_t)((t + 1) % 2) * B * d.Ts, L.dacc + (int64_t)(t % 2) * B * d.Ts,
               L.datt_all, L.de_all, L.ds, L.PK, L.ds32};
-    dec_attn_bwd_kernel<<<B, kAttThreads, att_bwd_smem(d), st>>>(ab);
-    gemm_split(mk(B, H, K, L.ds + (int64_t)t * L.PK, (int64_t)T * L.PK, false, L.wstr, L.PK, false, L.p2, L.PK),
+    dec_attn_bwd_kernel<<<2 * B, kAttThreads, att_bwd_smem(d), st>>>(ab);
+    ph.reset(new Phase(st, "k10_g2_gemm", 2.0 * B * H * K));
+    gemm_split(mk(B, H, K, L.ds + (int64_t)t * B * L.PK, L.PK, false, L.wstr, L.PK, false, L.p2, L.PK),
                L.ks_2, st);
     CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PK,
                (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
-               last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PZ};
+               last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR};
+    ph.reset(new Phase(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 20));
     dec_cell_bwd_kernel<<<(unsigned)ceil_div(cell_threads, 256), 256, 0, st>>>(cb);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch(2);
+    ph.reset();
   }
+  ph.reset(new Phase(st, "k10_dec_bwd_hoisted",
+                     2.0 * BT * 4 * H * (E + H + Emb + 1) + 2.0 * BT * Emb * 4 * H + 2.0 * BT * H * K));
   // the decoder cell's weight gradients over all B*T rows: [W_att; R] from [att ‖ s]_{t-1},
   // [W_trg; b] from [trg_{t-1} | 1]; d trg_{t-1} -> the trg table
-  gemm_bf16_tc(mk(E, 4 * H, (int)BT, L.xa, L.PXA, true, L.dz, L.PZ, true, g.s_W + (int64_t)Emb * 4 * H, 4 * H), st);
-  gemm_bf16_tc(mk(H, 4 * H, (int)BT, L.xa + E, L.PXA, true, L.dz, L.PZ, true, g.s_R, 4 * H), st);
+  gemm_bf16_tc(mk(E, 4 * H, (int)BT, L.xa, L.PXA, true, L.dz, L.PDR, true, g.s_W + (int64_t)Emb * 4 * H, 4 * H), st);
+  gemm_bf16_tc(mk(H, 4 * H, (int)BT, L.xa + E, L.PXA, true, L.dz, L.PDR, true, g.s_R, 4 * H), st);
   {
-    TcGemm w = mk(Emb + 1, 4 * H, (int)BT, L.ro + H, L.PRO, true, L.dz, L.PZ, true, g.s_W, 4 * H);
+    TcGemm w = mk(Emb + 1, 4 * H, (int)BT, L.ro + H, L.PRO, true, L.dz, L.PDR, true, g.s_W, 4 * H);
     w.m_split = Emb;
     w.C2 = g.s_b;
     w.ldc2 = 4 * H;
     gemm_bf16_tc(w, st);
-    TcGemm x = mk((int)BT, Emb, 4 * H, L.dz, L.PZ, false, L.wtrg, L.PZ, false, L.dro + H, L.PRF);
-    x.beta = 1.f;
-    gemm_bf16_tc(x, st);
+    // d trg_{t-1} = [DZ | d ro] [W_trg | W_ro,trg]^T (the cell input and the readout input, one GEMM)
+    gemm_bf16_tc(mk((int)BT, Emb, L.PZ + Rd, L.dz, L.PDR, false, L.wtrgcat, L.PDR, false, L.dtrg, Emb), st);
   }
-  embedding_bwd(BT, prev_ids, d.Vt, Emb, L.dro + H, L.PRF, g.trg_W, false, L.emb_ws, st);
+  embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
   // s_tr: d W_s over all rows, d b_s as a fixed-order column sum
   gemm_bf16_tc(mk(H, K, (int)BT, L.ro, L.PRO, true, L.ds, L.PK, true, g.str_W, K), st);
   colsum(L.ds32, BT, K, K, g.str_b, L.colws, st);
   // the attention's accumulations over t
+  ph.reset(new Phase(st, "k10_attn_accum", 0.0, 2.0 * BTs * K + 4.0 * T * B * (K + E)));
   {
     CtxGrad cg{B, d.Ts, T, K, src_lens, L.enc_ctx, L.PK, p.fb_W, p.fb_b, p.e_W, L.str_all, L.acc_all, L.de_all,
                L.dctx, L.part};
@@ -890,16 +1124,18 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
     colsum(L.de_all, (int64_t)T * B, d.Ts, d.Ts, L.tmp, L.colws, st);
     colsum(L.tmp, d.Ts, 1, 1, g.e_b, L.colws, st);
   }
-  dec_enc_grad_kernel<<<dim3((unsigned)ceil_div(E, kEncCols), (unsigned)B), kEncCols, (size_t)T * d.Ts * 4, st>>>(
-      B, d.Ts, T, E, L.a_all, L.datt_all, d_enc, E);
-  SL_CUDA_TRY(cudaGetLastError());
-  count_launch();
+  ph.reset(new Phase(st, "k10_dec_bwd_hoisted", 4.0 * BTs * E * K));
   {
-    TcGemm x = mk((int)BTs, E, K, L.dctx, L.PK, false, L.wctx, L.PK, false, d_enc, E);
-    x.beta = 1.f;
-    gemm_bf16_tc(x, st);
+    gemm_bf16_tc(mk((int)BTs, E, K, L.dctx, L.PK, false, L.wctx, L.PK, false, d_enc, E), st);
     gemm_bf16_tc(mk(E, K, (int)BTs, enc, ld_enc, true, L.dctx, L.PK, true, g.ctx_W, K), st);
   }
+  ph.reset(new Phase(st, "k10_attn_accum", 0.0, 4.0 * T * B * E + 8.0 * BTs * E));
+  dec_enc_grad_kernel<<<dim3((unsigned)ceil_div(E, kEncCols), (unsigned)ceil_div(d.Ts, kEncPos), (unsigned)B), 128,
+                        (size_t)T * kEncPos * 4, st>>>(
+      B, d.Ts, T, E, L.a_all, L.datt_all, d_enc, E);  // += sum_t a_t (x) d att_t
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+
 }
 
 }  // namespace sl

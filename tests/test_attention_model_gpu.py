@@ -58,17 +58,15 @@ def test_encoder_receives_decoder_gradient(cuda):
     """The encoder part of the model's gradient equals the reference BLSTM stack's
     gradient for the d enc the decoder produced (bf16 tolerance)."""
     m, src, trg, lens, tl = make(5)
-    m.step(src, lens, trg, trg_lens=tl)  # one step to populate d_enc; then recompute the grads
-    m.init_uniform(5)
-    m.opt = type(m.opt)(m.params, lr=0.0, clip_norm=0.0, names=m.opt.names)
-    m.step(src, lens, trg, trg_lens=tl)
+    m.forward(src, lens, trg)
+    W, b = m.out_p
+    m.out.forward_backward(m.readout, trg, tl, W, b, dx=m.d_readout, dW=m.out_g[0], db=m.out_g[1])
+    m.dec.backward(m.enc_out, lens, m.prev_ids, m.dec_p, m.readout, m.d_readout, m.dec_g, d_enc=m.d_enc)
+    m.enc.backward(m.d_enc)
     torch.cuda.synchronize()
     H, E = DIMS["hidden"], DIMS["emb"]
     x = m.x0[:, :, :E].float().cpu().numpy()
-    params = []
-    for l in range(DIMS["enc_layers"]):
-        v = [t.detach().cpu().numpy() for t in m.enc.p_views[l]]
-        params.append(tuple(v))
+    params = [tuple(t.detach().cpu().numpy() for t in m.enc.p_views[l]) for l in range(DIMS["enc_layers"])]
     ref = oracle.Reference(64)
     y, dx, grads = ref.blstm_stack(x, lens.cpu().numpy(), params, dy=m.d_enc.cpu().numpy())
     yg = m.enc_out[:, :, :2 * H].float().cpu().numpy()
