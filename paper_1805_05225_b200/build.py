@@ -27,7 +27,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", 
                   "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
-                  "-diag-suppress", "177,550"]
+                  "-diag-suppress", "177,550", "--diag-error", "20013,20014,20015"]
 
 
 def _headers():

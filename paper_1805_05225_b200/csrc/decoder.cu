@@ -43,6 +43,7 @@
 #include "embedding.h"
 #include "gemm.h"
 #include "profile.h"
+#include "tc.cuh"
 
 namespace sl {
 namespace {
@@ -597,6 +598,366 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttThreads) dec_att
   cl.sync();  // CTA 1's shared memory stays alive until CTA 0 has read it
 }
 
+// ---- the same two attention kernels with the row's operands staged by TMA --------------
+// C CTAs (one cluster) per batch row, 256 threads each.  CTA r owns the positions
+// s = r (mod C) and, for the context, one 16 B-aligned column slice of enc; at
+// kernel start one warp issues a 1-D bulk copy (cp.async.bulk) per row segment the
+// CTA will read — its enc_ctx rows and enc slice in the forward, its enc and
+// enc_ctx rows in the backward — completing on two mbarriers, so every byte is in
+// flight at once and the phases then read shared memory.  ~95 KB per CTA: two
+// CTAs per SM, one loading while the other computes.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+constexpr int kStThreads = 256;
+__host__ __device__ inline int st_cols(int E, int C) { return ((E + C - 1) / C + 7) / 8 * 8; }
+__host__ __device__ inline size_t st_align(size_t x) { return (x + 127) / 128 * 128; }
+// shared-memory carve-ups (bytes), shared by host (launch size) and device
+struct FwdSt {
+  size_t red, es, acc, cpart, rctx, renc, total;
+  __host__ __device__ FwdSt(int Ts, int K, int E, int C) {
+    const int nrm = (Ts + C - 1) / C, Ec = st_cols(E, C);
+    red = 16;
+    es = red + (size_t)nrm * 4 * 4;
+    acc = es + (size_t)Ts * 4;
+    cpart = (acc + (size_t)Ts * 4 + 15) / 16 * 16;  // float4 accesses
+    rctx = st_align(cpart + (size_t)Ec * 4);
+    renc = st_align(rctx + (size_t)nrm * K * 2);
+    total = renc + (size_t)Ts * Ec * 2;
+  }
+};
+struct BwdSt {
+  size_t av, acc, dacc, da, de, red, pdst, renc, rctx, total;
+  __host__ __device__ BwdSt(int Ts, int K, int E, int C) {
+    const int nrm = (Ts + C - 1) / C;
+    av = 16;
+    acc = av + (size_t)Ts * 4;
+    dacc = acc + (size_t)Ts * 4;
+    da = dacc + (size_t)Ts * 4;
+    de = da + (size_t)Ts * 4;
+    red = de + (size_t)Ts * 4;
+    pdst = red + (size_t)nrm * 8 * 4;
+    renc = st_align(pdst + (size_t)K * 4);
+    const size_t renc_bytes = (size_t)nrm * E * 2, dsum_bytes = (size_t)2 * K * 4;
+    rctx = st_align(renc + (renc_bytes > dsum_bytes ? renc_bytes : dsum_bytes));  // renc doubles as dsum [2][K]
+    total = rctx + (size_t)nrm * K * 2;
+  }
+};
+
+template <int C>
+__global__ void __launch_bounds__(kStThreads) dec_attn_fwd_tma_kernel(AttFwd a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) uint8_t smraw[];
+  const int Ts = a.Ts, K = a.K, E = a.E, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int r = (int)cl.block_rank(), b = blockIdx.x / C;
+  const FwdSt L(Ts, K, E, C);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
+  float* red = reinterpret_cast<float*>(smraw + L.red);
+  float* es = reinterpret_cast<float*>(smraw + L.es);
+  float* acc = reinterpret_cast<float*>(smraw + L.acc);
+  float* cpart = reinterpret_cast<float*>(smraw + L.cpart);
+  bf16* rctx = reinterpret_cast<bf16*>(smraw + L.rctx);
+  bf16* renc = reinterpret_cast<bf16*>(smraw + L.renc);
+  const int Ec = st_cols(E, C), c0 = r * Ec, nc = max(0, min(E - c0, Ec));
+  cluster_arrive_relaxed();
+  const int len = min(max(a.lens[b], 0), Ts);
+  const int nr = r < len ? (len - r + C - 1) / C : 0;  // this CTA's positions s = r + C j
+  const size_t tb = (size_t)a.t * a.B + b;
+  if (tid == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)(nr * K * 2));
+      tc::mbar_arrive_expect_tx(&bars[1], (uint32_t)(nc > 0 ? len * nc * 2 : 0));
+    }
+    __syncwarp();
+    for (int j = lane; j < nr; j += 32)
+      bulk_g2s(rctx + (size_t)j * K, a.enc_ctx + ((int64_t)b * Ts + r + C * j) * a.pk, (uint32_t)K * 2, &bars[0]);
+    if (nc > 0)
+      for (int s = lane; s < len; s += 32)
+        bulk_g2s(renc + (size_t)s * Ec, a.enc + ((int64_t)b * Ts + s) * a.ld_enc + c0, (uint32_t)nc * 2, &bars[1]);
+  }
+  for (int s = tid; s < Ts; s += kStThreads) acc[s] = a.acc_all[tb * Ts + s];
+  const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
+  const bool act = k0 < K;
+  float cv[8], wv[8], vk[8];
+  if (act) {
+    float st[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) st[i] = a.b_s[k0 + i];
+    for (int z = 0; z < a.nsplit; ++z) {
+      const float* pz = a.P + z * a.p_stride + (int64_t)b * a.p_ld + k0;
+      const float4 u0 = ldf4(pz), u1 = ldf4(pz + 4);
+      st[0] += u0.x, st[1] += u0.y, st[2] += u0.z, st[3] += u0.w;
+      st[4] += u1.x, st[5] += u1.y, st[6] += u1.z, st[7] += u1.w;
+    }
+    if (r == 0 && g == 0) {
+      const float s0[4] = {st[0], st[1], st[2], st[3]}, s1[4] = {st[4], st[5], st[6], st[7]};
+      stf4(a.str_all + tb * K + k0, s0);
+      stf4(a.str_all + tb * K + k0 + 4, s1);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cv[i] = st[i] + a.b_fb[k0 + i];
+      wv[i] = a.W_fb[k0 + i];
+      vk[i] = a.v[k0 + i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cv[i] = wv[i] = vk[i] = 0.f;
+  }
+  __syncthreads();
+  tc::mbar_wait(&bars[0], 0);
+  for (int j = g; j < nr; j += 2) {  // e_s = <v, tanh(e_in_s)> over this CTA's positions
+    const int s = r + C * j;
+    float f[8];
+    if (act) ld8(rctx + (size_t)j * K + k0, f);
+    const float as = acc[s];
+    float sum = 0.f;
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += vk[i] * tanh_approx(f[i] + as * wv[i] + cv[i]);
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[j * 4 + wig] = sum;
+  }
+  __syncthreads();
+  cluster_wait();
+  const float bv = *a.b_v;
+  for (int j = tid; j < nr; j += kStThreads) {
+    const int s = r + C * j;
+    const float e = ((red[j * 4] + red[j * 4 + 1]) + red[j * 4 + 2]) + red[j * 4 + 3] + bv;
+#pragma unroll
+    for (int p = 0; p < C; ++p) cl.map_shared_rank(es, p)[s] = e;
+  }
+  cl.sync();
+  if (tid < 32) {  // masked softmax over the valid positions (tape.cpp:952-960), in every CTA
+    float m = -INFINITY;
+    for (int s = lane; s < len; s += 32) m = fmaxf(m, es[s]);
+    m = warp_max(m);
+    float sum = 0.f;
+    for (int s = lane; s < len; s += 32) {
+      const float ex = expf(es[s] - m);
+      es[s] = ex;
+      sum += ex;
+    }
+    sum = warp_sum(sum);
+    const float inv = len > 0 ? 1.f / sum : 0.f;
+    __syncwarp();
+    for (int s = lane; s < Ts; s += 32) {
+      const float av = s < len ? es[s] * inv : 0.f;
+      es[s] = av;
+      if (r == 0) {
+        a.a_all[tb * Ts + s] = av;
+        a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = acc[s] + av;
+      }
+    }
+  }
+  __syncthreads();
+  {  // att (this CTA's column slice) = sum_s a_s enc_s (tape.cpp:1005-1014), two position groups
+    const int gc = tid / 128, cq = tid % 128, cc = cq * 4;
+    const bool on = cc < nc;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    if (nc > 0) tc::mbar_wait(&bars[1], 0);
+    if (on) {
+      for (int s = gc; s < len; s += 2) {
+        float f[4];
+        ld4(renc + (size_t)s * Ec + cc, f);
+        const float as = es[s];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] += as * f[i];
+      }
+    }
+    if (gc == 1 && on) stf4(cpart + cc, o);
+    __syncthreads();
+    if (gc == 0 && on) {
+      const float4 o2 = ldf4(cpart + cc);
+      o[0] += o2.x, o[1] += o2.y, o[2] += o2.z, o[3] += o2.w;
+      const int64_t row = (int64_t)a.t * a.B + b;
+      st4(a.ro + row * a.pro + a.oa + c0 + cc, o);
+      if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + c0 + cc, o);
+    }
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kStThreads) dec_attn_bwd_tma_kernel(AttBwd a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) uint8_t smraw[];
+  const int K = a.K, Ts = a.Ts, E = a.E, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int r = (int)cl.block_rank(), b = blockIdx.x / C;
+  const BwdSt L(Ts, K, E, C);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
+  float* av = reinterpret_cast<float*>(smraw + L.av);
+  float* acc = reinterpret_cast<float*>(smraw + L.acc);
+  float* dacc = reinterpret_cast<float*>(smraw + L.dacc);
+  float* da = reinterpret_cast<float*>(smraw + L.da);
+  float* de = reinterpret_cast<float*>(smraw + L.de);
+  float* red = reinterpret_cast<float*>(smraw + L.red);
+  float* pdst = reinterpret_cast<float*>(smraw + L.pdst);
+  bf16* renc = reinterpret_cast<bf16*>(smraw + L.renc);
+  float* dsum = reinterpret_cast<float*>(smraw + L.renc);  // [2][K], after the d_a phase
+  bf16* rctx = reinterpret_cast<bf16*>(smraw + L.rctx);
+  cluster_arrive_relaxed();
+  const int len = min(max(a.lens[b], 0), Ts);
+  const int nr = r < len ? (len - r + C - 1) / C : 0;
+  const size_t tb = (size_t)a.t * a.B + b;
+  const int64_t row = (int64_t)a.t * a.B + b;
+  if (tid == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)(nr * E * 2));
+      tc::mbar_arrive_expect_tx(&bars[1], (uint32_t)(nr * K * 2));
+    }
+    __syncwarp();
+    for (int j = lane; j < nr; j += 32) {
+      const int64_t src = (int64_t)b * Ts + r + C * j;
+      bulk_g2s(renc + (size_t)j * E, a.enc + src * a.ld_enc, (uint32_t)E * 2, &bars[0]);
+      bulk_g2s(rctx + (size_t)j * K, a.enc_ctx + src * a.pk, (uint32_t)K * 2, &bars[1]);
+    }
+  }
+  for (int s = tid; s < Ts; s += kStThreads) {
+    av[s] = a.a_all[tb * Ts + s];
+    acc[s] = a.acc_all[tb * Ts + s];
+    dacc[s] = (a.dacc_in && s < len) ? a.dacc_in[(int64_t)b * Ts + s] : 0.f;
+  }
+  {  // d att_t for this thread's 8 columns; d_a over this CTA's positions (all 8 warps per position)
+    const int e0 = tid * 8;
+    const bool on = e0 < E;
+    float dv[8];
+    if (on) {
+      const float* pd = a.dro + row * a.prf + a.oa + e0;
+      const float4 u0 = ldf4(pd), u1 = ldf4(pd + 4);
+      dv[0] = u0.x, dv[1] = u0.y, dv[2] = u0.z, dv[3] = u0.w, dv[4] = u1.x, dv[5] = u1.y, dv[6] = u1.z, dv[7] = u1.w;
+      for (int z = 0; z < a.n1; ++z) {
+        const float* pz = a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + e0;
+        const float4 w0 = ldf4(pz), w1 = ldf4(pz + 4);
+        dv[0] += w0.x, dv[1] += w0.y, dv[2] += w0.z, dv[3] += w0.w;
+        dv[4] += w1.x, dv[5] += w1.y, dv[6] += w1.z, dv[7] += w1.w;
+      }
+      if (r == 0) {
+        const float d0[4] = {dv[0], dv[1], dv[2], dv[3]}, d1[4] = {dv[4], dv[5], dv[6], dv[7]};
+        stf4(a.datt_all + tb * E + e0, d0);
+        stf4(a.datt_all + tb * E + e0 + 4, d1);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dv[i] = 0.f;
+    }
+    tc::mbar_wait(&bars[0], 0);
+    for (int j = 0; j < nr; ++j) {
+      float sum = 0.f;
+      if (on) {
+        float f[8];
+        ld8(renc + (size_t)j * E + e0, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sum += dv[i] * f[i];
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) red[j * 8 + warp] = sum;
+    }
+  }
+  __syncthreads();
+  cluster_wait();
+  for (int j = tid; j < nr; j += kStThreads) {
+    const int s = r + C * j;
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sum += red[j * 8 + w];
+    sum += dacc[s];
+#pragma unroll
+    for (int p = 0; p < C; ++p) cl.map_shared_rank(da, p)[s] = sum;
+  }
+  cl.sync();
+  if (tid < 32) {  // softmax adjoint, in every CTA
+    float dot = 0.f;
+    for (int s = lane; s < len; s += 32) dot += av[s] * da[s];
+    dot = warp_sum(dot);
+    for (int s = lane; s < Ts; s += 32) {
+      const float d = s < len ? av[s] * (da[s] - dot) : 0.f;
+      de[s] = d;
+      if (r == 0) a.de_all[tb * Ts + s] = d;
+    }
+  }
+  __syncthreads();
+  {  // tanh adjoint over this CTA's positions: two groups of 128 threads, 8 key columns each
+    const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
+    const bool act = k0 < K;
+    float wv[8], cv[8], vk[8], ds[8];
+    if (act) {
+      const float* st = a.str_all + tb * K + k0;
+      const float4 s0v = ldf4(st), s1v = ldf4(st + 4);
+      const float sv[8] = {s0v.x, s0v.y, s0v.z, s0v.w, s1v.x, s1v.y, s1v.z, s1v.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        wv[i] = a.W_fb[k0 + i];
+        cv[i] = sv[i] + a.b_fb[k0 + i];
+        vk[i] = a.v[k0 + i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = cv[i] = vk[i] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ds[i] = 0.f;
+    tc::mbar_wait(&bars[1], 0);
+    for (int j = g; j < nr; j += 2) {
+      const int s = r + C * j;
+      const float as = acc[s], des = de[s];
+      float pa = 0.f;
+      if (act) {
+        float f[8];
+        ld8(rctx + (size_t)j * K + k0, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float uu = tanh_approx(f[i] + as * wv[i] + cv[i]);
+          const float dein = des * vk[i] * (1.f - uu * uu);
+          ds[i] += dein;
+          pa += wv[i] * dein;
+        }
+      }
+      pa = warp_sum(pa);
+      if (lane == 0) red[j * 8 + wig] = pa;  // (red reused: the d_a partials are consumed)
+    }
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dsum[g * K + k0 + i] = ds[i];
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < K; k += kStThreads) pdst[k] = dsum[k] + dsum[K + k];
+  for (int s = r + C * tid; s < Ts; s += C * kStThreads) {
+    const int j = (s - r) / C;
+    a.dacc_out[(int64_t)b * Ts + s] =
+        s < len ? dacc[s] + (((red[j * 8] + red[j * 8 + 1]) + red[j * 8 + 2]) + red[j * 8 + 3]) : 0.f;
+  }
+  cl.sync();
+  if (r == 0) {
+    for (int k = tid; k < K; k += kStThreads) {
+      float d = pdst[k];
+#pragma unroll
+      for (int p = 1; p < C; ++p) d += cl.map_shared_rank(pdst, p)[k];
+      a.ds32[row * K + k] = d;
+      a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
+    }
+  }
+  cl.sync();  // the peers' shared memory stays alive until CTA 0 has read it
+}
+
 // ---- after the loop: the accumulations over t ----------------------------------------------
 struct CtxGrad {
   int B, Ts, T, K;
@@ -923,6 +1284,36 @@ void gemm_split(TcGemm g, int ks, cudaStream_t st) {
 size_t att_fwd_smem(const DecDims& d) { return (size_t)(6 * d.Ts + 4 + 1024) * 4; }
 size_t att_bwd_smem(const DecDims& d) { return (size_t)(5 * d.K + 13 * d.Ts) * 4; }
 
+template <int C, typename Args>
+void launch_cluster(void (*kern)(Args), int B, size_t smem, const Args& args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(C * B));
+  cfg.blockDim = dim3(kStThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args));
+}
+
+// cluster size of the TMA-staged attention kernels: the smallest C whose per-CTA
+// staging fits two CTAs per SM; 0 = the register-streaming kernels (or SL_DEC_ATT_REGS)
+int att_cluster(const DecDims& d) {
+  if (getenv("SL_DEC_ATT_REGS")) return 0;
+  if (d.E > 2 * 1024) return 0;
+  for (int C : {4, 8}) {
+    if (st_cols(d.E, C) > 512) continue;
+    const size_t need = std::max(FwdSt(d.Ts, d.K, d.E, C).total, BwdSt(d.Ts, d.K, d.E, C).total);
+    if (need <= 110 * 1024) return C;
+  }
+  return 0;
+}
+
 void configure() {  // opt in to > 48 KB dynamic shared memory once
   static bool done = false;
   if (done) return;
@@ -930,6 +1321,10 @@ void configure() {  // opt in to > 48 KB dynamic shared memory once
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_ctx_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_enc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_fwd_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_fwd_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
   const char* m = getenv("SL_DEC_TANH");
   const int mode = m ? atoi(m) : 0;
   SL_CUDA_TRY(cudaMemcpyToSymbol(c_tanh_mode, &mode, sizeof(int)));
@@ -999,6 +1394,7 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
   ph.reset();
   const int cell_threads = B * (H / 4);
   const double att_bytes = 2.0 * B * d.Ts * (K + E);
+  const int ac = att_cluster(d);
   for (int t = 0; t < T; ++t) {
     if (t > 0) {
       Phase p1(st, "k10_cell_gemm", 2.0 * B * (E + H) * 4 * H);
@@ -1016,7 +1412,9 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
               p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO, L.OA,
               L.xa, L.PXA};
     ph.reset(new Phase(st, "k10_attn_fwd", 0.0, att_bytes));
-    dec_attn_fwd_kernel<<<2 * B, kAttThreads, att_fwd_smem(d), st>>>(af);
+    if (ac == 4) launch_cluster<4>(dec_attn_fwd_tma_kernel<4>, B, FwdSt(d.Ts, K, E, 4).total, af, st);
+    else if (ac == 8) launch_cluster<8>(dec_attn_fwd_tma_kernel<8>, B, FwdSt(d.Ts, K, E, 8).total, af, st);
+    else dec_attn_fwd_kernel<<<2 * B, kAttThreads, att_fwd_smem(d), st>>>(af);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch(2);
     ph.reset();
@@ -1063,6 +1461,7 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   ph.reset();
   const int cell_threads = B * (H / 4);
   const double att_bytes = 2.0 * B * d.Ts * (K + E);
+  const int ac = att_cluster(d);
   for (int t = T - 1; t >= 0; --t) {
     const bool last = t == T - 1;
     if (!last) {
@@ -1076,7 +1475,9 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
               L.OA, p.fb_W, p.fb_b, p.e_W, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all,
               last ? nullptr : L.dacc + (int64_t)((t + 1) % 2) * B * d.Ts, L.dacc + (int64_t)(t % 2) * B * d.Ts,
               L.datt_all, L.de_all, L.ds, L.PK, L.ds32};
-    dec_attn_bwd_kernel<<<2 * B, kAttThreads, att_bwd_smem(d), st>>>(ab);
+    if (ac == 4) launch_cluster<4>(dec_attn_bwd_tma_kernel<4>, B, BwdSt(d.Ts, K, E, 4).total, ab, st);
+    else if (ac == 8) launch_cluster<8>(dec_attn_bwd_tma_kernel<8>, B, BwdSt(d.Ts, K, E, 8).total, ab, st);
+    else dec_attn_bwd_kernel<<<2 * B, kAttThreads, att_bwd_smem(d), st>>>(ab);
     ph.reset(new Phase(st, "k10_g2_gemm", 2.0 * B * H * K));
     gemm_split(mk(B, H, K, L.ds + (int64_t)t * B * L.PK, L.PK, false, L.wstr, L.PK, false, L.p2, L.PK),
                L.ks_2, st);
