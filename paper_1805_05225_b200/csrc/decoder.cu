@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cmath>
 #include <memory>
+#include <utility>
 
 #include "convert.h"
 #include "decoder.h"
@@ -50,8 +51,6 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 
-constexpr int kAttThreads = 512;
-constexpr int kAttWarps = kAttThreads / 32;
 constexpr int kCtxPos = 8;  // source positions per CTA in the pass-2 d enc_ctx kernel
 
 __constant__ int c_tanh_mode;  // 0: tanh.approx.f32 (one MUFU op), 1: 1 - 2 / (1 + e^{2x}) (two, ~1e-7 abs)
@@ -68,6 +67,15 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // wait for the peer just before the first remote shared-memory access
 __device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// Programmatic dependent launch (PDL): the per-step kernels are launched with
+// programmatic stream serialization, trigger their dependents at entry and, after
+// a prologue that only touches data that is static during the loop (enc, enc_ctx,
+// weights, the hoisted GEMM outputs), wait for the preceding grid.  The next
+// kernel's launch, its CTAs' ramp-up and its big static loads overlap the tail of
+// the previous one.  (Kernels launched without the attribute: both are no-ops.)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // bulk L2 prefetch of a contiguous 16 B-aligned range (multiple of 16 B): one instruction
 // puts a whole row segment in flight, so a later phase's loads hit L2
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -121,13 +129,16 @@ struct CellFwd {
   int64_t pxa;
   bf16* ro;  // [T*B, pro]: s_t -> row (t, b), column 0
   int64_t pro;
+  int b0, nb;  // this launch's batch rows [b0, b0 + nb) (concurrent batch slices)
 };
 
 __global__ void dec_cell_fwd_kernel(CellFwd a) {
+  pdl_trigger();
+  pdl_wait();
   const int qn = a.H / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.B * qn) return;
-  const int b = idx / qn, j = (idx - b * qn) * 4;
+  if (idx >= a.nb * qn) return;
+  const int b = a.b0 + idx / qn, j = (idx % qn) * 4;
   const int64_t row = (int64_t)a.t * a.B + b;  // every per-step buffer is time-major: a step is contiguous
   const int H = a.H;
   float z[4][4];
@@ -184,13 +195,16 @@ struct CellBwd {
   float* dc_out;       // d c_{t-1}
   bf16* dz;            // [B*T, pz]
   int64_t pz;
+  int b0, nb;
 };
 
 __global__ void dec_cell_bwd_kernel(CellBwd a) {
+  pdl_trigger();
+  pdl_wait();
   const int qn = a.H / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.B * qn) return;
-  const int b = idx / qn, j = (idx - b * qn) * 4;
+  if (idx >= a.nb * qn) return;
+  const int b = a.b0 + idx / qn, j = (idx % qn) * 4;
   const int64_t row = (int64_t)a.t * a.B + b;
   const int H = a.H;
   float gh[4] = {0.f, 0.f, 0.f, 0.f}, gc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -226,7 +240,24 @@ __global__ void dec_cell_bwd_kernel(CellBwd a) {
   stf4(a.dc_out + (int64_t)b * H + j, dcp);
 }
 
-// ---- attention step, one CTA per batch row ---------------------------------------------
+// ---- attention step: small independent CTAs ------------------------------------------------
+// Every step's attention is split into kernels whose CTAs need no cross-CTA
+// synchronisation — (row, 8 positions) for the energies and the tanh adjoint,
+// (row, 512 encoder columns) for the context and d_a — ~1000-2000 CTAs per launch, so
+// the loads of many resident CTAs overlap each other's arithmetic (a CTA per row, with
+// its phases separated by barriers, left the step latency-bound at ~30 % of HBM).
+// Inside a CTA every load a thread needs is issued before the first use (no
+// dependent chains of memory latencies), and the per-row softmax (and its adjoint)
+// over the Ts energies is recomputed by every CTA that needs it.  All cross-CTA sums
+// are written as partials and reduced in a fixed order (deterministic).
+constexpr int kPos = 8;        // positions per CTA (energies, tanh adjoint)
+constexpr int kCols = 512;     // encoder columns per CTA (context, d_a): 128 threads x 4
+constexpr int kAtt = 128;      // threads per (row, 8 positions) CTA
+constexpr int kGrp = 4;        // position groups of the (row, 512 columns) CTAs: 4 x 128 threads
+constexpr int kPerGrp = 16;    // positions per thread and batch in those CTAs (context)
+constexpr int kPerGrpDa = 8;   // (d_a: one warp reduction per position, fewer registers)
+constexpr int kMaxSplit = 8;   // split-K partials summed in-kernel
+
 struct AttFwd {
   int B, Ts, T, K, E, t, nsplit;
   const int32_t* lens;
@@ -237,6 +268,7 @@ struct AttFwd {
   int64_t pk;
   const bf16* enc;  // [B*Ts, ld_enc]
   int64_t ld_enc;
+  float* es;       // [B][Ts] energies of this step
   float* str_all;  // [T][B][K]: s_tr (with b_s)
   float* a_all;    // [T][B][Ts]
   float* acc_all;  // [T+1][B][Ts]: acc_all[t] = accum_{t-1}
@@ -245,158 +277,173 @@ struct AttFwd {
   int oa;
   bf16* xa;  // att_t -> row (t+1, b), column 0
   int64_t pxa;
+  int b0;  // grid.y covers rows [b0, b0 + gridDim.y)
 };
 
-// One CTA PAIR (a 2-CTA cluster) per batch row: CTA r takes the source positions
-// s = r (mod 2) for the energies and half of the encoder columns for the context;
-// the energies meet in both CTAs' shared memory over DSMEM.  Inside a CTA four
-// groups of 128 threads split the positions and every thread owns 8 key columns
-// (their s_tr, W_fb, v in registers); loads are issued four positions at a time
-// so enough bytes are in flight to stream the row's enc_ctx / enc from L2.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttThreads) dec_attn_fwd_kernel(AttFwd a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ float sm[];
-  const int Ts = a.Ts, K = a.K, tid = threadIdx.x, lane = tid % 32;
-  const int r = (int)cl.block_rank(), b = blockIdx.x / 2;
-  float* red = sm;            // [Ts][4] per-warp partial energies
-  float* es = red + 4 * Ts;   // [Ts] energies, then a
-  float* acc = es + Ts;       // [Ts] accum_{t-1}
-  float* ctx = sm + (6 * Ts + 3) / 4 * 4;  // [256][4] context partials of the second position group (16 B aligned)
-  cluster_arrive_relaxed();
-  const int len = min(max(a.lens[b], 0), Ts);
-  const size_t tb = (size_t)a.t * a.B + b;
-  if (tid < 64) {  // this CTA's enc_ctx rows (energies) and enc column half (context) into L2 now
-    for (int s = r + 2 * tid; s < len; s += 128)
-      prefetch_l2(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk, (uint32_t)K * 2);
-  } else if (tid < 128) {
-    for (int s = tid - 64; s < len; s += 64)
-      prefetch_l2(a.enc + ((int64_t)b * Ts + s) * a.ld_enc + r * (a.E / 2), (uint32_t)a.E);
-  }
-  for (int s = tid; s < Ts; s += kAttThreads) acc[s] = a.acc_all[tb * Ts + s];
-  const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
-  const bool act = k0 < K;
-  float cv[8], wv[8], vk[8];
-  if (act) {
-    float st[8];
+// s_tr (+ b_s) for 8 key columns: the split-K partials, all loads issued together
+__device__ __forceinline__ void str_cols(const float* P, int nsplit, int64_t p_stride, const float* bias, int k0,
+                                         float (&st)[8]) {
+  constexpr int kMaxStr = 4;  // the s_tr GEMM's split count (ksplit_for(..., 4))
+  float4 u[kMaxStr][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) st[i] = a.b_s[k0 + i];
-    for (int z = 0; z < a.nsplit; ++z) {
-      const float* pz = a.P + z * a.p_stride + (int64_t)b * a.p_ld + k0;
-      const float4 u0 = ldf4(pz), u1 = ldf4(pz + 4);
-      st[0] += u0.x, st[1] += u0.y, st[2] += u0.z, st[3] += u0.w;
-      st[4] += u1.x, st[5] += u1.y, st[6] += u1.z, st[7] += u1.w;
+  for (int z = 0; z < kMaxStr; ++z)
+    if (z < nsplit) {
+      u[z][0] = ldf4(P + z * p_stride + k0);
+      u[z][1] = ldf4(P + z * p_stride + k0 + 4);
     }
-    if (r == 0 && g == 0) {
+  const float4 b0 = ldf4(bias + k0), b1 = ldf4(bias + k0 + 4);
+  st[0] = b0.x, st[1] = b0.y, st[2] = b0.z, st[3] = b0.w, st[4] = b1.x, st[5] = b1.y, st[6] = b1.z, st[7] = b1.w;
+#pragma unroll
+  for (int z = 0; z < kMaxStr; ++z)
+    if (z < nsplit) {
+      st[0] += u[z][0].x, st[1] += u[z][0].y, st[2] += u[z][0].z, st[3] += u[z][0].w;
+      st[4] += u[z][1].x, st[5] += u[z][1].y, st[6] += u[z][1].z, st[7] += u[z][1].w;
+    }
+}
+
+// e[b, s] = <v, tanh(enc_ctx[b, s] + accum_{t-1}[b, s] W_fb + b_fb + s_tr[b])> + b_v
+// for 8 positions; a thread owns 8 key columns (K <= 1024)
+__global__ void __launch_bounds__(kAtt, 6) dec_att_energy_kernel(AttFwd a) {
+  __shared__ float red[kPos][4];
+  pdl_trigger();
+  const int b = a.b0 + blockIdx.y, j0 = blockIdx.x * kPos, Ts = a.Ts, K = a.K, tid = threadIdx.x;
+  const int lane = tid % 32, warp = tid / 32, k0 = tid * 8;
+  const bool act = k0 < K;
+  const size_t tb = (size_t)a.t * a.B + b;
+  uint4 x[kPos];  // rows j0.. exist for every j0 < Ts: load before knowing which are valid
+#pragma unroll
+  for (int p = 0; p < kPos; ++p) {
+    const int s = min(j0 + p, Ts - 1);
+    x[p] = act ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0) : make_uint4(0, 0, 0, 0);
+  }
+  const int len = min(max(a.lens[b], 0), Ts);
+  float4 f0, f1, w0, w1, v0, v1;
+  if (act) f0 = ldf4(a.b_fb + k0), f1 = ldf4(a.b_fb + k0 + 4), w0 = ldf4(a.W_fb + k0), w1 = ldf4(a.W_fb + k0 + 4),
+           v0 = ldf4(a.v + k0), v1 = ldf4(a.v + k0 + 4);
+  pdl_wait();  // s_tr partials (s_tr GEMM) and accum_{t-1} (previous step) from here on
+  float acp[kPos];
+#pragma unroll
+  for (int p = 0; p < kPos; ++p) acp[p] = a.acc_all[tb * Ts + min(j0 + p, Ts - 1)];
+  float st[8], cv[8], wv[8], vk[8];
+  if (act) {
+    str_cols(a.P + (int64_t)b * a.p_ld, a.nsplit, a.p_stride, a.b_s, k0, st);
+    const float bf[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+    const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const float vf[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cv[i] = st[i] + bf[i], wv[i] = wf[i], vk[i] = vf[i];
+    if (blockIdx.x == 0) {
       const float s0[4] = {st[0], st[1], st[2], st[3]}, s1[4] = {st[4], st[5], st[6], st[7]};
       stf4(a.str_all + tb * K + k0, s0);
       stf4(a.str_all + tb * K + k0 + 4, s1);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      cv[i] = st[i] + a.b_fb[k0 + i];
-      wv[i] = a.W_fb[k0 + i];
-      vk[i] = a.v[k0 + i];
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) cv[i] = wv[i] = vk[i] = 0.f;
   }
-  __syncthreads();
-  // energies of this CTA's positions s = r + 2 (g + 4 m), four per batch
-  for (int s0 = r + 2 * g; s0 < len; s0 += 32) {
-    uint4 x[4];
+  const int n = min(kPos, len - j0);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int s = s0 + 8 * u;
-      x[u] = (act && s < len) ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0)
-                              : make_uint4(0, 0, 0, 0);
-    }
-    float p[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int s = s0 + 8 * u;
-      float f[8];
-      unpack8(x[u], f);
-      const float as = s < len ? acc[s] : 0.f;
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sum += vk[i] * tanh_approx(f[i] + as * wv[i] + cv[i]);
-      p[u] = warp_sum(act ? sum : 0.f);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (s0 + 8 * u < len) red[(s0 + 8 * u) * 4 + wig] = p[u];
-    }
-  }
-  __syncthreads();
-  cluster_wait();
-  float* peer_es = cl.map_shared_rank(es, r ^ 1);
-  const float bv = *a.b_v;
-  for (int s = r + 2 * tid; s < len; s += 2 * kAttThreads) {
-    const float e = ((red[s * 4] + red[s * 4 + 1]) + red[s * 4 + 2]) + red[s * 4 + 3] + bv;
-    es[s] = e;
-    peer_es[s] = e;
-  }
-  cl.sync();
-  if (tid < 32) {  // masked softmax over the valid positions (tape.cpp:952-960), in both CTAs
-    float m = -INFINITY;
-    for (int s = lane; s < len; s += 32) m = fmaxf(m, es[s]);
-    m = warp_max(m);
+  for (int p = 0; p < kPos; ++p) {
     float sum = 0.f;
-    for (int s = lane; s < len; s += 32) {
-      const float ex = expf(es[s] - m);
-      es[s] = ex;
-      sum += ex;
+    if (p < n) {
+      float f[8];
+      unpack8(x[p], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += vk[i] * tanh_approx(f[i] + acp[p] * wv[i] + cv[i]);
     }
     sum = warp_sum(sum);
-    const float inv = len > 0 ? 1.f / sum : 0.f;
-    __syncwarp();
-    for (int s = lane; s < Ts; s += 32) {
-      const float av = s < len ? es[s] * inv : 0.f;
-      es[s] = av;
-      if (r == 0) {
-        a.a_all[tb * Ts + s] = av;
-        a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = acc[s] + av;
-      }
-    }
+    if (lane == 0) red[p][warp] = sum;
   }
   __syncthreads();
-  {  // att = sum_s a_s enc_s (tape.cpp:1005-1014): this CTA's half of the columns, two position groups
-    const int gc = tid / 256, qc = tid % 256, Eh = a.E / 2, e0 = r * Eh + qc * 4;
-    const bool on = qc * 4 < Eh;
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + e0;
-    for (int s0 = gc; s0 < len; s0 += 8) {
-      float f[4][4];
+  if (tid < n) a.es[(int64_t)b * Ts + j0 + tid] = ((red[tid][0] + red[tid][1]) + red[tid][2]) + red[tid][3] + *a.b_v;
+}
+
+// masked softmax of a row's energies into shared memory (tape.cpp:952-960); warp 0.
+// The first 128 energies come in with one round of loads (registers), the rest (Ts > 128) in a loop.
+__device__ __forceinline__ void row_softmax(const float* e, int len, int Ts, float* a_sm) {
+  const int lane = threadIdx.x % 32;
+  float r[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + 2 * u;
-        if (on && s < len) ld4(x + (int64_t)s * a.ld_enc, f[u]);
-        else f[u][0] = f[u][1] = f[u][2] = f[u][3] = 0.f;
-      }
+  for (int i = 0; i < 4; ++i) r[i] = lane + 32 * i < len ? e[lane + 32 * i] : -INFINITY;
+  float m = fmaxf(fmaxf(r[0], r[1]), fmaxf(r[2], r[3]));
+  for (int s = lane + 128; s < len; s += 32) m = fmaxf(m, e[s]);
+  m = warp_max(m);
+  float sum = 0.f;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float as = s0 + 2 * u < len ? es[s0 + 2 * u] : 0.f;
+  for (int i = 0; i < 4; ++i) {
+    const float ex = lane + 32 * i < len ? expf(r[i] - m) : 0.f;
+    r[i] = ex;
+    sum += ex;
+  }
+  for (int s = lane + 128; s < len; s += 32) {
+    const float ex = expf(e[s] - m);
+    a_sm[s] = ex;
+    sum += ex;
+  }
+  sum = warp_sum(sum);
+  const float inv = len > 0 ? 1.f / sum : 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] += as * f[u][i];
-      }
+  for (int i = 0; i < 4; ++i)
+    if (lane + 32 * i < Ts) a_sm[lane + 32 * i] = r[i] * inv;
+  __syncwarp();
+  for (int s = lane + 128; s < Ts; s += 32) a_sm[s] = s < len ? a_sm[s] * inv : 0.f;
+}
+
+// a = softmax(e) (recomputed per CTA), accum_t = accum_{t-1} + a, att = sum_s a_s enc_s
+// (tape.cpp:1005-1014) for 512 encoder columns: 4 groups of 128 threads split the
+// positions, each thread loads its (up to) 16 positions' 4 columns at once
+__global__ void __launch_bounds__(kAtt * kGrp, 2) dec_att_context_kernel(AttFwd a) {
+  extern __shared__ float asm_[];  // [Ts] a, then [kGrp - 1][kCols] partial contexts
+  pdl_trigger();
+  float* part = asm_ + (a.Ts + 3) / 4 * 4;
+  const int b = a.b0 + blockIdx.y, Ts = a.Ts, tid = threadIdx.x, g = tid / kAtt, q = tid % kAtt;
+  const int c = blockIdx.x * kCols + q * 4;
+  const bool on = c < a.E;
+  const size_t tb = (size_t)a.t * a.B + b;
+  const int len = min(max(a.lens[b], 0), Ts);
+  const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + c;
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  uint2 raw[kPerGrp];
+  auto load = [&](int s0) {
+#pragma unroll
+    for (int u = 0; u < kPerGrp; ++u) {
+      const int s = s0 + kGrp * u;
+      raw[u] = (on && s < len) ? *reinterpret_cast<const uint2*>(x + (int64_t)s * a.ld_enc) : make_uint2(0, 0);
     }
-    if (gc == 1 && on) stf4(ctx + qc * 4, o);
-    __syncthreads();
-    if (gc == 0 && on) {
-      const float4 o2 = ldf4(ctx + qc * 4);
-      o[0] += o2.x, o[1] += o2.y, o[2] += o2.z, o[3] += o2.w;
-      const int64_t row = (int64_t)a.t * a.B + b;
-      st4(a.ro + row * a.pro + a.oa + e0, o);
-      if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + e0, o);
+  };
+  load(g);    // the first batch of encoder rows is in flight before the wait ...
+  pdl_wait();  // ... for the energies of this step
+  if (tid < 32) row_softmax(a.es + (int64_t)b * Ts, len, Ts, asm_);
+  __syncthreads();  // a is ready
+  for (int s0 = g; s0 < len; s0 += kGrp * kPerGrp) {
+    if (s0 != g) load(s0);
+#pragma unroll
+    for (int u = 0; u < kPerGrp; ++u) {
+      const int s = s0 + kGrp * u;
+      const float as = s < len ? asm_[s] : 0.f;
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[u].x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[u].y));
+      o[0] += as * lo.x, o[1] += as * lo.y, o[2] += as * hi.x, o[3] += as * hi.y;
     }
+  }
+  if (blockIdx.x == 0)
+    for (int s = tid; s < Ts; s += kAtt * kGrp) {
+      a.a_all[tb * Ts + s] = asm_[s];
+      a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = a.acc_all[tb * Ts + s] + asm_[s];
+    }
+  if (g > 0) stf4(part + (g - 1) * kCols + q * 4, o);
+  __syncthreads();
+  if (g == 0 && on) {
+#pragma unroll
+    for (int h = 0; h < kGrp - 1; ++h) addf4(o, ldf4(part + h * kCols + q * 4));
+    const int64_t row = (int64_t)a.t * a.B + b;
+    st4(a.ro + row * a.pro + a.oa + c, o);
+    if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + c, o);
   }
 }
 
 struct AttBwd {
-  int B, Ts, T, K, E, t, n1;
+  int B, Ts, T, K, E, t, n1, nch, nsc;
   const int32_t* lens;
   const float* P1;  // G1 partials: d att_t (from the cell at t+1) at columns 0..E
   int64_t p1_ld, p1_stride;
@@ -411,551 +458,179 @@ struct AttBwd {
   const float *str_all, *a_all, *acc_all;
   const float* dacc_in;  // d accum_t [B][Ts] (null at t = T-1)
   float* dacc_out;       // d accum_{t-1}
+  float* dap;            // [B][nch][Ts] d_a partials per column chunk
+  float* dsp;            // [B][nsc][K] d s_tr partials per position chunk
   float* datt_all;       // [T][B][E]
   float* de_all;         // [T][B][Ts]
   bf16* ds;              // d s_tr -> row (t, b) of [T*B, pds]
   int64_t pds;
-  float* ds32;  // [B*T, K]
+  float* ds32;  // [T*B, K]
+  int b0;
 };
 
-// Adjoint of one attention step, restricted to what the recurrence needs:
-// d_a = enc d_att + d accum_t (tape.cpp:1031-1041), de = a (d_a - <a, d_a>)
-// (tape.cpp:966-978), d e_in = de v (1 - u^2) -> d s_tr = sum_s d e_in and
-// d accum_{t-1} = d accum_t + d e_in W_fb.  One CTA pair per batch row (CTA r:
-// positions s = r mod 2); d_a meets over DSMEM, the pair's d s_tr halves are
-// summed in a fixed order by CTA 0.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kAttThreads) dec_attn_bwd_kernel(AttBwd a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ float sm[];
-  const int K = a.K, Ts = a.Ts, E = a.E, tid = threadIdx.x, lane = tid % 32;
-  const int r = (int)cl.block_rank(), b = blockIdx.x / 2;
-  float* dsum = sm;             // [4][K]
-  float* pdst = dsum + 4 * K;   // [K] this CTA's d s_tr
-  float* av = pdst + K;         // [Ts]
-  float* acc = av + Ts;         // [Ts]
-  float* dacc = acc + Ts;       // [Ts] d accum_t
-  float* da = dacc + Ts;        // [Ts]
-  float* de = da + Ts;          // [Ts]
-  float* red = de + Ts;         // [Ts][8]
-  cluster_arrive_relaxed();
-  const int len = min(max(a.lens[b], 0), Ts);
+// d att_t (readout part + the cell at t+1's dx) for 512 columns, and this chunk's part of
+// d_a[s] = <d att_t, enc_s> for every position (tape.cpp:1031-1041); the position split
+// and batched loads as in the context kernel
+__global__ void __launch_bounds__(kAtt * kGrp, 2) dec_att_da_kernel(AttBwd a) {
+  extern __shared__ float red[];  // [Ts][4]: per-warp partials (the 4 warps of the position's group)
+  pdl_trigger();
+  const int b = a.b0 + blockIdx.y, Ts = a.Ts, tid = threadIdx.x, lane = tid % 32, g = tid / kAtt, q = tid % kAtt;
+  const int wig = q / 32, c = blockIdx.x * kCols + q * 4;
+  const bool on = c < a.E;
   const size_t tb = (size_t)a.t * a.B + b;
   const int64_t row = (int64_t)a.t * a.B + b;
-  if (tid < 64) {  // this CTA's enc rows (d_a) and enc_ctx rows (tanh adjoint) into L2 now
-    for (int s = r + 2 * tid; s < len; s += 128)
-      prefetch_l2(a.enc + ((int64_t)b * Ts + s) * a.ld_enc, (uint32_t)E * 2);
-  } else if (tid < 128) {
-    for (int s = r + 2 * (tid - 64); s < len; s += 128)
-      prefetch_l2(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk, (uint32_t)K * 2);
-  }
-  for (int s = tid; s < Ts; s += kAttThreads) {
-    av[s] = a.a_all[tb * Ts + s];
-    acc[s] = a.acc_all[tb * Ts + s];
-    dacc[s] = (a.dacc_in && s < len) ? a.dacc_in[(int64_t)b * Ts + s] : 0.f;
-  }
-  {  // d_a of this CTA's positions: two groups of 256 threads, 8 encoder columns each
-    const int gc = tid / 256, qc = tid % 256, wig = qc / 32, e0 = qc * 8;
-    const bool on = e0 < E;
-    float dv[8];
-    if (on) {
-      const float* pd = a.dro + row * a.prf + a.oa + e0;
-      const float4 u0 = ldf4(pd), u1 = ldf4(pd + 4);
-      dv[0] = u0.x, dv[1] = u0.y, dv[2] = u0.z, dv[3] = u0.w, dv[4] = u1.x, dv[5] = u1.y, dv[6] = u1.z, dv[7] = u1.w;
-      for (int z = 0; z < a.n1; ++z) {
-        const float* pz = a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + e0;
-        const float4 w0 = ldf4(pz), w1 = ldf4(pz + 4);
-        dv[0] += w0.x, dv[1] += w0.y, dv[2] += w0.z, dv[3] += w0.w;
-        dv[4] += w1.x, dv[5] += w1.y, dv[6] += w1.z, dv[7] += w1.w;
-      }
-      if (r == 0 && gc == 0) {
-        const float d0[4] = {dv[0], dv[1], dv[2], dv[3]}, d1[4] = {dv[4], dv[5], dv[6], dv[7]};
-        stf4(a.datt_all + tb * E + e0, d0);
-        stf4(a.datt_all + tb * E + e0 + 4, d1);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dv[i] = 0.f;
-    }
-    for (int s0 = r + 2 * gc; s0 < len; s0 += 16) {  // positions s0, s0+4, s0+8, s0+12
-      uint4 x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + 4 * u;
-        x[u] = (on && s < len) ? *reinterpret_cast<const uint4*>(a.enc + ((int64_t)b * Ts + s) * a.ld_enc + e0)
-                               : make_uint4(0, 0, 0, 0);
-      }
-      float p[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float f[8];
-        unpack8(x[u], f);
-        float sum = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sum += dv[i] * f[i];
-        p[u] = warp_sum(sum);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (s0 + 4 * u < len) red[(s0 + 4 * u) * 8 + wig] = p[u];
-      }
-    }
-  }
-  __syncthreads();
-  cluster_wait();
-  float* peer_da = cl.map_shared_rank(da, r ^ 1);
-  for (int s = r + 2 * tid; s < len; s += 2 * kAttThreads) {
-    float sum = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sum += red[s * 8 + w];
-    sum += dacc[s];
-    da[s] = sum;
-    peer_da[s] = sum;
-  }
-  cl.sync();
-  if (tid < 32) {  // softmax adjoint, in both CTAs
-    float dot = 0.f;
-    for (int s = lane; s < len; s += 32) dot += av[s] * da[s];
-    dot = warp_sum(dot);
-    for (int s = lane; s < Ts; s += 32) {
-      const float d = s < len ? av[s] * (da[s] - dot) : 0.f;
-      de[s] = d;
-      if (r == 0) a.de_all[tb * Ts + s] = d;
-    }
-  }
-  __syncthreads();
-  {  // tanh adjoint over this CTA's positions: four groups of 128 threads, 8 key columns each
-    const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
-    const bool act = k0 < K;
-    float wv[8], cv[8], vk[8], ds[8];
-    if (act) {
-      const float* st = a.str_all + tb * K + k0;
-      const float4 s0v = ldf4(st), s1v = ldf4(st + 4);
-      const float sv[8] = {s0v.x, s0v.y, s0v.z, s0v.w, s1v.x, s1v.y, s1v.z, s1v.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        wv[i] = a.W_fb[k0 + i];
-        cv[i] = sv[i] + a.b_fb[k0 + i];
-        vk[i] = a.v[k0 + i];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) wv[i] = cv[i] = vk[i] = 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ds[i] = 0.f;
-    for (int s0 = r + 2 * g; s0 < len; s0 += 32) {  // positions s0 + 8u
-      uint4 x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + 8 * u;
-        x[u] = (act && s < len) ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0)
-                                : make_uint4(0, 0, 0, 0);
-      }
-      float p[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + 8 * u;
-        const float as = s < len ? acc[s] : 0.f, des = s < len ? de[s] : 0.f;
-        float f[8];
-        unpack8(x[u], f);
-        float pa = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float uu = tanh_approx(f[i] + as * wv[i] + cv[i]);
-          const float dein = des * vk[i] * (1.f - uu * uu);
-          ds[i] += dein;
-          pa += wv[i] * dein;
-        }
-        p[u] = warp_sum(act ? pa : 0.f);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (s0 + 8 * u < len) red[(s0 + 8 * u) * 8 + wig] = p[u];  // (red reused: d_a is consumed)
-      }
-    }
-    if (act) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dsum[g * K + k0 + i] = ds[i];
-    }
-  }
-  __syncthreads();
-  for (int k = tid; k < K; k += kAttThreads) pdst[k] = ((dsum[k] + dsum[K + k]) + dsum[2 * K + k]) + dsum[3 * K + k];
-  for (int s = r + 2 * tid; s < Ts; s += 2 * kAttThreads)
-    a.dacc_out[(int64_t)b * Ts + s] =
-        s < len ? dacc[s] + (((red[s * 8] + red[s * 8 + 1]) + red[s * 8 + 2]) + red[s * 8 + 3]) : 0.f;
-  cl.sync();
-  if (r == 0) {
-    const float* peer = cl.map_shared_rank(pdst, 1);
-    for (int k = tid; k < K; k += kAttThreads) {
-      const float d = pdst[k] + peer[k];
-      a.ds32[row * K + k] = d;
-      a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
-    }
-  }
-  cl.sync();  // CTA 1's shared memory stays alive until CTA 0 has read it
-}
-
-// ---- the same two attention kernels with the row's operands staged by TMA --------------
-// C CTAs (one cluster) per batch row, 256 threads each.  CTA r owns the positions
-// s = r (mod C) and, for the context, one 16 B-aligned column slice of enc; at
-// kernel start one warp issues a 1-D bulk copy (cp.async.bulk) per row segment the
-// CTA will read — its enc_ctx rows and enc slice in the forward, its enc and
-// enc_ctx rows in the backward — completing on two mbarriers, so every byte is in
-// flight at once and the phases then read shared memory.  ~95 KB per CTA: two
-// CTAs per SM, one loading while the other computes.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   tc::smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
-               : "memory");
-}
-constexpr int kStThreads = 256;
-__host__ __device__ inline int st_cols(int E, int C) { return ((E + C - 1) / C + 7) / 8 * 8; }
-__host__ __device__ inline size_t st_align(size_t x) { return (x + 127) / 128 * 128; }
-// shared-memory carve-ups (bytes), shared by host (launch size) and device
-struct FwdSt {
-  size_t red, es, acc, cpart, rctx, renc, total;
-  __host__ __device__ FwdSt(int Ts, int K, int E, int C) {
-    const int nrm = (Ts + C - 1) / C, Ec = st_cols(E, C);
-    red = 16;
-    es = red + (size_t)nrm * 4 * 4;
-    acc = es + (size_t)Ts * 4;
-    cpart = (acc + (size_t)Ts * 4 + 15) / 16 * 16;  // float4 accesses
-    rctx = st_align(cpart + (size_t)Ec * 4);
-    renc = st_align(rctx + (size_t)nrm * K * 2);
-    total = renc + (size_t)Ts * Ec * 2;
-  }
-};
-struct BwdSt {
-  size_t av, acc, dacc, da, de, red, pdst, renc, rctx, total;
-  __host__ __device__ BwdSt(int Ts, int K, int E, int C) {
-    const int nrm = (Ts + C - 1) / C;
-    av = 16;
-    acc = av + (size_t)Ts * 4;
-    dacc = acc + (size_t)Ts * 4;
-    da = dacc + (size_t)Ts * 4;
-    de = da + (size_t)Ts * 4;
-    red = de + (size_t)Ts * 4;
-    pdst = red + (size_t)nrm * 8 * 4;
-    renc = st_align(pdst + (size_t)K * 4);
-    const size_t renc_bytes = (size_t)nrm * E * 2, dsum_bytes = (size_t)2 * K * 4;
-    rctx = st_align(renc + (renc_bytes > dsum_bytes ? renc_bytes : dsum_bytes));  // renc doubles as dsum [2][K]
-    total = rctx + (size_t)nrm * K * 2;
-  }
-};
-
-template <int C>
-__global__ void __launch_bounds__(kStThreads) dec_attn_fwd_tma_kernel(AttFwd a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(128) uint8_t smraw[];
-  const int Ts = a.Ts, K = a.K, E = a.E, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
-  const int r = (int)cl.block_rank(), b = blockIdx.x / C;
-  const FwdSt L(Ts, K, E, C);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
-  float* red = reinterpret_cast<float*>(smraw + L.red);
-  float* es = reinterpret_cast<float*>(smraw + L.es);
-  float* acc = reinterpret_cast<float*>(smraw + L.acc);
-  float* cpart = reinterpret_cast<float*>(smraw + L.cpart);
-  bf16* rctx = reinterpret_cast<bf16*>(smraw + L.rctx);
-  bf16* renc = reinterpret_cast<bf16*>(smraw + L.renc);
-  const int Ec = st_cols(E, C), c0 = r * Ec, nc = max(0, min(E - c0, Ec));
-  cluster_arrive_relaxed();
   const int len = min(max(a.lens[b], 0), Ts);
-  const int nr = r < len ? (len - r + C - 1) / C : 0;  // this CTA's positions s = r + C j
-  const size_t tb = (size_t)a.t * a.B + b;
-  if (tid == 0) {
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
-    tc::fence_barrier_init();
+  const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + c;
+  uint2 raw[kPerGrpDa];
+  auto load = [&](int s0) {
+#pragma unroll
+    for (int u = 0; u < kPerGrpDa; ++u) {
+      const int s = s0 + kGrp * u;
+      raw[u] = (on && s < len) ? *reinterpret_cast<const uint2*>(x + (int64_t)s * a.ld_enc) : make_uint2(0, 0);
+    }
+  };
+  load(g);     // the first batch of encoder rows is in flight before the wait ...
+  pdl_wait();  // ... for d att_t (G1 partials)
+  float dv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (on) {
+    addf4(dv, ldf4(a.dro + row * a.prf + a.oa + c));
+#pragma unroll
+    for (int z = 0; z < kMaxSplit; ++z)
+      if (z < a.n1) addf4(dv, ldf4(a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + c));
+    if (g == 0) stf4(a.datt_all + tb * a.E + c, dv);
+  }
+  for (int s0 = g; s0 < len; s0 += kGrp * kPerGrpDa) {
+    if (s0 != g) load(s0);
+#pragma unroll
+    for (int u = 0; u < kPerGrpDa; ++u) {
+      const int s = s0 + kGrp * u;
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[u].x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[u].y));
+      float sum = ((dv[0] * lo.x + dv[1] * lo.y) + dv[2] * hi.x) + dv[3] * hi.y;
+      sum = warp_sum(sum);
+      if (lane == 0 && s < len) red[s * 4 + wig] = sum;
+    }
   }
   __syncthreads();
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)(nr * K * 2));
-      tc::mbar_arrive_expect_tx(&bars[1], (uint32_t)(nc > 0 ? len * nc * 2 : 0));
-    }
-    __syncwarp();
-    for (int j = lane; j < nr; j += 32)
-      bulk_g2s(rctx + (size_t)j * K, a.enc_ctx + ((int64_t)b * Ts + r + C * j) * a.pk, (uint32_t)K * 2, &bars[0]);
-    if (nc > 0)
-      for (int s = lane; s < len; s += 32)
-        bulk_g2s(renc + (size_t)s * Ec, a.enc + ((int64_t)b * Ts + s) * a.ld_enc + c0, (uint32_t)nc * 2, &bars[1]);
-  }
-  for (int s = tid; s < Ts; s += kStThreads) acc[s] = a.acc_all[tb * Ts + s];
-  const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
+  for (int s = tid; s < len; s += kAtt * kGrp)
+    a.dap[((int64_t)b * a.nch + blockIdx.x) * Ts + s] = ((red[s * 4] + red[s * 4 + 1]) + red[s * 4 + 2]) + red[s * 4 + 3];
+}
+
+// softmax adjoint de = a (d_a - <a, d_a>) (tape.cpp:966-978; recomputed per CTA from the
+// d_a partials), then for 8 positions d e_in = de v (1 - u^2): this chunk's d s_tr
+// partial and d accum_{t-1} = d accum_t + d e_in W_fb
+__global__ void __launch_bounds__(kAtt, 6) dec_att_tanh_kernel(AttBwd a) {
+  extern __shared__ float sm[];  // de[Ts], then red[kPos][4]
+  pdl_trigger();
+  float* de = sm;
+  float* red = sm + a.Ts;
+  const int b = a.b0 + blockIdx.y, j0 = blockIdx.x * kPos, Ts = a.Ts, K = a.K, tid = threadIdx.x;
+  const int lane = tid % 32, warp = tid / 32, k0 = tid * 8;
+  const size_t tb = (size_t)a.t * a.B + b;
   const bool act = k0 < K;
-  float cv[8], wv[8], vk[8];
+  uint4 x[kPos];
+#pragma unroll
+  for (int p = 0; p < kPos; ++p) {
+    const int s = min(j0 + p, Ts - 1);
+    x[p] = act ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0) : make_uint4(0, 0, 0, 0);
+  }
+  const int len = min(max(a.lens[b], 0), Ts);
+  pdl_wait();  // d_a partials (previous kernel) and the step's saves from here on
+  float acp[kPos];
+#pragma unroll
+  for (int p = 0; p < kPos; ++p) acp[p] = a.acc_all[tb * Ts + min(j0 + p, Ts - 1)];
+  for (int s = tid; s < Ts; s += kAtt) {  // d_a = sum of the column-chunk partials + d accum_t
+    float d = 0.f;
+    if (s < len) {
+      float u[kMaxSplit];
+#pragma unroll
+      for (int h = 0; h < kMaxSplit; ++h)
+        if (h < a.nch) u[h] = a.dap[((int64_t)b * a.nch + h) * Ts + s];
+#pragma unroll
+      for (int h = 0; h < kMaxSplit; ++h)
+        if (h < a.nch) d += u[h];
+      if (a.dacc_in) d += a.dacc_in[(int64_t)b * Ts + s];
+    }
+    de[s] = d;
+  }
+  float st[8], wv[8], cv[8], vk[8], ds[8];
   if (act) {
-    float st[8];
+    const float4 s0v = ldf4(a.str_all + tb * K + k0), s1v = ldf4(a.str_all + tb * K + k0 + 4);
+    const float4 f0 = ldf4(a.b_fb + k0), f1 = ldf4(a.b_fb + k0 + 4), w0 = ldf4(a.W_fb + k0), w1 = ldf4(a.W_fb + k0 + 4);
+    const float4 v0 = ldf4(a.v + k0), v1 = ldf4(a.v + k0 + 4);
+    st[0] = s0v.x, st[1] = s0v.y, st[2] = s0v.z, st[3] = s0v.w, st[4] = s1v.x, st[5] = s1v.y, st[6] = s1v.z, st[7] = s1v.w;
+    const float bf[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+    const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const float vf[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) st[i] = a.b_s[k0 + i];
-    for (int z = 0; z < a.nsplit; ++z) {
-      const float* pz = a.P + z * a.p_stride + (int64_t)b * a.p_ld + k0;
-      const float4 u0 = ldf4(pz), u1 = ldf4(pz + 4);
-      st[0] += u0.x, st[1] += u0.y, st[2] += u0.z, st[3] += u0.w;
-      st[4] += u1.x, st[5] += u1.y, st[6] += u1.z, st[7] += u1.w;
-    }
-    if (r == 0 && g == 0) {
-      const float s0[4] = {st[0], st[1], st[2], st[3]}, s1[4] = {st[4], st[5], st[6], st[7]};
-      stf4(a.str_all + tb * K + k0, s0);
-      stf4(a.str_all + tb * K + k0 + 4, s1);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      cv[i] = st[i] + a.b_fb[k0 + i];
-      wv[i] = a.W_fb[k0 + i];
-      vk[i] = a.v[k0 + i];
-    }
+    for (int i = 0; i < 8; ++i) cv[i] = st[i] + bf[i], wv[i] = wf[i], vk[i] = vf[i];
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) cv[i] = wv[i] = vk[i] = 0.f;
   }
+  const int n = min(kPos, len - j0);
   __syncthreads();
-  tc::mbar_wait(&bars[0], 0);
-  for (int j = g; j < nr; j += 2) {  // e_s = <v, tanh(e_in_s)> over this CTA's positions
-    const int s = r + C * j;
-    float f[8];
-    if (act) ld8(rctx + (size_t)j * K + k0, f);
-    const float as = acc[s];
-    float sum = 0.f;
-    if (act) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sum += vk[i] * tanh_approx(f[i] + as * wv[i] + cv[i]);
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) red[j * 4 + wig] = sum;
-  }
-  __syncthreads();
-  cluster_wait();
-  const float bv = *a.b_v;
-  for (int j = tid; j < nr; j += kStThreads) {
-    const int s = r + C * j;
-    const float e = ((red[j * 4] + red[j * 4 + 1]) + red[j * 4 + 2]) + red[j * 4 + 3] + bv;
-#pragma unroll
-    for (int p = 0; p < C; ++p) cl.map_shared_rank(es, p)[s] = e;
-  }
-  cl.sync();
-  if (tid < 32) {  // masked softmax over the valid positions (tape.cpp:952-960), in every CTA
-    float m = -INFINITY;
-    for (int s = lane; s < len; s += 32) m = fmaxf(m, es[s]);
-    m = warp_max(m);
-    float sum = 0.f;
-    for (int s = lane; s < len; s += 32) {
-      const float ex = expf(es[s] - m);
-      es[s] = ex;
-      sum += ex;
-    }
-    sum = warp_sum(sum);
-    const float inv = len > 0 ? 1.f / sum : 0.f;
-    __syncwarp();
-    for (int s = lane; s < Ts; s += 32) {
-      const float av = s < len ? es[s] * inv : 0.f;
-      es[s] = av;
-      if (r == 0) {
-        a.a_all[tb * Ts + s] = av;
-        a.acc_all[((size_t)(a.t + 1) * a.B + b) * Ts + s] = acc[s] + av;
-      }
-    }
-  }
-  __syncthreads();
-  {  // att (this CTA's column slice) = sum_s a_s enc_s (tape.cpp:1005-1014), two position groups
-    const int gc = tid / 128, cq = tid % 128, cc = cq * 4;
-    const bool on = cc < nc;
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    if (nc > 0) tc::mbar_wait(&bars[1], 0);
-    if (on) {
-      for (int s = gc; s < len; s += 2) {
-        float f[4];
-        ld4(renc + (size_t)s * Ec + cc, f);
-        const float as = es[s];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] += as * f[i];
-      }
-    }
-    if (gc == 1 && on) stf4(cpart + cc, o);
-    __syncthreads();
-    if (gc == 0 && on) {
-      const float4 o2 = ldf4(cpart + cc);
-      o[0] += o2.x, o[1] += o2.y, o[2] += o2.z, o[3] += o2.w;
-      const int64_t row = (int64_t)a.t * a.B + b;
-      st4(a.ro + row * a.pro + a.oa + c0 + cc, o);
-      if (a.t + 1 < a.T) st4(a.xa + (row + a.B) * a.pxa + c0 + cc, o);
-    }
-  }
-}
-
-template <int C>
-__global__ void __launch_bounds__(kStThreads) dec_attn_bwd_tma_kernel(AttBwd a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(128) uint8_t smraw[];
-  const int K = a.K, Ts = a.Ts, E = a.E, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
-  const int r = (int)cl.block_rank(), b = blockIdx.x / C;
-  const BwdSt L(Ts, K, E, C);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
-  float* av = reinterpret_cast<float*>(smraw + L.av);
-  float* acc = reinterpret_cast<float*>(smraw + L.acc);
-  float* dacc = reinterpret_cast<float*>(smraw + L.dacc);
-  float* da = reinterpret_cast<float*>(smraw + L.da);
-  float* de = reinterpret_cast<float*>(smraw + L.de);
-  float* red = reinterpret_cast<float*>(smraw + L.red);
-  float* pdst = reinterpret_cast<float*>(smraw + L.pdst);
-  bf16* renc = reinterpret_cast<bf16*>(smraw + L.renc);
-  float* dsum = reinterpret_cast<float*>(smraw + L.renc);  // [2][K], after the d_a phase
-  bf16* rctx = reinterpret_cast<bf16*>(smraw + L.rctx);
-  cluster_arrive_relaxed();
-  const int len = min(max(a.lens[b], 0), Ts);
-  const int nr = r < len ? (len - r + C - 1) / C : 0;
-  const size_t tb = (size_t)a.t * a.B + b;
-  const int64_t row = (int64_t)a.t * a.B + b;
-  if (tid == 0) {
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
-    tc::fence_barrier_init();
-  }
-  __syncthreads();
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)(nr * E * 2));
-      tc::mbar_arrive_expect_tx(&bars[1], (uint32_t)(nr * K * 2));
-    }
-    __syncwarp();
-    for (int j = lane; j < nr; j += 32) {
-      const int64_t src = (int64_t)b * Ts + r + C * j;
-      bulk_g2s(renc + (size_t)j * E, a.enc + src * a.ld_enc, (uint32_t)E * 2, &bars[0]);
-      bulk_g2s(rctx + (size_t)j * K, a.enc_ctx + src * a.pk, (uint32_t)K * 2, &bars[1]);
-    }
-  }
-  for (int s = tid; s < Ts; s += kStThreads) {
-    av[s] = a.a_all[tb * Ts + s];
-    acc[s] = a.acc_all[tb * Ts + s];
-    dacc[s] = (a.dacc_in && s < len) ? a.dacc_in[(int64_t)b * Ts + s] : 0.f;
-  }
-  {  // d att_t for this thread's 8 columns; d_a over this CTA's positions (all 8 warps per position)
-    const int e0 = tid * 8;
-    const bool on = e0 < E;
-    float dv[8];
-    if (on) {
-      const float* pd = a.dro + row * a.prf + a.oa + e0;
-      const float4 u0 = ldf4(pd), u1 = ldf4(pd + 4);
-      dv[0] = u0.x, dv[1] = u0.y, dv[2] = u0.z, dv[3] = u0.w, dv[4] = u1.x, dv[5] = u1.y, dv[6] = u1.z, dv[7] = u1.w;
-      for (int z = 0; z < a.n1; ++z) {
-        const float* pz = a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + e0;
-        const float4 w0 = ldf4(pz), w1 = ldf4(pz + 4);
-        dv[0] += w0.x, dv[1] += w0.y, dv[2] += w0.z, dv[3] += w0.w;
-        dv[4] += w1.x, dv[5] += w1.y, dv[6] += w1.z, dv[7] += w1.w;
-      }
-      if (r == 0) {
-        const float d0[4] = {dv[0], dv[1], dv[2], dv[3]}, d1[4] = {dv[4], dv[5], dv[6], dv[7]};
-        stf4(a.datt_all + tb * E + e0, d0);
-        stf4(a.datt_all + tb * E + e0 + 4, d1);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dv[i] = 0.f;
-    }
-    tc::mbar_wait(&bars[0], 0);
-    for (int j = 0; j < nr; ++j) {
-      float sum = 0.f;
-      if (on) {
-        float f[8];
-        ld8(renc + (size_t)j * E + e0, f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sum += dv[i] * f[i];
-      }
-      sum = warp_sum(sum);
-      if (lane == 0) red[j * 8 + warp] = sum;
-    }
-  }
-  __syncthreads();
-  cluster_wait();
-  for (int j = tid; j < nr; j += kStThreads) {
-    const int s = r + C * j;
-    float sum = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sum += red[j * 8 + w];
-    sum += dacc[s];
-#pragma unroll
-    for (int p = 0; p < C; ++p) cl.map_shared_rank(da, p)[s] = sum;
-  }
-  cl.sync();
-  if (tid < 32) {  // softmax adjoint, in every CTA
+  if (tid < 32) {
     float dot = 0.f;
-    for (int s = lane; s < len; s += 32) dot += av[s] * da[s];
+    for (int s = lane; s < len; s += 32) dot += a.a_all[tb * Ts + s] * de[s];
     dot = warp_sum(dot);
+    __syncwarp();
     for (int s = lane; s < Ts; s += 32) {
-      const float d = s < len ? av[s] * (da[s] - dot) : 0.f;
+      const float d = s < len ? a.a_all[tb * Ts + s] * (de[s] - dot) : 0.f;
       de[s] = d;
-      if (r == 0) a.de_all[tb * Ts + s] = d;
+      if (blockIdx.x == 0) a.de_all[tb * Ts + s] = d;
     }
   }
   __syncthreads();
-  {  // tanh adjoint over this CTA's positions: two groups of 128 threads, 8 key columns each
-    const int g = tid / 128, q = tid % 128, wig = q / 32, k0 = q * 8;
-    const bool act = k0 < K;
-    float wv[8], cv[8], vk[8], ds[8];
-    if (act) {
-      const float* st = a.str_all + tb * K + k0;
-      const float4 s0v = ldf4(st), s1v = ldf4(st + 4);
-      const float sv[8] = {s0v.x, s0v.y, s0v.z, s0v.w, s1v.x, s1v.y, s1v.z, s1v.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ds[i] = 0.f;
+#pragma unroll
+  for (int p = 0; p < kPos; ++p) {
+    float pa = 0.f;
+    if (p < n && act) {
+      const float des = de[j0 + p];
+      float f[8];
+      unpack8(x[p], f);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        wv[i] = a.W_fb[k0 + i];
-        cv[i] = sv[i] + a.b_fb[k0 + i];
-        vk[i] = a.v[k0 + i];
+        const float uu = tanh_approx(f[i] + acp[p] * wv[i] + cv[i]);
+        const float dein = des * vk[i] * (1.f - uu * uu);
+        ds[i] += dein;
+        pa += wv[i] * dein;
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) wv[i] = cv[i] = vk[i] = 0.f;
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ds[i] = 0.f;
-    tc::mbar_wait(&bars[1], 0);
-    for (int j = g; j < nr; j += 2) {
-      const int s = r + C * j;
-      const float as = acc[s], des = de[s];
-      float pa = 0.f;
-      if (act) {
-        float f[8];
-        ld8(rctx + (size_t)j * K + k0, f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float uu = tanh_approx(f[i] + as * wv[i] + cv[i]);
-          const float dein = des * vk[i] * (1.f - uu * uu);
-          ds[i] += dein;
-          pa += wv[i] * dein;
-        }
-      }
-      pa = warp_sum(pa);
-      if (lane == 0) red[j * 8 + wig] = pa;  // (red reused: the d_a partials are consumed)
-    }
-    if (act) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dsum[g * K + k0 + i] = ds[i];
-    }
+    pa = warp_sum(pa);
+    if (lane == 0) red[p * 4 + warp] = pa;
+  }
+  if (act && n > 0) {
+    float* d = a.dsp + ((int64_t)b * a.nsc + blockIdx.x) * K + k0;
+    const float d0[4] = {ds[0], ds[1], ds[2], ds[3]}, d1[4] = {ds[4], ds[5], ds[6], ds[7]};
+    stf4(d, d0);
+    stf4(d + 4, d1);
   }
   __syncthreads();
-  for (int k = tid; k < K; k += kStThreads) pdst[k] = dsum[k] + dsum[K + k];
-  for (int s = r + C * tid; s < Ts; s += C * kStThreads) {
-    const int j = (s - r) / C;
-    a.dacc_out[(int64_t)b * Ts + s] =
-        s < len ? dacc[s] + (((red[j * 8] + red[j * 8 + 1]) + red[j * 8 + 2]) + red[j * 8 + 3]) : 0.f;
+  if (tid < n) {
+    const int s = j0 + tid;
+    a.dacc_out[(int64_t)b * Ts + s] = (a.dacc_in ? a.dacc_in[(int64_t)b * Ts + s] : 0.f) +
+                                      (((red[tid * 4] + red[tid * 4 + 1]) + red[tid * 4 + 2]) + red[tid * 4 + 3]);
   }
-  cl.sync();
-  if (r == 0) {
-    for (int k = tid; k < K; k += kStThreads) {
-      float d = pdst[k];
-#pragma unroll
-      for (int p = 1; p < C; ++p) d += cl.map_shared_rank(pdst, p)[k];
-      a.ds32[row * K + k] = d;
-      a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
-    }
-  }
-  cl.sync();  // the peers' shared memory stays alive until CTA 0 has read it
+  if (blockIdx.x == 0)
+    for (int s = len + tid; s < Ts; s += kAtt) a.dacc_out[(int64_t)b * Ts + s] = 0.f;
+}
+
+// d s_tr[b] = sum of the position-chunk partials in chunk order -> fp32 and the bf16 GEMM operand
+__global__ void dec_att_dstr_kernel(AttBwd a) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = a.b0 + blockIdx.y, k = blockIdx.x * 256 + threadIdx.x;
+  if (k >= a.K) return;
+  const int len = min(max(a.lens[b], 0), a.Ts);
+  const int nsc = (len + kPos - 1) / kPos;  // chunks that ran
+  float d = 0.f;
+  for (int q = 0; q < nsc; ++q) d += a.dsp[((int64_t)b * a.nsc + q) * a.K + k];
+  const int64_t row = (int64_t)a.t * a.B + b;
+  a.ds32[row * a.K + k] = d;
+  a.ds[row * a.pds + k] = __float2bfloat16_rn(d);
 }
 
 // ---- after the loop: the accumulations over t ----------------------------------------------
@@ -1171,12 +846,28 @@ int sm_count() {
   return n;
 }
 
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool off = getenv("SL_DEC_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 // split-K count for a batch-row GEMM (M <= 256 rows): fill the SM pairs, >= 4 K blocks per unit
 // (the value gemm_bf16_tc2 re-derives: no empty units)
-int ksplit_for(int M, int N, int K) {
+int ksplit_for(int M, int N, int K, int max_split = kMaxSplit) {
   const int tiles = (int)(ceil_div(M, 256) * ceil_div(N, 256));
   const int nk = (int)ceil_div(K, 64);
-  const int want = std::max(1, std::min(sm_count() / 2 / tiles, nk / 4));
+  const int want = std::max(1, std::min(std::min(sm_count() / 2 / tiles, nk / 4), max_split));
   return (int)ceil_div(nk, ceil_div(nk, want));
 }
 
@@ -1187,7 +878,7 @@ struct Lay {
   bf16 *wd2, *wtrg, *wstr, *wctx, *wro, *wtrgcat;
   bf16 *enc_ctx, *xa, *ro, *dz, *ds, *drob, *dctx;
   int32_t* ids_tm;
-  float *pre, *dtrg;
+  float *pre, *dtrg, *es, *dap, *dsp;
   float *xw, *pf, *pstr, *p1, *p2, *c_all, *gates, *str_all, *a_all, *acc_all, *de_all, *datt_all, *ds32, *dro,
       *dc, *dacc, *part, *colws, *tmp;
   void* emb_ws;
@@ -1206,7 +897,7 @@ Lay layout(const DecDims& d, void* base) {
   L.PRF = L.PRO;
   L.PDR = L.PZ + L.PR;
   L.ks_f = ksplit_for(d.B, 4 * d.H, d.E + d.H);
-  L.ks_s = ksplit_for(d.B, d.K, d.H);
+  L.ks_s = ksplit_for(d.B, d.K, d.H, 4);  // summed in the energy kernel (str_cols: at most 4)
   L.ks_1 = ksplit_for(d.B, d.E + d.H, 4 * d.H);
   L.ks_2 = ksplit_for(d.B, d.H, d.K);
   L.ctx_blocks = (int)(d.B * ceil_div(d.Ts, kCtxPos));
@@ -1237,6 +928,9 @@ Lay layout(const DecDims& d, void* base) {
   L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
   L.pre = tf(BT * d.Rd);
   L.dtrg = tf(BT * d.Emb);
+  L.es = tf((int64_t)d.B * d.Ts);
+  L.dap = tf((int64_t)d.B * ceil_div(d.E, kCols) * d.Ts);
+  L.dsp = tf((int64_t)d.B * ceil_div(d.Ts, kPos) * d.K);
   L.xw = tf(BT * 4 * d.H);
   L.pf = tf((int64_t)L.ks_f * d.B * 4 * d.H);
   L.pstr = tf((int64_t)L.ks_s * d.B * L.PK);
@@ -1275,56 +969,19 @@ TcGemm mk(int M, int N, int K, const bf16* A, int64_t lda, bool a_mn, const bf16
   TcGemm g{M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, 1.f, 0.f, nullptr};
   return g;
 }
-void gemm_split(TcGemm g, int ks, cudaStream_t st) {
+// split-K partials of a batch slice: partial z at C + z * stride (stride = full batch x ldc)
+void gemm_split(TcGemm g, int ks, int64_t stride, cudaStream_t st) {
   g.ksplit = ks;
-  g.split_stride = (int64_t)g.M * g.ldc;
+  g.split_stride = stride;
   gemm_bf16_tc(g, st);
 }
 
-size_t att_fwd_smem(const DecDims& d) { return (size_t)(6 * d.Ts + 4 + 1024) * 4; }
-size_t att_bwd_smem(const DecDims& d) { return (size_t)(5 * d.K + 13 * d.Ts) * 4; }
-
-template <int C, typename Args>
-void launch_cluster(void (*kern)(Args), int B, size_t smem, const Args& args, cudaStream_t st) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(C * B));
-  cfg.blockDim = dim3(kStThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args));
-}
-
-// cluster size of the TMA-staged attention kernels: the smallest C whose per-CTA
-// staging fits two CTAs per SM; 0 = the register-streaming kernels (or SL_DEC_ATT_REGS)
-int att_cluster(const DecDims& d) {
-  if (getenv("SL_DEC_ATT_REGS")) return 0;
-  if (d.E > 2 * 1024) return 0;
-  for (int C : {4, 8}) {
-    if (st_cols(d.E, C) > 512) continue;
-    const size_t need = std::max(FwdSt(d.Ts, d.K, d.E, C).total, BwdSt(d.Ts, d.K, d.E, C).total);
-    if (need <= 110 * 1024) return C;
-  }
-  return 0;
-}
 
 void configure() {  // opt in to > 48 KB dynamic shared memory once
   static bool done = false;
   if (done) return;
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_ctx_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_enc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_fwd_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_fwd_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-  SL_CUDA_TRY(cudaFuncSetAttribute(dec_attn_bwd_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
   const char* m = getenv("SL_DEC_TANH");
   const int mode = m ? atoi(m) : 0;
   SL_CUDA_TRY(cudaMemcpyToSymbol(c_tanh_mode, &mode, sizeof(int)));
@@ -1339,9 +996,9 @@ void decoder_check(const DecDims& d) {
              SL_ERR_SHAPE, "attn_decoder: dimensions must be positive, batch <= 256 per call");
   SL_REQUIRE(d.H % 8 == 0 && d.E % 8 == 0 && d.K % 8 == 0 && d.Rd % 8 == 0, SL_ERR_UNSUPPORTED,
              "attn_decoder: hidden, enc, key and readout dims must be multiples of 8");
-  SL_REQUIRE(d.K <= 1024 && d.E <= 2048 && d.Ts <= 1024 && d.T <= 1024 && (int64_t)d.T * d.Ts <= 48 * 1024,
+  SL_REQUIRE(d.K <= 1024 && d.E <= 4096 && d.Ts <= 1024 && d.T <= 1024 && (int64_t)d.T * d.Ts <= 48 * 1024,
              SL_ERR_UNSUPPORTED,
-             "attn_decoder: key_dim <= 1024, enc_dim <= 2048, src/trg time <= 1024, src*trg time <= 48K supported");
+             "attn_decoder: key_dim <= 1024, enc_dim <= 4096, src/trg time <= 1024, src*trg time <= 48K supported");
 }
 
 size_t decoder_workspace_bytes(const DecDims& d) { return layout(d, nullptr).bytes; }
@@ -1392,32 +1049,31 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
     gemm_bf16_tc(x, st);
   }
   ph.reset();
-  const int cell_threads = B * (H / 4);
-  const double att_bytes = 2.0 * B * d.Ts * (K + E);
-  const int ac = att_cluster(d);
+  ph.reset(new Phase(st, "k10_dec_fwd_steps",
+                     2.0 * BT * ((E + H) * 4 * H + H * K) + 2.0 * BT * d.Ts * (K + E)));
   for (int t = 0; t < T; ++t) {
-    if (t > 0) {
-      Phase p1(st, "k10_cell_gemm", 2.0 * B * (E + H) * 4 * H);
-      gemm_split(mk(B, 4 * H, E + H, L.xa + (int64_t)t * B * L.PXA, L.PXA, false, L.wd2, L.PZ, true, L.pf, 4 * H),
-                 L.ks_f, st);
+    {  // (the launches take a batch-row range [b0, b0 + nb): one range = the whole batch)
+      const int b0 = 0, nb = B;
+      cudaStream_t ss = st;
+      const int64_t r0 = (int64_t)t * B + b0;  // first time-major row of the slice at step t
+      if (t > 0)
+        gemm_split(mk(nb, 4 * H, E + H, L.xa + r0 * L.PXA, L.PXA, false, L.wd2, L.PZ, true, L.pf + (int64_t)b0 * 4 * H,
+                      4 * H),
+                   L.ks_f, (int64_t)B * 4 * H, ss);
+      CellFwd cf{B, T, H, E, t, t > 0 ? L.ks_f : 0, L.pf, 4 * H, (int64_t)B * 4 * H, L.xw, L.c_all, L.gates,
+                 L.xa, L.PXA, L.ro, L.PRO, b0, nb};
+      launch_pdl(dec_cell_fwd_kernel, dim3((unsigned)ceil_div(nb * (H / 4), 256)), dim3(256), 0, ss, cf);
+      gemm_split(mk(nb, K, H, L.ro + r0 * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr + (int64_t)b0 * L.PK, L.PK),
+                 L.ks_s, (int64_t)B * L.PK, ss);
+      AttFwd af{B, d.Ts, T, K, E, t, L.ks_s, src_lens, L.pstr, L.PK, (int64_t)B * L.PK, p.str_b, p.fb_W, p.fb_b,
+                p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.es, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO,
+                L.OA, L.xa, L.PXA, b0};
+      launch_pdl(dec_att_energy_kernel, dim3((unsigned)ceil_div(d.Ts, kPos), (unsigned)nb), dim3(kAtt), 0, ss, af);
+      launch_pdl(dec_att_context_kernel, dim3((unsigned)ceil_div(E, kCols), (unsigned)nb), dim3(kAtt * kGrp),
+                 (size_t)((d.Ts + 3) / 4 * 4 + (kGrp - 1) * kCols) * 4, ss, af);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch(3);
     }
-    ph.reset(new Phase(st, "k10_cell_fwd", 0.0, 4.0 * B * H * 16));
-    CellFwd cf{B, T, H, E, t, t > 0 ? L.ks_f : 0, L.pf, 4 * H, (int64_t)B * 4 * H, L.xw, L.c_all, L.gates,
-               L.xa, L.PXA, L.ro, L.PRO};
-    dec_cell_fwd_kernel<<<(unsigned)ceil_div(cell_threads, 256), 256, 0, st>>>(cf);
-    ph.reset(new Phase(st, "k10_str_gemm", 2.0 * B * H * K));
-    gemm_split(mk(B, K, H, L.ro + (int64_t)t * B * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr, L.PK),
-               L.ks_s, st);
-    AttFwd af{B, d.Ts, T, K, E, t, L.ks_s, src_lens, L.pstr, L.PK, (int64_t)B * L.PK, p.str_b, p.fb_W, p.fb_b,
-              p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO, L.OA,
-              L.xa, L.PXA};
-    ph.reset(new Phase(st, "k10_attn_fwd", 0.0, att_bytes));
-    if (ac == 4) launch_cluster<4>(dec_attn_fwd_tma_kernel<4>, B, FwdSt(d.Ts, K, E, 4).total, af, st);
-    else if (ac == 8) launch_cluster<8>(dec_attn_fwd_tma_kernel<8>, B, FwdSt(d.Ts, K, E, 8).total, af, st);
-    else dec_attn_fwd_kernel<<<2 * B, kAttThreads, att_fwd_smem(d), st>>>(af);
-    SL_CUDA_TRY(cudaGetLastError());
-    count_launch(2);
-    ph.reset();
   }
   ph.reset(new Phase(st, "k10_dec_fwd_hoisted", 2.0 * BT * (L.OA + E) * d.Rd));
   TcGemm r = mk((int)BT, d.Rd, L.OA + E, L.ro, L.PRO, false, L.wro, L.PR, true, L.pre, d.Rd);
@@ -1459,36 +1115,37 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   gemm_bf16_tc(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
                st);
   ph.reset();
-  const int cell_threads = B * (H / 4);
-  const double att_bytes = 2.0 * B * d.Ts * (K + E);
-  const int ac = att_cluster(d);
+  ph.reset(new Phase(st, "k10_dec_bwd_steps",
+                     2.0 * BT * ((E + H) * 4 * H + H * K) + 4.0 * BT * d.Ts * (K + E)));
+  const int nch = (int)ceil_div(E, kCols), nsc = (int)ceil_div(d.Ts, kPos);
   for (int t = T - 1; t >= 0; --t) {
     const bool last = t == T - 1;
-    if (!last) {
-      Phase p1(st, "k10_g1_gemm", 2.0 * B * (E + H) * 4 * H);
-      gemm_split(mk(B, E + H, 4 * H, L.dz + (int64_t)(t + 1) * B * L.PDR, L.PDR, false, L.wd2, L.PZ, false, L.p1,
-                    E + H),
-                 L.ks_1, st);
+    {
+      const int b0 = 0, nb = B;
+      cudaStream_t ss = st;
+      if (!last)
+        gemm_split(mk(nb, E + H, 4 * H, L.dz + ((int64_t)(t + 1) * B + b0) * L.PDR, L.PDR, false, L.wd2, L.PZ, false,
+                      L.p1 + (int64_t)b0 * (E + H), E + H),
+                   L.ks_1, (int64_t)B * (E + H), ss);
+      AttBwd ab{B, d.Ts, T, K, E, t, last ? 0 : L.ks_1, nch, nsc, src_lens, L.p1, E + H, (int64_t)B * (E + H), L.dro,
+                L.PRF, L.OA, p.fb_W, p.fb_b, p.e_W, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all,
+                last ? nullptr : L.dacc + (int64_t)((t + 1) % 2) * B * d.Ts, L.dacc + (int64_t)(t % 2) * B * d.Ts,
+                L.dap, L.dsp, L.datt_all, L.de_all, L.ds, L.PK, L.ds32, b0};
+      launch_pdl(dec_att_da_kernel, dim3((unsigned)nch, (unsigned)nb), dim3(kAtt * kGrp), (size_t)d.Ts * 16, ss, ab);
+      launch_pdl(dec_att_tanh_kernel, dim3((unsigned)nsc, (unsigned)nb), dim3(kAtt), (size_t)(d.Ts + 4 * kPos) * 4,
+                 ss, ab);
+      launch_pdl(dec_att_dstr_kernel, dim3((unsigned)ceil_div(K, 256), (unsigned)nb), dim3(256), 0, ss, ab);
+      gemm_split(mk(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, false, L.wstr, L.PK, false,
+                    L.p2 + (int64_t)b0 * L.PK, L.PK),
+                 L.ks_2, (int64_t)B * L.PK, ss);
+      CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PK,
+                 (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
+                 last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR,
+                 b0, nb};
+      launch_pdl(dec_cell_bwd_kernel, dim3((unsigned)ceil_div(nb * (H / 4), 256)), dim3(256), 0, ss, cb);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch(4);
     }
-    ph.reset(new Phase(st, "k10_attn_bwd", 0.0, att_bytes));
-    AttBwd ab{B, d.Ts, T, K, E, t, last ? 0 : L.ks_1, src_lens, L.p1, E + H, (int64_t)B * (E + H), L.dro, L.PRF,
-              L.OA, p.fb_W, p.fb_b, p.e_W, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all,
-              last ? nullptr : L.dacc + (int64_t)((t + 1) % 2) * B * d.Ts, L.dacc + (int64_t)(t % 2) * B * d.Ts,
-              L.datt_all, L.de_all, L.ds, L.PK, L.ds32};
-    if (ac == 4) launch_cluster<4>(dec_attn_bwd_tma_kernel<4>, B, BwdSt(d.Ts, K, E, 4).total, ab, st);
-    else if (ac == 8) launch_cluster<8>(dec_attn_bwd_tma_kernel<8>, B, BwdSt(d.Ts, K, E, 8).total, ab, st);
-    else dec_attn_bwd_kernel<<<2 * B, kAttThreads, att_bwd_smem(d), st>>>(ab);
-    ph.reset(new Phase(st, "k10_g2_gemm", 2.0 * B * H * K));
-    gemm_split(mk(B, H, K, L.ds + (int64_t)t * B * L.PK, L.PK, false, L.wstr, L.PK, false, L.p2, L.PK),
-               L.ks_2, st);
-    CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PK,
-               (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
-               last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR};
-    ph.reset(new Phase(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 20));
-    dec_cell_bwd_kernel<<<(unsigned)ceil_div(cell_threads, 256), 256, 0, st>>>(cb);
-    SL_CUDA_TRY(cudaGetLastError());
-    count_launch(2);
-    ph.reset();
   }
   ph.reset(new Phase(st, "k10_dec_bwd_hoisted",
                      2.0 * BT * 4 * H * (E + H + Emb + 1) + 2.0 * BT * Emb * 4 * H + 2.0 * BT * H * K));

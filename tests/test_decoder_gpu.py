@@ -115,17 +115,3 @@ def test_decoder_shape_errors(cuda):
     with pytest.raises(lstm.ShapeError):
         AttnDecoder(4, 7, 5, 12, 16, 8, 2000, 8, 11)  # key_dim > 1024
 
-
-def test_decoder_register_attention_kernels(cuda, monkeypatch):
-    """The register-streaming attention kernels (used when a row's operands do not fit
-    the TMA staging) agree with the restatement too."""
-    monkeypatch.setenv("SL_DEC_ATT_REGS", "1")
-    dims = CASES[1]
-    P, enc_x, lens, ids, d_ro = make_case(11, *dims)
-    ro, grads, d_enc = run_gpu(dims, P, enc_x, lens, ids, d_ro)
-    r_ro, g, r_denc = oracle.attn_decoder_np(lens, enc_x.float().numpy(), ids, P, d_readout=d_ro,
-                                             relu_mask=(ro > 0).cpu().numpy())
-    assert rel(ro, r_ro) < TOL and rel(d_enc, r_denc) < TOL
-    for n, _ in NAMES:
-        if n != "e_b":
-            assert rel(grads[n], g[n]) < TOL, n
