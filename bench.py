@@ -337,9 +337,9 @@ def run_ours(args, rank, world, local_rank):
     lib.sl_profile_enable(0)
     launches = (lib.sl_launch_count() - n0)
     ms = e0.elapsed_time(e1)
-    entries = (Entry * 32)()
-    n = lib.sl_profile_read(entries, 32, 1)
-    phases = {e.name.decode(): {"calls": e.calls, "ms": e.ms, "flops": e.flops}
+    entries = (Entry * 64)()
+    n = lib.sl_profile_read(entries, 64, 1)
+    phases = {e.name.decode(): {"calls": e.calls, "ms": e.ms, "flops": e.flops, "bytes": e.bytes}
               for e in entries[:n]}
     eager_ms = ms
     graph = None
@@ -487,21 +487,27 @@ def main():
     if top[0]:
         name, e = top
         per_launch_ms = e["ms"] / max(e["calls"], 1)
-        achieved = e["flops"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e12
-        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        hbm = e["flops"] == 0 and e.get("bytes", 0) > 0  # a bandwidth-bound phase
+        if hbm:
+            achieved = e["bytes"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e9
+            peak = peaks.get("hbm_gbs", 7700.0)
+        else:
+            achieved = e["flops"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e12
+            peak = peaks.get("bf16_tflops_sustained", 1400.0)
         traffic = None
         try:  # DRAM bytes per launch of this kernel from the committed ncu capture
             traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(name)
         except Exception:
             pass
-        roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+        roof = {"kernel": name, "bound": "hbm" if hbm else "tensor", "achieved": achieved, "peak": peak,
+                "unit": "GB/s" if hbm else "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)"
-                if peaks else "fallback 1400",
+                "peak_source": ("MEASURED_PEAKS.json " + ("hbm_gbs" if hbm else "bf16_tflops_sustained"))
+                if peaks else "fallback",
                 "share_of_step": e["ms"] / r["ms"],
                 "phases": {k: {"calls": v["calls"], "ms_per_call": v["ms"] / max(v["calls"], 1),
-                               "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+                               "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
+                               "gbs": v.get("bytes", 0) / max(v["ms"], 1e-9) / 1e6}
                            for k, v in ph.items()}}
     # recurrence phases: per-step latency against the W_h-from-SMEM bound the
     # north star names (bytes of W_h resident across the SMs / (SMs x 128 B/clk x f_SM))

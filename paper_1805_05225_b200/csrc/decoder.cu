@@ -1049,26 +1049,32 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
     gemm_bf16_tc(x, st);
   }
   ph.reset();
-  ph.reset(new Phase(st, "k10_dec_fwd_steps",
-                     2.0 * BT * ((E + H) * 4 * H + H * K) + 2.0 * BT * d.Ts * (K + E)));
+  ph.reset();
+  const double ctx_bytes = 2.0 * B * d.Ts * K, enc_bytes = 2.0 * B * d.Ts * E;  // per step, bf16 enc_ctx / enc
   for (int t = 0; t < T; ++t) {
     {  // (the launches take a batch-row range [b0, b0 + nb): one range = the whole batch)
       const int b0 = 0, nb = B;
       cudaStream_t ss = st;
       const int64_t r0 = (int64_t)t * B + b0;  // first time-major row of the slice at step t
-      if (t > 0)
+      if (t > 0) {
+        Phase q(ss, "k10_cell_gemm", 2.0 * nb * (E + H) * 4 * H);
         gemm_split(mk(nb, 4 * H, E + H, L.xa + r0 * L.PXA, L.PXA, false, L.wd2, L.PZ, true, L.pf + (int64_t)b0 * 4 * H,
                       4 * H),
                    L.ks_f, (int64_t)B * 4 * H, ss);
+      }
+      std::unique_ptr<Phase> q(new Phase(ss, "k10_cell_fwd", 0.0, 4.0 * nb * H * (4 * L.ks_f + 12)));
       CellFwd cf{B, T, H, E, t, t > 0 ? L.ks_f : 0, L.pf, 4 * H, (int64_t)B * 4 * H, L.xw, L.c_all, L.gates,
                  L.xa, L.PXA, L.ro, L.PRO, b0, nb};
       launch_pdl(dec_cell_fwd_kernel, dim3((unsigned)ceil_div(nb * (H / 4), 256)), dim3(256), 0, ss, cf);
+      q.reset(new Phase(ss, "k10_str_gemm", 2.0 * nb * H * K));
       gemm_split(mk(nb, K, H, L.ro + r0 * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr + (int64_t)b0 * L.PK, L.PK),
                  L.ks_s, (int64_t)B * L.PK, ss);
       AttFwd af{B, d.Ts, T, K, E, t, L.ks_s, src_lens, L.pstr, L.PK, (int64_t)B * L.PK, p.str_b, p.fb_W, p.fb_b,
                 p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.es, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO,
                 L.OA, L.xa, L.PXA, b0};
+      q.reset(new Phase(ss, "k10_att_energy", 0.0, ctx_bytes));
       launch_pdl(dec_att_energy_kernel, dim3((unsigned)ceil_div(d.Ts, kPos), (unsigned)nb), dim3(kAtt), 0, ss, af);
+      q.reset(new Phase(ss, "k10_att_context", 0.0, enc_bytes));
       launch_pdl(dec_att_context_kernel, dim3((unsigned)ceil_div(E, kCols), (unsigned)nb), dim3(kAtt * kGrp),
                  (size_t)((d.Ts + 3) / 4 * 4 + (kGrp - 1) * kCols) * 4, ss, af);
       SL_CUDA_TRY(cudaGetLastError());
@@ -1115,26 +1121,33 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   gemm_bf16_tc(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
                st);
   ph.reset();
-  ph.reset(new Phase(st, "k10_dec_bwd_steps",
-                     2.0 * BT * ((E + H) * 4 * H + H * K) + 4.0 * BT * d.Ts * (K + E)));
+  ph.reset();
+  const double ctx_bytes = 2.0 * B * d.Ts * K, enc_bytes = 2.0 * B * d.Ts * E;
   const int nch = (int)ceil_div(E, kCols), nsc = (int)ceil_div(d.Ts, kPos);
   for (int t = T - 1; t >= 0; --t) {
     const bool last = t == T - 1;
     {
       const int b0 = 0, nb = B;
       cudaStream_t ss = st;
-      if (!last)
+      std::unique_ptr<Phase> q;
+      if (!last) {
+        q.reset(new Phase(ss, "k10_g1_gemm", 2.0 * nb * (E + H) * 4 * H));
         gemm_split(mk(nb, E + H, 4 * H, L.dz + ((int64_t)(t + 1) * B + b0) * L.PDR, L.PDR, false, L.wd2, L.PZ, false,
                       L.p1 + (int64_t)b0 * (E + H), E + H),
                    L.ks_1, (int64_t)B * (E + H), ss);
+      }
       AttBwd ab{B, d.Ts, T, K, E, t, last ? 0 : L.ks_1, nch, nsc, src_lens, L.p1, E + H, (int64_t)B * (E + H), L.dro,
                 L.PRF, L.OA, p.fb_W, p.fb_b, p.e_W, L.enc_ctx, L.PK, enc, ld_enc, L.str_all, L.a_all, L.acc_all,
                 last ? nullptr : L.dacc + (int64_t)((t + 1) % 2) * B * d.Ts, L.dacc + (int64_t)(t % 2) * B * d.Ts,
                 L.dap, L.dsp, L.datt_all, L.de_all, L.ds, L.PK, L.ds32, b0};
+      q.reset(new Phase(ss, "k10_att_da", 0.0, enc_bytes));
       launch_pdl(dec_att_da_kernel, dim3((unsigned)nch, (unsigned)nb), dim3(kAtt * kGrp), (size_t)d.Ts * 16, ss, ab);
+      q.reset(new Phase(ss, "k10_att_tanh", 0.0, ctx_bytes));
       launch_pdl(dec_att_tanh_kernel, dim3((unsigned)nsc, (unsigned)nb), dim3(kAtt), (size_t)(d.Ts + 4 * kPos) * 4,
                  ss, ab);
+      q.reset(new Phase(ss, "k10_att_dstr", 0.0, 4.0 * nb * K * (nsc + 2)));
       launch_pdl(dec_att_dstr_kernel, dim3((unsigned)ceil_div(K, 256), (unsigned)nb), dim3(256), 0, ss, ab);
+      q.reset(new Phase(ss, "k10_g2_gemm", 2.0 * nb * H * K));
       gemm_split(mk(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, false, L.wstr, L.PK, false,
                     L.p2 + (int64_t)b0 * L.PK, L.PK),
                  L.ks_2, (int64_t)B * L.PK, ss);
@@ -1142,6 +1155,7 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
                  (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
                  last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR,
                  b0, nb};
+      q.reset(new Phase(ss, "k10_cell_bwd", 0.0, 4.0 * nb * H * (4 * L.ks_1 + 4 * L.ks_2 + 16)));
       launch_pdl(dec_cell_bwd_kernel, dim3((unsigned)ceil_div(nb * (H / 4), 256)), dim3(256), 0, ss, cb);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch(4);
