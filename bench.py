@@ -1,18 +1,19 @@
 """Benchmark of the BASELINE.json metric on B200.
 
 Metric: "LSTM fwd+bwd target tokens/sec (6xBLSTM n=1000, T=60) at 1/2/4/8 B200
-vs CPU" (BASELINE.json), on configs[3] — the Listing-1 training step — as far
-as it is wired: one step = the source / target embedding lookups (V = 20K
-each; width 620, models.hpp:14) from token ids, forward + backward
-(BPTT) of the 6-layer bidirectional LSTM encoder (H = 1000) and the 1-layer
-LSTM decoder (H = 1000, input [620-wide previous-target embedding ‖ 2000-wide
-context], models.cpp:161), the output softmax layer (V = 20K) with the
-label-smoothed CE loss, T_src = T_tgt = 60, then the fused global-norm clip +
-Adam step over all parameters, plus at N > 1 the data-parallel NCCL gradient
-all-reduce overlapped with BPTT.  The MLP attention is built
-and measured standalone (scripts/bench_attention.py) but not in this step:
-the decoder's context input is the encoder output at the same position
-(model.py).  tokens = target (sequence, time) positions.
+vs CPU" (BASELINE.json), on configs[3] — the Listing-1 attention model's
+training step (make_attention_model, models.cpp:26-184): source / target
+embedding lookups (V = 20K each; width 620, models.hpp:14) from
+token ids, forward + backward of the 6-layer bidirectional LSTM encoder
+(H = 1000), enc_ctx, the `output` subnetwork run step by step with teacher
+forcing (the LSTM decoder cell with input feeding of the previous attention,
+the MLP attention with weight feedback, the relu readout; decoder.py), the
+output softmax layer (V = 20K) with the label-smoothed CE loss, T_src = T_tgt
+= 60, then the fused global-norm clip + Adam step over all parameters, plus at
+N > 1 the data-parallel NCCL gradient all-reduce overlapped with BPTT.
+--no-attention runs the earlier step without attention (decoder context = the
+encoder output at the same position).  tokens = target (sequence, time)
+positions.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
