@@ -286,11 +286,11 @@ __device__ __forceinline__ void str_cols(const float* P, int nsplit, int64_t p_s
   constexpr int kMaxStr = 4;  // the s_tr GEMM's split count (ksplit_for(..., 4))
   float4 u[kMaxStr][2];
 #pragma unroll
-  for (int z = 0; z < kMaxStr; ++z)
-    if (z < nsplit) {
-      u[z][0] = ldf4(P + z * p_stride + k0);
-      u[z][1] = ldf4(P + z * p_stride + k0 + 4);
-    }
+  for (int z = 0; z < kMaxStr; ++z) {  // unconditional (clamped) loads: all in flight together
+    const int zc = max(min(z, nsplit - 1), 0);
+    u[z][0] = ldf4(P + zc * p_stride + k0);
+    u[z][1] = ldf4(P + zc * p_stride + k0 + 4);
+  }
   const float4 b0 = ldf4(bias + k0), b1 = ldf4(bias + k0 + 4);
   st[0] = b0.x, st[1] = b0.y, st[2] = b0.z, st[3] = b0.w, st[4] = b1.x, st[5] = b1.y, st[6] = b1.z, st[7] = b1.w;
 #pragma unroll
@@ -310,12 +310,13 @@ __global__ void __launch_bounds__(kAtt, 6) dec_att_energy_kernel(AttFwd a) {
   const int lane = tid % 32, warp = tid / 32, k0 = tid * 8;
   const bool act = k0 < K;
   const size_t tb = (size_t)a.t * a.B + b;
-  uint4 x[kPos];  // rows j0.. exist for every j0 < Ts: load before knowing which are valid
+  // Unconditional loads from clamped (always valid) addresses, masked when consumed: a
+  // `cond ? load : 0` select makes the compiler retire each load before issuing the next.
+  uint4 x[kPos];
+  const int kc = act ? k0 : 0;
 #pragma unroll
-  for (int p = 0; p < kPos; ++p) {
-    const int s = min(j0 + p, Ts - 1);
-    x[p] = act ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0) : make_uint4(0, 0, 0, 0);
-  }
+  for (int p = 0; p < kPos; ++p)
+    x[p] = *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + min(j0 + p, Ts - 1)) * a.pk + kc);
   const int len = min(max(a.lens[b], 0), Ts);
   float4 f0, f1, w0, w1, v0, v1;
   if (act) f0 = ldf4(a.b_fb + k0), f1 = ldf4(a.b_fb + k0 + 4), w0 = ldf4(a.W_fb + k0), w1 = ldf4(a.W_fb + k0 + 4),
@@ -364,7 +365,10 @@ __device__ __forceinline__ void row_softmax(const float* e, int len, int Ts, flo
   const int lane = threadIdx.x % 32;
   float r[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) r[i] = lane + 32 * i < len ? e[lane + 32 * i] : -INFINITY;
+  for (int i = 0; i < 4; ++i) r[i] = lane + 32 * i < Ts ? e[lane + 32 * i] : 0.f;  // (no wait on len)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (lane + 32 * i >= len) r[i] = -INFINITY;
   float m = fmaxf(fmaxf(r[0], r[1]), fmaxf(r[2], r[3]));
   for (int s = lane + 128; s < len; s += 32) m = fmaxf(m, e[s]);
   m = warp_max(m);
@@ -404,12 +408,11 @@ __global__ void __launch_bounds__(kAtt * kGrp, 2) dec_att_context_kernel(AttFwd 
   const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + c;
   float o[4] = {0.f, 0.f, 0.f, 0.f};
   uint2 raw[kPerGrp];
+  const bf16* xc = on ? x : x - c;  // unconditional loads from clamped rows / columns, masked when consumed
   auto load = [&](int s0) {
 #pragma unroll
-    for (int u = 0; u < kPerGrp; ++u) {
-      const int s = s0 + kGrp * u;
-      raw[u] = (on && s < len) ? *reinterpret_cast<const uint2*>(x + (int64_t)s * a.ld_enc) : make_uint2(0, 0);
-    }
+    for (int u = 0; u < kPerGrp; ++u)
+      raw[u] = *reinterpret_cast<const uint2*>(xc + (int64_t)min(s0 + kGrp * u, Ts - 1) * a.ld_enc);
   };
   load(g);    // the first batch of encoder rows is in flight before the wait ...
   pdl_wait();  // ... for the energies of this step
@@ -482,21 +485,25 @@ __global__ void __launch_bounds__(kAtt * kGrp, 2) dec_att_da_kernel(AttBwd a) {
   const int len = min(max(a.lens[b], 0), Ts);
   const bf16* x = a.enc + (int64_t)b * Ts * a.ld_enc + c;
   uint2 raw[kPerGrpDa];
+  const bf16* xc = on ? x : x - c;  // unconditional clamped loads (see the context kernel)
   auto load = [&](int s0) {
 #pragma unroll
-    for (int u = 0; u < kPerGrpDa; ++u) {
-      const int s = s0 + kGrp * u;
-      raw[u] = (on && s < len) ? *reinterpret_cast<const uint2*>(x + (int64_t)s * a.ld_enc) : make_uint2(0, 0);
-    }
+    for (int u = 0; u < kPerGrpDa; ++u)
+      raw[u] = *reinterpret_cast<const uint2*>(xc + (int64_t)min(s0 + kGrp * u, Ts - 1) * a.ld_enc);
   };
   load(g);     // the first batch of encoder rows is in flight before the wait ...
   pdl_wait();  // ... for d att_t (G1 partials)
   float dv[4] = {0.f, 0.f, 0.f, 0.f};
   if (on) {
     addf4(dv, ldf4(a.dro + row * a.prf + a.oa + c));
+    if (a.n1 > 0) {
+      float4 u[kMaxSplit];  // unconditional (clamped) loads: all in flight together
 #pragma unroll
-    for (int z = 0; z < kMaxSplit; ++z)
-      if (z < a.n1) addf4(dv, ldf4(a.P1 + z * a.p1_stride + (int64_t)b * a.p1_ld + c));
+      for (int z = 0; z < kMaxSplit; ++z) u[z] = ldf4(a.P1 + min(z, a.n1 - 1) * a.p1_stride + (int64_t)b * a.p1_ld + c);
+#pragma unroll
+      for (int z = 0; z < kMaxSplit; ++z)
+        if (z < a.n1) addf4(dv, u[z]);
+    }
     if (g == 0) stf4(a.datt_all + tb * a.E + c, dv);
   }
   for (int s0 = g; s0 < len; s0 += kGrp * kPerGrpDa) {
@@ -520,38 +527,36 @@ __global__ void __launch_bounds__(kAtt * kGrp, 2) dec_att_da_kernel(AttBwd a) {
 // d_a partials), then for 8 positions d e_in = de v (1 - u^2): this chunk's d s_tr
 // partial and d accum_{t-1} = d accum_t + d e_in W_fb
 __global__ void __launch_bounds__(kAtt, 6) dec_att_tanh_kernel(AttBwd a) {
-  extern __shared__ float sm[];  // de[Ts], then red[kPos][4]
+  extern __shared__ float sm[];  // de[Ts], a[Ts], then red[kPos][4]
   pdl_trigger();
   float* de = sm;
-  float* red = sm + a.Ts;
+  float* as_ = sm + a.Ts;
+  float* red = sm + 2 * a.Ts;
   const int b = a.b0 + blockIdx.y, j0 = blockIdx.x * kPos, Ts = a.Ts, K = a.K, tid = threadIdx.x;
   const int lane = tid % 32, warp = tid / 32, k0 = tid * 8;
   const size_t tb = (size_t)a.t * a.B + b;
   const bool act = k0 < K;
-  uint4 x[kPos];
+  uint4 x[kPos];  // unconditional clamped loads (see the energy kernel)
+  const int kc = act ? k0 : 0;
 #pragma unroll
-  for (int p = 0; p < kPos; ++p) {
-    const int s = min(j0 + p, Ts - 1);
-    x[p] = act ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s) * a.pk + k0) : make_uint4(0, 0, 0, 0);
-  }
+  for (int p = 0; p < kPos; ++p)
+    x[p] = *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + min(j0 + p, Ts - 1)) * a.pk + kc);
   const int len = min(max(a.lens[b], 0), Ts);
   pdl_wait();  // d_a partials (previous kernel) and the step's saves from here on
   float acp[kPos];
 #pragma unroll
   for (int p = 0; p < kPos; ++p) acp[p] = a.acc_all[tb * Ts + min(j0 + p, Ts - 1)];
   for (int s = tid; s < Ts; s += kAtt) {  // d_a = sum of the column-chunk partials + d accum_t
+    float u[kMaxSplit];  // unconditional (clamped) loads, masked below
+#pragma unroll
+    for (int h = 0; h < kMaxSplit; ++h) u[h] = a.dap[((int64_t)b * a.nch + min(h, a.nch - 1)) * Ts + s];
+    const float dacc = a.dacc_in ? a.dacc_in[(int64_t)b * Ts + s] : 0.f;
+    as_[s] = a.a_all[tb * Ts + s];
     float d = 0.f;
-    if (s < len) {
-      float u[kMaxSplit];
 #pragma unroll
-      for (int h = 0; h < kMaxSplit; ++h)
-        if (h < a.nch) u[h] = a.dap[((int64_t)b * a.nch + h) * Ts + s];
-#pragma unroll
-      for (int h = 0; h < kMaxSplit; ++h)
-        if (h < a.nch) d += u[h];
-      if (a.dacc_in) d += a.dacc_in[(int64_t)b * Ts + s];
-    }
-    de[s] = d;
+    for (int h = 0; h < kMaxSplit; ++h)
+      if (h < a.nch) d += u[h];
+    de[s] = s < len ? d + dacc : 0.f;
   }
   float st[8], wv[8], cv[8], vk[8], ds[8];
   if (act) {
@@ -572,11 +577,11 @@ __global__ void __launch_bounds__(kAtt, 6) dec_att_tanh_kernel(AttBwd a) {
   __syncthreads();
   if (tid < 32) {
     float dot = 0.f;
-    for (int s = lane; s < len; s += 32) dot += a.a_all[tb * Ts + s] * de[s];
+    for (int s = lane; s < len; s += 32) dot += as_[s] * de[s];
     dot = warp_sum(dot);
     __syncwarp();
     for (int s = lane; s < Ts; s += 32) {
-      const float d = s < len ? a.a_all[tb * Ts + s] * (de[s] - dot) : 0.f;
+      const float d = s < len ? as_[s] * (de[s] - dot) : 0.f;
       de[s] = d;
       if (blockIdx.x == 0) a.de_all[tb * Ts + s] = d;
     }
@@ -1143,7 +1148,7 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
       q.reset(new Phase(ss, "k10_att_da", 0.0, enc_bytes));
       launch_pdl(dec_att_da_kernel, dim3((unsigned)nch, (unsigned)nb), dim3(kAtt * kGrp), (size_t)d.Ts * 16, ss, ab);
       q.reset(new Phase(ss, "k10_att_tanh", 0.0, ctx_bytes));
-      launch_pdl(dec_att_tanh_kernel, dim3((unsigned)nsc, (unsigned)nb), dim3(kAtt), (size_t)(d.Ts + 4 * kPos) * 4,
+      launch_pdl(dec_att_tanh_kernel, dim3((unsigned)nsc, (unsigned)nb), dim3(kAtt), (size_t)(2 * d.Ts + 4 * kPos) * 4,
                  ss, ab);
       q.reset(new Phase(ss, "k10_att_dstr", 0.0, 4.0 * nb * K * (nsc + 2)));
       launch_pdl(dec_att_dstr_kernel, dim3((unsigned)ceil_div(K, 256), (unsigned)nb), dim3(256), 0, ss, ab);
