@@ -677,17 +677,20 @@ __global__ void __launch_bounds__(128) dec_ctx_grad_kernel(CtxGrad a) {
     vk[i] = act ? a.v[k0 + i] : 0.f;
     dw[i] = db[i] = dv[i] = 0.f;
   }
+  const int kc = act ? k0 : 0;
 #pragma unroll
-  for (int p = 0; p < kCtxPos; ++p) {
-    x[p] = (act && p < n) ? *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + s0 + p) * a.pk + k0)
-                          : make_uint4(0, 0, 0, 0);
+  for (int p = 0; p < kCtxPos; ++p) {  // unconditional clamped loads (masked by des = 0 below)
+    x[p] = *reinterpret_cast<const uint4*>(a.enc_ctx + ((int64_t)b * Ts + min(s0 + p, Ts - 1)) * a.pk + kc);
 #pragma unroll
     for (int i = 0; i < 8; ++i) dc[p][i] = 0.f;
   }
   if (act && n > 0) {
+    const float* str = a.str_all + (size_t)b * K + k0;
+    const size_t tstride = (size_t)a.B * K;
+    float4 n0 = ldf4(str), n1 = ldf4(str + 4);  // s_tr of step t + 1 in flight while step t computes
     for (int t = 0; t < T; ++t) {
-      const float* st = a.str_all + ((size_t)t * a.B + b) * K + k0;
-      const float4 s0v = ldf4(st), s1v = ldf4(st + 4);
+      const float4 s0v = n0, s1v = n1;
+      if (t + 1 < T) n0 = ldf4(str + (t + 1) * tstride), n1 = ldf4(str + (t + 1) * tstride + 4);
       const float sv[8] = {s0v.x + bv[0], s0v.y + bv[1], s0v.z + bv[2], s0v.w + bv[3],
                            s1v.x + bv[4], s1v.y + bv[5], s1v.z + bv[6], s1v.w + bv[7]};
 #pragma unroll
@@ -756,8 +759,12 @@ __global__ void __launch_bounds__(128) dec_enc_grad_kernel(int B, int Ts, int T,
   float o[kEncPos][4];
 #pragma unroll
   for (int s = 0; s < kEncPos; ++s) o[s][0] = o[s][1] = o[s][2] = o[s][3] = 0.f;
+  const float* dp = datt_all + (size_t)b * E + e;
+  const size_t tstride = (size_t)B * E;
+  float4 nd = ldf4(dp);  // d att of step t + 1 in flight while step t accumulates
   for (int t = 0; t < T; ++t) {
-    const float4 d = ldf4(datt_all + ((size_t)t * B + b) * E + e);
+    const float4 d = nd;
+    if (t + 1 < T) nd = ldf4(dp + (t + 1) * tstride);
     const float4* at = reinterpret_cast<const float4*>(sa + t * kEncPos);
 #pragma unroll
     for (int q = 0; q < kEncPos / 4; ++q) {
