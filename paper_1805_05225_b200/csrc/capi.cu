@@ -850,6 +850,10 @@ extern "C" int sl_debug_gemm_bf16_split(int M, int N, int K, const void* A, int6
   });
 }
 
+extern "C" int sl_debug_gemm_trace(unsigned long long* dev_buf) {
+  return guarded([&] { gemm_tc2_set_trace(dev_buf); });
+}
+
 extern "C" int sl_debug_set_trace(unsigned long long* dev_buf, int cta) {
   g_rec_trace = dev_buf;
   g_rec_trace_cta = cta;

@@ -64,5 +64,7 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 // when the operands allow (gemm_bf16_tc2_ok) unless SL_GEMM_1CTA is set.
 bool gemm_bf16_tc2_ok(const TcGemm& g);
 void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream);
+// debug: per-CTA timeline stamps of the pair GEMM into buf (null: off)
+void gemm_tc2_set_trace(unsigned long long* buf);
 
 }  // namespace sl

@@ -28,7 +28,8 @@ namespace {
 constexpr int BMP = 256, BNP = 256, BK = 64, kStages = 6, kEpiWarps = 8, kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kHalf = 128 * 64 * 2;  // 16 KB: 128 rows (or cols) x 64 K of bf16
 constexpr uint32_t kStage = 2 * kHalf;    // A half + B half per CTA
-constexpr uint32_t kSmem = kStages * kStage + 1024;
+constexpr uint32_t kEpiTile = 32 * 33 * 4;  // per epilogue warp: a 32 x 32 fp32 staging tile (+1 pad)
+constexpr uint32_t kSmem = kStages * kStage + kEpiWarps * kEpiTile + 1024;
 
 struct P2 {
   int M, N, K, nm, nn, nk;
@@ -41,6 +42,8 @@ struct P2 {
   int64_t ldc2;
   __nv_bfloat16* Cb;
   int skip_epi;  // experiments only: load the accumulator but store nothing (wrong results)
+  int stage_epi;  // one work unit per CTA pair and a plain fp32 output: stage the epilogue through
+                  // shared memory so every warp store covers 128 contiguous bytes of one row
   float4* sm_part;  // softmax partials (gemm.h TcGemm::sm_part)
   int sm_ld;
   const int32_t* sm_targets;
@@ -113,6 +116,20 @@ __device__ __forceinline__ void arrive_remote(uint32_t bar_cl, uint32_t count) {
                : "memory");
 }
 
+// debug timeline (sl_debug_gemm_trace): per CTA 8 globaltimer stamps (entry, after the
+// prologue, first TMA issued, last MMA committed, accumulator ready in the epilogue,
+// epilogue done, final cluster sync, TMEM released)
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GT(i)                                                           \
+  do {                                                                  \
+    if (g_gemm_trace) g_gemm_trace[(size_t)blockIdx.x * 8 + (i)] = gtimer(); \
+  } while (0)
+
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -127,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   const bool leader = r == 0;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
+  if (threadIdx.x == 0) GT(0);
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -149,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   tc::fence_before_sync();
   __syncthreads();
   cluster_sync_all();
+  if (threadIdx.x == 0) GT(1);
   tc::fence_after_sync();
   const uint32_t tmem = tmem_sh;
   const int ntiles = p.nm * p.nn * p.ksplit;  // work units
@@ -169,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           const int k0 = kb * BK;
           if (A_MN) tma3d_pair(sa, &tmA, fb, 0, k0, m0 / 64);
           else tma2d_pair(sa, &tmA, fb, k0, m0);
+          if (kb == kb0 && t == pair) GT(2);
           if (B_MN) tma3d_pair(sb, &tmB, fb, 0, k0, n0 / 64);
           else tma2d_pair(sb, &tmB, fb, k0, n0);
           if (++st == kStages) {
@@ -209,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           }
         }
         commit_pair(&tfull_bar[acc]);
+        GT(3);
       }
     }
   } else {  // ---------------- epilogue (warps 2..9 -> TMEM lane quarters 2,3,0,1, x2 column halves)
@@ -223,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       unit_kb(p, t, tile, kb0, kb1, z);
       const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP;
       tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      if (warp == 2 && lane == 0 && it == 0) GT(4);
       tc::fence_after_sync();
       const int row = m0 + 32 * q + lane;
       const bool second = row >= p.m_split;
@@ -307,8 +329,36 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 make_float4(sm_m, sm_s, sm_t, sm_y);
           continue;
         }
+        if (p.stage_epi) {  // (uniform) transpose through shared memory: row-contiguous stores
+          float* tile = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + kStages * kStage +
+                                                 (warp - 2) * kEpiTile);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = v[j];  // bank (lane + j) % 32: conflict-free
+          __syncwarp();
+          const int rbase = m0 + 32 * q;
+          float* cz = p.C + z * p.split_stride + col0 + lane;
+          const bool colok = col0 + lane < p.N;
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr)
+            if (colok && rbase + rr < p.M) cz[(int64_t)(rbase + rr) * p.ldc] = p.alpha * tile[rr * 33 + lane];
+          __syncwarp();
+          continue;
+        }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
-        if (vec && col0 + 32 <= p.N) {
+        if (vec && col0 + 32 <= p.N && p.beta == 0.f && !p.bias && (p.ldc % 8) == 0 &&
+            ((uintptr_t)crow & 31) == 0) {
+          // plain fp32 tile (split-K partials, plain outputs): 32 B vector stores — full
+          // sectors and half the store requests of float4 (the epilogue is request-bound)
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            float* dst = crow + col0 + j;
+            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst),
+                         "f"(p.alpha * v[j]), "f"(p.alpha * v[j + 1]), "f"(p.alpha * v[j + 2]),
+                         "f"(p.alpha * v[j + 3]), "f"(p.alpha * v[j + 4]), "f"(p.alpha * v[j + 5]),
+                         "f"(p.alpha * v[j + 6]), "f"(p.alpha * v[j + 7])
+                         : "memory");
+          }
+        } else if (vec && col0 + 32 <= p.N) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             float4 o = make_float4(p.alpha * v[j], p.alpha * v[j + 1], p.alpha * v[j + 2],
@@ -343,13 +393,16 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) arrive_remote(tempty_leader[acc], 32);  // release the accumulator (leader's barrier)
+      if (warp == 2 && lane == 0) GT(5);
     }
   }
   tc::fence_before_sync();
   __syncthreads();
   cluster_sync_all();  // the peer's MMAs / arrivals are done before TMEM goes away
+  if (threadIdx.x == 0) GT(6);
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if (lane == 0) GT(7);
   }
 }
 
@@ -416,6 +469,10 @@ void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream
 
 }  // namespace
 
+void gemm_tc2_set_trace(unsigned long long* buf) {
+  SL_CUDA_TRY(cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf)));
+}
+
 int gemm_tc2_ksplit(int M, int N, int K) {
   const int tiles = (int)(ceil_div(M, BMP) * ceil_div(N, BNP));
   const int nk = (int)ceil_div(K, BK);
@@ -469,6 +526,13 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   // bulk-tensor output stores when the output is written (not accumulated) and
   // its rows are 16 B aligned; the per-row path stays for beta != 0
   p.skip_epi = getenv("SL_GEMM_SKIP_EPI") != nullptr;
+  {
+    const int units = p.nm * p.nn * p.ksplit;
+    static const bool no_stage = getenv("SL_GEMM_NO_STAGED_EPI") != nullptr;
+    // measured slower than the 32 B vector stores at the decoder's shapes: opt-in only
+    p.stage_epi = getenv("SL_GEMM_STAGED_EPI") != nullptr && !no_stage && units <= sms2() / 2 && !g.Cb &&
+                  g.beta == 0.f && !g.bias && g.m_split >= g.M && g.C != nullptr;
+  }
   p.sm_part = g.sm_part;
   p.sm_ld = g.sm_ld;
   p.sm_targets = g.sm_targets;
