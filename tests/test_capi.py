@@ -107,3 +107,22 @@ def test_bf16_activation_flags():
     assert 0 < r1 <= r0 - 64 * 30 * 256 * 2
     for f in (1, 7, 64, 199, 2000):
         assert L.sl_lstm_bf16_pitch(f) == lstm.bf16_pitch(f) == (f + 64) // 64 * 64
+
+
+def test_attn_decoder_descriptor_validation():
+    """sl_attn_decoder_workspace_size: host-only shape checks (0 + sl_last_error on bad dims)."""
+    from paper_1805_05225_b200.decoder import _Desc
+    L = lstm.lib()
+    L.sl_attn_decoder_workspace_size.restype = ctypes.c_size_t
+    L.sl_attn_decoder_workspace_size.argtypes = [ctypes.POINTER(_Desc)]
+    ok = _Desc(256, 60, 60, 620, 2000, 1000, 1000, 1000, 20000)
+    n = L.sl_attn_decoder_workspace_size(ctypes.byref(ok))
+    assert n > 0
+    small = _Desc(4, 7, 5, 12, 16, 8, 16, 8, 11)
+    assert 0 < L.sl_attn_decoder_workspace_size(ctypes.byref(small)) < n
+    for bad, needle in ((_Desc(4, 7, 5, 12, 16, 8, 2000, 8, 11), b"key_dim <= 1024"),
+                        (_Desc(4, 7, 5, 12, 16, 9, 16, 8, 11), b"multiples of 8"),
+                        (_Desc(0, 7, 5, 12, 16, 8, 16, 8, 11), b"positive"),
+                        (_Desc(300, 7, 5, 12, 16, 8, 16, 8, 11), b"batch <= 256")):
+        assert L.sl_attn_decoder_workspace_size(ctypes.byref(bad)) == 0
+        assert needle in L.sl_last_error()
