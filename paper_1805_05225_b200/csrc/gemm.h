@@ -53,7 +53,8 @@ struct TcGemm {
   int sm_ld = 0;
   const int32_t* sm_targets = nullptr;
   // optional (pair GEMM only): split K into ksplit ranges; range z writes its plain
-  // fp32 partial product (alpha = 1, no bias / beta / C2) to C + z * split_stride
+  // partial product (alpha = 1, no bias / beta / C2) to C + z * split_stride (fp32) or,
+  // with Cb, to Cb + z * split_stride (bf16)
   int ksplit = 1;
   int64_t split_stride = 0;
 };

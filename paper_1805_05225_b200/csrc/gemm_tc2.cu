@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
         if (p.Cb) {
           if (row >= p.M) continue;
-          __nv_bfloat16* brow = p.Cb + (int64_t)row * p.ldc + col0;
+          __nv_bfloat16* brow = p.Cb + z * p.split_stride + (int64_t)row * p.ldc + col0;
           if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
             const bool bvec = p.bias && ((uintptr_t)(p.bias + col0) & 15) == 0;
 #pragma unroll
@@ -510,8 +510,8 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   p.kb_per = p.nk;
   p.split_stride = 0;
   if (g.ksplit > 1) {  // fp32 partial products only (the caller reduces them)
-    SL_REQUIRE(!g.Cb && !g.bias && g.beta == 0.f && g.m_split >= g.M, SL_ERR_INVALID_ARGUMENT,
-               "gemm_bf16_tc2: split-K writes plain fp32 partials");
+    SL_REQUIRE(!g.bias && g.beta == 0.f && g.m_split >= g.M && !g.sm_part, SL_ERR_INVALID_ARGUMENT,
+               "gemm_bf16_tc2: split-K writes plain (fp32 or bf16) partials");
     p.kb_per = (int)ceil_div(p.nk, g.ksplit);
     p.ksplit = (int)ceil_div(p.nk, p.kb_per);  // no empty units
     SL_REQUIRE(p.ksplit == g.ksplit, SL_ERR_INVALID_ARGUMENT,
