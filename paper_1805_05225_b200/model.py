@@ -364,3 +364,41 @@ def _numel(shape):
     for s in shape:
         k *= s
     return k
+
+
+class GraphedStep:
+    """A model's whole training step captured once as a CUDA graph and replayed —
+    the user-facing call for repeated steps of one shape: every kernel of the
+    step (embeddings, encoder, decoder, output layer, optimizer with its
+    device-side step counter) replays without host launch gaps.  Each call
+    copies the step's host inputs (pinned) into the captured device buffers,
+    replays the graph and returns the loss read back to the host.
+
+        step = GraphedStep(model, src_ids, src_lens, targets)   # device tensors of the shape
+        loss = step(src_host, lens_host, trg_host)               # pinned host tensors
+
+    Single-GPU (the data-parallel all-reduce is not captured)."""
+
+    def __init__(self, model, src_ids, src_lens, targets):
+        self.model = model
+        self.inputs = [src_ids.clone(), src_lens.clone(), targets.clone()]
+        self.loss_h = torch.empty((), dtype=torch.float32).pin_memory()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside the capture (lazy allocations, attributes)
+            model.step(*self.inputs)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss = model.step(*self.inputs)
+
+    def __call__(self, src_ids, src_lens, targets, sync: bool = True):
+        for dst, src in zip(self.inputs, (src_ids, src_lens, targets)):
+            dst.copy_(src, non_blocking=True)
+        self.graph.replay()
+        self.loss_h.copy_(self.loss, non_blocking=True)
+        if not sync:
+            return self.loss_h
+        torch.cuda.current_stream().synchronize()
+        return float(self.loss_h)

@@ -75,3 +75,18 @@ def test_encoder_receives_decoder_gradient(cuda):
         for mine, theirs in zip(m.enc.g_views[l], grads[l]):
             r = np.abs(mine.cpu().numpy() - theirs).max() / np.abs(theirs).max()
             assert r < 2e-2, (l, r)
+
+
+def test_graphed_step_matches_eager(cuda):
+    """model.GraphedStep (the public graphed-step call: host inputs in, host loss out)
+    runs exactly the eager step."""
+    from paper_1805_05225_b200.model import GraphedStep
+    m1, src, trg, lens, tl = make(9)
+    m2, _, _, _, _ = make(9)
+    gs = GraphedStep(m2, src, lens, trg)  # runs one warm-up step, then captures
+    m1.step(src, lens, trg)  # the same warm-up step
+    l1 = [float(m1.step(src, lens, trg)) for _ in range(3)]
+    hs = [t.cpu().pin_memory() for t in (src, lens, trg)]
+    l2 = [gs(*hs) for _ in range(3)]
+    assert l1 == l2
+    assert torch.equal(m1.params, m2.params)
