@@ -271,6 +271,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           __nv_bfloat16* brow = p.Cb + z * p.split_stride + (int64_t)row * p.ldc + col0;
           if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
             const bool bvec = p.bias && ((uintptr_t)(p.bias + col0) & 15) == 0;
+            // 32 B stores (two 8-column groups per request) when the row segment allows:
+            // the epilogue's uncoalesced per-row stores are request-bound
+            const bool v32 = ((uintptr_t)brow & 31) == 0;
+            uint4 wlo = make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
               float o[8];
@@ -291,7 +295,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               w.y = *reinterpret_cast<uint32_t*>(&t1);
               w.z = *reinterpret_cast<uint32_t*>(&t2);
               w.w = *reinterpret_cast<uint32_t*>(&t3);
-              *reinterpret_cast<uint4*>(brow + j) = w;
+              if (!v32) {
+                *reinterpret_cast<uint4*>(brow + j) = w;
+              } else if ((j & 8) == 0) {
+                wlo = w;
+              } else {
+                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(brow + j - 8),
+                             "r"(wlo.x), "r"(wlo.y), "r"(wlo.z), "r"(wlo.w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                             : "memory");
+              }
               if (p.sm_part) {  // statistics of the stored (bf16) values
                 const float zb[8] = {__low2float(t0), __high2float(t0), __low2float(t1), __high2float(t1),
                                      __low2float(t2), __high2float(t2), __low2float(t3), __high2float(t3)};
