@@ -28,8 +28,7 @@ namespace {
 constexpr int BMP = 256, BNP = 256, BK = 64, kStages = 6, kEpiWarps = 8, kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kHalf = 128 * 64 * 2;  // 16 KB: 128 rows (or cols) x 64 K of bf16
 constexpr uint32_t kStage = 2 * kHalf;    // A half + B half per CTA
-constexpr uint32_t kEpiTile = 32 * 33 * 4;  // per epilogue warp: a 32 x 32 fp32 staging tile (+1 pad)
-constexpr uint32_t kSmem = kStages * kStage + kEpiWarps * kEpiTile + 1024;
+constexpr uint32_t kSmem = kStages * kStage + 1024;
 
 struct P2 {
   int M, N, K, nm, nn, nk;
@@ -42,8 +41,7 @@ struct P2 {
   int64_t ldc2;
   __nv_bfloat16* Cb;
   int skip_epi;  // experiments only: load the accumulator but store nothing (wrong results)
-  int stage_epi;  // one work unit per CTA pair and a plain fp32 output: stage the epilogue through
-                  // shared memory so every warp store covers 128 contiguous bytes of one row
+
   float4* sm_part;  // softmax partials (gemm.h TcGemm::sm_part)
   int sm_ld;
   const int32_t* sm_targets;
@@ -341,21 +339,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 make_float4(sm_m, sm_s, sm_t, sm_y);
           continue;
         }
-        if (p.stage_epi) {  // (uniform) transpose through shared memory: row-contiguous stores
-          float* tile = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + kStages * kStage +
-                                                 (warp - 2) * kEpiTile);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = v[j];  // bank (lane + j) % 32: conflict-free
-          __syncwarp();
-          const int rbase = m0 + 32 * q;
-          float* cz = p.C + z * p.split_stride + col0 + lane;
-          const bool colok = col0 + lane < p.N;
-#pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr)
-            if (colok && rbase + rr < p.M) cz[(int64_t)(rbase + rr) * p.ldc] = p.alpha * tile[rr * 33 + lane];
-          __syncwarp();
-          continue;
-        }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
         if (vec && col0 + 32 <= p.N && p.beta == 0.f && !p.bias && (p.ldc % 8) == 0 &&
             ((uintptr_t)crow & 31) == 0) {
@@ -538,13 +521,6 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   // bulk-tensor output stores when the output is written (not accumulated) and
   // its rows are 16 B aligned; the per-row path stays for beta != 0
   p.skip_epi = getenv("SL_GEMM_SKIP_EPI") != nullptr;
-  {
-    const int units = p.nm * p.nn * p.ksplit;
-    static const bool no_stage = getenv("SL_GEMM_NO_STAGED_EPI") != nullptr;
-    // measured slower than the 32 B vector stores at the decoder's shapes: opt-in only
-    p.stage_epi = getenv("SL_GEMM_STAGED_EPI") != nullptr && !no_stage && units <= sms2() / 2 && !g.Cb &&
-                  g.beta == 0.f && !g.bias && g.m_split >= g.M && g.C != nullptr;
-  }
   p.sm_part = g.sm_part;
   p.sm_ld = g.sm_ld;
   p.sm_targets = g.sm_targets;
