@@ -452,7 +452,8 @@ def main():
                 f"H={H} with input feeding [prev trg {D0} ‖ prev att {2 * H}] + MLP attention (key {H}, weight "
                 f"feedback) + relu readout {H} + output softmax V={args.vocab} with label-smoothed CE (eps 0.1), "
                 f"teacher forcing, T_src=T_tgt={T}, fwd+bwd + fused clip(5.0)+Adam over all parameters "
-                f"(+DP grad all-reduce at N>1); no dropout")
+                f"(+DP grad all-reduce at N>1); dropout 0.3 on the output_prob input (the reference's "
+                f"counter-based mask, bit-identical)")
     else:
         work = (f"config4 training step: {emb_s}{L}xBLSTM encoder H={H} D0={D0} + LSTM decoder "
                 f"H={H} (input {D0}+{2 * H}){out_s}, T_src=T_tgt={T}, fwd+bwd + fused "

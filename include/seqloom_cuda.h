@@ -246,6 +246,21 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
                  float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
                  void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream);
 
+/* ---- input dropout (the output_prob layer's, models.hpp:18) --------------------
+ * The reference's counter-based Tape::dropout (tape.cpp:540-600, applied by
+ * eval_layer, compiler.cpp:554-562) on x [B, T, F] keyed by its own Time
+ * coordinate: y[b,t,f] = x[b,t,f] / (1 - rate) if
+ * u01(mix64(key, mix64(t + 2, b*F + f))) >= rate, else 0 (rng.hpp), bit-identical
+ * to the reference.  key = mix64(key0, batch_counter), key0 = mix64(seed,
+ * fnv1a("<layer>#<input index>")); batch_counter = *counter (device int32, e.g.
+ * the optimizer's step counter, so a captured graph draws a new mask per replay)
+ * or counter_value when counter is NULL.  The backward is the same map on dy
+ * (the mask is recomputed, never stored).  rate in [0, 1). */
+int sl_dropout_fwd(int32_t batch, int32_t time, int32_t features, float rate, uint64_t key0,
+                   const int32_t* counter, int64_t counter_value, const float* x, float* y, sl_stream_t stream);
+int sl_dropout_bwd(int32_t batch, int32_t time, int32_t features, float rate, uint64_t key0,
+                   const int32_t* counter, int64_t counter_value, const float* dy, float* dx, sl_stream_t stream);
+
 /* ---- embedding lookup -------------------------------------------
  * The reference's Linear layer on ids = gather_rows(table, ids) (compiler.cpp:
  * 584-589, tape.cpp:448-492): row r of out (row stride out_ld) = table[ids[r]],
@@ -278,7 +293,7 @@ int sl_embedding_bwd(int64_t n_ids, const int32_t* ids, int32_t vocab, int32_t d
  *   k1_xw_gemm, k2_rec_fwd, k3_rec_bwd, k4_dx_gemm, k4_dw_gemm, k4_dr_gemm,
  *   k5_cell_fwd, k5_cell_bwd, k6_grad_norm, k6_adam, k7_logits_gemm, k7_softmax_ce,
  *   k7_dx_gemm, k7_dw_gemm, k8_attention_fwd, k8_attention_bwd, k9_embedding_fwd,
- *   k10_dec_*,
+ *   k10_dec_*, k11_dropout,
  *   k9_embedding_bwd */
 typedef struct sl_profile_entry {
   char name[32];

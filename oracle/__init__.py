@@ -130,6 +130,9 @@ class Reference:
                                              [_d] * 15 + [c, ctypes.c_int])
         if hasattr(L, "ref_gather_rows"):
             L.ref_gather_rows.argtypes = [ctypes.c_int] * 4 + [_d, _i, _d, _d, _d, c, ctypes.c_int]
+        if hasattr(L, "ref_dropout"):
+            L.ref_dropout.argtypes = ([ctypes.c_int] * 3 + [_d, ctypes.c_double, ctypes.c_ulonglong, c, ctypes.c_int,
+                                                            ctypes.c_ulonglong, _d, _d, _d, c, ctypes.c_int])
         if hasattr(L, "ref_output_ce"):
             L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
                                         [c, ctypes.c_int])
@@ -448,3 +451,80 @@ def attn_decoder_np(src_lens, enc, prev_ids, P, d_readout=None, relu_mask=None):
         if flat[r] >= 0:
             g["trg_W"][flat[r]] += rows[r]
     return readout, g, d_enc
+
+
+
+def _dropout(self, x, rate, seed, qualified, input_index, batch_counter, d_out=None):
+    """The reference's input dropout on a [B, T, F] value (Tape::dropout): (out, dx or None)."""
+    B, T, F = x.shape
+    x, d_out = _f64(x), _f64(d_out)
+    out = np.zeros((B, T, F))
+    dx = np.zeros((B, T, F)) if d_out is not None else None
+    err = ctypes.create_string_buffer(512)
+    rc = self.lib.ref_dropout(B, T, F, _ptr(x), float(rate), int(seed), qualified.encode(), int(input_index),
+                              int(batch_counter), _ptr(d_out), _ptr(out), _ptr(dx), err, 512)
+    self._check(rc, err)
+    return out, dx
+
+
+Reference.dropout = _dropout
+
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x):
+    """rng.hpp splitmix64 on Python ints (uint64 arithmetic)."""
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def mix64(a, b):
+    return splitmix64(a ^ ((splitmix64(b) + 0x9E3779B97F4A7C15) & _M64))
+
+
+def fnv1a(s: str):
+    h = 0xCBF29CE484222325
+    for ch in s.encode():
+        h = ((h ^ ch) * 0x100000001B3) & _M64
+    return h
+
+
+def _splitmix64_np(x):
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def dropout_key(seed: int, qualified: str, input_index: int, batch_counter: int) -> int:
+    """compiler.cpp:559-560: mix64(mix64(seed, fnv1a(qualified#index)), batch_counter)."""
+    return mix64(mix64(seed, fnv1a(f"{qualified}#{input_index}")), batch_counter)
+
+
+def dropout_mask_np(key: int, B: int, T: int, F: int, rate: float):
+    """Keep mask of Tape::dropout for a [B, T, F] value keyed by its own Time
+    coordinate (tape.cpp:549-570, 67-71): survives(key, t + 2, b*F + f) =
+    u01(mix64(key, mix64(t + 2, pos))) >= rate, u01(h) = (splitmix64(h) >> 11) * 2^-53."""
+    with np.errstate(over="ignore"):
+        t = np.arange(T, dtype=np.uint64)[None, :, None] + np.uint64(2)
+        pos = (np.arange(B, dtype=np.uint64)[:, None, None] * np.uint64(F) +
+               np.arange(F, dtype=np.uint64)[None, None, :])
+        inner = _splitmix64_np(pos) + np.uint64(0x9E3779B97F4A7C15)   # mix64(t + 2, pos)
+        m1 = _splitmix64_np(t ^ inner)
+        outer = _splitmix64_np(m1) + np.uint64(0x9E3779B97F4A7C15)     # mix64(key, m1)
+        h = _splitmix64_np(np.uint64(key) ^ outer)
+        u = (_splitmix64_np(h) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return u >= rate
+
+
+def dropout_np(x, key, rate, d_out=None, real=np.float32):
+    """out = x * keep / (1 - rate) with the reference's inv_keep = Real(1) / (Real(1) - rate)."""
+    B, T, F = x.shape
+    keep = dropout_mask_np(key, B, T, F, rate)
+    inv = real(1) / (real(1) - real(rate))
+    out = np.where(keep, np.asarray(x, real) * inv, real(0))
+    if d_out is None:
+        return out
+    return out, np.where(keep, np.asarray(d_out, real) * inv, real(0))

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "seqloom/layers.hpp"
+#include "seqloom/rng.hpp"
 #include "seqloom/tape.hpp"
 
 using namespace seqloom;
@@ -180,6 +181,32 @@ int ref_gather_rows(int B, int T, int V, int D, const double* table, const int* 
     NodeId loss = sum_all(t, t.mul(on, gy));
     GradBuffer g = t.backward(loss);
     put(t.param_gradients(g).at("emb/W"), d_table);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
+// The reference's input dropout as eval_layer applies it (compiler.cpp:554-562 ->
+// Tape::dropout, tape.cpp:540-600) to a [B, T, F] value computed once per batch
+// (kStaticStep: elements keyed by their own Time coordinate), with the layer key
+// mix64(mix64(seed, fnv1a(qualified + "#" + input_index)), batch_counter); with
+// d_out, the gradient through L = sum(out * d_out).
+int ref_dropout(int B, int T, int F, const double* x, double rate, unsigned long long seed, const char* qualified,
+                int input_index, unsigned long long batch_counter, const double* d_out, double* out, double* dx,
+                char* err, int errlen) {
+  try {
+    Tape t(d_out != nullptr);
+    NodeId xn = t.param("x", make({{Axis::Batch, B}, {Axis::Time, T}, {Axis::Feature, F}}, x));
+    DropoutKey key{mix64(mix64(seed, fnv1a(std::string(qualified) + "#" + std::to_string(input_index))),
+                         batch_counter)};
+    NodeId on = t.dropout(xn, static_cast<Real>(rate), key, kStaticStep, true);
+    put(t.value(on), out);
+    if (!d_out) return 0;
+    NodeId gy = t.constant(make({{Axis::Batch, B}, {Axis::Time, T}, {Axis::Feature, F}}, d_out));
+    NodeId loss = sum_all(t, t.mul(on, gy));
+    GradBuffer g = t.backward(loss);
+    put(t.param_gradients(g).at("x"), dx);
     return 0;
   } catch (const std::exception& e) {
     return fail(e, err, errlen);

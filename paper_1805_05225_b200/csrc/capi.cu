@@ -16,6 +16,7 @@
 #include "embedding.h"
 #include "cell.h"
 #include "decoder.h"
+#include "dropout.h"
 #include "convert.h"
 #include "gemm.h"
 #include "profile.h"
@@ -479,6 +480,25 @@ int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params
     decoder_bwd(d, p, g, static_cast<const __nv_bfloat16*>(enc_bf16), enc_ld, src_lens, prev_ids, readout,
                 d_readout, d_enc, workspace, reinterpret_cast<cudaStream_t>(stream));
   });
+}
+
+static int dropout_call(int32_t B, int32_t T, int32_t F, float rate, uint64_t key0, const int32_t* counter,
+                        int64_t counter_value, const float* in, float* out, sl_stream_t stream) {
+  return guarded([&] {
+    SL_REQUIRE(rate >= 0.f && rate < 1.f, SL_ERR_INVALID_ARGUMENT,
+               "dropout rate must be in [0, 1), got " + std::to_string(rate));  // tape.cpp:541-544
+    SL_REQUIRE(B >= 0 && T >= 0 && F >= 0, SL_ERR_SHAPE, "dropout: negative extent");
+    SL_REQUIRE((in && out) || (int64_t)B * T * F == 0, SL_ERR_INVALID_ARGUMENT, "dropout: null pointer argument");
+    dropout_apply(B, T, F, rate, key0, counter, counter_value, in, out, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int sl_dropout_fwd(int32_t batch, int32_t time, int32_t features, float rate, uint64_t key0,
+                   const int32_t* counter, int64_t counter_value, const float* x, float* y, sl_stream_t stream) {
+  return dropout_call(batch, time, features, rate, key0, counter, counter_value, x, y, stream);
+}
+int sl_dropout_bwd(int32_t batch, int32_t time, int32_t features, float rate, uint64_t key0,
+                   const int32_t* counter, int64_t counter_value, const float* dy, float* dx, sl_stream_t stream) {
+  return dropout_call(batch, time, features, rate, key0, counter, counter_value, dy, dx, stream);
 }
 
 int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* v, int32_t step,

@@ -230,8 +230,10 @@ class Seq2SeqAttention:
       label-smoothed CE, output.OutputCE) on the readout;  then the fused
       global-norm clip + Adam step.
 
-    Dropout on the output_prob input (models.hpp:18) is not applied (a
-    deterministic step; it would be one fused mask multiply).  The encoder's top
+    Dropout 0.3 on the output_prob input (models.hpp:18) is the reference's own
+    counter-based mask (dropout.py: bit-identical), its batch counter read from the
+    optimizer's device-side step counter so a captured graph draws a new mask each
+    step (dropout=0 turns it off).  The encoder's top
     layer writes the padded bf16 layout the decoder's GEMMs read directly.
     Parameters use the reference's qualified manifest names
     (compiler.cpp:470-500) and live in ONE flat fp32 buffer; the gradient
@@ -240,7 +242,8 @@ class Seq2SeqAttention:
 
     def __init__(self, enc_layers: int, batch: int, src_time: int, trg_time: int, emb: int, hidden: int,
                  vocab: int, src_vocab: int, trg_vocab: int, key: int | None = None, readout: int | None = None,
-                 device=None, lr: float = 1e-3, clip_norm: float = 5.0, label_smoothing: float = 0.1):
+                 device=None, lr: float = 1e-3, clip_norm: float = 5.0, label_smoothing: float = 0.1,
+                 dropout: float = 0.3, seed: int = 1):
         from .decoder import NAMES, AttnDecoder, param_shapes
         self.L, self.B, self.Ts, self.T, self.E, self.H = enc_layers, batch, src_time, trg_time, emb, hidden
         self.K, self.Rd = key or hidden, readout or hidden
@@ -298,6 +301,12 @@ class Seq2SeqAttention:
         self.out = OutputCE(batch, trg_time, self.Rd, vocab, label_smoothing, device=self.device)
         self.readout = torch.empty(batch, trg_time, self.Rd, dtype=torch.float32, device=self.device)
         self.d_readout = torch.empty_like(self.readout)
+        self.dropout = None
+        if dropout > 0:
+            from .dropout import Dropout
+            self.dropout = Dropout(dropout, seed, "output/output_prob", 0)
+            self.dropped = torch.empty_like(self.readout)
+            self.d_dropped = torch.empty_like(self.readout)
         self.d_enc = torch.empty(batch, src_time, Ed, dtype=torch.float32, device=self.device)
         self.prev_ids = torch.full((batch, trg_time), -1, dtype=torch.int32, device=self.device)
         self.opt = Adam(self.params, lr=lr, clip_norm=clip_norm, names=names)
@@ -336,8 +345,15 @@ class Seq2SeqAttention:
         trg_lens = src_lens if trg_lens is None else trg_lens
         self.forward(src_ids, src_lens, targets)
         W, b = self.out_p
-        loss, _, _, _ = self.out.forward_backward(self.readout, targets, trg_lens, W, b, dx=self.d_readout,
-                                                  dW=self.out_g[0], db=self.out_g[1])
+        if self.dropout is not None:  # batch counter = optimizer steps done (the device-side Adam counter)
+            ctr = self.opt.scratch[12:16].view(torch.int32)
+            self.dropout.forward(self.readout, self.dropped, counter=ctr)
+            loss, _, _, _ = self.out.forward_backward(self.dropped, targets, trg_lens, W, b, dx=self.d_dropped,
+                                                      dW=self.out_g[0], db=self.out_g[1])
+            self.dropout.backward(self.d_dropped, self.d_readout, counter=ctr)
+        else:
+            loss, _, _, _ = self.out.forward_backward(self.readout, targets, trg_lens, W, b, dx=self.d_readout,
+                                                      dW=self.out_g[0], db=self.out_g[1])
         if reducer is not None:
             reducer(-2, self.out_bucket)
         self.dec.backward(self.enc_out, src_lens, self.prev_ids, self.dec_p, self.readout, self.d_readout,

@@ -115,3 +115,29 @@ def test_decoder_shape_errors(cuda):
     with pytest.raises(lstm.ShapeError):
         AttnDecoder(4, 7, 5, 12, 16, 8, 2000, 8, 11)  # key_dim > 1024
 
+
+
+def test_dropout_matches_reference_mask_bitwise(cuda):
+    """sl_dropout_fwd/bwd: the reference's counter-based mask (oracle.dropout_np, pinned
+    to Tape::dropout), bit-identical values and gradients; the device-side counter
+    path equals the host-value path."""
+    from paper_1805_05225_b200.dropout import Dropout
+    rng = np.random.default_rng(3)
+    B, T, F = 16, 60, 1000
+    x = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
+    d = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
+    for seed, counter, rate in ((1, 0, 0.3), (77, 12, 0.5)):
+        dr = Dropout(rate, seed, "output/output_prob", 0)
+        xg, dg = torch.as_tensor(x).cuda(), torch.as_tensor(d).cuda()
+        y, dx = torch.empty_like(xg), torch.empty_like(xg)
+        dr.forward(xg, y, counter_value=counter)
+        dr.backward(dg, dx, counter_value=counter)
+        key = oracle.dropout_key(seed, "output/output_prob", 0, counter)
+        ry, rdx = oracle.dropout_np(x, key, rate, d_out=d)
+        assert np.array_equal(y.cpu().numpy(), ry) and np.array_equal(dx.cpu().numpy(), rdx)
+        ctr = torch.tensor([counter], dtype=torch.int32, device="cuda")
+        y2 = torch.empty_like(xg)
+        dr.forward(xg, y2, counter=ctr)
+        assert torch.equal(y, y2)
+    with pytest.raises(ValueError):
+        Dropout(1.0, 1, "x")

@@ -93,3 +93,20 @@ def test_decoder_restatement_masks_padded_sources():
     for n in g1:
         if n not in ("enc_ctx_W", "enc_ctx_b"):
             assert np.allclose(g1[n], g2[n], rtol=0, atol=1e-14), n
+
+
+def test_dropout_restatement_pinned_to_reference():
+    """The output_prob input dropout: the numpy restatement of the reference's
+    counter-based mask (rng.hpp splitmix64/mix64/fnv1a, tape.cpp:540-600) equals the
+    reference's own Tape::dropout bit for bit (values and gradient)."""
+    ref = _ref()
+    rng = np.random.default_rng(0)
+    B, T, F = 3, 5, 7
+    x, d = rng.uniform(-1, 1, (B, T, F)), rng.uniform(-1, 1, (B, T, F))
+    for seed, counter, rate in ((1, 0, 0.3), (12345, 7, 0.5), (2**63 + 5, 3, 0.1)):
+        out, dx = ref.dropout(x, rate, seed, "output/output_prob", 0, counter, d_out=d)
+        key = oracle.dropout_key(seed, "output/output_prob", 0, counter)
+        o2, d2 = oracle.dropout_np(x, key, rate, d_out=d, real=np.float64)
+        assert np.array_equal(out, o2) and np.array_equal(dx, d2)
+        keep = oracle.dropout_mask_np(key, B, T, F, rate)
+        assert 0 < keep.sum() < keep.size
