@@ -30,14 +30,17 @@ __global__ void dropout_kernel(int B, int T, int F, float rate, float inv_keep, 
                                float* __restrict__ out) {
   const uint64_t key = mix64(key0, (uint64_t)(counter ? (int64_t)*counter : counter_value));
   const double thr = (double)rate;
-  const int64_t n = (int64_t)B * T * F;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t bt = i / F;
-    const int f = (int)(i - bt * F);
-    const int b = (int)(bt / T), t = (int)(bt - (int64_t)b * T);
-    const uint64_t h = mix64(key, mix64((uint64_t)(t + 2), (uint64_t)b * F + f));
-    const double u = (double)(splitmix64(h) >> 11) * 0x1.0p-53;
-    out[i] = u >= thr ? in[i] * inv_keep : 0.f;
+  // one CTA per (b, t) row: no 64-bit division per element
+  for (int64_t r = blockIdx.x; r < (int64_t)B * T; r += gridDim.x) {
+    const int b = (int)(r / T), t = (int)(r - (int64_t)b * T);
+    const uint64_t ct = (uint64_t)(t + 2);
+    const float* src = in + r * F;
+    float* dst = out + r * F;
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      const uint64_t h = mix64(key, mix64(ct, (uint64_t)b * F + f));
+      const double u = (double)(splitmix64(h) >> 11) * 0x1.0p-53;
+      dst[f] = u >= thr ? src[f] * inv_keep : 0.f;
+    }
   }
 }
 
@@ -49,7 +52,7 @@ void dropout_apply(int B, int T, int F, float rate, uint64_t key0, const int32_t
   if (n == 0) return;
   const float inv_keep = 1.0f / (1.0f - rate);  // Real(1) / (Real(1) - rate), fp32 like the reference build
   Phase ph(st, "k11_dropout", 0.0, 8.0 * n);
-  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+  const int grid = (int)std::min<int64_t>((int64_t)B * T, 148 * 16);
   dropout_kernel<<<grid, 256, 0, st>>>(B, T, F, rate, inv_keep, key0, counter, counter_value, in, out);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
