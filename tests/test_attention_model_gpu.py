@@ -92,3 +92,58 @@ def test_graphed_step_matches_eager(cuda):
     l2 = [gs(*hs) for _ in range(3)]
     assert l1 == l2
     assert torch.equal(m1.params, m2.params)
+
+
+def test_whole_model_gradients_match_reference_composition(cuda):
+    """The bench workload's forward + backward end to end — src lookup, the 2-layer
+    BLSTM encoder, the attention decoder, the reference's dropout, output_prob + CE —
+    against the composition of the reference-pinned oracles: the reference build's own
+    BLSTM stack, attn_decoder_np, dropout_np (bit-identical mask), output_ce_np, and the
+    embedding scatter.  bf16 tolerance on the loss and every parameter gradient."""
+    m, src, trg, lens, tl = make(11)
+    m.forward(src, lens, trg)
+    ctr = m.opt.scratch[12:16].view(torch.int32)
+    m.dropout.forward(m.readout, m.dropped, counter=ctr)
+    W, b = m.out_p
+    loss, _, _, _ = m.out.forward_backward(m.dropped, trg, tl, W, b, dx=m.d_dropped, dW=m.out_g[0], db=m.out_g[1])
+    m.dropout.backward(m.d_dropped, m.d_readout, counter=ctr)
+    m.dec.backward(m.enc_out, lens, m.prev_ids, m.dec_p, m.readout, m.d_readout, m.dec_g, d_enc=m.d_enc)
+    dx0 = m.enc.backward(m.d_enc)
+    m.src_emb.backward(src, dx0, m.src_g)
+    torch.cuda.synchronize()
+    npy = lambda t: t.detach().float().cpu().numpy()
+    H, E, L = DIMS["hidden"], DIMS["emb"], DIMS["enc_layers"]
+    ids, ln, tg = npy(src).astype(np.int32), npy(lens).astype(np.int32), npy(trg).astype(np.int32)
+    # forward composition
+    x0 = npy(m.src_p)[ids]
+    params = [tuple(npy(t) for t in m.enc.p_views[l]) for l in range(L)]
+    ref = oracle.Reference(64)
+    y, _, _ = ref.blstm_stack(x0, ln, params)
+    P = {k: npy(v) for k, v in m.dec_p.items()}
+    prev = npy(m.prev_ids).astype(np.int32)
+    ro_gpu = npy(m.readout)
+    key = oracle.dropout_key(1, "output/output_prob", 0, int(ctr.item()))
+    # decoder backward needs d_readout: chain output_ce_np <- dropout <- readout
+    readout = oracle.attn_decoder_np(ln, y, prev, P)
+    drop = oracle.dropout_np(readout, key, 0.3, real=np.float64)
+    r_loss, d_drop, r_dW, r_db = oracle.output_ce_np(drop, npy(tl).astype(np.int32), tg, npy(W), npy(b), 0.1)
+    _, d_ro = oracle.dropout_np(readout, key, 0.3, d_out=d_drop, real=np.float64)
+    _, g, d_enc = oracle.attn_decoder_np(ln, y, prev, P, d_readout=d_ro, relu_mask=ro_gpu > 0)
+    _, dx, eg = ref.blstm_stack(x0, ln, params, dy=d_enc)
+    d_src = np.zeros_like(npy(m.src_p))
+    np.add.at(d_src, ids.reshape(-1), dx.reshape(-1, E))
+    rel = lambda a, r: float(np.abs(np.asarray(a, np.float64) - r).max() / max(np.abs(r).max(), 1e-30))
+    cos = lambda a, r: float(np.dot(np.ravel(a).astype(np.float64), np.ravel(r)) /
+                             max(np.linalg.norm(np.ravel(a)) * np.linalg.norm(np.ravel(r)), 1e-300))
+    assert abs(float(loss) - r_loss) < 2e-2 * abs(r_loss)
+    pairs = [(npy(m.out_g[0]), r_dW), (npy(m.out_g[1]), r_db), (npy(m.src_g), d_src)]
+    pairs += [(npy(m.dec_g[n]), g[n]) for n in m.dec_g if n != "e_b"]
+    pairs += [(npy(mine), theirs) for l in range(L) for mine, theirs in zip(m.enc.g_views[l], eg[l])]
+    # the whole gradient vector norm-wise within the bf16 tolerance; every tensor's direction
+    # right (tensors whose gradient is orders of magnitude below the rest — e.g. the weight
+    # feedback of a freshly initialised model, ~1e-8 — only see upstream bf16 noise at their scale)
+    flat_m = np.concatenate([np.ravel(a) for a, _ in pairs]).astype(np.float64)
+    flat_r = np.concatenate([np.ravel(r) for _, r in pairs])
+    assert rel(flat_m, flat_r) < 2e-2
+    for i, (a, r) in enumerate(pairs):
+        assert cos(a, r) > 0.99, (i, cos(a, r), rel(a, r))
