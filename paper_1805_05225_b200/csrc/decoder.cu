@@ -23,17 +23,19 @@
 //    dW temporaries, tape.cpp:1174-1215) and d trg / d enc.
 //  * Per step only the serial work remains: one split-K GEMM [att ‖ s] W_{att,R}
 //    whose partial products are summed inside the gate kernel, the small s_tr
-//    GEMM, and ONE attention kernel per batch row (energies + masked softmax +
-//    context in one pass over that row's enc_ctx / enc, both bf16 and small
-//    enough to stay L2-resident across the steps).
-//  * Backward: the per-step attention kernel computes only what the
-//    recurrence needs (d s_tr and d accum_{t-1}); the big accumulations over t
-//    — d enc_ctx, d W_fb, d b_fb, d v, d enc = sum_t a_t (x) d att_t — run once
-//    after the loop from small saved per-step vectors (a_t, d att_t, de_t),
-//    recomputing tanh in registers, so the loop never read-modify-writes a
-//    [B, Ts, K] accumulator.  All reductions are fixed-order (deterministic).
-#include <cooperative_groups.h>
-
+//    GEMM, and two attention kernels (energies per (row, 8 positions); softmax +
+//    context per (row, 512 columns)) reading enc_ctx / enc in bf16; the backward
+//    mirrors it (G1 GEMM, d_a per (row, 512 columns), softmax + tanh adjoint per
+//    (row, 8 positions), a fixed-order d s_tr reduction, G2 GEMM, gate adjoint).
+//    Time-major per-step buffers (a step's rows are contiguous), loads issued
+//    unconditionally before their first use, programmatic dependent launch
+//    between the per-step kernels.
+//  * Backward: the per-step attention kernels compute only what the recurrence
+//    needs (d s_tr and d accum_{t-1}); the big accumulations over t — d enc_ctx,
+//    d W_fb, d b_fb, d v, d enc = sum_t a_t (x) d att_t — run once after the loop
+//    from small saved per-step vectors (a_t, d att_t, de_t), recomputing tanh in
+//    registers, so the loop never read-modify-writes a [B, Ts, K] accumulator.
+//    All reductions are fixed-order (deterministic).
 #include <algorithm>
 #include <cmath>
 #include <memory>
@@ -44,7 +46,6 @@
 #include "embedding.h"
 #include "gemm.h"
 #include "profile.h"
-#include "tc.cuh"
 
 namespace sl {
 namespace {
@@ -63,10 +64,6 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// split cluster barrier: announce this CTA has started (its shared memory exists) early,
-// wait for the peer just before the first remote shared-memory access
-__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 // Programmatic dependent launch (PDL): the per-step kernels are launched with
 // programmatic stream serialization, trigger their dependents at entry and, after
 // a prologue that only touches data that is static during the loop (enc, enc_ctx,
@@ -76,11 +73,6 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// bulk L2 prefetch of a contiguous 16 B-aligned range (multiple of 16 B): one instruction
-// puts a whole row segment in flight, so a later phase's loads hit L2
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -100,12 +92,6 @@ __device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
   }
 }
 __device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
-__device__ __forceinline__ void ld4(const bf16* p, float (&f)[4]) {
-  const uint2 q = *reinterpret_cast<const uint2*>(p);
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.x));
-  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.y));
-  f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y;
-}
 __device__ __forceinline__ void st4(bf16* p, const float (&f)[4]) {
   const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
   *reinterpret_cast<uint2*>(p) =
