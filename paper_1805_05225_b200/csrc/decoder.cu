@@ -773,6 +773,30 @@ __global__ void __launch_bounds__(128) dec_enc_grad_kernel(int B, int Ts, int T,
   }
 }
 
+// sum of split-K partials in split order -> rows < m_split to C, the rest to C2
+__global__ void splitk_sum_kernel(const float* __restrict__ part, int ks, int64_t stride, int M, int N, int64_t ldp,
+                                  float* C, int64_t ldc, int m_split, float* C2, int64_t ldc2) {
+  const int r = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c >= N) return;
+  const float* p = part + (int64_t)r * ldp + c;
+  float* dst = r < m_split ? C + (int64_t)r * ldc : C2 + (int64_t)(r - m_split) * ldc2;
+  if (c + 4 <= N && (ldp % 4) == 0 && (((uintptr_t)(dst + c)) & 15) == 0) {
+    float4 acc = ldf4(p);
+    for (int z = 1; z < ks; ++z) {
+      const float4 v = ldf4(p + z * stride);
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(dst + c) = acc;
+  } else {
+    for (int i = 0; i < 4 && c + i < N; ++i) {
+      float acc = p[i];
+      for (int z = 1; z < ks; ++z) acc += p[z * stride + i];
+      dst[c + i] = acc;
+    }
+  }
+}
+
 // fixed-order column sums: out[c] = sum_r x[r * ld + c] (stage 1: row chunks, stage 2: chunks in order)
 constexpr int kColChunks = 64;
 __global__ void colsum1_kernel(const float* x, int64_t rows, int cols, int64_t ld, int64_t per, float* part) {
@@ -844,6 +868,17 @@ int sm_count() {
   return n;
 }
 
+// Weight-gradient GEMMs (K = all B*T rows) with few output tiles leave most SMs idle:
+// split K so the tiles x splits fill the CTA pairs, then sum the fp32 partials in a
+// fixed order (deterministic).  Returns the split count (1: run as is).
+int wgrad_ks(int M, int N, int K) {
+  const int pairs = sm_count() / 2, tiles = (int)(ceil_div(M, 256) * ceil_div(N, 256));
+  if (tiles * 2 >= pairs) return 1;
+  const int nk = (int)ceil_div(K, 64);
+  const int want = std::max(1, std::min(std::min(pairs / tiles, nk / 8), 8));
+  return (int)ceil_div(nk, ceil_div(nk, want));
+}
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   static const bool off = getenv("SL_DEC_NO_PDL") != nullptr;
@@ -877,6 +912,8 @@ struct Lay {
   bf16 *enc_ctx, *xa, *ro, *dz, *ds, *drob, *dctx;
   int32_t* ids_tm;
   float *pre, *dtrg, *es, *dap, *dsp;
+  float* wpart;  // split-K partials of the weight-gradient GEMMs
+  size_t wpart_floats;
   float *xw, *pf, *pstr, *p1, *p2, *c_all, *gates, *str_all, *a_all, *acc_all, *de_all, *datt_all, *ds32, *dro,
       *dc, *dacc, *part, *colws, *tmp;
   void* emb_ws;
@@ -929,6 +966,18 @@ Lay layout(const DecDims& d, void* base) {
   L.es = tf((int64_t)d.B * d.Ts);
   L.dap = tf((int64_t)d.B * ceil_div(d.E, kCols) * d.Ts);
   L.dsp = tf((int64_t)d.B * ceil_div(d.Ts, kPos) * d.K);
+  {
+    const int64_t BT = (int64_t)d.B * d.T, BTs = (int64_t)d.B * d.Ts;
+    const int64_t shapes[][3] = {{d.H, d.Rd, BT}, {d.Emb + 1, d.Rd, BT}, {d.E, d.Rd, BT}, {d.H, d.K, BT},
+                                 {d.E, d.K, BTs}, {d.Emb + 1, 4 * d.H, BT}, {d.H, 4 * d.H, BT}};
+    size_t need = 0;
+    for (const auto& sh : shapes) {
+      const int ks = wgrad_ks((int)sh[0], (int)sh[1], (int)sh[2]);
+      if (ks > 1) need = std::max(need, (size_t)ks * sh[0] * round_up(sh[1], 4));
+    }
+    L.wpart_floats = need;
+    L.wpart = need ? tf((int64_t)need) : nullptr;
+  }
   L.xw = tf(BT * 4 * d.H);
   L.pf = tf((int64_t)L.ks_f * d.B * 4 * d.H);
   L.pstr = tf((int64_t)L.ks_s * d.B * L.PK);
@@ -962,10 +1011,33 @@ void colsum(const float* x, int64_t rows, int cols, int64_t ld, float* out, floa
   count_launch(2);
 }
 
+
 TcGemm mk(int M, int N, int K, const bf16* A, int64_t lda, bool a_mn, const bf16* B, int64_t ldb, bool b_mn, float* C,
           int64_t ldc) {
   TcGemm g{M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, 1.f, 0.f, nullptr};
   return g;
+}
+
+void gemm_wgrad(const TcGemm& g, float* part, size_t part_floats, cudaStream_t st) {
+  const int ks = wgrad_ks(g.M, g.N, g.K);
+  const int64_t ldp = round_up(g.N, 4);
+  if (ks <= 1 || !part || (size_t)ks * g.M * ldp > part_floats || g.beta != 0.f || g.bias || g.Cb) {
+    gemm_bf16_tc(g, st);
+    return;
+  }
+  TcGemm p = g;
+  p.C = part;
+  p.ldc = ldp;
+  p.m_split = 1 << 30;
+  p.C2 = nullptr;
+  p.ldc2 = 0;
+  p.ksplit = ks;
+  p.split_stride = (int64_t)g.M * ldp;
+  gemm_bf16_tc(p, st);
+  splitk_sum_kernel<<<dim3((unsigned)ceil_div(ceil_div(g.N, 4), 256), (unsigned)g.M), 256, 0, st>>>(
+      part, ks, (int64_t)g.M * ldp, g.M, g.N, ldp, g.C, g.ldc, g.m_split, g.C2, g.ldc2);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
 }
 // split-K partials of a batch slice: partial z at C + z * stride (stride = full batch x ldc)
 void gemm_split(TcGemm g, int ks, int64_t stride, cudaStream_t st) {
@@ -1108,16 +1180,16 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
   gemm_bf16_tc(mk((int)BT, L.OA + E, Rd, L.drob, L.PDR, false, L.wro, L.PR, false, L.dro, L.PRF), st);
-  gemm_bf16_tc(mk(H, Rd, (int)BT, L.ro, L.PRO, true, L.drob, L.PDR, true, g.ro_W, Rd), st);
+  gemm_wgrad(mk(H, Rd, (int)BT, L.ro, L.PRO, true, L.drob, L.PDR, true, g.ro_W, Rd), L.wpart, L.wpart_floats, st);
   {
     TcGemm w = mk(Emb + 1, Rd, (int)BT, L.ro + H, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)H * Rd, Rd);
     w.m_split = Emb;
     w.C2 = g.ro_b;
     w.ldc2 = Rd;
-    gemm_bf16_tc(w, st);
+    gemm_wgrad(w, L.wpart, L.wpart_floats, st);
   }
-  gemm_bf16_tc(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
-               st);
+  gemm_wgrad(mk(E, Rd, (int)BT, L.ro + L.OA, L.PRO, true, L.drob, L.PDR, true, g.ro_W + (int64_t)(H + Emb) * Rd, Rd),
+             L.wpart, L.wpart_floats, st);
   ph.reset();
   ph.reset();
   const double ctx_bytes = 2.0 * B * d.Ts * K, enc_bytes = 2.0 * B * d.Ts * E;
@@ -1176,7 +1248,7 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   }
   embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
   // s_tr: d W_s over all rows, d b_s as a fixed-order column sum
-  gemm_bf16_tc(mk(H, K, (int)BT, L.ro, L.PRO, true, L.ds, L.PK, true, g.str_W, K), st);
+  gemm_wgrad(mk(H, K, (int)BT, L.ro, L.PRO, true, L.ds, L.PK, true, g.str_W, K), L.wpart, L.wpart_floats, st);
   colsum(L.ds32, BT, K, K, g.str_b, L.colws, st);
   // the attention's accumulations over t
   ph.reset(new Phase(st, "k10_attn_accum", 0.0, 2.0 * BTs * K + 4.0 * T * B * (K + E)));
@@ -1197,7 +1269,7 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
   ph.reset(new Phase(st, "k10_dec_bwd_hoisted", 4.0 * BTs * E * K));
   {
     gemm_bf16_tc(mk((int)BTs, E, K, L.dctx, L.PK, false, L.wctx, L.PK, false, d_enc, E), st);
-    gemm_bf16_tc(mk(E, K, (int)BTs, enc, ld_enc, true, L.dctx, L.PK, true, g.ctx_W, K), st);
+    gemm_wgrad(mk(E, K, (int)BTs, enc, ld_enc, true, L.dctx, L.PK, true, g.ctx_W, K), L.wpart, L.wpart_floats, st);
   }
   ph.reset(new Phase(st, "k10_attn_accum", 0.0, 4.0 * T * B * E + 8.0 * BTs * E));
   dec_enc_grad_kernel<<<dim3((unsigned)ceil_div(E, kEncCols), (unsigned)ceil_div(d.Ts, kEncPos), (unsigned)B), 128,
