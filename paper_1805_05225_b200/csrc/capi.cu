@@ -870,6 +870,14 @@ extern "C" int sl_debug_gemm_bf16_split(int M, int N, int K, const void* A, int6
   });
 }
 
+extern "C" int sl_debug_small_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                                   int b_kn, float* C, int64_t ldc, const float* bias, sl_stream_t stream) {
+  return guarded([&] {
+    small_gemm_bf16(M, N, K, static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B), ldb,
+                    b_kn != 0, C, ldc, bias, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
 extern "C" int sl_debug_gemm_trace(unsigned long long* dev_buf) {
   return guarded([&] { gemm_tc2_set_trace(dev_buf); });
 }

@@ -907,6 +907,7 @@ int ksplit_for(int M, int N, int K, int max_split = kMaxSplit) {
 struct Lay {
   int PZ, PXA, OA, PRO, PK, PR, PRF, PDR;  // PDR: pitch of the [DZ | d readout] rows
   int ks_f, ks_s, ks_1, ks_2;
+  bool small;
   int ctx_blocks;
   bf16 *wd2, *wtrg, *wstr, *wctx, *wro, *wtrgcat;
   bf16 *enc_ctx, *xa, *ro, *dz, *ds, *drob, *dctx;
@@ -932,9 +933,12 @@ Lay layout(const DecDims& d, void* base) {
   L.PRF = L.PRO;
   L.PDR = L.PZ + L.PR;
   L.ks_f = ksplit_for(d.B, 4 * d.H, d.E + d.H);
-  L.ks_s = ksplit_for(d.B, d.K, d.H, 4);  // summed in the energy kernel (str_cols: at most 4)
+  // the s_tr / d s projections (K = H or K columns, ~0.5 GFLOP) run on the mma.sync small-M
+  // GEMM (SL_DEC_TC_SMALL=1: the tcgen05 pair GEMM with split-K instead)
+  L.small = getenv("SL_DEC_TC_SMALL") == nullptr;
+  L.ks_s = L.small ? 1 : ksplit_for(d.B, d.K, d.H, 4);  // summed in the energy kernel (str_cols: at most 4)
   L.ks_1 = ksplit_for(d.B, d.E + d.H, 4 * d.H);
-  L.ks_2 = ksplit_for(d.B, d.H, d.K);
+  L.ks_2 = L.small ? 1 : ksplit_for(d.B, d.H, d.K);
   L.ctx_blocks = (int)(d.B * ceil_div(d.Ts, kCtxPos));
   char* p = static_cast<char*>(base);
   size_t off = 0;
@@ -1137,8 +1141,13 @@ void decoder_fwd(const DecDims& d, const DecParams& p, const bf16* enc, int64_t 
                  L.xa, L.PXA, L.ro, L.PRO, b0, nb};
       launch_pdl(dec_cell_fwd_kernel, dim3((unsigned)ceil_div(nb * (H / 4), 256)), dim3(256), 0, ss, cf);
       q.reset(new Phase(ss, "k10_str_gemm", 2.0 * nb * H * K));
-      gemm_split(mk(nb, K, H, L.ro + r0 * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr + (int64_t)b0 * L.PK, L.PK),
-                 L.ks_s, (int64_t)B * L.PK, ss);
+      if (L.small)  // s_tr = s_t W_s on the mma.sync small-M GEMM: one fp32 result, no split
+        small_gemm_bf16(nb, K, H, L.ro + r0 * L.PRO, L.PRO, L.wstr, L.PK, true, L.pstr + (int64_t)b0 * L.PK, L.PK,
+                        nullptr, ss);
+      else
+        gemm_split(mk(nb, K, H, L.ro + r0 * L.PRO, L.PRO, false, L.wstr, L.PK, true, L.pstr + (int64_t)b0 * L.PK,
+                      L.PK),
+                   L.ks_s, (int64_t)B * L.PK, ss);
       AttFwd af{B, d.Ts, T, K, E, t, L.ks_s, src_lens, L.pstr, L.PK, (int64_t)B * L.PK, p.str_b, p.fb_W, p.fb_b,
                 p.e_W, p.e_b, L.enc_ctx, L.PK, enc, ld_enc, L.es, L.str_all, L.a_all, L.acc_all, L.ro, L.PRO,
                 L.OA, L.xa, L.PXA, b0};
@@ -1218,9 +1227,13 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
       q.reset(new Phase(ss, "k10_att_dstr", 0.0, 4.0 * nb * K * (nsc + 2)));
       launch_pdl(dec_att_dstr_kernel, dim3((unsigned)ceil_div(K, 256), (unsigned)nb), dim3(256), 0, ss, ab);
       q.reset(new Phase(ss, "k10_g2_gemm", 2.0 * nb * H * K));
-      gemm_split(mk(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, false, L.wstr, L.PK, false,
-                    L.p2 + (int64_t)b0 * L.PK, L.PK),
-                 L.ks_2, (int64_t)B * L.PK, ss);
+      if (L.small)  // d s += d s_tr W_s^T on the small-M GEMM
+        small_gemm_bf16(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, L.wstr, L.PK, false,
+                        L.p2 + (int64_t)b0 * L.PK, L.PK, nullptr, ss);
+      else
+        gemm_split(mk(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, false, L.wstr, L.PK, false,
+                      L.p2 + (int64_t)b0 * L.PK, L.PK),
+                   L.ks_2, (int64_t)B * L.PK, ss);
       CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PK,
                  (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
                  last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR,

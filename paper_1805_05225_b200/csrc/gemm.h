@@ -65,6 +65,10 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream);
 // when the operands allow (gemm_bf16_tc2_ok) unless SL_GEMM_1CTA is set.
 bool gemm_bf16_tc2_ok(const TcGemm& g);
 void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream);
+// small-M GEMM on warp-level mma.sync (small_gemm.cu): C[M,N] = A[M,K] op(B) (+ bias),
+// A row-major; b_kn: B [K, N] row-major, else B [N, K] row-major; fp32 C, no split
+void small_gemm_bf16(int M, int N, int K, const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
+                     bool b_kn, float* C, int64_t ldc, const float* bias, cudaStream_t st);
 // debug: per-CTA timeline stamps of the pair GEMM into buf (null: off)
 void gemm_tc2_set_trace(unsigned long long* buf);
 

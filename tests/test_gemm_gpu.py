@@ -74,3 +74,30 @@ def test_gemm_bf16_tc_bf16_output(cuda):
     torch.cuda.synchronize()
     ref = (A.float() @ B.float() + bias).bfloat16().float()
     assert (out.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("M,N,K,b_kn", [(256, 1000, 1000, True), (256, 1000, 1000, False), (37, 72, 104, True),
+                                        (37, 77, 104, False), (1, 8, 8, True), (300, 130, 56, False)])
+def test_small_gemm_matches_torch(cuda, M, N, K, b_kn):
+    """The mma.sync small-M GEMM (decoder per-step projections) against an fp32 matmul
+    of the same bf16 operands."""
+    import ctypes
+    from paper_1805_05225_b200 import lstm
+    L = lstm.lib()
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    L.sl_debug_small_gemm.argtypes = [ctypes.c_int] * 3 + [vp, i64, vp, i64, ctypes.c_int, vp, i64, vp, vp]
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    pad = lambda n: (n + 7) // 8 * 8 + 8
+    A = (torch.rand(M, pad(K), device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = ((torch.rand(K, pad(N), device="cuda", generator=g) if b_kn else
+          torch.rand(N, pad(K), device="cuda", generator=g)) * 2 - 1).bfloat16()
+    bias = torch.rand(N, device="cuda", generator=g)
+    C = torch.full((M, N + 3), float("nan"), device="cuda")
+    assert L.sl_debug_small_gemm(M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], int(b_kn),
+                                 C.data_ptr(), C.shape[1], bias.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream) == 0
+    opB = B[:, :N].float() if b_kn else B[:, :K].float().t()
+    ref = A[:, :K].float() @ opB + bias
+    torch.cuda.synchronize()
+    assert torch.allclose(C[:, :N], ref, rtol=1e-4, atol=1e-4 * K ** 0.5)
+    assert torch.isnan(C[:, N:]).all()  # nothing written past N
