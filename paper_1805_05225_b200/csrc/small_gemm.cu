@@ -4,8 +4,9 @@
 // 0.5 GFLOP GEMMs are bound by fixed costs, not by the tensor pipe: the tcgen05
 // pair GEMM spends ~10 us on launch, TMEM / barrier setup and a split-K partial
 // epilogue; this kernel has no setup, no split and writes the final fp32 result
-// once (128 CTAs of 128 threads; a 6-deep cp.async pipeline over 32-wide K tiles —
-// the K loop is latency-bound, so the depth, not the MMA rate, sets its time).
+// once (128 CTAs of 128 threads; a 3-deep cp.async pipeline over 128-wide K tiles —
+// the K loop is latency-bound: few, wide K steps beat many narrow ones: 6.7-7.6 us
+// against 8.1-8.3 us for 6 x 32-wide and 7.6-7.8 us for 4 x 128-wide stages).
 //   C[M, N] = A[M, K] op(B) (+ bias[N]);  A row-major (lda);
 //   b_kn: B stored [K, N] row-major (ldb), else B stored [N, K] row-major (ldb).
 // K, lda, ldb multiples of 8 (16 B rows); N arbitrary; fp32 C (ldc).
@@ -15,7 +16,7 @@
 namespace sl {
 namespace {
 
-constexpr int BM = 32, BN = 64, BK = 32, kThreads = 128;
+constexpr int BM = 32, BN = 64, BK = 128, kThreads = 128;
 constexpr int APAD = BK + 8;  // smem row pitch (elements) of the A and [N][K] B tiles: conflict-free ldmatrix
 constexpr int BPAD = BN + 8;  // smem row pitch of the [K][N] B tile
 
@@ -31,35 +32,44 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kStages = 6;  // K tiles in flight: the K loop is latency-, not compute-bound
+constexpr int kStages = 3;  // K tiles in flight: the K loop is latency-, not compute-bound
+constexpr int kAVec = BM * BK / 8 / kThreads;                         // 16 B vectors per thread per A tile
+constexpr int kBVec = BN * BK / 8 / kThreads;                         // ... per B tile
+constexpr int kSA = BM * APAD, kSBkn = BK * BPAD, kSBnk = BN * APAD;  // elements per stage
+template <bool B_KN>
+constexpr size_t smem_bytes() { return (size_t)kStages * (kSA + (B_KN ? kSBkn : kSBnk)) * 2; }
 
 template <bool B_KN>
 __global__ void __launch_bounds__(kThreads) small_gemm_kernel(int M, int N, int K, const __nv_bfloat16* __restrict__ A,
                                                               int64_t lda, const __nv_bfloat16* __restrict__ Bm,
                                                               int64_t ldb, float* __restrict__ C, int64_t ldc,
                                                               const float* __restrict__ bias) {
-  __shared__ __align__(16) __nv_bfloat16 sa[kStages][BM * APAD];
-  __shared__ __align__(16) __nv_bfloat16 sb[kStages][B_KN ? BK * BPAD : BN * APAD];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr int kSB = B_KN ? kSBkn : kSBnk;
+  auto sa = reinterpret_cast<__nv_bfloat16 (*)[kSA]>(smem_raw);
+  auto sb = reinterpret_cast<__nv_bfloat16 (*)[kSB]>(smem_raw + (size_t)kStages * kSA * 2);
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   // one K tile: A 32 x 32 (one 16 B vector per thread), B 64 x 32 (two per thread), zero-filled
   // outside the matrix (N must then be a multiple of 8 for [K][N] B: 16 B never straddles N)
   auto issue = [&](int kt, int buf) {
     const int k0 = kt * BK;
-    {
-      const int r = tid / 4, c = (tid % 4) * 8, gr = m0 + r, gk = k0 + c;
+#pragma unroll
+    for (int v = 0; v < kAVec; ++v) {
+      const int i = tid + v * kThreads;
+      const int r = i / (BK / 8), c = (i % (BK / 8)) * 8, gr = m0 + r, gk = k0 + c;
       const bool ok = gr < M && gk < K;
       cp_async16(&sa[buf][r * APAD + c], ok ? A + (int64_t)gr * lda + gk : A, ok);
     }
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < kBVec; ++v) {
       const int i = tid + v * kThreads;
       if constexpr (B_KN) {
-        const int r = i / 8, c = (i % 8) * 8, gk = k0 + r, gn = n0 + c;
+        const int r = i / (BN / 8), c = (i % (BN / 8)) * 8, gk = k0 + r, gn = n0 + c;
         const bool ok = gk < K && gn < N;
         cp_async16(&sb[buf][r * BPAD + c], ok ? Bm + (int64_t)gk * ldb + gn : Bm, ok);
       } else {
-        const int r = i / 4, c = (i % 4) * 8, gn = n0 + r, gk = k0 + c;
+        const int r = i / (BK / 8), c = (i % (BK / 8)) * 8, gn = n0 + r, gk = k0 + c;
         const bool ok = gn < N && gk < K;
         cp_async16(&sb[buf][r * APAD + c], ok ? Bm + (int64_t)gn * ldb + gk : Bm, ok);
       }
@@ -159,9 +169,19 @@ void small_gemm_bf16(int M, int N, int K, const __nv_bfloat16* A, int64_t lda, c
              SL_ERR_INVALID_ARGUMENT,
              "small_gemm_bf16: K, lda, ldb (and N for a [K, N] B) multiples of 8, 16 B aligned operands");
   if (M <= 0 || N <= 0) return;
+  static bool configured = false;  // > 48 KB dynamic shared memory needs the opt-in, once per process
+  if (!configured) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(small_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_bytes<true>()));
+    SL_CUDA_TRY(cudaFuncSetAttribute(small_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_bytes<false>()));
+    configured = true;
+  }
   const dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
-  if (b_kn) small_gemm_kernel<true><<<grid, kThreads, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias);
-  else small_gemm_kernel<false><<<grid, kThreads, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias);
+  if (b_kn)
+    small_gemm_kernel<true><<<grid, kThreads, smem_bytes<true>(), st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias);
+  else
+    small_gemm_kernel<false><<<grid, kThreads, smem_bytes<false>(), st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
