@@ -60,9 +60,16 @@ CASES = [(4, 7, 5, 12, 16, 8, 16, 8, 11), (16, 23, 9, 20, 64, 32, 48, 24, 50),
          (8, 60, 60, 620, 2000, 1000, 1000, 1000, 300)]
 
 
-@pytest.mark.parametrize("dims", CASES)
-def test_decoder_matches_restatement(cuda, dims):
+# edge cases: long sources (Ts > 128: the softmax's looped tail, several energy / context
+# tiles per row) with a length-1 source row; the largest batch one call takes (256); one target step
+EDGE = [((3, 300, 6, 12, 16, 8, 16, 8, 11), [300, 1, 137]), ((256, 5, 3, 8, 8, 8, 8, 8, 7), None),
+        ((5, 129, 2, 8, 24, 16, 8, 16, 9), [129, 128, 1, 64, 2]), ((4, 7, 1, 8, 8, 8, 8, 8, 5), None)]
+
+
+def check_against_restatement(dims, lens_override=None):
     P, enc_x, lens, ids, d_ro = make_case(sum(dims), *dims)
+    if lens_override is not None:
+        lens = np.asarray(lens_override, dtype=np.int32)
     ro, grads, d_enc = run_gpu(dims, P, enc_x, lens, ids, d_ro)
     # the relu derivative as the GPU saw it: bf16 operands may round a pre-activation
     # within its error of 0 to the other side (each such flip moves a whole readout_W
@@ -80,6 +87,16 @@ def test_decoder_matches_restatement(cuda, dims):
             assert abs(float(grads[n]) - float(g[n][0])) < 1e-3 * max(1.0, np.abs(g["e_W"]).max()), n
             continue
         assert rel(grads[n], g[n]) < TOL, (n, rel(grads[n], g[n]))
+
+
+@pytest.mark.parametrize("dims", CASES)
+def test_decoder_matches_restatement(cuda, dims):
+    check_against_restatement(dims)
+
+
+@pytest.mark.parametrize("dims,lens", EDGE)
+def test_decoder_edge_cases_match_restatement(cuda, dims, lens):
+    check_against_restatement(dims, lens)
 
 
 def test_decoder_deterministic_and_masked(cuda):
