@@ -4,9 +4,10 @@
 // 0.5 GFLOP GEMMs are bound by fixed costs, not by the tensor pipe: the tcgen05
 // pair GEMM spends ~10 us on launch, TMEM / barrier setup and a split-K partial
 // epilogue; this kernel has no setup, no split and writes the final fp32 result
-// once (128 CTAs of 128 threads; a 3-deep cp.async pipeline over 128-wide K tiles —
-// the K loop is latency-bound: few, wide K steps beat many narrow ones: 6.7-7.6 us
-// against 8.1-8.3 us for 6 x 32-wide and 7.6-7.8 us for 4 x 128-wide stages).
+// once (128 CTAs of 128 threads; a double-buffered cp.async pipeline over 256-wide K
+// tiles — the K loop is latency-bound: few, wide K steps beat many narrow ones:
+// 6.3-6.6 us per call against 6.7-7.6 us for 3 x 128-wide, 7.6-7.8 us for 4 x 128-wide
+// and 8.1-8.3 us for 6 x 32-wide stages; 3 x 256-wide is no faster).
 //   C[M, N] = A[M, K] op(B) (+ bias[N]);  A row-major (lda);
 //   b_kn: B stored [K, N] row-major (ldb), else B stored [N, K] row-major (ldb).
 // K, lda, ldb multiples of 8 (16 B rows); N arbitrary; fp32 C (ldc).
@@ -16,7 +17,7 @@
 namespace sl {
 namespace {
 
-constexpr int BM = 32, BN = 64, BK = 128, kThreads = 128;
+constexpr int BM = 32, BN = 64, BK = 256, kThreads = 128;
 constexpr int APAD = BK + 8;  // smem row pitch (elements) of the A and [N][K] B tiles: conflict-free ldmatrix
 constexpr int BPAD = BN + 8;  // smem row pitch of the [K][N] B tile
 
@@ -32,7 +33,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kStages = 3;  // K tiles in flight: the K loop is latency-, not compute-bound
+constexpr int kStages = 2;  // K tiles in flight: the K loop is latency-, not compute-bound
 constexpr int kAVec = BM * BK / 8 / kThreads;                         // 16 B vectors per thread per A tile
 constexpr int kBVec = BN * BK / 8 / kThreads;                         // ... per B tile
 constexpr int kSA = BM * APAD, kSBkn = BK * BPAD, kSBnk = BN * APAD;  // elements per stage
