@@ -436,9 +436,33 @@ def run_ours(args, rank, world, local_rank):
                 e2e=e2e, eager_ms=eager_ms / args.steps, graph=graph is not None)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start the N ranks ourselves (one
+    process per GPU, torch.distributed.run on 127.0.0.1) with the same
+    arguments; NCCL_DEBUG=INFO so each rank's communicator lines (nranks=N)
+    are in the log.  Returns the launcher's exit code."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     L, B, T, D0, H = args.layers, args.batch, args.time, args.input, args.hidden
@@ -481,6 +505,7 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks=N) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     r = run_ours(args, rank, world, local_rank)
     tokens = world * B * T * args.steps
@@ -537,7 +562,7 @@ def main():
            "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
            "data": "synthetic (x ~ U(-1,1), params ~ U(+-1/sqrt(H)), dy ~ U(-1,1))",
-           "config": dict(cfg, cuda_graph=r["graph"], eager_ms_per_step=r["eager_ms"]),
+           "config": cfg, "cuda_graph": r["graph"], "eager_ms_per_step": r["eager_ms"],
            "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
            "roofline": roof,
            "algorithmic_tflops": flops_per_token(L, D0, H, args.vocab, args.attention, T) * B * T * world / (r["ms"] / args.steps / 1e3) / 1e12}

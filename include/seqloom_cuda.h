@@ -237,7 +237,9 @@ int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params
  *   x [B, T, D] fp32, targets [B, T] int32 in [0, V), W [D, V], b [V];
  *   *loss (device float); dx [B, T, D], dW [D, V], db [V] may be NULL;
  *   *bad_target (device int32) is set when a valid position's id is out of
- *   range (the reference raises IndexError naming the layer).
+ *   range (the reference raises IndexError naming the layer); the loss and
+ *   that row's dZ are then NaN, so every gradient is non-finite and
+ *   sl_adam_step leaves the parameters untouched.
  * bf16 tensor-core GEMMs with fp32 accumulation; the fp32 logits are never
  * written to HBM (bf16 logits + fused online-softmax statistics). */
 size_t sl_output_ce_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab);
@@ -265,9 +267,11 @@ int sl_dropout_bwd(int32_t batch, int32_t time, int32_t features, float rate, ui
  * The reference's Linear layer on ids = gather_rows(table, ids) (compiler.cpp:
  * 584-589, tape.cpp:448-492): row r of out (row stride out_ld) = table[ids[r]],
  * table [vocab, dim] fp32.  An id outside [0, vocab) is the reference's
- * IndexError naming the layer: the row is zero-filled and *bad_row (device
- * int32) receives the first offending row (INT32_MAX when every id is valid) —
- * the host raises after synchronising.  Flags:
+ * IndexError naming the layer: the row is filled with NaN (so the step's loss
+ * and gradients become non-finite and sl_adam_step skips the update, as the
+ * reference raises before any update) and *bad_row (device int32) receives the
+ * first offending row (INT32_MAX when every id is valid) — the host raises
+ * after synchronising.  Flags:
  *   SL_EMB_ONES_COLUMN   (bf16 only) also write 1.0 at column dim and zeros up
  *                        to out_ld: the padded layer-0 LSTM input of a layer
  *                        flagged SL_LAYER_X_BF16 (out_ld = sl_lstm_bf16_pitch(dim))

@@ -136,7 +136,16 @@ class Reference:
         if hasattr(L, "ref_output_ce"):
             L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
                                         [c, ctypes.c_int])
+        if hasattr(L, "ref_param_manifest_order"):
+            L.ref_param_manifest_order.argtypes = [c, c, ctypes.c_int, c, ctypes.c_int]
         self.bits = 8 * L.ref_real_bytes()
+
+    def param_manifest_order(self, names):
+        """The reference ParamStore::manifest() order of these parameter names."""
+        out = ctypes.create_string_buffer(sum(len(n) + 1 for n in names) + 16)
+        err = ctypes.create_string_buffer(512)
+        self._check(self.lib.ref_param_manifest_order("\n".join(names).encode(), out, len(out), err, 512), err)
+        return [n for n in out.value.decode().split("\n") if n]
 
     @staticmethod
     def _check(rc, err):

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "seqloom/layers.hpp"
+#include "seqloom/param_store.hpp"
 #include "seqloom/rng.hpp"
 #include "seqloom/tape.hpp"
 
@@ -59,6 +60,30 @@ NodeId sum_all(Tape& t, NodeId v) {
 extern "C" {
 
 int ref_real_bytes() { return static_cast<int>(sizeof(Real)); }
+
+// The reference ParamStore's manifest order (param_store.hpp:12, 40-45) for the
+// '\n'-separated names in `names`: written back '\n'-separated into out.
+int ref_param_manifest_order(const char* names, char* out, int outlen, char* err, int errlen) {
+  try {
+    ParamStore ps;
+    std::string all(names), cur;
+    for (char ch : all + "\n") {
+      if (ch == '\n') {
+        if (!cur.empty()) ps.insert(cur, Tensor::zeros(Shape{{Axis::Feature, 1}}));
+        cur.clear();
+      } else {
+        cur += ch;
+      }
+    }
+    std::string res;
+    for (const auto& [name, shape] : ps.manifest()) res += name + "\n";
+    if ((int)res.size() + 1 > outlen) throw std::runtime_error("ref_param_manifest_order: out too small");
+    std::memcpy(out, res.c_str(), res.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
 
 // One LSTM layer over [B, T, D].  dy == nullptr → forward only.
 int ref_lstm_sequence(int B, int T, int D, int H, int direction, const double* x,

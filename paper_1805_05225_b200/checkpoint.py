@@ -7,6 +7,11 @@ SURVEY §8 f4): a directory with
   params.bin  little-endian 32-bit floats of every parameter, concatenated in
               manifest order
 
+The manifest order is the reference ParamStore's: lexicographic by name
+(param_store.hpp:12 — a std::map<std::string, ...>, so byte-wise order, which
+"fixes the checkpoint serialization order"), whatever order the parameters
+have in the flat device buffer; loading maps back by name.
+
 Parameter names follow the reference (compiler.cpp:488-492 `{layer}/W|R|b`).
 The flat device buffer is copied to the host once per save / load.  As an
 extension the Adam moments and step go to `adam.bin` (same layout, m then v),
@@ -23,6 +28,11 @@ import numpy as np
 import torch
 
 FORMAT_VERSION = 1
+
+
+def ordered(manifest):
+    """The manifest in the reference ParamStore's iteration order (byte-wise by name)."""
+    return sorted(manifest, key=lambda m: m[0].encode())
 
 
 def _manifest_json(manifest):
@@ -53,6 +63,7 @@ def _scatter(data: np.ndarray, flat: torch.Tensor, manifest) -> None:
 def save(directory: str, params: torch.Tensor, manifest, optimizer=None, epoch: int = 0, lr: float | None = None,
          pretrain_stage: int = 0, rng_state=None, best_cv: float | None = None) -> None:
     os.makedirs(directory, exist_ok=True)
+    manifest = ordered(manifest)
     _gather(params, manifest).tofile(os.path.join(directory, "params.bin"))
     meta = {"format_version": FORMAT_VERSION, "config_hash": config_hash(manifest),
             "params": _manifest_json(manifest), "epoch": epoch,
@@ -75,6 +86,7 @@ def load(directory: str, params: torch.Tensor, manifest, optimizer=None) -> dict
     """Read a checkpoint into the flat buffer (and optimizer state when present).
     The manifest must match name for name and shape for shape, like the
     reference's loader; returns meta.json."""
+    manifest = ordered(manifest)
     with open(os.path.join(directory, "meta.json")) as f:
         meta = json.load(f)
     if meta.get("format_version") != FORMAT_VERSION:

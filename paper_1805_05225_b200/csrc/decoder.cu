@@ -906,6 +906,7 @@ int ksplit_for(int M, int N, int K, int max_split = kMaxSplit) {
 
 struct Lay {
   int PZ, PXA, OA, PRO, PK, PR, PRF, PDR;  // PDR: pitch of the [DZ | d readout] rows
+  int PH;  // pitch of the d s = d s_tr W_s^T partials (H columns)
   int ks_f, ks_s, ks_1, ks_2;
   bool small;
   int ctx_blocks;
@@ -929,6 +930,7 @@ Lay layout(const DecDims& d, void* base) {
   L.OA = (int)round_up(d.H + d.Emb + 1, 8);
   L.PRO = (int)round_up(L.OA + d.E, 64);
   L.PK = (int)round_up(d.K, 64);
+  L.PH = (int)round_up(d.H, 64);
   L.PR = (int)round_up(d.Rd, 64);
   L.PRF = L.PRO;
   L.PDR = L.PZ + L.PR;
@@ -986,7 +988,7 @@ Lay layout(const DecDims& d, void* base) {
   L.pf = tf((int64_t)L.ks_f * d.B * 4 * d.H);
   L.pstr = tf((int64_t)L.ks_s * d.B * L.PK);
   L.p1 = tf((int64_t)L.ks_1 * d.B * (d.E + d.H));
-  L.p2 = tf((int64_t)L.ks_2 * d.B * L.PK);
+  L.p2 = tf((int64_t)L.ks_2 * d.B * L.PH);
   L.c_all = tf(BT * d.H);
   L.gates = tf(BT * 5 * d.H);
   L.str_all = tf((int64_t)d.T * d.B * d.K);
@@ -1229,13 +1231,13 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
       q.reset(new Phase(ss, "k10_g2_gemm", 2.0 * nb * H * K));
       if (L.small)  // d s += d s_tr W_s^T on the small-M GEMM
         small_gemm_bf16(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, L.wstr, L.PK, false,
-                        L.p2 + (int64_t)b0 * L.PK, L.PK, nullptr, ss);
+                        L.p2 + (int64_t)b0 * L.PH, L.PH, nullptr, ss);
       else
         gemm_split(mk(nb, H, K, L.ds + ((int64_t)t * B + b0) * L.PK, L.PK, false, L.wstr, L.PK, false,
-                      L.p2 + (int64_t)b0 * L.PK, L.PK),
-                   L.ks_2, (int64_t)B * L.PK, ss);
-      CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PK,
-                 (int64_t)B * L.PK, L.dro, L.PRF, L.gates, L.c_all,
+                      L.p2 + (int64_t)b0 * L.PH, L.PH),
+                   L.ks_2, (int64_t)B * L.PH, ss);
+      CellBwd cb{B, T, H, E, t, last ? 0 : L.ks_1, L.p1, E + H, (int64_t)B * (E + H), L.ks_2, L.p2, L.PH,
+                 (int64_t)B * L.PH, L.dro, L.PRF, L.gates, L.c_all,
                  last ? nullptr : L.dc + (int64_t)((t + 1) % 2) * B * H, L.dc + (int64_t)(t % 2) * B * H, L.dz, L.PDR,
                  b0, nb};
       q.reset(new Phase(ss, "k10_cell_bwd", 0.0, 4.0 * nb * H * (4 * L.ks_1 + 4 * L.ks_2 + 16)));

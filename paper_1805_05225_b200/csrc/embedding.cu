@@ -27,12 +27,16 @@ namespace sl {
 namespace {
 
 // ids < 0 with SL_EMB_NEGATIVE_ZERO: a zero row, no error (the decoder's
-// "previous target" at t = 0, the reference's initial_output = 0, models.cpp:96)
-__device__ __forceinline__ bool id_ok(int id, int V, int flags, int64_t r, int lane, int* bad_row) {
-  if (id >= 0 && id < V) return true;
-  if (id < 0 && (flags & SL_EMB_NEGATIVE_ZERO)) return false;
+// "previous target" at t = 0, the reference's initial_output = 0, models.cpp:96).
+// Any other id outside [0, V) is the reference's IndexError: the row is filled
+// with NaN so the step's loss and gradients are non-finite and a fused optimizer
+// step skips the update (the reference raises before touching any parameter).
+enum IdClass { kIdOk = 0, kIdZero = 1, kIdBad = 2 };
+__device__ __forceinline__ int id_class(int id, int V, int flags, int64_t r, int lane, int* bad_row) {
+  if (id >= 0 && id < V) return kIdOk;
+  if (id < 0 && (flags & SL_EMB_NEGATIVE_ZERO)) return kIdZero;
   if (lane == 0) atomicMin(bad_row, (int)min(r, (int64_t)INT32_MAX));  // IndexError (tape.cpp:464-467)
-  return false;
+  return kIdBad;
 }
 
 __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ ids, int V, int D,
@@ -43,8 +47,10 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ ids, int V,
   if (r >= n) return;
   const int id = ids[r];
   float* dst = out + r * ld;
-  if (!id_ok(id, V, flags, r, lane, bad_row)) {
-    for (int j = lane; j < D; j += 32) dst[j] = 0.f;
+  const int cls = id_class(id, V, flags, r, lane, bad_row);
+  if (cls != kIdOk) {
+    const float fill = cls == kIdBad ? __int_as_float(0x7fc00000) : 0.f;
+    for (int j = lane; j < D; j += 32) dst[j] = fill;
     return;
   }
   const float* src = table + (int64_t)id * D;
@@ -66,14 +72,16 @@ __global__ void gather_bf16_kernel(int64_t n, const int32_t* __restrict__ ids, i
   const int lane = threadIdx.x % 32;
   if (r >= n) return;
   const int id = ids[r];
-  const bool ok = id_ok(id, V, flags, r, lane, bad_row);
+  const int cls = id_class(id, V, flags, r, lane, bad_row);
+  const bool ok = cls == kIdOk;
+  const float fill = cls == kIdBad ? __int_as_float(0x7fc00000) : 0.f;  // NaN poisons a bad id's row
   const float* src = table + (int64_t)(ok ? id : 0) * D;
   __nv_bfloat16* dst = out + r * ld;
   const bool ones = flags & SL_EMB_ONES_COLUMN;
   const int64_t end = ones ? ld : D;
   if ((ld % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
     for (int64_t j = 2 * lane; j < end; j += 64) {
-      float a = 0.f, b = 0.f;
+      float a = j < D ? fill : 0.f, b = j + 1 < D ? fill : 0.f;
       if (ok && j < D) a = __ldg(src + j);
       if (ok && j + 1 < D) b = __ldg(src + j + 1);
       if (ones && j == D) a = 1.f;
@@ -83,7 +91,7 @@ __global__ void gather_bf16_kernel(int64_t n, const int32_t* __restrict__ ids, i
     }
   } else {
     for (int64_t j = lane; j < end; j += 32)
-      dst[j] = __float2bfloat16_rn(ok && j < D ? __ldg(src + j) : (ones && j == D ? 1.f : 0.f));
+      dst[j] = __float2bfloat16_rn(ok && j < D ? __ldg(src + j) : j < D ? fill : (ones && j == D ? 1.f : 0.f));
   }
 }
 

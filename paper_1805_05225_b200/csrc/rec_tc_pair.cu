@@ -48,6 +48,7 @@ constexpr int kMaxStages = 8;
 constexpr uint32_t kChunk = 128 * 64 * 2;   // 128 rows x 64 K bf16
 constexpr uint32_t kXwGate = 128 * 32 * 2;  // x W tile of one gate: 128 rows x 32 units bf16
 constexpr uint32_t kSmemMax = 227 * 1024;
+constexpr int kGrpCtrs = 32;                // step counters per (direction, batch tile): one per K group
 
 uint32_t pair_smem(int Kp, int stages, int kb) {
   return (uint32_t)kNHalf * Kp * 2 + stages * kChunk * kb + 1024;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int gunits = a.kb * 64;
   const int kc_off = (a.debug_flags & 128) ? (u0 / gunits) % ngrp
                      : (a.debug_flags & 256) ? (u0 / gunits + ngrp / 2) % ngrp : pair % ngrp;
-  unsigned* ctr = a.bar + (d * 2 + r) * 16;
+  unsigned* ctr = a.bar + (d * 2 + r) * kGrpCtrs;
   auto group_pairs = [&](int g) {  // pairs publishing into K group g
     return max(0, min(gunits / kPairUnits, a.P - g * (gunits / kPairUnits)));
   };
@@ -459,6 +460,8 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   for (int st = kMaxStages; st >= 2 && !a.stages; --st)
     if (pair_smem(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_pair: R slice does not fit in shared memory");
+  SL_REQUIRE(a.Kp / 64 / a.kb <= kGrpCtrs && 4 * kGrpCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
+             "rec_fwd_pair: too many K groups for the step counters");
   const uint32_t smem = pair_smem(a.Kp, a.stages, a.kb);
   SL_CUDA_TRY(cudaFuncSetAttribute(rec_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];

@@ -69,7 +69,14 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(__nv_bfloat16* __restrict_
   }
   const int y = targets[row];
   if (y < 0 || y >= V) {  // reference: IndexError naming the layer (tape.cpp:1265-1268)
-    if (lane == 0) atomicMax(bad_target, 1);
+    // poison the step: a NaN loss and NaN dZ row make every gradient non-finite, so
+    // the fused optimizer step skips the update (the reference raises before it)
+    if (lane == 0) {
+      atomicMax(bad_target, 1);
+      atomicAdd(&sc->loss_sum, (double)__int_as_float(0x7fc00000));
+    }
+    const __nv_bfloat16 nan = __float2bfloat16_rn(__int_as_float(0x7fc00000));
+    for (int j = lane; j < V; j += 32) z[j] = nan;
     return;
   }
   float m = -INFINITY;

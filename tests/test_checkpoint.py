@@ -27,10 +27,11 @@ def test_checkpoint_round_trip_and_layout(tmp_path):
     opt = _Opt(62)
     checkpoint.save(str(tmp_path), flat, manifest, optimizer=opt, epoch=3, best_cv=1.25)
     meta = json.load(open(tmp_path / "meta.json"))
-    assert [p["name"] for p in meta["params"]] == [m[0] for m in manifest]
-    assert meta["params"][0]["shape"] == [3, 8] and meta["epoch"] == 3 and meta["best_cv"] == 1.25
+    # the reference ParamStore's order: lexicographic by name (param_store.hpp:12), R < W < b
+    assert [p["name"] for p in meta["params"]] == ["enc0_fw/R", "enc0_fw/W", "enc0_fw/b", "src/W"]
+    assert meta["params"][1]["shape"] == [3, 8] and meta["epoch"] == 3 and meta["best_cv"] == 1.25
     raw = np.fromfile(tmp_path / "params.bin", dtype="<f4")  # manifest order, no gaps
-    want = np.concatenate([flat[o:o + int(np.prod(s))].numpy() for _, o, s in manifest])
+    want = np.concatenate([flat[o:o + int(np.prod(s))].numpy() for _, o, s in checkpoint.ordered(manifest)])
     assert np.array_equal(raw, want)
     flat2, opt2 = torch.zeros(62), _Opt(62)
     opt2.m.zero_(), opt2.v.zero_(), opt2.set_device_step(0)
@@ -44,3 +45,24 @@ def test_checkpoint_round_trip_and_layout(tmp_path):
         bad = list(manifest)
         bad[1] = ("enc0_fw/R", 24, (8, 2))
         checkpoint.load(str(tmp_path), flat2, bad)
+
+
+def test_checkpoint_order_is_the_reference_param_store_order(tmp_path):
+    """The whole Listing-1 model's manifest serialises in ParamStore::manifest()
+    order (the reference itself, oracle/_ref: a std::map, param_store.hpp:12)."""
+    oracle = pytest.importorskip("oracle")
+    try:
+        ref = oracle.Reference(32)
+    except FileNotFoundError:
+        pytest.skip("reference build absent")
+    from paper_1805_05225_b200.decoder import NAMES
+    names = [f"enc{l}_{d}/{n}" for l in range(6) for d in ("fw", "bw") for n in ("W", "R", "b")]
+    names += [r for _, r in NAMES] + ["output/output_prob/W", "output/output_prob/b", "src/W"]
+    manifest, off = [], 0
+    for n in names:
+        manifest.append((n, off, (2,)))
+        off += 2
+    flat = torch.arange(off, dtype=torch.float32)
+    checkpoint.save(str(tmp_path), flat, manifest)
+    meta = json.load(open(tmp_path / "meta.json"))
+    assert [p["name"] for p in meta["params"]] == ref.param_manifest_order(names)
