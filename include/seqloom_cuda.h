@@ -82,6 +82,16 @@ int sl_version(void);
 /* Last error message of the calling thread ("" when none). */
 const char* sl_last_error(void);
 
+/* Which kernels a descriptor runs on (0 = invalid descriptor, see sl_last_error):
+ *   SL_PATH_BF16_TC     SL_PREC_BF16: bf16 tcgen05 GEMMs and persistent recurrences
+ *   SL_PATH_FP32_X3_TC  SL_PREC_FP32 on the tensor cores: split-bf16 ("x3") tcgen05
+ *                       GEMMs and recurrences, A B = A_hi B_hi + A_lo B_hi + A_hi B_lo
+ *                       with fp32 accumulation (relative error ~1e-5), fp32 state
+ *   SL_PATH_FP32_SIMT   SL_PREC_FP32 for hidden sizes the x3 recurrences do not
+ *                       cover: fp32 CUDA-core GEMMs and recurrences */
+enum sl_path { SL_PATH_BF16_TC = 1, SL_PATH_FP32_X3_TC = 2, SL_PATH_FP32_SIMT = 3 };
+int sl_lstm_layer_path(const sl_lstm_layer* layer);
+
 /* Validate a descriptor: SL_OK, or the error (and message) fwd/bwd would raise. */
 int sl_lstm_layer_check(const sl_lstm_layer* layer);
 
@@ -229,6 +239,22 @@ int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params
                         const float* d_readout, float* d_enc, void* workspace, size_t workspace_bytes,
                         sl_stream_t stream);
 
+/* The same decoder at the reference's precision (SL_PREC_FP32 semantics, rel.
+ * 1e-4): enc is the fp32 encoder output [B, Ts, enc_dim] (contiguous), every
+ * product runs on the split-bf16 tcgen05 GEMM (A B = A_hi B_hi + A_lo B_hi +
+ * A_hi B_lo, fp32 accumulation), the cell state, attention and activations
+ * are fp32.  Same descriptor, parameters and gradients as above; no batch or
+ * width limits beyond src_time <= 4096.  The workspace carries the forward's
+ * saved activations to the backward. */
+size_t sl_attn_decoder_f32_workspace_size(const sl_attn_decoder* dec);
+int sl_attn_decoder_fwd_f32(const sl_attn_decoder* dec, const sl_attn_decoder_params* params, const float* enc,
+                            const int32_t* src_lens, const int32_t* prev_ids, float* readout, int32_t* bad_row,
+                            void* workspace, size_t workspace_bytes, sl_stream_t stream);
+int sl_attn_decoder_bwd_f32(const sl_attn_decoder* dec, const sl_attn_decoder_params* params,
+                            const sl_attn_decoder_grads* grads, const float* enc, const int32_t* src_lens,
+                            const int32_t* prev_ids, const float* readout, const float* d_readout, float* d_enc,
+                            void* workspace, size_t workspace_bytes, sl_stream_t stream);
+
 /* ---- output layer + loss ---------------------------------------
  * The decoder's Softmax layer and its training loss in one call: logits =
  * x W + b (reference compiler.cpp:651-663), log_softmax (tape.cpp:879-924),
@@ -247,6 +273,15 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
                  const int32_t* targets, const int32_t* seq_lens, const float* W, const float* b,
                  float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
                  void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream);
+
+/* The same at the reference's precision (SL_PREC_FP32 semantics, rel. 1e-4):
+ * fp32 logits in the workspace, every GEMM on the split-bf16 tcgen05 path (x3),
+ * expf / logf softmax statistics.  db requires dW. */
+size_t sl_output_ce_f32_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab);
+int sl_output_ce_f32(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, const float* x,
+                     const int32_t* targets, const int32_t* seq_lens, const float* W, const float* b,
+                     float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
+                     void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream);
 
 /* ---- input dropout (the output_prob layer's, models.hpp:18) --------------------
  * The reference's counter-based Tape::dropout (tape.cpp:540-600, applied by

@@ -49,7 +49,8 @@ def sequence(x, lens, W, R, b, direction, dy=None, dh_last=None, dc_last=None):
         h = o * tc
         hs.append(h)
         cs.append(c)
-        acts.append((i, f, g, o, tc))
+        if dy is not None:  # forward-only calls keep no per-step activations
+            acts.append((i, f, g, o, tc))
     Hs = torch.stack(hs[1:], 1)                               # [B, T, H] processing order
     valid = torch.arange(T, device=dev).unsqueeze(0) < lens.long().unsqueeze(1)
     y = torch.zeros(B, T, H, dtype=torch.float64, device=dev)

@@ -80,10 +80,28 @@ Dims dims(const sl_lstm_layer* L) {
   return Dims{L->batch, L->time, L->input_dim, L->hidden, L->num_dirs, L->flags};
 }
 
+int sm_count();
+
+// SL_PREC_FP32 runs on the tensor cores as split-bf16 ("x3": every product
+// A B = A_hi B_hi + A_lo B_hi + A_hi B_lo, fp32 accumulation) whenever the x3
+// recurrences support the hidden size; the SIMT fp32 kernels cover the rest.
+bool use_x3(const Dims& d, int prec) {
+  return prec == SL_PREC_FP32 && tc_rec_fwd_x3_shape(d.H, sm_count()).C > 0 &&
+         tc_rec_bwd_x3_shape(d.H, sm_count()).C > 0;
+}
+int64_t g4(const Dims& d) { return 4 * (int64_t)d.H; }
+size_t x3_gemm_ws(const Dims& d, bool bwd) {
+  const int M = (int)d.BT(), G = 4 * d.H, Gc = d.nd * G;
+  if (!bwd) return gemm_f32x3_workspace_bytes(false, false, M, Gc, d.D, false);
+  return std::max({gemm_f32x3_workspace_bytes(false, true, M, d.D, Gc, false),   // dX = DZ Wcat^T
+                   gemm_f32x3_workspace_bytes(true, false, d.D, G, M, true),     // [dW; db] = [X | 1]^T DZ_d
+                   gemm_f32x3_workspace_bytes(true, false, d.H, G, M, false)});  // dR = Hprev^T DZ_d
+}
+
 struct ReserveView {
   float* gates[2] = {nullptr, nullptr};
   float* cprev[2] = {nullptr, nullptr};
-  float* hprev[2] = {nullptr, nullptr};
+  float* hprev[2] = {nullptr, nullptr};  // fp32 paths: h_{s-1} [B*T, H]
   __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
   __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
   __nv_bfloat16* hprevb[2] = {nullptr, nullptr};  // bf16 path: h_{s-1} [B*T, Hp]
@@ -125,6 +143,10 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
     if (prec == SL_PREC_BF16) {
       r.gatesb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * 4 * save_hq(d.H));  // step-major, rec_tc.h
       r.cprevb[k] = c.take<__nv_bfloat16>((size_t)d.BT() * save_hq(d.H));
+    } else if (use_x3(d, prec)) {  // x3: the same step-major saves in fp32
+      r.gates[k] = c.take<float>((size_t)d.BT() * 4 * save_hq(d.H));
+      r.cprev[k] = c.take<float>((size_t)d.BT() * save_hq(d.H));
+      r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
     } else {
       r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
       r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
@@ -157,6 +179,10 @@ struct FwdWork {
   __nv_bfloat16* wcat = nullptr;
   __nv_bfloat16* rt[2] = {nullptr, nullptr};
   __nv_bfloat16* hbufb[2] = {nullptr, nullptr};  // bf16 path: h ring [2][B][Kp]
+  __nv_bfloat16* hbuflo[2] = {nullptr, nullptr};  // x3 path: lo halves of h, same ring layout
+  __nv_bfloat16* rtx3[2] = {nullptr, nullptr};    // x3 path: packed R^T hi + lo
+  float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
+  void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
   unsigned* bar = nullptr;
 };
 
@@ -178,6 +204,19 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
       w.rt[k] = c.take<__nv_bfloat16>(tc_rec_pack_elems(sh));
       w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, sh));
     }
+  } else if (use_x3(d, prec)) {
+    const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count());
+    w.xw_ld = d.nd * g4(d);
+    float* xw = c.take<float>((size_t)d.BT() * w.xw_ld);
+    for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * g4(d) : nullptr;
+    w.bcat = c.take<float>((size_t)w.xw_ld);
+    w.wcatf = c.take<float>((size_t)d.D * w.xw_ld);
+    w.gws = c.take<char>(x3_gemm_ws(d, false));
+    for (int k = 0; k < d.nd; ++k) {
+      w.rtx3[k] = c.take<__nv_bfloat16>(tc_rec_x3_pack_elems(sh));
+      w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, sh));
+      w.hbuflo[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, sh));
+    }
   } else {
     w.xw_ld = 4 * d.H;
     for (int k = 0; k < d.nd; ++k) {
@@ -197,6 +236,10 @@ struct BwdWork {
   __nv_bfloat16* dzb = nullptr;           // bf16 path: DZ of both directions [B*T, nd*G4p]
   __nv_bfloat16* dzring[2] = {nullptr, nullptr};  // bf16 path: DZ ring (rec_tc.h dz_ring_off)
   __nv_bfloat16* rb[2] = {nullptr, nullptr};      // bf16 path: packed R row slices
+  __nv_bfloat16* dzringlo[2] = {nullptr, nullptr};  // x3 path: lo halves of DZ, same ring layout
+  float* dzf = nullptr;                           // x3 path: DZ of both directions fp32 [B*T, nd*4H]
+  float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
+  void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
   unsigned* bar = nullptr;
 };
 
@@ -213,6 +256,16 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
       w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
       w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(sh));
     }
+  } else if (use_x3(d, prec)) {
+    const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count());
+    w.dzf = c.take<float>((size_t)d.BT() * d.nd * g4(d));
+    w.wcatf = c.take<float>((size_t)d.D * d.nd * g4(d));
+    w.gws = c.take<char>(x3_gemm_ws(d, true));
+    for (int k = 0; k < d.nd; ++k) {
+      w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
+      w.dzringlo[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
+      w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_x3_pack_elems(sh));
+    }
   } else {
     for (int k = 0; k < d.nd; ++k) {
       w.dz[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
@@ -226,6 +279,130 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
 
 int dir_sign(const sl_lstm_layer* L, int k) {
   return L->num_dirs == 2 ? (k == 0 ? 1 : -1) : L->direction;
+}
+
+
+// out[c] = beta * out[c] + sum_r x[r * ld + c] (ascending r)
+__global__ void colsum_f32_kernel(int rows, int cols, const float* __restrict__ x, int64_t ld, float beta,
+                                  float* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += x[(int64_t)r * ld + c];
+  out[c] = beta != 0.f ? beta * out[c] + s : s;
+}
+
+// ---- SL_PREC_FP32 on the tensor cores (split-bf16 "x3") ------------------------
+// K1: XW = X [W_fw | W_bw] + [b_fw | b_bw] as ONE fp32-class GEMM (fp32 out);
+// K2: the x3 pair recurrence, one launch per direction.
+void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t* lens, const float* const* W,
+            const float* const* R, const float* const* b, float* y, float* h_last, float* c_last,
+            const ReserveView& rv, const FwdWork& w, cudaStream_t st) {
+  const int64_t G = g4(d), Gc = d.nd * G;
+  for (int k = 0; k < d.nd; ++k) {
+    SL_CUDA_TRY(cudaMemcpy2DAsync(w.wcatf + k * G, Gc * sizeof(float), W[k], G * sizeof(float),
+                                  G * sizeof(float), d.D, cudaMemcpyDeviceToDevice, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(w.bcat + k * G, b[k], G * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  {
+    Phase ph(st, "k1_xw_gemm", 2.0 * d.BT() * d.D * (double)Gc);
+    gemm_f32x3(false, false, (int)d.BT(), (int)Gc, d.D, x, d.D, w.wcatf, Gc, 0.f, w.xw[0], Gc, w.bcat, nullptr, 0,
+               w.gws, st);
+  }
+  const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count());
+  for (int k = 0; k < d.nd; ++k) {
+    TcRecFwdArgs a{};
+    a.B = d.B;
+    a.T = d.T;
+    a.H = d.H;
+    a.nd = 1;
+    a.dir0 = k;
+    a.dirsign[0] = dir_sign(L, k);
+    a.lens = lens;
+    a.xwf[0] = w.xw[k];
+    a.xw_ld = Gc;
+    a.y = y;
+    a.y_ld = (int64_t)d.nd * d.H;
+    a.h_last = h_last;
+    a.c_last = c_last;
+    a.gatesf[0] = rv.gates[k];
+    a.cprevf[0] = rv.cprev[k];
+    a.hprevf[0] = rv.hprev[k];
+    a.hprev_ld = d.H;
+    a.hbuf[0] = w.hbufb[k];
+    a.hbuf_lo[0] = w.hbuflo[k];
+    a.bar = w.bar;
+    tc_rec_x3_pack(R[k], d.H, sh, w.rtx3[k], st);
+    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
+    SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
+    SL_CUDA_TRY(cudaMemsetAsync(w.hbuflo[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
+    Phase ph(st, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H);
+    rec_fwd_pair_x3(a, sh, w.rtx3[k], st);
+  }
+}
+
+// K3: the x3 BPTT, one launch per direction, DZ of both directions side by side in
+// fp32; K4: dX = DZ Wcat^T, [dW; db] = [X | 1]^T DZ_d, dR = Hprev_d^T DZ_d, fp32-class.
+void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t* lens, const float* const* W,
+            const float* const* R, const float* dy, const float* dh_last, const float* dc_last, float* dx,
+            float* const* dW, float* const* dR, float* const* db, float beta, const ReserveView& rv,
+            const BwdWork& w, cudaStream_t st) {
+  const int64_t G = g4(d), Gc = d.nd * G;
+  const int M = (int)d.BT();
+  const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count());
+  for (int k = 0; k < d.nd; ++k) {
+    TcRecBwdArgs a{};
+    a.B = d.B;
+    a.T = d.T;
+    a.H = d.H;
+    a.nd = 1;
+    a.dir0 = k;
+    a.dirsign[0] = dir_sign(L, k);
+    a.lens = lens;
+    a.dy = dy;
+    a.dy_ld = (int64_t)d.nd * d.H;
+    a.dh_last = dh_last;
+    a.dc_last = dc_last;
+    a.gatesf[0] = rv.gates[k];
+    a.cprevf[0] = rv.cprev[k];
+    a.dzring[0] = w.dzring[k];
+    a.dzring_lo[0] = w.dzringlo[k];
+    a.dzcatf = w.dzf;
+    a.dzcat_ld = Gc;
+    a.dz_dir_off = G;
+    a.bar = w.bar;
+    tc_rec_bwd_x3_pack(R[k], d.H, sh, w.rb[k], st);
+    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
+    SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
+    SL_CUDA_TRY(cudaMemsetAsync(w.dzringlo[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
+    Phase ph(st, "k3_rec_bwd", 2.0 * d.BT() * d.H * 4.0 * d.H);
+    rec_bwd_x3(a, sh, w.rb[k], st);
+  }
+  if (dx) {
+    for (int k = 0; k < d.nd; ++k)
+      SL_CUDA_TRY(cudaMemcpy2DAsync(w.wcatf + k * G, Gc * sizeof(float), W[k], G * sizeof(float),
+                                    G * sizeof(float), d.D, cudaMemcpyDeviceToDevice, st));
+    Phase ph(st, "k4_dx_gemm", 2.0 * M * (double)Gc * d.D);
+    gemm_f32x3(false, true, M, d.D, (int)Gc, w.dzf, Gc, w.wcatf, Gc, beta, dx, d.D, nullptr, nullptr, 0, w.gws, st);
+  }
+  for (int k = 0; k < d.nd; ++k) {
+    float* dbk = db ? db[k] : nullptr;
+    if ((dW && dW[k]) || dbk) {
+      Phase ph(st, "k4_dw_gemm", 2.0 * M * (double)G * d.D);
+      if (dW && dW[k]) {
+        gemm_f32x3(true, false, d.D, (int)G, M, x, d.D, w.dzf + k * G, Gc, beta, dW[k], G, nullptr, dbk, G, w.gws, st);
+      } else {  // db alone: fixed-order column sums of DZ_d
+        colsum_f32_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, w.dzf + k * G, Gc, beta, dbk);
+        SL_CUDA_TRY(cudaGetLastError());
+        count_launch();
+      }
+    }
+    if (dR && dR[k]) {
+      Phase ph(st, "k4_dr_gemm", 2.0 * M * (double)G * d.H);
+      gemm_f32x3(true, false, d.H, (int)G, M, rv.hprev[k], d.H, w.dzf + k * G, Gc, beta, dR[k], G, nullptr, nullptr,
+                 0, w.gws, st);
+    }
+  }
 }
 
 template <typename F>
@@ -359,6 +536,29 @@ int sl_output_ce(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, 
   });
 }
 
+size_t sl_output_ce_f32_workspace_size(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab) {
+  if (batch <= 0 || time <= 0 || input_dim <= 0 || vocab <= 0) return 0;
+  return output_ce_f32_workspace_bytes(batch, time, input_dim, vocab);
+}
+
+int sl_output_ce_f32(int32_t batch, int32_t time, int32_t input_dim, int32_t vocab, const float* x,
+                     const int32_t* targets, const int32_t* seq_lens, const float* W, const float* b,
+                     float epsilon, float* loss, float* dx, float* dW, float* db, int accumulate,
+                     void* workspace, size_t workspace_bytes, int32_t* bad_target, sl_stream_t stream) {
+  return guarded([&] {
+    SL_REQUIRE(epsilon >= 0.f && epsilon < 1.f, SL_ERR_INVALID_ARGUMENT,
+               "label smoothing epsilon must be in [0, 1)");  // reference tape.cpp:1226-1228
+    SL_REQUIRE(batch > 0 && time > 0 && input_dim > 0 && vocab > 0, SL_ERR_SHAPE,
+               "output_ce: log_probs must end in Feature axis (B, T, D, V > 0)");
+    SL_REQUIRE(x && targets && seq_lens && W && b && loss && bad_target, SL_ERR_INVALID_ARGUMENT,
+               "output_ce: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= output_ce_f32_workspace_bytes(batch, time, input_dim, vocab),
+               SL_ERR_WORKSPACE, "output_ce: workspace too small");
+    output_ce_f32(batch, time, input_dim, vocab, x, targets, seq_lens, W, b, epsilon, loss, dx, dW, db,
+                  accumulate != 0, workspace, bad_target, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
 size_t sl_embedding_workspace_size(int64_t n_ids, int32_t vocab) {
   if (n_ids < 0 || vocab <= 0) return 0;
   return embedding_workspace_bytes(n_ids, vocab);
@@ -482,6 +682,59 @@ int sl_attn_decoder_bwd(const sl_attn_decoder* dec, const sl_attn_decoder_params
   });
 }
 
+size_t sl_attn_decoder_f32_workspace_size(const sl_attn_decoder* dec) {
+  try {
+    const DecDims d = dec_dims(dec);
+    decoder_f32_check(d);
+    set_error("");
+    return decoder_f32_workspace_bytes(d);
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return 0;
+  }
+}
+
+int sl_attn_decoder_fwd_f32(const sl_attn_decoder* dec, const sl_attn_decoder_params* params, const float* enc,
+                            const int32_t* src_lens, const int32_t* prev_ids, float* readout, int32_t* bad_row,
+                            void* workspace, size_t workspace_bytes, sl_stream_t stream) {
+  return guarded([&] {
+    const DecDims d = dec_dims(dec);
+    decoder_f32_check(d);
+    const DecParams p = dec_params(params);
+    SL_REQUIRE(enc && src_lens && prev_ids && readout && bad_row, SL_ERR_INVALID_ARGUMENT,
+               "attn_decoder: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= decoder_f32_workspace_bytes(d), SL_ERR_WORKSPACE,
+               "attn_decoder: workspace too small");
+    decoder_f32_fwd(d, p, enc, src_lens, prev_ids, readout, bad_row, workspace, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int sl_attn_decoder_bwd_f32(const sl_attn_decoder* dec, const sl_attn_decoder_params* params,
+                            const sl_attn_decoder_grads* grads, const float* enc, const int32_t* src_lens,
+                            const int32_t* prev_ids, const float* readout, const float* d_readout, float* d_enc,
+                            void* workspace, size_t workspace_bytes, sl_stream_t stream) {
+  return guarded([&] {
+    const DecDims d = dec_dims(dec);
+    decoder_f32_check(d);
+    const DecParams p = dec_params(params);
+    SL_REQUIRE(grads, SL_ERR_INVALID_ARGUMENT, "attn_decoder: null grads");
+    const sl_attn_decoder_grads& q = *grads;
+    float* all[] = {q.enc_ctx_W, q.enc_ctx_b, q.s_W, q.s_R, q.s_b, q.fb_W, q.fb_b,
+                    q.s_tr_W, q.s_tr_b, q.e_W, q.e_b, q.readout_W, q.readout_b, q.trg_W};
+    for (float* x : all)
+      SL_REQUIRE(x && ((uintptr_t)x & 15) == 0, SL_ERR_INVALID_ARGUMENT,
+                 "attn_decoder: gradient pointers must be non-null and 16 B aligned");
+    SL_REQUIRE(enc && src_lens && prev_ids && readout && d_readout && d_enc, SL_ERR_INVALID_ARGUMENT,
+               "attn_decoder: null pointer argument");
+    SL_REQUIRE(workspace && workspace_bytes >= decoder_f32_workspace_bytes(d), SL_ERR_WORKSPACE,
+               "attn_decoder: workspace too small");
+    const DecGrads g{q.enc_ctx_W, q.enc_ctx_b, q.s_W, q.s_R, q.s_b, q.fb_W, q.fb_b,
+                     q.s_tr_W, q.s_tr_b, q.e_W, q.e_b, q.readout_W, q.readout_b, q.trg_W};
+    decoder_f32_bwd(d, p, g, enc, src_lens, prev_ids, readout, d_readout, d_enc, workspace,
+                    reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
 static int dropout_call(int32_t B, int32_t T, int32_t F, float rate, uint64_t key0, const int32_t* counter,
                         int64_t counter_value, const float* in, float* out, sl_stream_t stream) {
   return guarded([&] {
@@ -515,6 +768,18 @@ int sl_adam_step(int64_t n, float* params, const float* grads, float* m, float* 
 }
 
 const char* sl_last_error(void) { return g_last_error.c_str(); }
+
+int sl_lstm_layer_path(const sl_lstm_layer* L) {
+  int path = 0;
+  if (guarded([&] {
+        validate(L);
+        const Dims d = dims(L);
+        path = L->precision == SL_PREC_BF16 ? SL_PATH_BF16_TC : use_x3(d, L->precision) ? SL_PATH_FP32_X3_TC
+                                                                                        : SL_PATH_FP32_SIMT;
+      }) != SL_OK)
+    return 0;
+  return path;
+}
 
 int sl_lstm_layer_check(const sl_lstm_layer* L) {
   return guarded([&] { validate(L); });
@@ -564,6 +829,10 @@ int sl_lstm_layer_fwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
     if (reserve) {
       rv = carve_reserve(d, prec, reserve, &need_r);
       SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_fwd: reserve too small");
+    }
+    if (use_x3(d, prec)) {
+      fwd_x3(L, d, x, seq_lens, W, R, b, y, h_last, c_last, rv, w, stream);
+      return;
     }
     SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), stream));
     const double k1_flops = 2.0 * d.BT() * d.D * 4.0 * d.H * d.nd;
@@ -691,8 +960,12 @@ int sl_lstm_layer_bwd(const sl_lstm_layer* L, const float* x, const int32_t* seq
                "sl_lstm_layer_bwd: workspace too small");
     ReserveView rv = carve_reserve(d, prec, const_cast<void*>(reserve), &need_r);
     SL_REQUIRE(reserve_bytes >= need_r, SL_ERR_WORKSPACE, "sl_lstm_layer_bwd: reserve too small");
-    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), stream));
     const float beta = accumulate ? 1.f : 0.f;
+    if (use_x3(d, prec)) {
+      bwd_x3(L, d, x, seq_lens, W, R, dy, dh_last, dc_last, dx, dW, dR, db, beta, rv, w, stream);
+      return;
+    }
+    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), stream));
     const int M = (int)d.BT(), G = 4 * d.H;
     const double fx = 2.0 * M * G * (double)d.D;
     const double rec_flops = 2.0 * d.BT() * d.H * 4.0 * d.H * d.nd;
@@ -875,6 +1148,19 @@ extern "C" int sl_debug_small_gemm(int M, int N, int K, const void* A, int64_t l
   return guarded([&] {
     small_gemm_bf16(M, N, K, static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B), ldb,
                     b_kn != 0, C, ldc, bias, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" size_t sl_debug_gemm_f32x3_ws(int transA, int transB, int M, int N, int K) {
+  return gemm_f32x3_workspace_bytes(transA != 0, transB != 0, M, N, K, false);
+}
+
+extern "C" int sl_debug_gemm_f32x3(int transA, int transB, int M, int N, int K, const float* A, int64_t lda,
+                                   const float* B, int64_t ldb, float beta, float* C, int64_t ldc, const float* bias,
+                                   void* ws, sl_stream_t stream) {
+  return guarded([&] {
+    gemm_f32x3(transA != 0, transB != 0, M, N, K, A, lda, B, ldb, beta, C, ldc, bias, nullptr, 0, ws,
+               reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

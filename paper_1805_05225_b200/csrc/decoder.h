@@ -31,4 +31,14 @@ void decoder_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const 
                  int64_t ld_enc, const int32_t* src_lens, const int32_t* prev_ids, const float* readout,
                  const float* d_readout, float* d_enc, void* ws, cudaStream_t st);
 
+// SL_PREC_FP32 (decoder_f32.cu): fp32 encoder output [B, Ts, E] (contiguous),
+// every product on the split-bf16 tcgen05 GEMM, fp32 state and attention
+void decoder_f32_check(const DecDims& d);
+size_t decoder_f32_workspace_bytes(const DecDims& d);
+void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, const int32_t* src_lens,
+                     const int32_t* prev_ids, float* readout, int32_t* bad_row, void* ws, cudaStream_t st);
+void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const float* enc,
+                     const int32_t* src_lens, const int32_t* prev_ids, const float* readout, const float* d_readout,
+                     float* d_enc, void* ws, cudaStream_t st);
+
 }  // namespace sl

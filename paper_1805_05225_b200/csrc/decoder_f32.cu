@@ -1,0 +1,418 @@
+// The Listing-1 attention decoder at the reference's precision (SL_PREC_FP32):
+// the same computation as decoder.cu — the `output` subnetwork of models.cpp:
+// 83-166 run step by step with teacher forcing as compiler.cpp:770-905 does,
+// plus the base layer enc_ctx (models.cpp:60) —
+//
+//   enc_ctx = enc W_ctx + b_ctx                                   (once)
+//   for t:  s_t, c_t = lstm_step([trg_{t-1} ‖ att_{t-1}], s_{t-1}, c_{t-1})   (tape.cpp:1074-1141)
+//           s_tr = s_t W_s + b_s;  e = tanh(enc_ctx + accum_{t-1} W_fb + b_fb + s_tr) v + b_v
+//           a_t = softmax over the valid source positions;  accum_t = accum_{t-1} + a_t
+//           att_t = sum_j a_t[j] enc_j
+//   readout = relu([s ‖ trg_prev ‖ att] W_ro + b_ro)             (all t at once)
+//
+// with every product fp32-class: the split-bf16 tcgen05 GEMM (gemm_f32x3.cu,
+// A B = A_hi B_hi + A_lo B_hi + A_hi B_lo in fp32 TMEM, relative error ~1e-5),
+// fp32 activations, cell state and attention (attention.cu, the 1e-4-tested
+// single-step kernels), expf / tanhf.
+//   * hoisted whole-sequence GEMMs: enc_ctx, trg_{t-1} W_trg + b for all t, the
+//     readout, and in the backward every weight gradient over all T*B rows, d trg
+//     and d enc through W_ctx;
+//   * per step only the recurrence: [att ‖ s]_{t-1} [W_att; R] (weights split
+//     once per call, only the [B, E+H] activations per step), the fused gate
+//     kernel, the attention step; the backward mirrors it (attention adjoint,
+//     gate adjoint, DZ_t [W_att; R]^T).
+// Time-major per-step buffers (row t*B + b), fixed-order reductions.
+#include <algorithm>
+
+#include "attention.h"
+#include "decoder.h"
+#include "embedding.h"
+#include "gemm.h"
+#include "profile.h"
+
+namespace sl {
+namespace {
+
+struct FLay {
+  int64_t XA, RO;  // row pitches: [att ‖ s] (E + H), readout input [s ‖ trg ‖ att] (H + Emb + E)
+  float *xw, *xa, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all, *z;
+  float *dro, *dpre, *dz, *dxa, *dc, *ds, *datt, *dacc, *dctx, *dtrg;
+  float* w2;  // [E + H, 4H] staging of [W_att; R]
+  int32_t* ids_tm;
+  __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
+  void *att_ws, *gws, *emb_ws;
+  size_t bytes;
+};
+
+size_t gemm_ws_bytes(const DecDims& d) {
+  const int B = d.B, H = d.H, E = d.E, K = d.K, Emb = d.Emb, Rd = d.Rd;
+  const int BT = B * d.T, BTs = B * d.Ts, XA = E + H, RO = H + Emb + E;
+  return std::max({gemm_f32x3_workspace_bytes(false, false, BTs, K, E, false),      // enc_ctx
+                   gemm_f32x3_workspace_bytes(false, false, BT, 4 * H, Emb, false),  // trg W_trg + b
+                   gemm_f32x3_workspace_bytes(false, false, B, 4 * H, XA, false),    // z (presplit B)
+                   gemm_f32x3_workspace_bytes(false, true, B, XA, 4 * H, false),     // d xa (presplit B)
+                   gemm_f32x3_workspace_bytes(false, false, BT, Rd, RO, false),      // readout
+                   gemm_f32x3_workspace_bytes(false, true, BT, RO, Rd, false),       // d readout input
+                   gemm_f32x3_workspace_bytes(true, false, RO, Rd, BT, true),        // [d W_ro; d b_ro]
+                   gemm_f32x3_workspace_bytes(true, false, E, 4 * H, BT, false),     // d W_att
+                   gemm_f32x3_workspace_bytes(true, false, H, 4 * H, BT, false),     // d R
+                   gemm_f32x3_workspace_bytes(true, false, Emb, 4 * H, BT, true),    // [d W_trg; d b]
+                   gemm_f32x3_workspace_bytes(false, true, BT, Emb, 4 * H, false),   // d trg
+                   gemm_f32x3_workspace_bytes(true, false, E, K, BTs, true),         // [d W_ctx; d b_ctx]
+                   gemm_f32x3_workspace_bytes(false, true, BTs, E, K, false)});      // d enc += d enc_ctx W_ctx^T
+}
+
+FLay flayout(const DecDims& d, void* base) {
+  FLay L{};
+  const int64_t B = d.B, T = d.T, H = d.H, E = d.E, K = d.K;
+  const int64_t BT = B * T, BTs = B * d.Ts;
+  L.XA = E + H;
+  L.RO = H + d.Emb + E;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    off = round_up(off, 256);
+    void* r = p ? p + off : nullptr;
+    off += bytes;
+    return r;
+  };
+  auto tf = [&](int64_t n) { return static_cast<float*>(take((size_t)n * 4)); };
+  L.xw = tf(BT * 4 * H);
+  L.xa = tf((T + 1) * B * L.XA);
+  L.ro = tf(BT * L.RO);
+  L.s_all = tf(BT * H);
+  L.att_all = tf(BT * E);
+  L.c_all = tf(BT * H);
+  L.gates = tf(BT * 5 * H);
+  L.enc_ctx = tf(BTs * K);
+  L.a_all = tf(T * B * d.Ts);
+  L.acc_all = tf((T + 1) * B * d.Ts);
+  L.z = tf(B * 4 * H);
+  L.dro = tf(BT * L.RO);
+  L.dpre = tf(BT * d.Rd);
+  L.dz = tf(BT * 4 * H);
+  L.dxa = tf(B * L.XA);
+  L.dc = tf(2 * B * H);
+  L.ds = tf(B * H);
+  L.datt = tf(B * E);
+  L.dacc = tf(2 * B * d.Ts);
+  L.dctx = tf(BTs * K);
+  L.dtrg = tf(BT * d.Emb);
+  L.w2 = tf(L.XA * 4 * H);
+  L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
+  L.wd2_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)(4 * H), (int)L.XA) * 2));
+  L.wd2_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)L.XA, (int)(4 * H)) * 2));
+  L.att_ws = take(attention_workspace_bytes(d.B, d.K, d.H, d.Ts));
+  L.gws = take(gemm_ws_bytes(d));
+  L.emb_ws = take(embedding_workspace_bytes(BT, d.Vt));
+  L.bytes = off + 256;
+  return L;
+}
+
+__global__ void f32_ids_tm_kernel(const int32_t* __restrict__ ids, int B, int T, int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * T) return;
+  const int t = (int)(i / B), b = (int)(i % B);
+  out[i] = ids[(int64_t)b * T + t];
+}
+
+// the cell at step t (tape.cpp:1095-1135): z = [att ‖ s]_{t-1} [W_att; R] (null at t = 0) +
+// trg_{t-1} W_trg + b; s_t into s_all, the next step's [att ‖ s] row and the readout input
+struct GateF {
+  int B, T, H, E, t;
+  const float* z;    // [B, 4H] or null
+  const float* xw;   // [T*B, 4H]
+  float *gates, *c_all, *s_all;
+  float* xa;         // [(T+1)*B, XA]
+  int64_t XA;
+  float* ro;         // [T*B, RO]
+  int64_t RO;
+};
+__global__ void f32_cell_fwd_kernel(GateF a) {
+  const int64_t n = (int64_t)a.B * a.H;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int b = (int)(e / a.H), j = (int)(e % a.H), H = a.H;
+  const int64_t row = (int64_t)a.t * a.B + b;
+  const float* x = a.xw + row * 4 * H;
+  float z[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) z[g] = x[g * H + j] + (a.z ? a.z[(int64_t)b * 4 * H + g * H + j] : 0.f);
+  const float cp = a.t > 0 ? a.c_all[(row - a.B) * H + j] : 0.f;
+  const float gi = sigmoidf_(z[0]), gf = sigmoidf_(z[1]), gg = tanhf(z[2]), go = sigmoidf_(z[3]);
+  const float c = gf * cp + gi * gg;
+  const float tc = tanhf(c);
+  const float h = go * tc;
+  a.c_all[row * H + j] = c;
+  float* gs = a.gates + row * 5 * H + j;
+  gs[0] = gi, gs[H] = gf, gs[2 * H] = gg, gs[3 * H] = go, gs[4 * H] = tc;
+  a.s_all[row * H + j] = h;
+  a.ro[row * a.RO + j] = h;
+  a.xa[(row + a.B) * a.XA + a.E + j] = h;
+}
+
+// readout [b, t] = relu(pre [t*B + b])
+__global__ void f32_relu_kernel(const float* __restrict__ pre, float* __restrict__ out, int B, int T, int Rd) {
+  const int64_t n = (int64_t)B * T * Rd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Rd);
+    const int64_t bt = i / Rd;
+    const int b = (int)(bt / T), t = (int)(bt % T);
+    out[i] = fmaxf(pre[((int64_t)t * B + b) * Rd + c], 0.f);
+  }
+}
+
+// d pre [t*B + b] = d readout [b, t] * [readout > 0]
+__global__ void f32_relu_bwd_kernel(const float* __restrict__ ro, const float* __restrict__ dro,
+                                    float* __restrict__ dpre, int B, int T, int Rd) {
+  const int64_t n = (int64_t)B * T * Rd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Rd);
+    const int64_t bt = i / Rd;
+    const int b = (int)(bt / T), t = (int)(bt % T);
+    dpre[((int64_t)t * B + b) * Rd + c] = ro[i] > 0.f ? dro[i] : 0.f;
+  }
+}
+
+// the upstream gradients of step t: d att_t (readout + the cell at t + 1), d s_t (readout +
+// the cell at t + 1; the attention adds its d s_tr W_s^T)
+struct GradIn {
+  int B, H, E, t, has_next;
+  const float* dro;  // [T*B, RO]
+  int64_t RO;
+  int Emb;
+  const float* dxa;  // [B, XA]: d [att ‖ s]_t from the cell at t + 1
+  int64_t XA;
+  float *datt, *ds;
+};
+__global__ void f32_grad_in_kernel(GradIn a) {
+  const int W = a.E + a.H;
+  const int64_t n = (int64_t)a.B * W;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int b = (int)(e / W), c = (int)(e % W);
+  const float* r = a.dro + ((int64_t)a.t * a.B + b) * a.RO;
+  if (c < a.E) {
+    float v = r[a.H + a.Emb + c];
+    if (a.has_next) v += a.dxa[(int64_t)b * a.XA + c];
+    a.datt[(int64_t)b * a.E + c] = v;
+  } else {
+    const int j = c - a.E;
+    float v = r[j];
+    if (a.has_next) v += a.dxa[(int64_t)b * a.XA + a.E + j];
+    a.ds[(int64_t)b * a.H + j] = v;
+  }
+}
+
+// the cell adjoint at step t (tape.cpp:1157-1170): gh = d s_t, gc = d c_t -> DZ_t, d c_{t-1}
+struct CellBF {
+  int B, H, t;
+  const float *ds, *gates, *c_all, *dc_in;
+  float *dz, *dc_out;
+};
+__global__ void f32_cell_bwd_kernel(CellBF a) {
+  const int64_t n = (int64_t)a.B * a.H;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int b = (int)(e / a.H), j = (int)(e % a.H), H = a.H;
+  const int64_t row = (int64_t)a.t * a.B + b;
+  const float gh = a.ds[e], gc = a.dc_in ? a.dc_in[e] : 0.f;
+  const float* gs = a.gates + row * 5 * H + j;
+  const float gi = gs[0], gf = gs[H], gg = gs[2 * H], go = gs[3 * H], tc = gs[4 * H];
+  const float cp = a.t > 0 ? a.c_all[(row - a.B) * H + j] : 0.f;
+  const float d_o = gh * tc;
+  const float dc = gc + gh * go * (1.f - tc * tc);
+  a.dc_out[e] = dc * gf;
+  float* dz = a.dz + row * 4 * H + j;
+  dz[0] = dc * gg * gi * (1.f - gi);
+  dz[H] = dc * cp * gf * (1.f - gf);
+  dz[2 * H] = dc * gi * (1.f - gg * gg);
+  dz[3 * H] = d_o * go * (1.f - go);
+}
+
+unsigned grid_of(int64_t n) { return (unsigned)ceil_div(n, 256); }
+
+AttnArgs att_args(const DecDims& d, const FLay& L, const DecParams& p, const float* enc, const int32_t* lens,
+                  int t) {
+  AttnArgs a{};
+  a.B = d.B;
+  a.Ts = d.Ts;
+  a.K = d.K;
+  a.E = d.E;
+  a.H = d.H;
+  a.lens = lens;
+  a.enc_ctx = L.enc_ctx;
+  a.enc = enc;
+  a.accum = L.acc_all + (int64_t)t * d.B * d.Ts;  // accum_{t-1}
+  a.W_fb = p.fb_W;
+  a.b_fb = p.fb_b;
+  a.v = p.e_W;
+  a.b_v = p.e_b;
+  return a;
+}
+
+}  // namespace
+
+size_t decoder_f32_workspace_bytes(const DecDims& d) { return flayout(d, nullptr).bytes; }
+
+void decoder_f32_check(const DecDims& d) {
+  SL_REQUIRE(d.B > 0 && d.Ts > 0 && d.T > 0 && d.Emb > 0 && d.E > 0 && d.H > 0 && d.K > 0 && d.Rd > 0 && d.Vt > 0,
+             SL_ERR_SHAPE, "attn_decoder: dimensions must be positive");
+  SL_REQUIRE(d.Ts <= 4096, SL_ERR_UNSUPPORTED, "attn_decoder (fp32): src_time <= 4096");
+}
+
+void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, const int32_t* src_lens,
+                     const int32_t* prev_ids, float* readout, int32_t* bad_row, void* ws, cudaStream_t st) {
+  decoder_f32_check(d);
+  const FLay L = flayout(d, ws);
+  const int B = d.B, T = d.T, H = d.H, E = d.E, K = d.K, Emb = d.Emb;
+  const int64_t BT = (int64_t)B * T, BTs = (int64_t)B * d.Ts;
+  {
+    Phase ph(st, "k10_dec_fwd_hoisted", 2.0 * BTs * E * K + 2.0 * BT * Emb * 4 * H);
+    SL_CUDA_TRY(cudaMemsetAsync(L.xa, 0, sizeof(float) * B * L.XA, st));  // [att ‖ s]_{-1} = 0
+    SL_CUDA_TRY(cudaMemsetAsync(L.acc_all, 0, sizeof(float) * BTs, st));  // accum_{-1} = 0
+    // [W_att; R] (rows Emb.. of s/W stacked on s/R) split once into the two K-tripled
+    // images the per-step GEMMs read, through an fp32 staging copy of the stacked matrix
+    {
+      float* w2 = L.w2;
+      SL_CUDA_TRY(cudaMemcpyAsync(w2, p.s_W + (int64_t)Emb * 4 * H, sizeof(float) * E * 4 * H,
+                                  cudaMemcpyDeviceToDevice, st));
+      SL_CUDA_TRY(cudaMemcpyAsync(w2 + (int64_t)E * 4 * H, p.s_R, sizeof(float) * H * 4 * H,
+                                  cudaMemcpyDeviceToDevice, st));
+      x3_split_b(false, 4 * H, E + H, w2, 4 * H, L.wd2_f, st);
+      x3_split_b(true, E + H, 4 * H, w2, 4 * H, L.wd2_b, st);
+    }
+    f32_ids_tm_kernel<<<grid_of(BT), 256, 0, st>>>(prev_ids, B, T, L.ids_tm);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    // trg_{t-1} straight into the readout-input rows (columns H..H+Emb)
+    embedding_fwd(BT, L.ids_tm, d.Vt, Emb, p.trg_W, L.ro + H, L.RO, SL_EMB_NEGATIVE_ZERO, bad_row, st);
+    gemm_f32x3(false, false, (int)BTs, K, E, enc, E, p.ctx_W, K, 0.f, L.enc_ctx, K, p.ctx_b, nullptr, 0, L.gws, st);
+    gemm_f32x3(false, false, (int)BT, 4 * H, Emb, L.ro + H, L.RO, p.s_W, 4 * H, 0.f, L.xw, 4 * H, p.s_b, nullptr, 0,
+               L.gws, st);
+  }
+  for (int t = 0; t < T; ++t) {
+    if (t > 0) {
+      Phase q(st, "k10_cell_gemm", 2.0 * B * (E + H) * 4.0 * H);
+      gemm_f32x3_pb(false, false, B, 4 * H, E + H, L.xa + (int64_t)t * B * L.XA, L.XA, L.wd2_f, 0.f, L.z, 4 * H,
+                    nullptr, L.gws, st);
+    }
+    {
+      Phase q(st, "k10_cell_fwd", 0.0, 4.0 * B * H * 12);
+      GateF g{B, T, H, E, t, t > 0 ? L.z : nullptr, L.xw, L.gates, L.c_all, L.s_all, L.xa, L.XA, L.ro, L.RO};
+      f32_cell_fwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(g);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch();
+    }
+    AttnArgs a = att_args(d, L, p, enc, src_lens, t);
+    a.att = L.att_all + (int64_t)t * B * E;
+    a.a = L.a_all + (int64_t)t * B * d.Ts;
+    a.accum_out = L.acc_all + (int64_t)(t + 1) * B * d.Ts;
+    attention_fwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.att_ws, st);
+    // att_t -> the readout input (columns H + Emb..) and the next step's [att ‖ s] row
+    SL_CUDA_TRY(cudaMemcpy2DAsync(L.ro + (int64_t)t * B * L.RO + H + Emb, L.RO * 4, a.att, (size_t)E * 4,
+                                  (size_t)E * 4, B, cudaMemcpyDeviceToDevice, st));
+    if (t + 1 < T)
+      SL_CUDA_TRY(cudaMemcpy2DAsync(L.xa + (int64_t)(t + 1) * B * L.XA, L.XA * 4, a.att, (size_t)E * 4,
+                                    (size_t)E * 4, B, cudaMemcpyDeviceToDevice, st));
+  }
+  {
+    Phase ph(st, "k10_dec_fwd_hoisted", 2.0 * BT * L.RO * d.Rd);
+    gemm_f32x3(false, false, (int)BT, d.Rd, (int)L.RO, L.ro, L.RO, p.ro_W, d.Rd, 0.f, L.dpre, d.Rd, p.ro_b, nullptr,
+               0, L.gws, st);  // pre-activation (dpre is free until the backward)
+    f32_relu_kernel<<<std::min<unsigned>(grid_of(BT * d.Rd), 148 * 8), 256, 0, st>>>(L.dpre, readout, B, T, d.Rd);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+}
+
+void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, const float* enc,
+                     const int32_t* src_lens, const int32_t* prev_ids, const float* readout, const float* d_readout,
+                     float* d_enc, void* ws, cudaStream_t st) {
+  decoder_f32_check(d);
+  (void)prev_ids;  // the forward's time-major ids are in the workspace
+  const FLay L = flayout(d, ws);
+  const int B = d.B, T = d.T, H = d.H, E = d.E, K = d.K, Emb = d.Emb, Rd = d.Rd;
+  const int64_t BT = (int64_t)B * T, BTs = (int64_t)B * d.Ts;
+  {
+    Phase ph(st, "k10_dec_bwd_hoisted", 4.0 * BT * L.RO * Rd);
+    f32_relu_bwd_kernel<<<std::min<unsigned>(grid_of(BT * Rd), 148 * 8), 256, 0, st>>>(readout, d_readout, L.dpre,
+                                                                                         B, T, Rd);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    // d readout input = d pre W_ro^T; [d W_ro; d b_ro] = [X | 1]^T d pre
+    gemm_f32x3(false, true, (int)BT, (int)L.RO, Rd, L.dpre, Rd, p.ro_W, Rd, 0.f, L.dro, L.RO, nullptr, nullptr, 0,
+               L.gws, st);
+    gemm_f32x3(true, false, (int)L.RO, Rd, (int)BT, L.ro, L.RO, L.dpre, Rd, 0.f, g.ro_W, Rd, nullptr, g.ro_b, Rd,
+               L.gws, st);
+    // the attention adjoint accumulates over t into these
+    SL_CUDA_TRY(cudaMemsetAsync(L.dctx, 0, sizeof(float) * BTs * K, st));
+    SL_CUDA_TRY(cudaMemsetAsync(d_enc, 0, sizeof(float) * BTs * E, st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.fb_W, 0, sizeof(float) * K, st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.fb_b, 0, sizeof(float) * K, st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.e_W, 0, sizeof(float) * K, st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.e_b, 0, sizeof(float), st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.str_W, 0, sizeof(float) * H * K, st));
+    SL_CUDA_TRY(cudaMemsetAsync(g.str_b, 0, sizeof(float) * K, st));
+  }
+  for (int t = T - 1; t >= 0; --t) {
+    const int cur = t & 1, nxt = cur ^ 1;  // ping-pong: d c / d accum of step t in [cur], of t - 1 -> [nxt]
+    {
+      Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * (E + H) * 3);
+      GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, L.dxa, L.XA, L.datt, L.ds};
+      f32_grad_in_kernel<<<grid_of((int64_t)B * (E + H)), 256, 0, st>>>(gi);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch();
+    }
+    AttnArgs a = att_args(d, L, p, enc, src_lens, t);
+    a.a_saved = L.a_all + (int64_t)t * B * d.Ts;
+    a.d_att = L.datt;
+    a.d_accum_out = t + 1 < T ? L.dacc + (int64_t)cur * B * d.Ts : nullptr;
+    a.d_accum = L.dacc + (int64_t)nxt * B * d.Ts;
+    a.d_enc_ctx = L.dctx;
+    a.d_enc = d_enc;
+    a.d_W_fb = g.fb_W;
+    a.d_b_fb = g.fb_b;
+    a.d_v = g.e_W;
+    a.d_b_v = g.e_b;
+    a.accumulate = 1;  // every accumulator was zeroed above; d accum_{t-1} is zeroed per step
+    SL_CUDA_TRY(cudaMemsetAsync(a.d_accum, 0, sizeof(float) * B * d.Ts, st));
+    attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, g.str_W, g.str_b, L.att_ws, st);
+    {
+      Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 12);
+      CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, L.dz,
+                L.dc + (int64_t)nxt * B * H};
+      f32_cell_bwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(cb);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch();
+    }
+    if (t > 0) {  // d [att ‖ s]_{t-1} = DZ_t [W_att; R]^T
+      Phase q(st, "k10_g1_gemm", 2.0 * B * 4.0 * H * (E + H));
+      gemm_f32x3_pb(false, true, B, (int)L.XA, 4 * H, L.dz + (int64_t)t * B * 4 * H, 4 * H, L.wd2_b, 0.f, L.dxa,
+                    L.XA, nullptr, L.gws, st);
+    }
+  }
+  {
+    Phase ph(st, "k10_dec_bwd_hoisted",
+             2.0 * BT * 4 * H * (E + H + 2.0 * Emb) + 4.0 * BTs * E * K);
+    // the cell's weight gradients over all B*T rows: [W_att; R] from [att ‖ s]_{t-1} (block t of xa)
+    gemm_f32x3(true, false, E, 4 * H, (int)BT, L.xa, L.XA, L.dz, 4 * H, 0.f, g.s_W + (int64_t)Emb * 4 * H, 4 * H,
+               nullptr, nullptr, 0, L.gws, st);
+    gemm_f32x3(true, false, H, 4 * H, (int)BT, L.xa + E, L.XA, L.dz, 4 * H, 0.f, g.s_R, 4 * H, nullptr, nullptr, 0,
+               L.gws, st);
+    // [W_trg; b] from [trg_{t-1} | 1]
+    gemm_f32x3(true, false, Emb, 4 * H, (int)BT, L.ro + H, L.RO, L.dz, 4 * H, 0.f, g.s_W, 4 * H, nullptr, g.s_b,
+               4 * H, L.gws, st);
+    // d trg_{t-1} = DZ W_trg^T + the readout's trg columns -> the trg table
+    SL_CUDA_TRY(cudaMemcpy2DAsync(L.dtrg, (size_t)Emb * 4, L.dro + H, L.RO * 4, (size_t)Emb * 4, BT,
+                                  cudaMemcpyDeviceToDevice, st));
+    gemm_f32x3(false, true, (int)BT, Emb, 4 * H, L.dz, 4 * H, p.s_W, 4 * H, 1.f, L.dtrg, Emb, nullptr, nullptr, 0,
+               L.gws, st);
+    embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
+    // enc_ctx = enc W_ctx + b_ctx: [d W_ctx; d b_ctx] = [enc | 1]^T d enc_ctx; d enc += d enc_ctx W_ctx^T
+    gemm_f32x3(true, false, E, K, (int)BTs, enc, E, L.dctx, K, 0.f, g.ctx_W, K, nullptr, g.ctx_b, K, L.gws, st);
+    gemm_f32x3(false, true, (int)BTs, E, K, L.dctx, K, p.ctx_W, K, 1.f, d_enc, E, nullptr, nullptr, 0, L.gws, st);
+  }
+}
+
+}  // namespace sl

@@ -14,6 +14,14 @@ void gemm_f32(bool transA, bool transB, int M, int N, int K, float alpha, const 
 // stored [K, M] (transA) and the column sums of op(B) (= ones^T op(B)) are also
 // written to ones_row_out (+ beta * previous) — the bias gradient for free.
 size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K, bool a_ones);
+// B split once for repeated GEMMs (e.g. a weight used every time step): x3_split_b
+// writes the K-tripled bf16 image of op(B) (x3_b_elems elements); gemm_f32x3_pb then
+// splits only A per call (its scratch: gemm_f32x3_workspace_bytes of the same shape).
+size_t x3_b_elems(bool transB, int N, int K);
+void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfloat16* B3, cudaStream_t st);
+void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                   const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
+                   cudaStream_t st);
 void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
                 int64_t ld_ones, void* ws, cudaStream_t st);

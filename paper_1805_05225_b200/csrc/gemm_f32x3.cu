@@ -7,6 +7,8 @@
 // the tolerances the reference's fp32 CPU path is held to, at tensor-core
 // speed.  Used where a small fp32 GEMM would otherwise leave most SMs idle on
 // the SIMT path (the attention step's s W_s projections: M = batch).
+#include <algorithm>
+
 #include "convert.h"
 #include "gemm.h"
 #include "profile.h"
@@ -24,11 +26,11 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
 // ones_col >= 0 (K = rows only): that column is 1 (hi) / 0 (lo) for k < K.
 // One CTA row per (extended) source row, two contiguous columns per thread.
 __global__ void split3_kernel(const float* __restrict__ S, int64_t ld, int rows, int cols, bool k_cols, int Kp,
-                              int lo_mask, int ones_col, __nv_bfloat16* __restrict__ D, int64_t dld) {
-  const int r = blockIdx.y;
+                              int lo_mask, int ones_col, __nv_bfloat16* __restrict__ D, int64_t dld, int rows_ext) {
+  for (int r = blockIdx.y; r < rows_ext; r += gridDim.y) {  // (grid y is capped at 65535)
   const int cols_ext = k_cols ? Kp : cols + (ones_col >= 0 ? 1 : 0);
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c >= cols_ext) return;
+  if (c >= cols_ext) continue;
   float x[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -54,14 +56,16 @@ __global__ void split3_kernel(const float* __restrict__ S, int64_t ld, int rows,
       *dst = use_lo ? lo[0] : hi[0];
     }
   }
+  }
 }
 
 // C[m, n] = sum_z P[z][m, n] (fixed order: deterministic) + bias[n] + beta C[m, n]; rows >= m_split -> C2
-__global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t pstride, int64_t pld, int N,
+__global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t pstride, int64_t pld, int M, int N,
                                      float beta, float* C, int64_t ldc, const float* __restrict__ bias, int m_split,
                                      float* C2, int64_t ldc2) {
-  const int m = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
+  for (int m = blockIdx.y; m < M; m += gridDim.y) {  // (grid y is capped at 65535)
   const float* src = P + (int64_t)m * pld + n;
   float s = 0.f;
 #pragma unroll 4
@@ -70,6 +74,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t
   float* dst = m >= m_split ? C2 + (int64_t)(m - m_split) * ldc2 + n : C + (int64_t)m * ldc + n;
   if (beta != 0.f) s += beta * *dst;
   *dst = s;
+  }
 }
 
 struct X3Dims {
@@ -89,7 +94,16 @@ X3Dims x3_dims(bool transA, bool transB, int M, int N, int K, bool a_ones) {
   if (!transB) d.b_rows = 3 * (int64_t)d.Kp, d.b_ld = round_up(N, 64);
   else d.b_rows = N, d.b_ld = 3 * (int64_t)d.Kp;
   const int Mt = M + (a_ones ? 1 : 0);
-  d.ksplit = gemm_tc2_ksplit(Mt, N, 3 * d.Kp);
+  // The tensor core's fp32 accumulation is not round-to-nearest: its error grows
+  // linearly with the number of accumulated K steps (measured, scripts/x3_accuracy.py:
+  // ~3e-5 relative at K = 4096, ~1e-4 at 20000, ~3e-4 at 60000).  Long K is therefore
+  // split into ranges of <= kMaxKBlocks 64-wide blocks whose fp32 partials are summed
+  // in a fixed order on the CUDA cores (round-to-nearest): the error stays at the
+  // one-range level for any K.
+  constexpr int kMaxKBlocks = 48;
+  const int nk = (int)ceil_div(3 * (int64_t)d.Kp, 64);
+  const int want = std::max(gemm_tc2_ksplit(Mt, N, 3 * d.Kp), (int)ceil_div(nk, kMaxKBlocks));
+  d.ksplit = (int)ceil_div(nk, ceil_div(nk, want));
   d.p_ld = round_up(N, 4);
   d.p_stride = round_up((int64_t)Mt * d.p_ld, 64);
   return d;
@@ -99,8 +113,8 @@ void split3(const float* S, int64_t ld, int rows, int cols, bool k_cols, int Kp,
             __nv_bfloat16* D, int64_t dld, cudaStream_t st) {
   const int rows_ext = k_cols ? rows : Kp;
   const int cols_ext = k_cols ? Kp : cols + (ones_col >= 0 ? 1 : 0);
-  const dim3 grid((unsigned)ceil_div(cols_ext, 256), (unsigned)rows_ext);
-  split3_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld);
+  const dim3 grid((unsigned)ceil_div(cols_ext, 256), (unsigned)std::min(rows_ext, 65535));
+  split3_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld, rows_ext);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -113,23 +127,41 @@ size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K,
          (d.ksplit > 1 ? (size_t)d.ksplit * d.p_stride * 4 : 0);
 }
 
-void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
-                int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
-                int64_t ld_ones, void* ws, cudaStream_t st) {
+size_t x3_b_elems(bool transB, int N, int K) {
+  const X3Dims d = x3_dims(false, transB, 1, N, K, false);
+  return (size_t)(d.b_rows * d.b_ld);
+}
+
+void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfloat16* B3, cudaStream_t st) {
+  const X3Dims d = x3_dims(false, transB, 1, N, K, false);
+  if (!transB) split3(B, ldb, K, N, false, d.Kp, 0b100, -1, B3, d.b_ld, st);
+  else split3(B, ldb, N, K, true, d.Kp, 0b100, -1, B3, d.b_ld, st);
+}
+
+namespace {
+// the GEMM over split operands: a3 from the scratch, b3 split here or presplit
+void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
+             int64_t ldb, const __nv_bfloat16* b_pre, float beta, float* C, int64_t ldc, const float* bias,
+             float* ones_row_out, int64_t ld_ones, void* ws, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   const bool a_ones = ones_row_out != nullptr;
   SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
   const X3Dims d = x3_dims(transA, transB, M, N, K, a_ones);
   auto* a3 = static_cast<__nv_bfloat16*>(ws);
-  auto* b3 = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ws) + round_up(d.a_rows * d.a_ld * 2, 256));
+  char* after_a = static_cast<char*>(ws) + round_up(d.a_rows * d.a_ld * 2, 256);
+  const __nv_bfloat16* b3 = b_pre;
   // A copies: hi, lo, hi (lo_mask 0b010); B copies: hi, hi, lo (0b100)
   if (!transA) split3(A, lda, M, K, true, d.Kp, 0b010, -1, a3, d.a_ld, st);
   else split3(A, lda, K, M, false, d.Kp, 0b010, a_ones ? M : -1, a3, d.a_ld, st);
-  if (!transB) split3(B, ldb, K, N, false, d.Kp, 0b100, -1, b3, d.b_ld, st);
-  else split3(B, ldb, N, K, true, d.Kp, 0b100, -1, b3, d.b_ld, st);
+  if (!b3) {
+    auto* b3w = reinterpret_cast<__nv_bfloat16*>(after_a);
+    if (!transB) split3(B, ldb, K, N, false, d.Kp, 0b100, -1, b3w, d.b_ld, st);
+    else split3(B, ldb, N, K, true, d.Kp, 0b100, -1, b3w, d.b_ld, st);
+    b3 = b3w;
+  }
   TcGemm g{M + (a_ones ? 1 : 0), N, 3 * d.Kp, a3, d.a_ld, transA, b3, d.b_ld, !transB, C, ldc, 1.f, beta, bias};
   if (d.ksplit > 1) {  // small output: split K over the idle SMs, then a fixed-order reduction
-    float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(b3) + round_up(d.b_rows * d.b_ld * 2, 256));
+    float* part = reinterpret_cast<float*>(after_a + round_up(d.b_rows * d.b_ld * 2, 256));
     g.C = part;
     g.ldc = d.p_ld;
     g.beta = 0.f;
@@ -138,8 +170,8 @@ void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, i
     g.split_stride = d.p_stride;
     gemm_bf16_tc(g, st);
     const int Mt = M + (a_ones ? 1 : 0);
-    splitk_reduce_kernel<<<dim3((unsigned)ceil_div(N, 256), (unsigned)Mt), 256, 0, st>>>(
-        part, d.ksplit, d.p_stride, d.p_ld, N, beta, C, ldc, bias, a_ones ? M : (1 << 30), ones_row_out, ld_ones);
+    splitk_reduce_kernel<<<dim3((unsigned)ceil_div(N, 256), (unsigned)std::min(Mt, 65535)), 256, 0, st>>>(
+        part, d.ksplit, d.p_stride, d.p_ld, Mt, N, beta, C, ldc, bias, a_ones ? M : (1 << 30), ones_row_out, ld_ones);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
     return;
@@ -150,6 +182,19 @@ void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, i
     g.ldc2 = ld_ones;
   }
   gemm_bf16_tc(g, st);
+}
+}  // namespace
+
+void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
+                int64_t ld_ones, void* ws, cudaStream_t st) {
+  x3_core(transA, transB, M, N, K, A, lda, B, ldb, nullptr, beta, C, ldc, bias, ones_row_out, ld_ones, ws, st);
+}
+
+void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                   const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
+                   cudaStream_t st) {
+  x3_core(transA, transB, M, N, K, A, lda, nullptr, 0, B3, beta, C, ldc, bias, nullptr, 0, ws, st);
 }
 
 }  // namespace sl

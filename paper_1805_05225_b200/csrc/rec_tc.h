@@ -52,6 +52,13 @@ struct TcRecFwdArgs {
   unsigned long long* trace;  // optional per-step phase timestamps (debug), [T][8] for trace_cta
   int trace_cta;
   int xw_tma;       // pair kernel: x W tiles may be TMA-loaded (set internally)
+  // ---- fp32-class ("x3", split-bf16) pair kernel only: one direction per launch
+  int dir0;                      // global index of launch direction 0 (y columns, h_last / c_last rows)
+  const float* xwf[2];           // hoisted x W + b, fp32 [B*T, xw_ld]
+  __nv_bfloat16* hbuf_lo[2];     // lo halves of h (h - bf16(h)), same ring layout as hbuf (the hi halves)
+  float* gatesf[2];              // saved (i,f,g,o) fp32, step-major (gate_save_off)
+  float* cprevf[2];              // saved c_{s-1} fp32, step-major (cprev_save_off)
+  float* hprevf[2];              // saved h_{s-1} fp32 [B*T, hprev_ld]
   int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores,
                     // 4 = no step-counter waits (wrong results)
 };
@@ -89,6 +96,12 @@ struct TcRecBwdArgs {
   int trace_cta;
   int debug_flags;  // experiments only: 8 = skip the DZ copy for K4, 16 = skip dy / saved-activation
                     // loads (wrong results)
+  // ---- fp32-class ("x3") kernel only: one direction per launch
+  int dir0;                        // global index of launch direction 0 (dy columns, final-state rows)
+  const float* gatesf[2];          // saved (i,f,g,o) fp32 (K2 x3), step-major
+  const float* cprevf[2];          // saved c_{s-1} fp32, step-major
+  __nv_bfloat16* dzring_lo[2];     // lo halves of DZ (DZ - bf16(DZ)), dzring layout, zeroed
+  float* dzcatf;                   // out: DZ fp32 [B*T, dzcat_ld], dir (dir0 + d) at col (dir0 + d)*dz_dir_off
 };
 
 // K-split partition of the BPTT kernel: clusters of C CTAs, each finalizing U
@@ -108,6 +121,15 @@ size_t tc_rec_bwd_pair_pack_elems(const TcBwdShape& sh);
 void tc_rec_bwd_pair_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream);
 void rec_bwd_pair(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* const* RB, cudaStream_t stream);
 
+// fp32-class BPTT (split-bf16, "x3"): the K-split kernel with R resident as hi
+// and lo bf16 slices, DZ exchanged as hi and lo rings, dh = DZ_hi R_hi^T +
+// DZ_lo R_hi^T + DZ_hi R_lo^T in fp32 TMEM, fp32 partial exchange, saves and DZ.
+// One direction per launch.
+TcBwdShape tc_rec_bwd_x3_shape(int H, int sms);  // C == 0: unsupported
+size_t tc_rec_bwd_x3_pack_elems(const TcBwdShape& sh);  // hi rows then lo rows
+void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream);
+void rec_bwd_x3(const TcRecBwdArgs& a, const TcBwdShape& sh, const __nv_bfloat16* RB, cudaStream_t stream);
+
 // K-split partition of the forward kernel: clusters of C CTAs, each finalizing
 // U units (the cluster owns C*U units, MMA N = 4*C*U), P CTAs per direction,
 // Kp = H padded to 64*C.
@@ -126,5 +148,15 @@ void rec_fwd_tc(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* cons
 bool tc_rec_fwd_pair_fits(int H, int nd, int sms);
 void rec_fwd_pair(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                   cudaStream_t stream);
+
+// fp32-class forward recurrence (split-bf16, "x3"): the pair kernel with 16
+// units per pair, R^T resident as hi and lo bf16 slices, h exchanged as hi and
+// lo bf16 rings, z = h_hi R_hi + h_lo R_hi + h_hi R_lo accumulated in fp32
+// TMEM; fp32 x W, cell state, saves and outputs.  One direction per launch
+// (both directions' hi+lo R do not fit in shared memory at once).
+TcFwdShape tc_rec_fwd_x3_shape(int H, int sms);  // C == 0: unsupported
+size_t tc_rec_x3_pack_elems(const TcFwdShape& sh);   // one direction's packed R^T (hi rows, then lo rows)
+void tc_rec_x3_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT, cudaStream_t stream);
+void rec_fwd_pair_x3(const TcRecFwdArgs& a, const TcFwdShape& sh, const __nv_bfloat16* RT, cudaStream_t stream);
 
 }  // namespace sl

@@ -1,6 +1,6 @@
-// K3 — persistent tensor-core BPTT (SL_PREC_BF16 path): the mirror of K2.
+// K3 — persistent tensor-core BPTT: the mirror of K2.
 //
-// One launch runs all T steps of both directions backwards.  CTA c of
+// One launch runs all T steps of the launch's directions backwards.  CTA c of
 // direction d owns hidden units [c*U, c*U+U): it keeps R[units, :] (the rows
 // of R feeding those units' h, all 4H gate columns, bf16, K-major) resident in
 // shared memory, and per step s (descending):
@@ -12,10 +12,18 @@
 //   warps 2..   one/two threads per batch row: gh = dy + dh_rec, the cell-gate
 //               adjoint of tape.cpp:1157-1170 with the carried dc, writing
 //               DZ_s to the ring (for the next step) and to the [B*T, 8H]
-//               DZ matrix the hoisted K4 GEMMs consume; db is reduced on the fly.
+//               DZ matrix the hoisted K4 GEMMs consume.
 // As in K2 the two 128-row batch tiles are independent recurrences with their
 // own step counters, so one tile's epilogue overlaps the other's MMAs.
+// Two instantiations:
+//   X3 = false (SL_PREC_BF16): bf16 R / DZ / saves, both directions per launch;
+//   X3 = true  (SL_PREC_FP32, fp32-class): R resident as hi and lo bf16 slices,
+//              DZ as hi and lo rings, dh = DZ_hi R_hi^T + DZ_lo R_hi^T +
+//              DZ_hi R_lo^T accumulated in fp32 TMEM, fp32 partial exchange
+//              between the K-split CTAs, fp32 saves (K2 x3) and fp32 DZ for
+//              K4; one direction per launch.
 #include <cstdlib>
+#include <type_traits>
 
 #include "profile.h"
 #include "rec_tc.h"
@@ -32,10 +40,13 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 
 __host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
-uint32_t bwd_smem(int C, int U, int Kc, int stages) {  // stages of two 16 KB chunks
-  // per batch tile: [C-1 slots][128 rows][U] bf16 partials from the peers
-  const uint32_t recv = C > 1 ? (uint32_t)2 * (C - 1) * U * 128 * 2 : 0;
-  return (uint32_t)nb_of(C, U) * Kc * 2 + stages * kTile * 2 + recv + 1024;
+// stages of kb 16 KB chunks per precision part (the host passes the stage count
+// in units of two chunks for kb = 1, see launch_bwd)
+uint32_t bwd_smem(int C, int U, int Kc, int stages, bool x3 = false) {
+  const uint32_t parts = x3 ? 2 : 1;
+  // per batch tile: [C-1 slots][128 rows][U] partials from the peers (bf16, x3: fp32)
+  const uint32_t recv = C > 1 ? (uint32_t)2 * (C - 1) * U * 128 * (x3 ? 4 : 2) : 0;
+  return parts * (uint32_t)nb_of(C, U) * Kc * 2 + parts * stages * kTile * 2 + recv + 1024;
 }
 
 // C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
@@ -46,7 +57,7 @@ uint32_t bwd_smem(int C, int U, int Kc, int stages) {  // stages of two 16 KB ch
 // slower: the per-thread math and stores then sit on the critical path.)
 constexpr int bwd_split(int U) { return U >= 8 ? 2 : 1; }
 
-template <int C, int U, int MT, int SPLIT = bwd_split(U), int UT = U / SPLIT>
+template <int C, int U, int MT, bool X3, int SPLIT = bwd_split(U), int UT = U / SPLIT>
 __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     rec_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
                       const __grid_constant__ CUtensorMap tmR1,
@@ -54,7 +65,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                       const __grid_constant__ CUtensorMap tmZ1, TcRecBwdArgs a) {
   constexpr int NB = nb_of(C, U);  // MMA N: the cluster's units
   constexpr int kEpiTile = 128 * SPLIT;
-  constexpr uint32_t kRecvBytes = (uint32_t)(C - 1) * 128 * U * 2;  // per tile and use
+  constexpr int kParts = X3 ? 2 : 1;
+  using RecvT = typename std::conditional<X3, float, __nv_bfloat16>::type;
+  constexpr uint32_t kRecvBytes = (uint32_t)(C - 1) * 128 * U * sizeof(RecvT);  // per tile and use
   constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : (MT * NB <= 64) ? 64 : (MT * NB <= 128) ? 128 : 256;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
@@ -69,26 +82,30 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int cl = cta / C;                  // cluster index within the direction
   const int u0 = cl * C * U + r * U;       // first unit this CTA finalizes
   const int Kc = a.Kz / C;
+  // X3: tmZ0 = the hi ring, tmZ1 = the lo ring (one direction per launch)
   const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
-  const CUtensorMap* tmZ = d == 0 ? &tmZ0 : &tmZ1;
+  const CUtensorMap* tmZ = (X3 || d == 0) ? &tmZ0 : &tmZ1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
-  const uint32_t r_bytes = (uint32_t)NB * Kc * 2;
+  const uint32_t r_part = (uint32_t)NB * Kc * 2;  // one precision part of the R slice
+  const uint32_t r_bytes = r_part * kParts;
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
-  const uint32_t stage_bytes = kTile * a.kb;  // a.kb 64-wide K chunks per TMA box
-  // [MT][C-1 slots][128 rows][U] bf16 partials from the peers: one buffer per
+  const uint32_t part_bytes = kTile * a.kb;  // a.kb 64-wide K chunks per TMA box
+  const uint32_t stage_bytes = part_bytes * kParts;
+  // [MT][C-1 slots][128 rows][U] partials from the peers: one buffer per
   // batch tile (a shared buffer would couple the two tiles' recurrences through
   // its free/full handshake) and row-major, so each sender thread writes its
   // row's slice with 16 B DSMEM stores
-  __nv_bfloat16* recv = reinterpret_cast<__nv_bfloat16*>(sA + a.stages * stage_bytes);
+  RecvT* recv = reinterpret_cast<RecvT*>(sA + a.stages * stage_bytes);
   const int nkc = Kc / 64;
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
     tc::prefetch_tmap(tmR);
     tc::prefetch_tmap(tmZ);
+    if (X3) tc::prefetch_tmap(&tmZ1);
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
@@ -139,18 +156,17 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     }
     return n;
   };
-  // debug trace: one CTA (trace_cta >= 0, [T][16]) or every CTA (trace_cta < 0, [grid][T][16])
-  unsigned long long* trace =
-      (a.trace && (a.trace_cta < 0 || (int)blockIdx.x == a.trace_cta))
-          ? a.trace + (a.trace_cta < 0 ? (size_t)blockIdx.x * a.T * 16 : 0) : nullptr;
   const int ngrp = nkc / a.kb;  // TMA boxes per tile
   const int kc_off = cta % ngrp;
 
   if (warp == 0) {  // ---------------------------------------------- producer
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
-      for (int kc = 0; kc < nkc; ++kc)
+      for (int kc = 0; kc < nkc; ++kc) {
         tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
+        if constexpr (X3)  // the lo rows follow the P * NB hi rows
+          tc::tma_load_2d(sR + r_part + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, a.P * NB + cta * NB);
+      }
     }
     int st = 0;  // ring position, tracked by every lane (lane 0 issues)
     uint32_t ph = 0;
@@ -159,7 +175,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     // 16-unit chunk of the 4 gates and of c_{s-1}, all rows of the launch
     const int pf_u = (u0 / 16) * 16;
     const int pf_rows = min(a.B - a.b0, MT * 128);
-    const bool pf = a.gates[d] != nullptr && u0 < a.H && !(a.debug_flags & 32);
+    const bool pf = (X3 ? a.gatesf[d] != nullptr : a.gates[d] != nullptr) && u0 < a.H;
+    const uint32_t pf_elem = X3 ? 4 : 2;
     // lane k polls the k-th box of this CTA's K slice in issue order
     const int kg_lane = (lane + kc_off) % ngrp;
     const int gb_lane = r * (Kc / bw) + kg_lane;
@@ -169,9 +186,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       if (pf && lane == 0) {
         const int ps = Tmax - 1 - s;
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          prefetch_l2(a.gates[d] + gate_save_off(ps, g, a.b0, a.B, a.H, pf_u), pf_rows * 32);
-        prefetch_l2(a.cprev[d] + cprev_save_off(ps, a.b0, a.B, a.H, pf_u), pf_rows * 32);
+        for (int g = 0; g < 4; ++g) {
+          const size_t o = gate_save_off(ps, g, a.b0, a.B, a.H, pf_u);
+          if constexpr (X3) prefetch_l2(a.gatesf[d] + o, pf_rows * 16 * pf_elem);
+          else prefetch_l2(a.gates[d] + o, pf_rows * 16 * pf_elem);
+        }
+        const size_t o = cprev_save_off(ps, a.b0, a.B, a.H, pf_u);
+        if constexpr (X3) prefetch_l2(a.cprevf[d] + o, pf_rows * 16 * pf_elem);
+        else prefetch_l2(a.cprev[d] + o, pf_rows * 16 * pf_elem);
       }
       for (int mt = 0; mt < MT; ++mt) {
         const unsigned target = exp_lane * (unsigned)s;
@@ -182,13 +204,15 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           const unsigned m = __ballot_sync(0xffffffffu, rdy);
           while (done < ngrp && ((m >> done) & 1u)) {
             if (lane == 0) {
-              if (done == 0 && trace) trace[s * 16 + (mt == 0 ? 0 : 3)] = gtimer();
               const int kg = (done + kc_off) % ngrp;
               tc::fence_proxy_async_global();  // the box's DZ (generic-proxy stores) -> TMA reads
               tc::mbar_wait(&empty_bar[st], ph ^ 1);
               tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
               tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
                           (r * (Kc / 64) + kg * a.kb) * 8, slot);
+              if constexpr (X3)
+                tma_load_4d(sA + st * stage_bytes + part_bytes, &tmZ1, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
+                            (r * (Kc / 64) + kg * a.kb) * 8, slot);
             }
             if (++st == nst) {
               st = 0;
@@ -214,17 +238,23 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            if (kq == 0 && trace) trace[s * 16 + (mt == 0 ? 1 : 4)] = gtimer();
-            if (kq == ngrp - 1 && trace) trace[s * 16 + (mt == 0 ? 2 : 5)] = gtimer();
             for (int j = 0; j < a.kb; ++j) {
-            const int kc = kg * a.kb + j;
-            // A: the stage holds [kb * 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk
-            const uint32_t sa = base + r_bytes + st * stage_bytes + j * kTile;
-            const uint32_t sb = base + (uint32_t)kc * NB * 128;
+              const int kc = kg * a.kb + j;
+              // A: the stage holds [kb * 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk
+              const uint32_t sa = base + r_bytes + st * stage_bytes + j * kTile;
+              const uint32_t sb = base + (uint32_t)kc * NB * 128;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_f16(tmem + mt * NB, tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128),
-                          tc::make_sdesc(sb + k * 32, 0, 1024), idesc, (kq | j | k) != 0);
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
+                const uint64_t bh = tc::make_sdesc(sb + k * 32, 0, 1024);
+                tc::mma_f16(tmem + mt * NB, ah, bh, idesc, (kq | j | k) != 0);
+                if constexpr (X3) {
+                  const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
+                  const uint64_t bl = tc::make_sdesc(sb + r_part + k * 32, 0, 1024);
+                  tc::mma_f16(tmem + mt * NB, al, bh, idesc, true);  // DZ_lo R_hi^T
+                  tc::mma_f16(tmem + mt * NB, ah, bl, idesc, true);  // DZ_hi R_lo^T
+                }
+              }
             }
             tc::mma_commit(&empty_bar[st]);
             if (++st == nst) {
@@ -246,13 +276,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     const bool valid_row = row < a.B;
     const int len = valid_row ? a.lens[row] : 0;
     const int dir = a.dirsign[d];
+    const int gdir = X3 ? a.dir0 + d : d;  // global direction: dy / DZ columns, final-state rows
     const int H = a.H, T = a.T;
     const int lo = half * UT;
     const int ut0 = u0 + lo;
     const int nu = max(0, min(UT, H - ut0));
     __nv_bfloat16* zr = a.dzring[d];
-    const __nv_bfloat16* gates = a.gates[d];
-    const __nv_bfloat16* cprev = a.cprev[d];
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + mt * NB;
     float gcar[UT];
 #pragma unroll
@@ -264,22 +293,26 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
-      Bf16Vec<UT> gv[4], cp;
+      // saved gates / c_{s-1} of this step: fp32 (x3) or packed bf16 (registers)
+      typename std::conditional<X3, float[4][UT], Bf16Vec<UT>[4]>::type gv;
+      typename std::conditional<X3, float[UT], Bf16Vec<UT>>::type cp;
       float dyv[UT];
-      if (active && !(a.debug_flags & 16)) {  // prefetch this step's saved activations and upstream grad
+      if (active) {  // prefetch this step's saved activations and upstream grad
         const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
+        if constexpr (X3) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) gv[g].load(gates + gate_save_off(s, g, row, a.B, H, ut0), nu, true);
-        cp.load(cprev + cprev_save_off(s, row, a.B, H, ut0), nu, true);
-        load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)d * H + ut0, dyv, nu,
-                     vec && (a.dy_ld % 4) == 0);
+          for (int g = 0; g < 4; ++g) load_f32<UT>(a.gatesf[d] + gate_save_off(s, g, row, a.B, H, ut0), gv[g], nu, true);
+          load_f32<UT>(a.cprevf[d] + cprev_save_off(s, row, a.B, H, ut0), cp, nu, true);
+        } else {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) gv[g].load(a.gates[d] + gate_save_off(s, g, row, a.B, H, ut0), nu, true);
+          cp.load(a.cprev[d] + cprev_save_off(s, row, a.B, H, ut0), nu, true);
+        }
+        load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)gdir * H + ut0, dyv, nu, vec && (a.dy_ld % 4) == 0);
       }
       float dh[UT];
-      const bool tr0 = trace && e == 0 && lane == 0;
-      if (tr0) trace[it * 16 + 12] = gtimer();
       tc::mbar_wait(&tfull_bar[mt], it & 1);
       tc::fence_after_sync();
-      if (tr0) trace[it * 16 + 8] = gtimer();
       if constexpr (C > 1) {
         // reduce-scatter of the K-split partials: send each peer the columns of
         // the units it finalizes (coalesced: a warp writes 32 consecutive rows)
@@ -296,24 +329,33 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           const uint32_t dst = mapa(
               tc::smem_u32(recv + (((size_t)mt * (C - 1) + slot_at_p) * 128 + rl) * U + lo), p);
           const uint32_t rbar = mapa(tc::smem_u32(&recv_full[mt]), p);
-          static_assert(UT % 4 == 0, "DSMEM partial sends move 4 or 8 bf16 per store");
-          Bf16Vec<UT> w;
-          w.pack(v);
+          static_assert(UT % 4 == 0, "DSMEM partial sends move 4 or 8 values per store");
           // st.async: each store completes its bytes on p's receive barrier, so
           // no release fence (which would wait for this thread's pending global
           // stores) sits on the exchange path
-          if constexpr (UT % 8 == 0) {
+          if constexpr (X3) {  // fp32 partials: the reduction stays fp32-exact
 #pragma unroll
-            for (int u = 0; u < UT; u += 8)
-              st_async_v4(dst + u * 2, make_uint4(w.w[u / 2], w.w[u / 2 + 1], w.w[u / 2 + 2], w.w[u / 2 + 3]),
+            for (int u = 0; u < UT; u += 4)
+              st_async_v4(dst + u * 4,
+                          make_uint4(__float_as_uint(v[u]), __float_as_uint(v[u + 1]), __float_as_uint(v[u + 2]),
+                                     __float_as_uint(v[u + 3])),
                           rbar);
           } else {
+            Bf16Vec<UT> w;
+            w.pack(v);
+            if constexpr (UT % 8 == 0) {
 #pragma unroll
-            for (int u = 0; u < UT; u += 4) st_async_v2(dst + u * 2, make_uint2(w.w[u / 2], w.w[u / 2 + 1]), rbar);
+              for (int u = 0; u < UT; u += 8)
+                st_async_v4(dst + u * 2, make_uint4(w.w[u / 2], w.w[u / 2 + 1], w.w[u / 2 + 2], w.w[u / 2 + 3]),
+                            rbar);
+            } else {
+#pragma unroll
+              for (int u = 0; u < UT; u += 4)
+                st_async_v2(dst + u * 2, make_uint2(w.w[u / 2], w.w[u / 2 + 1]), rbar);
+            }
           }
         }
       }
-      if (tr0) trace[it * 16 + 9] = gtimer();
       tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
@@ -321,11 +363,16 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         mbar_wait_cluster(&recv_full[mt], use & 1);
         if ((e % (4 * SPLIT)) == 0 && lane == 0)  // phase `use` is complete: arm the next use
           tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
-        if (tr0) trace[it * 16 + 10] = gtimer();
 #pragma unroll 1
         for (int sl = 0; sl < C - 1; ++sl) {
-          const __nv_bfloat16* src = recv + (((size_t)mt * (C - 1) + sl) * 128 + rl) * U + lo;
-          if constexpr (UT % 8 == 0) {
+          const RecvT* src = recv + (((size_t)mt * (C - 1) + sl) * 128 + rl) * U + lo;
+          if constexpr (X3) {
+#pragma unroll
+            for (int u = 0; u < UT; u += 4) {
+              const float4 f = *reinterpret_cast<const float4*>(src + u);
+              dh[u] += f.x, dh[u + 1] += f.y, dh[u + 2] += f.z, dh[u + 3] += f.w;
+            }
+          } else if constexpr (UT % 8 == 0) {
 #pragma unroll
             for (int u = 0; u < UT; u += 8) {
               float f[8];
@@ -341,62 +388,93 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         // the senders learn that their slots are free from ONE arrive per peer
         // after the tile's publish barrier below (every reader is done by then)
       }
-      if (tr0) trace[it * 16 + 13] = gtimer();
 
-      Bf16Vec<UT> dzp[4];  // DZ_s packed: the ring copy now, the K4 copy after publishing
+      // DZ_s: fp32 (x3) or packed bf16 — the ring copy now, the K4 copy after publishing
+      typename std::conditional<X3, float[4 * UT], Bf16Vec<UT>[4]>::type dzs;
       if (valid_row) {
         const int hq8 = dz_ring_hq(H);
         if (active) {
-          float dz[4 * UT];
           const bool last = (s == len - 1);
           if (last && (a.dh_last || a.dc_last)) {  // the final-state adjoints enter at s = len - 1
 #pragma unroll
             for (int u = 0; u < UT; ++u) {
-              if (a.dh_last) dh[u] += a.dh_last[((size_t)d * a.B + row) * H + ut0 + u];
-              if (a.dc_last) gcar[u] += a.dc_last[((size_t)d * a.B + row) * H + ut0 + u];
+              if (u >= nu) continue;
+              if (a.dh_last) dh[u] += a.dh_last[((size_t)gdir * a.B + row) * H + ut0 + u];
+              if (a.dc_last) gcar[u] += a.dc_last[((size_t)gdir * a.B + row) * H + ut0 + u];
             }
           }
-          const float2 one = f2s(1.f), mone = f2s(-1.f);
+          if constexpr (X3) {  // the reference's adjoint, fp32 (tape.cpp:1157-1170)
 #pragma unroll
-          for (int u = 0; u < UT; u += 2) {  // two units per paired-fp32 instruction
-            const float2 gh = add2(f2(dh[u], dh[u + 1]), f2(dyv[u], dyv[u + 1]));
-            const float2 gc = f2(gcar[u], gcar[u + 1]);
-            const float2 gi = bf16x2_f2(gv[0].w[u / 2]), gf = bf16x2_f2(gv[1].w[u / 2]);
-            const float2 gg = bf16x2_f2(gv[2].w[u / 2]), go = bf16x2_f2(gv[3].w[u / 2]);
-            const float2 cpu = bf16x2_f2(cp.w[u / 2]);
-            const float2 tcv = tanh2(fma2(gf, cpu, mul2(gi, gg)));
-            const float2 d_o = mul2(gh, tcv);                                      // tape.cpp:1161
-            const float2 dcn = fma2(mul2(gh, go), fma2(mul2(mone, tcv), tcv, one), gc);  // tape.cpp:1162
-            const float2 cg = mul2(dcn, gf);                                       // tape.cpp:1166
-            gcar[u] = cg.x, gcar[u + 1] = cg.y;
-            const float2 zi = mul2(mul2(dcn, gg), mul2(gi, fma2(mone, gi, one)));    // tape.cpp:1167
-            const float2 zf = mul2(mul2(dcn, cpu), mul2(gf, fma2(mone, gf, one)));   // tape.cpp:1168
-            const float2 zg = mul2(mul2(dcn, gi), fma2(mul2(mone, gg), gg, one));    // tape.cpp:1169
-            const float2 zo = mul2(mul2(d_o, go), fma2(mone, go, one));              // tape.cpp:1170
-            dz[u] = zi.x, dz[u + 1] = zi.y;
-            dz[UT + u] = zf.x, dz[UT + u + 1] = zf.y;
-            dz[2 * UT + u] = zg.x, dz[2 * UT + u + 1] = zg.y;
-            dz[3 * UT + u] = zo.x, dz[3 * UT + u + 1] = zo.y;
+            for (int u = 0; u < UT; ++u) {
+              const float gh = dh[u] + dyv[u], gc = gcar[u];
+              const float gi = gv[0][u], gf = gv[1][u], gg = gv[2][u], go = gv[3][u];
+              const float tcv = tanhf(gf * cp[u] + gi * gg);
+              const float d_o = gh * tcv;
+              const float dcn = gc + gh * go * (1.f - tcv * tcv);
+              gcar[u] = dcn * gf;
+              dzs[u] = dcn * gg * gi * (1.f - gi);
+              dzs[UT + u] = dcn * cp[u] * gf * (1.f - gf);
+              dzs[2 * UT + u] = dcn * gi * (1.f - gg * gg);
+              dzs[3 * UT + u] = d_o * go * (1.f - go);
+            }
+          } else {
+            float dz[4 * UT];
+            const float2 one = f2s(1.f), mone = f2s(-1.f);
+#pragma unroll
+            for (int u = 0; u < UT; u += 2) {  // two units per paired-fp32 instruction
+              const float2 gh = add2(f2(dh[u], dh[u + 1]), f2(dyv[u], dyv[u + 1]));
+              const float2 gc = f2(gcar[u], gcar[u + 1]);
+              const float2 gi = bf16x2_f2(gv[0].w[u / 2]), gf = bf16x2_f2(gv[1].w[u / 2]);
+              const float2 gg = bf16x2_f2(gv[2].w[u / 2]), go = bf16x2_f2(gv[3].w[u / 2]);
+              const float2 cpu = bf16x2_f2(cp.w[u / 2]);
+              const float2 tcv = tanh2(fma2(gf, cpu, mul2(gi, gg)));
+              const float2 d_o = mul2(gh, tcv);                                      // tape.cpp:1161
+              const float2 dcn = fma2(mul2(gh, go), fma2(mul2(mone, tcv), tcv, one), gc);  // tape.cpp:1162
+              const float2 cg = mul2(dcn, gf);                                       // tape.cpp:1166
+              gcar[u] = cg.x, gcar[u + 1] = cg.y;
+              const float2 zi = mul2(mul2(dcn, gg), mul2(gi, fma2(mone, gi, one)));    // tape.cpp:1167
+              const float2 zf = mul2(mul2(dcn, cpu), mul2(gf, fma2(mone, gf, one)));   // tape.cpp:1168
+              const float2 zg = mul2(mul2(dcn, gi), fma2(mul2(mone, gg), gg, one));    // tape.cpp:1169
+              const float2 zo = mul2(mul2(d_o, go), fma2(mone, go, one));              // tape.cpp:1170
+              dz[u] = zi.x, dz[u + 1] = zi.y;
+              dz[UT + u] = zf.x, dz[UT + u + 1] = zf.y;
+              dz[2 * UT + u] = zg.x, dz[2 * UT + u + 1] = zg.y;
+              dz[3 * UT + u] = zo.x, dz[3 * UT + u + 1] = zo.y;
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) dzs[g].pack(dz + g * UT);
           }
-#pragma unroll
-          for (int g = 0; g < 4; ++g) dzp[g].pack(dz + g * UT);
-          if (tr0) trace[it * 16 + 14] = gtimer();
         } else {
+          if constexpr (X3) {
 #pragma unroll
-          for (int g = 0; g < 4; ++g) dzp[g].zero();
+            for (int u = 0; u < 4 * UT; ++u) dzs[u] = 0.f;
+          } else {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) dzs[g].zero();
+          }
         }
+        constexpr int CW = UT < 8 ? UT : 8;  // the ring's 8-unit chunks are Bp * 16 B apart
 #pragma unroll
         for (int g = 0; g < 4; ++g)
 #pragma unroll
-          for (int c = 0; c < UT; c += 8) {  // the ring's 8-unit chunks are Bp * 16 B apart
-            Bf16Vec<(UT < 8 ? UT : 8)> part;
+          for (int c = 0; c < UT; c += CW) {
+            const size_t off = dz_ring_off((it + 1) & 1, row, g * hq8 + ut0 + c, dz_ring_bp(a.B), a.Kz);
+            const int n = max(0, min(CW, nu - c));
+            if constexpr (X3) {
+              store_bf16<CW>(zr + off, dzs + g * UT + c, n);
+              float l[CW];  // DZ_lo = DZ - bf16(DZ)
 #pragma unroll
-            for (int w = 0; w < (UT < 8 ? UT : 8) / 2; ++w) part.w[w] = dzp[g].w[c / 2 + w];
-            part.store(zr + dz_ring_off((it + 1) & 1, row, g * hq8 + ut0 + c, dz_ring_bp(a.B), a.Kz),
-                       max(0, min(UT < 8 ? UT : 8, nu - c)));
+              for (int u = 0; u < CW; ++u)
+                l[u] = dzs[g * UT + c + u] - __bfloat162float(__float2bfloat16_rn(dzs[g * UT + c + u]));
+              store_bf16<CW>(a.dzring_lo[d] + off, l, n);
+            } else {
+              Bf16Vec<CW> part;
+#pragma unroll
+              for (int w = 0; w < CW / 2; ++w) part.w[w] = dzs[g].w[c / 2 + w];
+              part.store(zr + off, n);
+            }
           }
       }
-      if (tr0) trace[it * 16 + 11] = gtimer();
       named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
@@ -415,12 +493,17 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
           for (int pi = 1; pi < C; ++pi)
             mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), kEpiTile);
-        if (trace) trace[it * 16 + 6 + mt] = gtimer();
       }
-      if (valid_row && !(a.debug_flags & 8)) {  // the K4 operand copy is off the cross-CTA critical path
-        __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+      if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
+        if constexpr (X3) {
+          float* zc = a.dzcatf + pos * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) dzp[g].store(zc + g * H, nu);
+          for (int g = 0; g < 4; ++g) store_f32<UT>(zc + g * H, dzs + g * UT, nu);
+        } else {
+          __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) dzs[g].store(zc + g * H, nu);
+        }
       }
     }
     if (valid_row) {  // DZ rows of positions beyond the longest sequence
@@ -428,10 +511,16 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 #pragma unroll
       for (int u = 0; u < UT; ++u) zero[u] = 0.f;
       for (int s = Tmax; s < T; ++s) {
-        __nv_bfloat16* zc =
-            a.dzcat + ((size_t)row * T + s) * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+        if constexpr (X3) {
+          float* zc = a.dzcatf + ((size_t)row * T + s) * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) store_bf16<UT>(zc + g * H, zero, nu);
+          for (int g = 0; g < 4; ++g) store_f32<UT>(zc + g * H, zero, nu);
+        } else {
+          __nv_bfloat16* zc =
+              a.dzcat + ((size_t)row * T + s) * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) store_bf16<UT>(zc + g * H, zero, nu);
+        }
       }
     }
   }
@@ -441,7 +530,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 }
 
 // RB[(cl*C + r)*NB + n][kk] = R[cl*C*U + n][r*Kc + kk]  (bf16; zero outside the layer)
+// LO: the rounding remainder R - bf16(R) instead, written P * NB rows further on.
 // One CTA per packed row; threads along kk (coalesced on both sides), 32-bit math.
+template <bool LO>
 __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U, int NB, int P,
                                int Kc, __nv_bfloat16* __restrict__ RB) {
   const int rowi = blockIdx.x;
@@ -449,13 +540,16 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   const int cl = cta / C, r = cta % C;
   const int unit = cl * C * U + n;
   const bool live = n < C * U && unit < H;
-  __nv_bfloat16* dst = RB + (size_t)rowi * Kc;
+  __nv_bfloat16* dst = RB + ((LO ? (size_t)P * NB : 0) + rowi) * Kc;
+  auto cvt = [](float v) {
+    return __float2bfloat16_rn(LO ? v - __bfloat162float(__float2bfloat16_rn(v)) : v);
+  };
   const int hq8 = dz_ring_hq(H);
   if (hq8 != H) {  // gate blocks padded to a multiple of 8 columns in the DZ ring
     for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
       const int col = r * Kc + kk, g = col / hq8, u = col % hq8;
       const float v = (live && g < 4 && u < H) ? __ldg(R + (size_t)unit * 4 * H + (size_t)g * H + u) : 0.f;
-      dst[kk] = __float2bfloat16_rn(v);
+      dst[kk] = cvt(v);
     }
     return;
   }
@@ -473,25 +567,28 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
       for (int u = 0; u < 4; ++u) v[u] = kk + u < valid ? __ldg(src + kk + u) : 0.f;
     }
     if (kk + 4 <= Kc) {
-      const __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+      const __nv_bfloat16 b0 = cvt(v[0]), b1 = cvt(v[1]), b2 = cvt(v[2]), b3 = cvt(v[3]);
+      __nv_bfloat162 p0, p1;
+      p0.x = b0, p0.y = b1, p1.x = b2, p1.y = b3;
       *reinterpret_cast<uint2*>(dst + kk) =
           make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
     } else {
-      for (int u = 0; u < 4 && kk + u < Kc; ++u) dst[kk + u] = __float2bfloat16_rn(v[u]);
+      for (int u = 0; u < 4 && kk + u < Kc; ++u) dst[kk + u] = cvt(v[u]);
     }
   }
 }
 
-template <int C, int U, int MT>
+template <int C, int U, int MT, bool X3>
 void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs& a,
                 cudaStream_t stream) {
-  auto kern = rec_bwd_tc_kernel<C, U, MT>;
-  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.kb == 2 ? a.stages : (a.stages + 1) / 2);
+  auto kern = rec_bwd_tc_kernel<C, U, MT, X3>;
+  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.kb == 2 ? a.stages : (a.stages + 1) / 2, X3);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (C > 1)
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   TcRecBwdArgs copy = a;
-  CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[a.nd > 1 ? 1 : 0];
+  // X3 (one direction): tz[0] = the hi ring, tz[1] = the lo ring
+  CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[(X3 || a.nd > 1) ? 1 : 0];
   constexpr int kSplit = bwd_split(U);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.P * a.nd);
@@ -516,6 +613,40 @@ void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs
   }
   SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, z0, z1, copy));
   count_launch();
+}
+
+// the DZ ring in its interleaved layout, as {8 rows x 8 k (128 contiguous B),
+// 8-row groups, K-chunks, slot}: 128 B TMA rows, box = 128 rows x kb*64 K
+CUtensorMap dz_ring_map(const __nv_bfloat16* ring, int B, int Kz, int kb) {
+  const int Bp = dz_ring_bp(B);
+  cuuint64_t zd[4] = {64, (cuuint64_t)Bp / 8, (cuuint64_t)Kz / 8, 2};
+  cuuint64_t zs[3] = {128, (cuuint64_t)Bp * 16, (cuuint64_t)Kz / 8 * Bp * 16};
+  cuuint32_t zb[4] = {64, 16, (cuuint32_t)kb * 8, 1};
+  return tmap(ring, 4, zd, zs, zb, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+template <bool X3>
+void dispatch_bwd(const TcBwdShape& sh, int MT, const CUtensorMap* tr, const CUtensorMap* tz,
+                  const TcRecBwdArgs& a, cudaStream_t stream) {
+  const int key = sh.C * 1000 + sh.U * 10 + MT;
+  switch (key) {
+#define SL_BWD_CASE(C_, U_, MT_) \
+  case C_ * 1000 + U_ * 10 + MT_: launch_bwd<C_, U_, MT_, X3>(tr, tz, a, stream); break;
+    SL_BWD_CASE(4, 4, 1) SL_BWD_CASE(4, 4, 2) SL_BWD_CASE(4, 8, 1) SL_BWD_CASE(4, 8, 2)
+    SL_BWD_CASE(4, 16, 1) SL_BWD_CASE(4, 16, 2) SL_BWD_CASE(2, 4, 1) SL_BWD_CASE(2, 4, 2)
+    SL_BWD_CASE(2, 8, 1) SL_BWD_CASE(2, 8, 2) SL_BWD_CASE(2, 16, 1) SL_BWD_CASE(2, 16, 2)
+    SL_BWD_CASE(1, 4, 1) SL_BWD_CASE(1, 4, 2) SL_BWD_CASE(1, 8, 1) SL_BWD_CASE(1, 8, 2)
+    SL_BWD_CASE(1, 16, 1) SL_BWD_CASE(1, 16, 2)
+#undef SL_BWD_CASE
+    default: throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_tc: unsupported partition"};
+  }
+}
+
+int pick_stages(const TcBwdShape& sh, int kb, bool x3) {
+  const int Kc = sh.Kz / sh.C;
+  for (int st = kStages; st >= 2; --st)
+    if (bwd_smem(sh.C, sh.U, Kc, kb == 2 ? st : (st + 1) / 2, x3) <= kSmemMax) return st;
+  return 0;
 }
 
 }  // namespace
@@ -550,7 +681,7 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
   }
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  pack_rb_kernel<<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -568,23 +699,15 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
   CUtensorMap tr[2], tz[2];
+  a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
   for (int k = 0; k < a.nd; ++k) {
     cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)a.P * NB};
     cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
     tr[k] = tmap(RB[k], 2, rd, rs, rb);
-    a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
-    // the DZ ring in its interleaved layout, as {8 rows x 8 k (128 contiguous B),
-    // 8-row groups, K-chunks, slot}: 128 B TMA rows, box = 128 rows x kb*64 K
-    const int Bp = dz_ring_bp(a.B);
-    cuuint64_t zd[4] = {64, (cuuint64_t)Bp / 8, (cuuint64_t)a.Kz / 8, 2};
-    cuuint64_t zs[3] = {128, (cuuint64_t)Bp * 16, (cuuint64_t)a.Kz / 8 * Bp * 16};
-    cuuint32_t zb[4] = {64, 16, (cuuint32_t)a.kb * 8, 1};
-    tz[k] = tmap(a.dzring[k], 4, zd, zs, zb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    tz[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, a.kb);
   }
-  a.stages = 0;
-  for (int st = kStages; st >= 2 && !a.stages; --st)
-    if (bwd_smem(sh.C, sh.U, Kc, a.kb == 2 ? st : (st + 1) / 2) <= kSmemMax) a.stages = st;
+  a.stages = pick_stages(sh, a.kb, false);
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
   SL_REQUIRE(a.Kz / (a.kb * 64) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
              "rec_bwd_tc: too many DZ boxes for the step counters");
@@ -592,19 +715,64 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
     a.bar = bar0 + kBarPerChunk * (b0 / 256);
-    const int MT = (a.B - b0) > 128 ? 2 : 1;
-    const int key = sh.C * 1000 + sh.U * 10 + MT;
-    switch (key) {
-#define SL_BWD_CASE(C_, U_, MT_) \
-  case C_ * 1000 + U_ * 10 + MT_: launch_bwd<C_, U_, MT_>(tr, tz, a, stream); break;
-      SL_BWD_CASE(4, 4, 1) SL_BWD_CASE(4, 4, 2) SL_BWD_CASE(4, 8, 1) SL_BWD_CASE(4, 8, 2)
-      SL_BWD_CASE(4, 16, 1) SL_BWD_CASE(4, 16, 2) SL_BWD_CASE(2, 4, 1) SL_BWD_CASE(2, 4, 2)
-      SL_BWD_CASE(2, 8, 1) SL_BWD_CASE(2, 8, 2) SL_BWD_CASE(2, 16, 1) SL_BWD_CASE(2, 16, 2)
-      SL_BWD_CASE(1, 4, 1) SL_BWD_CASE(1, 4, 2) SL_BWD_CASE(1, 8, 1) SL_BWD_CASE(1, 8, 2)
-      SL_BWD_CASE(1, 16, 1) SL_BWD_CASE(1, 16, 2)
-#undef SL_BWD_CASE
-      default: throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_tc: unsupported partition"};
+    dispatch_bwd<false>(sh, (a.B - b0) > 128 ? 2 : 1, tr, tz, a, stream);
+  }
+}
+
+TcBwdShape tc_rec_bwd_x3_shape(int H, int sms) {
+  for (int C : {4, 2, 1}) {
+    const int usable = C == 4 ? std::min(sms, 128) : sms;
+    for (int U : {8, 4, 16}) {
+      const int P = (int)ceil_div(H, (int64_t)C * U) * C;
+      const int Kz = (int)round_up(4 * (int64_t)dz_ring_hq(H), 64 * C);
+      if (P <= usable && Kz / 64 <= kBoxCtrs) {  // kb = 1 (rec_bwd_x3)
+        TcBwdShape sh{C, U, P, Kz};
+        if (pick_stages(sh, 1, true) >= 2) return sh;
+      }
     }
+  }
+  return TcBwdShape{0, 0, 0, 0};
+}
+
+size_t tc_rec_bwd_x3_pack_elems(const TcBwdShape& sh) {
+  return (size_t)2 * sh.P * nb_of(sh.C, sh.U) * (sh.Kz / sh.C);
+}
+
+void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream) {
+  const int NB = nb_of(sh.C, sh.U);
+  const int Kc = sh.Kz / sh.C;
+  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  SL_CUDA_TRY(cudaGetLastError());
+  pack_rb_kernel<true><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch(2);
+}
+
+void rec_bwd_x3(const TcRecBwdArgs& a0, const TcBwdShape& sh, const __nv_bfloat16* RB, cudaStream_t stream) {
+  TcRecBwdArgs a = a0;
+  SL_REQUIRE(a.nd == 1, SL_ERR_INVALID_ARGUMENT, "rec_bwd_x3: one direction per launch");
+  a.U = sh.U;
+  a.P = sh.P;
+  a.Kz = sh.Kz;
+  const int NB = nb_of(sh.C, sh.U);
+  const int Kc = sh.Kz / sh.C;
+  a.kb = 1;  // hi + lo parts of a stage: one 64-wide chunk each keeps >= 2 stages in shared memory
+  CUtensorMap tr[1], tz[2];
+  cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)2 * a.P * NB};
+  cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
+  cuuint32_t rb[2] = {64, (cuuint32_t)NB};
+  tr[0] = tmap(RB, 2, rd, rs, rb);
+  tz[0] = dz_ring_map(a.dzring[0], a.B, a.Kz, a.kb);
+  tz[1] = dz_ring_map(a.dzring_lo[0], a.B, a.Kz, a.kb);
+  a.stages = pick_stages(sh, a.kb, true);
+  SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_x3: R slice does not fit in shared memory");
+  SL_REQUIRE(a.Kz / (a.kb * 64) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
+             "rec_bwd_x3: too many DZ boxes for the step counters");
+  unsigned* bar0 = a.bar;
+  for (int b0 = 0; b0 < a.B; b0 += 256) {
+    a.b0 = b0;
+    a.bar = bar0 + kBarPerChunk * (b0 / 256);
+    dispatch_bwd<true>(sh, (a.B - b0) > 128 ? 2 : 1, tr, tz, a, stream);
   }
 }
 

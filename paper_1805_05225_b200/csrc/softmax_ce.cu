@@ -16,6 +16,7 @@
 //   2. one warp per row folds the block statistics into lse / loss and turns
 //      the row of Z into dZ in place (bf16);
 //   3. dX = dZ W^T and [dW; db] = [X | 1]^T dZ on the same GEMM.
+#include <algorithm>
 #include <cmath>
 
 #include "convert.h"
@@ -126,6 +127,83 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(__nv_bfloat16* __restrict_
   }
 }
 
+// fp32-class variant (SL_PREC_FP32): one warp per row of fp32 logits Z: an online
+// (max, sum exp) pass with sum z and z_y, lse = m + log(s), then Z -> dZ in place.
+// Reference arithmetic: expf / logf (tape.cpp:879-924, 1224-1298).
+__global__ void __launch_bounds__(256) ce_rows_f32_kernel(float* __restrict__ Z, int64_t ldz, int rows, int T,
+                                                          int V, const int32_t* __restrict__ targets,
+                                                          const int32_t* __restrict__ lens, float eps, CeScratch* sc,
+                                                          int* bad_target) {
+  const int lane = threadIdx.x % 32;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int b = row / T, t = row % T;
+  float* z = Z + (int64_t)row * ldz;
+  const bool vec = (V % 4) == 0 && (ldz % 4) == 0;
+  if (t >= lens[b]) {  // masked position (tape.cpp:1256-1262): no loss, zero gradient
+    for (int j = lane; j < V; j += 32) z[j] = 0.f;
+    return;
+  }
+  const int y = targets[row];
+  if (y < 0 || y >= V) {  // reference IndexError: poison the step (see ce_rows_kernel)
+    if (lane == 0) {
+      atomicMax(bad_target, 1);
+      atomicAdd(&sc->loss_sum, (double)__int_as_float(0x7fc00000));
+    }
+    for (int j = lane; j < V; j += 32) z[j] = __int_as_float(0x7fc00000);
+    return;
+  }
+  float m = -INFINITY, s = 0.f, tz = 0.f;
+  auto fold = [&](float v) {
+    if (v > m) {
+      s = s * expf(m - v) + 1.f;
+      m = v;
+    } else {
+      s += expf(v - m);
+    }
+    tz += v;
+  };
+  if (vec) {
+    for (int j = lane * 4; j < V; j += 128) {
+      const float4 q = *reinterpret_cast<const float4*>(z + j);
+      fold(q.x), fold(q.y), fold(q.z), fold(q.w);
+    }
+  } else {
+    for (int j = lane; j < V; j += 32) fold(z[j]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - mm));
+    m = mm;
+    tz += __shfl_xor_sync(0xffffffffu, tz, o);
+  }
+  const float zy = z[y];
+  const float lse = m + logf(s);
+  if (lane == 0)
+    atomicAdd(&sc->loss_sum, (double)lse - (1.0 - (double)eps) * (double)zy - (double)eps / V * (double)tz);
+  const float inv_n = 1.f / (float)max(sc->n_valid, 1);
+  const float base = -eps / (float)V;
+  __syncwarp();
+  if (vec) {
+    for (int j = lane * 4; j < V; j += 128) {
+      float4 q = *reinterpret_cast<const float4*>(z + j);
+      float g[4] = {expf(q.x - lse) + base, expf(q.y - lse) + base, expf(q.z - lse) + base, expf(q.w - lse) + base};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (j + k == y) g[k] -= 1.f - eps;
+      *reinterpret_cast<float4*>(z + j) = make_float4(g[0] * inv_n, g[1] * inv_n, g[2] * inv_n, g[3] * inv_n);
+    }
+  } else {
+    for (int j = lane; j < V; j += 32) {
+      float g = expf(z[j] - lse) + base;
+      if (j == y) g -= 1.f - eps;
+      z[j] = g * inv_n;
+    }
+  }
+}
+
 __global__ void ce_finalize_kernel(const CeScratch* sc, float* loss_out) {
   *loss_out = (float)(sc->loss_sum / (double)max(sc->n_valid, 1));
 }
@@ -204,6 +282,53 @@ void output_ce(int B, int T, int D, int V, const float* x, const int32_t* target
     g.ldc2 = V;
     if (!db) g.M = D;
     gemm_bf16_tc(g, stream);
+  }
+}
+
+size_t output_ce_f32_workspace_bytes(int B, int T, int D, int V) {
+  const int64_t rows = (int64_t)B * T;
+  const size_t x3 = std::max({gemm_f32x3_workspace_bytes(false, false, (int)rows, V, D, false),   // logits
+                              gemm_f32x3_workspace_bytes(false, true, (int)rows, D, V, false),    // dX
+                              gemm_f32x3_workspace_bytes(true, false, D, V, (int)rows, true)});   // [dW; db]
+  return (size_t)round_up(rows * V * 4, 256) + (size_t)round_up(sizeof(CeScratch), 256) + x3;
+}
+
+void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* targets, const int32_t* lens,
+                   const float* W, const float* b, float eps, float* loss_out, float* dx, float* dW, float* db,
+                   bool accumulate, void* workspace, int* bad_target, cudaStream_t stream) {
+  const int64_t rows = (int64_t)B * T;
+  char* w = static_cast<char*>(workspace);
+  float* z = reinterpret_cast<float*>(w);
+  auto* sc = reinterpret_cast<CeScratch*>(w + round_up(rows * V * 4, 256));
+  void* gws = w + round_up(rows * V * 4, 256) + round_up(sizeof(CeScratch), 256);
+  SL_CUDA_TRY(cudaMemsetAsync(bad_target, 0, sizeof(int), stream));
+  ce_count_kernel<<<1, 256, 0, stream>>>(lens, B, T, sc);
+  SL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  const double f = 2.0 * rows * D * (double)V;
+  {
+    Phase ph(stream, "k7_logits_gemm", f);
+    gemm_f32x3(false, false, (int)rows, V, D, x, D, W, V, 0.f, z, V, b, nullptr, 0, gws, stream);
+  }
+  {
+    Phase ph(stream, "k7_softmax_ce", 0.0, 12.0 * rows * V);
+    ce_rows_f32_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, stream>>>(z, V, (int)rows, T, V, targets, lens, eps,
+                                                                         sc, bad_target);
+    SL_CUDA_TRY(cudaGetLastError());
+    ce_finalize_kernel<<<1, 1, 0, stream>>>(sc, loss_out);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch(2);
+  }
+  const float beta = accumulate ? 1.f : 0.f;
+  if (dx) {
+    Phase ph(stream, "k7_dx_gemm", f);
+    gemm_f32x3(false, true, (int)rows, D, V, z, V, W, V, beta, dx, D, nullptr, nullptr, 0, gws, stream);
+  }
+  if (dW) {
+    Phase ph(stream, "k7_dw_gemm", f);
+    gemm_f32x3(true, false, D, V, (int)rows, x, D, z, V, beta, dW, V, nullptr, db, V, gws, stream);
+  } else if (db) {
+    SL_REQUIRE(false, SL_ERR_INVALID_ARGUMENT, "output_ce (fp32): db needs dW");
   }
 }
 

@@ -17,4 +17,10 @@ void output_ce(int B, int T, int D, int V, const float* x, const int32_t* target
                const float* W, const float* b, float eps, float* loss_out, float* dx, float* dW, float* db,
                bool accumulate, void* workspace, int* bad_target, cudaStream_t stream);
 
+// the same at the reference's precision: fp32 logits, split-bf16 tcgen05 GEMMs (x3)
+size_t output_ce_f32_workspace_bytes(int B, int T, int D, int V);
+void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* targets, const int32_t* lens,
+                   const float* W, const float* b, float eps, float* loss_out, float* dx, float* dW, float* db,
+                   bool accumulate, void* workspace, int* bad_target, cudaStream_t stream);
+
 }  // namespace sl

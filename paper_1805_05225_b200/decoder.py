@@ -48,7 +48,10 @@ class _Ptrs(ctypes.Structure):
 
 class AttnDecoder:
     def __init__(self, batch: int, src_time: int, trg_time: int, emb: int, enc: int, hidden: int, key: int,
-                 readout: int, trg_vocab: int, device=None, layer: str = "output/trg"):
+                 readout: int, trg_vocab: int, device=None, layer: str = "output/trg", precision: str = "bf16"):
+        """precision "bf16": enc is the padded bf16 encoder output (sl_attn_decoder_*);
+        "fp32": the reference's precision — enc fp32 [B, Ts, E], split-bf16 tensor-core
+        GEMMs and fp32 attention (sl_attn_decoder_*_f32, rel. 1e-4)."""
         self.B, self.Ts, self.T, self.Emb, self.E, self.H, self.K, self.Rd, self.Vt = (
             batch, src_time, trg_time, emb, enc, hidden, key, readout, trg_vocab)
         self.layer = layer
@@ -62,7 +65,15 @@ class AttnDecoder:
         L.sl_attn_decoder_fwd.argtypes = [P(_Desc), P(_Ptrs), vp, ctypes.c_int64, vp, vp, vp, vp, vp, sz, vp]
         L.sl_attn_decoder_bwd.argtypes = [P(_Desc), P(_Ptrs), P(_Ptrs), vp, ctypes.c_int64, vp, vp, vp, vp, vp,
                                           vp, sz, vp]
-        self.ws_bytes = L.sl_attn_decoder_workspace_size(ctypes.byref(self.desc))
+        L.sl_attn_decoder_f32_workspace_size.restype = sz
+        L.sl_attn_decoder_f32_workspace_size.argtypes = [P(_Desc)]
+        L.sl_attn_decoder_fwd_f32.argtypes = [P(_Desc), P(_Ptrs), vp, vp, vp, vp, vp, vp, sz, vp]
+        L.sl_attn_decoder_bwd_f32.argtypes = [P(_Desc), P(_Ptrs), P(_Ptrs), vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be bf16 or fp32, got {precision!r}")
+        self.precision = precision
+        self.ws_bytes = (L.sl_attn_decoder_f32_workspace_size if precision == "fp32" else
+                         L.sl_attn_decoder_workspace_size)(ctypes.byref(self.desc))
         if self.ws_bytes == 0:
             raise lstm.ShapeError(L.sl_last_error().decode())
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
@@ -77,15 +88,24 @@ class AttnDecoder:
         return _Ptrs(*vals)
 
     def forward(self, enc_bf16, src_lens, prev_ids, params, readout=None):
-        """enc_bf16 [B, Ts, ld] (padded bf16 encoder output, 1.0 at column E),
-        prev_ids [B, T] int32 (< 0: the zero initial output), params: dict of
-        fp32 tensors (NAMES) -> readout [B, T, Rd] fp32."""
-        assert enc_bf16.dtype == torch.bfloat16 and enc_bf16.shape[:2] == (self.B, self.Ts)
+        """enc_bf16 [B, Ts, ld] (padded bf16 encoder output, 1.0 at column E; fp32
+        [B, Ts, E] for precision fp32), prev_ids [B, T] int32 (< 0: the zero initial
+        output), params: dict of fp32 tensors (NAMES) -> readout [B, T, Rd] fp32."""
+        if self.precision == "fp32":
+            lstm._need(enc_bf16, (self.B, self.Ts, self.E), "enc")
+        else:
+            assert enc_bf16.dtype == torch.bfloat16 and enc_bf16.shape[:2] == (self.B, self.Ts)
         lstm._need(src_lens, (self.B,), "src_lens", torch.int32)
         lstm._need(prev_ids, (self.B, self.T), "prev_ids", torch.int32)
         if readout is None:
             readout = torch.empty(self.B, self.T, self.Rd, dtype=torch.float32, device=self.device)
         self._pp = self._ptrs(params, "params")
+        if self.precision == "fp32":
+            lstm._check(lstm.lib().sl_attn_decoder_fwd_f32(
+                ctypes.byref(self.desc), ctypes.byref(self._pp), enc_bf16.data_ptr(), src_lens.data_ptr(),
+                prev_ids.data_ptr(), readout.data_ptr(), self.bad.data_ptr(), self.workspace.data_ptr(),
+                self.ws_bytes, lstm._stream()))
+            return readout
         lstm._check(lstm.lib().sl_attn_decoder_fwd(
             ctypes.byref(self.desc), ctypes.byref(self._pp), enc_bf16.data_ptr(), enc_bf16.stride(1),
             src_lens.data_ptr(), prev_ids.data_ptr(), readout.data_ptr(), self.bad.data_ptr(),
@@ -98,6 +118,12 @@ class AttnDecoder:
             d_enc = torch.empty(self.B, self.Ts, self.E, dtype=torch.float32, device=self.device)
         lstm._need(d_readout, (self.B, self.T, self.Rd), "d_readout")
         pp, gp = self._ptrs(params, "params"), self._ptrs(grads, "grads")
+        if self.precision == "fp32":
+            lstm._check(lstm.lib().sl_attn_decoder_bwd_f32(
+                ctypes.byref(self.desc), ctypes.byref(pp), ctypes.byref(gp), enc_bf16.data_ptr(), src_lens.data_ptr(),
+                prev_ids.data_ptr(), readout.data_ptr(), d_readout.data_ptr(), d_enc.data_ptr(),
+                self.workspace.data_ptr(), self.ws_bytes, lstm._stream()))
+            return d_enc
         lstm._check(lstm.lib().sl_attn_decoder_bwd(
             ctypes.byref(self.desc), ctypes.byref(pp), ctypes.byref(gp), enc_bf16.data_ptr(), enc_bf16.stride(1),
             src_lens.data_ptr(), prev_ids.data_ptr(), readout.data_ptr(), d_readout.data_ptr(), d_enc.data_ptr(),

@@ -28,6 +28,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libseqloom_cuda.so")
 
 SL_OK, SL_ERR_INVALID_ARGUMENT, SL_ERR_SHAPE, SL_ERR_CUDA, SL_ERR_WORKSPACE, SL_ERR_UNSUPPORTED = range(6)
 PRECISIONS = {"fp32": 0, "bf16": 1}
+PATHS = {1: "bf16_tc", 2: "fp32_x3_tc", 3: "fp32_simt"}  # seqloom_cuda.h enum sl_path
 SL_LAYER_X_BF16, SL_LAYER_Y_BF16 = 1, 2
 
 
@@ -61,6 +62,7 @@ def lib() -> ctypes.CDLL:
         L.sl_version.restype = ctypes.c_int
         L.sl_last_error.restype = ctypes.c_char_p
         L.sl_lstm_layer_check.argtypes = [P(_Layer)]
+        L.sl_lstm_layer_path.argtypes = [P(_Layer)]
         L.sl_lstm_reserve_size.restype = sz
         L.sl_lstm_reserve_size.argtypes = [P(_Layer)]
         L.sl_lstm_workspace_size.restype = sz
@@ -153,6 +155,12 @@ class LSTMLayer:
         flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
         d = _Layer(batch, time, input_dim, hidden, num_dirs, direction, PRECISIONS[precision], flags)
         return lib().sl_lstm_workspace_size(ctypes.byref(d))
+
+    @property
+    def path(self) -> str:
+        """The kernels this layer runs on: "bf16_tc", "fp32_x3_tc" (fp32-class on
+        the tensor cores) or "fp32_simt" (sl_lstm_layer_path)."""
+        return PATHS[lib().sl_lstm_layer_path(ctypes.byref(self.desc))]
 
     @property
     def shape(self):

@@ -243,8 +243,15 @@ class Seq2SeqAttention:
     def __init__(self, enc_layers: int, batch: int, src_time: int, trg_time: int, emb: int, hidden: int,
                  vocab: int, src_vocab: int, trg_vocab: int, key: int | None = None, readout: int | None = None,
                  device=None, lr: float = 1e-3, clip_norm: float = 5.0, label_smoothing: float = 0.1,
-                 dropout: float = 0.3, seed: int = 1):
+                 dropout: float = 0.3, seed: int = 1, precision: str = "bf16"):
+        """precision "fp32": every layer at the reference's precision (rel. 1e-4;
+        split-bf16 "x3" tensor-core GEMMs and recurrences, fp32 activations);
+        "bf16": bf16 operands with fp32 accumulation and state (rel. 2e-2)."""
         from .decoder import NAMES, AttnDecoder, param_shapes
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be bf16 or fp32, got {precision!r}")
+        self.precision = precision
+        bf16 = precision == "bf16"
         self.L, self.B, self.Ts, self.T, self.E, self.H = enc_layers, batch, src_time, trg_time, emb, hidden
         self.K, self.Rd = key or hidden, readout or hidden
         self.V, self.Vs, self.Vt = vocab, src_vocab, trg_vocab
@@ -267,8 +274,8 @@ class Seq2SeqAttention:
         total = al(src_off + src_vocab * emb)
         self.params = torch.zeros(total, dtype=torch.float32, device=self.device)
         self.grads = torch.zeros_like(self.params)
-        self.enc = BLSTMEncoder(enc_layers, batch, src_time, emb, H, "bf16", self.device,
-                                params=self.params[:n_enc], grads=self.grads[:n_enc], x0_bf16=True, top_bf16=True)
+        self.enc = BLSTMEncoder(enc_layers, batch, src_time, emb, H, precision, self.device,
+                                params=self.params[:n_enc], grads=self.grads[:n_enc], x0_bf16=bf16, top_bf16=bf16)
         names = self.enc.param_slices()
         shapes = {}
         for l, D in enumerate(self.enc.in_dims):
@@ -296,9 +303,12 @@ class Seq2SeqAttention:
         names.append(("src/W", src_off, n_src))
         shapes["src/W"] = (src_vocab, emb)
         self.src_emb = Embedding(src_vocab, emb, batch * src_time, layer="src", device=self.device)
-        self.x0 = torch.zeros(batch, src_time, lstm.bf16_pitch(emb), dtype=torch.bfloat16, device=self.device)
-        self.dec = AttnDecoder(batch, src_time, trg_time, emb, Ed, H, self.K, self.Rd, trg_vocab, self.device)
-        self.out = OutputCE(batch, trg_time, self.Rd, vocab, label_smoothing, device=self.device)
+        self.x0 = (torch.zeros(batch, src_time, lstm.bf16_pitch(emb), dtype=torch.bfloat16, device=self.device)
+                   if bf16 else torch.zeros(batch, src_time, emb, dtype=torch.float32, device=self.device))
+        self.dec = AttnDecoder(batch, src_time, trg_time, emb, Ed, H, self.K, self.Rd, trg_vocab, self.device,
+                               precision=precision)
+        self.out = OutputCE(batch, trg_time, self.Rd, vocab, label_smoothing, device=self.device,
+                            precision=precision)
         self.readout = torch.empty(batch, trg_time, self.Rd, dtype=torch.float32, device=self.device)
         self.d_readout = torch.empty_like(self.readout)
         self.dropout = None
@@ -333,20 +343,23 @@ class Seq2SeqAttention:
     def forward(self, src_ids, src_lens, targets):
         """src_ids [B, Ts], targets [B, T] int32 -> readout [B, T, Rd] (fp32)."""
         self.src_ids = src_ids
-        self.src_emb.forward(src_ids, self.src_p, out=self.x0, bf16_pitch=self.x0.shape[-1])
+        self.src_emb.forward(src_ids, self.src_p, out=self.x0,
+                             bf16_pitch=self.x0.shape[-1] if self.x0.dtype == torch.bfloat16 else None)
         self.enc_out = self.enc.forward(self.x0, src_lens)
         self.prev_ids[:, 1:].copy_(targets[:, :-1])  # prev:trg, the zero initial output at t = 0
         self.src_lens = src_lens
         return self.dec.forward(self.enc_out, src_lens, self.prev_ids, self.dec_p, readout=self.readout)
 
-    def step(self, src_ids, src_lens, targets, trg_lens=None, reducer=None, grad_scale: float = 1.0):
-        """One training step; returns the device loss (mean label-smoothed CE
-        over the valid target positions, trg_lens defaulting to src_lens)."""
+    def forward_backward(self, src_ids, src_lens, targets, trg_lens=None, reducer=None):
+        """Loss and every parameter gradient of one batch (into self.grads), no
+        optimizer update; returns the device loss (mean label-smoothed CE over the
+        valid target positions, trg_lens defaulting to src_lens).  reducer(bucket id,
+        bucket) fires as each gradient bucket completes (dp.BucketAllReducer)."""
         trg_lens = src_lens if trg_lens is None else trg_lens
         self.forward(src_ids, src_lens, targets)
         W, b = self.out_p
         if self.dropout is not None:  # batch counter = optimizer steps done (the device-side Adam counter)
-            ctr = self.opt.scratch[12:16].view(torch.int32)
+            ctr = self.dropout_counter()
             self.dropout.forward(self.readout, self.dropped, counter=ctr)
             loss, _, _, _ = self.out.forward_backward(self.dropped, targets, trg_lens, W, b, dx=self.d_dropped,
                                                       dW=self.out_g[0], db=self.out_g[1])
@@ -364,9 +377,29 @@ class Seq2SeqAttention:
         self.src_emb.backward(self.src_ids, dx, self.src_g)
         if reducer is not None:
             reducer(-4, self.src_bucket)
+        return loss
+
+    def dropout_counter(self):
+        """The dropout batch counter: the optimizer's device-side step counter."""
+        return self.opt.scratch[12:16].view(torch.int32)
+
+    def step(self, src_ids, src_lens, targets, trg_lens=None, reducer=None, grad_scale: float = 1.0):
+        """One training step: forward_backward, the data-parallel gradient
+        all-reduce (reducer), then the fused clip + Adam update; returns the device
+        loss."""
+        loss = self.forward_backward(src_ids, src_lens, targets, trg_lens, reducer)
+        if reducer is not None:
             reducer.wait()
         self.opt.step(self.grads, grad_scale=grad_scale)
         return loss
+
+    def named_params(self):
+        """{manifest name: (param view, grad view)} of every parameter."""
+        out = {}
+        for name, off, shape in self.manifest:
+            n = _numel(shape)
+            out[name] = (self.params[off:off + n].view(shape), self.grads[off:off + n].view(shape))
+        return out
 
     def check_ids(self):
         """Synchronise; raise the reference's IndexError for a bad source / target id."""

@@ -16,7 +16,10 @@ from . import lstm
 
 class OutputCE:
     def __init__(self, batch: int, time: int, input_dim: int, vocab: int, epsilon: float = 0.1,
-                 layer: str = "output_prob", device=None):
+                 layer: str = "output_prob", device=None, precision: str = "bf16"):
+        """precision "bf16": bf16 logits with the fused online-softmax epilogue
+        (sl_output_ce); "fp32": the reference's precision — fp32 logits and
+        split-bf16 tensor-core GEMMs (sl_output_ce_f32, rel. 1e-4)."""
         self.B, self.T, self.D, self.V = batch, time, input_dim, vocab
         self.eps, self.layer = epsilon, layer
         self.device = torch.device(device or "cuda")
@@ -27,7 +30,15 @@ class OutputCE:
         vp = ctypes.c_void_p
         L.sl_output_ce.argtypes = [i32] * 4 + [vp] * 5 + [ctypes.c_float] + [vp] * 4 + [ctypes.c_int, vp,
                                                                                          ctypes.c_size_t, vp, vp]
-        self.ws_bytes = L.sl_output_ce_workspace_size(batch, time, input_dim, vocab)
+        L.sl_output_ce_f32_workspace_size.restype = ctypes.c_size_t
+        L.sl_output_ce_f32_workspace_size.argtypes = [i32] * 4
+        L.sl_output_ce_f32.argtypes = L.sl_output_ce.argtypes
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be bf16 or fp32, got {precision!r}")
+        self.precision = precision
+        self._call = L.sl_output_ce_f32 if precision == "fp32" else L.sl_output_ce
+        self.ws_bytes = (L.sl_output_ce_f32_workspace_size if precision == "fp32" else
+                         L.sl_output_ce_workspace_size)(batch, time, input_dim, vocab)
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -47,7 +58,7 @@ class OutputCE:
             dW = torch.empty(D, V, dtype=torch.float32, device=dev)
         if db is None:
             db = torch.empty(V, dtype=torch.float32, device=dev)
-        lstm._check(lstm.lib().sl_output_ce(B, T, D, V, lstm._p(x), lstm._p(targets), lstm._p(seq_lens),
+        lstm._check(self._call(B, T, D, V, lstm._p(x), lstm._p(targets), lstm._p(seq_lens),
                                             lstm._p(W), lstm._p(b), self.eps, lstm._p(self.loss), lstm._p(dx),
                                             lstm._p(dW), lstm._p(db), int(accumulate), lstm._p(self.workspace),
                                             self.ws_bytes, lstm._p(self.bad), lstm._stream()))

@@ -126,3 +126,17 @@ def test_attn_decoder_descriptor_validation():
                         (_Desc(300, 7, 5, 12, 16, 8, 16, 8, 11), b"batch <= 256")):
         assert L.sl_attn_decoder_workspace_size(ctypes.byref(bad)) == 0
         assert needle in L.sl_last_error()
+
+
+def test_fp32_layers_run_on_the_tensor_cores():
+    """SL_PREC_FP32 maps to the split-bf16 tcgen05 path for every BASELINE shape
+    (configs 1-5: H = 128, 1000, 1024; B up to 1024), not the SIMT kernels."""
+    from paper_1805_05225_b200 import lstm
+    L = lstm.lib()
+    for (B, T, D, H, nd) in [(8, 20, 128, 128, 1), (128, 60, 1024, 1024, 1), (256, 60, 620, 1000, 2),
+                             (256, 60, 2000, 1000, 2), (256, 60, 2620, 1000, 1), (1024, 500, 2048, 1024, 2),
+                             (4, 9, 16, 24, 2)]:
+        d = lstm._Layer(B, T, D, H, nd, 1, lstm.PRECISIONS["fp32"], 0)
+        assert lstm.PATHS[L.sl_lstm_layer_path(ctypes.byref(d))] == "fp32_x3_tc", (B, T, D, H, nd)
+        d = lstm._Layer(B, T, D, H, nd, 1, lstm.PRECISIONS["bf16"], 0)
+        assert lstm.PATHS[L.sl_lstm_layer_path(ctypes.byref(d))] == "bf16_tc"

@@ -63,7 +63,9 @@ CASES = [(4, 7, 5, 12, 16, 8, 16, 8, 11), (16, 23, 9, 20, 64, 32, 48, 24, 50),
 # edge cases: long sources (Ts > 128: the softmax's looped tail, several energy / context
 # tiles per row) with a length-1 source row; the largest batch one call takes (256); one target step
 EDGE = [((3, 300, 6, 12, 16, 8, 16, 8, 11), [300, 1, 137]), ((256, 5, 3, 8, 8, 8, 8, 8, 7), None),
-        ((5, 129, 2, 8, 24, 16, 8, 16, 9), [129, 128, 1, 64, 2]), ((4, 7, 1, 8, 8, 8, 8, 8, 5), None)]
+        ((5, 129, 2, 8, 24, 16, 8, 16, 9), [129, 128, 1, 64, 2]), ((4, 7, 1, 8, 8, 8, 8, 8, 5), None),
+        # key_dim well below hidden: the d s = d s_tr W_s^T partials have their own row pitch
+        ((4, 7, 5, 16, 32, 128, 32, 16, 11), None), ((6, 9, 4, 8, 16, 1000, 64, 16, 7), None)]
 
 
 def check_against_restatement(dims, lens_override=None):

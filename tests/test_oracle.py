@@ -306,3 +306,19 @@ def test_gather_rows_restatement_matches_reference_bitwise():
     assert np.array_equal(g_r.astype(np.float32), g_o)
     with pytest.raises(IndexError, match="in layer 'emb'"):
         ref.gather_rows(tbl, np.full((1, 1), V, np.int32))
+
+
+def test_torch64_output_ce_restatement_matches_numpy_restatement():
+    """The fp64-torch restatement the config-4 output-layer GPU test uses
+    (tests/test_output_gpu.py::_output_ce_torch64) equals oracle.output_ce_np."""
+    import torch
+    from test_output_gpu import _output_ce_torch64
+    rng = np.random.default_rng(4)
+    B, T, D, V = 5, 7, 11, 37
+    x, W, b = rng.uniform(-1, 1, (B, T, D)), rng.uniform(-1, 1, (D, V)), rng.uniform(-1, 1, V)
+    lens = np.array([7, 3, 5, 1, 7], np.int32)
+    tg = rng.integers(0, V, (B, T)).astype(np.int32)
+    ref = oracle.output_ce_np(x, lens, tg, W, b, 0.1)
+    got = _output_ce_torch64(*(torch.as_tensor(a) for a in (x, lens, tg, W, b)), 0.1)
+    for r, g in zip(ref, got):
+        assert np.allclose(np.asarray(g), r, rtol=1e-12, atol=1e-14)
