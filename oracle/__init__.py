@@ -32,7 +32,7 @@ def build(force: bool = False) -> None:
     """Compile the restatement and, when /root/reference exists, the reference."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj"):
-        targets += ["ref", "ref-tests", "dropin"]
+        targets += ["ref", "ref-tests", "dropin", "dropin-step"]
     subprocess.run(["make", "-C", HERE, "-j8"] + (["-B"] if force else []) + targets,
                    check=True, stdout=subprocess.DEVNULL)
 
@@ -136,9 +136,24 @@ class Reference:
         if hasattr(L, "ref_output_ce"):
             L.ref_output_ce.argtypes = ([ctypes.c_int] * 4 + [_d, _i, _i, _d, _d, ctypes.c_double] + [_d] * 4 +
                                         [c, ctypes.c_int])
+        if hasattr(L, "ref_lstm_two_steps"):
+            L.ref_lstm_two_steps.argtypes = [ctypes.c_int] * 3 + [_d] * 13 + [c, ctypes.c_int]
         if hasattr(L, "ref_param_manifest_order"):
             L.ref_param_manifest_order.argtypes = [c, c, ctypes.c_int, c, ctypes.c_int]
         self.bits = 8 * L.ref_real_bytes()
+
+    def two_steps(self, x, h0, c0, W, R, b):
+        """The graph of the reference's lstm_step FD test (tape_test.cpp:477-492):
+        L = sum(step2.h) + sum(step1.h); returns (L, dx, dh0, dc0, dW, dR, db)."""
+        x, h0, c0, W, R, b = map(_f64, (x, h0, c0, W, R, b))
+        B, D = x.shape
+        H = R.shape[0]
+        out = [np.zeros_like(a) for a in (x, h0, c0, W, R, b)]
+        loss = np.zeros(1)
+        err = ctypes.create_string_buffer(512)
+        self._check(self.lib.ref_lstm_two_steps(B, D, H, *(_ptr(a) for a in (x, h0, c0, W, R, b)), _ptr(loss),
+                                                *(_ptr(a) for a in out), err, 512), err)
+        return (float(loss[0]), *out)
 
     def param_manifest_order(self, names):
         """The reference ParamStore::manifest() order of these parameter names."""

@@ -156,6 +156,38 @@ int ref_lstm_step(int B, int D, int H, const double* x, const double* h0, const 
   }
 }
 
+// The graph of the reference's own finite-difference test of lstm_step
+// (tape_test.cpp:477-492): out = lstm_step(W,R,b,x,h0,c0); out2 = lstm_step(W,R,b,x,out.h,out.c);
+// L = sum(out2.h) + sum(out.h); all six inputs are parameters.  Writes L and the gradients.
+int ref_lstm_two_steps(int B, int D, int H, const double* x, const double* h0, const double* c0,
+                       const double* W, const double* R, const double* b, double* loss, double* dx,
+                       double* dh0, double* dc0, double* dW, double* dR, double* db, char* err, int errlen) {
+  try {
+    Tape t;
+    NodeId Wn = t.param("W", make({{Axis::Feature, D}, {Axis::Other, 4 * H}}, W));
+    NodeId Rn = t.param("R", make({{Axis::Feature, H}, {Axis::Other, 4 * H}}, R));
+    NodeId bn = t.param("b", make({{Axis::Feature, 4 * H}}, b));
+    NodeId xn = t.param("x", make({{Axis::Batch, B}, {Axis::Feature, D}}, x));
+    NodeId hn = t.param("h0", make({{Axis::Batch, B}, {Axis::Feature, H}}, h0));
+    NodeId cn = t.param("c0", make({{Axis::Batch, B}, {Axis::Feature, H}}, c0));
+    auto out = t.lstm_step(Wn, Rn, bn, xn, hn, cn);
+    auto out2 = t.lstm_step(Wn, Rn, bn, xn, out.h, out.c);
+    NodeId l = t.add(sum_all(t, out2.h), sum_all(t, out.h));
+    *loss = static_cast<double>(t.value(l).scalar_value());
+    GradBuffer g = t.backward(l);
+    auto grads = t.param_gradients(g);
+    put(grads.at("x"), dx);
+    put(grads.at("h0"), dh0);
+    put(grads.at("c0"), dc0);
+    put(grads.at("W"), dW);
+    put(grads.at("R"), dR);
+    put(grads.at("b"), db);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 // The decoder output layer + loss exactly as the reference builds it:
 // ce_label_smoothing(log_softmax(add(matmul(x, W), b)), targets, eps)
 // (compiler.cpp:651-663, tape.cpp:879-924, 1224-1298), gradients by

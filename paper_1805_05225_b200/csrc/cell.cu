@@ -1,8 +1,10 @@
 // Decoder cell step (K5): Tape::lstm_step forward/backward (tape.cpp:1074-1219)
 // for the Listing-1 decoder `s` cell that the graph executor calls once per
-// target step (compiler.cpp:640-650).  Z = x W + h0 R + b is two GEMMs into a
-// stream-ordered scratch; the gate math / its adjoint are one fused
-// elementwise kernel each.
+// target step (compiler.cpp:640-650).  Z = x W + h0 R + b is two fp32-class
+// tensor-core GEMMs (split-bf16 x3) into a stream-ordered scratch; the gate
+// math / its adjoint are one fused elementwise kernel each (expf / tanhf, fp32).
+#include <algorithm>
+
 #include "cell.h"
 #include "gemm.h"
 #include "profile.h"
@@ -70,42 +72,60 @@ __global__ void colsum_kernel(int B, int N, const float* __restrict__ dz, float*
 
 int grid_for(int64_t n) { return (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8); }
 
+// stream-ordered scratch of one call: [z or dz : B x 4H fp32 | split-bf16 GEMM operands]
+size_t cell_ws(int B, int D, int H) {
+  const size_t g = std::max({gemm_f32x3_workspace_bytes(false, false, B, 4 * H, D, false),
+                             gemm_f32x3_workspace_bytes(false, false, B, 4 * H, H, false),
+                             gemm_f32x3_workspace_bytes(false, true, B, D, 4 * H, false),
+                             gemm_f32x3_workspace_bytes(false, true, B, H, 4 * H, false),
+                             gemm_f32x3_workspace_bytes(true, false, D, 4 * H, B, true),
+                             gemm_f32x3_workspace_bytes(true, false, H, 4 * H, B, false)});
+  return (size_t)round_up((int64_t)B * 4 * H * 4, 256) + g;
+}
+
 }  // namespace
 
+// Both GEMMs of the step on the tensor cores at fp32 class (gemm_f32x3.cu: split-bf16,
+// fp32 accumulation): Z = x W + b, Z += h0 R (tape.cpp:1103-1109).
 void cell_fwd(int B, int D, int H, const float* x, const float* h0, const float* c0,
               const float* W, const float* R, const float* b, float* h, float* c, float* saved,
               cudaStream_t stream) {
-  float* z = nullptr;
-  SL_CUDA_TRY(cudaMallocAsync(&z, sizeof(float) * (size_t)B * 4 * H, stream));
-  gemm_f32(false, false, B, 4 * H, D, 1.f, x, D, W, 4 * H, 0.f, z, 4 * H, b, stream);
-  gemm_f32(false, false, B, 4 * H, H, 1.f, h0, H, R, 4 * H, 1.f, z, 4 * H, nullptr, stream);
+  char* ws = nullptr;
+  SL_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), cell_ws(B, D, H), stream));
+  float* z = reinterpret_cast<float*>(ws);
+  void* g = ws + round_up((int64_t)B * 4 * H * 4, 256);
+  gemm_f32x3(false, false, B, 4 * H, D, x, D, W, 4 * H, 0.f, z, 4 * H, b, nullptr, 0, g, stream);
+  gemm_f32x3(false, false, B, 4 * H, H, h0, H, R, 4 * H, 1.f, z, 4 * H, nullptr, nullptr, 0, g, stream);
   cell_gates_kernel<<<grid_for((int64_t)B * H), 256, 0, stream>>>(B, H, z, c0, h, c, saved);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
-  SL_CUDA_TRY(cudaFreeAsync(z, stream));
+  SL_CUDA_TRY(cudaFreeAsync(ws, stream));
 }
 
 void cell_bwd(int B, int D, int H, const float* x, const float* h0, const float* c0,
               const float* W, const float* R, const float* saved, const float* gh,
               const float* gc, float* dx, float* dh0, float* dc0, float* dW, float* dR,
               float* db, int accumulate, cudaStream_t stream) {
-  float* dz = nullptr;
+  char* ws = nullptr;
   const float beta = accumulate ? 1.f : 0.f;
-  SL_CUDA_TRY(cudaMallocAsync(&dz, sizeof(float) * (size_t)B * 4 * H, stream));
+  SL_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ws), cell_ws(B, D, H), stream));
+  float* dz = reinterpret_cast<float*>(ws);
+  void* g = ws + round_up((int64_t)B * 4 * H * 4, 256);
   cell_dz_kernel<<<grid_for((int64_t)B * H), 256, 0, stream>>>(B, H, saved, c0, gh, gc, dz, dc0,
                                                                accumulate);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
-  if (dx) gemm_f32(false, true, B, D, 4 * H, 1.f, dz, 4 * H, W, 4 * H, beta, dx, D, nullptr, stream);
-  if (dh0) gemm_f32(false, true, B, H, 4 * H, 1.f, dz, 4 * H, R, 4 * H, beta, dh0, H, nullptr, stream);
-  if (dW) gemm_f32(true, false, D, 4 * H, B, 1.f, x, D, dz, 4 * H, beta, dW, 4 * H, nullptr, stream);
-  if (dR) gemm_f32(true, false, H, 4 * H, B, 1.f, h0, H, dz, 4 * H, beta, dR, 4 * H, nullptr, stream);
-  if (db) {
+  if (dx) gemm_f32x3(false, true, B, D, 4 * H, dz, 4 * H, W, 4 * H, beta, dx, D, nullptr, nullptr, 0, g, stream);
+  if (dh0) gemm_f32x3(false, true, B, H, 4 * H, dz, 4 * H, R, 4 * H, beta, dh0, H, nullptr, nullptr, 0, g, stream);
+  if (dW) {  // [dW; db] = [x | 1]^T dz in one GEMM
+    gemm_f32x3(true, false, D, 4 * H, B, x, D, dz, 4 * H, beta, dW, 4 * H, nullptr, db, 4 * H, g, stream);
+  } else if (db) {
     colsum_kernel<<<(unsigned)ceil_div(4 * H, 256), 256, 0, stream>>>(B, 4 * H, dz, db, accumulate);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
   }
-  SL_CUDA_TRY(cudaFreeAsync(dz, stream));
+  if (dR) gemm_f32x3(true, false, H, 4 * H, B, h0, H, dz, 4 * H, beta, dR, 4 * H, nullptr, nullptr, 0, g, stream);
+  SL_CUDA_TRY(cudaFreeAsync(ws, stream));
 }
 
 }  // namespace sl

@@ -16,13 +16,12 @@
 // test build (oracle/Makefile: dropin) compiles this TU with SEQLOOM_DROPIN_
 // FRIEND_HACK, which exposes them without editing the reference sources.
 //
-// Precision: SEQLOOM_CUDA_PRECISION=bf16 selects SL_PREC_BF16, default fp32.
+// Precision: SEQLOOM_CUDA_PRECISION=bf16 selects SL_PREC_BF16, default fp32
+// (fp32-class split-bf16 tensor cores).  Device buffers come from a process-wide
+// pool (dropin_util.hpp): no cudaMalloc per call after warm-up.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-#include <cstring>
 #include <memory>
-#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -40,55 +39,11 @@
 #endif
 #include "seqloom/layers.hpp"
 #include "seqloom_cuda.h"
+#include "dropin_util.hpp"
 
 namespace seqloom {
-namespace {
 
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw std::runtime_error(std::string("lstm_sequence (cuda): ") + what + ": " +
-                                                 cudaGetErrorString(e));
-}
-
-// Maps a C-ABI status to the reference's exception types (layers.cpp:10-16).
-void rethrow(int rc) {
-  if (rc == SL_OK) return;
-  const std::string msg = sl_last_error();
-  if (rc == SL_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
-  if (rc == SL_ERR_SHAPE) throw ShapeError(msg);
-  throw std::runtime_error("lstm_sequence (cuda): " + msg);
-}
-
-struct DevBuf {
-  void* p = nullptr;
-  explicit DevBuf(size_t bytes) { ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
-  ~DevBuf() { cudaFree(p); }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  float* f() const { return static_cast<float*>(p); }
-};
-
-std::shared_ptr<DevBuf> upload(const Tensor& t) {
-  auto buf = std::make_shared<DevBuf>(sizeof(float) * (size_t)t.size());
-  std::vector<float> tmp(t.data().begin(), t.data().end());  // Real -> float
-  ck(cudaMemcpy(buf->p, tmp.data(), sizeof(float) * tmp.size(), cudaMemcpyHostToDevice), "H2D");
-  return buf;
-}
-
-Tensor download(const DevBuf& d, Shape shape) {
-  Tensor t = Tensor::zeros(std::move(shape));
-  std::vector<float> tmp((size_t)t.size());
-  ck(cudaMemcpy(tmp.data(), d.p, sizeof(float) * tmp.size(), cudaMemcpyDeviceToHost), "D2H");
-  auto dst = t.data();
-  for (size_t i = 0; i < tmp.size(); ++i) dst[i] = static_cast<Real>(tmp[i]);
-  return t;
-}
-
-int precision_from_env() {
-  const char* p = std::getenv("SEQLOOM_CUDA_PRECISION");
-  return (p && std::strcmp(p, "bf16") == 0) ? SL_PREC_BF16 : SL_PREC_FP32;
-}
-
-}  // namespace
+using namespace cuda_dropin;
 
 NodeId lstm_sequence(Tape& tape, NodeId W, NodeId R, NodeId b, NodeId xs, int direction) {
   const Tensor& x = tape.value(xs);
@@ -114,12 +69,12 @@ NodeId lstm_sequence(Tape& tape, NodeId W, NodeId R, NodeId b, NodeId xs, int di
 
   sl_lstm_layer L{(int32_t)B, (int32_t)T, (int32_t)D, (int32_t)H, 1, direction,
                   precision_from_env(), 0};
-  rethrow(sl_lstm_layer_check(&L));
+  rethrow(sl_lstm_layer_check(&L), "lstm_sequence");
   const bool grad = tape.any_needs_grad({W, R, b, xs});
   auto dx_ = upload(x), dW_ = upload(tW), dR_ = upload(tR), db_ = upload(tb);
-  auto dl_ = std::make_shared<DevBuf>(sizeof(int32_t) * B);
+  auto dl_ = std::make_shared<DevBuf>(sizeof(int32_t) * B);  // (pool block of B int32)
   ck(cudaMemcpy(dl_->p, lens.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice), "H2D lens");
-  auto y_ = std::make_shared<DevBuf>(sizeof(float) * B * T * H);
+  auto y_ = alloc((size_t)(B * T * H));
   const size_t ws_bytes = sl_lstm_workspace_size(&L), rs_bytes = sl_lstm_reserve_size(&L);
   auto ws_ = std::make_shared<DevBuf>(ws_bytes);
   auto rs_ = grad ? std::make_shared<DevBuf>(rs_bytes) : nullptr;
@@ -128,8 +83,8 @@ NodeId lstm_sequence(Tape& tape, NodeId W, NodeId R, NodeId b, NodeId xs, int di
   const float* bp[1] = {db_->f()};
   rethrow(sl_lstm_layer_fwd(&L, dx_->f(), static_cast<int32_t*>(dl_->p), Wp, Rp, bp, y_->f(),
                             nullptr, nullptr, rs_ ? rs_->p : nullptr, rs_ ? rs_bytes : 0, ws_->p,
-                            ws_bytes, nullptr));
-  ck(cudaDeviceSynchronize(), "forward");
+                            ws_bytes, nullptr),
+          "lstm_sequence");
   Tensor y = download(*y_, {{Axis::Batch, B}, {Axis::Time, T}, {Axis::Feature, H}});
   if (x.seq_lens()) y.set_seq_lens(*x.seq_lens());
   NodeId yid = tape.emit(std::move(y), grad);
@@ -139,10 +94,8 @@ NodeId lstm_sequence(Tape& tape, NodeId W, NodeId R, NodeId b, NodeId xs, int di
       const Tensor* gy = g.get(yid);
       if (!gy) return;
       auto dy_ = upload(*gy);
-      auto gx_ = std::make_shared<DevBuf>(sizeof(float) * B * T * D);
-      auto gW_ = std::make_shared<DevBuf>(sizeof(float) * D * 4 * H);
-      auto gR_ = std::make_shared<DevBuf>(sizeof(float) * H * 4 * H);
-      auto gb_ = std::make_shared<DevBuf>(sizeof(float) * 4 * H);
+      auto gx_ = alloc((size_t)(B * T * D)), gW_ = alloc((size_t)(D * 4 * H));
+      auto gR_ = alloc((size_t)(H * 4 * H)), gb_ = alloc((size_t)(4 * H));
       const float* Wq[1] = {dW_->f()};
       const float* Rq[1] = {dR_->f()};
       float* gWq[1] = {gW_->f()};
@@ -150,8 +103,8 @@ NodeId lstm_sequence(Tape& tape, NodeId W, NodeId R, NodeId b, NodeId xs, int di
       float* gbq[1] = {gb_->f()};
       rethrow(sl_lstm_layer_bwd(&L, dx_->f(), static_cast<int32_t*>(dl_->p), Wq, Rq, dy_->f(),
                                 nullptr, nullptr, gx_->f(), gWq, gRq, gbq, 0, rs_->p, rs_bytes,
-                                ws_->p, ws_bytes, nullptr));
-      ck(cudaDeviceSynchronize(), "backward");
+                                ws_->p, ws_bytes, nullptr),
+              "lstm_sequence");
       // GradBuffer::accumulate contract (tape.cpp:76-89), only for inputs needing grads
       if (tp.needs_grad(xs)) g.accumulate(xs, download(*gx_, tp.value(xs).shape()));
       if (tp.needs_grad(W)) g.accumulate(W, download(*gW_, tp.value(W).shape()));
