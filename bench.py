@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("SL_BENCH_PREC", "fp32"),
                     help="fp32 (default, the reference's precision: split-bf16 x3 tensor cores, rel. 1e-4) or bf16")
+    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=4,
+                    help="BASELINE.json configs[i-1]: 4 (default) = the headline training step; 1-3 = LSTM "
+                         "layer / stack fwd+bwd; 5 = the inference sweep")
     ap.add_argument("--no-bf16-line", action="store_true",
                     help="skip the bf16-mode companion measurement reported beside the fp32 headline")
     ap.add_argument("--batch", type=int, default=256, help="sequences per GPU (weak scaling)")
@@ -494,6 +497,268 @@ def relaunch(args) -> int:
     return subprocess.call(cmd, env=env)
 
 
+# ---------------------------------------------------------------- configs 1, 2, 3, 5
+# BASELINE.json configs (SURVEY §8 shapes table, §9 decisions): layers, directions, H, D0, B, T
+LAYER_CONFIGS = {
+    1: dict(layers=1, dirs=1, H=128, D0=128, B=8, T=20, train=True,
+            name="config1: single-layer unidirectional LSTM n=128, B=8, T=20, fp32 fwd+bwd (D=H)"),
+    2: dict(layers=1, dirs=1, H=1024, D0=1024, B=128, T=60, train=True,
+            name="config2: single-layer LSTM n=1024, B=128, T=60 fwd+bwd on 1xB200 (D=H; kernel micro-benchmark)"),
+    3: dict(layers=4, dirs=2, H=1000, D0=620, B=256, T=60, train=True,
+            name="config3: 4-layer bidirectional LSTM encoder n=1000, B=256, T=60 fwd+bwd, both directions "
+                 "concurrent (D0=620)"),
+    5: dict(layers=6, dirs=2, H=1024, D0=40, B=None, T=None, train=False,
+            name="config5: 6-layer BLSTM n=1024 encoder inference (F=40 input features), batch-sharded "
+                 "(no communication)"),
+}
+SWEEP = [(1, 60), (16, 60), (64, 60), (256, 60), (1024, 60), (1, 500), (16, 500), (64, 500), (256, 500), (1024, 500)]
+
+
+def _layer_stack(spec, B, T, precision, dev):
+    from paper_1805_05225_b200 import lstm
+    from paper_1805_05225_b200.encoder import BLSTMEncoder
+    if spec["dirs"] == 2:
+        enc = BLSTMEncoder(spec["layers"], B, T, spec["D0"], spec["H"], precision, dev, train=spec["train"])
+        enc.init_uniform(seed=1)
+        return enc
+    H, D = spec["H"], spec["D0"]
+    layer = lstm.LSTMLayer(B, T, D, H, 1, 1, precision, dev)
+    s = H ** -0.5
+    g = torch_gen(dev, 1)
+    import torch
+    W = [(torch.rand(D, 4 * H, device=dev, generator=g) * 2 - 1) * s]
+    R = [(torch.rand(H, 4 * H, device=dev, generator=g) * 2 - 1) * s]
+    b = [(torch.rand(4 * H, device=dev, generator=g) * 2 - 1) * s]
+    y, dx = torch.empty(B, T, H, device=dev), torch.empty(B, T, D, device=dev)
+    dW, dR, db = [torch.empty_like(W[0])], [torch.empty_like(R[0])], [torch.empty_like(b[0])]
+
+    class One:
+        def forward(self, x, lens, train=True):
+            layer.forward(x, lens, W, R, b, y=y)
+            return y
+
+        def backward(self, dy):
+            layer.backward(dy, dx=dx, dW=dW, dR=dR, db=db, need_dx=True)
+            return dx
+    return One()
+
+
+def torch_gen(dev, seed):
+    import torch
+    return torch.Generator(device=dev).manual_seed(seed)
+
+
+def _time_layers(args, spec, B, T, precision, local_rank, rank):
+    """K timed steps of fwd(+bwd) of the config's stack (CUDA graph replay), with the
+    per-phase events of one eager pass and the H2D/D2H end-to-end leg."""
+    import torch
+    from paper_1805_05225_b200 import lstm
+    dev = torch.device("cuda", local_rank)
+    net = _layer_stack(spec, B, T, precision, dev)
+    g = torch_gen(dev, 100 + rank)
+    x = torch.rand(B, T, spec["D0"], device=dev, generator=g) * 2 - 1
+    lens = torch.full((B,), T, dtype=torch.int32, device=dev)
+    out_w = spec["dirs"] * spec["H"]
+    dy = torch.rand(B, T, out_w, device=dev, generator=g) * 2 - 1
+    lib = lstm.lib()
+    lib.sl_profile_enable.argtypes = [ctypes.c_int]
+    lib.sl_launch_count.restype = ctypes.c_ulonglong
+
+    def step():
+        y = net.forward(x, lens, train=spec["train"])
+        if spec["train"]:
+            net.backward(dy)
+        return y
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    class Entry(ctypes.Structure):
+        _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_int32), ("ms", ctypes.c_double),
+                    ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+    lib.sl_profile_read(None, 0, 1)
+    lib.sl_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    lib.sl_profile_enable(0)
+    eager_ms = e0.elapsed_time(e1)
+    entries = (Entry * 64)()
+    n = lib.sl_profile_read(entries, 64, 1)
+    phases = {e.name.decode(): {"calls": e.calls, "ms": e.ms, "flops": e.flops, "bytes": e.bytes}
+              for e in entries[:n]}
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    c0 = lib.sl_launch_count()
+    with torch.cuda.graph(graph):
+        y_out = step()
+    per_step = lib.sl_launch_count() - c0
+    graph.replay()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # end to end: pinned host input in, the output (inference) / a checksum (training) out
+    hx = x.cpu().pin_memory()
+    hy = torch.empty(y_out.shape, dtype=y_out.dtype).pin_memory() if not spec["train"] else \
+        torch.empty((), dtype=torch.float32).pin_memory()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x.copy_(hx, non_blocking=True)
+        graph.replay()
+        if spec["train"]:
+            hy.copy_(y_out.float().sum(), non_blocking=True)
+        else:
+            hy.copy_(y_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = time.perf_counter() - t0
+    return dict(ms=ms, eager_ms=eager_ms, phases=phases, launches=per_step * args.steps, clocks=clocks.summary(),
+                e2e_s=e2e_s, h2d=hx.numel() * hx.element_size(), d2h=hy.numel() * hy.element_size())
+
+
+def cpu_reference_layers(args, spec, B, T, steps=1):
+    """The reference's lstm_sequence (oracle/_ref, fp32, OpenBLAS 1 thread per tape) on
+    B/N-row shards per host thread, fwd(+bwd) of every layer-direction
+    of the config; layers run one after another in the reference: step time = sum."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    import oracle
+    try:
+        ref, kind = oracle.Reference(32), "reference"
+    except FileNotFoundError:
+        ref, kind = oracle.Restatement(), "port"
+    threads = max(1, min(os.cpu_count() or 1, 64, B))
+    rows = -(-B // threads)
+    H, L, nd = spec["H"], spec["layers"], spec["dirs"]
+    rng = np.random.default_rng(0)
+    s = 1 / np.sqrt(H)
+    shapes = sorted({spec["D0"]} | ({nd * H} if L > 1 else set()))
+    params = {D: tuple(rng.uniform(-s, s, shp) for shp in ((D, 4 * H), (H, 4 * H), (4 * H,))) for D in shapes}
+    xs = {D: rng.uniform(-1, 1, (rows, T, D)) for D in shapes}
+    lens = np.full(rows, T, np.int32)
+    dy = rng.uniform(-1, 1, (rows, T, H)) if spec["train"] else None
+
+    def one(out):
+        tt = {}
+        for D in shapes:
+            t0 = time.perf_counter()
+            if kind == "reference":
+                ref.sequence(xs[D], lens, *params[D], 1, dy)
+            elif dy is not None:
+                ref.sequence_bwd(xs[D], lens, *params[D], 1, dy)
+            else:
+                ref.sequence_fwd(xs[D], lens, *params[D], 1)
+            tt[D] = time.perf_counter() - t0
+        out.append(tt)
+
+    secs = []
+    for _ in range(steps):
+        res = []
+        ths = [threading.Thread(target=one, args=(res,)) for _ in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        per = {D: max(r[D] for r in res) for D in shapes}
+        secs.append(sum(nd * per[spec["D0"] if l == 0 else nd * H] for l in range(L)))
+    sec = statistics.median(secs)
+    return {"value": threads * rows * T / sec, "unit": "tokens/s" if spec["train"] else "frames/s",
+            "cores": threads, "kind": kind, "seconds_per_step": sec,
+            "sample": f"{threads} threads x {rows}-sequence shard (T={T}): one lstm_sequence "
+                      f"{'fwd+bwd' if spec['train'] else 'fwd'} per distinct layer input width {shapes} (H={H}), "
+                      f"step = sum over the {L} x {nd} layer-directions (the reference runs them one after "
+                      f"another); fp32 reference build, OpenBLAS 1 thread/tape; median of {steps}"}
+
+
+def run_layer_config(args, rank, world, local_rank):
+    """--config 1, 2, 3 (training fwd+bwd) or 5 (inference sweep): one JSON line, same schema."""
+    import torch
+    spec = LAYER_CONFIGS[args.config]
+    H, L, nd = spec["H"], spec["layers"], spec["dirs"]
+    torch.cuda.set_device(local_rank)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    x3 = 3 if args.precision == "fp32" else 1
+    points = SWEEP if args.config == 5 else [(spec["B"], spec["T"])]
+    lines = []
+    for (B, T) in points:
+        r = _time_layers(args, spec, B, T, args.precision, local_rank, rank)
+        tokens = world * B * T * args.steps
+        ph = r["phases"]
+        top = max(ph.items(), key=lambda kv: kv[1]["ms"]) if ph else (None, None)
+        roof = None
+        if top[0]:
+            name, e = top
+            per_launch_ms = e["ms"] / max(e["calls"], 1)
+            achieved = x3 * e["flops"] / max(e["calls"], 1) / (per_launch_ms / 1e3) / 1e12
+            peak = peaks.get("bf16_tflops_sustained", 1400.0)
+            roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None, "share_of_step": e["ms"] / r["eager_ms"],
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)" if peaks else "fallback",
+                    "achieved_counts": "executed tensor FLOP/s (x3: 3 bf16 products per fp32 product)" if x3 == 3
+                    else "algorithmic FLOP/s",
+                    "phases": {k: {"calls": v["calls"], "ms_per_call": v["ms"] / max(v["calls"], 1)}
+                               for k, v in ph.items()}}
+            f_sm = (r["clocks"].get("sm_mhz") or 1965.0) * 1e6
+            rec = {}
+            for pname in ("k2_rec_fwd", "k3_rec_bwd"):
+                e = ph.get(pname)
+                if not e:
+                    continue
+                ndl = 1 if x3 == 3 else nd
+                us = e["ms"] / max(e["calls"], 1) * 1e3 / T
+                smem_us = ndl * 4 * H * H * 2 * (2 if x3 == 3 else 1) / (148 * 128 * f_sm) * 1e6
+                tens_us = x3 * 2.0 * min(B, 256) * 4 * H * H * ndl / (peak * 1e12) * 1e6
+                rec[pname] = {"us_per_step": us, "wh_smem_bound_us": smem_us, "tensor_bound_us": tens_us,
+                              "ratio_to_bound": us / max(smem_us, tens_us)}
+            roof["recurrence_per_step"] = rec
+        lines.append({"B": B, "T": T, "value": tokens / (r["ms"] / 1e3), "ms_per_step": r["ms"] / args.steps,
+                      "e2e": {"value": tokens / r["e2e_s"], "unit": "tokens/s" if spec["train"] else "frames/s",
+                              "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                              "timing": "host wall clock: pinned input H2D, graph replay, output D2H"},
+                      "gpu_launches": r["launches"], "clocks": r["clocks"], "roofline": roof,
+                      "eager_ms_per_step": r["eager_ms"] / args.steps})
+    head = lines[-1]  # config 5: the largest point (B=1024, T=500) is the headline
+    unit = "tokens/s" if spec["train"] else "frames/s"
+    cfg = {"workload": spec["name"], "layers": L, "directions": nd, "hidden": H, "input_dim": spec["D0"],
+           "batch_per_gpu": head["B"], "global_batch": head["B"] * world, "seq_len": head["T"],
+           "parallelism": f"dp{world}" if spec["train"] else f"batch-sharded x{world} (no communication)",
+           "seq_lens": "all = T", "l2": "inputs, weights and saved activations exceed the 126 MB L2"
+           if args.config != 1 else "config 1 fits in L2 (126 MB): timed as back-to-back graph replays"}
+    out = {"metric": f"LSTM {'fwd+bwd' if spec['train'] else 'inference'} {unit} ({spec['name'].split(':')[0]})",
+           "value": head["value"], "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": args.precision.replace("fp", "f"), "data": "synthetic (x ~ U(-1,1), params ~ U(+-1/sqrt(H)))",
+           "config": cfg, "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+           "roofline": head["roofline"], "eager_ms_per_step": head["eager_ms_per_step"]}
+    if args.config == 5:
+        out["sweep"] = [{k: v for k, v in p.items() if k in ("B", "T", "value", "ms_per_step")} for p in lines]
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            out["cpu_baseline"] = cpu_reference_layers(args, spec, min(head["B"], 256), min(head["T"], 60))
+            out["cpu_baseline"]["sample"] += (" (config 5: the B=256, T=60 point)" if args.config == 5 else "")
+        except Exception as exc:
+            out["cpu_baseline"] = {"error": repr(exc)}
+    return out
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -545,6 +810,18 @@ def main():
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks=N) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.config != 4:
+        out = run_layer_config(args, rank, world, local_rank)
+        if world > 1:  # max over ranks of the step time (weak scaling: every rank runs the per-GPU batch)
+            t = torch.tensor([out["ms_per_step"]], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out["ms_per_step"] = float(t.item())
+            out["value"] = world * out["config"]["batch_per_gpu"] * out["config"]["seq_len"] / (out["ms_per_step"] / 1e3)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
