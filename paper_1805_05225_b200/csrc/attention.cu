@@ -440,9 +440,11 @@ static int vec_e(const AttnArgs& p) {
 }
 
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {
-  p.s_tr = static_cast<float*>(ws);
-  gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws),
-             st);  // s_tr = s W_s + b_s
+  p.s_tr = p.s_tr_out ? p.s_tr_out : static_cast<float*>(ws);
+  if (p.W_s3_fwd)  // s_tr = s W_s + b_s
+    gemm_f32x3_pb(false, false, p.B, p.K, p.H, s, p.H, p.W_s3_fwd, 0.f, p.s_tr, p.K, b_s, x3_ws(p, ws), st);
+  else
+    gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
   float* e = row_buf(p, ws);
   Phase ph(st, "k8_attention_fwd", 0.0, 4.0 * p.B * p.Ts * (double)(p.K + p.E));
   const dim3 g1((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
@@ -461,10 +463,13 @@ void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_
 
 void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, float* d_s, float* d_W_s,
                    float* d_b_s, void* ws, cudaStream_t st) {
-  p.s_tr = static_cast<float*>(ws);
-  p.d_s_tr = p.s_tr + (size_t)p.B * p.K;
-  gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws),
-             st);  // recompute s_tr
+  p.d_s_tr = static_cast<float*>(ws) + (size_t)p.B * p.K;
+  if (p.s_tr_in) {  // the forward's s_tr
+    p.s_tr = const_cast<float*>(p.s_tr_in);
+  } else {  // recompute s_tr
+    p.s_tr = static_cast<float*>(ws);
+    gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
+  }
   if (!p.accumulate) {
     SL_CUDA_TRY(cudaMemsetAsync(p.d_W_fb, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_b_fb, 0, sizeof(float) * p.K, st));
@@ -486,7 +491,9 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     count_launch(2);
   }
   const float beta = p.accumulate ? 1.f : 0.f;
-  if (d_s)  // d s = d s_tr W_s^T
+  if (d_s && p.W_s3_bwd)  // d s = d s_tr W_s^T
+    gemm_f32x3_pb(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, p.W_s3_bwd, beta, d_s, p.H, nullptr, x3_ws(p, ws), st);
+  else if (d_s)
     gemm_f32x3(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, W_s, p.K, beta, d_s, p.H, nullptr, nullptr, 0,
                x3_ws(p, ws), st);
   if (d_W_s)  // [d W_s; d b_s] = [s | 1]^T d s_tr

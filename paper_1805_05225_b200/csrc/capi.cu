@@ -240,6 +240,7 @@ struct BwdWork {
   float* dzf = nullptr;                           // x3 path: DZ of both directions fp32 [B*T, nd*4H]
   float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
   void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
+  __nv_bfloat16* dz3 = nullptr;                   // x3 path: DZ_d split once for both dW and dR
   unsigned* bar = nullptr;
 };
 
@@ -261,6 +262,7 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
     w.dzf = c.take<float>((size_t)d.BT() * d.nd * g4(d));
     w.wcatf = c.take<float>((size_t)d.D * d.nd * g4(d));
     w.gws = c.take<char>(x3_gemm_ws(d, true));
+    w.dz3 = c.take<__nv_bfloat16>(x3_b_elems(false, 4 * d.H, (int)d.BT()));
     for (int k = 0; k < d.nd; ++k) {
       w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
       w.dzringlo[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
@@ -387,20 +389,24 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
   }
   for (int k = 0; k < d.nd; ++k) {
     float* dbk = db ? db[k] : nullptr;
-    if ((dW && dW[k]) || dbk) {
+    const bool want_w = dW && dW[k], want_r = dR && dR[k];
+    if (want_w || want_r) {  // DZ_d's K-tripled image, split once for both weight-gradient GEMMs
+      Phase ph(st, "x3_split", 0.0, 10.0 * M * G);
+      x3_split_b(false, (int)G, M, w.dzf + k * G, Gc, w.dz3, st);
+    }
+    if (want_w || dbk) {
       Phase ph(st, "k4_dw_gemm", 2.0 * M * (double)G * d.D);
-      if (dW && dW[k]) {
-        gemm_f32x3(true, false, d.D, (int)G, M, x, d.D, w.dzf + k * G, Gc, beta, dW[k], G, nullptr, dbk, G, w.gws, st);
+      if (want_w) {
+        gemm_f32x3_pb(true, false, d.D, (int)G, M, x, d.D, w.dz3, beta, dW[k], G, nullptr, w.gws, st, dbk, G);
       } else {  // db alone: fixed-order column sums of DZ_d
         colsum_f32_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, w.dzf + k * G, Gc, beta, dbk);
         SL_CUDA_TRY(cudaGetLastError());
         count_launch();
       }
     }
-    if (dR && dR[k]) {
+    if (want_r) {
       Phase ph(st, "k4_dr_gemm", 2.0 * M * (double)G * d.H);
-      gemm_f32x3(true, false, d.H, (int)G, M, rv.hprev[k], d.H, w.dzf + k * G, Gc, beta, dR[k], G, nullptr, nullptr,
-                 0, w.gws, st);
+      gemm_f32x3_pb(true, false, d.H, (int)G, M, rv.hprev[k], d.H, w.dz3, beta, dR[k], G, nullptr, w.gws, st);
     }
   }
 }

@@ -40,6 +40,8 @@ struct FLay {
   float* w2;  // [E + H, 4H] staging of [W_att; R]
   int32_t* ids_tm;
   __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
+  __nv_bfloat16 *ws_f, *ws_b;    // W_s split for s_tr = s W_s and d s = d s_tr W_s^T
+  float* str_all;                // [T, B, K] s_tr of every step (the backward reuses it)
   void *att_ws, *gws, *emb_ws;
   size_t bytes;
 };
@@ -102,6 +104,9 @@ FLay flayout(const DecDims& d, void* base) {
   L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
   L.wd2_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)(4 * H), (int)L.XA) * 2));
   L.wd2_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)L.XA, (int)(4 * H)) * 2));
+  L.ws_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)K, (int)H) * 2));
+  L.ws_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)H, (int)K) * 2));
+  L.str_all = tf(T * B * K);
   L.att_ws = take(attention_workspace_bytes(d.B, d.K, d.H, d.Ts));
   L.gws = take(gemm_ws_bytes(d));
   L.emb_ws = take(embedding_workspace_bytes(BT, d.Vt));
@@ -248,6 +253,8 @@ AttnArgs att_args(const DecDims& d, const FLay& L, const DecParams& p, const flo
   a.b_fb = p.fb_b;
   a.v = p.e_W;
   a.b_v = p.e_b;
+  a.W_s3_fwd = L.ws_f;
+  a.W_s3_bwd = L.ws_b;
   return a;
 }
 
@@ -282,6 +289,8 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
       x3_split_b(false, 4 * H, E + H, w2, 4 * H, L.wd2_f, st);
       x3_split_b(true, E + H, 4 * H, w2, 4 * H, L.wd2_b, st);
     }
+    x3_split_b(false, K, H, p.str_W, K, L.ws_f, st);  // W_s [H, K], both roles
+    x3_split_b(true, H, K, p.str_W, K, L.ws_b, st);
     f32_ids_tm_kernel<<<grid_of(BT), 256, 0, st>>>(prev_ids, B, T, L.ids_tm);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -308,6 +317,7 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     a.att = L.att_all + (int64_t)t * B * E;
     a.a = L.a_all + (int64_t)t * B * d.Ts;
     a.accum_out = L.acc_all + (int64_t)(t + 1) * B * d.Ts;
+    a.s_tr_out = L.str_all + (int64_t)t * B * K;
     attention_fwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.att_ws, st);
     // att_t -> the readout input (columns H + Emb..) and the next step's [att ‖ s] row
     SL_CUDA_TRY(cudaMemcpy2DAsync(L.ro + (int64_t)t * B * L.RO + H + Emb, L.RO * 4, a.att, (size_t)E * 4,
@@ -376,6 +386,7 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     a.d_v = g.e_W;
     a.d_b_v = g.e_b;
     a.accumulate = 1;  // every accumulator was zeroed above; d accum_{t-1} is zeroed per step
+    a.s_tr_in = L.str_all + (int64_t)t * B * K;
     SL_CUDA_TRY(cudaMemsetAsync(a.d_accum, 0, sizeof(float) * B * d.Ts, st));
     attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, g.str_W, g.str_b, L.att_ws, st);
     {

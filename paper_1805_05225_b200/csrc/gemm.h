@@ -21,7 +21,7 @@ size_t x3_b_elems(bool transB, int N, int K);
 void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfloat16* B3, cudaStream_t st);
 void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
                    const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
-                   cudaStream_t st);
+                   cudaStream_t st, float* ones_row_out = nullptr, int64_t ld_ones = 0);
 void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float beta, float* C, int64_t ldc, const float* bias, float* ones_row_out,
                 int64_t ld_ones, void* ws, cudaStream_t st);
@@ -65,6 +65,11 @@ struct TcGemm {
   // with Cb, to Cb + z * split_stride (bf16)
   int ksplit = 1;
   int64_t split_stride = 0;
+  // optional (pair GEMM, fp32 C only): accumulate K in chunks of kchunk 64-wide blocks —
+  // each chunk in a fresh TMEM accumulator, the chunk sums added in fp32 registers by the
+  // epilogue (round-to-nearest) — so the tensor core's accumulation error stays at the
+  // one-chunk level for any K (gemm_f32x3.cu)
+  int kchunk = 0;
 };
 // number of K splits the pair GEMM would use to fill the SMs for this shape
 int gemm_tc2_ksplit(int M, int N, int K);

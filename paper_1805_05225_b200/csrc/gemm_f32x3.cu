@@ -59,6 +59,46 @@ __global__ void split3_kernel(const float* __restrict__ S, int64_t ld, int rows,
   }
 }
 
+// The same split, 8 contiguous columns per thread: two 16 B loads, three 16 B stores
+// (every row and the ld's 16 B aligned, cols_ext % 8 == 0 handled by the caller).
+__global__ void split3_v8_kernel(const float* __restrict__ S, int64_t ld, int rows, int cols, bool k_cols, int Kp,
+                                 int lo_mask, int ones_col, __nv_bfloat16* __restrict__ D, int64_t dld,
+                                 int rows_ext, int cols_ext) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= cols_ext) return;
+  for (int r = blockIdx.y; r < rows_ext; r += gridDim.y) {
+    float x[8];
+    if (r < rows && c + 8 <= cols) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(S + (int64_t)r * ld + c));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(S + (int64_t)r * ld + c + 4));
+      x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int cc = c + i;
+        x[i] = (r < rows && cc < cols) ? S[(int64_t)r * ld + cc] : (r < rows && cc == ones_col) ? 1.f : 0.f;
+      }
+    }
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat16 h0, l0, h1, l1;
+      split_bf16(x[2 * i], h0, l0);
+      split_bf16(x[2 * i + 1], h1, l1);
+      __nv_bfloat162 hh, ll;
+      hh.x = h0, hh.y = h1, ll.x = l0, ll.y = l1;
+      hi[i] = *reinterpret_cast<uint32_t*>(&hh);
+      lo[i] = *reinterpret_cast<uint32_t*>(&ll);
+    }
+    const uint4 vh = make_uint4(hi[0], hi[1], hi[2], hi[3]), vl = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+    for (int copy = 0; copy < 3; ++copy) {
+      __nv_bfloat16* dst = k_cols ? D + (int64_t)r * dld + copy * Kp + c : D + (int64_t)(copy * Kp + r) * dld + c;
+      *reinterpret_cast<uint4*>(dst) = ((lo_mask >> copy) & 1) ? vl : vh;
+    }
+  }
+}
+
 // C[m, n] = sum_z P[z][m, n] (fixed order: deterministic) + bias[n] + beta C[m, n]; rows >= m_split -> C2
 __global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t pstride, int64_t pld, int M, int N,
                                      float beta, float* C, int64_t ldc, const float* __restrict__ bias, int m_split,
@@ -76,6 +116,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t
   *dst = s;
   }
 }
+
+constexpr int kX3ChunkBlocks = 48;  // K blocks (of 64) per tensor-core accumulation chunk
 
 struct X3Dims {
   int Kp;
@@ -96,14 +138,12 @@ X3Dims x3_dims(bool transA, bool transB, int M, int N, int K, bool a_ones) {
   const int Mt = M + (a_ones ? 1 : 0);
   // The tensor core's fp32 accumulation is not round-to-nearest: its error grows
   // linearly with the number of accumulated K steps (measured, scripts/x3_accuracy.py:
-  // ~3e-5 relative at K = 4096, ~1e-4 at 20000, ~3e-4 at 60000).  Long K is therefore
-  // split into ranges of <= kMaxKBlocks 64-wide blocks whose fp32 partials are summed
-  // in a fixed order on the CUDA cores (round-to-nearest): the error stays at the
-  // one-range level for any K.
-  constexpr int kMaxKBlocks = 48;
-  const int nk = (int)ceil_div(3 * (int64_t)d.Kp, 64);
-  const int want = std::max(gemm_tc2_ksplit(Mt, N, 3 * d.Kp), (int)ceil_div(nk, kMaxKBlocks));
-  d.ksplit = (int)ceil_div(nk, ceil_div(nk, want));
+  // ~3e-5 relative at K = 4096, ~1e-4 at 20000, ~3e-4 at 60000).  The GEMM therefore
+  // accumulates K in chunks of kX3ChunkBlocks 64-wide blocks, each in a fresh TMEM
+  // accumulator, and sums the chunks in fp32 registers (round-to-nearest) in its
+  // epilogue (TcGemm::kchunk): the error stays at the one-chunk level for any K.
+  // Split-K (fp32 partials + a fixed-order reduction) only for tile-starved outputs.
+  d.ksplit = gemm_tc2_ksplit(Mt, N, 3 * d.Kp);
   d.p_ld = round_up(N, 4);
   d.p_stride = round_up((int64_t)Mt * d.p_ld, 64);
   return d;
@@ -113,8 +153,18 @@ void split3(const float* S, int64_t ld, int rows, int cols, bool k_cols, int Kp,
             __nv_bfloat16* D, int64_t dld, cudaStream_t st) {
   const int rows_ext = k_cols ? rows : Kp;
   const int cols_ext = k_cols ? Kp : cols + (ones_col >= 0 ? 1 : 0);
-  const dim3 grid((unsigned)ceil_div(cols_ext, 256), (unsigned)std::min(rows_ext, 65535));
-  split3_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld, rows_ext);
+  // (the image's row padding up to the next multiple of 8 columns is written as zeros)
+  const int cols_v8 = (int)round_up(cols_ext, 8);
+  const bool v8 = cols_v8 <= (k_cols ? Kp : dld) && (ld % 4) == 0 && (dld % 8) == 0 && (Kp % 8) == 0 &&
+                  ((uintptr_t)S & 15) == 0 && ((uintptr_t)D & 15) == 0;
+  if (v8) {
+    const dim3 grid((unsigned)ceil_div(cols_v8, 8 * 128), (unsigned)std::min(rows_ext, 65535));
+    split3_v8_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld, rows_ext,
+                                            cols_v8);
+  } else {
+    const dim3 grid((unsigned)ceil_div(cols_ext, 256), (unsigned)std::min(rows_ext, 65535));
+    split3_kernel<<<grid, 128, 0, st>>>(S, ld, rows, cols, k_cols, Kp, lo_mask, ones_col, D, dld, rows_ext);
+  }
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -160,6 +210,10 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
     b3 = b3w;
   }
   TcGemm g{M + (a_ones ? 1 : 0), N, 3 * d.Kp, a3, d.a_ld, transA, b3, d.b_ld, !transB, C, ldc, 1.f, beta, bias};
+  {  // chunked accumulation only where one work unit's K range is longer than a chunk
+    const int64_t nk = ceil_div(3 * (int64_t)d.Kp, 64);
+    if (ceil_div(nk, d.ksplit) > kX3ChunkBlocks) g.kchunk = kX3ChunkBlocks;
+  }
   if (d.ksplit > 1) {  // small output: split K over the idle SMs, then a fixed-order reduction
     float* part = reinterpret_cast<float*>(after_a + round_up(d.b_rows * d.b_ld * 2, 256));
     g.C = part;
@@ -193,8 +247,8 @@ void gemm_f32x3(bool transA, bool transB, int M, int N, int K, const float* A, i
 
 void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
                    const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
-                   cudaStream_t st) {
-  x3_core(transA, transB, M, N, K, A, lda, nullptr, 0, B3, beta, C, ldc, bias, nullptr, 0, ws, st);
+                   cudaStream_t st, float* ones_row_out, int64_t ld_ones) {
+  x3_core(transA, transB, M, N, K, A, lda, nullptr, 0, B3, beta, C, ldc, bias, ones_row_out, ld_ones, ws, st);
 }
 
 }  // namespace sl

@@ -47,6 +47,7 @@ struct P2 {
   const int32_t* sm_targets;
   int ksplit, kb_per;    // split-K: work unit t -> tile t % tiles, K blocks [z kb_per, (z + 1) kb_per), z = t / tiles
   int64_t split_stride;  // ... written to C + z * split_stride
+  int kchunk;            // CHUNK kernels: K blocks per accumulation chunk
 };
 
 // K-block range of work unit t (split-K; ksplit == 1: the whole K)
@@ -128,7 +129,54 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (g_gemm_trace) g_gemm_trace[(size_t)blockIdx.x * 8 + (i)] = gtimer(); \
   } while (0)
 
-template <bool A_MN, bool B_MN>
+// fp32 output of 32 accumulator columns of one row (alpha, bias, beta; 32 B / 16 B / scalar stores)
+__device__ __forceinline__ void store_row32(const P2& p, float* crow, int col0, const float (&v)[32], bool vec) {
+  if (vec && col0 + 32 <= p.N && p.beta == 0.f && !p.bias && (p.ldc % 8) == 0 && ((uintptr_t)crow & 31) == 0) {
+    // plain fp32 tile (split-K partials, plain outputs): 32 B vector stores — full
+    // sectors and half the store requests of float4 (the epilogue is request-bound)
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      float* dst = crow + col0 + j;
+      asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(p.alpha * v[j]),
+                   "f"(p.alpha * v[j + 1]), "f"(p.alpha * v[j + 2]), "f"(p.alpha * v[j + 3]), "f"(p.alpha * v[j + 4]),
+                   "f"(p.alpha * v[j + 5]), "f"(p.alpha * v[j + 6]), "f"(p.alpha * v[j + 7])
+                   : "memory");
+    }
+  } else if (vec && col0 + 32 <= p.N) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 o = make_float4(p.alpha * v[j], p.alpha * v[j + 1], p.alpha * v[j + 2], p.alpha * v[j + 3]);
+      if (p.bias) {
+        const float4 bb = *reinterpret_cast<const float4*>(p.bias + col0 + j);
+        o.x += bb.x;
+        o.y += bb.y;
+        o.z += bb.z;
+        o.w += bb.w;
+      }
+      float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
+      if (p.beta != 0.f) {
+        const float4 old = *dst;
+        o.x += p.beta * old.x;
+        o.y += p.beta * old.y;
+        o.z += p.beta * old.z;
+        o.w += p.beta * old.w;
+      }
+      *dst = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col0 + j >= p.N) break;
+      float o = p.alpha * v[j];
+      if (p.bias) o += p.bias[col0 + j];
+      float* dst = crow + col0 + j;
+      if (p.beta != 0.f) o += p.beta * *dst;
+      *dst = o;
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN, bool CHUNK>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB, P2 p) {
@@ -201,33 +249,37 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       constexpr uint32_t idesc = tc::make_idesc(BMP, BNP, 1, A_MN, B_MN);
       int st = 0;
       uint32_t ph = 0;
-      int it = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++it) {
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
-        tc::fence_after_sync();
+      int it = 0;  // accumulator uses: one per unit, or (CHUNK) one per K chunk
+      for (int t = pair; t < ntiles; t += npairs) {
         int tile, kb0, kb1, z;
         unit_kb(p, t, tile, kb0, kb1, z);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full_bar[st], ph);
+        const int step = CHUNK ? p.kchunk : (kb1 - kb0);
+        for (int c0 = kb0; c0 < kb1; c0 += step, ++it) {
+          const int c1 = min(kb1, c0 + step);
+          const int acc = it & 1;
+          tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
           tc::fence_after_sync();
-          const uint32_t sa = base + st * kStage, sb = sa + kHalf;
+          for (int kb = c0; kb < c1; ++kb) {
+            tc::mbar_wait(&full_bar[st], ph);
+            tc::fence_after_sync();
+            const uint32_t sa = base + st * kStage, sb = sa + kHalf;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? tc::make_sdesc(sa + k * 2048, 8192, 1024)
-                                     : tc::make_sdesc(sa + k * 32, 0, 1024);
-            const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, 8192, 1024)
-                                     : tc::make_sdesc(sb + k * 32, 0, 1024);
-            mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = A_MN ? tc::make_sdesc(sa + k * 2048, 8192, 1024)
+                                       : tc::make_sdesc(sa + k * 32, 0, 1024);
+              const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, 8192, 1024)
+                                       : tc::make_sdesc(sb + k * 32, 0, 1024);
+              mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb != c0 || k != 0) ? 1u : 0u);
+            }
+            commit_pair(&empty_bar[st]);  // frees the slot in both CTAs
+            if (++st == kStages) {
+              st = 0;
+              ph ^= 1;
+            }
           }
-          commit_pair(&empty_bar[st]);  // frees the slot in both CTAs
-          if (++st == kStages) {
-            st = 0;
-            ph ^= 1;
-          }
+          commit_pair(&tfull_bar[acc]);
+          GT(3);
         }
-        commit_pair(&tfull_bar[acc]);
-        GT(3);
       }
     }
   } else {  // ---------------- epilogue (warps 2..9 -> TMEM lane quarters 2,3,0,1, x2 column halves)
@@ -236,6 +288,46 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const uint32_t tempty_leader[2] = {mapa_u32(tc::smem_u32(&tempty_bar[0]), 0),
                                        mapa_u32(tc::smem_u32(&tempty_bar[1]), 0)};
     int it = 0;
+    if constexpr (CHUNK) {  // ---- chunked accumulation: fp32 C only
+      for (int t = pair; t < ntiles; t += npairs) {
+        int tile, kb0, kb1, z;
+        unit_kb(p, t, tile, kb0, kb1, z);
+        const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP;
+        float sum[128];  // this thread's row x the warp's 128 columns, summed over the chunks in fp32
+#pragma unroll
+        for (int j = 0; j < 128; ++j) sum[j] = 0.f;
+        for (int c0 = kb0; c0 < kb1; c0 += p.kchunk, ++it) {
+          const int acc = it & 1;
+          tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+          tc::fence_after_sync();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float v[32];
+            tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + half * 128 + c * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sum[c * 32 + j] += v[j];
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) arrive_remote(tempty_leader[acc], 32);  // this chunk's accumulator is free again
+        }
+        const int row = m0 + 32 * q + lane;
+        if (row >= p.M) continue;
+        const bool second = row >= p.m_split;
+        float* crow = second ? p.C2 + (int64_t)(row - p.m_split) * p.ldc2
+                             : p.C + z * p.split_stride + (int64_t)row * p.ldc;
+        if (crow == nullptr || (second ? p.C2 : p.C) == nullptr) continue;
+        const bool vec = second ? (p.ldc2 % 4) == 0 && ((uintptr_t)p.C2 & 15) == 0
+                                : (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = sum[c * 32 + j];
+          store_row32(p, crow, n0 + half * 128 + c * 32, v, vec);
+        }
+      }
+    } else
     for (int t = pair; t < ntiles; t += npairs, ++it) {
       const int acc = it & 1;
       int tile, kb0, kb1, z;
@@ -447,9 +539,9 @@ int sms2() {
   return n;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool CHUNK>
 void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream_t s) {
-  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN>;
+  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, CHUNK>;
   static bool configured = false;
   if (!configured) {
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -526,10 +618,19 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   p.sm_targets = g.sm_targets;
   SL_REQUIRE(!g.sm_part || (g.Cb && g.sm_targets), SL_ERR_INVALID_ARGUMENT,
              "gemm: softmax partials need the bf16 output and the targets");
-  if (!g.a_mn && g.b_mn) launch2<false, true>(ta, tb, p, stream);
-  else if (!g.a_mn && !g.b_mn) launch2<false, false>(ta, tb, p, stream);
-  else if (g.a_mn && g.b_mn) launch2<true, true>(ta, tb, p, stream);
-  else launch2<true, false>(ta, tb, p, stream);
+  p.kchunk = g.kchunk;
+  if (g.kchunk > 0) {
+    SL_REQUIRE(!g.Cb && !g.sm_part, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: chunked accumulation writes fp32 C");
+    if (!g.a_mn && g.b_mn) launch2<false, true, true>(ta, tb, p, stream);
+    else if (!g.a_mn && !g.b_mn) launch2<false, false, true>(ta, tb, p, stream);
+    else if (g.a_mn && g.b_mn) launch2<true, true, true>(ta, tb, p, stream);
+    else launch2<true, false, true>(ta, tb, p, stream);
+    return;
+  }
+  if (!g.a_mn && g.b_mn) launch2<false, true, false>(ta, tb, p, stream);
+  else if (!g.a_mn && !g.b_mn) launch2<false, false, false>(ta, tb, p, stream);
+  else if (g.a_mn && g.b_mn) launch2<true, true, false>(ta, tb, p, stream);
+  else launch2<true, false, false>(ta, tb, p, stream);
 }
 
 }  // namespace sl
