@@ -205,7 +205,7 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
       w.hbufb[k] = c.take<__nv_bfloat16>(tc_rec_hbuf_elems(d.B, sh));
     }
   } else if (use_x3(d, prec)) {
-    const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count());
+    const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count(), d.nd);
     w.xw_ld = d.nd * g4(d);
     float* xw = c.take<float>((size_t)d.BT() * w.xw_ld);
     for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * g4(d) : nullptr;
@@ -311,35 +311,42 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     gemm_f32x3(false, false, (int)d.BT(), (int)Gc, d.D, x, d.D, w.wcatf, Gc, 0.f, w.xw[0], Gc, w.bcat, nullptr, 0,
                w.gws, st);
   }
-  const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count());
-  for (int k = 0; k < d.nd; ++k) {
+  const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count(), d.nd);
+  const int per_launch = sh.pair == 2 ? d.nd : 1;  // both directions at once, or one per launch
+  SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
+  for (int k0 = 0; k0 < d.nd; k0 += per_launch) {
     TcRecFwdArgs a{};
     a.B = d.B;
     a.T = d.T;
     a.H = d.H;
-    a.nd = 1;
-    a.dir0 = k;
-    a.dirsign[0] = dir_sign(L, k);
+    a.nd = per_launch;
+    a.dir0 = sh.pair == 2 ? 0 : k0;
     a.lens = lens;
-    a.xwf[0] = w.xw[k];
     a.xw_ld = Gc;
     a.y = y;
     a.y_ld = (int64_t)d.nd * d.H;
     a.h_last = h_last;
     a.c_last = c_last;
-    a.gatesf[0] = rv.gates[k];
-    a.cprevf[0] = rv.cprev[k];
-    a.hprevf[0] = rv.hprev[k];
     a.hprev_ld = d.H;
-    a.hbuf[0] = w.hbufb[k];
-    a.hbuf_lo[0] = w.hbuflo[k];
     a.bar = w.bar;
-    tc_rec_x3_pack(R[k], d.H, sh, w.rtx3[k], st);
-    SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
-    SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
-    SL_CUDA_TRY(cudaMemsetAsync(w.hbuflo[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
-    Phase ph(st, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H);
-    rec_fwd_pair_x3(a, sh, w.rtx3[k], st);
+    const __nv_bfloat16* rt[2] = {nullptr, nullptr};
+    for (int j = 0; j < per_launch; ++j) {
+      const int k = k0 + j;
+      a.dirsign[j] = dir_sign(L, k);
+      a.xwf[j] = w.xw[k];
+      a.gatesf[j] = rv.gates[k];
+      a.cprevf[j] = rv.cprev[k];
+      a.hprevf[j] = rv.hprev[k];
+      a.hbuf[j] = w.hbufb[k];
+      a.hbuf_lo[j] = w.hbuflo[k];
+      tc_rec_x3_pack(R[k], d.H, sh, w.rtx3[k], st);
+      rt[j] = w.rtx3[k];
+      SL_CUDA_TRY(cudaMemsetAsync(w.hbufb[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
+      SL_CUDA_TRY(cudaMemsetAsync(w.hbuflo[k], 0, sizeof(__nv_bfloat16) * tc_rec_hbuf_elems(d.B, sh), st));
+    }
+    if (k0 > 0) SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
+    Phase ph(st, "k2_rec_fwd", 2.0 * d.BT() * d.H * 4.0 * d.H * per_launch);
+    rec_fwd_pair_x3(a, sh, rt, st);
   }
 }
 

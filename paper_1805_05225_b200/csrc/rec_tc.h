@@ -154,9 +154,13 @@ void rec_fwd_pair(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* co
 // lo bf16 rings, z = h_hi R_hi + h_lo R_hi + h_hi R_lo accumulated in fp32
 // TMEM; fp32 x W, cell state, saves and outputs.  One direction per launch
 // (both directions' hi+lo R do not fit in shared memory at once).
-TcFwdShape tc_rec_fwd_x3_shape(int H, int sms);  // C == 0: unsupported
+// nd == 2 and the grid fits: both directions in ONE launch (shape.pair == 2: 32 units
+// per pair, R_hi resident, R_lo streamed through the ring with h); otherwise one
+// direction per launch (shape.pair == 1: 16 units per pair, R hi + lo resident).
+TcFwdShape tc_rec_fwd_x3_shape(int H, int sms, int nd = 1);  // C == 0: unsupported
 size_t tc_rec_x3_pack_elems(const TcFwdShape& sh);   // one direction's packed R^T (hi rows, then lo rows)
 void tc_rec_x3_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT, cudaStream_t stream);
-void rec_fwd_pair_x3(const TcRecFwdArgs& a, const TcFwdShape& sh, const __nv_bfloat16* RT, cudaStream_t stream);
+void rec_fwd_pair_x3(const TcRecFwdArgs& a, const TcFwdShape& sh, const __nv_bfloat16* const* RT,
+                     cudaStream_t stream);
 
 }  // namespace sl

@@ -46,26 +46,39 @@ namespace sl {
 namespace {
 using namespace rtc;
 
-template <bool X3>
+// kBF16: bf16 path; kX3: fp32-class, one direction per launch, R hi + lo resident;
+// kX3C: fp32-class, both directions concurrently, R_hi resident and R_lo streamed
+// through the ring with h (a stage = [h_hi | h_lo | R_lo] of one K chunk)
+enum Mode { kBF16 = 0, kX3 = 1, kX3C = 2 };
+template <int M>
 struct PairCfg {
-  static constexpr int kPU = X3 ? 16 : 32;   // hidden units per pair
-  static constexpr int kN = 4 * kPU;         // MMA N (both CTAs' R slices)
-  static constexpr int kNHalf = kN / 2;      // R^T rows held per CTA (per precision part)
-  static constexpr int kParts = X3 ? 2 : 1;  // hi (+ lo) copies of R and h
+  static constexpr bool X3 = M != kBF16;
+  static constexpr int kPU = M == kX3 ? 16 : 32;           // hidden units per pair
+  static constexpr int kN = 4 * kPU;                       // MMA N (both CTAs' R slices)
+  static constexpr int kNHalf = kN / 2;                    // R^T rows held per CTA (per precision part)
+  static constexpr int kRParts = M == kX3 ? 2 : 1;         // resident R copies (hi, + lo)
+  static constexpr int kHParts = X3 ? 2 : 1;               // h copies per stage (hi, + lo)
+  static constexpr uint32_t kRloBytes = M == kX3C ? kNHalf * 128 : 0;  // streamed R_lo per 64-K chunk
+  static constexpr int kSplit = M == kX3C ? 4 : 2;         // epilogue threads per batch row
+  static constexpr int kEpi = 128 * kSplit;                // epilogue threads
+  static constexpr int kThreads = 64 + kEpi;
+  static constexpr int kUT = kPU / kSplit;                 // units per epilogue thread
 };
-constexpr int kSplit = 2;                   // epilogue threads per batch row
-constexpr int kEpi = 128 * kSplit;          // epilogue threads
-constexpr int kThreads = 64 + kEpi;
 constexpr int kMaxStages = 8;
 constexpr uint32_t kChunk = 128 * 64 * 2;   // 128 rows x 64 K bf16
 constexpr uint32_t kXwGate = 128 * 32 * 2;  // x W tile of one gate: 128 rows x 32 units bf16
 constexpr uint32_t kSmemMax = 227 * 1024;
 constexpr int kGrpCtrs = 32;                // step counters per (direction, batch tile): one per K group
 
-template <bool X3>
+template <int M>
+__host__ __device__ inline uint32_t stage_bytes_of(int kb) {
+  using Cfg = PairCfg<M>;
+  return (uint32_t)(Cfg::kHParts * kChunk + Cfg::kRloBytes) * kb;
+}
+template <int M>
 uint32_t pair_smem(int Kp, int stages, int kb) {
-  using Cfg = PairCfg<X3>;
-  return (uint32_t)Cfg::kParts * Cfg::kNHalf * Kp * 2 + stages * Cfg::kParts * kChunk * kb + 1024;
+  using Cfg = PairCfg<M>;
+  return (uint32_t)Cfg::kRParts * Cfg::kNHalf * Kp * 2 + stages * stage_bytes_of<M>(kb) + 1024;
 }
 
 #ifdef SL_EXPERIMENTS
@@ -81,15 +94,16 @@ uint32_t pair_smem(int Kp, int stages, int kb) {
 
 __device__ __forceinline__ float sig_precise(float z) { return 1.0f / (1.0f + expf(-z)); }
 
-template <bool X3>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MODE>
+__global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
     rec_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmR0, const __grid_constant__ CUtensorMap tmR1,
                         const __grid_constant__ CUtensorMap tmH0, const __grid_constant__ CUtensorMap tmH1,
                         const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                         TcRecFwdArgs a) {
-  using Cfg = PairCfg<X3>;
+  using Cfg = PairCfg<MODE>;
+  constexpr bool X3 = Cfg::X3;
   constexpr int kPU = Cfg::kPU, kN = Cfg::kN, kNHalf = Cfg::kNHalf;
-  constexpr int kUT = kPU / kSplit;  // units per epilogue thread
+  constexpr int kUT = Cfg::kUT, kEpi = Cfg::kEpi;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t r_bar, tfull_bar, tempty_bar;
@@ -111,11 +125,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
   const int nkc = a.Kp / 64;
-  const uint32_t r_bytes = (uint32_t)Cfg::kParts * kNHalf * a.Kp * 2;
+  const uint32_t r_bytes = (uint32_t)Cfg::kRParts * kNHalf * a.Kp * 2;
   uint8_t* sR = smem;
   uint8_t* sH = smem + r_bytes;
-  const uint32_t part_bytes = kChunk * a.kb;             // one precision part of a stage
-  const uint32_t stage_bytes = part_bytes * Cfg::kParts;
+  const uint32_t part_bytes = kChunk * a.kb;             // one precision part of h in a stage
+  const uint32_t stage_bytes = stage_bytes_of<MODE>(a.kb);
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) tc::mbar_arrive_expect_tx(&r_bar, 2 * r_bytes);
       for (int kc = 0; kc < nkc; ++kc) {
         tma_load_2d_pair(sR + (size_t)kc * kNHalf * 128, tmR, r_bar_l, kc * 64, pair * kN + r * kNHalf);
-        if constexpr (X3)  // the lo rows follow the P * kN hi rows
+        if constexpr (MODE == kX3)  // the lo rows follow the P * kN hi rows
           tma_load_2d_pair(sR + (size_t)(nkc + kc) * kNHalf * 128, tmR, r_bar_l, kc * 64,
                            a.P * kN + pair * kN + r * kNHalf);
       }
@@ -225,6 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
             const uint32_t fb = mapa(tc::smem_u32(&full_bar[st]), 0);
+            if constexpr (MODE == kX3C)  // this group's R_lo chunks (no dependency on the step)
+              for (int j = 0; j < a.kb; ++j)
+                tma_load_2d_pair(sH + st * stage_bytes + 2 * part_bytes + j * Cfg::kRloBytes, tmR, fb,
+                                 (kg * a.kb + j) * 64, a.P * kN + pair * kN + r * kNHalf);
             tma_load_4d_pair(sH + st * stage_bytes, tmH, fb, 0, (a.b0 + r * 128) / 8, kg * a.kb * 8, s & 1);
             if constexpr (X3)
               tma_load_4d_pair(sH + st * stage_bytes + part_bytes, tmX, fb, 0, (a.b0 + r * 128) / 8,
@@ -264,7 +282,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_f16_pair(tmem, ah, bh, idesc, (kq | j | k) != 0);
               if constexpr (X3) {
                 const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
-                const uint64_t bl = tc::make_sdesc(sb + (uint32_t)nkc * kNHalf * 128 + k * 32, 0, 1024);
+                const uint32_t sbl = MODE == kX3C
+                                         ? base + r_bytes + st * stage_bytes + 2 * part_bytes + j * Cfg::kRloBytes
+                                         : sb + (uint32_t)nkc * kNHalf * 128;
+                const uint64_t bl = tc::make_sdesc(sbl + k * 32, 0, 1024);
                 mma_f16_pair(tmem, al, bh, idesc, true);  // h_lo R_hi
                 mma_f16_pair(tmem, ah, bl, idesc, true);  // h_hi R_lo
               }
@@ -502,13 +523,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 #undef TR
 
-// RT rows [pair * 64 + g * 16 + j] = column g*H + pair*16 + j of R (the x3 pair
-// kernel's order), lo rows at + P * 64: (R - bf16(R)) rounded to bf16.  One block
+// RT rows [pair * 4UC + g * UC + j] = column g*H + pair*UC + j of R (the x3 pair
+// kernels' order), lo rows at + P * 4UC: (R - bf16(R)) rounded to bf16.  One block
 // per (pair, gate) x 64 k, 16 B stores along k.
-template <bool LO>
+template <int UC, bool LO>
 __global__ void __launch_bounds__(256) pack_rt_x3_kernel(const float* __restrict__ R, int H, int Kp, int P,
                                                          __nv_bfloat16* __restrict__ RT) {
-  constexpr int UC = 16;
   __shared__ float tile[64][UC + 1];
   const int cg = blockIdx.x;  // (pair, gate)
   const int cta = cg / 4, g = cg % 4;
@@ -534,12 +554,12 @@ __global__ void __launch_bounds__(256) pack_rt_x3_kernel(const float* __restrict
   }
 }
 
-template <bool X3>
+template <int MODE>
 void launch_pair(const TcRecFwdArgs& a0, const CUtensorMap* tr, const CUtensorMap* th, const CUtensorMap* tx,
                  cudaStream_t stream) {
   TcRecFwdArgs a = a0;
-  const uint32_t smem = pair_smem<X3>(a.Kp, a.stages, a.kb);
-  auto kern = rec_fwd_pair_kernel<X3>;
+  const uint32_t smem = pair_smem<MODE>(a.Kp, a.stages, a.kb);
+  auto kern = rec_fwd_pair_kernel<MODE>;
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], h0 = th[0], h1 = th[a.nd > 1 ? 1 : 0];
   CUtensorMap x0 = tx[0], x1 = tx[a.nd > 1 ? 1 : 0];
@@ -549,7 +569,7 @@ void launch_pair(const TcRecFwdArgs& a0, const CUtensorMap* tr, const CUtensorMa
     a.bar = bar0 + kBarPerChunk * (b0 / 256);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * a.P * a.nd);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(PairCfg<MODE>::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attrs[2];
@@ -582,14 +602,14 @@ CUtensorMap ring_map(const __nv_bfloat16* ring, int B, int Kp, int kb) {
 }  // namespace
 
 bool tc_rec_fwd_pair_fits(int H, int nd, int sms) {
-  const int P = (int)ceil_div(H, PairCfg<false>::kPU);
+  const int P = (int)ceil_div(H, PairCfg<kBF16>::kPU);
   const int Kp = (int)round_up(H, 64);
-  return (int64_t)2 * P * nd <= sms && pair_smem<false>(Kp, 2, 2) <= kSmemMax;
+  return (int64_t)2 * P * nd <= sms && pair_smem<kBF16>(Kp, 2, 2) <= kSmemMax;
 }
 
 void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                   cudaStream_t stream) {
-  using Cfg = PairCfg<false>;
+  using Cfg = PairCfg<kBF16>;
   TcRecFwdArgs a = a0;
   a.U = Cfg::kPU;
   a.P = sh.P;
@@ -617,57 +637,78 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
   }
   a.stages = 0;
   for (int st = kMaxStages; st >= 2 && !a.stages; --st)
-    if (pair_smem<false>(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
+    if (pair_smem<kBF16>(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_pair: R slice does not fit in shared memory");
   SL_REQUIRE(a.Kp / 64 / a.kb <= kGrpCtrs && 4 * kGrpCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
              "rec_fwd_pair: too many K groups for the step counters");
-  launch_pair<false>(a, tr, th, tx, stream);
+  launch_pair<kBF16>(a, tr, th, tx, stream);
 }
 
-TcFwdShape tc_rec_fwd_x3_shape(int H, int sms) {
-  using Cfg = PairCfg<true>;
+TcFwdShape tc_rec_fwd_x3_shape(int H, int sms, int nd) {
+  if (nd == 2) {  // both directions concurrently (R_lo streamed), when the grid fits
+    using Cc = PairCfg<kX3C>;
+    const int P = (int)ceil_div(H, Cc::kPU);
+    const int Kp = (int)round_up(H, 64);
+    if ((int64_t)4 * P <= sms && pair_smem<kX3C>(Kp, 2, 1) <= kSmemMax && Kp / 64 <= kGrpCtrs) {
+      TcFwdShape sh{1, Cc::kPU, P, Kp};
+      sh.pair = 2;  // kX3C
+      return sh;
+    }
+  }
+  using Cfg = PairCfg<kX3>;
   const int P = (int)ceil_div(H, Cfg::kPU);
   const int Kp = (int)round_up(H, 64);
-  if ((int64_t)2 * P > sms || pair_smem<true>(Kp, 2, 1) > kSmemMax || Kp / 64 > kGrpCtrs)
+  if ((int64_t)2 * P > sms || pair_smem<kX3>(Kp, 2, 1) > kSmemMax || Kp / 64 > kGrpCtrs)
     return TcFwdShape{0, 0, 0, 0};
   TcFwdShape sh{1, Cfg::kPU, P, Kp};
-  sh.pair = 1;
+  sh.pair = 1;  // kX3: one direction per launch
   return sh;
 }
 
-size_t tc_rec_x3_pack_elems(const TcFwdShape& sh) { return (size_t)2 * sh.P * PairCfg<true>::kN * sh.Kp; }
+size_t tc_rec_x3_pack_elems(const TcFwdShape& sh) { return (size_t)2 * sh.P * 4 * sh.U * sh.Kp; }
 
 void tc_rec_x3_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT, cudaStream_t stream) {
   const dim3 grid((unsigned)sh.P * 4, (unsigned)(sh.Kp / 64));
-  pack_rt_x3_kernel<false><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
-  SL_CUDA_TRY(cudaGetLastError());
-  pack_rt_x3_kernel<true><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+  if (sh.U == 32) {
+    pack_rt_x3_kernel<32, false><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+    SL_CUDA_TRY(cudaGetLastError());
+    pack_rt_x3_kernel<32, true><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+  } else {
+    pack_rt_x3_kernel<16, false><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+    SL_CUDA_TRY(cudaGetLastError());
+    pack_rt_x3_kernel<16, true><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+  }
   SL_CUDA_TRY(cudaGetLastError());
   count_launch(2);
 }
 
-void rec_fwd_pair_x3(const TcRecFwdArgs& a0, const TcFwdShape& sh, const __nv_bfloat16* RT,
+// x3: sh.pair == 1 -> one direction (a.nd == 1, RT[0]); sh.pair == 2 -> both (a.nd == 2)
+void rec_fwd_pair_x3(const TcRecFwdArgs& a0, const TcFwdShape& sh, const __nv_bfloat16* const* RT,
                      cudaStream_t stream) {
-  using Cfg = PairCfg<true>;
   TcRecFwdArgs a = a0;
-  SL_REQUIRE(a.nd == 1, SL_ERR_INVALID_ARGUMENT, "rec_fwd_pair_x3: one direction per launch");
-  a.U = Cfg::kPU;
+  const bool conc = sh.pair == 2;
+  SL_REQUIRE(conc ? a.nd == 2 : a.nd == 1, SL_ERR_INVALID_ARGUMENT, "rec_fwd_pair_x3: direction count");
+  a.U = sh.U;
   a.P = sh.P;
   a.Kp = sh.Kp;
   a.kb = 1;
   a.xw_tma = 0;
-  CUtensorMap tr[1], th[1], tl[1];
-  cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)2 * a.P * Cfg::kN};
-  cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
-  cuuint32_t rb[2] = {64, (cuuint32_t)Cfg::kNHalf};
-  tr[0] = tmap(RT, 2, rd, rs, rb);
-  th[0] = ring_map(a.hbuf[0], a.B, a.Kp, a.kb);
-  tl[0] = ring_map(a.hbuf_lo[0], a.B, a.Kp, a.kb);
+  const int kN = 4 * sh.U, kNHalf = kN / 2;
+  CUtensorMap tr[2], th[2], tl[2];
+  for (int k = 0; k < a.nd; ++k) {
+    cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)2 * a.P * kN};
+    cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
+    cuuint32_t rb[2] = {64, (cuuint32_t)kNHalf};
+    tr[k] = tmap(RT[k], 2, rd, rs, rb);
+    th[k] = ring_map(a.hbuf[k], a.B, a.Kp, a.kb);
+    tl[k] = ring_map(a.hbuf_lo[k], a.B, a.Kp, a.kb);
+  }
   a.stages = 0;
   for (int st = kMaxStages; st >= 2 && !a.stages; --st)
-    if (pair_smem<true>(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
+    if ((conc ? pair_smem<kX3C>(a.Kp, st, a.kb) : pair_smem<kX3>(a.Kp, st, a.kb)) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_pair_x3: R slice does not fit in shared memory");
-  launch_pair<true>(a, tr, th, tl, stream);
+  if (conc) launch_pair<kX3C>(a, tr, th, tl, stream);
+  else launch_pair<kX3>(a, tr, th, tl, stream);
 }
 
 }  // namespace sl
