@@ -897,8 +897,8 @@ def result_line(args, r, world, cfg, peaks, precision):
             if not e:
                 continue
             us = e["ms"] / max(e["calls"], 1) * 1e3 / T  # per time step of one launch
-            nd_launch = 1 if x3 == 3 else 2              # x3: one direction per launch
-            wh_bytes = nd_launch * 4 * H * H * 2 * (2 if x3 == 3 else 1)  # bf16 R (x3: hi + lo)
+            nd_launch = 2  # both directions per launch (x3 too: R_hi resident, R_lo streamed from L2)
+            wh_bytes = nd_launch * 4 * H * H * 2  # the resident bf16 R (x3: R_hi; R_lo streams from L2)
             smem_us = wh_bytes / (148 * 128 * f_sm) * 1e6
             tensor_us = x3 * 2.0 * B * 4 * H * H * nd_launch / (peaks.get("bf16_tflops_sustained", 1400.0) * 1e12) * 1e6
             rec[pname] = {"us_per_step": us, "directions_per_launch": nd_launch, "wh_smem_bound_us": smem_us,

@@ -258,7 +258,7 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
       w.rb[k] = c.take<__nv_bfloat16>(tc_rec_bwd_pack_elems(sh));
     }
   } else if (use_x3(d, prec)) {
-    const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count());
+    const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count(), d.nd);
     w.dzf = c.take<float>((size_t)d.BT() * d.nd * g4(d));
     w.wcatf = c.take<float>((size_t)d.D * d.nd * g4(d));
     w.gws = c.take<char>(x3_gemm_ws(d, true));
@@ -358,34 +358,40 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
             const BwdWork& w, cudaStream_t st) {
   const int64_t G = g4(d), Gc = d.nd * G;
   const int M = (int)d.BT();
-  const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count());
-  for (int k = 0; k < d.nd; ++k) {
+  const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count(), d.nd);
+  const int per_launch = sh.pair == 2 ? d.nd : 1;  // both directions at once, or one per launch
+  for (int k0 = 0; k0 < d.nd; k0 += per_launch) {
     TcRecBwdArgs a{};
     a.B = d.B;
     a.T = d.T;
     a.H = d.H;
-    a.nd = 1;
-    a.dir0 = k;
-    a.dirsign[0] = dir_sign(L, k);
+    a.nd = per_launch;
+    a.dir0 = sh.pair == 2 ? 0 : k0;
     a.lens = lens;
     a.dy = dy;
     a.dy_ld = (int64_t)d.nd * d.H;
     a.dh_last = dh_last;
     a.dc_last = dc_last;
-    a.gatesf[0] = rv.gates[k];
-    a.cprevf[0] = rv.cprev[k];
-    a.dzring[0] = w.dzring[k];
-    a.dzring_lo[0] = w.dzringlo[k];
     a.dzcatf = w.dzf;
     a.dzcat_ld = Gc;
     a.dz_dir_off = G;
     a.bar = w.bar;
-    tc_rec_bwd_x3_pack(R[k], d.H, sh, w.rb[k], st);
+    const __nv_bfloat16* rb[2] = {nullptr, nullptr};
+    for (int j = 0; j < per_launch; ++j) {
+      const int k = k0 + j;
+      a.dirsign[j] = dir_sign(L, k);
+      a.gatesf[j] = rv.gates[k];
+      a.cprevf[j] = rv.cprev[k];
+      a.dzring[j] = w.dzring[k];
+      a.dzring_lo[j] = w.dzringlo[k];
+      tc_rec_bwd_x3_pack(R[k], d.H, sh, w.rb[k], st);
+      rb[j] = w.rb[k];
+      SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
+      SL_CUDA_TRY(cudaMemsetAsync(w.dzringlo[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
+    }
     SL_CUDA_TRY(cudaMemsetAsync(w.bar, 0, rec_bar_count(d.B) * sizeof(unsigned), st));
-    SL_CUDA_TRY(cudaMemsetAsync(w.dzring[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
-    SL_CUDA_TRY(cudaMemsetAsync(w.dzringlo[k], 0, sizeof(__nv_bfloat16) * 2 * dz_ring_bp(d.B) * sh.Kz, st));
-    Phase ph(st, "k3_rec_bwd", 2.0 * d.BT() * d.H * 4.0 * d.H);
-    rec_bwd_x3(a, sh, w.rb[k], st);
+    Phase ph(st, "k3_rec_bwd", 2.0 * d.BT() * d.H * 4.0 * d.H * per_launch);
+    rec_bwd_x3(a, sh, rb, st);
   }
   if (dx) {
     for (int k = 0; k < d.nd; ++k)

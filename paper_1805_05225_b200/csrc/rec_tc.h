@@ -125,10 +125,13 @@ void rec_bwd_pair(const TcRecBwdArgs& a, const TcBwdShape& sh, __nv_bfloat16* co
 // and lo bf16 slices, DZ exchanged as hi and lo rings, dh = DZ_hi R_hi^T +
 // DZ_lo R_hi^T + DZ_hi R_lo^T in fp32 TMEM, fp32 partial exchange, saves and DZ.
 // One direction per launch.
-TcBwdShape tc_rec_bwd_x3_shape(int H, int sms);  // C == 0: unsupported
+// nd == 2 and the grid fits: both directions in ONE launch (shape.pair == 2: R_hi
+// resident, R_lo streamed with DZ in 32-K stages); otherwise one direction per
+// launch (shape.pair == 1: R hi + lo resident).
+TcBwdShape tc_rec_bwd_x3_shape(int H, int sms, int nd = 1);  // C == 0: unsupported
 size_t tc_rec_bwd_x3_pack_elems(const TcBwdShape& sh);  // hi rows then lo rows
 void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream);
-void rec_bwd_x3(const TcRecBwdArgs& a, const TcBwdShape& sh, const __nv_bfloat16* RB, cudaStream_t stream);
+void rec_bwd_x3(const TcRecBwdArgs& a, const TcBwdShape& sh, const __nv_bfloat16* const* RB, cudaStream_t stream);
 
 // K-split partition of the forward kernel: clusters of C CTAs, each finalizing
 // U units (the cluster owns C*U units, MMA N = 4*C*U), P CTAs per direction,

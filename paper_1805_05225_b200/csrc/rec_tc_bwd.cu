@@ -40,14 +40,33 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 
 __host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
-// stages of kb 16 KB chunks per precision part (the host passes the stage count
-// in units of two chunks for kb = 1, see launch_bwd)
-uint32_t bwd_smem(int C, int U, int Kc, int stages, bool x3 = false) {
-  const uint32_t parts = x3 ? 2 : 1;
-  // per batch tile: [C-1 slots][128 rows][U] partials from the peers (bf16, x3: fp32)
-  const uint32_t recv = C > 1 ? (uint32_t)2 * (C - 1) * U * 128 * (x3 ? 4 : 2) : 0;
-  return parts * (uint32_t)nb_of(C, U) * Kc * 2 + parts * stages * kTile * 2 + recv + 1024;
+// kBF16: bf16 R / DZ, both directions per launch; kX3: fp32-class, one direction per
+// launch, R hi + lo resident; kX3C: fp32-class, both directions per launch, R_hi
+// resident and R_lo streamed with DZ (a stage = [DZ_hi | DZ_lo | R_lo] of 32 K)
+enum BwdMode { kBF16 = 0, kX3 = 1, kX3C = 2 };
+
+// K elements of the DZ ring a stage carries: 64 * kb, or 32 for kX3C
+__host__ __device__ inline int stage_k(int mode, int kb) { return mode == kX3C ? 32 : 64 * kb; }
+__host__ __device__ inline uint32_t bwd_stage_bytes(int mode, int NB, int kb) {
+  const int kk = stage_k(mode, kb);
+  return (uint32_t)(mode == kBF16 ? 1 : 2) * 128 * kk * 2 + (mode == kX3C ? (uint32_t)NB * kk * 2 : 0u);
 }
+uint32_t bwd_smem_m(int mode, int C, int U, int Kc, int stages, int kb) {
+  const int NB = nb_of(C, U);
+  const uint32_t rparts = mode == kX3 ? 2 : 1;
+  // [C-1 slots][128 rows][U] partials from the peers (bf16, x3: fp32): one buffer per
+  // batch tile, or (kX3C) one buffer the two tiles use in turn
+  const uint32_t recv = C > 1 ? (uint32_t)(mode == kX3C ? 1 : 2) * (C - 1) * U * 128 * (mode == kBF16 ? 2 : 4) : 0;
+  return rparts * (uint32_t)NB * Kc * 2 + (uint32_t)stages * bwd_stage_bytes(mode, NB, kb) + recv + 1024;
+}
+// (bf16 shape probing: two 16 KB chunks per stage unit)
+uint32_t bwd_smem(int C, int U, int Kc, int stages) { return bwd_smem_m(kBF16, C, U, Kc, stages, 2); }
+
+// TMA descriptors of one launch, per direction: R (resident rows; kX3: hi then lo),
+// the DZ ring (hi), the DZ_lo ring (x3), R_lo as 8-K core-matrix boxes (kX3C)
+struct BwdMaps {
+  CUtensorMap R[2], Z[2], Zlo[2], Rlo[2];
+};
 
 // C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
 // U   hidden units each CTA finalizes (the cluster owns C*U units)
@@ -57,15 +76,12 @@ uint32_t bwd_smem(int C, int U, int Kc, int stages, bool x3 = false) {
 // slower: the per-thread math and stores then sit on the critical path.)
 constexpr int bwd_split(int U) { return U >= 8 ? 2 : 1; }
 
-template <int C, int U, int MT, bool X3, int SPLIT = bwd_split(U), int UT = U / SPLIT>
+template <int C, int U, int MT, int MODE, int SPLIT = bwd_split(U), int UT = U / SPLIT>
 __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
-    rec_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmR0,
-                      const __grid_constant__ CUtensorMap tmR1,
-                      const __grid_constant__ CUtensorMap tmZ0,
-                      const __grid_constant__ CUtensorMap tmZ1, TcRecBwdArgs a) {
+    rec_bwd_tc_kernel(const __grid_constant__ BwdMaps mp, TcRecBwdArgs a) {
+  constexpr bool X3 = MODE != kBF16;
   constexpr int NB = nb_of(C, U);  // MMA N: the cluster's units
   constexpr int kEpiTile = 128 * SPLIT;
-  constexpr int kParts = X3 ? 2 : 1;
   using RecvT = typename std::conditional<X3, float, __nv_bfloat16>::type;
   constexpr uint32_t kRecvBytes = (uint32_t)(C - 1) * 128 * U * sizeof(RecvT);  // per tile and use
   constexpr uint32_t kTmemCols = (MT * NB <= 32) ? 32 : (MT * NB <= 64) ? 64 : (MT * NB <= 128) ? 128 : 256;
@@ -82,18 +98,20 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int cl = cta / C;                  // cluster index within the direction
   const int u0 = cl * C * U + r * U;       // first unit this CTA finalizes
   const int Kc = a.Kz / C;
-  // X3: tmZ0 = the hi ring, tmZ1 = the lo ring (one direction per launch)
-  const CUtensorMap* tmR = d == 0 ? &tmR0 : &tmR1;
-  const CUtensorMap* tmZ = (X3 || d == 0) ? &tmZ0 : &tmZ1;
+  const CUtensorMap* tmR = &mp.R[d];
+  const CUtensorMap* tmZ = &mp.Z[d];
+  const CUtensorMap* tmZl = &mp.Zlo[d];
+  const CUtensorMap* tmRl = &mp.Rlo[d];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
   const uint32_t r_part = (uint32_t)NB * Kc * 2;  // one precision part of the R slice
-  const uint32_t r_bytes = r_part * kParts;
+  const uint32_t r_bytes = r_part * (MODE == kX3 ? 2 : 1);
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
-  const uint32_t part_bytes = kTile * a.kb;  // a.kb 64-wide K chunks per TMA box
-  const uint32_t stage_bytes = part_bytes * kParts;
+  const int kst = stage_k(MODE, a.kb);           // DZ columns per stage (= per TMA box)
+  const uint32_t part_bytes = 128u * kst * 2;    // one precision part of DZ in a stage
+  const uint32_t stage_bytes = bwd_stage_bytes(MODE, NB, a.kb);
   // [MT][C-1 slots][128 rows][U] partials from the peers: one buffer per
   // batch tile (a shared buffer would couple the two tiles' recurrences through
   // its free/full handshake) and row-major, so each sender thread writes its
@@ -105,7 +123,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     tmax_sh = 0;
     tc::prefetch_tmap(tmR);
     tc::prefetch_tmap(tmZ);
-    if (X3) tc::prefetch_tmap(&tmZ1);
+    if (X3) tc::prefetch_tmap(tmZl);
+    if (MODE == kX3C) tc::prefetch_tmap(tmRl);
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
@@ -141,7 +160,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   // CTA publishes DZ_s of its units to every box its columns fall in (<= 2 per
   // gate), and a consumer streams each box of its K slice as soon as THAT box's
   // producers (a handful of CTAs) published — not the slowest of all P.
-  const int bw = a.kb * 64;
+  const int bw = kst;
   unsigned* ctr = a.bar + d * 2 * kBoxCtrs;
   const int hq8c = dz_ring_hq(a.H);
   auto box_producers = [&](int gb) -> unsigned {  // CTAs whose DZ columns hit box gb
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     }
     return n;
   };
-  const int ngrp = nkc / a.kb;  // TMA boxes per tile
+  const int ngrp = Kc / kst;  // TMA boxes per tile
   const int kc_off = cta % ngrp;
 
   if (warp == 0) {  // ---------------------------------------------- producer
@@ -164,7 +183,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
       for (int kc = 0; kc < nkc; ++kc) {
         tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
-        if constexpr (X3)  // the lo rows follow the P * NB hi rows
+        if constexpr (MODE == kX3)  // the lo rows follow the P * NB hi rows
           tc::tma_load_2d(sR + r_part + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, a.P * NB + cta * NB);
       }
     }
@@ -208,11 +227,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               tc::fence_proxy_async_global();  // the box's DZ (generic-proxy stores) -> TMA reads
               tc::mbar_wait(&empty_bar[st], ph ^ 1);
               tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
-              tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
-                          (r * (Kc / 64) + kg * a.kb) * 8, slot);
+              const int kcol8 = (r * Kc + kg * kst) / 8;  // the box's first 8-column chunk of the ring
+              if constexpr (MODE == kX3C)  // this box's R_lo rows (no dependency on the step)
+                tma_load_3d(sA + st * stage_bytes + 2 * part_bytes, tmRl, &full_bar[st], 0, a.P * NB + cta * NB,
+                            (kg * kst) / 8);
+              tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8, kcol8, slot);
               if constexpr (X3)
-                tma_load_4d(sA + st * stage_bytes + part_bytes, &tmZ1, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
-                            (r * (Kc / 64) + kg * a.kb) * 8, slot);
+                tma_load_4d(sA + st * stage_bytes + part_bytes, tmZl, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
+                            kcol8, slot);
             }
             if (++st == nst) {
               st = 0;
@@ -238,22 +260,24 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            for (int j = 0; j < a.kb; ++j) {
-              const int kc = kg * a.kb + j;
-              // A: the stage holds [kb * 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk
-              const uint32_t sa = base + r_bytes + st * stage_bytes + j * kTile;
-              const uint32_t sb = base + (uint32_t)kc * NB * 128;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
-                const uint64_t bh = tc::make_sdesc(sb + k * 32, 0, 1024);
-                tc::mma_f16(tmem + mt * NB, ah, bh, idesc, (kq | j | k) != 0);
-                if constexpr (X3) {
-                  const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
-                  const uint64_t bl = tc::make_sdesc(sb + r_part + k * 32, 0, 1024);
-                  tc::mma_f16(tmem + mt * NB, al, bh, idesc, true);  // DZ_lo R_hi^T
-                  tc::mma_f16(tmem + mt * NB, ah, bl, idesc, true);  // DZ_hi R_lo^T
-                }
+            // A: the stage holds [kst / 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk;
+            // B_hi: the resident SW128 K-major R rows (128 B per 64-K chunk row)
+            const uint32_t sa = base + r_bytes + st * stage_bytes;
+            const int k0 = kg * kst;  // first K (gate column) of the box within the slice
+#pragma unroll 1
+            for (int k = 0; k < kst / 16; ++k) {
+              const int kk = k0 + 16 * k;
+              const uint32_t sb = base + (uint32_t)(kk / 64) * NB * 128 + (uint32_t)((kk % 64) / 16) * 32;
+              const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
+              const uint64_t bh = tc::make_sdesc(sb, 0, 1024);
+              tc::mma_f16(tmem + mt * NB, ah, bh, idesc, (kq | k) != 0);
+              if constexpr (X3) {
+                const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
+                // R_lo: resident SW128 (kX3) or the stage's [kst / 8][NB rows][8] core matrices (kX3C)
+                const uint64_t bl = MODE == kX3 ? tc::make_sdesc(sb + r_part, 0, 1024)
+                                                : tc::make_sdesc_noswz(sa + 2 * part_bytes + k * 2 * NB * 16, NB * 16, 128);
+                tc::mma_f16(tmem + mt * NB, al, bh, idesc, true);  // DZ_lo R_hi^T
+                tc::mma_f16(tmem + mt * NB, ah, bl, idesc, true);  // DZ_hi R_lo^T
               }
             }
             tc::mma_commit(&empty_bar[st]);
@@ -276,7 +300,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     const bool valid_row = row < a.B;
     const int len = valid_row ? a.lens[row] : 0;
     const int dir = a.dirsign[d];
-    const int gdir = X3 ? a.dir0 + d : d;  // global direction: dy / DZ columns, final-state rows
+    const int gdir = MODE == kX3 ? a.dir0 + d : d;  // global direction: dy / DZ columns, final-state rows
     const int H = a.H, T = a.T;
     const int lo = half * UT;
     const int ut0 = u0 + lo;
@@ -289,7 +313,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 
     for (int it = 0; it < Tmax; ++it) {
       const int s = Tmax - 1 - it;  // processing step
-      const int use = it;  // this tile's exchange buffer is used once per step
+      // uses of the exchange buffer: once per step per tile, or (kX3C: one buffer for both
+      // tiles) MT it + mt — the senders of a use wait until the receiver consumed the
+      // previous one (at most one use ahead: a sender's MMA input needed the receiver's
+      // publish of the previous step, which follows its consumption)
+      constexpr bool kShared = MODE == kX3C;
+      const int use = kShared ? MT * it + mt : it;
+      const int fb = kShared ? 0 : mt;             // free-barrier set
+      const size_t rtile = kShared ? 0 : (size_t)mt;  // receive-buffer tile
       const bool active = valid_row && s < len;
       const int t = active ? src_time(s, len, dir) : s;
       const size_t pos = (size_t)row * T + t;
@@ -320,14 +351,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         for (int pi = 1; pi < C; ++pi) {
           const int p = (r + pi) % C;
           if (use > 0) {  // one cluster-scope acquire per warp, then warp-ordered
-            if (lane == 0) mbar_wait_cluster(&free_bar[mt][p], (use - 1) & 1);
+            if (lane == 0) mbar_wait_cluster(&free_bar[fb][p], (use - 1) & 1);
             __syncwarp();
           }
           float v[UT];
           tmem_ld_cols<UT>(tbase + p * U + lo, v);
           const int slot_at_p = (r - p + C) % C - 1;  // my slot in p's buffer
           const uint32_t dst = mapa(
-              tc::smem_u32(recv + (((size_t)mt * (C - 1) + slot_at_p) * 128 + rl) * U + lo), p);
+              tc::smem_u32(recv + ((rtile * (C - 1) + slot_at_p) * 128 + rl) * U + lo), p);
           const uint32_t rbar = mapa(tc::smem_u32(&recv_full[mt]), p);
           static_assert(UT % 4 == 0, "DSMEM partial sends move 4 or 8 values per store");
           // st.async: each store completes its bytes on p's receive barrier, so
@@ -360,12 +391,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
       if constexpr (C > 1) {
-        mbar_wait_cluster(&recv_full[mt], use & 1);
+        mbar_wait_cluster(&recv_full[mt], it & 1);
         if ((e % (4 * SPLIT)) == 0 && lane == 0)  // phase `use` is complete: arm the next use
           tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
 #pragma unroll 1
         for (int sl = 0; sl < C - 1; ++sl) {
-          const RecvT* src = recv + (((size_t)mt * (C - 1) + sl) * 128 + rl) * U + lo;
+          const RecvT* src = recv + ((rtile * (C - 1) + sl) * 128 + rl) * U + lo;
           if constexpr (X3) {
 #pragma unroll
             for (int u = 0; u < UT; u += 4) {
@@ -492,7 +523,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         }
         if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
           for (int pi = 1; pi < C; ++pi)
-            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), kEpiTile);
+            mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[MODE == kX3C ? 0 : mt][r]), (r + pi) % C),
+                                       kEpiTile);
       }
       if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
         if constexpr (X3) {
@@ -578,17 +610,14 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   }
 }
 
-template <int C, int U, int MT, bool X3>
-void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs& a,
-                cudaStream_t stream) {
-  auto kern = rec_bwd_tc_kernel<C, U, MT, X3>;
-  const uint32_t smem = bwd_smem(C, U, a.Kz / C, a.kb == 2 ? a.stages : (a.stages + 1) / 2, X3);
+template <int C, int U, int MT, int MODE>
+void launch_bwd(const BwdMaps& mp, const TcRecBwdArgs& a, cudaStream_t stream) {
+  auto kern = rec_bwd_tc_kernel<C, U, MT, MODE>;
+  const uint32_t smem = bwd_smem_m(MODE, C, U, a.Kz / C, a.stages, a.kb);
   SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   if (C > 1)
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   TcRecBwdArgs copy = a;
-  // X3 (one direction): tz[0] = the hi ring, tz[1] = the lo ring
-  CUtensorMap r0 = tr[0], r1 = tr[a.nd > 1 ? 1 : 0], z0 = tz[0], z1 = tz[(X3 || a.nd > 1) ? 1 : 0];
   constexpr int kSplit = bwd_split(U);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.P * a.nd);
@@ -611,27 +640,26 @@ void launch_bwd(const CUtensorMap* tr, const CUtensorMap* tz, const TcRecBwdArgs
     cfg.attrs = attrs + 1;
     cfg.numAttrs = 1;
   }
-  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, r0, r1, z0, z1, copy));
+  SL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mp, copy));
   count_launch();
 }
 
 // the DZ ring in its interleaved layout, as {8 rows x 8 k (128 contiguous B),
-// 8-row groups, K-chunks, slot}: 128 B TMA rows, box = 128 rows x kb*64 K
-CUtensorMap dz_ring_map(const __nv_bfloat16* ring, int B, int Kz, int kb) {
+// 8-row groups, K-chunks of 8, slot}: 128 B TMA rows, box = 128 rows x kk K
+CUtensorMap dz_ring_map(const __nv_bfloat16* ring, int B, int Kz, int kk) {
   const int Bp = dz_ring_bp(B);
   cuuint64_t zd[4] = {64, (cuuint64_t)Bp / 8, (cuuint64_t)Kz / 8, 2};
   cuuint64_t zs[3] = {128, (cuuint64_t)Bp * 16, (cuuint64_t)Kz / 8 * Bp * 16};
-  cuuint32_t zb[4] = {64, 16, (cuuint32_t)kb * 8, 1};
+  cuuint32_t zb[4] = {64, 16, (cuuint32_t)kk / 8, 1};
   return tmap(ring, 4, zd, zs, zb, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-template <bool X3>
-void dispatch_bwd(const TcBwdShape& sh, int MT, const CUtensorMap* tr, const CUtensorMap* tz,
-                  const TcRecBwdArgs& a, cudaStream_t stream) {
+template <int MODE>
+void dispatch_bwd(const TcBwdShape& sh, int MT, const BwdMaps& mp, const TcRecBwdArgs& a, cudaStream_t stream) {
   const int key = sh.C * 1000 + sh.U * 10 + MT;
   switch (key) {
 #define SL_BWD_CASE(C_, U_, MT_) \
-  case C_ * 1000 + U_ * 10 + MT_: launch_bwd<C_, U_, MT_, X3>(tr, tz, a, stream); break;
+  case C_ * 1000 + U_ * 10 + MT_: launch_bwd<C_, U_, MT_, MODE>(mp, a, stream); break;
     SL_BWD_CASE(4, 4, 1) SL_BWD_CASE(4, 4, 2) SL_BWD_CASE(4, 8, 1) SL_BWD_CASE(4, 8, 2)
     SL_BWD_CASE(4, 16, 1) SL_BWD_CASE(4, 16, 2) SL_BWD_CASE(2, 4, 1) SL_BWD_CASE(2, 4, 2)
     SL_BWD_CASE(2, 8, 1) SL_BWD_CASE(2, 8, 2) SL_BWD_CASE(2, 16, 1) SL_BWD_CASE(2, 16, 2)
@@ -642,10 +670,10 @@ void dispatch_bwd(const TcBwdShape& sh, int MT, const CUtensorMap* tr, const CUt
   }
 }
 
-int pick_stages(const TcBwdShape& sh, int kb, bool x3) {
+int pick_stages(int mode, const TcBwdShape& sh, int kb) {
   const int Kc = sh.Kz / sh.C;
   for (int st = kStages; st >= 2; --st)
-    if (bwd_smem(sh.C, sh.U, Kc, kb == 2 ? st : (st + 1) / 2, x3) <= kSmemMax) return st;
+    if (bwd_smem_m(mode, sh.C, sh.U, Kc, st, kb) <= kSmemMax) return st;
   return 0;
 }
 
@@ -698,16 +726,16 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   a.Kz = sh.Kz;
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  CUtensorMap tr[2], tz[2];
+  BwdMaps mp{};
   a.kb = (Kc / 64) % 2 == 0 ? 2 : 1;
   for (int k = 0; k < a.nd; ++k) {
     cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)a.P * NB};
     cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
-    tr[k] = tmap(RB[k], 2, rd, rs, rb);
-    tz[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, a.kb);
+    mp.R[k] = tmap(RB[k], 2, rd, rs, rb);
+    mp.Z[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, stage_k(kBF16, a.kb));
   }
-  a.stages = pick_stages(sh, a.kb, false);
+  a.stages = pick_stages(kBF16, sh, a.kb);
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");
   SL_REQUIRE(a.Kz / (a.kb * 64) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
              "rec_bwd_tc: too many DZ boxes for the step counters");
@@ -715,19 +743,29 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
     a.bar = bar0 + kBarPerChunk * (b0 / 256);
-    dispatch_bwd<false>(sh, (a.B - b0) > 128 ? 2 : 1, tr, tz, a, stream);
+    dispatch_bwd<kBF16>(sh, (a.B - b0) > 128 ? 2 : 1, mp, a, stream);
   }
 }
 
-TcBwdShape tc_rec_bwd_x3_shape(int H, int sms) {
-  for (int C : {4, 2, 1}) {
+TcBwdShape tc_rec_bwd_x3_shape(int H, int sms, int nd) {
+  if (nd == 2) {  // kX3C: both directions per launch, R_hi resident, R_lo streamed (4-CTA clusters)
+    const int C = 4, U = 16;
+    const int P = (int)ceil_div(H, (int64_t)C * U) * C;
+    const int Kz = (int)round_up(4 * (int64_t)dz_ring_hq(H), 64 * C);
+    TcBwdShape sh{C, U, P, Kz};
+    sh.pair = 2;
+    if ((int64_t)2 * P <= std::min(sms, 128) && Kz / stage_k(kX3C, 1) <= kBoxCtrs && pick_stages(kX3C, sh, 1) >= 2)
+      return sh;
+  }
+  for (int C : {4, 2, 1}) {  // kX3: one direction per launch
     const int usable = C == 4 ? std::min(sms, 128) : sms;
     for (int U : {8, 4, 16}) {
       const int P = (int)ceil_div(H, (int64_t)C * U) * C;
       const int Kz = (int)round_up(4 * (int64_t)dz_ring_hq(H), 64 * C);
-      if (P <= usable && Kz / 64 <= kBoxCtrs) {  // kb = 1 (rec_bwd_x3)
+      if (P <= usable && Kz / 64 <= kBoxCtrs) {  // kb = 1
         TcBwdShape sh{C, U, P, Kz};
-        if (pick_stages(sh, 1, true) >= 2) return sh;
+        sh.pair = 1;
+        if (pick_stages(kX3, sh, 1) >= 2) return sh;
       }
     }
   }
@@ -748,31 +786,42 @@ void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat
   count_launch(2);
 }
 
-void rec_bwd_x3(const TcRecBwdArgs& a0, const TcBwdShape& sh, const __nv_bfloat16* RB, cudaStream_t stream) {
+// sh.pair == 2 (kX3C): a.nd == 2, both directions; sh.pair == 1 (kX3): a.nd == 1
+void rec_bwd_x3(const TcRecBwdArgs& a0, const TcBwdShape& sh, const __nv_bfloat16* const* RB, cudaStream_t stream) {
   TcRecBwdArgs a = a0;
-  SL_REQUIRE(a.nd == 1, SL_ERR_INVALID_ARGUMENT, "rec_bwd_x3: one direction per launch");
+  const int mode = sh.pair == 2 ? kX3C : kX3;
+  SL_REQUIRE(mode == kX3C ? a.nd == 2 : a.nd == 1, SL_ERR_INVALID_ARGUMENT, "rec_bwd_x3: direction count");
   a.U = sh.U;
   a.P = sh.P;
   a.Kz = sh.Kz;
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  a.kb = 1;  // hi + lo parts of a stage: one 64-wide chunk each keeps >= 2 stages in shared memory
-  CUtensorMap tr[1], tz[2];
-  cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)2 * a.P * NB};
-  cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
-  cuuint32_t rb[2] = {64, (cuuint32_t)NB};
-  tr[0] = tmap(RB, 2, rd, rs, rb);
-  tz[0] = dz_ring_map(a.dzring[0], a.B, a.Kz, a.kb);
-  tz[1] = dz_ring_map(a.dzring_lo[0], a.B, a.Kz, a.kb);
-  a.stages = pick_stages(sh, a.kb, true);
+  a.kb = 1;
+  BwdMaps mp{};
+  for (int k = 0; k < a.nd; ++k) {
+    cuuint64_t rd[2] = {(cuuint64_t)Kc, (cuuint64_t)2 * a.P * NB};
+    cuuint64_t rs[1] = {(cuuint64_t)Kc * 2};
+    cuuint32_t rb[2] = {64, (cuuint32_t)NB};
+    mp.R[k] = tmap(RB[k], 2, rd, rs, rb);
+    mp.Z[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, stage_k(mode, 1));
+    mp.Zlo[k] = dz_ring_map(a.dzring_lo[k], a.B, a.Kz, stage_k(mode, 1));
+    if (mode == kX3C) {  // R_lo rows as {8 k, rows, K chunks of 8}: a box lands as [kk / 8][NB rows][8]
+      cuuint64_t ld[3] = {8, (cuuint64_t)2 * a.P * NB, (cuuint64_t)Kc / 8};
+      cuuint64_t ls[2] = {(cuuint64_t)Kc * 2, 16};
+      cuuint32_t lb[3] = {8, (cuuint32_t)NB, (cuuint32_t)stage_k(kX3C, 1) / 8};
+      mp.Rlo[k] = tmap(RB[k], 3, ld, ls, lb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
+  }
+  a.stages = pick_stages(mode, sh, a.kb);
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_x3: R slice does not fit in shared memory");
-  SL_REQUIRE(a.Kz / (a.kb * 64) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
+  SL_REQUIRE(a.Kz / stage_k(mode, 1) <= kBoxCtrs && 4 * kBoxCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
              "rec_bwd_x3: too many DZ boxes for the step counters");
   unsigned* bar0 = a.bar;
   for (int b0 = 0; b0 < a.B; b0 += 256) {
     a.b0 = b0;
     a.bar = bar0 + kBarPerChunk * (b0 / 256);
-    dispatch_bwd<true>(sh, (a.B - b0) > 128 ? 2 : 1, tr, tz, a, stream);
+    if (mode == kX3C) dispatch_bwd<kX3C>(sh, (a.B - b0) > 128 ? 2 : 1, mp, a, stream);
+    else dispatch_bwd<kX3>(sh, (a.B - b0) > 128 ? 2 : 1, mp, a, stream);
   }
 }
 
