@@ -292,12 +292,14 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_da_kernel(AttnArgs p, fl
     for (int j = 0; j < kJC; ++j) {
       if (j < n) {
         const size_t off = ((size_t)b * Ts + j0 + j) * E + x;
-        Vec<VE> o;
-        if (p.accumulate) o.load_plain(p.d_enc + off);
-        else o.zero();
+        if (!p.defer) {
+          Vec<VE> o;
+          if (p.accumulate) o.load_plain(p.d_enc + off);
+          else o.zero();
 #pragma unroll
-        for (int w = 0; w < VE; ++w) o.f[w] += aj[j] * g.f[w];
-        o.store(p.d_enc + off);
+          for (int w = 0; w < VE; ++w) o.f[w] += aj[j] * g.f[w];
+          o.store(p.d_enc + off);
+        }
         if (j0 + j < len) {
           Vec<VE> q;
           q.load(p.enc + off);
@@ -335,9 +337,10 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, co
       const float d = (lane < n && jj < len) ? a_b[jj] * (da_b[jj] + (up_b ? up_b[jj] : 0.f) - dot) : 0.f;
       de_sh[lane] = d;
       dbv = d;
+      if (p.de_out && lane < n) p.de_out[(size_t)b * Ts + jj] = d;
     }
     dbv = warp_sum(dbv);
-    if (lane == 0 && dbv != 0.f) atomicAdd(p.d_b_v, dbv);
+    if (lane == 0 && dbv != 0.f && !p.defer) atomicAdd(p.d_b_v, dbv);
   }
   __syncthreads();
   float part[kJE], de[kJE], acc[kJE];
@@ -374,20 +377,24 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, co
         } else {
           gk.zero();
         }
-        if (p.accumulate) {
-          Vec<VK> o;
-          o.load_plain(p.d_enc_ctx + off);
+        if (!p.defer) {
+          if (p.accumulate) {
+            Vec<VK> o;
+            o.load_plain(p.d_enc_ctx + off);
 #pragma unroll
-          for (int i = 0; i < VK; ++i) gk.f[i] += o.f[i];
+            for (int i = 0; i < VK; ++i) gk.f[i] += o.f[i];
+          }
+          gk.store(p.d_enc_ctx + off);
         }
-        gk.store(p.d_enc_ctx + off);
       }
     }
     if (nv > 0) {
       ds.atomic_add(p.d_s_tr + (size_t)b * K + k);
-      ds.atomic_add(p.d_b_fb + k);
-      dwf.atomic_add(p.d_W_fb + k);
-      dv.atomic_add(p.d_v + k);
+      if (!p.defer) {
+        ds.atomic_add(p.d_b_fb + k);
+        dwf.atomic_add(p.d_W_fb + k);
+        dv.atomic_add(p.d_v + k);
+      }
     }
   }
   block_reduce_chunk(part, n, red, sum_sh);
@@ -463,14 +470,14 @@ void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_
 
 void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, float* d_s, float* d_W_s,
                    float* d_b_s, void* ws, cudaStream_t st) {
-  p.d_s_tr = static_cast<float*>(ws) + (size_t)p.B * p.K;
+  p.d_s_tr = p.d_s_tr_out ? p.d_s_tr_out : static_cast<float*>(ws) + (size_t)p.B * p.K;
   if (p.s_tr_in) {  // the forward's s_tr
     p.s_tr = const_cast<float*>(p.s_tr_in);
   } else {  // recompute s_tr
     p.s_tr = static_cast<float*>(ws);
     gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
   }
-  if (!p.accumulate) {
+  if (!p.accumulate && !p.defer) {
     SL_CUDA_TRY(cudaMemsetAsync(p.d_W_fb, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_b_fb, 0, sizeof(float) * p.K, st));
     SL_CUDA_TRY(cudaMemsetAsync(p.d_v, 0, sizeof(float) * p.K, st));

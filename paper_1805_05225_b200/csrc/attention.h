@@ -40,6 +40,13 @@ struct AttnArgs {
   const __nv_bfloat16* W_s3_bwd;
   float* s_tr_out;
   const float* s_tr_in;
+  // optional (the decoder's loop): defer every accumulation over the steps — the
+  // backward then writes only d s (via d s_tr, to d_s_tr_out when set), d accum and
+  // the softmax adjoint de [B, Ts] (to de_out); d enc, d enc_ctx, d W_fb, d b_fb,
+  // d v and d b_v are left to the caller (decoder_f32.cu sums them after the loop)
+  int defer;
+  float* d_s_tr_out;
+  float* de_out;
 };
 
 size_t attention_workspace_bytes(int B, int K, int H, int Ts);

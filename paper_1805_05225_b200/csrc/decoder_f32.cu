@@ -33,11 +33,15 @@
 namespace sl {
 namespace {
 
+constexpr int kEncPos = 16;   // positions per thread in the d enc accumulation
+constexpr int kCtxPos = 8;    // positions per thread in the d enc_ctx accumulation
+
 struct FLay {
   int64_t XA, RO;  // row pitches: [att ‖ s] (E + H), readout input [s ‖ trg ‖ att] (H + Emb + E)
   float *xw, *xa, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all, *z;
-  float *dro, *dpre, *dz, *dxa, *dc, *ds, *datt, *dacc, *dctx, *dtrg;
+  float *dro, *dpre, *dz, *dxa, *dc, *ds, *dacc, *dctx, *dtrg;
   float* w2;  // [E + H, 4H] staging of [W_att; R]
+  float *datt_all, *de_all, *ds_all, *apart;  // deferred attention accumulations (per step saves)
   int32_t* ids_tm;
   __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
   __nv_bfloat16 *ws_f, *ws_b;    // W_s split for s_tr = s W_s and d s = d s_tr W_s^T
@@ -61,7 +65,8 @@ size_t gemm_ws_bytes(const DecDims& d) {
                    gemm_f32x3_workspace_bytes(true, false, Emb, 4 * H, BT, true),    // [d W_trg; d b]
                    gemm_f32x3_workspace_bytes(false, true, BT, Emb, 4 * H, false),   // d trg
                    gemm_f32x3_workspace_bytes(true, false, E, K, BTs, true),         // [d W_ctx; d b_ctx]
-                   gemm_f32x3_workspace_bytes(false, true, BTs, E, K, false)});      // d enc += d enc_ctx W_ctx^T
+                   gemm_f32x3_workspace_bytes(false, true, BTs, E, K, false),        // d enc += d enc_ctx W_ctx^T
+                   gemm_f32x3_workspace_bytes(true, false, H, K, BT, true)});        // [d W_s; d b_s]
 }
 
 FLay flayout(const DecDims& d, void* base) {
@@ -96,11 +101,14 @@ FLay flayout(const DecDims& d, void* base) {
   L.dxa = tf(B * L.XA);
   L.dc = tf(2 * B * H);
   L.ds = tf(B * H);
-  L.datt = tf(B * E);
   L.dacc = tf(2 * B * d.Ts);
   L.dctx = tf(BTs * K);
   L.dtrg = tf(BT * d.Emb);
   L.w2 = tf(L.XA * 4 * H);
+  L.datt_all = tf(T * B * E);
+  L.de_all = tf(T * B * d.Ts);
+  L.ds_all = tf(T * B * K);
+  L.apart = tf(B * ceil_div(d.Ts, kCtxPos) * 3 * K + 64);
   L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
   L.wd2_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)(4 * H), (int)L.XA) * 2));
   L.wd2_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)L.XA, (int)(4 * H)) * 2));
@@ -235,6 +243,116 @@ __global__ void f32_cell_bwd_kernel(CellBF a) {
   dz[3 * H] = d_o * go * (1.f - go);
 }
 
+// d enc[b, s, :] = sum_t a_t[b, s] d att_t[b, :]  (the generic_attention adjoint w.r.t.
+// its base, tape.cpp:1047-1058, accumulated over the steps in t order).  A thread owns 4
+// columns x kEncPos positions; the block stages a_t[b, s0 .. s0 + kEncPos) of every t.
+__global__ void __launch_bounds__(128) f32_enc_grad_kernel(int B, int Ts, int T, int E, const float* __restrict__ a_all,
+                                                         const float* __restrict__ datt_all, float* __restrict__ d_enc) {
+  extern __shared__ float a_sh[];  // [T][kEncPos]
+  const int b = blockIdx.z, s0 = blockIdx.y * kEncPos, e = (blockIdx.x * 128 + threadIdx.x) * 4;
+  for (int i = threadIdx.x; i < T * kEncPos; i += 128) {
+    const int t = i / kEncPos, j = i % kEncPos;
+    a_sh[i] = s0 + j < Ts ? a_all[((int64_t)t * B + b) * Ts + s0 + j] : 0.f;
+  }
+  __syncthreads();
+  if (e >= E) return;
+  float4 acc[kEncPos];
+#pragma unroll
+  for (int j = 0; j < kEncPos; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = 0; t < T; ++t) {
+    const float4 g = *reinterpret_cast<const float4*>(datt_all + ((int64_t)t * B + b) * E + e);
+#pragma unroll
+    for (int j = 0; j < kEncPos; ++j) {
+      const float w = a_sh[t * kEncPos + j];
+      acc[j].x += w * g.x, acc[j].y += w * g.y, acc[j].z += w * g.z, acc[j].w += w * g.w;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kEncPos; ++j)
+    if (s0 + j < Ts) *reinterpret_cast<float4*>(d_enc + ((int64_t)b * Ts + s0 + j) * E + e) = acc[j];
+}
+
+__device__ __forceinline__ float tanh_fast_f(float x) {  // as attention.cu's energies
+  x = fminf(fmaxf(x, -15.f), 15.f);
+  return 1.f - __fdividef(2.f, 1.f + __expf(2.f * x));
+}
+
+// the energy adjoints summed over the steps (tape.cpp:966-978 then the tanh / weight
+// feedback adjoints): d enc_ctx[b, s, k] = sum_t de_t[b, s] v_k (1 - u_t^2) with
+// u_t = tanh(enc_ctx + accum_{t-1} W_fb + b_fb + s_tr_t) recomputed, and this block's
+// partial sums over its positions of d W_fb (accum gk), d b_fb (gk), d v (u de) per k
+// (reduced in a fixed order afterwards).  A thread owns one k x kCtxPos positions.
+__global__ void __launch_bounds__(128) f32_ctx_grad_kernel(int B, int Ts, int T, int K, const float* __restrict__ enc_ctx,
+                                                         const float* __restrict__ acc_all,
+                                                         const float* __restrict__ de_all,
+                                                         const float* __restrict__ str_all, const float* __restrict__ W_fb,
+                                                         const float* __restrict__ b_fb, const float* __restrict__ v,
+                                                         float* __restrict__ d_ctx, float* __restrict__ part) {
+  extern __shared__ float sh[];  // acc [T][kCtxPos], de [T][kCtxPos]
+  float* acc_sh = sh;
+  float* de_sh = sh + T * kCtxPos;
+  const int b = blockIdx.z, sc = blockIdx.y, s0 = sc * kCtxPos, k = blockIdx.x * 128 + threadIdx.x;
+  for (int i = threadIdx.x; i < T * kCtxPos; i += 128) {
+    const int t = i / kCtxPos, j = i % kCtxPos;
+    const bool ok = s0 + j < Ts;
+    acc_sh[i] = ok ? acc_all[((int64_t)t * B + b) * Ts + s0 + j] : 0.f;  // accum_{t-1} (block t)
+    de_sh[i] = ok ? de_all[((int64_t)t * B + b) * Ts + s0 + j] : 0.f;
+  }
+  __syncthreads();
+  if (k >= K) return;
+  float x[kCtxPos], g[kCtxPos];
+#pragma unroll
+  for (int j = 0; j < kCtxPos; ++j) {
+    x[j] = s0 + j < Ts ? enc_ctx[((int64_t)b * Ts + s0 + j) * K + k] : 0.f;
+    g[j] = 0.f;
+  }
+  const float w = W_fb[k], c = b_fb[k], vk = v[k];
+  float dwf = 0.f, dbf = 0.f, dv = 0.f;
+  for (int t = 0; t < T; ++t) {
+    const float str = str_all[((int64_t)t * B + b) * K + k];
+#pragma unroll
+    for (int j = 0; j < kCtxPos; ++j) {
+      const float a = acc_sh[t * kCtxPos + j], de = de_sh[t * kCtxPos + j];
+      const float u = tanh_fast_f(x[j] + a * w + c + str);
+      const float gk = de * vk * (1.f - u * u);
+      g[j] += gk;
+      dwf += a * gk;
+      dbf += gk;
+      dv += u * de;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kCtxPos; ++j)
+    if (s0 + j < Ts) d_ctx[((int64_t)b * Ts + s0 + j) * K + k] = g[j];
+  const int64_t row = (int64_t)b * gridDim.y + sc;
+  part[(row * 3 + 0) * K + k] = dwf;
+  part[(row * 3 + 1) * K + k] = dbf;
+  part[(row * 3 + 2) * K + k] = dv;
+}
+
+// out_q[k] = sum over rows r (ascending) of part[(r * 3 + q) * K + k], q = 0, 1, 2;
+// and (thread 0 of block 0) *dbv = sum of de_all in a fixed order
+__global__ void f32_ctx_reduce_kernel(int rows, int K, const float* __restrict__ part, float* dwf, float* dbf,
+                                      float* dv, const float* __restrict__ de_all, int64_t n_de, float* dbv) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < K) {
+    float a = 0.f, c = 0.f, e = 0.f;
+    for (int r = 0; r < rows; ++r) {
+      a += part[((int64_t)r * 3 + 0) * K + k];
+      c += part[((int64_t)r * 3 + 1) * K + k];
+      e += part[((int64_t)r * 3 + 2) * K + k];
+    }
+    dwf[k] = a, dbf[k] = c, dv[k] = e;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // d b_v: the energies' bias gradient
+    float sum = 0.f;
+    for (int64_t i = threadIdx.x; i < n_de; i += 32) sum += de_all[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (threadIdx.x == 0) *dbv = sum;
+  }
+}
+
 unsigned grid_of(int64_t n) { return (unsigned)ceil_div(n, 256); }
 
 AttnArgs att_args(const DecDims& d, const FLay& L, const DecParams& p, const float* enc, const int32_t* lens,
@@ -265,7 +383,8 @@ size_t decoder_f32_workspace_bytes(const DecDims& d) { return flayout(d, nullptr
 void decoder_f32_check(const DecDims& d) {
   SL_REQUIRE(d.B > 0 && d.Ts > 0 && d.T > 0 && d.Emb > 0 && d.E > 0 && d.H > 0 && d.K > 0 && d.Rd > 0 && d.Vt > 0,
              SL_ERR_SHAPE, "attn_decoder: dimensions must be positive");
-  SL_REQUIRE(d.Ts <= 4096, SL_ERR_UNSUPPORTED, "attn_decoder (fp32): src_time <= 4096");
+  SL_REQUIRE(d.Ts <= 4096 && d.T <= 1024, SL_ERR_UNSUPPORTED, "attn_decoder (fp32): src_time <= 4096, trg_time <= 1024");
+  SL_REQUIRE(d.E % 4 == 0, SL_ERR_UNSUPPORTED, "attn_decoder (fp32): enc_dim must be a multiple of 4");
 }
 
 void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, const int32_t* src_lens,
@@ -355,28 +474,19 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
                L.gws, st);
     gemm_f32x3(true, false, (int)L.RO, Rd, (int)BT, L.ro, L.RO, L.dpre, Rd, 0.f, g.ro_W, Rd, nullptr, g.ro_b, Rd,
                L.gws, st);
-    // the attention adjoint accumulates over t into these
-    SL_CUDA_TRY(cudaMemsetAsync(L.dctx, 0, sizeof(float) * BTs * K, st));
-    SL_CUDA_TRY(cudaMemsetAsync(d_enc, 0, sizeof(float) * BTs * E, st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.fb_W, 0, sizeof(float) * K, st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.fb_b, 0, sizeof(float) * K, st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.e_W, 0, sizeof(float) * K, st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.e_b, 0, sizeof(float), st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.str_W, 0, sizeof(float) * H * K, st));
-    SL_CUDA_TRY(cudaMemsetAsync(g.str_b, 0, sizeof(float) * K, st));
   }
   for (int t = T - 1; t >= 0; --t) {
     const int cur = t & 1, nxt = cur ^ 1;  // ping-pong: d c / d accum of step t in [cur], of t - 1 -> [nxt]
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * (E + H) * 3);
-      GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, L.dxa, L.XA, L.datt, L.ds};
+      GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, L.dxa, L.XA, L.datt_all + (int64_t)t * B * E, L.ds};
       f32_grad_in_kernel<<<grid_of((int64_t)B * (E + H)), 256, 0, st>>>(gi);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
     }
     AttnArgs a = att_args(d, L, p, enc, src_lens, t);
     a.a_saved = L.a_all + (int64_t)t * B * d.Ts;
-    a.d_att = L.datt;
+    a.d_att = L.datt_all + (int64_t)t * B * E;
     a.d_accum_out = t + 1 < T ? L.dacc + (int64_t)cur * B * d.Ts : nullptr;
     a.d_accum = L.dacc + (int64_t)nxt * B * d.Ts;
     a.d_enc_ctx = L.dctx;
@@ -385,10 +495,13 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     a.d_b_fb = g.fb_b;
     a.d_v = g.e_W;
     a.d_b_v = g.e_b;
-    a.accumulate = 1;  // every accumulator was zeroed above; d accum_{t-1} is zeroed per step
+    a.accumulate = 1;  // d s accumulates onto the readout / next-step part; d accum_{t-1} zeroed per step
     a.s_tr_in = L.str_all + (int64_t)t * B * K;
+    a.defer = 1;  // d enc, d enc_ctx, d W_fb, d b_fb, d v, d b_v, d W_s, d b_s: after the loop
+    a.d_s_tr_out = L.ds_all + (int64_t)t * B * K;
+    a.de_out = L.de_all + (int64_t)t * B * d.Ts;
     SL_CUDA_TRY(cudaMemsetAsync(a.d_accum, 0, sizeof(float) * B * d.Ts, st));
-    attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, g.str_W, g.str_b, L.att_ws, st);
+    attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, nullptr, nullptr, L.att_ws, st);
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 12);
       CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, L.dz,
@@ -420,6 +533,26 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     gemm_f32x3(false, true, (int)BT, Emb, 4 * H, L.dz, 4 * H, p.s_W, 4 * H, 1.f, L.dtrg, Emb, nullptr, nullptr, 0,
                L.gws, st);
     embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
+    // the attention's accumulations over t (deferred out of the loop)
+    {
+      Phase q(st, "k10_dec_bwd_deferred", 2.0 * T * BTs * (E + 6.0 * K));
+      const dim3 ge((unsigned)ceil_div(E, 512), (unsigned)ceil_div(d.Ts, kEncPos), (unsigned)B);
+      f32_enc_grad_kernel<<<ge, 128, (size_t)T * kEncPos * 4, st>>>(B, d.Ts, T, E, L.a_all, L.datt_all, d_enc);
+      SL_CUDA_TRY(cudaGetLastError());
+      const int nsc = (int)ceil_div(d.Ts, kCtxPos);
+      const dim3 gc((unsigned)ceil_div(K, 128), (unsigned)nsc, (unsigned)B);
+      f32_ctx_grad_kernel<<<gc, 128, (size_t)2 * T * kCtxPos * 4, st>>>(B, d.Ts, T, K, L.enc_ctx, L.acc_all, L.de_all,
+                                                                          L.str_all, p.fb_W, p.fb_b, p.e_W, L.dctx,
+                                                                          L.apart);
+      SL_CUDA_TRY(cudaGetLastError());
+      f32_ctx_reduce_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(B * nsc, K, L.apart, g.fb_W, g.fb_b, g.e_W,
+                                                                          L.de_all, (int64_t)T * B * d.Ts, g.e_b);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch(3);
+      // s_tr = s W_s + b_s: [d W_s; d b_s] = [S | 1]^T d S_tr over all T*B rows
+      gemm_f32x3(true, false, H, K, (int)BT, L.s_all, H, L.ds_all, K, 0.f, g.str_W, K, nullptr, g.str_b, K, L.gws,
+                 st);
+    }
     // enc_ctx = enc W_ctx + b_ctx: [d W_ctx; d b_ctx] = [enc | 1]^T d enc_ctx; d enc += d enc_ctx W_ctx^T
     gemm_f32x3(true, false, E, K, (int)BTs, enc, E, L.dctx, K, 0.f, g.ctx_W, K, nullptr, g.ctx_b, K, L.gws, st);
     gemm_f32x3(false, true, (int)BTs, E, K, L.dctx, K, p.ctx_W, K, 1.f, d_enc, E, nullptr, nullptr, 0, L.gws, st);
