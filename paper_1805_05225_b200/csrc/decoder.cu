@@ -881,7 +881,11 @@ int wgrad_ks(int M, int N, int K) {
 
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+#ifdef SL_EXPERIMENTS
   static const bool off = getenv("SL_DEC_NO_PDL") != nullptr;
+#else
+  constexpr bool off = false;
+#endif
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -937,7 +941,11 @@ Lay layout(const DecDims& d, void* base) {
   L.ks_f = ksplit_for(d.B, 4 * d.H, d.E + d.H);
   // the s_tr / d s projections (K = H or K columns, ~0.5 GFLOP) run on the mma.sync small-M
   // GEMM (SL_DEC_TC_SMALL=1: the tcgen05 pair GEMM with split-K instead)
+#ifdef SL_EXPERIMENTS
   L.small = getenv("SL_DEC_TC_SMALL") == nullptr;
+#else
+  L.small = true;
+#endif
   L.ks_s = L.small ? 1 : ksplit_for(d.B, d.K, d.H, 4);  // summed in the energy kernel (str_cols: at most 4)
   L.ks_1 = ksplit_for(d.B, d.E + d.H, 4 * d.H);
   L.ks_2 = L.small ? 1 : ksplit_for(d.B, d.H, d.K);
@@ -1058,8 +1066,12 @@ void configure() {  // opt in to > 48 KB dynamic shared memory once
   if (done) return;
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_ctx_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SL_CUDA_TRY(cudaFuncSetAttribute(dec_enc_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#ifdef SL_EXPERIMENTS
   const char* m = getenv("SL_DEC_TANH");
   const int mode = m ? atoi(m) : 0;
+#else
+  constexpr int mode = 0;
+#endif
   SL_CUDA_TRY(cudaMemcpyToSymbol(c_tanh_mode, &mode, sizeof(int)));
   done = true;
 }

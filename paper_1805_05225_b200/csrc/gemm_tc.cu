@@ -341,7 +341,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStr
 
 void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
   if (g.M <= 0 || g.N <= 0) return;
-  static const bool one_cta = getenv("SL_GEMM_1CTA") != nullptr;
+  constexpr bool one_cta = false;  // (the single-CTA form stays for operands the pair GEMM cannot load)
   SL_REQUIRE(!g.sm_part || gemm_bf16_tc2_ok(g), SL_ERR_UNSUPPORTED,
              "gemm_bf16_tc: softmax partials need the CTA-pair GEMM");
   if ((!one_cta || g.sm_part) && gemm_bf16_tc2_ok(g)) {

@@ -40,7 +40,6 @@ struct P2 {
   float* C2;
   int64_t ldc2;
   __nv_bfloat16* Cb;
-  int skip_epi;  // experiments only: load the accumulator but store nothing (wrong results)
 
   float4* sm_part;  // softmax partials (gemm.h TcGemm::sm_part)
   int sm_ld;
@@ -352,10 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         float v[32];
         tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + c, v);
         const int col0 = n0 + c;
-        if (p.skip_epi) {
-          if (v[0] == 12345.f) p.C2[0] = v[1];  // keep the load live
-          continue;
-        }
         if (p.Cb) {
           if (row >= p.M) continue;
           __nv_bfloat16* brow = p.Cb + z * p.split_stride + (int64_t)row * p.ldc + col0;
@@ -612,7 +607,6 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   const CUtensorMap tb = g.b_mn ? tm3d_mn(g.B, g.N, g.K, g.ldb) : tm2d(g.B, g.K, g.N, g.ldb, 128);
   // bulk-tensor output stores when the output is written (not accumulated) and
   // its rows are 16 B aligned; the per-row path stays for beta != 0
-  p.skip_epi = getenv("SL_GEMM_SKIP_EPI") != nullptr;
   p.sm_part = g.sm_part;
   p.sm_ld = g.sm_ld;
   p.sm_targets = g.sm_targets;

@@ -175,7 +175,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kc = kg * a.kb + j;
             const uint32_t sa = base + r_bytes + st * stage_bytes + j * kHTileBytes;
             const uint32_t sb = base + (uint32_t)kc * N * 128;
+#ifdef SL_EXPERIMENTS
             if (!(a.debug_flags & 1))
+#endif
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 tc::mma_f16(tmem + mt * N, tc::make_sdesc(sa + k * 32, 0, 1024),
@@ -294,7 +296,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[mt][r]), (r + pi) % C), 32);
       }
 
+#ifdef SL_EXPERIMENTS
       if (valid_row && !(a.debug_flags & 2)) {
+#else
+      if (valid_row) {
+#endif
         if (active) {
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
@@ -322,7 +328,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         red_release_gpu(ctr + mt, 1u);
         SL_TRACE(6 + mt);
       }
+#ifdef SL_EXPERIMENTS
       if (valid_row && !(a.debug_flags & 2)) {
+#else
+      if (valid_row) {
+#endif
         if (active) {
           if (save) {
 #pragma unroll
@@ -491,14 +501,16 @@ void launch_fwd(const CUtensorMap* tr, const CUtensorMap* th, const TcRecFwdArgs
 }  // namespace
 
 TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms) {
-  // 2-CTA clusters (N = 4*C*U = 128, the full-rate MMA width; each CTA streams
-  // only its K-half of h) trade the h stream for a DSMEM partial exchange;
-  // opt-in (SL_FWD_CLUSTER=1) until that exchange beats the single-CTA form.
+  // the CTA-pair kernel (M = 256 x N = 128 MMAs, 32 units per pair) where it fits;
+  // otherwise the single-CTA form.  (2-CTA K-split clusters, N = 4*C*U = 128, trade
+  // the h stream for a DSMEM partial exchange: measured slower, experiments builds only.)
+#ifdef SL_EXPERIMENTS
   const char* env = getenv("SL_FWD_CLUSTER");
   const bool cluster = env && env[0] == '1';
-  // CTA-pair kernel (M = 256 x N = 128 MMAs, 32 units per pair) unless disabled
-  const char* penv = getenv("SL_FWD_PAIR");
-  if (!(penv && penv[0] == '0') && !cluster && tc_rec_fwd_pair_fits(H, nd, sms)) {
+#else
+  constexpr bool cluster = false;
+#endif
+  if (!cluster && tc_rec_fwd_pair_fits(H, nd, sms)) {
     TcFwdShape sh{1, 32, (int)ceil_div(H, 32), (int)round_up(H, 64)};
     sh.pair = 1;
     return sh;

@@ -26,6 +26,22 @@
 //                   (tape.cpp:1157-1170) and write DZ_s to the ring and to the
 //                   K4 operand.
 // Semantics as rec_tc_bwd.cu.
+
+#ifndef SL_EXPERIMENTS
+// Experiments builds only (-DSL_EXPERIMENTS): measured slower than the 4-CTA
+// cluster form on B200, and the encoder's 16 clusters of 8 CTAs do not fit.
+#include "rec_tc.h"
+namespace sl {
+bool tc_rec_bwd_pair_fits(int, int, int, int, TcBwdShape*) { return false; }
+size_t tc_rec_bwd_pair_pack_elems(const TcBwdShape&) { return 0; }
+void tc_rec_bwd_pair_pack(const float*, int, const TcBwdShape&, __nv_bfloat16*, cudaStream_t) {
+  throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_pair: experiments build only"};
+}
+void rec_bwd_pair(const TcRecBwdArgs&, const TcBwdShape&, __nv_bfloat16* const*, cudaStream_t) {
+  throw Error{SL_ERR_UNSUPPORTED, "rec_bwd_pair: experiments build only"};
+}
+}  // namespace sl
+#else
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -511,3 +527,5 @@ void rec_bwd_pair(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* c
 }
 
 }  // namespace sl
+
+#endif  // SL_EXPERIMENTS

@@ -475,25 +475,6 @@ def test_cuda_graph_replay_matches_eager_steps(cuda):
     assert torch.equal(a.opt.m, b.opt.m) and torch.equal(a.opt.v, b.opt.v)
 
 
-@pytest.mark.parametrize("nd,H", [(1, 1024), (2, 300)])
-def test_bwd_pair_kernel_opt_in(cuda, monkeypatch, nd, H):
-    # the CTA-pair BPTT (rec_tc_bwd_pair.cu, opt-in SL_BWD_PAIR=1) against fp64
-    monkeypatch.setenv("SL_BWD_PAIR", "1")
-    B, T, D = 200, 13, 96
-    x, lens, W, R, b = _seeded(51, B, T, D, H)
-    params = [(W, R, b)] + ([_seeded(52, 1, 1, D, H)[2:]] if nd == 2 else [])
-    dy = torch.rand(B, T, nd * H, device="cuda") * 2 - 1
-    out = run_layer(x, lens, params, nd, 1, "bf16", dy)
-    dx = 0
-    for k in range(nd):
-        Wk, Rk, bk = params[k]
-        ref = torch_ref.sequence(x, lens, Wk, Rk, bk, (1, -1)[k], dy[:, :, k * H:(k + 1) * H])
-        for g in ("dW", "dR", "db"):
-            assert rel(out[g][k], ref[g]) < TOL["bf16"], g
-        dx = dx + ref["dx"]
-    assert rel(out["dx"], dx) < TOL["bf16"]
-
-
 def test_seq2seq_with_output_layer_matches_fp64(cuda):
     # the full bench step incl. the output softmax + label-smoothed CE: the
     # decoder receives dL/dy from the output layer (not a synthetic gradient)
