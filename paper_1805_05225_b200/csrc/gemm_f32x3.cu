@@ -119,6 +119,16 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int S, int64_t
 
 constexpr int kX3ChunkBlocks = 48;  // K blocks (of 64) per tensor-core accumulation chunk
 
+int sm_count_x3() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;
+  }
+  return n;
+}
+
 struct X3Dims {
   int Kp;
   int64_t a_rows, a_ld, b_rows, b_ld;  // stored bf16 operands
@@ -142,8 +152,17 @@ X3Dims x3_dims(bool transA, bool transB, int M, int N, int K, bool a_ones) {
   // accumulates K in chunks of kX3ChunkBlocks 64-wide blocks, each in a fresh TMEM
   // accumulator, and sums the chunks in fp32 registers (round-to-nearest) in its
   // epilogue (TcGemm::kchunk): the error stays at the one-chunk level for any K.
-  // Split-K (fp32 partials + a fixed-order reduction) only for tile-starved outputs.
-  d.ksplit = gemm_tc2_ksplit(Mt, N, 3 * d.Kp);
+  // Split-K (fp32 partials + a fixed-order reduction) only for outputs with fewer
+  // 256 x 256 tiles than CTA pairs (e.g. the decoder's per-step M = batch products):
+  // enough K ranges to occupy the pairs, >= 4 K blocks each.
+  {
+    const int tiles = (int)(ceil_div(Mt, 256) * ceil_div(N, 256));
+    const int pairs = std::max(1, sm_count_x3() / 2);
+    const int nk = (int)ceil_div(3 * (int64_t)d.Kp, 64);
+    int ks = 1;
+    if (tiles < pairs) ks = std::max(1, std::min(pairs / tiles, nk / 4));
+    d.ksplit = (int)ceil_div(nk, ceil_div(nk, ks));  // the count the pair GEMM runs (no empty ranges)
+  }
   d.p_ld = round_up(N, 4);
   d.p_stride = round_up((int64_t)Mt * d.p_ld, 64);
   return d;

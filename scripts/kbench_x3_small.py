@@ -17,7 +17,7 @@ for (name, M, N, K, tB) in [("cell z = xa W", 256, 4000, 3000, 0), ("g1 dxa = dz
     C = torch.empty(M, N, device="cuda")
     ws = torch.empty(L.sl_debug_gemm_f32x3_ws(0, tB, M, N, K), dtype=torch.uint8, device="cuda")
     f = lambda: L.sl_debug_gemm_f32x3(0, tB, M, N, K, A.data_ptr(), K, B.data_ptr(), B.stride(0), 0.0, C.data_ptr(),
-                                      N, None, ws.data_ptr(), s)
+                                      N, None, ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
     for _ in range(5): f()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
