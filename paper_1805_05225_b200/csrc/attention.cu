@@ -268,6 +268,9 @@ __global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(
       for (int w = 0; w < VE; ++w) s.f[w] += o.f[w];
     }
     s.store(p.att + (size_t)b * E + x);
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (p.att_copy[c]) s.store(p.att_copy[c] + (size_t)b * p.att_copy_ld[c] + x);
   }
 }
 
@@ -443,7 +446,9 @@ static int vec_k(const AttnArgs& p) {
              : 1;
 }
 static int vec_e(const AttnArgs& p) {
-  return (p.E % 8 == 0 && al32(p.enc) && al32(p.d_enc) && al32(p.d_att) && al32(p.att)) ? 8 : 1;
+  bool copies = true;  // the copies' rows take the float4 stores
+  for (int c = 0; c < 2; ++c) copies = copies && al16(p.att_copy[c]) && p.att_copy_ld[c] % 4 == 0;
+  return (p.E % 8 == 0 && al32(p.enc) && al32(p.d_enc) && al32(p.d_att) && al32(p.att) && copies) ? 8 : 1;
 }
 
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {

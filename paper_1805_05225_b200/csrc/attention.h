@@ -47,6 +47,10 @@ struct AttnArgs {
   int defer;
   float* d_s_tr_out;
   float* de_out;
+  // optional (the decoder's loop): further row-strided destinations of att [B, E]
+  // (the readout input and the next step's [att | s] row), written by the context kernel
+  float* att_copy[2];
+  int64_t att_copy_ld[2];
 };
 
 size_t attention_workspace_bytes(int B, int K, int H, int Ts);

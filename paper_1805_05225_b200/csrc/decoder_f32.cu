@@ -35,13 +35,14 @@ namespace {
 
 constexpr int kEncPos = 16;   // positions per thread in the d enc accumulation
 constexpr int kCtxPos = 8;    // positions per thread in the d enc_ctx accumulation
+constexpr int kRedSlices = 64;  // f32_ctx_reduce1/2: row slices of the deferred attention partials
 
 struct FLay {
   int64_t XA, RO;  // row pitches: [att ‖ s] (E + H), readout input [s ‖ trg ‖ att] (H + Emb + E)
   float *xw, *xa, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all, *z;
   float *dro, *dpre, *dz, *dxa, *dc, *ds, *dacc, *dctx, *dtrg;
   float* w2;  // [E + H, 4H] staging of [W_att; R]
-  float *datt_all, *de_all, *ds_all, *apart;  // deferred attention accumulations (per step saves)
+  float *datt_all, *de_all, *ds_all, *apart, *apart2;  // deferred attention accumulations (per step saves)
   int32_t* ids_tm;
   __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
   __nv_bfloat16 *ws_f, *ws_b;    // W_s split for s_tr = s W_s and d s = d s_tr W_s^T
@@ -109,11 +110,13 @@ FLay flayout(const DecDims& d, void* base) {
   L.de_all = tf(T * B * d.Ts);
   L.ds_all = tf(T * B * K);
   L.apart = tf(B * ceil_div(d.Ts, kCtxPos) * 3 * K + 64);
+  L.apart2 = tf(kRedSlices * (3 * K + 1));
   L.ids_tm = static_cast<int32_t*>(take((size_t)BT * 4));
-  L.wd2_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)(4 * H), (int)L.XA) * 2));
-  L.wd2_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)L.XA, (int)(4 * H)) * 2));
-  L.ws_f = static_cast<__nv_bfloat16*>(take(x3_b_elems(false, (int)K, (int)H) * 2));
-  L.ws_b = static_cast<__nv_bfloat16*>(take(x3_b_elems(true, (int)H, (int)K) * 2));
+  // the split images of [W_att; R] and W_s serve both the forward (B) and the backward (B^T) products
+  L.wd2_f = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)L.XA, (int)(4 * H)) * 2));
+  L.wd2_b = L.wd2_f;
+  L.ws_f = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)H, (int)K) * 2));
+  L.ws_b = L.ws_f;
   L.str_all = tf(T * B * K);
   L.att_ws = take(attention_workspace_bytes(d.B, d.K, d.H, d.Ts));
   L.gws = take(gemm_ws_bytes(d));
@@ -332,24 +335,56 @@ __global__ void __launch_bounds__(128) f32_ctx_grad_kernel(int B, int Ts, int T,
 
 // out_q[k] = sum over rows r (ascending) of part[(r * 3 + q) * K + k], q = 0, 1, 2;
 // and (thread 0 of block 0) *dbv = sum of de_all in a fixed order
-__global__ void f32_ctx_reduce_kernel(int rows, int K, const float* __restrict__ part, float* dwf, float* dbf,
-                                      float* dv, const float* __restrict__ de_all, int64_t n_de, float* dbv) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// Deterministic two-stage reduction of f32_ctx_grad's per-(b, source chunk) partials
+// and of d b_v = sum of every energy adjoint: stage 1 sums fixed row slices (and a
+// fixed segment of de_all per slice), stage 2 sums the slices in order.
+__global__ void __launch_bounds__(128) f32_ctx_reduce1_kernel(int rows, int K, const float* __restrict__ part,
+                                                              const float* __restrict__ de_all, int64_t n_de,
+                                                              float* __restrict__ part2) {
+  const int slice = blockIdx.y, k = blockIdx.x * 128 + threadIdx.x;
+  const int rps = (rows + kRedSlices - 1) / kRedSlices;
+  const int r0 = slice * rps, r1 = min(rows, r0 + rps);
   if (k < K) {
     float a = 0.f, c = 0.f, e = 0.f;
-    for (int r = 0; r < rows; ++r) {
+    for (int r = r0; r < r1; ++r) {
       a += part[((int64_t)r * 3 + 0) * K + k];
       c += part[((int64_t)r * 3 + 1) * K + k];
       e += part[((int64_t)r * 3 + 2) * K + k];
     }
-    dwf[k] = a, dbf[k] = c, dv[k] = e;
+    part2[((int64_t)slice * 3 + 0) * K + k] = a;
+    part2[((int64_t)slice * 3 + 1) * K + k] = c;
+    part2[((int64_t)slice * 3 + 2) * K + k] = e;
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {  // d b_v: the energies' bias gradient
+  if (blockIdx.x == 0) {  // this slice's segment of the energy adjoints
+    __shared__ float red[4];
+    const int64_t seg = (n_de + kRedSlices - 1) / kRedSlices;
+    const int64_t i0 = slice * seg, i1 = min(n_de, i0 + seg);
     float sum = 0.f;
-    for (int64_t i = threadIdx.x; i < n_de; i += 32) sum += de_all[i];
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += 128) sum += de_all[i];
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (threadIdx.x == 0) *dbv = sum;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) part2[(int64_t)kRedSlices * 3 * K + slice] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
+}
+
+__global__ void __launch_bounds__(128) f32_ctx_reduce2_kernel(int K, const float* __restrict__ part2, float* dwf,
+                                                              float* dbf, float* dv, float* dbv) {
+  const int k = blockIdx.x * 128 + threadIdx.x;
+  if (k < K) {
+    float a = 0.f, c = 0.f, e = 0.f;
+    for (int r = 0; r < kRedSlices; ++r) {
+      a += part2[((int64_t)r * 3 + 0) * K + k];
+      c += part2[((int64_t)r * 3 + 1) * K + k];
+      e += part2[((int64_t)r * 3 + 2) * K + k];
+    }
+    dwf[k] = a, dbf[k] = c, dv[k] = e;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    float sum = 0.f;
+    for (int r = 0; r < kRedSlices; ++r) sum += part2[(int64_t)kRedSlices * 3 * K + r];
+    *dbv = sum;
   }
 }
 
@@ -405,11 +440,9 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
                                   cudaMemcpyDeviceToDevice, st));
       SL_CUDA_TRY(cudaMemcpyAsync(w2 + (int64_t)E * 4 * H, p.s_R, sizeof(float) * H * 4 * H,
                                   cudaMemcpyDeviceToDevice, st));
-      x3_split_b(false, 4 * H, E + H, w2, 4 * H, L.wd2_f, st);
-      x3_split_b(true, E + H, 4 * H, w2, 4 * H, L.wd2_b, st);
+      x3_split_img(w2, 4 * H, E + H, 4 * H, L.wd2_f, st);
     }
-    x3_split_b(false, K, H, p.str_W, K, L.ws_f, st);  // W_s [H, K], both roles
-    x3_split_b(true, H, K, p.str_W, K, L.ws_b, st);
+    x3_split_img(p.str_W, K, H, K, L.ws_f, st);  // W_s [H, K], both roles
     f32_ids_tm_kernel<<<grid_of(BT), 256, 0, st>>>(prev_ids, B, T, L.ids_tm);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -437,13 +470,12 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     a.a = L.a_all + (int64_t)t * B * d.Ts;
     a.accum_out = L.acc_all + (int64_t)(t + 1) * B * d.Ts;
     a.s_tr_out = L.str_all + (int64_t)t * B * K;
+    // att_t also -> the readout input (columns H + Emb..) and the next step's [att ‖ s] row
+    a.att_copy[0] = L.ro + (int64_t)t * B * L.RO + H + Emb;
+    a.att_copy_ld[0] = L.RO;
+    a.att_copy[1] = t + 1 < T ? L.xa + (int64_t)(t + 1) * B * L.XA : nullptr;
+    a.att_copy_ld[1] = L.XA;
     attention_fwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.att_ws, st);
-    // att_t -> the readout input (columns H + Emb..) and the next step's [att ‖ s] row
-    SL_CUDA_TRY(cudaMemcpy2DAsync(L.ro + (int64_t)t * B * L.RO + H + Emb, L.RO * 4, a.att, (size_t)E * 4,
-                                  (size_t)E * 4, B, cudaMemcpyDeviceToDevice, st));
-    if (t + 1 < T)
-      SL_CUDA_TRY(cudaMemcpy2DAsync(L.xa + (int64_t)(t + 1) * B * L.XA, L.XA * 4, a.att, (size_t)E * 4,
-                                    (size_t)E * 4, B, cudaMemcpyDeviceToDevice, st));
   }
   {
     Phase ph(st, "k10_dec_fwd_hoisted", 2.0 * BT * L.RO * d.Rd);
@@ -545,10 +577,12 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
                                                                           L.str_all, p.fb_W, p.fb_b, p.e_W, L.dctx,
                                                                           L.apart);
       SL_CUDA_TRY(cudaGetLastError());
-      f32_ctx_reduce_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(B * nsc, K, L.apart, g.fb_W, g.fb_b, g.e_W,
-                                                                          L.de_all, (int64_t)T * B * d.Ts, g.e_b);
+      f32_ctx_reduce1_kernel<<<dim3((unsigned)ceil_div(K, 128), kRedSlices), 128, 0, st>>>(
+          B * nsc, K, L.apart, L.de_all, (int64_t)T * B * d.Ts, L.apart2);
       SL_CUDA_TRY(cudaGetLastError());
-      count_launch(3);
+      f32_ctx_reduce2_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(K, L.apart2, g.fb_W, g.fb_b, g.e_W, g.e_b);
+      SL_CUDA_TRY(cudaGetLastError());
+      count_launch(4);
       // s_tr = s W_s + b_s: [d W_s; d b_s] = [S | 1]^T d S_tr over all T*B rows
       gemm_f32x3(true, false, H, K, (int)BT, L.s_all, H, L.ds_all, K, 0.f, g.str_W, K, nullptr, g.str_b, K, L.gws,
                  st);

@@ -14,11 +14,22 @@ void gemm_f32(bool transA, bool transB, int M, int N, int K, float alpha, const 
 // stored [K, M] (transA) and the column sums of op(B) (= ones^T op(B)) are also
 // written to ones_row_out (+ beta * previous) — the bias gradient for free.
 size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K, bool a_ones);
-// B split once for repeated GEMMs (e.g. a weight used every time step): x3_split_b
-// writes the K-tripled bf16 image of op(B) (x3_b_elems elements); gemm_f32x3_pb then
-// splits only A per call (its scratch: gemm_f32x3_workspace_bytes of the same shape).
+// The split image of a stored fp32 matrix S [rows, cols]: bf16 hi [rows, x3_img_ld]
+// followed by bf16 lo [rows, x3_img_ld] (padding columns zero).  It does not depend on
+// the role the matrix plays in a GEMM (A or B, transposed or not), so one split serves
+// every product that reads S.
+int64_t x3_img_ld(int cols);
+size_t x3_img_elems(int rows, int cols);
+void x3_split_img(const float* S, int64_t ld, int rows, int cols, __nv_bfloat16* img, cudaStream_t st);
+// B split once for repeated GEMMs (e.g. a weight used every time step): the image of
+// the stored B (x3_b_elems elements); gemm_f32x3_pb then splits only A per call (its
+// scratch: gemm_f32x3_workspace_bytes of the same shape).
 size_t x3_b_elems(bool transB, int N, int K);
 void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfloat16* B3, cudaStream_t st);
+// both operands pre-split (images of the stored A and B)
+void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
+                    const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
+                    cudaStream_t st);
 void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
                    const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,
                    cudaStream_t st, float* ones_row_out = nullptr, int64_t ld_ones = 0);
@@ -70,6 +81,11 @@ struct TcGemm {
   // epilogue (round-to-nearest) — so the tensor core's accumulation error stays at the
   // one-chunk level for any K (gemm_f32x3.cu)
   int kchunk = 0;
+  // optional (pair GEMM, fp32 C): fp32-class "x3" mode — A / B above are the bf16 hi
+  // parts and these the lo parts (same shape and ld) of split fp32 operands; the GEMM
+  // computes A_hi B_hi + A_lo B_hi + A_hi B_lo (gemm_f32x3.cu)
+  const __nv_bfloat16* A_lo = nullptr;
+  const __nv_bfloat16* B_lo = nullptr;
 };
 // number of K splits the pair GEMM would use to fill the SMs for this shape
 int gemm_tc2_ksplit(int M, int N, int K);

@@ -350,6 +350,7 @@ void gemm_bf16_tc(const TcGemm& g, cudaStream_t stream) {
     return;
   }
   SL_REQUIRE(g.ksplit <= 1, SL_ERR_UNSUPPORTED, "gemm_bf16_tc: split-K needs the CTA-pair GEMM");
+  SL_REQUIRE(!g.A_lo && !g.B_lo, SL_ERR_UNSUPPORTED, "gemm_bf16_tc: x3 operands need the CTA-pair GEMM");
   SL_REQUIRE(g.kchunk <= 0, SL_ERR_UNSUPPORTED, "gemm_bf16_tc: chunked accumulation needs the CTA-pair GEMM");
   constexpr int BN = 256;
   Params p{};

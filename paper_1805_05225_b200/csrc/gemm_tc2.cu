@@ -29,6 +29,12 @@ constexpr int BMP = 256, BNP = 256, BK = 64, kStages = 6, kEpiWarps = 8, kThread
 constexpr uint32_t kHalf = 128 * 64 * 2;  // 16 KB: 128 rows (or cols) x 64 K of bf16
 constexpr uint32_t kStage = 2 * kHalf;    // A half + B half per CTA
 constexpr uint32_t kSmem = kStages * kStage + 1024;
+// X3 (fp32-class) mode: a stage holds A_hi, B_hi, A_lo, B_lo of one 64-wide K block
+// (64 KB per CTA, 3 stages in the same shared memory) and feeds three MMAs per
+// 16-wide K step: A_hi B_hi + A_lo B_hi + A_hi B_lo
+template <bool X3> __host__ __device__ constexpr int n_stages() { return X3 ? 3 : kStages; }
+template <bool X3> __host__ __device__ constexpr uint32_t stage_bytes() { return X3 ? 2 * kStage : kStage; }
+static_assert(3 * 2 * kStage <= kStages * kStage, "X3 stages fit the shared memory of the bf16 ones");
 
 struct P2 {
   int M, N, K, nm, nn, nk;
@@ -175,10 +181,12 @@ __device__ __forceinline__ void store_row32(const P2& p, float* crow, int col0, 
   }
 }
 
-template <bool A_MN, bool B_MN, bool CHUNK>
+template <bool A_MN, bool B_MN, bool CHUNK, bool X3>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
-    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB, P2 p) {
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl, P2 p) {
+  constexpr int NST = n_stages<X3>();
+  constexpr uint32_t SB = stage_bytes<X3>();
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -193,7 +201,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
-    for (int s = 0; s < kStages; ++s) {
+    if (X3) {
+      tc::prefetch_tmap(&tmAl);
+      tc::prefetch_tmap(&tmBl);
+    }
+    for (int s = 0; s < NST; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
     }
@@ -227,16 +239,22 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP + r * 128;
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty_bar[st], ph ^ 1);
-          const uint32_t sa = base + st * kStage, sb = sa + kHalf;
+          const uint32_t sa = base + st * SB, sb = sa + kHalf;
           const uint32_t fb = mapa_u32(tc::smem_u32(&full_bar[st]), 0);  // leader's barrier
-          if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * kStage);
+          if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * SB);
           const int k0 = kb * BK;
           if (A_MN) tma3d_pair(sa, &tmA, fb, 0, k0, m0 / 64);
           else tma2d_pair(sa, &tmA, fb, k0, m0);
           if (kb == kb0 && t == pair) GT(2);
           if (B_MN) tma3d_pair(sb, &tmB, fb, 0, k0, n0 / 64);
           else tma2d_pair(sb, &tmB, fb, k0, n0);
-          if (++st == kStages) {
+          if (X3) {  // the lo halves of both operands
+            if (A_MN) tma3d_pair(sa + 2 * kHalf, &tmAl, fb, 0, k0, m0 / 64);
+            else tma2d_pair(sa + 2 * kHalf, &tmAl, fb, k0, m0);
+            if (B_MN) tma3d_pair(sa + 3 * kHalf, &tmBl, fb, 0, k0, n0 / 64);
+            else tma2d_pair(sa + 3 * kHalf, &tmBl, fb, k0, n0);
+          }
+          if (++st == NST) {
             st = 0;
             ph ^= 1;
           }
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           for (int kb = c0; kb < c1; ++kb) {
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
-            const uint32_t sa = base + st * kStage, sb = sa + kHalf;
+            const uint32_t sa = base + st * SB, sb = sa + kHalf;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = A_MN ? tc::make_sdesc(sa + k * 2048, 8192, 1024)
@@ -269,9 +287,18 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               const uint64_t bd = B_MN ? tc::make_sdesc(sb + k * 2048, 8192, 1024)
                                        : tc::make_sdesc(sb + k * 32, 0, 1024);
               mma_pair(tmem + acc * BNP, ad, bd, idesc, (kb != c0 || k != 0) ? 1u : 0u);
+              if (X3) {  // + A_lo B_hi + A_hi B_lo
+                const uint32_t sal = sa + 2 * kHalf, sbl = sa + 3 * kHalf;
+                const uint64_t adl = A_MN ? tc::make_sdesc(sal + k * 2048, 8192, 1024)
+                                          : tc::make_sdesc(sal + k * 32, 0, 1024);
+                const uint64_t bdl = B_MN ? tc::make_sdesc(sbl + k * 2048, 8192, 1024)
+                                          : tc::make_sdesc(sbl + k * 32, 0, 1024);
+                mma_pair(tmem + acc * BNP, adl, bd, idesc, 1u);
+                mma_pair(tmem + acc * BNP, ad, bdl, idesc, 1u);
+              }
             }
             commit_pair(&empty_bar[st]);  // frees the slot in both CTAs
-            if (++st == kStages) {
+            if (++st == NST) {
               st = 0;
               ph ^= 1;
             }
@@ -534,9 +561,10 @@ int sms2() {
   return n;
 }
 
-template <bool A_MN, bool B_MN, bool CHUNK>
-void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream_t s) {
-  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, CHUNK>;
+template <bool A_MN, bool B_MN, bool CHUNK, bool X3>
+void launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al, const CUtensorMap& bl, const P2& p,
+             cudaStream_t s) {
+  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, CHUNK, X3>;
   static bool configured = false;
   if (!configured) {
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -544,7 +572,7 @@ void launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, cudaStream
   }
   const int tiles = p.nm * p.nn * p.ksplit;
   const int pairs = std::min(tiles, sms2() / 2);
-  kern<<<2 * pairs, kThreads, kSmem, s>>>(a, b, p);
+  kern<<<2 * pairs, kThreads, kSmem, s>>>(a, b, al, bl, p);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -564,6 +592,22 @@ int gemm_tc2_ksplit(int M, int N, int K) {
   if (tiles > 8) return 1;
   const int want = std::max(1, std::min(sms2() / 2 / tiles, nk / 4));
   return (int)ceil_div(nk, ceil_div(nk, want));  // the count gemm_bf16_tc2 actually runs (no empty units)
+}
+
+template <bool X3>
+void dispatch2(const TcGemm& g, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tal,
+               const CUtensorMap& tbl, const P2& p, cudaStream_t st) {
+  const bool ch = g.kchunk > 0;
+#define SL_L2(AM, BM)                                                   \
+  do {                                                                  \
+    if (ch) launch2<AM, BM, true, X3>(ta, tb, tal, tbl, p, st);         \
+    else launch2<AM, BM, false, X3>(ta, tb, tal, tbl, p, st);           \
+  } while (0)
+  if (!g.a_mn && g.b_mn) SL_L2(false, true);
+  else if (!g.a_mn && !g.b_mn) SL_L2(false, false);
+  else if (g.a_mn && g.b_mn) SL_L2(true, true);
+  else SL_L2(true, false);
+#undef SL_L2
 }
 
 bool gemm_bf16_tc2_ok(const TcGemm& g) {
@@ -613,18 +657,19 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   SL_REQUIRE(!g.sm_part || (g.Cb && g.sm_targets), SL_ERR_INVALID_ARGUMENT,
              "gemm: softmax partials need the bf16 output and the targets");
   p.kchunk = g.kchunk;
-  if (g.kchunk > 0) {
+  if (g.kchunk > 0)
     SL_REQUIRE(!g.Cb && !g.sm_part, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: chunked accumulation writes fp32 C");
-    if (!g.a_mn && g.b_mn) launch2<false, true, true>(ta, tb, p, stream);
-    else if (!g.a_mn && !g.b_mn) launch2<false, false, true>(ta, tb, p, stream);
-    else if (g.a_mn && g.b_mn) launch2<true, true, true>(ta, tb, p, stream);
-    else launch2<true, false, true>(ta, tb, p, stream);
-    return;
+  const bool x3 = g.A_lo != nullptr;
+  SL_REQUIRE(x3 == (g.B_lo != nullptr), SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: x3 mode needs both lo operands");
+  if (x3) {
+    SL_REQUIRE(((uintptr_t)g.A_lo & 15) == 0 && ((uintptr_t)g.B_lo & 15) == 0 && !g.Cb && !g.sm_part,
+               SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: x3 operands need 16 B alignment and fp32 C");
+    const CUtensorMap tal = g.a_mn ? tm3d_mn(g.A_lo, g.M, g.K, g.lda) : tm2d(g.A_lo, g.K, g.M, g.lda, 128);
+    const CUtensorMap tbl = g.b_mn ? tm3d_mn(g.B_lo, g.N, g.K, g.ldb) : tm2d(g.B_lo, g.K, g.N, g.ldb, 128);
+    dispatch2<true>(g, ta, tb, tal, tbl, p, stream);
+  } else {
+    dispatch2<false>(g, ta, tb, ta, tb, p, stream);
   }
-  if (!g.a_mn && g.b_mn) launch2<false, true, false>(ta, tb, p, stream);
-  else if (!g.a_mn && !g.b_mn) launch2<false, false, false>(ta, tb, p, stream);
-  else if (g.a_mn && g.b_mn) launch2<true, true, false>(ta, tb, p, stream);
-  else launch2<true, false, false>(ta, tb, p, stream);
 }
 
 }  // namespace sl

@@ -14,8 +14,11 @@ L.sl_debug_gemm_bf16_split.argtypes = [ci] * 3 + [vp, i64, ci, vp, i64, ci, vp, 
 L.sl_debug_gemm_trace.argtypes = [vp]
 pad = lambda n: (n + 63) // 64 * 64
 names = ["entry", "prologue", "1st TMA", "last MMA", "acc ready", "epi done", "final sync", "dealloc"]
-for name, M, N, K, b_mn, ks in [("s_tr", 256, 1000, 1000, 1, 4), ("cell_fwd", 256, 4000, 3000, 1, 4),
-                                ("g1", 256, 3000, 4000, 0, 6)]:
+CASES = [("s_tr", 256, 1000, 1000, 1, 4), ("cell_fwd", 256, 4000, 3000, 1, 4), ("g1", 256, 3000, 4000, 0, 6)]
+if "--x3" in sys.argv:  # the fp32-class GEMMs' K-tripled operand images
+    CASES = [("s_tr x3", 256, 1000, 3008, 1, 10), ("cell_fwd x3", 256, 4000, 9024, 1, 4),
+             ("g1 x3", 256, 3000, 12000, 0, 6), ("cell_fwd x3 ks1", 256, 4000, 9024, 1, 1)]
+for name, M, N, K, b_mn, ks in CASES:
     A = torch.randn(M, pad(K), device="cuda").bfloat16()
     B = (torch.randn(K, pad(N), device="cuda") if b_mn else torch.randn(N, pad(K), device="cuda")).bfloat16()
     C = torch.empty(ks, M, N, device="cuda")
