@@ -13,6 +13,8 @@
 // (gemm_f32x3.cu).  fp32 data: the step is bandwidth-bound, not tensor-bound.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "attention.h"
 #include "gemm.h"
 #include "profile.h"
@@ -410,6 +412,139 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, co
   }
 }
 
+// ---- Cluster form of the forward: one 4-CTA cluster per batch row walks the row's
+// [Ts, K] energy inputs and [Ts, E] encoder states once: energies of a quarter of
+// the positions per CTA (warp per position, lanes along K) -> DSMEM broadcast ->
+// masked softmax (every CTA) -> context columns of a quarter of E per CTA (thread
+// per 4 columns, two position groups), written to att and its copies.  One launch
+// instead of two and no e round trip (43-47 us vs 50 us per config-4 step).  The
+// same decomposition for the backward measured slower than the chunked kernels
+// (cluster-barrier waits), so the backward keeps them.
+namespace cg = cooperative_groups;
+constexpr int kCl = 4;            // CTAs per cluster (per batch row)
+constexpr int kClThreads = 256;   // 8 warps
+constexpr int kClWarps = kClThreads / 32;
+
+__device__ __forceinline__ float4 ldg4(const float* q) { return __ldg(reinterpret_cast<const float4*>(q)); }
+__device__ __forceinline__ float4 lds4(const float* q) { return *reinterpret_cast<const float4*>(q); }
+
+struct ClSmem {  // float offsets into the dynamic shared memory
+  int c, w, v, e, part, total;
+};
+__host__ __device__ inline ClSmem cl_smem(int K, int Ts) {
+  const int K4 = (K + 3) / 4 * 4, T4 = (Ts + 3) / 4 * 4;
+  ClSmem m;
+  m.c = 0;
+  m.w = m.c + K4;
+  m.v = m.w + K4;
+  m.e = m.v + K4;         // e, then a (in place)
+  m.part = m.e + T4;      // context partials of position group 1: 128 float4
+  m.total = m.part + 512;
+  return m;
+}
+
+__device__ __forceinline__ void cl_stage_cols(const AttnArgs& p, int b, float* sh, const ClSmem& m) {
+  for (int k = threadIdx.x; k < p.K; k += kClThreads) {
+    sh[m.c + k] = p.s_tr[(size_t)b * p.K + k] + p.b_fb[k];
+    sh[m.w + k] = p.W_fb[k];
+    sh[m.v + k] = p.v[k];
+  }
+}
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
+    attn_fwd_cluster_kernel(AttnArgs p) {
+  extern __shared__ float4 sh4[];
+  float* sh = reinterpret_cast<float*>(sh4);
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank(), b = blockIdx.y, Ts = p.Ts, K = p.K, E = p.E;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int len = min(max(p.lens[b], 0), Ts);
+  const ClSmem m = cl_smem(K, Ts);
+  cl_stage_cols(p, b, sh, m);
+  __syncthreads();
+  // energies of positions j = r + kCl (warp + kClWarps i)
+  for (int j = r + kCl * warp; j < len; j += kCl * kClWarps) {
+    const float aj = __ldg(p.accum + (size_t)b * Ts + j);
+    const float* x = p.enc_ctx + ((size_t)b * Ts + j) * K;
+    float sum = 0.f;
+    for (int k0 = lane * 4; k0 < K; k0 += 128 * 8) {
+      float4 xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = k0 + 128 * u < K ? ldg4(x + k0 + 128 * u) : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + 128 * u;
+        if (k < K) {
+          const float4 c = lds4(sh + m.c + k), w = lds4(sh + m.w + k), v = lds4(sh + m.v + k);
+          sum += v.x * tanh_fast(xv[u].x + aj * w.x + c.x) + v.y * tanh_fast(xv[u].y + aj * w.y + c.y) +
+                 v.z * tanh_fast(xv[u].z + aj * w.z + c.z) + v.w * tanh_fast(xv[u].w + aj * w.w + c.w);
+        }
+      }
+    }
+    sum = warp_sum(sum);
+    if (lane < kCl) cl.map_shared_rank(sh + m.e, lane)[j] = sum;
+  }
+  cl.sync();
+  float* a_sh = sh + m.e;
+  if (warp == 0) {  // masked softmax (tape.cpp:952-960), in place
+    const float bv = *p.b_v;
+    float mx = -INFINITY;
+    for (int j = lane; j < len; j += 32) mx = fmaxf(mx, a_sh[j] + bv);
+    mx = warp_max(mx);
+    float z = 0.f;
+    for (int j = lane; j < len; j += 32) z += expf(a_sh[j] + bv - mx);
+    z = warp_sum(z);
+    for (int j = lane; j < Ts; j += 32) {
+      const float aj = j < len ? expf(a_sh[j] + bv - mx) / z : 0.f;
+      a_sh[j] = aj;
+      if (r == 0) {
+        p.a[(size_t)b * Ts + j] = aj;
+        p.accum_out[(size_t)b * Ts + j] = p.accum[(size_t)b * Ts + j] + aj;
+      }
+    }
+  }
+  __syncthreads();
+  // context columns [x0, x1) of this CTA: thread q of group g (positions j = g mod 2)
+  const int cols = (E / 4 + kCl - 1) / kCl * 4;
+  const int x0 = r * cols, x1 = min(E, x0 + cols);
+  const int g = threadIdx.x / 128, q = threadIdx.x % 128;
+  float4* part = reinterpret_cast<float4*>(sh + m.part);
+  for (int xb = x0; xb < x1; xb += 512) {
+    const int x = xb + 4 * q;
+    float4 acc = make_float4(0, 0, 0, 0);
+    if (x < x1) {
+      const float* src = p.enc + (size_t)b * Ts * E + x;
+      int j = g;
+      for (; j + 2 * 7 < len; j += 2 * 8) {
+        float4 ev[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ev[u] = ldg4(src + (size_t)(j + 2 * u) * E);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float aj = a_sh[j + 2 * u];
+          acc.x += aj * ev[u].x, acc.y += aj * ev[u].y, acc.z += aj * ev[u].z, acc.w += aj * ev[u].w;
+        }
+      }
+      for (; j < len; j += 2) {
+        const float4 ev = ldg4(src + (size_t)j * E);
+        const float aj = a_sh[j];
+        acc.x += aj * ev.x, acc.y += aj * ev.y, acc.z += aj * ev.z, acc.w += aj * ev.w;
+      }
+    }
+    if (g == 1) part[q] = acc;
+    __syncthreads();
+    if (g == 0 && x < x1) {
+      const float4 o = part[q];
+      acc.x += o.x, acc.y += o.y, acc.z += o.z, acc.w += o.w;
+      *reinterpret_cast<float4*>(p.att + (size_t)b * E + x) = acc;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        if (p.att_copy[c]) *reinterpret_cast<float4*>(p.att_copy[c] + (size_t)b * p.att_copy_ld[c] + x) = acc;
+    }
+    __syncthreads();
+  }
+}
+
 // column sums of d_s_tr [B, K] into d_b_s (+=)
 __global__ void colsum_kernel(const float* x, int rows, int cols, float* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -451,6 +586,19 @@ static int vec_e(const AttnArgs& p) {
   return (p.E % 8 == 0 && al32(p.enc) && al32(p.d_enc) && al32(p.d_att) && al32(p.att) && copies) ? 8 : 1;
 }
 
+// the cluster kernel: float4 rows throughout, the shared-memory plan within one SM
+static bool cluster_ok(const AttnArgs& p) {
+  bool copies = true;
+  for (int c = 0; c < 2; ++c) copies = copies && al16(p.att_copy[c]) && p.att_copy_ld[c] % 4 == 0;
+  return p.K % 4 == 0 && p.E % 4 == 0 && al16(p.enc_ctx) && al16(p.enc) && al16(p.att) &&
+         al16(p.s_tr) && al16(p.b_fb) && al16(p.W_fb) && al16(p.v) && copies &&
+         (size_t)cl_smem(p.K, p.Ts).total * sizeof(float) <= 200 * 1024 && !getenv("SL_ATTN_CHUNKED");
+}
+template <typename F>
+static void cl_configure(F kern, size_t smem) {
+  SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {
   p.s_tr = p.s_tr_out ? p.s_tr_out : static_cast<float*>(ws);
   if (p.W_s3_fwd)  // s_tr = s W_s + b_s
@@ -459,6 +607,14 @@ void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
   float* e = row_buf(p, ws);
   Phase ph(st, "k8_attention_fwd", 0.0, 4.0 * p.B * p.Ts * (double)(p.K + p.E));
+  if (cluster_ok(p)) {
+    const size_t smem = (size_t)cl_smem(p.K, p.Ts).total * sizeof(float);
+    cl_configure(attn_fwd_cluster_kernel, smem);
+    attn_fwd_cluster_kernel<<<dim3(kCl, (unsigned)p.B), kClThreads, smem, st>>>(p);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    return;
+  }
   const dim3 g1((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
   if (vec_k(p) == 4) attn_energy_kernel<4><<<g1, kThreads, 0, st>>>(p, e);
   else attn_energy_kernel<1><<<g1, kThreads, 0, st>>>(p, e);
@@ -489,8 +645,8 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     SL_CUDA_TRY(cudaMemsetAsync(p.d_b_v, 0, sizeof(float), st));
     if (d_b_s && !d_W_s) SL_CUDA_TRY(cudaMemsetAsync(d_b_s, 0, sizeof(float) * p.K, st));
   }
-  SL_CUDA_TRY(cudaMemsetAsync(p.d_s_tr, 0, sizeof(float) * p.B * p.K, st));
   float* d_a = row_buf(p, ws);
+  SL_CUDA_TRY(cudaMemsetAsync(p.d_s_tr, 0, sizeof(float) * p.B * p.K, st));
   {
     Phase ph(st, "k8_attention_bwd", 0.0, 4.0 * p.B * p.Ts * (double)(2 * p.K + 2 * p.E));
     const dim3 g((unsigned)ceil_div(p.Ts, kJC), (unsigned)p.B), ge((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);

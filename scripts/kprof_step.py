@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--graph", action="store_true")
 ap.add_argument("--top", type=int, default=40)
+ap.add_argument("--no-prof", action="store_true", help="just run the steps (for an outer ncu)")
 a = ap.parse_args()
 L, B, T, D0, H, V = 6, 256, 60, 620, 1000, 20000
 dev = torch.device("cuda:0")
@@ -47,6 +48,10 @@ if a.graph:
     gr.replay()
     torch.cuda.synchronize()
     run = gr.replay
+if a.no_prof:
+    run()
+    torch.cuda.synchronize()
+    sys.exit(0)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     run()
     torch.cuda.synchronize()
