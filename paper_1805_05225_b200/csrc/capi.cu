@@ -90,6 +90,10 @@ bool use_x3(const Dims& d, int prec) {
          tc_rec_bwd_x3_shape(d.H, sm_count()).C > 0;
 }
 int64_t g4(const Dims& d) { return 4 * (int64_t)d.H; }
+// row stride of the DZ image: the K4 weight-gradient GEMMs read one direction's
+// column slice as 64-wide MN-major blocks, which may run up to 64 columns past it
+int64_t dzi_ld(const Dims& d) { return x3_img_ld(d.nd * 4 * d.H) + 64; }
+
 size_t x3_gemm_ws(const Dims& d, bool bwd) {
   const int M = (int)d.BT(), G = 4 * d.H, Gc = d.nd * G;
   if (!bwd) return gemm_f32x3_workspace_bytes(false, false, M, Gc, d.D, false);
@@ -237,10 +241,9 @@ struct BwdWork {
   __nv_bfloat16* dzring[2] = {nullptr, nullptr};  // bf16 path: DZ ring (rec_tc.h dz_ring_off)
   __nv_bfloat16* rb[2] = {nullptr, nullptr};      // bf16 path: packed R row slices
   __nv_bfloat16* dzringlo[2] = {nullptr, nullptr};  // x3 path: lo halves of DZ, same ring layout
-  float* dzf = nullptr;                           // x3 path: DZ of both directions fp32 [B*T, nd*4H]
+  __nv_bfloat16* dzi = nullptr;  // x3 path: DZ of both directions as its split image (hi, lo) [B*T, dzi_ld]
   float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
   void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
-  __nv_bfloat16* dz3 = nullptr;                   // x3 path: DZ_d split once for both dW and dR
   unsigned* bar = nullptr;
 };
 
@@ -259,10 +262,9 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
     }
   } else if (use_x3(d, prec)) {
     const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count(), d.nd);
-    w.dzf = c.take<float>((size_t)d.BT() * d.nd * g4(d));
+    w.dzi = c.take<__nv_bfloat16>((size_t)2 * d.BT() * dzi_ld(d));
     w.wcatf = c.take<float>((size_t)d.D * d.nd * g4(d));
     w.gws = c.take<char>(x3_gemm_ws(d, true));
-    w.dz3 = c.take<__nv_bfloat16>(x3_b_elems(false, 4 * d.H, (int)d.BT()));
     for (int k = 0; k < d.nd; ++k) {
       w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
       w.dzringlo[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
@@ -285,12 +287,15 @@ int dir_sign(const sl_lstm_layer* L, int k) {
 
 
 // out[c] = beta * out[c] + sum_r x[r * ld + c] (ascending r)
-__global__ void colsum_f32_kernel(int rows, int cols, const float* __restrict__ x, int64_t ld, float beta,
-                                  float* out) {
+__global__ void colsum_img_kernel(int rows, int cols, const __nv_bfloat16* __restrict__ hi, int64_t ld, int64_t lo,
+                                  float beta, float* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += x[(int64_t)r * ld + c];
+  for (int r = 0; r < rows; ++r) {
+    const int64_t i = (int64_t)r * ld + c;
+    s += __bfloat162float(hi[i]) + __bfloat162float(hi[lo + i]);
+  }
   out[c] = beta != 0.f ? beta * out[c] + s : s;
 }
 
@@ -372,8 +377,9 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.dy_ld = (int64_t)d.nd * d.H;
     a.dh_last = dh_last;
     a.dc_last = dc_last;
-    a.dzcatf = w.dzf;
-    a.dzcat_ld = Gc;
+    a.dzimg = w.dzi;
+    a.dzimg_rows = M;
+    a.dzcat_ld = dzi_ld(d);
     a.dz_dir_off = G;
     a.bar = w.bar;
     const __nv_bfloat16* rb[2] = {nullptr, nullptr};
@@ -398,28 +404,30 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
       SL_CUDA_TRY(cudaMemcpy2DAsync(w.wcatf + k * G, Gc * sizeof(float), W[k], G * sizeof(float),
                                     G * sizeof(float), d.D, cudaMemcpyDeviceToDevice, st));
     Phase ph(st, "k4_dx_gemm", 2.0 * M * (double)Gc * d.D);
-    gemm_f32x3(false, true, M, d.D, (int)Gc, w.dzf, Gc, w.wcatf, Gc, beta, dx, d.D, nullptr, nullptr, 0, w.gws, st);
+    gemm_f32x3_ex(false, true, M, d.D, (int)Gc, nullptr, 0, w.dzi, w.wcatf, Gc, nullptr, beta, dx, d.D, nullptr,
+                  nullptr, 0, w.gws, st, dzi_ld(d), (int64_t)M * dzi_ld(d));
   }
+  // the weight gradients read direction k's column slice of the same DZ image
+  const int64_t zl = dzi_ld(d), zlo = (int64_t)M * zl;
   for (int k = 0; k < d.nd; ++k) {
     float* dbk = db ? db[k] : nullptr;
     const bool want_w = dW && dW[k], want_r = dR && dR[k];
-    if (want_w || want_r) {  // DZ_d's K-tripled image, split once for both weight-gradient GEMMs
-      Phase ph(st, "x3_split", 0.0, 10.0 * M * G);
-      x3_split_b(false, (int)G, M, w.dzf + k * G, Gc, w.dz3, st);
-    }
+    const __nv_bfloat16* zk = w.dzi + k * G;
     if (want_w || dbk) {
       Phase ph(st, "k4_dw_gemm", 2.0 * M * (double)G * d.D);
       if (want_w) {
-        gemm_f32x3_pb(true, false, d.D, (int)G, M, x, d.D, w.dz3, beta, dW[k], G, nullptr, w.gws, st, dbk, G);
-      } else {  // db alone: fixed-order column sums of DZ_d
-        colsum_f32_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, w.dzf + k * G, Gc, beta, dbk);
+        gemm_f32x3_ex(true, false, d.D, (int)G, M, x, d.D, nullptr, nullptr, 0, zk, beta, dW[k], G, nullptr, dbk, G,
+                      w.gws, st, 0, 0, zl, zlo);
+      } else {  // db alone: fixed-order column sums of DZ_d (hi + lo)
+        colsum_img_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, zk, zl, zlo, beta, dbk);
         SL_CUDA_TRY(cudaGetLastError());
         count_launch();
       }
     }
     if (want_r) {
       Phase ph(st, "k4_dr_gemm", 2.0 * M * (double)G * d.H);
-      gemm_f32x3_pb(true, false, d.H, (int)G, M, rv.hprev[k], d.H, w.dz3, beta, dR[k], G, nullptr, w.gws, st);
+      gemm_f32x3_ex(true, false, d.H, (int)G, M, rv.hprev[k], d.H, nullptr, nullptr, 0, zk, beta, dR[k], G, nullptr,
+                    nullptr, 0, w.gws, st, 0, 0, zl, zlo);
     }
   }
 }

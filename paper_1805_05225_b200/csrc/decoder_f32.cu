@@ -40,7 +40,9 @@ constexpr int kRedSlices = 64;  // f32_ctx_reduce1/2: row slices of the deferred
 struct FLay {
   int64_t XA, RO;  // row pitches: [att ‖ s] (E + H), readout input [s ‖ trg ‖ att] (H + Emb + E)
   float *xw, *xa, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all, *z;
-  float *dro, *dpre, *dz, *dxa, *dc, *ds, *dacc, *dctx, *dtrg;
+  float *dro, *dpre, *dxa, *dc, *ds, *dacc, *dctx, *dtrg;
+  __nv_bfloat16* dzi;  // the cell's DZ [B*T, 4H] as its split image (every consumer is a GEMM)
+  int64_t dzi_ld;
   float* w2;  // [E + H, 4H] staging of [W_att; R]
   float *datt_all, *de_all, *ds_all, *apart, *apart2;  // deferred attention accumulations (per step saves)
   int32_t* ids_tm;
@@ -98,7 +100,8 @@ FLay flayout(const DecDims& d, void* base) {
   L.z = tf(B * 4 * H);
   L.dro = tf(BT * L.RO);
   L.dpre = tf(BT * d.Rd);
-  L.dz = tf(BT * 4 * H);
+  L.dzi = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)BT, (int)(4 * H)) * 2));
+  L.dzi_ld = x3_img_ld((int)(4 * H));
   L.dxa = tf(B * L.XA);
   L.dc = tf(2 * B * H);
   L.ds = tf(B * H);
@@ -224,8 +227,15 @@ __global__ void f32_grad_in_kernel(GradIn a) {
 struct CellBF {
   int B, H, t;
   const float *ds, *gates, *c_all, *dc_in;
-  float *dz, *dc_out;
+  __nv_bfloat16* dzi;  // DZ image: hi rows at dzi (stride ld), lo rows lo elements further on
+  int64_t ld, lo;
+  float* dc_out;
 };
+__device__ __forceinline__ void put_split(__nv_bfloat16* hi, int64_t lo, float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  hi[0] = h;
+  hi[lo] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
 __global__ void f32_cell_bwd_kernel(CellBF a) {
   const int64_t n = (int64_t)a.B * a.H;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -239,11 +249,11 @@ __global__ void f32_cell_bwd_kernel(CellBF a) {
   const float d_o = gh * tc;
   const float dc = gc + gh * go * (1.f - tc * tc);
   a.dc_out[e] = dc * gf;
-  float* dz = a.dz + row * 4 * H + j;
-  dz[0] = dc * gg * gi * (1.f - gi);
-  dz[H] = dc * cp * gf * (1.f - gf);
-  dz[2 * H] = dc * gi * (1.f - gg * gg);
-  dz[3 * H] = d_o * go * (1.f - go);
+  __nv_bfloat16* dz = a.dzi + row * a.ld + j;
+  put_split(dz, a.lo, dc * gg * gi * (1.f - gi));
+  put_split(dz + H, a.lo, dc * cp * gf * (1.f - gf));
+  put_split(dz + 2 * H, a.lo, dc * gi * (1.f - gg * gg));
+  put_split(dz + 3 * H, a.lo, d_o * go * (1.f - go));
 }
 
 // d enc[b, s, :] = sum_t a_t[b, s] d att_t[b, :]  (the generic_attention adjoint w.r.t.
@@ -536,34 +546,34 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, nullptr, nullptr, L.att_ws, st);
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 12);
-      CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, L.dz,
-                L.dc + (int64_t)nxt * B * H};
+      CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, L.dzi,
+                L.dzi_ld, BT * L.dzi_ld, L.dc + (int64_t)nxt * B * H};
       f32_cell_bwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(cb);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
     }
     if (t > 0) {  // d [att ‖ s]_{t-1} = DZ_t [W_att; R]^T
       Phase q(st, "k10_g1_gemm", 2.0 * B * 4.0 * H * (E + H));
-      gemm_f32x3_pb(false, true, B, (int)L.XA, 4 * H, L.dz + (int64_t)t * B * 4 * H, 4 * H, L.wd2_b, 0.f, L.dxa,
-                    L.XA, nullptr, L.gws, st);
+      gemm_f32x3_ex(false, true, B, (int)L.XA, 4 * H, nullptr, 0, L.dzi + (int64_t)t * B * L.dzi_ld, nullptr, 0,
+                    L.wd2_b, 0.f, L.dxa, L.XA, nullptr, nullptr, 0, L.gws, st, L.dzi_ld, BT * L.dzi_ld);
     }
   }
   {
     Phase ph(st, "k10_dec_bwd_hoisted",
              2.0 * BT * 4 * H * (E + H + 2.0 * Emb) + 4.0 * BTs * E * K);
     // the cell's weight gradients over all B*T rows: [W_att; R] from [att ‖ s]_{t-1} (block t of xa)
-    gemm_f32x3(true, false, E, 4 * H, (int)BT, L.xa, L.XA, L.dz, 4 * H, 0.f, g.s_W + (int64_t)Emb * 4 * H, 4 * H,
-               nullptr, nullptr, 0, L.gws, st);
-    gemm_f32x3(true, false, H, 4 * H, (int)BT, L.xa + E, L.XA, L.dz, 4 * H, 0.f, g.s_R, 4 * H, nullptr, nullptr, 0,
-               L.gws, st);
+    gemm_f32x3_ex(true, false, E, 4 * H, (int)BT, L.xa, L.XA, nullptr, nullptr, 0, L.dzi, 0.f,
+                  g.s_W + (int64_t)Emb * 4 * H, 4 * H, nullptr, nullptr, 0, L.gws, st);
+    gemm_f32x3_ex(true, false, H, 4 * H, (int)BT, L.xa + E, L.XA, nullptr, nullptr, 0, L.dzi, 0.f, g.s_R, 4 * H,
+                  nullptr, nullptr, 0, L.gws, st);
     // [W_trg; b] from [trg_{t-1} | 1]
-    gemm_f32x3(true, false, Emb, 4 * H, (int)BT, L.ro + H, L.RO, L.dz, 4 * H, 0.f, g.s_W, 4 * H, nullptr, g.s_b,
-               4 * H, L.gws, st);
+    gemm_f32x3_ex(true, false, Emb, 4 * H, (int)BT, L.ro + H, L.RO, nullptr, nullptr, 0, L.dzi, 0.f, g.s_W, 4 * H,
+                  nullptr, g.s_b, 4 * H, L.gws, st);
     // d trg_{t-1} = DZ W_trg^T + the readout's trg columns -> the trg table
     SL_CUDA_TRY(cudaMemcpy2DAsync(L.dtrg, (size_t)Emb * 4, L.dro + H, L.RO * 4, (size_t)Emb * 4, BT,
                                   cudaMemcpyDeviceToDevice, st));
-    gemm_f32x3(false, true, (int)BT, Emb, 4 * H, L.dz, 4 * H, p.s_W, 4 * H, 1.f, L.dtrg, Emb, nullptr, nullptr, 0,
-               L.gws, st);
+    gemm_f32x3_ex(false, true, (int)BT, Emb, 4 * H, nullptr, 0, L.dzi, p.s_W, 4 * H, nullptr, 1.f, L.dtrg, Emb,
+                  nullptr, nullptr, 0, L.gws, st);
     embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
     // the attention's accumulations over t (deferred out of the loop)
     {

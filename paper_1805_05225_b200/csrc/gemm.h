@@ -26,6 +26,14 @@ void x3_split_img(const float* S, int64_t ld, int rows, int cols, __nv_bfloat16*
 // scratch: gemm_f32x3_workspace_bytes of the same shape).
 size_t x3_b_elems(bool transB, int N, int K);
 void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfloat16* B3, cudaStream_t st);
+// the general form: each operand either fp32 (split here) or a pre-split image (A3 /
+// B3 non-null: the fp32 pointer is then unused).  An image's hi part is at A3 with
+// row stride a3_ld and its lo part a3_lo elements further on (0: the x3_split_img
+// layout of the stored operand).  ones_row_out needs A split here.
+void gemm_f32x3_ex(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                   const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, float beta,
+                   float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
+                   cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0);
 // both operands pre-split (images of the stored A and B)
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
                     const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,

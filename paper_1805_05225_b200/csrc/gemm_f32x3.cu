@@ -163,7 +163,7 @@ namespace {
 void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
              const __nv_bfloat16* a_pre, const float* B, int64_t ldb, const __nv_bfloat16* b_pre, float beta,
              float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
-             cudaStream_t st) {
+             cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0) {
   if (M <= 0 || N <= 0) return;
   const bool a_ones = ones_row_out != nullptr;
   SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
@@ -184,10 +184,12 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
     b3 = b3w;
   }
   w += round_up(x3_img_elems((int)d.b_rows, (int)d.b_cols) * 2, 256);
-  const int64_t a_ld = x3_img_ld((int)d.a_cols), b_ld = x3_img_ld((int)d.b_cols);
+  // (a caller's image may carry its own stride and lo offset)
+  const int64_t a_ld = a_pre && a3_ld ? a3_ld : x3_img_ld((int)d.a_cols);
+  const int64_t b_ld = b_pre && b3_ld ? b3_ld : x3_img_ld((int)d.b_cols);
   TcGemm g{M + (a_ones ? 1 : 0), N, K, a3, a_ld, transA, b3, b_ld, !transB, C, ldc, 1.f, beta, bias};
-  g.A_lo = a3 + d.a_rows * a_ld;
-  g.B_lo = b3 + d.b_rows * b_ld;
+  g.A_lo = a3 + (a_pre && a3_lo ? a3_lo : d.a_rows * a_ld);
+  g.B_lo = b3 + (b_pre && b3_lo ? b3_lo : d.b_rows * b_ld);
   {  // chunked accumulation only where one work unit's K range is longer than a chunk
     const int64_t nk = ceil_div(K, 64);
     if (ceil_div(nk, d.ksplit) > kX3ChunkBlocks) g.kchunk = kX3ChunkBlocks;
@@ -229,6 +231,14 @@ void gemm_f32x3_pb(bool transA, bool transB, int M, int N, int K, const float* A
                    cudaStream_t st, float* ones_row_out, int64_t ld_ones) {
   x3_core(transA, transB, M, N, K, A, lda, nullptr, nullptr, 0, B3, beta, C, ldc, bias, ones_row_out, ld_ones, ws,
           st);
+}
+
+void gemm_f32x3_ex(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                   const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, float beta,
+                   float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
+                   cudaStream_t st, int64_t a3_ld, int64_t a3_lo, int64_t b3_ld, int64_t b3_lo) {
+  x3_core(transA, transB, M, N, K, A, lda, A3, B, ldb, B3, beta, C, ldc, bias, ones_row_out, ld_ones, ws, st, a3_ld,
+          a3_lo, b3_ld, b3_lo);
 }
 
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,

@@ -101,7 +101,10 @@ struct TcRecBwdArgs {
   const float* gatesf[2];          // saved (i,f,g,o) fp32 (K2 x3), step-major
   const float* cprevf[2];          // saved c_{s-1} fp32, step-major
   __nv_bfloat16* dzring_lo[2];     // lo halves of DZ (DZ - bf16(DZ)), dzring layout, zeroed
-  float* dzcatf;                   // out: DZ fp32 [B*T, dzcat_ld], dir (dir0 + d) at col (dir0 + d)*dz_dir_off
+  // out: DZ's split image (gemm.h x3_split_img layout): hi [B*T, dzcat_ld] at dzimg, lo
+  // dzimg_rows * dzcat_ld elements further on; dir (dir0 + d) at col (dir0 + d)*dz_dir_off
+  __nv_bfloat16* dzimg;
+  int64_t dzimg_rows;
 };
 
 // K-split partition of the BPTT kernel: clusters of C CTAs, each finalizing U

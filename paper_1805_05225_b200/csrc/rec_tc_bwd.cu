@@ -527,10 +527,17 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                                        kEpiTile);
       }
       if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
-        if constexpr (X3) {
-          float* zc = a.dzcatf + pos * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
+        if constexpr (X3) {  // the split image the K4 GEMMs read: hi and lo
+          __nv_bfloat16* zh = a.dzimg + pos * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
+          __nv_bfloat16* zl = zh + a.dzimg_rows * a.dzcat_ld;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) store_f32<UT>(zc + g * H, dzs + g * UT, nu);
+          for (int g = 0; g < 4; ++g) {
+            float l[UT];
+#pragma unroll
+            for (int u = 0; u < UT; ++u) l[u] = dzs[g * UT + u] - __bfloat162float(__float2bfloat16_rn(dzs[g * UT + u]));
+            store_bf16<UT>(zh + g * H, dzs + g * UT, nu);
+            store_bf16<UT>(zl + g * H, l, nu);
+          }
         } else {
           __nv_bfloat16* zc = a.dzcat + pos * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;
 #pragma unroll
@@ -544,9 +551,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       for (int u = 0; u < UT; ++u) zero[u] = 0.f;
       for (int s = Tmax; s < T; ++s) {
         if constexpr (X3) {
-          float* zc = a.dzcatf + ((size_t)row * T + s) * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
+          __nv_bfloat16* zh = a.dzimg + ((size_t)row * T + s) * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) store_f32<UT>(zc + g * H, zero, nu);
+          for (int g = 0; g < 4; ++g) {
+            store_bf16<UT>(zh + g * H, zero, nu);
+            store_bf16<UT>(zh + a.dzimg_rows * a.dzcat_ld + g * H, zero, nu);
+          }
         } else {
           __nv_bfloat16* zc =
               a.dzcat + ((size_t)row * T + s) * a.dzcat_ld + (size_t)d * a.dz_dir_off + ut0;

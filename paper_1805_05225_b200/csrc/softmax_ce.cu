@@ -130,18 +130,41 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(__nv_bfloat16* __restrict_
 // fp32-class variant (SL_PREC_FP32): one warp per row of fp32 logits Z: an online
 // (max, sum exp) pass with sum z and z_y, lse = m + log(s), then Z -> dZ in place.
 // Reference arithmetic: expf / logf (tape.cpp:879-924, 1224-1298).
-__global__ void __launch_bounds__(256) ce_rows_f32_kernel(float* __restrict__ Z, int64_t ldz, int rows, int T,
+// dZ goes to its split-bf16 image (gemm.h x3_split_img layout: hi [rows, ldi], then
+// lo; the padding columns zero), which both gradient GEMMs read — dZ is never
+// written as fp32 and never split separately.
+__device__ __forceinline__ void dz_store4(__nv_bfloat16* hi, __nv_bfloat16* lo, int64_t off, const float (&g)[4]) {
+  __align__(8) __nv_bfloat16 h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    h[k] = __float2bfloat16_rn(g[k]);
+    l[k] = __float2bfloat16_rn(g[k] - __bfloat162float(h[k]));
+  }
+  *reinterpret_cast<uint2*>(hi + off) = *reinterpret_cast<const uint2*>(h);
+  *reinterpret_cast<uint2*>(lo + off) = *reinterpret_cast<const uint2*>(l);
+}
+__device__ __forceinline__ void dz_store1(__nv_bfloat16* hi, __nv_bfloat16* lo, int64_t off, float g) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(g);
+  hi[off] = h;
+  lo[off] = __float2bfloat16_rn(g - __bfloat162float(h));
+}
+
+__global__ void __launch_bounds__(256) ce_rows_f32_kernel(const float* __restrict__ Z, int64_t ldz, int rows, int T,
                                                           int V, const int32_t* __restrict__ targets,
                                                           const int32_t* __restrict__ lens, float eps, CeScratch* sc,
-                                                          int* bad_target) {
+                                                          int* bad_target, __nv_bfloat16* __restrict__ dzi,
+                                                          int64_t ldi) {
   const int lane = threadIdx.x % 32;
   const int row = blockIdx.x * 8 + threadIdx.x / 32;
   if (row >= rows) return;
   const int b = row / T, t = row % T;
-  float* z = Z + (int64_t)row * ldz;
-  const bool vec = (V % 4) == 0 && (ldz % 4) == 0;
+  const float* z = Z + (int64_t)row * ldz;
+  __nv_bfloat16* hi = dzi + (int64_t)row * ldi;
+  __nv_bfloat16* lo = dzi + ((int64_t)rows + row) * ldi;
+  const bool vec = (V % 4) == 0 && (ldz % 4) == 0 && (ldi % 4) == 0;
+  for (int j = V + lane; j < ldi; j += 32) dz_store1(hi, lo, j, 0.f);  // padding
   if (t >= lens[b]) {  // masked position (tape.cpp:1256-1262): no loss, zero gradient
-    for (int j = lane; j < V; j += 32) z[j] = 0.f;
+    for (int j = lane; j < V; j += 32) dz_store1(hi, lo, j, 0.f);
     return;
   }
   const int y = targets[row];
@@ -150,7 +173,7 @@ __global__ void __launch_bounds__(256) ce_rows_f32_kernel(float* __restrict__ Z,
       atomicMax(bad_target, 1);
       atomicAdd(&sc->loss_sum, (double)__int_as_float(0x7fc00000));
     }
-    for (int j = lane; j < V; j += 32) z[j] = __int_as_float(0x7fc00000);
+    for (int j = lane; j < V; j += 32) dz_store1(hi, lo, j, __int_as_float(0x7fc00000));
     return;
   }
   float m = -INFINITY, s = 0.f, tz = 0.f;
@@ -191,15 +214,17 @@ __global__ void __launch_bounds__(256) ce_rows_f32_kernel(float* __restrict__ Z,
       float4 q = *reinterpret_cast<const float4*>(z + j);
       float g[4] = {expf(q.x - lse) + base, expf(q.y - lse) + base, expf(q.z - lse) + base, expf(q.w - lse) + base};
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 4; ++k) {
         if (j + k == y) g[k] -= 1.f - eps;
-      *reinterpret_cast<float4*>(z + j) = make_float4(g[0] * inv_n, g[1] * inv_n, g[2] * inv_n, g[3] * inv_n);
+        g[k] *= inv_n;
+      }
+      dz_store4(hi, lo, j, g);
     }
   } else {
     for (int j = lane; j < V; j += 32) {
       float g = expf(z[j] - lse) + base;
       if (j == y) g -= 1.f - eps;
-      z[j] = g * inv_n;
+      dz_store1(hi, lo, j, g * inv_n);
     }
   }
 }
@@ -290,7 +315,8 @@ size_t output_ce_f32_workspace_bytes(int B, int T, int D, int V) {
   const size_t x3 = std::max({gemm_f32x3_workspace_bytes(false, false, (int)rows, V, D, false),   // logits
                               gemm_f32x3_workspace_bytes(false, true, (int)rows, D, V, false),    // dX
                               gemm_f32x3_workspace_bytes(true, false, D, V, (int)rows, true)});   // [dW; db]
-  return (size_t)round_up(rows * V * 4, 256) + (size_t)round_up(sizeof(CeScratch), 256) + x3;
+  return (size_t)round_up(rows * V * 4, 256) + (size_t)round_up(x3_img_elems((int)rows, V) * 2, 256) +
+         (size_t)round_up(sizeof(CeScratch), 256) + x3;
 }
 
 void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* targets, const int32_t* lens,
@@ -299,8 +325,11 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   const int64_t rows = (int64_t)B * T;
   char* w = static_cast<char*>(workspace);
   float* z = reinterpret_cast<float*>(w);
-  auto* sc = reinterpret_cast<CeScratch*>(w + round_up(rows * V * 4, 256));
-  void* gws = w + round_up(rows * V * 4, 256) + round_up(sizeof(CeScratch), 256);
+  w += round_up(rows * V * 4, 256);
+  auto* dzi = reinterpret_cast<__nv_bfloat16*>(w);  // the split image of dZ
+  w += round_up(x3_img_elems((int)rows, V) * 2, 256);
+  auto* sc = reinterpret_cast<CeScratch*>(w);
+  void* gws = w + round_up(sizeof(CeScratch), 256);
   SL_CUDA_TRY(cudaMemsetAsync(bad_target, 0, sizeof(int), stream));
   ce_count_kernel<<<1, 256, 0, stream>>>(lens, B, T, sc);
   SL_CUDA_TRY(cudaGetLastError());
@@ -313,7 +342,7 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   {
     Phase ph(stream, "k7_softmax_ce", 0.0, 12.0 * rows * V);
     ce_rows_f32_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, stream>>>(z, V, (int)rows, T, V, targets, lens, eps,
-                                                                         sc, bad_target);
+                                                                         sc, bad_target, dzi, x3_img_ld(V));
     SL_CUDA_TRY(cudaGetLastError());
     ce_finalize_kernel<<<1, 1, 0, stream>>>(sc, loss_out);
     SL_CUDA_TRY(cudaGetLastError());
@@ -322,11 +351,13 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   const float beta = accumulate ? 1.f : 0.f;
   if (dx) {
     Phase ph(stream, "k7_dx_gemm", f);
-    gemm_f32x3(false, true, (int)rows, D, V, z, V, W, V, beta, dx, D, nullptr, nullptr, 0, gws, stream);
+    gemm_f32x3_ex(false, true, (int)rows, D, V, nullptr, 0, dzi, W, V, nullptr, beta, dx, D, nullptr, nullptr, 0,
+                  gws, stream);
   }
   if (dW) {
     Phase ph(stream, "k7_dw_gemm", f);
-    gemm_f32x3(true, false, D, V, (int)rows, x, D, z, V, beta, dW, V, nullptr, db, V, gws, stream);
+    gemm_f32x3_ex(true, false, D, V, (int)rows, x, D, nullptr, nullptr, 0, dzi, beta, dW, V, nullptr, db, V, gws,
+                  stream);
   } else if (db) {
     SL_REQUIRE(false, SL_ERR_INVALID_ARGUMENT, "output_ce (fp32): db needs dW");
   }
