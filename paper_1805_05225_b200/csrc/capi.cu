@@ -112,7 +112,15 @@ struct ReserveView {
   __nv_bfloat16* gatesb[2] = {nullptr, nullptr};  // bf16 path: saved (i,f,g,o), step-major (rec_tc.h)
   __nv_bfloat16* cprevb[2] = {nullptr, nullptr};  // bf16 path: saved c_{s-1}, step-major
   __nv_bfloat16* rt[2] = {nullptr, nullptr};      // bf16 path: packed R^T slices
+  __nv_bfloat16* wimg = nullptr;  // x3 path: split image of [W_fw | W_bw] [D, nd*4H] (K1 and K4-dX)
+  __nv_bfloat16* ximg = nullptr;  // x3 path: split image of [X | 1] [B*T, D + 1] (K1 and K4-dW)
 };
+
+// x3 operand images kept from the forward for the backward (gemm.h x3_split_into)
+int64_t wimg_ld(const Dims& d) { return x3_img_ld(d.nd * 4 * d.H); }
+int64_t ximg_ld(const Dims& d) { return x3_img_ld(d.D + 1); }
+size_t wimg_elems(const Dims& d) { return (size_t)2 * d.D * wimg_ld(d); }
+size_t ximg_elems(const Dims& d) { return (size_t)2 * d.BT() * ximg_ld(d); }
 
 int sm_count() {
   static int n = 0;
@@ -157,6 +165,10 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
       r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
     }
   }
+  if (use_x3(d, prec)) {
+    r.wimg = c.take<__nv_bfloat16>(wimg_elems(d));
+    r.ximg = c.take<__nv_bfloat16>(ximg_elems(d));
+  }
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
     const TcFwdShape sh = tc_rec_fwd_shape(d.H, d.nd, sm_count());
@@ -185,7 +197,8 @@ struct FwdWork {
   __nv_bfloat16* hbufb[2] = {nullptr, nullptr};  // bf16 path: h ring [2][B][Kp]
   __nv_bfloat16* hbuflo[2] = {nullptr, nullptr};  // x3 path: lo halves of h, same ring layout
   __nv_bfloat16* rtx3[2] = {nullptr, nullptr};    // x3 path: packed R^T hi + lo
-  float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
+  __nv_bfloat16* wimg = nullptr;                  // x3 path without a reserve: the K1 operand images
+  __nv_bfloat16* ximg = nullptr;
   void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
   unsigned* bar = nullptr;
 };
@@ -214,7 +227,8 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
     float* xw = c.take<float>((size_t)d.BT() * w.xw_ld);
     for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * g4(d) : nullptr;
     w.bcat = c.take<float>((size_t)w.xw_ld);
-    w.wcatf = c.take<float>((size_t)d.D * w.xw_ld);
+    w.wimg = c.take<__nv_bfloat16>(wimg_elems(d));
+    w.ximg = c.take<__nv_bfloat16>(ximg_elems(d));
     w.gws = c.take<char>(x3_gemm_ws(d, false));
     for (int k = 0; k < d.nd; ++k) {
       w.rtx3[k] = c.take<__nv_bfloat16>(tc_rec_x3_pack_elems(sh));
@@ -242,7 +256,6 @@ struct BwdWork {
   __nv_bfloat16* rb[2] = {nullptr, nullptr};      // bf16 path: packed R row slices
   __nv_bfloat16* dzringlo[2] = {nullptr, nullptr};  // x3 path: lo halves of DZ, same ring layout
   __nv_bfloat16* dzi = nullptr;  // x3 path: DZ of both directions as its split image (hi, lo) [B*T, dzi_ld]
-  float* wcatf = nullptr;                         // x3 path: [W_fw | W_bw] fp32 [D, nd*4H]
   void* gws = nullptr;                            // x3 path: split-bf16 GEMM scratch
   unsigned* bar = nullptr;
 };
@@ -263,7 +276,6 @@ BwdWork carve_bwd(const Dims& d, int prec, void* p, size_t* bytes) {
   } else if (use_x3(d, prec)) {
     const TcBwdShape sh = tc_rec_bwd_x3_shape(d.H, sm_count(), d.nd);
     w.dzi = c.take<__nv_bfloat16>((size_t)2 * d.BT() * dzi_ld(d));
-    w.wcatf = c.take<float>((size_t)d.D * d.nd * g4(d));
     w.gws = c.take<char>(x3_gemm_ws(d, true));
     for (int k = 0; k < d.nd; ++k) {
       w.dzring[k] = c.take<__nv_bfloat16>((size_t)2 * dz_ring_bp(d.B) * sh.Kz);
@@ -306,15 +318,20 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
             const float* const* R, const float* const* b, float* y, float* h_last, float* c_last,
             const ReserveView& rv, const FwdWork& w, cudaStream_t st) {
   const int64_t G = g4(d), Gc = d.nd * G;
+  // the split images of [W_fw | W_bw] (each direction straight into its column block)
+  // and of [X | 1]; with a reserve they stay there for the backward's dX and dW GEMMs
+  __nv_bfloat16* wi = rv.wimg ? rv.wimg : w.wimg;
+  __nv_bfloat16* xi = rv.ximg ? rv.ximg : w.ximg;
+  const int64_t wl = wimg_ld(d), xl = ximg_ld(d), M = d.BT();
   for (int k = 0; k < d.nd; ++k) {
-    SL_CUDA_TRY(cudaMemcpy2DAsync(w.wcatf + k * G, Gc * sizeof(float), W[k], G * sizeof(float),
-                                  G * sizeof(float), d.D, cudaMemcpyDeviceToDevice, st));
+    x3_split_into(W[k], G, d.D, (int)G, -1, wi + k * G, wl, G, (int64_t)d.D * wl, st);
     SL_CUDA_TRY(cudaMemcpyAsync(w.bcat + k * G, b[k], G * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
+  x3_split_into(x, d.D, (int)M, d.D, d.D, xi, xl, xl, M * xl, st);
   {
     Phase ph(st, "k1_xw_gemm", 2.0 * d.BT() * d.D * (double)Gc);
-    gemm_f32x3(false, false, (int)d.BT(), (int)Gc, d.D, x, d.D, w.wcatf, Gc, 0.f, w.xw[0], Gc, w.bcat, nullptr, 0,
-               w.gws, st);
+    gemm_f32x3_ex(false, false, (int)M, (int)Gc, d.D, nullptr, 0, xi, nullptr, 0, wi, 0.f, w.xw[0], Gc, w.bcat,
+                  nullptr, 0, w.gws, st, xl, M * xl, wl, (int64_t)d.D * wl);
   }
   const TcFwdShape sh = tc_rec_fwd_x3_shape(d.H, sm_count(), d.nd);
   const int per_launch = sh.pair == 2 ? d.nd : 1;  // both directions at once, or one per launch
@@ -399,13 +416,11 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     Phase ph(st, "k3_rec_bwd", 2.0 * d.BT() * d.H * 4.0 * d.H * per_launch);
     rec_bwd_x3(a, sh, rb, st);
   }
-  if (dx) {
-    for (int k = 0; k < d.nd; ++k)
-      SL_CUDA_TRY(cudaMemcpy2DAsync(w.wcatf + k * G, Gc * sizeof(float), W[k], G * sizeof(float),
-                                    G * sizeof(float), d.D, cudaMemcpyDeviceToDevice, st));
+  const int64_t wl = wimg_ld(d), xl = ximg_ld(d);
+  if (dx) {  // dX = DZ [W_fw | W_bw]^T from the forward's image of the weights
     Phase ph(st, "k4_dx_gemm", 2.0 * M * (double)Gc * d.D);
-    gemm_f32x3_ex(false, true, M, d.D, (int)Gc, nullptr, 0, w.dzi, w.wcatf, Gc, nullptr, beta, dx, d.D, nullptr,
-                  nullptr, 0, w.gws, st, dzi_ld(d), (int64_t)M * dzi_ld(d));
+    gemm_f32x3_ex(false, true, M, d.D, (int)Gc, nullptr, 0, w.dzi, nullptr, 0, rv.wimg, beta, dx, d.D, nullptr,
+                  nullptr, 0, w.gws, st, dzi_ld(d), (int64_t)M * dzi_ld(d), wl, (int64_t)d.D * wl);
   }
   // the weight gradients read direction k's column slice of the same DZ image
   const int64_t zl = dzi_ld(d), zlo = (int64_t)M * zl;
@@ -416,8 +431,8 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     if (want_w || dbk) {
       Phase ph(st, "k4_dw_gemm", 2.0 * M * (double)G * d.D);
       if (want_w) {
-        gemm_f32x3_ex(true, false, d.D, (int)G, M, x, d.D, nullptr, nullptr, 0, zk, beta, dW[k], G, nullptr, dbk, G,
-                      w.gws, st, 0, 0, zl, zlo);
+        gemm_f32x3_ex(true, false, d.D, (int)G, M, nullptr, 0, rv.ximg, nullptr, 0, zk, beta, dW[k], G, nullptr,
+                      dbk, G, w.gws, st, xl, (int64_t)M * xl, zl, zlo);
       } else {  // db alone: fixed-order column sums of DZ_d (hi + lo)
         colsum_img_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, zk, zl, zlo, beta, dbk);
         SL_CUDA_TRY(cudaGetLastError());

@@ -21,6 +21,11 @@ size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K,
 int64_t x3_img_ld(int cols);
 size_t x3_img_elems(int rows, int cols);
 void x3_split_img(const float* S, int64_t ld, int rows, int cols, __nv_bfloat16* img, cudaStream_t st);
+// the same into a window of a caller's image: hi rows at img (stride img_ld), lo rows
+// lo_off elements further on, img_cols (a multiple of 8) columns written per row —
+// the columns past `cols` as 0, except ones_col (>= 0): 1 in hi, 0 in lo
+void x3_split_into(const float* S, int64_t ld, int rows, int cols, int ones_col, __nv_bfloat16* img, int64_t img_ld,
+                   int64_t img_cols, int64_t lo_off, cudaStream_t st);
 // B split once for repeated GEMMs (e.g. a weight used every time step): the image of
 // the stored B (x3_b_elems elements); gemm_f32x3_pb then splits only A per call (its
 // scratch: gemm_f32x3_workspace_bytes of the same shape).
@@ -29,7 +34,8 @@ void x3_split_b(bool transB, int N, int K, const float* B, int64_t ldb, __nv_bfl
 // the general form: each operand either fp32 (split here) or a pre-split image (A3 /
 // B3 non-null: the fp32 pointer is then unused).  An image's hi part is at A3 with
 // row stride a3_ld and its lo part a3_lo elements further on (0: the x3_split_img
-// layout of the stored operand).  ones_row_out needs A split here.
+// layout of the stored operand).  With ones_row_out and a pre-split A (stored [K, M]),
+// the image must hold the ones column at column M (x3_split_into ones_col = M).
 void gemm_f32x3_ex(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
                    const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, float beta,
                    float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,

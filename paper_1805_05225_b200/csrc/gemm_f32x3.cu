@@ -20,15 +20,16 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
-// S [rows, cols] (ld) -> hi [rows, dld] and lo [rows, dld] at D and D + rows * dld;
-// columns >= cols are 0, except ones_col (if >= 0): 1 (hi) / 0 (lo).
-// Eight columns per thread (16 B stores), grid-stride over rows.
-template <bool V4>
+// S [rows, cols] (ld) -> hi rows at D (stride dld) and lo rows lo_off elements further
+// on; the first dcols (a multiple of 8) columns of each row are written, columns >= cols
+// as 0 except ones_col (if >= 0): 1 (hi) / 0 (lo).  Eight columns per thread (16 B
+// stores), grid-stride over rows.
+template <bool V4, bool A16>
 __global__ void split2_kernel(const float* __restrict__ S, int64_t ld, int rows, int cols, int ones_col,
-                              __nv_bfloat16* __restrict__ D, int64_t dld) {
+                              __nv_bfloat16* __restrict__ D, int64_t dld, int64_t dcols, int64_t lo_off) {
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c >= dld) return;
-  __nv_bfloat16* lo_base = D + (int64_t)rows * dld;
+  if (c >= dcols) return;
+  __nv_bfloat16* lo_base = D + lo_off;
   for (int r = blockIdx.y; r < rows; r += gridDim.y) {  // (grid y is capped at 65535)
     const float* src = S + (int64_t)r * ld;
     float x[8];
@@ -50,8 +51,14 @@ __global__ void split2_kernel(const float* __restrict__ S, int64_t ld, int rows,
       h[ones_col - c] = __float2bfloat16_rn(1.f);
       l[ones_col - c] = __float2bfloat16_rn(0.f);
     }
-    *reinterpret_cast<uint4*>(D + (int64_t)r * dld + c) = *reinterpret_cast<const uint4*>(h);
-    *reinterpret_cast<uint4*>(lo_base + (int64_t)r * dld + c) = *reinterpret_cast<const uint4*>(l);
+    if (A16) {
+      *reinterpret_cast<uint4*>(D + (int64_t)r * dld + c) = *reinterpret_cast<const uint4*>(h);
+      *reinterpret_cast<uint4*>(lo_base + (int64_t)r * dld + c) = *reinterpret_cast<const uint4*>(l);
+    } else {  // a window at an unaligned column offset
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c + i < dcols) D[(int64_t)r * dld + c + i] = h[i], lo_base[(int64_t)r * dld + c + i] = l[i];
+    }
   }
 }
 
@@ -121,16 +128,21 @@ X3Dims x3_dims(bool transA, bool transB, int M, int N, int K, bool a_ones) {
   return d;
 }
 
-void split_img(const float* S, int64_t ld, int rows, int cols, int ones_col, __nv_bfloat16* D, cudaStream_t st) {
+void split_into(const float* S, int64_t ld, int rows, int cols, int ones_col, __nv_bfloat16* D, int64_t dld,
+                int64_t dcols, int64_t lo_off, cudaStream_t st) {
   if (rows <= 0) return;
-  const int cols_ext = cols + (ones_col >= 0 ? 1 : 0);
-  const int64_t dld = x3_img_ld(cols_ext);
-  const dim3 grid((unsigned)ceil_div(dld, 8 * 128), (unsigned)std::min(rows, 65535));
+  const dim3 grid((unsigned)ceil_div(dcols, 8 * 128), (unsigned)std::min(rows, 65535));
   const bool v4 = (ld % 4) == 0 && ((uintptr_t)S & 15) == 0;
-  if (v4) split2_kernel<true><<<grid, 128, 0, st>>>(S, ld, rows, cols, ones_col, D, dld);
-  else split2_kernel<false><<<grid, 128, 0, st>>>(S, ld, rows, cols, ones_col, D, dld);
+  const bool a16 = dcols % 8 == 0 && dld % 8 == 0 && lo_off % 8 == 0 && ((uintptr_t)D & 15) == 0;
+  if (v4 && a16) split2_kernel<true, true><<<grid, 128, 0, st>>>(S, ld, rows, cols, ones_col, D, dld, dcols, lo_off);
+  else if (a16) split2_kernel<false, true><<<grid, 128, 0, st>>>(S, ld, rows, cols, ones_col, D, dld, dcols, lo_off);
+  else split2_kernel<false, false><<<grid, 128, 0, st>>>(S, ld, rows, cols, ones_col, D, dld, dcols, lo_off);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
+}
+void split_img(const float* S, int64_t ld, int rows, int cols, int ones_col, __nv_bfloat16* D, cudaStream_t st) {
+  const int64_t dld = x3_img_ld(cols + (ones_col >= 0 ? 1 : 0));
+  split_into(S, ld, rows, cols, ones_col, D, dld, dld, (int64_t)rows * dld, st);
 }
 
 }  // namespace
@@ -139,6 +151,10 @@ int64_t x3_img_ld(int cols) { return round_up((int64_t)cols, 64); }
 size_t x3_img_elems(int rows, int cols) { return (size_t)2 * rows * x3_img_ld(cols); }
 void x3_split_img(const float* S, int64_t ld, int rows, int cols, __nv_bfloat16* img, cudaStream_t st) {
   split_img(S, ld, rows, cols, -1, img, st);
+}
+void x3_split_into(const float* S, int64_t ld, int rows, int cols, int ones_col, __nv_bfloat16* img, int64_t img_ld,
+                   int64_t img_cols, int64_t lo_off, cudaStream_t st) {
+  split_into(S, ld, rows, cols, ones_col, img, img_ld, img_cols, lo_off, st);
 }
 
 size_t gemm_f32x3_workspace_bytes(bool transA, bool transB, int M, int N, int K, bool a_ones) {
@@ -167,7 +183,7 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
   if (M <= 0 || N <= 0) return;
   const bool a_ones = ones_row_out != nullptr;
   SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
-  SL_REQUIRE(!a_ones || !a_pre, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A split here");
+
   const X3Dims d = x3_dims(transA, transB, M, N, K, a_ones);
   char* w = static_cast<char*>(ws);
   const __nv_bfloat16* a3 = a_pre;

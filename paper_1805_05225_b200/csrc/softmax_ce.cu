@@ -133,16 +133,6 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(__nv_bfloat16* __restrict_
 // dZ goes to its split-bf16 image (gemm.h x3_split_img layout: hi [rows, ldi], then
 // lo; the padding columns zero), which both gradient GEMMs read — dZ is never
 // written as fp32 and never split separately.
-__device__ __forceinline__ void dz_store4(__nv_bfloat16* hi, __nv_bfloat16* lo, int64_t off, const float (&g)[4]) {
-  __align__(8) __nv_bfloat16 h[4], l[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    h[k] = __float2bfloat16_rn(g[k]);
-    l[k] = __float2bfloat16_rn(g[k] - __bfloat162float(h[k]));
-  }
-  *reinterpret_cast<uint2*>(hi + off) = *reinterpret_cast<const uint2*>(h);
-  *reinterpret_cast<uint2*>(lo + off) = *reinterpret_cast<const uint2*>(l);
-}
 __device__ __forceinline__ void dz_store1(__nv_bfloat16* hi, __nv_bfloat16* lo, int64_t off, float g) {
   const __nv_bfloat16 h = __float2bfloat16_rn(g);
   hi[off] = h;
@@ -161,7 +151,7 @@ __global__ void __launch_bounds__(256) ce_rows_f32_kernel(const float* __restric
   const float* z = Z + (int64_t)row * ldz;
   __nv_bfloat16* hi = dzi + (int64_t)row * ldi;
   __nv_bfloat16* lo = dzi + ((int64_t)rows + row) * ldi;
-  const bool vec = (V % 4) == 0 && (ldz % 4) == 0 && (ldi % 4) == 0;
+  const bool vec = (V % 8) == 0 && (ldz % 4) == 0 && (ldi % 8) == 0;
   for (int j = V + lane; j < ldi; j += 32) dz_store1(hi, lo, j, 0.f);  // padding
   if (t >= lens[b]) {  // masked position (tape.cpp:1256-1262): no loss, zero gradient
     for (int j = lane; j < V; j += 32) dz_store1(hi, lo, j, 0.f);
@@ -209,16 +199,21 @@ __global__ void __launch_bounds__(256) ce_rows_f32_kernel(const float* __restric
   const float inv_n = 1.f / (float)max(sc->n_valid, 1);
   const float base = -eps / (float)V;
   __syncwarp();
-  if (vec) {
-    for (int j = lane * 4; j < V; j += 128) {
-      float4 q = *reinterpret_cast<const float4*>(z + j);
-      float g[4] = {expf(q.x - lse) + base, expf(q.y - lse) + base, expf(q.z - lse) + base, expf(q.w - lse) + base};
+  if (vec) {  // 8 columns per lane: 16 B image stores
+    for (int j = lane * 8; j < V; j += 256) {
+      const float4 q0 = *reinterpret_cast<const float4*>(z + j), q1 = *reinterpret_cast<const float4*>(z + j + 4);
+      const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      __align__(16) __nv_bfloat16 h[8], l[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (j + k == y) g[k] -= 1.f - eps;
-        g[k] *= inv_n;
+      for (int k = 0; k < 8; ++k) {
+        float g = expf(q[k] - lse) + base;
+        if (j + k == y) g -= 1.f - eps;
+        g *= inv_n;
+        h[k] = __float2bfloat16_rn(g);
+        l[k] = __float2bfloat16_rn(g - __bfloat162float(h[k]));
       }
-      dz_store4(hi, lo, j, g);
+      *reinterpret_cast<uint4*>(hi + j) = *reinterpret_cast<const uint4*>(h);
+      *reinterpret_cast<uint4*>(lo + j) = *reinterpret_cast<const uint4*>(l);
     }
   } else {
     for (int j = lane; j < V; j += 32) {
