@@ -443,9 +443,16 @@ __host__ __device__ inline ClSmem cl_smem(int K, int Ts) {
   return m;
 }
 
-__device__ __forceinline__ void cl_stage_cols(const AttnArgs& p, int b, float* sh, const ClSmem& m) {
+__device__ __forceinline__ void cl_stage_cols(const AttnArgs& p, int b, float* sh, const ClSmem& m, int r) {
   for (int k = threadIdx.x; k < p.K; k += kClThreads) {
-    sh[m.c + k] = p.s_tr[(size_t)b * p.K + k] + p.b_fb[k];
+    float str;
+    if (p.s_tr_parts.n > 0) {  // s_tr = s W_s + b_s from the projection's split-K partials
+      str = x3_parts_sum(p.s_tr_parts, b, k) + p.s_tr_bias[k];
+      if (r == 0) p.s_tr[(size_t)b * p.K + k] = str;
+    } else {
+      str = p.s_tr[(size_t)b * p.K + k];
+    }
+    sh[m.c + k] = str + p.b_fb[k];
     sh[m.w + k] = p.W_fb[k];
     sh[m.v + k] = p.v[k];
   }
@@ -460,7 +467,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int len = min(max(p.lens[b], 0), Ts);
   const ClSmem m = cl_smem(K, Ts);
-  cl_stage_cols(p, b, sh, m);
+  cl_stage_cols(p, b, sh, m, r);
   __syncthreads();
   // energies of positions j = r + kCl (warp + kClWarps i)
   for (int j = r + kCl * warp; j < len; j += kCl * kClWarps) {
@@ -540,6 +547,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
         if (p.att_copy[c]) *reinterpret_cast<float4*>(p.att_copy[c] + (size_t)b * p.att_copy_ld[c] + x) = acc;
+      if (p.att_img) {
+        const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+        __align__(8) __nv_bfloat16 h[4], l[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          h[i] = __float2bfloat16_rn(v[i]);
+          l[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
+        }
+        __nv_bfloat16* dst = p.att_img + (size_t)b * p.att_img_ld + x;
+        *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
+        *reinterpret_cast<uint2*>(dst + p.att_img_lo) = *reinterpret_cast<const uint2*>(l);
+      }
     }
     __syncthreads();
   }
@@ -560,7 +579,9 @@ __global__ void colsum_kernel(const float* x, int rows, int cols, float* out) {
 static size_t x3_bytes(int B, int K, int H) {
   return std::max({gemm_f32x3_workspace_bytes(false, false, B, K, H, false),   // s_tr = s W_s
                    gemm_f32x3_workspace_bytes(false, true, B, H, K, false),    // d s = d s_tr W_s^T
-                   gemm_f32x3_workspace_bytes(true, false, H, K, B, true)});   // [d W_s; d b_s]
+                   gemm_f32x3_workspace_bytes(true, false, H, K, B, true),     // [d W_s; d b_s]
+                   gemm_f32x3_parts_workspace_bytes(false, false, B, K, H),    // (as partials)
+                   gemm_f32x3_parts_workspace_bytes(false, true, B, H, K)});
 }
 static size_t ws_head(int B, int K, int Ts) {
   return (size_t)round_up((int64_t)2 * B * K * sizeof(float), 256) + (size_t)round_up((int64_t)B * Ts * 4, 256);
@@ -590,7 +611,8 @@ static int vec_e(const AttnArgs& p) {
 static bool cluster_ok(const AttnArgs& p) {
   bool copies = true;
   for (int c = 0; c < 2; ++c) copies = copies && al16(p.att_copy[c]) && p.att_copy_ld[c] % 4 == 0;
-  return p.K % 4 == 0 && p.E % 4 == 0 && al16(p.enc_ctx) && al16(p.enc) && al16(p.att) &&
+  const bool img_ok = !p.att_img || (((uintptr_t)p.att_img & 7) == 0 && p.att_img_ld % 4 == 0 && p.att_img_lo % 4 == 0);
+  return img_ok && p.K % 4 == 0 && p.E % 4 == 0 && al16(p.enc_ctx) && al16(p.enc) && al16(p.att) &&
          al16(p.s_tr) && al16(p.b_fb) && al16(p.W_fb) && al16(p.v) && copies &&
          (size_t)cl_smem(p.K, p.Ts).total * sizeof(float) <= 200 * 1024 && !getenv("SL_ATTN_CHUNKED");
 }
@@ -601,7 +623,12 @@ static void cl_configure(F kern, size_t smem) {
 
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {
   p.s_tr = p.s_tr_out ? p.s_tr_out : static_cast<float*>(ws);
-  if (p.W_s3_fwd)  // s_tr = s W_s + b_s
+  p.s_tr_parts = X3Parts{nullptr, 0, 0, 0};
+  if (p.W_s3_fwd && cluster_ok(p)) {  // partials summed (+ b_s) by the attention kernel
+    p.s_tr_parts = gemm_f32x3_parts(false, false, p.B, p.K, p.H, s, p.H, p.s_img, nullptr, 0, p.W_s3_fwd,
+                                    x3_ws(p, ws), st, p.s_img_ld, p.s_img_lo);
+    p.s_tr_bias = b_s;
+  } else if (p.W_s3_fwd)  // s_tr = s W_s + b_s
     gemm_f32x3_pb(false, false, p.B, p.K, p.H, s, p.H, p.W_s3_fwd, 0.f, p.s_tr, p.K, b_s, x3_ws(p, ws), st);
   else
     gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
@@ -659,7 +686,10 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     count_launch(2);
   }
   const float beta = p.accumulate ? 1.f : 0.f;
-  if (d_s && p.W_s3_bwd)  // d s = d s_tr W_s^T
+  if (d_s && p.W_s3_bwd && p.ds_parts_out)  // d s = d s_tr W_s^T, summed by the caller's consumer
+    *p.ds_parts_out = gemm_f32x3_parts(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, nullptr, nullptr, 0, p.W_s3_bwd,
+                                       x3_ws(p, ws), st);
+  else if (d_s && p.W_s3_bwd)  // d s = d s_tr W_s^T
     gemm_f32x3_pb(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, p.W_s3_bwd, beta, d_s, p.H, nullptr, x3_ws(p, ws), st);
   else if (d_s)
     gemm_f32x3(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, W_s, p.K, beta, d_s, p.H, nullptr, nullptr, 0,

@@ -39,8 +39,10 @@ constexpr int kRedSlices = 64;  // f32_ctx_reduce1/2: row slices of the deferred
 
 struct FLay {
   int64_t XA, RO;  // row pitches: [att ‖ s] (E + H), readout input [s ‖ trg ‖ att] (H + Emb + E)
-  float *xw, *xa, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all, *z;
-  float *dro, *dpre, *dxa, *dc, *ds, *dacc, *dctx, *dtrg;
+  float *xw, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all;
+  __nv_bfloat16* xai;  // [att ‖ s]_{t-1} per step t as its split image [(T+1)*B, XA] (GEMM operand only)
+  int64_t xai_ld, xai_lo;
+  float *dro, *dpre, *dc, *ds, *dacc, *dctx, *dtrg;
   __nv_bfloat16* dzi;  // the cell's DZ [B*T, 4H] as its split image (every consumer is a GEMM)
   int64_t dzi_ld;
   float* w2;  // [E + H, 4H] staging of [W_att; R]
@@ -58,8 +60,8 @@ size_t gemm_ws_bytes(const DecDims& d) {
   const int BT = B * d.T, BTs = B * d.Ts, XA = E + H, RO = H + Emb + E;
   return std::max({gemm_f32x3_workspace_bytes(false, false, BTs, K, E, false),      // enc_ctx
                    gemm_f32x3_workspace_bytes(false, false, BT, 4 * H, Emb, false),  // trg W_trg + b
-                   gemm_f32x3_workspace_bytes(false, false, B, 4 * H, XA, false),    // z (presplit B)
-                   gemm_f32x3_workspace_bytes(false, true, B, XA, 4 * H, false),     // d xa (presplit B)
+                   gemm_f32x3_parts_workspace_bytes(false, false, B, 4 * H, XA),     // z (partials)
+                   gemm_f32x3_parts_workspace_bytes(false, true, B, XA, 4 * H),      // d xa (partials)
                    gemm_f32x3_workspace_bytes(false, false, BT, Rd, RO, false),      // readout
                    gemm_f32x3_workspace_bytes(false, true, BT, RO, Rd, false),       // d readout input
                    gemm_f32x3_workspace_bytes(true, false, RO, Rd, BT, true),        // [d W_ro; d b_ro]
@@ -88,7 +90,9 @@ FLay flayout(const DecDims& d, void* base) {
   };
   auto tf = [&](int64_t n) { return static_cast<float*>(take((size_t)n * 4)); };
   L.xw = tf(BT * 4 * H);
-  L.xa = tf((T + 1) * B * L.XA);
+  L.xai = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)((T + 1) * B), (int)L.XA) * 2));
+  L.xai_ld = x3_img_ld((int)L.XA);
+  L.xai_lo = (T + 1) * B * L.xai_ld;
   L.ro = tf(BT * L.RO);
   L.s_all = tf(BT * H);
   L.att_all = tf(BT * E);
@@ -97,12 +101,10 @@ FLay flayout(const DecDims& d, void* base) {
   L.enc_ctx = tf(BTs * K);
   L.a_all = tf(T * B * d.Ts);
   L.acc_all = tf((T + 1) * B * d.Ts);
-  L.z = tf(B * 4 * H);
   L.dro = tf(BT * L.RO);
   L.dpre = tf(BT * d.Rd);
   L.dzi = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)BT, (int)(4 * H)) * 2));
   L.dzi_ld = x3_img_ld((int)(4 * H));
-  L.dxa = tf(B * L.XA);
   L.dc = tf(2 * B * H);
   L.ds = tf(B * H);
   L.dacc = tf(2 * B * d.Ts);
@@ -139,11 +141,11 @@ __global__ void f32_ids_tm_kernel(const int32_t* __restrict__ ids, int B, int T,
 // trg_{t-1} W_trg + b; s_t into s_all, the next step's [att ‖ s] row and the readout input
 struct GateF {
   int B, T, H, E, t;
-  const float* z;    // [B, 4H] or null
+  X3Parts z;         // [B, 4H] = h_{t-1} part of the gates as split-K partials (n = 0: none)
   const float* xw;   // [T*B, 4H]
   float *gates, *c_all, *s_all;
-  float* xa;         // [(T+1)*B, XA]
-  int64_t XA;
+  __nv_bfloat16* xai;  // [att ‖ s] image rows (s written at column E of block t + 1)
+  int64_t xai_ld, xai_lo;
   float* ro;         // [T*B, RO]
   int64_t RO;
 };
@@ -156,7 +158,7 @@ __global__ void f32_cell_fwd_kernel(GateF a) {
   const float* x = a.xw + row * 4 * H;
   float z[4];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) z[g] = x[g * H + j] + (a.z ? a.z[(int64_t)b * 4 * H + g * H + j] : 0.f);
+  for (int g = 0; g < 4; ++g) z[g] = x[g * H + j] + x3_parts_sum(a.z, b, g * H + j);
   const float cp = a.t > 0 ? a.c_all[(row - a.B) * H + j] : 0.f;
   const float gi = sigmoidf_(z[0]), gf = sigmoidf_(z[1]), gg = tanhf(z[2]), go = sigmoidf_(z[3]);
   const float c = gf * cp + gi * gg;
@@ -167,7 +169,12 @@ __global__ void f32_cell_fwd_kernel(GateF a) {
   gs[0] = gi, gs[H] = gf, gs[2 * H] = gg, gs[3 * H] = go, gs[4 * H] = tc;
   a.s_all[row * H + j] = h;
   a.ro[row * a.RO + j] = h;
-  a.xa[(row + a.B) * a.XA + a.E + j] = h;
+  {
+    __nv_bfloat16* q = a.xai + (row + a.B) * a.xai_ld + a.E + j;
+    const __nv_bfloat16 hh = __float2bfloat16_rn(h);
+    q[0] = hh;
+    q[a.xai_lo] = __float2bfloat16_rn(h - __bfloat162float(hh));
+  }
 }
 
 // readout [b, t] = relu(pre [t*B + b])
@@ -200,8 +207,7 @@ struct GradIn {
   const float* dro;  // [T*B, RO]
   int64_t RO;
   int Emb;
-  const float* dxa;  // [B, XA]: d [att ‖ s]_t from the cell at t + 1
-  int64_t XA;
+  X3Parts dxa;       // [B, XA]: d [att ‖ s]_t from the cell at t + 1, as split-K partials
   float *datt, *ds;
 };
 __global__ void f32_grad_in_kernel(GradIn a) {
@@ -213,12 +219,12 @@ __global__ void f32_grad_in_kernel(GradIn a) {
   const float* r = a.dro + ((int64_t)a.t * a.B + b) * a.RO;
   if (c < a.E) {
     float v = r[a.H + a.Emb + c];
-    if (a.has_next) v += a.dxa[(int64_t)b * a.XA + c];
+    if (a.has_next) v += x3_parts_sum(a.dxa, b, c);
     a.datt[(int64_t)b * a.E + c] = v;
   } else {
     const int j = c - a.E;
     float v = r[j];
-    if (a.has_next) v += a.dxa[(int64_t)b * a.XA + a.E + j];
+    if (a.has_next) v += x3_parts_sum(a.dxa, b, a.E + j);
     a.ds[(int64_t)b * a.H + j] = v;
   }
 }
@@ -227,6 +233,7 @@ __global__ void f32_grad_in_kernel(GradIn a) {
 struct CellBF {
   int B, H, t;
   const float *ds, *gates, *c_all, *dc_in;
+  X3Parts ds_att;      // the attention's d s = d s_tr W_s^T as split-K partials (added to ds)
   __nv_bfloat16* dzi;  // DZ image: hi rows at dzi (stride ld), lo rows lo elements further on
   int64_t ld, lo;
   float* dc_out;
@@ -242,7 +249,7 @@ __global__ void f32_cell_bwd_kernel(CellBF a) {
   if (e >= n) return;
   const int b = (int)(e / a.H), j = (int)(e % a.H), H = a.H;
   const int64_t row = (int64_t)a.t * a.B + b;
-  const float gh = a.ds[e], gc = a.dc_in ? a.dc_in[e] : 0.f;
+  const float gh = a.ds[e] + x3_parts_sum(a.ds_att, b, j), gc = a.dc_in ? a.dc_in[e] : 0.f;
   const float* gs = a.gates + row * 5 * H + j;
   const float gi = gs[0], gf = gs[H], gg = gs[2 * H], go = gs[3 * H], tc = gs[4 * H];
   const float cp = a.t > 0 ? a.c_all[(row - a.B) * H + j] : 0.f;
@@ -440,7 +447,9 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
   const int64_t BT = (int64_t)B * T, BTs = (int64_t)B * d.Ts;
   {
     Phase ph(st, "k10_dec_fwd_hoisted", 2.0 * BTs * E * K + 2.0 * BT * Emb * 4 * H);
-    SL_CUDA_TRY(cudaMemsetAsync(L.xa, 0, sizeof(float) * B * L.XA, st));  // [att ‖ s]_{-1} = 0
+    // [att ‖ s]_{-1} = 0 (hi and lo rows of block 0)
+    SL_CUDA_TRY(cudaMemsetAsync(L.xai, 0, sizeof(__nv_bfloat16) * B * L.xai_ld, st));
+    SL_CUDA_TRY(cudaMemsetAsync(L.xai + L.xai_lo, 0, sizeof(__nv_bfloat16) * B * L.xai_ld, st));
     SL_CUDA_TRY(cudaMemsetAsync(L.acc_all, 0, sizeof(float) * BTs, st));  // accum_{-1} = 0
     // [W_att; R] (rows Emb.. of s/W stacked on s/R) split once into the two K-tripled
     // images the per-step GEMMs read, through an fp32 staging copy of the stacked matrix
@@ -463,14 +472,15 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
                L.gws, st);
   }
   for (int t = 0; t < T; ++t) {
-    if (t > 0) {
+    X3Parts zp{nullptr, 0, 0, 0};
+    if (t > 0) {  // [att ‖ s]_{t-1} [W_att; R] as split-K partials, summed by the gate kernel
       Phase q(st, "k10_cell_gemm", 2.0 * B * (E + H) * 4.0 * H);
-      gemm_f32x3_pb(false, false, B, 4 * H, E + H, L.xa + (int64_t)t * B * L.XA, L.XA, L.wd2_f, 0.f, L.z, 4 * H,
-                    nullptr, L.gws, st);
+      zp = gemm_f32x3_parts(false, false, B, 4 * H, E + H, nullptr, 0, L.xai + (int64_t)t * B * L.xai_ld, nullptr,
+                            0, L.wd2_f, L.gws, st, L.xai_ld, L.xai_lo);
     }
     {
       Phase q(st, "k10_cell_fwd", 0.0, 4.0 * B * H * 12);
-      GateF g{B, T, H, E, t, t > 0 ? L.z : nullptr, L.xw, L.gates, L.c_all, L.s_all, L.xa, L.XA, L.ro, L.RO};
+      GateF g{B, T, H, E, t, zp, L.xw, L.gates, L.c_all, L.s_all, L.xai, L.xai_ld, L.xai_lo, L.ro, L.RO};
       f32_cell_fwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(g);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
@@ -483,8 +493,13 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     // att_t also -> the readout input (columns H + Emb..) and the next step's [att ‖ s] row
     a.att_copy[0] = L.ro + (int64_t)t * B * L.RO + H + Emb;
     a.att_copy_ld[0] = L.RO;
-    a.att_copy[1] = t + 1 < T ? L.xa + (int64_t)(t + 1) * B * L.XA : nullptr;
-    a.att_copy_ld[1] = L.XA;
+    a.att_copy[1] = nullptr;
+    a.att_img = t + 1 < T ? L.xai + (int64_t)(t + 1) * B * L.xai_ld : nullptr;
+    a.att_img_ld = L.xai_ld;
+    a.att_img_lo = L.xai_lo;
+    a.s_img = L.xai + (int64_t)(t + 1) * B * L.xai_ld + E;  // s_t: block t + 1, columns E..
+    a.s_img_ld = L.xai_ld;
+    a.s_img_lo = L.xai_lo;
     attention_fwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.att_ws, st);
   }
   {
@@ -517,11 +532,12 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     gemm_f32x3(true, false, (int)L.RO, Rd, (int)BT, L.ro, L.RO, L.dpre, Rd, 0.f, g.ro_W, Rd, nullptr, g.ro_b, Rd,
                L.gws, st);
   }
+  X3Parts dxp{nullptr, 0, 0, 0};  // d [att ‖ s]_t from step t + 1 (partials)
   for (int t = T - 1; t >= 0; --t) {
     const int cur = t & 1, nxt = cur ^ 1;  // ping-pong: d c / d accum of step t in [cur], of t - 1 -> [nxt]
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * (E + H) * 3);
-      GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, L.dxa, L.XA, L.datt_all + (int64_t)t * B * E, L.ds};
+      GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, dxp, L.datt_all + (int64_t)t * B * E, L.ds};
       f32_grad_in_kernel<<<grid_of((int64_t)B * (E + H)), 256, 0, st>>>(gi);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
@@ -543,10 +559,12 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     a.d_s_tr_out = L.ds_all + (int64_t)t * B * K;
     a.de_out = L.de_all + (int64_t)t * B * d.Ts;
     SL_CUDA_TRY(cudaMemsetAsync(a.d_accum, 0, sizeof(float) * B * d.Ts, st));
+    X3Parts dsp{nullptr, 0, 0, 0};
+    a.ds_parts_out = &dsp;
     attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, nullptr, nullptr, L.att_ws, st);
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 12);
-      CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, L.dzi,
+      CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, dsp, L.dzi,
                 L.dzi_ld, BT * L.dzi_ld, L.dc + (int64_t)nxt * B * H};
       f32_cell_bwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(cb);
       SL_CUDA_TRY(cudaGetLastError());
@@ -554,18 +572,20 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     }
     if (t > 0) {  // d [att ‖ s]_{t-1} = DZ_t [W_att; R]^T
       Phase q(st, "k10_g1_gemm", 2.0 * B * 4.0 * H * (E + H));
-      gemm_f32x3_ex(false, true, B, (int)L.XA, 4 * H, nullptr, 0, L.dzi + (int64_t)t * B * L.dzi_ld, nullptr, 0,
-                    L.wd2_b, 0.f, L.dxa, L.XA, nullptr, nullptr, 0, L.gws, st, L.dzi_ld, BT * L.dzi_ld);
+      dxp = gemm_f32x3_parts(false, true, B, (int)L.XA, 4 * H, nullptr, 0, L.dzi + (int64_t)t * B * L.dzi_ld,
+                             nullptr, 0, L.wd2_b, L.gws, st, L.dzi_ld, BT * L.dzi_ld);
     }
   }
   {
     Phase ph(st, "k10_dec_bwd_hoisted",
              2.0 * BT * 4 * H * (E + H + 2.0 * Emb) + 4.0 * BTs * E * K);
     // the cell's weight gradients over all B*T rows: [W_att; R] from [att ‖ s]_{t-1} (block t of xa)
-    gemm_f32x3_ex(true, false, E, 4 * H, (int)BT, L.xa, L.XA, nullptr, nullptr, 0, L.dzi, 0.f,
-                  g.s_W + (int64_t)Emb * 4 * H, 4 * H, nullptr, nullptr, 0, L.gws, st);
-    gemm_f32x3_ex(true, false, H, 4 * H, (int)BT, L.xa + E, L.XA, nullptr, nullptr, 0, L.dzi, 0.f, g.s_R, 4 * H,
-                  nullptr, nullptr, 0, L.gws, st);
+    // (A = the [att ‖ s] image; the 64-wide blocks of d R's column window run 16 columns
+    // into the next row, which block T of the image keeps in bounds)
+    gemm_f32x3_ex(true, false, E, 4 * H, (int)BT, nullptr, 0, L.xai, nullptr, 0, L.dzi, 0.f,
+                  g.s_W + (int64_t)Emb * 4 * H, 4 * H, nullptr, nullptr, 0, L.gws, st, L.xai_ld, L.xai_lo);
+    gemm_f32x3_ex(true, false, H, 4 * H, (int)BT, nullptr, 0, L.xai + E, nullptr, 0, L.dzi, 0.f, g.s_R, 4 * H,
+                  nullptr, nullptr, 0, L.gws, st, L.xai_ld, L.xai_lo);
     // [W_trg; b] from [trg_{t-1} | 1]
     gemm_f32x3_ex(true, false, Emb, 4 * H, (int)BT, L.ro + H, L.RO, nullptr, nullptr, 0, L.dzi, 0.f, g.s_W, 4 * H,
                   nullptr, g.s_b, 4 * H, L.gws, st);

@@ -40,6 +40,24 @@ void gemm_f32x3_ex(bool transA, bool transB, int M, int N, int K, const float* A
                    const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, float beta,
                    float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
                    cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0);
+// Split-K partial products for a consumer that sums them itself (fixed order z =
+// 0..n-1, the order the reduction kernel uses): op(A) op(B) = sum_z p[z*stride + r*ld + c]
+// (no bias / beta).  Saves the reduction launch and its round trip for the small
+// per-step products whose consumer is an elementwise kernel anyway.
+struct X3Parts {
+  const float* p;
+  int n;
+  int64_t stride, ld;
+};
+__device__ __forceinline__ float x3_parts_sum(const X3Parts& q, int64_t r, int64_t c) {
+  float s = 0.f;
+  for (int z = 0; z < q.n; ++z) s += q.p[z * q.stride + r * q.ld + c];
+  return s;
+}
+size_t gemm_f32x3_parts_workspace_bytes(bool transA, bool transB, int M, int N, int K);
+X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                         const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, void* ws,
+                         cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0);
 // both operands pre-split (images of the stored A and B)
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
                     const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,

@@ -179,7 +179,8 @@ namespace {
 void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
              const __nv_bfloat16* a_pre, const float* B, int64_t ldb, const __nv_bfloat16* b_pre, float beta,
              float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
-             cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0) {
+             cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0,
+             X3Parts* parts = nullptr) {
   if (M <= 0 || N <= 0) return;
   const bool a_ones = ones_row_out != nullptr;
   SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
@@ -209,6 +210,17 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
   {  // chunked accumulation only where one work unit's K range is longer than a chunk
     const int64_t nk = ceil_div(K, 64);
     if (ceil_div(nk, d.ksplit) > kX3ChunkBlocks) g.kchunk = kX3ChunkBlocks;
+  }
+  if (parts) {  // the partials for the caller's consumer (ksplit may be 1)
+    SL_REQUIRE(!a_ones && beta == 0.f && !bias, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: partials are plain products");
+    float* part = reinterpret_cast<float*>(w);
+    g.C = part;
+    g.ldc = d.p_ld;
+    g.ksplit = d.ksplit;
+    g.split_stride = d.p_stride;
+    gemm_bf16_tc(g, st);
+    *parts = X3Parts{part, d.ksplit, d.p_stride, d.p_ld};
+    return;
   }
   if (d.ksplit > 1) {  // small output: split K over the idle SMs, then a fixed-order reduction
     float* part = reinterpret_cast<float*>(w);
@@ -255,6 +267,21 @@ void gemm_f32x3_ex(bool transA, bool transB, int M, int N, int K, const float* A
                    cudaStream_t st, int64_t a3_ld, int64_t a3_lo, int64_t b3_ld, int64_t b3_lo) {
   x3_core(transA, transB, M, N, K, A, lda, A3, B, ldb, B3, beta, C, ldc, bias, ones_row_out, ld_ones, ws, st, a3_ld,
           a3_lo, b3_ld, b3_lo);
+}
+
+size_t gemm_f32x3_parts_workspace_bytes(bool transA, bool transB, int M, int N, int K) {
+  const X3Dims d = x3_dims(transA, transB, M, N, K, false);
+  return round_up(x3_img_elems((int)d.a_rows, (int)d.a_cols) * 2, 256) +
+         round_up(x3_img_elems((int)d.b_rows, (int)d.b_cols) * 2, 256) + (size_t)d.ksplit * d.p_stride * 4;
+}
+
+X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
+                         const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, void* ws,
+                         cudaStream_t st, int64_t a3_ld, int64_t a3_lo, int64_t b3_ld, int64_t b3_lo) {
+  X3Parts q{nullptr, 0, 0, 0};
+  x3_core(transA, transB, M, N, K, A, lda, A3, B, ldb, B3, 0.f, nullptr, 0, nullptr, nullptr, 0, ws, st, a3_ld,
+          a3_lo, b3_ld, b3_lo, &q);
+  return q;
 }
 
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
