@@ -20,14 +20,19 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 HOST = os.path.join(PKG, "host")
-OBJ = os.path.join(PKG, "build_obj")
-LIB_DIR = os.path.join(PKG, "lib")
+# SL_EXPERIMENTS=1: a separate build with the measurement hooks (-DSL_EXPERIMENTS:
+# per-step trace stamps, the experimental kernels) into build_obj_exp/ and lib_exp/;
+# load it with SL_LIB_PATH=paper_1805_05225_b200/lib_exp/libseqloom_cuda.so
+EXPERIMENTS = os.environ.get("SL_EXPERIMENTS", "") not in ("", "0")
+OBJ = os.path.join(PKG, "build_obj_exp" if EXPERIMENTS else "build_obj")
+LIB_DIR = os.path.join(PKG, "lib_exp" if EXPERIMENTS else "lib")
 LIB = os.path.join(LIB_DIR, "libseqloom_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", 
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
-                  "-diag-suppress", "177,550", "--diag-error", "20013,20014,20015"]
+                  "-diag-suppress", "177,550", "--diag-error", "20013,20014,20015"] + \
+    (["-DSL_EXPERIMENTS"] if EXPERIMENTS else [])
 
 
 def _headers():

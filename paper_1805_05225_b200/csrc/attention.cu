@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include "attention.h"
+#include "fastmath.cuh"
 #include "gemm.h"
 #include "profile.h"
 
@@ -279,12 +280,42 @@ __global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(
 // backward 1: d_a[b, j] = <d_att_b, enc_bj> (valid j; tape.cpp:1031-1041) and
 // d enc_bj = a_j d_att_b (every j of the chunk: zero at padded positions)
 template <int VE>
-__global__ void __launch_bounds__(kThreads, 3) attn_bwd_da_kernel(AttnArgs p, float* __restrict__ d_a) {
+__global__ void __launch_bounds__(kThreads, 2) attn_bwd_da_kernel(AttnArgs p, float* __restrict__ d_a) {
   __shared__ float red[kWarps * kJC];
   const int b = blockIdx.y, j0 = blockIdx.x * kJC, Ts = p.Ts, E = p.E;
-  const int len = min(max(p.lens[b], 0), Ts);
   const int n = min(kJC, Ts - j0);
   float part[kJC], aj[kJC];
+  if (p.defer && E <= kThreads * VE) {
+    // deferred mode (the decoder's loop): only the dot products — every encoder row of
+    // the chunk is loaded at once (no dependency on the row's length; 2 CTAs per SM so
+    // the registers hold them), the length only masks the sums
+    const int x = threadIdx.x * VE;
+    Vec<VE> g;
+    constexpr int kHalf = kJC / 2;
+    const int len = min(max(p.lens[b], 0), Ts);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two batches of kJC / 2 rows in flight
+      Vec<VE> q[kHalf];
+      if (x < E) {
+        if (h == 0) g.load(p.d_att + (size_t)b * E + x);
+#pragma unroll
+        for (int j = 0; j < kHalf; ++j)
+          if (h * kHalf + j < n) q[j].load(p.enc + ((size_t)b * Ts + j0 + h * kHalf + j) * E + x);
+      }
+#pragma unroll
+      for (int j = 0; j < kHalf; ++j) {
+        const int jj = h * kHalf + j;
+        part[jj] = 0.f;
+        if (x < E && jj < n && j0 + jj < len) {
+#pragma unroll
+          for (int w = 0; w < VE; ++w) part[jj] += g.f[w] * q[j].f[w];
+        }
+      }
+    }
+    block_reduce_chunk(part, n, red, d_a + (size_t)b * Ts + j0);
+    return;
+  }
+  const int len = min(max(p.lens[b], 0), Ts);
 #pragma unroll
   for (int j = 0; j < kJC; ++j) {
     part[j] = 0.f;
@@ -321,14 +352,28 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_da_kernel(AttnArgs p, fl
 // then through tanh for the chunk: d e_in[j, k] = d_e_j v_k (1 - u^2) -> d enc_ctx,
 // d accum_j = d accum'_j + <d e_in[j], W_fb>, and the column sums d s_tr[b] /
 // d b_fb / d W_fb / d v (per-thread over the chunk, then vector atomics)
-template <int VK>
-__global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, const float* __restrict__ d_a) {
+template <int VK, bool DEFER>
+__global__ void __launch_bounds__(kThreads, DEFER ? 3 : 2) attn_bwd_de_kernel(AttnArgs p, const float* __restrict__ d_a) {
   __shared__ float red[kWarps * kJE];
   __shared__ float de_sh[kJE], sum_sh[kJE];
   const int b = blockIdx.y, j0 = blockIdx.x * kJE, Ts = p.Ts, K = p.K;
-  const int len = min(max(p.lens[b], 0), Ts);
   const int n = min(kJE, Ts - j0);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // The chunk's energy inputs and column constants do not depend on the row's length
+  // or on d a: their loads go out first, so the latency of the dependent prologue
+  // below (length -> softmax-adjoint dot -> de) hides under them.
+  const int k_first = threadIdx.x * VK;
+  Vec<VK> c0, w0, v0, x0[kJE];
+  float acc[kJE];
+  if (k_first < K) {
+    load_cols(p, b, k_first, c0, w0, v0);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < n) x0[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k_first);
+  }
+#pragma unroll
+  for (int j = 0; j < kJE; ++j) acc[j] = j < n ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
+  const int len = min(max(p.lens[b], 0), Ts);
   const float* da_b = d_a + (size_t)b * Ts;
   const float* a_b = p.a_saved + (size_t)b * Ts;
   const float* up_b = p.d_accum_out ? p.d_accum_out + (size_t)b * Ts : nullptr;
@@ -348,22 +393,49 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, co
     if (lane == 0 && dbv != 0.f && !p.defer) atomicAdd(p.d_b_v, dbv);
   }
   __syncthreads();
-  float part[kJE], de[kJE], acc[kJE];
+  float part[kJE], de[kJE];
 #pragma unroll
   for (int j = 0; j < kJE; ++j) {
     part[j] = 0.f;
     de[j] = de_sh[j];
-    acc[j] = (j < n && j0 + j < len) ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
   }
   const int nv = max(0, min(n, len - j0));  // valid positions of the chunk
-  for (int k = threadIdx.x * VK; k < K; k += kThreads * VK) {
-    Vec<VK> c, w, v, ds, dwf, dv;
-    load_cols(p, b, k, c, w, v);
-    ds.zero(), dwf.zero(), dv.zero();
-    Vec<VK> x[kJE];
+  auto cols = [&](int k, const Vec<VK>& c, const Vec<VK>& w, const Vec<VK>& v, const Vec<VK>(&x)[kJE]) {
+    if constexpr (VK % 2 == 0 && DEFER) {
+      {  // only d s_tr and d accum: paired-fp32 math (two columns per instruction)
+        using namespace fm;
+        float2 ds2[VK / 2];
 #pragma unroll
-    for (int j = 0; j < kJE; ++j)
-      if (j < nv) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+        for (int i = 0; i < VK / 2; ++i) ds2[i] = s2(0.f);
+#pragma unroll
+        for (int j = 0; j < kJE; ++j) {
+          if (j < nv) {
+            float2 pj = s2(0.f);
+#pragma unroll
+            for (int i = 0; i < VK / 2; ++i) {
+              const float2 w2 = make_float2(w.f[2 * i], w.f[2 * i + 1]);
+              const float2 c2 = make_float2(c.f[2 * i], c.f[2 * i + 1]);
+              const float2 v2 = make_float2(v.f[2 * i], v.f[2 * i + 1]);
+              const float2 x2 = make_float2(x[j].f[2 * i], x[j].f[2 * i + 1]);
+              const float2 u = tanh2(fma2(s2(acc[j]), w2, add2(x2, c2)));
+              const float2 gk = mul2(mul2(s2(de[j]), v2), fma2(make_float2(-u.x, -u.y), u, s2(1.f)));
+              ds2[i] = add2(ds2[i], gk);
+              pj = fma2(gk, w2, pj);
+            }
+            part[j] += pj.x + pj.y;
+          }
+        }
+        if (nv > 0) {
+          Vec<VK> ds;
+#pragma unroll
+          for (int i = 0; i < VK / 2; ++i) ds.f[2 * i] = ds2[i].x, ds.f[2 * i + 1] = ds2[i].y;
+          ds.atomic_add(p.d_s_tr + (size_t)b * K + k);
+        }
+        return;
+      }
+    }
+    Vec<VK> ds, dwf, dv;
+    ds.zero(), dwf.zero(), dv.zero();
 #pragma unroll
     for (int j = 0; j < kJE; ++j) {
       if (j < n) {
@@ -401,6 +473,15 @@ __global__ void __launch_bounds__(kThreads, 3) attn_bwd_de_kernel(AttnArgs p, co
         dv.atomic_add(p.d_v + k);
       }
     }
+  };
+  if (k_first < K) cols(k_first, c0, w0, v0, x0);
+  for (int k = k_first + kThreads * VK; k < K; k += kThreads * VK) {
+    Vec<VK> c, w, v, x[kJE];
+    load_cols(p, b, k, c, w, v);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < nv) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+    cols(k, c, w, v, x);
   }
   block_reduce_chunk(part, n, red, sum_sh);
   __syncthreads();
@@ -458,7 +539,7 @@ __device__ __forceinline__ void cl_stage_cols(const AttnArgs& p, int b, float* s
   }
 }
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 4)
     attn_fwd_cluster_kernel(AttnArgs p) {
   extern __shared__ float4 sh4[];
   float* sh = reinterpret_cast<float*>(sh4);
@@ -478,15 +559,22 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads)
       float4 xv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) xv[u] = k0 + 128 * u < K ? ldg4(x + k0 + 128 * u) : make_float4(0, 0, 0, 0);
+      float2 s2v = fm::s2(0.f);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int k = k0 + 128 * u;
-        if (k < K) {
+        if (k < K) {  // paired-fp32 math, two columns per instruction
+          using namespace fm;
           const float4 c = lds4(sh + m.c + k), w = lds4(sh + m.w + k), v = lds4(sh + m.v + k);
-          sum += v.x * tanh_fast(xv[u].x + aj * w.x + c.x) + v.y * tanh_fast(xv[u].y + aj * w.y + c.y) +
-                 v.z * tanh_fast(xv[u].z + aj * w.z + c.z) + v.w * tanh_fast(xv[u].w + aj * w.w + c.w);
+          const float2 t0 = tanh2(fma2(s2(aj), make_float2(w.x, w.y), add2(make_float2(xv[u].x, xv[u].y),
+                                                                             make_float2(c.x, c.y))));
+          const float2 t1 = tanh2(fma2(s2(aj), make_float2(w.z, w.w), add2(make_float2(xv[u].z, xv[u].w),
+                                                                             make_float2(c.z, c.w))));
+          s2v = fma2(make_float2(v.x, v.y), t0, s2v);
+          s2v = fma2(make_float2(v.z, v.w), t1, s2v);
         }
       }
+      sum += s2v.x + s2v.y;
     }
     sum = warp_sum(sum);
     if (lane < kCl) cl.map_shared_rank(sh + m.e, lane)[j] = sum;
@@ -680,8 +768,9 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     if (vec_e(p) == 8) attn_bwd_da_kernel<8><<<g, kThreads, 0, st>>>(p, d_a);
     else attn_bwd_da_kernel<1><<<g, kThreads, 0, st>>>(p, d_a);
     SL_CUDA_TRY(cudaGetLastError());
-    if (vec_k(p) == 4) attn_bwd_de_kernel<4><<<ge, kThreads, 0, st>>>(p, d_a);
-    else attn_bwd_de_kernel<1><<<ge, kThreads, 0, st>>>(p, d_a);
+    if (vec_k(p) == 4 && p.defer) attn_bwd_de_kernel<4, true><<<ge, kThreads, 0, st>>>(p, d_a);
+    else if (vec_k(p) == 4) attn_bwd_de_kernel<4, false><<<ge, kThreads, 0, st>>>(p, d_a);
+    else attn_bwd_de_kernel<1, false><<<ge, kThreads, 0, st>>>(p, d_a);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch(2);
   }

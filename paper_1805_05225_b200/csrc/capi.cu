@@ -396,6 +396,7 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.dc_last = dc_last;
     a.dzimg = w.dzi;
     a.dzimg_rows = M;
+    a.trace = g_rec_trace;  // (experiments builds stamp it; null otherwise)
     a.dzcat_ld = dzi_ld(d);
     a.dz_dir_off = G;
     a.bar = w.bar;

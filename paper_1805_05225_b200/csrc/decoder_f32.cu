@@ -26,6 +26,7 @@
 
 #include "attention.h"
 #include "decoder.h"
+#include "fastmath.cuh"
 #include "embedding.h"
 #include "gemm.h"
 #include "profile.h"
@@ -327,20 +328,29 @@ __global__ void __launch_bounds__(128) f32_ctx_grad_kernel(int B, int Ts, int T,
     g[j] = 0.f;
   }
   const float w = W_fb[k], c = b_fb[k], vk = v[k];
-  float dwf = 0.f, dbf = 0.f, dv = 0.f;
-  for (int t = 0; t < T; ++t) {
-    const float str = str_all[((int64_t)t * B + b) * K + k];
+  // paired-fp32 math over pairs of positions (two per instruction; MUFU-bound after)
+  using namespace fm;
+  float2 g2[kCtxPos / 2], dwf2 = s2(0.f), dbf2 = s2(0.f), dv2 = s2(0.f);
 #pragma unroll
-    for (int j = 0; j < kCtxPos; ++j) {
-      const float a = acc_sh[t * kCtxPos + j], de = de_sh[t * kCtxPos + j];
-      const float u = tanh_fast_f(x[j] + a * w + c + str);
-      const float gk = de * vk * (1.f - u * u);
-      g[j] += gk;
-      dwf += a * gk;
-      dbf += gk;
-      dv += u * de;
+  for (int j = 0; j < kCtxPos / 2; ++j) g2[j] = s2(0.f);
+  for (int t = 0; t < T; ++t) {
+    const float cs = c + str_all[((int64_t)t * B + b) * K + k];
+#pragma unroll
+    for (int j = 0; j < kCtxPos / 2; ++j) {
+      const float2 a = *reinterpret_cast<const float2*>(acc_sh + t * kCtxPos + 2 * j);
+      const float2 de = *reinterpret_cast<const float2*>(de_sh + t * kCtxPos + 2 * j);
+      const float2 u = tanh2(fma2(a, s2(w), add2(make_float2(x[2 * j], x[2 * j + 1]), s2(cs))));
+      const float2 gk = mul2(mul2(de, s2(vk)), fma2(make_float2(-u.x, -u.y), u, s2(1.f)));
+      g2[j] = add2(g2[j], gk);
+      dwf2 = fma2(a, gk, dwf2);
+      dbf2 = add2(dbf2, gk);
+      dv2 = fma2(u, de, dv2);
     }
   }
+  const float dwf = dwf2.x + dwf2.y, dbf = dbf2.x + dbf2.y, dv = dv2.x + dv2.y;
+#pragma unroll
+  for (int j = 0; j < kCtxPos; ++j)
+    g[j] = (j & 1) ? g2[j / 2].y : g2[j / 2].x;
 #pragma unroll
   for (int j = 0; j < kCtxPos; ++j)
     if (s0 + j < Ts) d_ctx[((int64_t)b * Ts + s0 + j) * K + k] = g[j];

@@ -1,0 +1,34 @@
+// Paired-fp32 helpers for the fp32 elementwise passes (Blackwell FFMA2 / FMUL2 /
+// FADD2: two lanes of math per issued instruction) and the two-MUFU tanh the fp32
+// attention kernels use: tanh(x) = 1 - 2 / (1 + e^{2x}) with ex2.approx and
+// rcp.approx, absolute error ~1e-7 (the energies and their adjoints only see tanh
+// through sums over K, so an absolute bound is the one that matters).  Saturates
+// correctly without a clamp: e^{2x} -> inf gives 1, -> 0 gives -1.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace sl {
+namespace fm {
+
+__device__ __forceinline__ float2 s2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 tanh2(float2 x) {
+  const float2 y = mul2(x, s2(2.8853900817779268f));  // 2 log2(e)
+  const float2 e = add2(make_float2(ex2(y.x), ex2(y.y)), s2(1.f));
+  return fma2(make_float2(rcp(e.x), rcp(e.y)), s2(-2.f), s2(1.f));
+}
+
+}  // namespace fm
+}  // namespace sl

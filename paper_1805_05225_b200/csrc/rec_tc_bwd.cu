@@ -156,6 +156,17 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   __syncthreads();
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
+#ifdef SL_EXPERIMENTS  // per-(CTA, iteration) stamps for scripts/trace_bwd.py (slot map there)
+  unsigned long long* trace = a.trace ? a.trace + (size_t)blockIdx.x * a.T * 16 : nullptr;
+#define TRB(it, k)                                           \
+  do {                                                       \
+    if (trace) trace[(size_t)(it) * 16 + (k)] = gtimer();    \
+  } while (0)
+#else
+#define TRB(it, k) \
+  do {             \
+  } while (0)
+#endif
   // Step counters per (direction, batch tile, DZ box of kb*64 ring columns): a
   // CTA publishes DZ_s of its units to every box its columns fall in (<= 2 per
   // gate), and a consumer streams each box of its K slice as soon as THAT box's
@@ -223,6 +234,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
           const unsigned m = __ballot_sync(0xffffffffu, rdy);
           while (done < ngrp && ((m >> done) & 1u)) {
             if (lane == 0) {
+              if (done == 0) TRB(s, 3 * mt);
               const int kg = (done + kc_off) % ngrp;
               tc::fence_proxy_async_global();  // the box's DZ (generic-proxy stores) -> TMA reads
               tc::mbar_wait(&empty_bar[st], ph ^ 1);
@@ -260,6 +272,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             const int kg = (kq + kc_off) % ngrp;
             tc::mbar_wait(&full_bar[st], ph);
             tc::fence_after_sync();
+            if (kq == 0) TRB(s, 1 + 3 * mt);
+            if (kq == ngrp - 1) TRB(s, 2 + 3 * mt);
             // A: the stage holds [kst / 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk;
             // B_hi: the resident SW128 K-major R rows (128 B per 64-K chunk row)
             const uint32_t sa = base + r_bytes + st * stage_bytes;
@@ -342,8 +356,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         load_f32<UT>(a.dy + pos * a.dy_ld + (size_t)gdir * H + ut0, dyv, nu, vec && (a.dy_ld % 4) == 0);
       }
       float dh[UT];
+      const bool tr0 = e == 0 && lane == 0;
+      if (tr0) TRB(it, 12);
       tc::mbar_wait(&tfull_bar[mt], it & 1);
       tc::fence_after_sync();
+      if (tr0) TRB(it, 8);
       if constexpr (C > 1) {
         // reduce-scatter of the K-split partials: send each peer the columns of
         // the units it finalizes (coalesced: a warp writes 32 consecutive rows)
@@ -390,8 +407,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       tmem_ld_cols<UT>(tbase + r * U + lo, dh);
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty_bar[mt]);
+      if (tr0) TRB(it, 9);
       if constexpr (C > 1) {
         mbar_wait_cluster(&recv_full[mt], it & 1);
+        if (tr0) TRB(it, 10);
         if ((e % (4 * SPLIT)) == 0 && lane == 0)  // phase `use` is complete: arm the next use
           tc::mbar_arrive_expect_tx(&recv_full[mt], kRecvBytes);
 #pragma unroll 1
@@ -419,6 +438,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
         // the senders learn that their slots are free from ONE arrive per peer
         // after the tile's publish barrier below (every reader is done by then)
       }
+      if (tr0) TRB(it, 13);
 
       // DZ_s: fp32 (x3) or packed bf16 — the ring copy now, the K4 copy after publishing
       typename std::conditional<X3, float[4 * UT], Bf16Vec<UT>[4]>::type dzs;
@@ -484,6 +504,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             for (int g = 0; g < 4; ++g) dzs[g].zero();
           }
         }
+        if (tr0) TRB(it, 14);
         constexpr int CW = UT < 8 ? UT : 8;  // the ring's 8-unit chunks are Bp * 16 B apart
 #pragma unroll
         for (int g = 0; g < 4; ++g)
@@ -506,6 +527,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             }
           }
       }
+      if (tr0) TRB(it, 11);
       named_sync(1 + mt, kEpiTile);
       if ((e % (4 * SPLIT)) == 0 && lane == 0) {
         tc::fence_proxy_async_global();
@@ -520,6 +542,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
                 red_relaxed_gpu(ctr + mt * kBoxCtrs + gb, 1u);
                 prev = gb;
               }
+          TRB(it, 6 + mt);
         }
         if constexpr (C > 1)  // every sender's slot in my receive buffer is free again
           for (int pi = 1; pi < C; ++pi)

@@ -24,7 +24,7 @@ from typing import Sequence
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libseqloom_cuda.so")
+LIB_PATH = os.environ.get("SL_LIB_PATH") or os.path.join(_PKG, "lib", "libseqloom_cuda.so")
 
 SL_OK, SL_ERR_INVALID_ARGUMENT, SL_ERR_SHAPE, SL_ERR_CUDA, SL_ERR_WORKSPACE, SL_ERR_UNSUPPORTED = range(6)
 PRECISIONS = {"fp32": 0, "bf16": 1}

@@ -18,6 +18,7 @@ ap.add_argument("--B", type=int, default=256)
 ap.add_argument("--T", type=int, default=60)
 ap.add_argument("--D", type=int, default=2000)
 ap.add_argument("--H", type=int, default=1000)
+ap.add_argument("--prec", default="bf16")
 a = ap.parse_args()
 B, T, D, H, nd = a.B, a.T, a.D, a.H, 2
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -28,7 +29,7 @@ W = [(torch.rand(D, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in ran
 R = [(torch.rand(H, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
 b = [(torch.rand(4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
 dy = torch.rand(B, T, nd * H, device="cuda", generator=g) * 2 - 1
-layer = lstm.LSTMLayer(B, T, D, H, nd, 1, "bf16")
+layer = lstm.LSTMLayer(B, T, D, H, nd, 1, a.prec)
 for _ in range(2):
     layer.forward(x, lens, W, R, b)
     layer.backward(dy)
