@@ -351,6 +351,8 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.c_last = c_last;
     a.hprev_ld = d.H;
     a.bar = w.bar;
+    a.trace = g_rec_trace;  // (experiments builds stamp it; null otherwise)
+    a.trace_cta = g_rec_trace_cta;
     const __nv_bfloat16* rt[2] = {nullptr, nullptr};
     for (int j = 0; j < per_launch; ++j) {
       const int k = k0 + j;
@@ -397,6 +399,7 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.dzimg = w.dzi;
     a.dzimg_rows = M;
     a.trace = g_rec_trace;  // (experiments builds stamp it; null otherwise)
+    a.debug_flags = g_rec_debug_flags;
     a.dzcat_ld = dzi_ld(d);
     a.dz_dir_off = G;
     a.bar = w.bar;

@@ -30,5 +30,12 @@ __device__ __forceinline__ float2 tanh2(float2 x) {
   return fma2(make_float2(rcp(e.x), rcp(e.y)), s2(-2.f), s2(1.f));
 }
 
+// 1 / (1 + e^{-x}), two MUFU ops per lane (relative error ~1e-7)
+__device__ __forceinline__ float2 sigmoid2(float2 x) {
+  const float2 y = mul2(x, s2(-1.4426950408889634f));  // -log2(e)
+  const float2 e = add2(make_float2(ex2(y.x), ex2(y.y)), s2(1.f));
+  return make_float2(rcp(e.x), rcp(e.y));
+}
+
 }  // namespace fm
 }  // namespace sl

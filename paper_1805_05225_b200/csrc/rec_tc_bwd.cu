@@ -28,6 +28,7 @@
 #include "profile.h"
 #include "rec_tc.h"
 #include "rec_tc_common.cuh"
+#include "fastmath.cuh"
 
 namespace sl {
 namespace {
@@ -157,10 +158,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const int Tmax = tmax_sh;
   const uint32_t tmem = tmem_sh;
 #ifdef SL_EXPERIMENTS  // per-(CTA, iteration) stamps for scripts/trace_bwd.py (slot map there)
-  unsigned long long* trace = a.trace ? a.trace + (size_t)blockIdx.x * a.T * 16 : nullptr;
+  unsigned long long* trace = a.trace ? a.trace + (size_t)blockIdx.x * a.T * 32 : nullptr;
 #define TRB(it, k)                                           \
   do {                                                       \
-    if (trace) trace[(size_t)(it) * 16 + (k)] = gtimer();    \
+    if (trace) trace[(size_t)(it) * 32 + (k)] = gtimer();    \
   } while (0)
 #else
 #define TRB(it, k) \
@@ -237,11 +238,21 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               if (done == 0) TRB(s, 3 * mt);
               const int kg = (done + kc_off) % ngrp;
               tc::fence_proxy_async_global();  // the box's DZ (generic-proxy stores) -> TMA reads
+#ifdef SL_EXPERIMENTS
+              const unsigned long long w0 = trace ? gtimer() : 0;
+#endif
               tc::mbar_wait(&empty_bar[st], ph ^ 1);
+#ifdef SL_EXPERIMENTS
+              if (trace) {  // time the producer waited for a free ring slot, and the last issue
+                trace[(size_t)s * 32 + 18 + mt] += gtimer() - w0;
+                if (done == ngrp - 1) trace[(size_t)s * 32 + 16 + mt] = gtimer();
+                if (done == ngrp / 2) trace[(size_t)s * 32 + 20 + mt] = gtimer();
+              }
+#endif
               tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
               const int kcol8 = (r * Kc + kg * kst) / 8;  // the box's first 8-column chunk of the ring
               if constexpr (MODE == kX3C)  // this box's R_lo rows (no dependency on the step)
-                tma_load_3d(sA + st * stage_bytes + 2 * part_bytes, tmRl, &full_bar[st], 0, a.P * NB + cta * NB,
+                tma_load_3d(sA + st * stage_bytes + 2 * part_bytes, tmRl, &full_bar[st], 0, (cta * NB) / 8,
                             (kg * kst) / 8);
               tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8, kcol8, slot);
               if constexpr (X3)
@@ -274,6 +285,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             tc::fence_after_sync();
             if (kq == 0) TRB(s, 1 + 3 * mt);
             if (kq == ngrp - 1) TRB(s, 2 + 3 * mt);
+            if (kq == ngrp / 2) TRB(s, 22 + mt);
             // A: the stage holds [kst / 8 K-chunks][128 rows][8] (SWIZZLE_NONE), 2 KB per chunk;
             // B_hi: the resident SW128 K-major R rows (128 B per 64-K chunk row)
             const uint32_t sa = base + r_bytes + st * stage_bytes;
@@ -342,6 +354,19 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       typename std::conditional<X3, float[4][UT], Bf16Vec<UT>[4]>::type gv;
       typename std::conditional<X3, float[UT], Bf16Vec<UT>>::type cp;
       float dyv[UT];
+#ifdef SL_EXPERIMENTS
+      if (active && (a.debug_flags & 16)) {  // timing experiment: no saved-activation / dy loads
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+          if constexpr (X3) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) gv[g][u] = 0.5f;
+            cp[u] = 0.1f;
+          }
+          dyv[u] = 0.01f;
+        }
+      } else
+#endif
       if (active) {  // prefetch this step's saved activations and upstream grad
         const bool vec = nu == UT && (UT % 4) == 0 && (H % 4) == 0;
         if constexpr (X3) {
@@ -358,6 +383,13 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
       float dh[UT];
       const bool tr0 = e == 0 && lane == 0;
       if (tr0) TRB(it, 12);
+#ifdef SL_EXPERIMENTS
+      if (tr0 && trace && it == 0) {  // placement: the SM this CTA runs on
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trace[31] = smid;
+      }
+#endif
       tc::mbar_wait(&tfull_bar[mt], it & 1);
       tc::fence_after_sync();
       if (tr0) TRB(it, 8);
@@ -455,11 +487,19 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             }
           }
           if constexpr (X3) {  // the reference's adjoint, fp32 (tape.cpp:1157-1170)
+            float tcs[UT];  // tanh(c_s), two units per paired instruction (two-MUFU tanh, abs. error ~1e-7)
+#pragma unroll
+            for (int u = 0; u < UT; u += 2) {
+              const float2 c2 = make_float2(gv[1][u] * cp[u] + gv[0][u] * gv[2][u],
+                                            gv[1][u + 1] * cp[u + 1] + gv[0][u + 1] * gv[2][u + 1]);
+              const float2 t2 = fm::tanh2(c2);
+              tcs[u] = t2.x, tcs[u + 1] = t2.y;
+            }
 #pragma unroll
             for (int u = 0; u < UT; ++u) {
               const float gh = dh[u] + dyv[u], gc = gcar[u];
               const float gi = gv[0][u], gf = gv[1][u], gg = gv[2][u], go = gv[3][u];
-              const float tcv = tanhf(gf * cp[u] + gi * gg);
+              const float tcv = tcs[u];
               const float d_o = gh * tcv;
               const float dcn = gc + gh * go * (1.f - tcv * tcv);
               gcar[u] = dcn * gf;
@@ -549,7 +589,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
             mbar_arrive_remote_relaxed(mapa(tc::smem_u32(&free_bar[MODE == kX3C ? 0 : mt][r]), (r + pi) % C),
                                        kEpiTile);
       }
-      if (valid_row) {  // the K4 operand copy is off the cross-CTA critical path
+#ifdef SL_EXPERIMENTS
+      const bool skip_k4 = (a.debug_flags & 8) != 0;  // timing experiment: no K4 operand copy
+#else
+      constexpr bool skip_k4 = false;
+#endif
+      if (valid_row && !skip_k4) {  // the K4 operand copy is off the cross-CTA critical path
         if constexpr (X3) {  // the split image the K4 GEMMs read: hi and lo
           __nv_bfloat16* zh = a.dzimg + pos * a.dzcat_ld + (size_t)gdir * a.dz_dir_off + ut0;
           __nv_bfloat16* zl = zh + a.dzimg_rows * a.dzcat_ld;
@@ -599,13 +644,20 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 // One CTA per packed row; threads along kk (coalesced on both sides), 32-bit math.
 template <bool LO>
 __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U, int NB, int P,
-                               int Kc, __nv_bfloat16* __restrict__ RB) {
+                               int Kc, __nv_bfloat16* __restrict__ RB, bool interleave = false) {
   const int rowi = blockIdx.x;
   const int cta = rowi / NB, n = rowi % NB;
   const int cl = cta / C, r = cta % C;
   const int unit = cl * C * U + n;
   const bool live = n < C * U && unit < H;
   __nv_bfloat16* dst = RB + ((LO ? (size_t)P * NB : 0) + rowi) * Kc;
+  // interleave (the streamed R_lo of kX3C): the lo rows in the core-matrix layout
+  // [Kc / 8][P * NB rows][8], so a TMA box of NB rows x 8 K is one contiguous 128 B-row run
+  // (16 B rows of a row-major slice would cost one TMA request each)
+  __nv_bfloat16* ilv = RB + (size_t)P * NB * Kc;
+  auto at = [&](int kk) -> __nv_bfloat16* {
+    return interleave ? ilv + ((size_t)(kk / 8) * P * NB + rowi) * 8 + kk % 8 : dst + kk;
+  };
   auto cvt = [](float v) {
     return __float2bfloat16_rn(LO ? v - __bfloat162float(__float2bfloat16_rn(v)) : v);
   };
@@ -614,7 +666,7 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
     for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
       const int col = r * Kc + kk, g = col / hq8, u = col % hq8;
       const float v = (live && g < 4 && u < H) ? __ldg(R + (size_t)unit * 4 * H + (size_t)g * H + u) : 0.f;
-      dst[kk] = cvt(v);
+      *at(kk) = cvt(v);
     }
     return;
   }
@@ -635,10 +687,10 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
       const __nv_bfloat16 b0 = cvt(v[0]), b1 = cvt(v[1]), b2 = cvt(v[2]), b3 = cvt(v[3]);
       __nv_bfloat162 p0, p1;
       p0.x = b0, p0.y = b1, p1.x = b2, p1.y = b3;
-      *reinterpret_cast<uint2*>(dst + kk) =
+      *reinterpret_cast<uint2*>(at(kk)) =
           make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
     } else {
-      for (int u = 0; u < 4 && kk + u < Kc; ++u) dst[kk + u] = cvt(v[u]);
+      for (int u = 0; u < 4 && kk + u < Kc; ++u) *at(kk + u) = cvt(v[u]);
     }
   }
 }
@@ -814,7 +866,8 @@ void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat
   const int Kc = sh.Kz / sh.C;
   pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
   SL_CUDA_TRY(cudaGetLastError());
-  pack_rb_kernel<true><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  pack_rb_kernel<true><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB,
+                                                                   sh.pair == 2);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch(2);
 }
@@ -838,11 +891,11 @@ void rec_bwd_x3(const TcRecBwdArgs& a0, const TcBwdShape& sh, const __nv_bfloat1
     mp.R[k] = tmap(RB[k], 2, rd, rs, rb);
     mp.Z[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, stage_k(mode, 1));
     mp.Zlo[k] = dz_ring_map(a.dzring_lo[k], a.B, a.Kz, stage_k(mode, 1));
-    if (mode == kX3C) {  // R_lo rows as {8 k, rows, K chunks of 8}: a box lands as [kk / 8][NB rows][8]
-      cuuint64_t ld[3] = {8, (cuuint64_t)2 * a.P * NB, (cuuint64_t)Kc / 8};
-      cuuint64_t ls[2] = {(cuuint64_t)Kc * 2, 16};
-      cuuint32_t lb[3] = {8, (cuuint32_t)NB, (cuuint32_t)stage_k(kX3C, 1) / 8};
-      mp.Rlo[k] = tmap(RB[k], 3, ld, ls, lb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (mode == kX3C) {  // interleaved R_lo {8 rows x 8 k, row groups, K chunks}: lands as [kk / 8][NB rows][8]
+      cuuint64_t ld[3] = {64, (cuuint64_t)a.P * NB / 8, (cuuint64_t)Kc / 8};
+      cuuint64_t ls[2] = {128, (cuuint64_t)a.P * NB * 16};
+      cuuint32_t lb[3] = {64, (cuuint32_t)NB / 8, (cuuint32_t)stage_k(kX3C, 1) / 8};
+      mp.Rlo[k] = tmap(RB[k] + (size_t)a.P * NB * Kc, 3, ld, ls, lb, CU_TENSOR_MAP_SWIZZLE_NONE);
     }
   }
   a.stages = pick_stages(mode, sh, a.kb);

@@ -41,6 +41,7 @@
 #include "profile.h"
 #include "rec_tc.h"
 #include "rec_tc_common.cuh"
+#include "fastmath.cuh"
 
 namespace sl {
 namespace {
@@ -92,7 +93,6 @@ uint32_t pair_smem(int Kp, int stages, int kb) {
   } while (0)
 #endif
 
-__device__ __forceinline__ float sig_precise(float z) { return 1.0f / (1.0f + expf(-z)); }
 
 template <int MODE>
 __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
@@ -384,16 +384,22 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
 
       if (valid_row) {
         if (active) {
-          if constexpr (X3) {  // reference arithmetic: 1/(1+exp(-z)), tanh (tape.cpp:1119-1135)
+          if constexpr (X3) {  // 1/(1+exp(-z)), tanh (tape.cpp:1119-1135): two-MUFU forms, paired fp32
 #pragma unroll
-            for (int u = 0; u < kUT; ++u) {
-              const float gi = sig_precise(z[u] + xf[0][u]);
-              const float gf = sig_precise(z[kUT + u] + xf[1][u]);
-              const float gg = tanhf(z[2 * kUT + u] + xf[2][u]);
-              const float go = sig_precise(z[3 * kUT + u] + xf[3][u]);
-              z[u] = gi, z[kUT + u] = gf, z[2 * kUT + u] = gg, z[3 * kUT + u] = go;
-              cst[u] = gf * cst[u] + gi * gg;
-              hst[u] = go * tanhf(cst[u]);
+            for (int u = 0; u < kUT; u += 2) {
+              using fm::add2;
+              const float2 gi = fm::sigmoid2(add2(f2(z[u], z[u + 1]), f2(xf[0][u], xf[0][u + 1])));
+              const float2 gf = fm::sigmoid2(add2(f2(z[kUT + u], z[kUT + u + 1]), f2(xf[1][u], xf[1][u + 1])));
+              const float2 gg = fm::tanh2(add2(f2(z[2 * kUT + u], z[2 * kUT + u + 1]), f2(xf[2][u], xf[2][u + 1])));
+              const float2 go = fm::sigmoid2(add2(f2(z[3 * kUT + u], z[3 * kUT + u + 1]), f2(xf[3][u], xf[3][u + 1])));
+              z[u] = gi.x, z[u + 1] = gi.y;
+              z[kUT + u] = gf.x, z[kUT + u + 1] = gf.y;
+              z[2 * kUT + u] = gg.x, z[2 * kUT + u + 1] = gg.y;
+              z[3 * kUT + u] = go.x, z[3 * kUT + u + 1] = go.y;
+              const float2 cn = fm::fma2(gf, f2(cst[u], cst[u + 1]), fm::mul2(gi, gg));  // c = f c + i g
+              cst[u] = cn.x, cst[u + 1] = cn.y;
+              const float2 h = fm::mul2(go, fm::tanh2(cn));                              // h = o tanh(c)
+              hst[u] = h.x, hst[u + 1] = h.y;
             }
           } else {
 #pragma unroll

@@ -83,5 +83,22 @@ for e in ev:
 print("--- by (kernel, grid)")
 for k, (c, t) in sorted(byg.items(), key=lambda kv: -kv[1][1])[:a.top]:
     print(f"{k:80s} {c:6d} {t / 1e3:9.3f} ms {t / c:9.2f} us/call")
+# idle time between consecutive device activities (kernels + memcpy/memset), by pair
+acts = sorted([e for e in json.load(open(trace))["traceEvents"]
+               if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda e: e["ts"])
+gaps = collections.defaultdict(lambda: [0, 0.0])
+nm = lambda e: re.sub(r"^void ", "", re.sub(r"\(.*", "", e["name"].replace("sl::(anonymous namespace)::", "")))[:34]
+tot_gap = 0.0
+for p_, n_ in zip(acts, acts[1:]):
+    g = n_["ts"] - (p_["ts"] + p_["dur"])
+    if g > 0:
+        tot_gap += g
+        k = f"{nm(p_)} -> {nm(n_)}"
+        gaps[k][0] += 1
+        gaps[k][1] += g
+span = acts[-1]["ts"] + acts[-1]["dur"] - acts[0]["ts"]
+print(f"--- span {span / 1e3:.2f} ms, idle {tot_gap / 1e3:.2f} ms over {len(acts)} activities")
+for k, (c, t) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[:12]:
+    print(f"{k:75s} {c:5d} {t / 1e3:8.3f} ms {t / c:6.2f} us")
 os.remove(trace)
 json.dump({n: {"calls": c, "us": t} for n, (c, t) in rows}, open(os.path.join("gpurun_out", f"kprof_{a.precision}.json"), "w"), indent=0)

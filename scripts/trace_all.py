@@ -17,6 +17,7 @@ ap.add_argument("--T", type=int, default=60)
 ap.add_argument("--D", type=int, default=2000)
 ap.add_argument("--H", type=int, default=1000)
 ap.add_argument("--nd", type=int, default=2)
+ap.add_argument("--prec", default="bf16")
 a = ap.parse_args()
 B, T, D, H, nd = a.B, a.T, a.D, a.H, a.nd
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -26,7 +27,7 @@ s = H ** -0.5
 W = [(torch.rand(D, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
 R = [(torch.rand(H, 4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
 b = [(torch.rand(4 * H, device="cuda", generator=g) * 2 - 1) * s for _ in range(nd)]
-layer = lstm.LSTMLayer(B, T, D, H, nd, 1, "bf16")
+layer = lstm.LSTMLayer(B, T, D, H, nd, 1, a.prec)
 for _ in range(2):
     layer.forward(x, lens, W, R, b)
 torch.cuda.synchronize()

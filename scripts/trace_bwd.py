@@ -36,7 +36,7 @@ for _ in range(2):
 torch.cuda.synchronize()
 grid = 128
 L = lstm.lib()
-buf = torch.zeros(grid * T * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(grid * T * 32, dtype=torch.int64, device="cuda")
 layer.forward(x, lens, W, R, b)
 L.sl_debug_set_flags(int(os.environ.get("SL_FLAGS", "0")))
 L.sl_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), -1)
@@ -44,7 +44,7 @@ layer.backward(dy)
 torch.cuda.synchronize()
 L.sl_debug_set_trace(None, 0)
 L.sl_debug_set_flags(0)
-t = buf.view(grid, T, 16).cpu().double() / 1000.0
+t = buf.view(grid, T, 32).cpu().double() / 1000.0
 t = t - t[:, 1, 0].min()
 sl = slice(3, T - 3)
 med = lambda v: round(float(v.median()), 2)
@@ -81,3 +81,32 @@ for c in [lastc[0][0], lastc[0][0] ^ 1, 0]:
           f"last-full {float(r[2]-r[0]):.2f} | epi: loop {float(r[12]-r[0]):+.2f} tfull {float(r[8]-base):.2f} "
           f"sends {float(r[9]-base):.2f} recv {float(r[10]-base):.2f} sum {float(r[13]-base):.2f} "
           f"math {float(r[14]-base):.2f} ring {float(r[11]-base):.2f} pub {float(r[6]-base):.2f}")
+
+# lateness vs placement: mean tile-0 publish time relative to the step's median, per CTA
+raw = buf.view(grid, T, 32).cpu()
+smid = raw[:, 0, 31].tolist()
+late = (t[:, sl, 6] - t[:, sl, 6].median(dim=0).values).mean(dim=1)
+order = torch.argsort(late, descending=True).tolist()
+print("latest CTAs (cta, smid, mean lateness us):", [(c, int(smid[c]), round(float(late[c]), 2)) for c in order[:12]])
+print("earliest CTAs:", [(c, int(smid[c]), round(float(late[c]), 2)) for c in order[-8:]])
+import statistics
+lo = [float(late[c]) for c in range(grid) if smid[c] < 74]
+hi = [float(late[c]) for c in range(grid) if smid[c] >= 74]
+print(f"mean lateness smid<74: {statistics.mean(lo) if lo else 0:.2f} ({len(lo)}), smid>=74: {statistics.mean(hi) if hi else 0:.2f} ({len(hi)})")
+
+rawd = buf.view(grid, T, 32).cpu().double() / 1000.0
+for mt in (0, 1):
+    lastiss = (t[:, sl, 16 + mt] - t[:, sl, 3 * mt])  # first ready/issue -> last issue
+    waitful = rawd[:, sl, 18 + mt]                     # summed waits for a free slot
+    lastfull = t[:, sl, 2 + 3 * mt] - t[:, sl, 16 + mt]
+    print(f"tile {mt}: first->last issue median {float(lastiss.median()):.2f} us; ring-full waits {float(waitful.median()):.2f} us; last issue->last full {float(lastfull.median()):.2f} us")
+for mt in (0, 1):
+    lat = t[:, sl, 22 + mt] - t[:, sl, 20 + mt]
+    print(f"tile {mt}: mid-box issue -> full at the MMA: median {float(lat.median()):.2f} us, 90% {float(torch.quantile(lat.flatten(), 0.9)):.2f}")
+# epilogue phases by die (smid < 74 / >= 74)
+die = torch.tensor([1 if sm >= 74 else 0 for sm in smid])
+for dd in (0, 1):
+    m = die == dd
+    row = {k: round(float((t[m][:, sl, j] - t[m][:, sl, i]).median()), 2) for k, (i, j) in ph.items()}
+    strm = float((t[m][:, sl, 2] - t[m][:, sl, 1]).median())
+    print(f"die {dd} ({int(m.sum())} CTAs): stream {strm:.2f}", row)
