@@ -34,7 +34,7 @@ namespace sl {
 namespace {
 using namespace rtc;
 
-constexpr int kStages = 6;
+constexpr int kStages = 8;  // ring slots (kBF16 / kX3 use at most 6)
 constexpr int kBoxCtrs = 128;  // step counters per (direction, batch tile): one per DZ box
 constexpr uint32_t kTile = 128 * 64 * 2;  // 16 KB A tile
 constexpr uint32_t kSmemMax = 227 * 1024;
@@ -42,19 +42,21 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 __host__ __device__ constexpr int nb_of(int C, int U) { return C * U < 16 ? 16 : C * U; }
 
 // kBF16: bf16 R / DZ, both directions per launch; kX3: fp32-class, one direction per
-// launch, R hi + lo resident; kX3C: fp32-class, both directions per launch, R_hi
-// resident and R_lo streamed with DZ (a stage = [DZ_hi | DZ_lo | R_lo] of 32 K)
+// launch, R hi + lo resident; kX3C: fp32-class, both directions per launch, R_hi and
+// R_lo streamed with DZ (a stage = [DZ_hi | DZ_lo | R_lo | R_hi] of 32 K): with no
+// resident R the shared memory holds 8 such stages, and the per-step stream (DZ of
+// both tiles plus the CTA's R slice, ~1.5 MB) is no longer latency-bound on 3 slots
 enum BwdMode { kBF16 = 0, kX3 = 1, kX3C = 2 };
 
 // K elements of the DZ ring a stage carries: 64 * kb, or 32 for kX3C
 __host__ __device__ inline int stage_k(int mode, int kb) { return mode == kX3C ? 32 : 64 * kb; }
 __host__ __device__ inline uint32_t bwd_stage_bytes(int mode, int NB, int kb) {
   const int kk = stage_k(mode, kb);
-  return (uint32_t)(mode == kBF16 ? 1 : 2) * 128 * kk * 2 + (mode == kX3C ? (uint32_t)NB * kk * 2 : 0u);
+  return (uint32_t)(mode == kBF16 ? 1 : 2) * 128 * kk * 2 + (mode == kX3C ? 2u * NB * kk * 2 : 0u);
 }
 uint32_t bwd_smem_m(int mode, int C, int U, int Kc, int stages, int kb) {
   const int NB = nb_of(C, U);
-  const uint32_t rparts = mode == kX3 ? 2 : 1;
+  const uint32_t rparts = mode == kX3 ? 2 : mode == kX3C ? 0 : 1;  // resident R parts
   // [C-1 slots][128 rows][U] partials from the peers (bf16, x3: fp32): one buffer per
   // batch tile, or (kX3C) one buffer the two tiles use in turn
   const uint32_t recv = C > 1 ? (uint32_t)(mode == kX3C ? 1 : 2) * (C - 1) * U * 128 * (mode == kBF16 ? 2 : 4) : 0;
@@ -66,7 +68,7 @@ uint32_t bwd_smem(int C, int U, int Kc, int stages) { return bwd_smem_m(kBF16, C
 // TMA descriptors of one launch, per direction: R (resident rows; kX3: hi then lo),
 // the DZ ring (hi), the DZ_lo ring (x3), R_lo as 8-K core-matrix boxes (kX3C)
 struct BwdMaps {
-  CUtensorMap R[2], Z[2], Zlo[2], Rlo[2];
+  CUtensorMap R[2], Z[2], Zlo[2], Rlo[2], Rhi[2];
 };
 
 // C   CTAs per cluster = K-split factor over the 4H gate columns of DZ
@@ -103,11 +105,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const CUtensorMap* tmZ = &mp.Z[d];
   const CUtensorMap* tmZl = &mp.Zlo[d];
   const CUtensorMap* tmRl = &mp.Rlo[d];
+  const CUtensorMap* tmRh = &mp.Rhi[d];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
   const uint32_t r_part = (uint32_t)NB * Kc * 2;  // one precision part of the R slice
-  const uint32_t r_bytes = r_part * (MODE == kX3 ? 2 : 1);
+  const uint32_t r_bytes = r_part * (MODE == kX3 ? 2 : MODE == kX3C ? 0 : 1);  // resident R
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
   const int kst = stage_k(MODE, a.kb);           // DZ columns per stage (= per TMA box)
@@ -125,7 +128,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     tc::prefetch_tmap(tmR);
     tc::prefetch_tmap(tmZ);
     if (X3) tc::prefetch_tmap(tmZl);
-    if (MODE == kX3C) tc::prefetch_tmap(tmRl);
+    if (MODE == kX3C) {
+      tc::prefetch_tmap(tmRl);
+      tc::prefetch_tmap(tmRh);
+    }
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   if (warp == 0) {  // ---------------------------------------------- producer
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
-      for (int kc = 0; kc < nkc; ++kc) {
+      for (int kc = 0; kc < (MODE == kX3C ? 0 : nkc); ++kc) {  // (kX3C streams R with DZ)
         tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
         if constexpr (MODE == kX3)  // the lo rows follow the P * NB hi rows
           tc::tma_load_2d(sR + r_part + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, a.P * NB + cta * NB);
@@ -251,9 +257,12 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 #endif
               tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
               const int kcol8 = (r * Kc + kg * kst) / 8;  // the box's first 8-column chunk of the ring
-              if constexpr (MODE == kX3C)  // this box's R_lo rows (no dependency on the step)
+              if constexpr (MODE == kX3C) {  // this box's R_lo and R_hi rows (no dependency on the step)
                 tma_load_3d(sA + st * stage_bytes + 2 * part_bytes, tmRl, &full_bar[st], 0, (cta * NB) / 8,
                             (kg * kst) / 8);
+                tma_load_3d(sA + st * stage_bytes + 2 * part_bytes + NB * kst * 2, tmRh, &full_bar[st], 0,
+                            (cta * NB) / 8, (kg * kst) / 8);
+              }
               tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8, kcol8, slot);
               if constexpr (X3)
                 tma_load_4d(sA + st * stage_bytes + part_bytes, tmZl, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
@@ -295,7 +304,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               const int kk = k0 + 16 * k;
               const uint32_t sb = base + (uint32_t)(kk / 64) * NB * 128 + (uint32_t)((kk % 64) / 16) * 32;
               const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
-              const uint64_t bh = tc::make_sdesc(sb, 0, 1024);
+              // B_hi: resident SW128 rows, or (kX3C) the stage's [kst / 8][NB rows][8] core matrices
+              const uint64_t bh = MODE == kX3C
+                                      ? tc::make_sdesc_noswz(sa + 2 * part_bytes + NB * kst * 2 + k * 2 * NB * 16,
+                                                             NB * 16, 128)
+                                      : tc::make_sdesc(sb, 0, 1024);
               tc::mma_f16(tmem + mt * NB, ah, bh, idesc, (kq | k) != 0);
               if constexpr (X3) {
                 const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
@@ -654,7 +667,7 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   // interleave (the streamed R_lo of kX3C): the lo rows in the core-matrix layout
   // [Kc / 8][P * NB rows][8], so a TMA box of NB rows x 8 K is one contiguous 128 B-row run
   // (16 B rows of a row-major slice would cost one TMA request each)
-  __nv_bfloat16* ilv = RB + (size_t)P * NB * Kc;
+  __nv_bfloat16* ilv = RB + (LO ? (size_t)P * NB * Kc : 0);
   auto at = [&](int kk) -> __nv_bfloat16* {
     return interleave ? ilv + ((size_t)(kk / 8) * P * NB + rowi) * 8 + kk % 8 : dst + kk;
   };
@@ -757,7 +770,7 @@ void dispatch_bwd(const TcBwdShape& sh, int MT, const BwdMaps& mp, const TcRecBw
 
 int pick_stages(int mode, const TcBwdShape& sh, int kb) {
   const int Kc = sh.Kz / sh.C;
-  for (int st = kStages; st >= 2; --st)
+  for (int st = mode == kX3C ? kStages : 6; st >= 2; --st)
     if (bwd_smem_m(mode, sh.C, sh.U, Kc, st, kb) <= kSmemMax) return st;
   return 0;
 }
@@ -833,7 +846,7 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
 }
 
 TcBwdShape tc_rec_bwd_x3_shape(int H, int sms, int nd) {
-  if (nd == 2) {  // kX3C: both directions per launch, R_hi resident, R_lo streamed (4-CTA clusters)
+  if (nd == 2) {  // kX3C: both directions per launch, R streamed with DZ (4-CTA clusters)
     const int C = 4, U = 16;
     const int P = (int)ceil_div(H, (int64_t)C * U) * C;
     const int Kz = (int)round_up(4 * (int64_t)dz_ring_hq(H), 64 * C);
@@ -864,7 +877,8 @@ size_t tc_rec_bwd_x3_pack_elems(const TcBwdShape& sh) {
 void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream) {
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB,
+                                                                    sh.pair == 2);
   SL_CUDA_TRY(cudaGetLastError());
   pack_rb_kernel<true><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB,
                                                                    sh.pair == 2);
@@ -896,6 +910,7 @@ void rec_bwd_x3(const TcRecBwdArgs& a0, const TcBwdShape& sh, const __nv_bfloat1
       cuuint64_t ls[2] = {128, (cuuint64_t)a.P * NB * 16};
       cuuint32_t lb[3] = {64, (cuuint32_t)NB / 8, (cuuint32_t)stage_k(kX3C, 1) / 8};
       mp.Rlo[k] = tmap(RB[k] + (size_t)a.P * NB * Kc, 3, ld, ls, lb, CU_TENSOR_MAP_SWIZZLE_NONE);
+      mp.Rhi[k] = tmap(RB[k], 3, ld, ls, lb, CU_TENSOR_MAP_SWIZZLE_NONE);  // R_hi streamed the same way
     }
   }
   a.stages = pick_stages(mode, sh, a.kb);
