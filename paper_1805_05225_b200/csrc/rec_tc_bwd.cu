@@ -50,13 +50,15 @@ enum BwdMode { kBF16 = 0, kX3 = 1, kX3C = 2 };
 
 // K elements of the DZ ring a stage carries: 64 * kb, or 32 for kX3C
 __host__ __device__ inline int stage_k(int mode, int kb) { return mode == kX3C ? 32 : 64 * kb; }
+// kBF16 and kX3C stream the CTA's R slice with DZ (kX3C: hi and lo); kX3 keeps it resident
+__host__ __device__ inline bool stream_r(int mode) { return mode != kX3; }
 __host__ __device__ inline uint32_t bwd_stage_bytes(int mode, int NB, int kb) {
   const int kk = stage_k(mode, kb);
-  return (uint32_t)(mode == kBF16 ? 1 : 2) * 128 * kk * 2 + (mode == kX3C ? 2u * NB * kk * 2 : 0u);
+  return (uint32_t)(mode == kBF16 ? 1 : 2) * 128 * kk * 2 + (stream_r(mode) ? (mode == kX3C ? 2u : 1u) * NB * kk * 2 : 0u);
 }
 uint32_t bwd_smem_m(int mode, int C, int U, int Kc, int stages, int kb) {
   const int NB = nb_of(C, U);
-  const uint32_t rparts = mode == kX3 ? 2 : mode == kX3C ? 0 : 1;  // resident R parts
+  const uint32_t rparts = mode == kX3 ? 2 : 0;  // resident R parts
   // [C-1 slots][128 rows][U] partials from the peers (bf16, x3: fp32): one buffer per
   // batch tile, or (kX3C) one buffer the two tiles use in turn
   const uint32_t recv = C > 1 ? (uint32_t)(mode == kX3C ? 1 : 2) * (C - 1) * U * 128 * (mode == kBF16 ? 2 : 4) : 0;
@@ -110,12 +112,14 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   const uint32_t base = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - tc::smem_u32(smem_raw));
   const uint32_t r_part = (uint32_t)NB * Kc * 2;  // one precision part of the R slice
-  const uint32_t r_bytes = r_part * (MODE == kX3 ? 2 : MODE == kX3C ? 0 : 1);  // resident R
+  const uint32_t r_bytes = r_part * (MODE == kX3 ? 2 : 0);  // resident R (kX3 only)
   uint8_t* sR = smem;
   uint8_t* sA = smem + r_bytes;
   const int kst = stage_k(MODE, a.kb);           // DZ columns per stage (= per TMA box)
   const uint32_t part_bytes = 128u * kst * 2;    // one precision part of DZ in a stage
   const uint32_t stage_bytes = bwd_stage_bytes(MODE, NB, a.kb);
+  // the streamed R_hi rows follow DZ (and, kX3C, R_lo) in a stage
+  const uint32_t rhi_off = (X3 ? 2 : 1) * part_bytes + (MODE == kX3C ? (uint32_t)NB * kst * 2 : 0u);
   // [MT][C-1 slots][128 rows][U] partials from the peers: one buffer per
   // batch tile (a shared buffer would couple the two tiles' recurrences through
   // its free/full handshake) and row-major, so each sender thread writes its
@@ -128,10 +132,8 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
     tc::prefetch_tmap(tmR);
     tc::prefetch_tmap(tmZ);
     if (X3) tc::prefetch_tmap(tmZl);
-    if (MODE == kX3C) {
-      tc::prefetch_tmap(tmRl);
-      tc::prefetch_tmap(tmRh);
-    }
+    if (MODE == kX3C) tc::prefetch_tmap(tmRl);
+    if (MODE != kX3) tc::prefetch_tmap(tmRh);
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
   if (warp == 0) {  // ---------------------------------------------- producer
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(&r_bar, r_bytes);
-      for (int kc = 0; kc < (MODE == kX3C ? 0 : nkc); ++kc) {  // (kX3C streams R with DZ)
+      for (int kc = 0; kc < (MODE == kX3 ? nkc : 0); ++kc) {  // (kBF16 / kX3C stream R with DZ)
         tc::tma_load_2d(sR + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, cta * NB);
         if constexpr (MODE == kX3)  // the lo rows follow the P * NB hi rows
           tc::tma_load_2d(sR + r_part + (size_t)kc * NB * 128, tmR, &r_bar, kc * 64, a.P * NB + cta * NB);
@@ -257,12 +259,11 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 #endif
               tc::mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
               const int kcol8 = (r * Kc + kg * kst) / 8;  // the box's first 8-column chunk of the ring
-              if constexpr (MODE == kX3C) {  // this box's R_lo and R_hi rows (no dependency on the step)
+              if constexpr (MODE == kX3C)  // this box's R rows (no dependency on the step)
                 tma_load_3d(sA + st * stage_bytes + 2 * part_bytes, tmRl, &full_bar[st], 0, (cta * NB) / 8,
                             (kg * kst) / 8);
-                tma_load_3d(sA + st * stage_bytes + 2 * part_bytes + NB * kst * 2, tmRh, &full_bar[st], 0,
-                            (cta * NB) / 8, (kg * kst) / 8);
-              }
+              if constexpr (MODE != kX3)
+                tma_load_3d(sA + st * stage_bytes + rhi_off, tmRh, &full_bar[st], 0, (cta * NB) / 8, (kg * kst) / 8);
               tma_load_4d(sA + st * stage_bytes, tmZ, &full_bar[st], 0, (a.b0 + mt * 128) / 8, kcol8, slot);
               if constexpr (X3)
                 tma_load_4d(sA + st * stage_bytes + part_bytes, tmZl, &full_bar[st], 0, (a.b0 + mt * 128) / 8,
@@ -304,11 +305,9 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
               const int kk = k0 + 16 * k;
               const uint32_t sb = base + (uint32_t)(kk / 64) * NB * 128 + (uint32_t)((kk % 64) / 16) * 32;
               const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
-              // B_hi: resident SW128 rows, or (kX3C) the stage's [kst / 8][NB rows][8] core matrices
-              const uint64_t bh = MODE == kX3C
-                                      ? tc::make_sdesc_noswz(sa + 2 * part_bytes + NB * kst * 2 + k * 2 * NB * 16,
-                                                             NB * 16, 128)
-                                      : tc::make_sdesc(sb, 0, 1024);
+              // B_hi: the stage's [kst / 8][NB rows][8] core matrices, or (kX3) resident SW128 rows
+              const uint64_t bh = MODE != kX3 ? tc::make_sdesc_noswz(sa + rhi_off + k * 2 * NB * 16, NB * 16, 128)
+                                              : tc::make_sdesc(sb, 0, 1024);
               tc::mma_f16(tmem + mt * NB, ah, bh, idesc, (kq | k) != 0);
               if constexpr (X3) {
                 const uint64_t al = tc::make_sdesc_noswz(sa + part_bytes + k * 2 * 2048, 2048, 128);
@@ -770,7 +769,7 @@ void dispatch_bwd(const TcBwdShape& sh, int MT, const BwdMaps& mp, const TcRecBw
 
 int pick_stages(int mode, const TcBwdShape& sh, int kb) {
   const int Kc = sh.Kz / sh.C;
-  for (int st = mode == kX3C ? kStages : 6; st >= 2; --st)
+  for (int st = stream_r(mode) ? kStages : 6; st >= 2; --st)
     if (bwd_smem_m(mode, sh.C, sh.U, Kc, st, kb) <= kSmemMax) return st;
   return 0;
 }
@@ -807,7 +806,7 @@ void tc_rec_bwd_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16*
   }
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB);
+  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB, true);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }
@@ -832,6 +831,11 @@ void rec_bwd_tc(const TcRecBwdArgs& a0, const TcBwdShape& sh, __nv_bfloat16* con
     cuuint32_t rb[2] = {64, (cuuint32_t)NB};
     mp.R[k] = tmap(RB[k], 2, rd, rs, rb);
     mp.Z[k] = dz_ring_map(a.dzring[k], a.B, a.Kz, stage_k(kBF16, a.kb));
+    // R streamed with DZ, from its interleaved pack {8 rows x 8 k, row groups, K chunks}
+    cuuint64_t hd[3] = {64, (cuuint64_t)a.P * NB / 8, (cuuint64_t)Kc / 8};
+    cuuint64_t hs[2] = {128, (cuuint64_t)a.P * NB * 16};
+    cuuint32_t hb[3] = {64, (cuuint32_t)NB / 8, (cuuint32_t)stage_k(kBF16, a.kb) / 8};
+    mp.Rhi[k] = tmap(RB[k], 3, hd, hs, hb, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   a.stages = pick_stages(kBF16, sh, a.kb);
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_bwd_tc: R slice does not fit in shared memory");

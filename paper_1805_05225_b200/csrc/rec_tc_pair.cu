@@ -58,10 +58,11 @@ struct PairCfg {
   static constexpr int kPU = M == kX3 ? 16 : 32;           // hidden units per pair
   static constexpr int kN = 4 * kPU;                       // MMA N (both CTAs' R slices)
   static constexpr int kNHalf = kN / 2;                    // R^T rows held per CTA (per precision part)
-  static constexpr int kRParts = M == kX3 ? 2 : M == kX3C ? 0 : 1;  // resident R copies (hi, + lo)
+  static constexpr bool kStreamR = M != kX3;                // R (x3: hi and lo) streamed with h
+  static constexpr int kRParts = M == kX3 ? 2 : 0;           // resident R copies (kX3: hi + lo)
   static constexpr int kHParts = X3 ? 2 : 1;               // h copies per stage (hi, + lo)
   static constexpr uint32_t kRloBytes = M == kX3C ? kNHalf * 128 : 0;  // streamed R_lo per 64-K chunk
-  static constexpr uint32_t kRhiBytes = kRloBytes;                      // (kX3C streams R_hi too)
+  static constexpr uint32_t kRhiBytes = kStreamR ? kNHalf * 128 : 0;   // streamed R_hi per 64-K chunk
   static constexpr int kSplit = M == kX3C ? 4 : 2;         // epilogue threads per batch row
   static constexpr int kEpi = 128 * kSplit;                // epilogue threads
   static constexpr int kThreads = 64 + kEpi;
@@ -132,6 +133,8 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
   uint8_t* sH = smem + r_bytes;
   const uint32_t part_bytes = kChunk * a.kb;             // one precision part of h in a stage
   const uint32_t stage_bytes = stage_bytes_of<MODE>(a.kb);
+  // streamed R_hi chunks sit after h (and, kX3C, after R_lo) in a stage
+  const uint32_t rhi_off = Cfg::kHParts * part_bytes + a.kb * Cfg::kRloBytes;
 
   if (threadIdx.x == 0) {
     tmax_sh = 0;
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
     if (lane == 0) {
       const uint32_t r_bar_l = mapa(tc::smem_u32(&r_bar), 0);
       if (leader) tc::mbar_arrive_expect_tx(&r_bar, 2 * r_bytes);
-      for (int kc = 0; kc < (MODE == kX3C ? 0 : nkc); ++kc) {  // (kX3C streams R with h)
+      for (int kc = 0; kc < (Cfg::kStreamR ? 0 : nkc); ++kc) {  // (kBF16 / kX3C stream R with h)
         tma_load_2d_pair(sR + (size_t)kc * kNHalf * 128, tmR, r_bar_l, kc * 64, pair * kN + r * kNHalf);
         if constexpr (MODE == kX3)  // the lo rows follow the P * kN hi rows
           tma_load_2d_pair(sR + (size_t)(nkc + kc) * kNHalf * 128, tmR, r_bar_l, kc * 64,
@@ -241,11 +244,12 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
             tc::mbar_wait(&empty_bar[st], ph ^ 1);
             if (leader) tc::mbar_arrive_expect_tx(&full_bar[st], 2 * stage_bytes);
             const uint32_t fb = mapa(tc::smem_u32(&full_bar[st]), 0);
-            if constexpr (MODE == kX3C)  // this group's R_lo and R_hi chunks (no dependency on the step)
+            if constexpr (Cfg::kStreamR)  // this group's R chunks (no dependency on the step)
               for (int j = 0; j < a.kb; ++j) {
-                tma_load_2d_pair(sH + st * stage_bytes + 2 * part_bytes + j * Cfg::kRloBytes, tmR, fb,
-                                 (kg * a.kb + j) * 64, a.P * kN + pair * kN + r * kNHalf);
-                tma_load_2d_pair(sH + st * stage_bytes + 2 * part_bytes + (a.kb + j) * Cfg::kRloBytes, tmR, fb,
+                if constexpr (MODE == kX3C)
+                  tma_load_2d_pair(sH + st * stage_bytes + 2 * part_bytes + j * Cfg::kRloBytes, tmR, fb,
+                                   (kg * a.kb + j) * 64, a.P * kN + pair * kN + r * kNHalf);
+                tma_load_2d_pair(sH + st * stage_bytes + rhi_off + j * Cfg::kRhiBytes, tmR, fb,
                                  (kg * a.kb + j) * 64, pair * kN + r * kNHalf);
               }
             tma_load_4d_pair(sH + st * stage_bytes, tmH, fb, 0, (a.b0 + r * 128) / 8, kg * a.kb * 8, s & 1);
@@ -280,9 +284,8 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
             const int kc = kg * a.kb + j;
             const uint32_t sa = base + r_bytes + st * stage_bytes + j * kChunk;
             // R_hi: resident, or (kX3C) the stage's chunk (same SW128 rows)
-            const uint32_t sb = MODE == kX3C ? base + r_bytes + st * stage_bytes + 2 * part_bytes +
-                                                   (uint32_t)(a.kb + j) * Cfg::kRloBytes
-                                             : base + (uint32_t)kc * kNHalf * 128;
+            const uint32_t sb = Cfg::kStreamR ? base + r_bytes + st * stage_bytes + rhi_off + j * Cfg::kRhiBytes
+                                              : base + (uint32_t)kc * kNHalf * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ah = tc::make_sdesc_noswz(sa + k * 2 * 2048, 2048, 128);
