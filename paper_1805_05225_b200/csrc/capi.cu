@@ -105,7 +105,8 @@ size_t x3_gemm_ws(const Dims& d, bool bwd) {
 struct ReserveView {
   float* gates[2] = {nullptr, nullptr};
   float* cprev[2] = {nullptr, nullptr};
-  float* hprev[2] = {nullptr, nullptr};  // fp32 paths: h_{s-1} [B*T, H]
+  float* hprev[2] = {nullptr, nullptr};  // fp32 SIMT path: h_{s-1} [B*T, H]
+  __nv_bfloat16* hprevi[2] = {nullptr, nullptr};  // x3 path: h_{s-1} as its split image [2][B*T][x3_img_ld(H)]
   __nv_bfloat16* xb = nullptr;    // bf16 path: x in bf16 [B*T, Dp]
   __nv_bfloat16* wcat = nullptr;  // bf16 path: [W_fw | W_bw] bf16 [D, nd*G4p]
   __nv_bfloat16* hprevb[2] = {nullptr, nullptr};  // bf16 path: h_{s-1} [B*T, Hp]
@@ -158,7 +159,7 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
     } else if (use_x3(d, prec)) {  // x3: the same step-major saves in fp32
       r.gates[k] = c.take<float>((size_t)d.BT() * 4 * save_hq(d.H));
       r.cprev[k] = c.take<float>((size_t)d.BT() * save_hq(d.H));
-      r.hprev[k] = c.take<float>((size_t)d.BT() * d.H);
+      r.hprevi[k] = c.take<__nv_bfloat16>(x3_img_elems((int)d.BT(), d.H));
     } else {
       r.gates[k] = c.take<float>((size_t)d.BT() * 4 * d.H);
       r.cprev[k] = c.take<float>((size_t)d.BT() * d.H);
@@ -349,7 +350,8 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.y_ld = (int64_t)d.nd * d.H;
     a.h_last = h_last;
     a.c_last = c_last;
-    a.hprev_ld = d.H;
+    a.hprev_ld = x3_img_ld(d.H);  // h_{s-1} image rows
+    a.hprevi_lo = d.BT() * x3_img_ld(d.H);
     a.bar = w.bar;
     a.trace = g_rec_trace;  // (experiments builds stamp it; null otherwise)
     a.trace_cta = g_rec_trace_cta;
@@ -360,7 +362,7 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
       a.xwf[j] = w.xw[k];
       a.gatesf[j] = rv.gates[k];
       a.cprevf[j] = rv.cprev[k];
-      a.hprevf[j] = rv.hprev[k];
+      a.hprevi[j] = rv.hprevi[k];
       a.hbuf[j] = w.hbufb[k];
       a.hbuf_lo[j] = w.hbuflo[k];
       tc_rec_x3_pack(R[k], d.H, sh, w.rtx3[k], st);
@@ -445,8 +447,8 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     }
     if (want_r) {
       Phase ph(st, "k4_dr_gemm", 2.0 * M * (double)G * d.H);
-      gemm_f32x3_ex(true, false, d.H, (int)G, M, rv.hprev[k], d.H, nullptr, nullptr, 0, zk, beta, dR[k], G, nullptr,
-                    nullptr, 0, w.gws, st, 0, 0, zl, zlo);
+      gemm_f32x3_ex(true, false, d.H, (int)G, M, nullptr, 0, rv.hprevi[k], nullptr, 0, zk, beta, dR[k], G, nullptr,
+                    nullptr, 0, w.gws, st, x3_img_ld(d.H), (int64_t)M * x3_img_ld(d.H), zl, zlo);
     }
   }
 }

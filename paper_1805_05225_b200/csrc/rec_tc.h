@@ -58,7 +58,8 @@ struct TcRecFwdArgs {
   __nv_bfloat16* hbuf_lo[2];     // lo halves of h (h - bf16(h)), same ring layout as hbuf (the hi halves)
   float* gatesf[2];              // saved (i,f,g,o) fp32, step-major (gate_save_off)
   float* cprevf[2];              // saved c_{s-1} fp32, step-major (cprev_save_off)
-  float* hprevf[2];              // saved h_{s-1} fp32 [B*T, hprev_ld]
+  __nv_bfloat16* hprevi[2];      // saved h_{s-1} as its split image (K4 dR operand): hi [B*T, hprev_ld],
+  int64_t hprevi_lo;             // lo hprevi_lo elements further on
   int debug_flags;  // experiments only: 1 = skip MMAs, 2 = skip epilogue math/stores,
                     // 4 = no step-counter waits (wrong results)
 };

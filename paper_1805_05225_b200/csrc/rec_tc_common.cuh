@@ -163,6 +163,16 @@ __device__ __forceinline__ void store_bf16(__nv_bfloat16* dst, const float* v, i
     if (i >= done && i < nu) dst[i] = __float2bfloat16_rn(v[i]);
 }
 
+// v as its split-bf16 image: hi at dst, lo (v - bf16(v)) lo_off elements further on
+template <int U>
+__device__ __forceinline__ void store_split(__nv_bfloat16* dst, int64_t lo_off, const float* v, int nu) {
+  float l[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) l[u] = v[u] - __bfloat162float(__float2bfloat16_rn(v[u]));
+  store_bf16<U>(dst, v, nu);
+  store_bf16<U>(dst + lo_off, l, nu);
+}
+
 // zero-filled beyond nu; vec = the row pitch allows vector access at all
 template <int U>
 __device__ __forceinline__ void load_f32(const float* src, float* v, int nu, bool vec) {

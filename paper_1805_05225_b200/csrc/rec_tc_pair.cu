@@ -470,12 +470,12 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
             if (a.gatesf[d]) {  // the saved (c, h)_{prev} of each step, off the critical path
               if (s == 0) {
                 store_f32<kUT>(a.cprevf[d] + cprev_save_off(0, row, a.B, H, ut0), zero, nu);
-                store_f32<kUT>(a.hprevf[d] + pos * a.hprev_ld + ut0, zero, nu);
+                store_split<kUT>(a.hprevi[d] + pos * a.hprev_ld + ut0, a.hprevi_lo, zero, nu);
               }
               if (s + 1 < len) {
                 const size_t pn = (size_t)row * T + src_time(s + 1, len, dir);
                 store_f32<kUT>(a.cprevf[d] + cprev_save_off(s + 1, row, a.B, H, ut0), cst, nu);
-                store_f32<kUT>(a.hprevf[d] + pn * a.hprev_ld + ut0, hst, nu);
+                store_split<kUT>(a.hprevi[d] + pn * a.hprev_ld + ut0, a.hprevi_lo, hst, nu);
               }
             }
           } else {
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
         } else {  // padded position t == s: zero output (tape.cpp:797), frozen state
           if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)gdir * H + ut0, zero, nu);
           if constexpr (X3) {
-            if (a.gatesf[d]) store_f32<kUT>(a.hprevf[d] + pos * a.hprev_ld + ut0, zero, nu);
+            if (a.gatesf[d]) store_split<kUT>(a.hprevi[d] + pos * a.hprev_ld + ut0, a.hprevi_lo, zero, nu);
           } else {
             if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
             if (a.gates[d]) store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
         const size_t pos = (size_t)row * T + s;
         if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)gdir * H + ut0, zero, nu);
         if constexpr (X3) {
-          if (a.gatesf[d]) store_f32<kUT>(a.hprevf[d] + pos * a.hprev_ld + ut0, zero, nu);
+          if (a.gatesf[d]) store_split<kUT>(a.hprevi[d] + pos * a.hprev_ld + ut0, a.hprevi_lo, zero, nu);
         } else {
           if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
           if (a.gates[d]) store_bf16<kUT>(a.hprev[d] + pos * a.hprev_ld + ut0, zero, nu);
