@@ -50,8 +50,16 @@ struct X3Parts {
   int64_t stride, ld;
 };
 __device__ __forceinline__ float x3_parts_sum(const X3Parts& q, int64_t r, int64_t c) {
+  // the first 8 partials' loads all in flight before the (in-order) adds; a partial
+  // past n contributes an exact +0
+  const float* p = q.p + r * q.ld + c;
+  float v[8];
+#pragma unroll
+  for (int z = 0; z < 8; ++z) v[z] = z < q.n ? __ldg(p + z * q.stride) : 0.f;
   float s = 0.f;
-  for (int z = 0; z < q.n; ++z) s += q.p[z * q.stride + r * q.ld + c];
+#pragma unroll
+  for (int z = 0; z < 8; ++z) s += v[z];
+  for (int z = 8; z < q.n; ++z) s += __ldg(p + z * q.stride);
   return s;
 }
 size_t gemm_f32x3_parts_workspace_bytes(bool transA, bool transB, int M, int N, int K);
