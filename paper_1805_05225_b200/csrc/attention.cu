@@ -425,12 +425,12 @@ __global__ void __launch_bounds__(kThreads, DEFER ? 3 : 2) attn_bwd_de_kernel(At
             part[j] += pj.x + pj.y;
           }
         }
-        if (nv > 0) {
-          Vec<VK> ds;
+        // this chunk's d s_tr partial (every chunk writes, zeros past the length): summed
+        // in chunk order by attn_ds_sum_split_kernel — deterministic, no atomics
+        Vec<VK> ds;
 #pragma unroll
-          for (int i = 0; i < VK / 2; ++i) ds.f[2 * i] = ds2[i].x, ds.f[2 * i + 1] = ds2[i].y;
-          ds.atomic_add(p.d_s_tr + (size_t)b * K + k);
-        }
+        for (int i = 0; i < VK / 2; ++i) ds.f[2 * i] = ds2[i].x, ds.f[2 * i + 1] = ds2[i].y;
+        ds.store(p.ds_part + ((size_t)blockIdx.x * p.B + b) * K + k);
         return;
       }
     }
@@ -652,6 +652,24 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 4)
   }
 }
 
+// d s_tr = sum over the source chunks (in order) of the tanh pass's partials, written
+// as fp32 (the deferred d W_s GEMM's operand) and as its split image (the per-step
+// d s = d s_tr W_s^T GEMM's A operand: hi [B, ld], lo lo_off further on)
+__global__ void attn_ds_sum_split_kernel(const float* __restrict__ part, int nchunk, int B, int K, float* out,
+                                         __nv_bfloat16* img, int64_t ld, int64_t lo_off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * ld) return;
+  const int b = (int)(i / ld), k = (int)(i % ld);
+  float v = 0.f;
+  if (k < K) {
+    for (int c = 0; c < nchunk; ++c) v += __ldg(part + ((size_t)c * B + b) * K + k);
+    out[(size_t)b * K + k] = v;
+  }
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  img[i] = h;
+  img[lo_off + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+
 // column sums of d_s_tr [B, K] into d_b_s (+=)
 __global__ void colsum_kernel(const float* x, int rows, int cols, float* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -674,7 +692,14 @@ static size_t x3_bytes(int B, int K, int H) {
 static size_t ws_head(int B, int K, int Ts) {
   return (size_t)round_up((int64_t)2 * B * K * sizeof(float), 256) + (size_t)round_up((int64_t)B * Ts * 4, 256);
 }
-size_t attention_workspace_bytes(int B, int K, int H, int Ts) { return ws_head(B, K, Ts) + x3_bytes(B, K, H) + 256; }
+// after the GEMM scratch: the deferred backward's per-chunk d s_tr partials
+static size_t ds_part_bytes(int B, int K, int Ts) { return (size_t)ceil_div(Ts, kJE) * B * K * sizeof(float); }
+size_t attention_workspace_bytes(int B, int K, int H, int Ts) {
+  return ws_head(B, K, Ts) + round_up(x3_bytes(B, K, H), 256) + ds_part_bytes(B, K, Ts) + 256;
+}
+static float* ds_part_buf(const AttnArgs& p, void* ws) {
+  return reinterpret_cast<float*>(static_cast<char*>(ws) + ws_head(p.B, p.K, p.Ts) + round_up(x3_bytes(p.B, p.K, p.H), 256));
+}
 static float* row_buf(const AttnArgs& p, void* ws) {  // e (forward) / d_a (backward) [B, Ts]
   return reinterpret_cast<float*>(static_cast<char*>(ws) + round_up((int64_t)2 * p.B * p.K * sizeof(float), 256));
 }
@@ -761,7 +786,9 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     if (d_b_s && !d_W_s) SL_CUDA_TRY(cudaMemsetAsync(d_b_s, 0, sizeof(float) * p.K, st));
   }
   float* d_a = row_buf(p, ws);
-  SL_CUDA_TRY(cudaMemsetAsync(p.d_s_tr, 0, sizeof(float) * p.B * p.K, st));
+  const bool ds_split = p.defer && vec_k(p) == 4;  // the paired tanh pass writes per-chunk partials
+  p.ds_part = ds_split ? ds_part_buf(p, ws) : nullptr;
+  if (!ds_split) SL_CUDA_TRY(cudaMemsetAsync(p.d_s_tr, 0, sizeof(float) * p.B * p.K, st));
   {
     Phase ph(st, "k8_attention_bwd", 0.0, 4.0 * p.B * p.Ts * (double)(2 * p.K + 2 * p.E));
     const dim3 g((unsigned)ceil_div(p.Ts, kJC), (unsigned)p.B), ge((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
@@ -775,9 +802,20 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
     count_launch(2);
   }
   const float beta = p.accumulate ? 1.f : 0.f;
+  const __nv_bfloat16* ds_img = nullptr;  // d s_tr's split image (deferred mode)
+  const int64_t ds_ld = x3_img_ld(p.K);
+  if (ds_split) {  // d s_tr = the chunks' partials summed in order, + its image for the d s GEMM
+    auto* img = static_cast<__nv_bfloat16*>(x3_ws(p, ws));  // the GEMM scratch's A-image slot
+    const int nchunk = (int)ceil_div(p.Ts, kJE);
+    attn_ds_sum_split_kernel<<<(unsigned)ceil_div((int64_t)p.B * ds_ld, 256), 256, 0, st>>>(
+        p.ds_part, nchunk, p.B, p.K, p.d_s_tr, img, ds_ld, (int64_t)p.B * ds_ld);
+    SL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    ds_img = img;
+  }
   if (d_s && p.W_s3_bwd && p.ds_parts_out)  // d s = d s_tr W_s^T, summed by the caller's consumer
-    *p.ds_parts_out = gemm_f32x3_parts(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, nullptr, nullptr, 0, p.W_s3_bwd,
-                                       x3_ws(p, ws), st);
+    *p.ds_parts_out = gemm_f32x3_parts(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, ds_img, nullptr, 0, p.W_s3_bwd,
+                                       x3_ws(p, ws), st, ds_img ? ds_ld : 0, ds_img ? (int64_t)p.B * ds_ld : 0);
   else if (d_s && p.W_s3_bwd)  // d s = d s_tr W_s^T
     gemm_f32x3_pb(false, true, p.B, p.H, p.K, p.d_s_tr, p.K, p.W_s3_bwd, beta, d_s, p.H, nullptr, x3_ws(p, ws), st);
   else if (d_s)

@@ -66,6 +66,8 @@ struct AttnArgs {
   int64_t att_img_ld, att_img_lo;
   const __nv_bfloat16* s_img;
   int64_t s_img_ld, s_img_lo;
+  // (internal) deferred backward: the tanh pass's per-chunk d s_tr partials
+  float* ds_part;
 };
 
 size_t attention_workspace_bytes(int B, int K, int H, int Ts);

@@ -40,3 +40,24 @@ def test_layer_fwd_bwd_bitwise_repeatable(cuda, prec, B, T, D, H):
             continue
         for k, (a, r) in enumerate(zip(out, ref)):
             assert torch.equal(a, r), (it, k, float((a - r).abs().max()))
+
+
+def test_decoder_f32_bitwise_repeatable(cuda):
+    """The fp32 attention decoder (per-step split-K partials summed in a fixed
+    order by their consumers, d s_tr from per-chunk partials, the deferred
+    accumulations reduced in slices): bitwise identical over repeated runs."""
+    from test_decoder_f32_gpu import run_f32
+    from test_decoder_gpu import make_case
+    import numpy as np
+    dims = (16, 11, 7, 24, 40, 32, 24, 28, 30)  # B, Ts, T, emb, enc, hidden, key, readout, V
+    P, enc_b, lens, ids, d_ro = make_case(sum(dims), *dims)
+    enc_x = np.random.default_rng(3).uniform(-1, 1, enc_b.shape).astype(np.float32)
+    ref = None
+    for it in range(6):
+        ro, grads, d_enc = run_f32(dims, P, enc_x, lens, ids, d_ro)
+        out = [ro.clone(), d_enc.clone()] + [grads[k].clone() for k in sorted(grads)]
+        if ref is None:
+            ref = out
+            continue
+        for k, (a, r) in enumerate(zip(out, ref)):
+            assert torch.equal(a, r), (it, k)
