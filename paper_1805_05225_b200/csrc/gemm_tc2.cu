@@ -53,7 +53,21 @@ struct P2 {
   int ksplit, kb_per;    // split-K: work unit t -> tile t % tiles, K blocks [z kb_per, (z + 1) kb_per), z = t / tiles
   int64_t split_stride;  // ... written to C + z * split_stride
   int kchunk;            // CHUNK kernels: K blocks per accumulation chunk
+  int group_m;           // rasterisation group (tile_mn)
 };
+
+// Output tile of a tile index: grouped rasterisation — consecutive indices walk GM
+// M-tiles (p.group_m) before the next N-tile, so the ~74 tiles in flight at once share
+// GM A row-blocks and ~74/GM B column-blocks and their operands stay L2-resident
+// (M-fastest over all nm M-tiles re-streamed A from HBM once per N-tile).
+__device__ __forceinline__ void tile_mn(const P2& p, int tile, int& mi, int& ni) {
+  const int gm = p.group_m;
+  const int per_group = gm * p.nn;
+  const int g = tile / per_group, l = tile % per_group;
+  const int rows = min(gm, p.nm - g * gm);  // the last group may be narrower
+  mi = g * gm + l % rows;
+  ni = l / rows;
+}
 
 // K-block range of work unit t (split-K; ksplit == 1: the whole K)
 __device__ __forceinline__ void unit_kb(const P2& p, int t, int& tile, int& kb0, int& kb1, int& z) {
@@ -236,7 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       for (int t = pair; t < ntiles; t += npairs) {
         int tile, kb0, kb1, z;
         unit_kb(p, t, tile, kb0, kb1, z);
-        const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP + r * 128;
+        int mi, ni;
+        tile_mn(p, tile, mi, ni);
+        const int m0 = mi * BMP + r * 128, n0 = ni * BNP + r * 128;
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty_bar[st], ph ^ 1);
           const uint32_t sa = base + st * SB, sb = sa + kHalf;
@@ -318,7 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       for (int t = pair; t < ntiles; t += npairs) {
         int tile, kb0, kb1, z;
         unit_kb(p, t, tile, kb0, kb1, z);
-        const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP;
+        int mi, ni;
+        tile_mn(p, tile, mi, ni);
+        const int m0 = mi * BMP + r * 128, n0 = ni * BNP;
         float sum[128];  // this thread's row x the warp's 128 columns, summed over the chunks in fp32
 #pragma unroll
         for (int j = 0; j < 128; ++j) sum[j] = 0.f;
@@ -358,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       const int acc = it & 1;
       int tile, kb0, kb1, z;
       unit_kb(p, t, tile, kb0, kb1, z);
-      const int m0 = (tile % p.nm) * BMP + r * 128, n0 = (tile / p.nm) * BNP;
+      int mi, ni;
+      tile_mn(p, tile, mi, ni);
+      const int m0 = mi * BMP + r * 128, n0 = ni * BNP;
       tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       if (warp == 2 && lane == 0 && it == 0) GT(4);
       tc::fence_after_sync();
@@ -657,6 +677,7 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   SL_REQUIRE(!g.sm_part || (g.Cb && g.sm_targets), SL_ERR_INVALID_ARGUMENT,
              "gemm: softmax partials need the bf16 output and the targets");
   p.kchunk = g.kchunk;
+  p.group_m = std::max(1, std::min(p.nm, 8));
   if (g.kchunk > 0)
     SL_REQUIRE(!g.Cb && !g.sm_part, SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: chunked accumulation writes fp32 C");
   const bool x3 = g.A_lo != nullptr;
