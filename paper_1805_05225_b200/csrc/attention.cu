@@ -13,8 +13,6 @@
 // (gemm_f32x3.cu).  fp32 data: the step is bandwidth-bound, not tensor-bound.
 #include <algorithm>
 
-#include <cooperative_groups.h>
-
 #include "attention.h"
 #include "fastmath.cuh"
 #include "gemm.h"
@@ -176,29 +174,55 @@ template <int VK>
 __global__ void __launch_bounds__(kThreads, 3) attn_energy_kernel(AttnArgs p, float* __restrict__ e_out) {
   __shared__ float red[kWarps * kJE];
   const int b = blockIdx.y, j0 = blockIdx.x * kJE, K = p.K, Ts = p.Ts;
-  const int len = min(max(p.lens[b], 0), Ts);
-  const int n = min(kJE, len - j0);
-  if (n <= 0) return;
-  float part[kJE], acc[kJE];
+  const int nT = min(kJE, Ts - j0);  // the chunk's positions (no dependency on the length)
+  // the chunk's energy inputs and column constants are loaded first, so the latency of
+  // the length lookup hides under them
+  const int kf = threadIdx.x * VK;
+  Vec<VK> c0, w0, v0, x0[kJE];
+  float acc[kJE], part[kJE];
+  if (kf < K) {
+    load_cols(p, b, kf, c0, w0, v0);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < nT) x0[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + kf);
+  }
 #pragma unroll
   for (int j = 0; j < kJE; ++j) {
     part[j] = 0.f;
-    acc[j] = j < n ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
+    acc[j] = j < nT ? __ldg(p.accum + (size_t)b * Ts + j0 + j) : 0.f;
   }
-  for (int k = threadIdx.x * VK; k < K; k += kThreads * VK) {
-    Vec<VK> c, w, v;
-    load_cols(p, b, k, c, w, v);
-    Vec<VK> x[kJE];
-#pragma unroll
-    for (int j = 0; j < kJE; ++j)
-      if (j < n) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+  const int len = min(max(p.lens[b], 0), Ts);
+  const int n = min(kJE, len - j0);
+  if (n <= 0) return;
+  auto cols = [&](const Vec<VK>& c, const Vec<VK>& w, const Vec<VK>& v, const Vec<VK>(&x)[kJE]) {
 #pragma unroll
     for (int j = 0; j < kJE; ++j) {
       if (j < n) {
+        if constexpr (VK % 2 == 0) {  // paired-fp32 math, two columns per instruction
+          using namespace fm;
+          float2 s2v = s2(0.f);
 #pragma unroll
-        for (int i = 0; i < VK; ++i) part[j] += v.f[i] * tanh_fast(x[j].f[i] + acc[j] * w.f[i] + c.f[i]);
+          for (int i = 0; i < VK; i += 2) {
+            const float2 t = tanh2(fma2(s2(acc[j]), make_float2(w.f[i], w.f[i + 1]),
+                                        add2(make_float2(x[j].f[i], x[j].f[i + 1]), make_float2(c.f[i], c.f[i + 1]))));
+            s2v = fma2(make_float2(v.f[i], v.f[i + 1]), t, s2v);
+          }
+          part[j] += s2v.x + s2v.y;
+        } else {
+#pragma unroll
+          for (int i = 0; i < VK; ++i) part[j] += v.f[i] * tanh_fast(x[j].f[i] + acc[j] * w.f[i] + c.f[i]);
+        }
       }
     }
+  };
+  if (kf < K) cols(c0, w0, v0, x0);
+  for (int k = kf + kThreads * VK; k < K; k += kThreads * VK) {
+    Vec<VK> c, w, v, x[kJE];
+    load_cols(p, b, k, c, w, v);
+#pragma unroll
+    for (int j = 0; j < kJE; ++j)
+      if (j < n) x[j].load(p.enc_ctx + ((size_t)b * Ts + j0 + j) * K + k);
+    cols(c, w, v, x);
   }
   block_reduce_chunk(part, n, red, e_out + (size_t)b * Ts + j0);
 }
@@ -225,6 +249,17 @@ template <int VE>
 __global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(AttnArgs p, const float* __restrict__ e) {
   extern __shared__ float a_sh[];  // [Ts] then [kCtxGroups - 1][kCtxThreads * VE] partials
   const int b = blockIdx.y, Ts = p.Ts, E = p.E;
+  const int ct = threadIdx.x % kCtxThreads, grp = threadIdx.x / kCtxThreads;
+  const int x = (blockIdx.x * kCtxThreads + ct) * VE;
+  constexpr int G = kCtxGroups;
+  // the first 4 encoder rows of the thread's group do not depend on the softmax: their
+  // loads go out before it (a_j = 0 past the length masks them)
+  Vec<VE> pre[4];
+  const bool use_pre = x < E && grp + 3 * G < Ts;
+  if (use_pre) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pre[i].load(p.enc + ((size_t)b * Ts + grp + i * G) * E + x);
+  }
   const int len = min(max(p.lens[b], 0), Ts);
   if (threadIdx.x < 32) row_softmax(p, e, b, len, a_sh);
   __syncthreads();
@@ -233,14 +268,20 @@ __global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(
       p.a[(size_t)b * Ts + j] = a_sh[j];
       p.accum_out[(size_t)b * Ts + j] = p.accum[(size_t)b * Ts + j] + a_sh[j];
     }
-  const int ct = threadIdx.x % kCtxThreads, grp = threadIdx.x / kCtxThreads;
-  const int x = (blockIdx.x * kCtxThreads + ct) * VE;
   float* part = a_sh + round_up_dev(Ts, 8);
   Vec<VE> s;
   s.zero();
   if (x < E) {
     int j = grp;
-    constexpr int G = kCtxGroups;
+    if (use_pre) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float aj = a_sh[grp + i * G];
+#pragma unroll
+        for (int w = 0; w < VE; ++w) s.f[w] += aj * pre[i].f[w];
+      }
+      j = grp + 4 * G;
+    }
     for (; j + 3 * G < len; j += 4 * G) {  // 4 independent loads in flight per thread
       Vec<VE> q[4];
 #pragma unroll
@@ -274,6 +315,15 @@ __global__ void __launch_bounds__(kCtxThreads * kCtxGroups) attn_context_kernel(
 #pragma unroll
     for (int c = 0; c < 2; ++c)
       if (p.att_copy[c]) s.store(p.att_copy[c] + (size_t)b * p.att_copy_ld[c] + x);
+    if (p.att_img) {  // att's split image rows (hi, lo)
+      __nv_bfloat16* dst = p.att_img + (size_t)b * p.att_img_ld + x;
+#pragma unroll
+      for (int w = 0; w < VE; ++w) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(s.f[w]);
+        dst[w] = h;
+        dst[p.att_img_lo + w] = __float2bfloat16_rn(s.f[w] - __bfloat162float(h));
+      }
+    }
   }
 }
 
@@ -493,165 +543,6 @@ __global__ void __launch_bounds__(kThreads, DEFER ? 3 : 2) attn_bwd_de_kernel(At
   }
 }
 
-// ---- Cluster form of the forward: one 4-CTA cluster per batch row walks the row's
-// [Ts, K] energy inputs and [Ts, E] encoder states once: energies of a quarter of
-// the positions per CTA (warp per position, lanes along K) -> DSMEM broadcast ->
-// masked softmax (every CTA) -> context columns of a quarter of E per CTA (thread
-// per 4 columns, two position groups), written to att and its copies.  One launch
-// instead of two and no e round trip (43-47 us vs 50 us per config-4 step).  The
-// same decomposition for the backward measured slower than the chunked kernels
-// (cluster-barrier waits), so the backward keeps them.
-namespace cg = cooperative_groups;
-constexpr int kCl = 4;            // CTAs per cluster (per batch row)
-constexpr int kClThreads = 256;   // 8 warps
-constexpr int kClWarps = kClThreads / 32;
-
-__device__ __forceinline__ float4 ldg4(const float* q) { return __ldg(reinterpret_cast<const float4*>(q)); }
-__device__ __forceinline__ float4 lds4(const float* q) { return *reinterpret_cast<const float4*>(q); }
-
-struct ClSmem {  // float offsets into the dynamic shared memory
-  int c, w, v, e, part, total;
-};
-__host__ __device__ inline ClSmem cl_smem(int K, int Ts) {
-  const int K4 = (K + 3) / 4 * 4, T4 = (Ts + 3) / 4 * 4;
-  ClSmem m;
-  m.c = 0;
-  m.w = m.c + K4;
-  m.v = m.w + K4;
-  m.e = m.v + K4;         // e, then a (in place)
-  m.part = m.e + T4;      // context partials of position group 1: 128 float4
-  m.total = m.part + 512;
-  return m;
-}
-
-__device__ __forceinline__ void cl_stage_cols(const AttnArgs& p, int b, float* sh, const ClSmem& m, int r) {
-  for (int k = threadIdx.x; k < p.K; k += kClThreads) {
-    float str;
-    if (p.s_tr_parts.n > 0) {  // s_tr = s W_s + b_s from the projection's split-K partials
-      str = x3_parts_sum(p.s_tr_parts, b, k) + p.s_tr_bias[k];
-      if (r == 0) p.s_tr[(size_t)b * p.K + k] = str;
-    } else {
-      str = p.s_tr[(size_t)b * p.K + k];
-    }
-    sh[m.c + k] = str + p.b_fb[k];
-    sh[m.w + k] = p.W_fb[k];
-    sh[m.v + k] = p.v[k];
-  }
-}
-
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kClThreads, 4)
-    attn_fwd_cluster_kernel(AttnArgs p) {
-  extern __shared__ float4 sh4[];
-  float* sh = reinterpret_cast<float*>(sh4);
-  cg::cluster_group cl = cg::this_cluster();
-  const int r = (int)cl.block_rank(), b = blockIdx.y, Ts = p.Ts, K = p.K, E = p.E;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int len = min(max(p.lens[b], 0), Ts);
-  const ClSmem m = cl_smem(K, Ts);
-  cl_stage_cols(p, b, sh, m, r);
-  __syncthreads();
-  // energies of positions j = r + kCl (warp + kClWarps i)
-  for (int j = r + kCl * warp; j < len; j += kCl * kClWarps) {
-    const float aj = __ldg(p.accum + (size_t)b * Ts + j);
-    const float* x = p.enc_ctx + ((size_t)b * Ts + j) * K;
-    float sum = 0.f;
-    for (int k0 = lane * 4; k0 < K; k0 += 128 * 8) {
-      float4 xv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) xv[u] = k0 + 128 * u < K ? ldg4(x + k0 + 128 * u) : make_float4(0, 0, 0, 0);
-      float2 s2v = fm::s2(0.f);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0 + 128 * u;
-        if (k < K) {  // paired-fp32 math, two columns per instruction
-          using namespace fm;
-          const float4 c = lds4(sh + m.c + k), w = lds4(sh + m.w + k), v = lds4(sh + m.v + k);
-          const float2 t0 = tanh2(fma2(s2(aj), make_float2(w.x, w.y), add2(make_float2(xv[u].x, xv[u].y),
-                                                                             make_float2(c.x, c.y))));
-          const float2 t1 = tanh2(fma2(s2(aj), make_float2(w.z, w.w), add2(make_float2(xv[u].z, xv[u].w),
-                                                                             make_float2(c.z, c.w))));
-          s2v = fma2(make_float2(v.x, v.y), t0, s2v);
-          s2v = fma2(make_float2(v.z, v.w), t1, s2v);
-        }
-      }
-      sum += s2v.x + s2v.y;
-    }
-    sum = warp_sum(sum);
-    if (lane < kCl) cl.map_shared_rank(sh + m.e, lane)[j] = sum;
-  }
-  cl.sync();
-  float* a_sh = sh + m.e;
-  if (warp == 0) {  // masked softmax (tape.cpp:952-960), in place
-    const float bv = *p.b_v;
-    float mx = -INFINITY;
-    for (int j = lane; j < len; j += 32) mx = fmaxf(mx, a_sh[j] + bv);
-    mx = warp_max(mx);
-    float z = 0.f;
-    for (int j = lane; j < len; j += 32) z += expf(a_sh[j] + bv - mx);
-    z = warp_sum(z);
-    for (int j = lane; j < Ts; j += 32) {
-      const float aj = j < len ? expf(a_sh[j] + bv - mx) / z : 0.f;
-      a_sh[j] = aj;
-      if (r == 0) {
-        p.a[(size_t)b * Ts + j] = aj;
-        p.accum_out[(size_t)b * Ts + j] = p.accum[(size_t)b * Ts + j] + aj;
-      }
-    }
-  }
-  __syncthreads();
-  // context columns [x0, x1) of this CTA: thread q of group g (positions j = g mod 2)
-  const int cols = (E / 4 + kCl - 1) / kCl * 4;
-  const int x0 = r * cols, x1 = min(E, x0 + cols);
-  const int g = threadIdx.x / 128, q = threadIdx.x % 128;
-  float4* part = reinterpret_cast<float4*>(sh + m.part);
-  for (int xb = x0; xb < x1; xb += 512) {
-    const int x = xb + 4 * q;
-    float4 acc = make_float4(0, 0, 0, 0);
-    if (x < x1) {
-      const float* src = p.enc + (size_t)b * Ts * E + x;
-      int j = g;
-      for (; j + 2 * 7 < len; j += 2 * 8) {
-        float4 ev[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) ev[u] = ldg4(src + (size_t)(j + 2 * u) * E);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float aj = a_sh[j + 2 * u];
-          acc.x += aj * ev[u].x, acc.y += aj * ev[u].y, acc.z += aj * ev[u].z, acc.w += aj * ev[u].w;
-        }
-      }
-      for (; j < len; j += 2) {
-        const float4 ev = ldg4(src + (size_t)j * E);
-        const float aj = a_sh[j];
-        acc.x += aj * ev.x, acc.y += aj * ev.y, acc.z += aj * ev.z, acc.w += aj * ev.w;
-      }
-    }
-    if (g == 1) part[q] = acc;
-    __syncthreads();
-    if (g == 0 && x < x1) {
-      const float4 o = part[q];
-      acc.x += o.x, acc.y += o.y, acc.z += o.z, acc.w += o.w;
-      *reinterpret_cast<float4*>(p.att + (size_t)b * E + x) = acc;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (p.att_copy[c]) *reinterpret_cast<float4*>(p.att_copy[c] + (size_t)b * p.att_copy_ld[c] + x) = acc;
-      if (p.att_img) {
-        const float v[4] = {acc.x, acc.y, acc.z, acc.w};
-        __align__(8) __nv_bfloat16 h[4], l[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          h[i] = __float2bfloat16_rn(v[i]);
-          l[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
-        }
-        __nv_bfloat16* dst = p.att_img + (size_t)b * p.att_img_ld + x;
-        *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
-        *reinterpret_cast<uint2*>(dst + p.att_img_lo) = *reinterpret_cast<const uint2*>(l);
-      }
-    }
-    __syncthreads();
-  }
-}
-
 // d s_tr = sum over the source chunks (in order) of the tanh pass's partials, written
 // as fp32 (the deferred d W_s GEMM's operand) and as its split image (the per-step
 // d s = d s_tr W_s^T GEMM's A operand: hi [B, ld], lo lo_off further on)
@@ -720,41 +611,15 @@ static int vec_e(const AttnArgs& p) {
   return (p.E % 8 == 0 && al32(p.enc) && al32(p.d_enc) && al32(p.d_att) && al32(p.att) && copies) ? 8 : 1;
 }
 
-// the cluster kernel: float4 rows throughout, the shared-memory plan within one SM
-static bool cluster_ok(const AttnArgs& p) {
-  bool copies = true;
-  for (int c = 0; c < 2; ++c) copies = copies && al16(p.att_copy[c]) && p.att_copy_ld[c] % 4 == 0;
-  const bool img_ok = !p.att_img || (((uintptr_t)p.att_img & 7) == 0 && p.att_img_ld % 4 == 0 && p.att_img_lo % 4 == 0);
-  return img_ok && p.K % 4 == 0 && p.E % 4 == 0 && al16(p.enc_ctx) && al16(p.enc) && al16(p.att) &&
-         al16(p.s_tr) && al16(p.b_fb) && al16(p.W_fb) && al16(p.v) && copies &&
-         (size_t)cl_smem(p.K, p.Ts).total * sizeof(float) <= 200 * 1024 && !getenv("SL_ATTN_CHUNKED");
-}
-template <typename F>
-static void cl_configure(F kern, size_t smem) {
-  SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-}
-
 void attention_fwd(AttnArgs p, const float* s, const float* W_s, const float* b_s, void* ws, cudaStream_t st) {
   p.s_tr = p.s_tr_out ? p.s_tr_out : static_cast<float*>(ws);
-  p.s_tr_parts = X3Parts{nullptr, 0, 0, 0};
-  if (p.W_s3_fwd && cluster_ok(p)) {  // partials summed (+ b_s) by the attention kernel
-    p.s_tr_parts = gemm_f32x3_parts(false, false, p.B, p.K, p.H, s, p.H, p.s_img, nullptr, 0, p.W_s3_fwd,
-                                    x3_ws(p, ws), st, p.s_img_ld, p.s_img_lo);
-    p.s_tr_bias = b_s;
-  } else if (p.W_s3_fwd)  // s_tr = s W_s + b_s
-    gemm_f32x3_pb(false, false, p.B, p.K, p.H, s, p.H, p.W_s3_fwd, 0.f, p.s_tr, p.K, b_s, x3_ws(p, ws), st);
+  if (p.W_s3_fwd)  // s_tr = s W_s + b_s (s from its image rows when given)
+    gemm_f32x3_ex(false, false, p.B, p.K, p.H, s, p.H, p.s_img, nullptr, 0, p.W_s3_fwd, 0.f, p.s_tr, p.K, b_s,
+                  nullptr, 0, x3_ws(p, ws), st, p.s_img ? p.s_img_ld : 0, p.s_img ? p.s_img_lo : 0);
   else
     gemm_f32x3(false, false, p.B, p.K, p.H, s, p.H, W_s, p.K, 0.f, p.s_tr, p.K, b_s, nullptr, 0, x3_ws(p, ws), st);
   float* e = row_buf(p, ws);
   Phase ph(st, "k8_attention_fwd", 0.0, 4.0 * p.B * p.Ts * (double)(p.K + p.E));
-  if (cluster_ok(p)) {
-    const size_t smem = (size_t)cl_smem(p.K, p.Ts).total * sizeof(float);
-    cl_configure(attn_fwd_cluster_kernel, smem);
-    attn_fwd_cluster_kernel<<<dim3(kCl, (unsigned)p.B), kClThreads, smem, st>>>(p);
-    SL_CUDA_TRY(cudaGetLastError());
-    count_launch();
-    return;
-  }
   const dim3 g1((unsigned)ceil_div(p.Ts, kJE), (unsigned)p.B);
   if (vec_k(p) == 4) attn_energy_kernel<4><<<g1, kThreads, 0, st>>>(p, e);
   else attn_energy_kernel<1><<<g1, kThreads, 0, st>>>(p, e);

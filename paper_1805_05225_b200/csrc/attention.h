@@ -52,18 +52,15 @@ struct AttnArgs {
   // (the readout input and the next step's [att | s] row), written by the context kernel
   float* att_copy[2];
   int64_t att_copy_ld[2];
-  // optional (the decoder's loop, with W_s3_*): the projections as split-K partials
-  // summed by their consumers — the forward's s_tr by the attention kernel itself (it
-  // writes s_tr + b_s to s_tr / s_tr_out), the backward's d s = d s_tr W_s^T handed to
-  // the caller through ds_parts_out instead of accumulated into d_s
-  X3Parts s_tr_parts;
-  const float* s_tr_bias;
+  // optional (the decoder's loop, with W_s3_bwd): the backward's d s = d s_tr W_s^T handed
+  // to the caller as split-K partials through ds_parts_out instead of accumulated into d_s
   X3Parts* ds_parts_out;
   // optional (the decoder's loop): att also written as split image rows (hi at att_img,
-  // row stride att_img_ld, lo att_img_lo further on), and s given by its image rows
-  // (the s_tr projection's A operand, no per-step split)
+  // row stride att_img_ld, lo att_img_lo further on)
   __nv_bfloat16* att_img;
   int64_t att_img_ld, att_img_lo;
+  // optional (the decoder's loop): s as its split image rows (the s_tr projection's A
+  // operand: no per-step split)
   const __nv_bfloat16* s_img;
   int64_t s_img_ld, s_img_lo;
   // (internal) deferred backward: the tanh pass's per-chunk d s_tr partials
