@@ -66,6 +66,13 @@ size_t gemm_f32x3_parts_workspace_bytes(bool transA, bool transB, int M, int N, 
 X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const float* A, int64_t lda,
                          const __nv_bfloat16* A3, const float* B, int64_t ldb, const __nv_bfloat16* B3, void* ws,
                          cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0);
+// C = op(A) op(B) + bias (fp32, single pass) and, per row and 128-column block, the
+// online-softmax statistics of C (TcGemm::sm_part) — the output layer's logits; falls
+// back to the plain GEMM (returns false, no statistics) where the shape needs split-K
+// or chunked accumulation
+bool gemm_f32x3_softmax_stats(int M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
+                              float* C, int64_t ldc, const float* bias, float4* sm_part, int sm_ld,
+                              const int32_t* targets, void* ws, cudaStream_t st);
 // both operands pre-split (images of the stored A and B)
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
                     const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,

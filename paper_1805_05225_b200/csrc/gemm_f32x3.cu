@@ -180,7 +180,7 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
              const __nv_bfloat16* a_pre, const float* B, int64_t ldb, const __nv_bfloat16* b_pre, float beta,
              float* C, int64_t ldc, const float* bias, float* ones_row_out, int64_t ld_ones, void* ws,
              cudaStream_t st, int64_t a3_ld = 0, int64_t a3_lo = 0, int64_t b3_ld = 0, int64_t b3_lo = 0,
-             X3Parts* parts = nullptr) {
+             X3Parts* parts = nullptr, const TcGemm* smx = nullptr) {
   if (M <= 0 || N <= 0) return;
   const bool a_ones = ones_row_out != nullptr;
   SL_REQUIRE(!a_ones || transA, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: ones row needs A stored [K, M]");
@@ -210,6 +210,11 @@ void x3_core(bool transA, bool transB, int M, int N, int K, const float* A, int6
   {  // chunked accumulation only where one work unit's K range is longer than a chunk
     const int64_t nk = ceil_div(K, 64);
     if (ceil_div(nk, d.ksplit) > kX3ChunkBlocks) g.kchunk = kX3ChunkBlocks;
+  }
+  if (smx) {  // softmax statistics in the epilogue (single pass only: the caller checked)
+    g.sm_part = smx->sm_part;
+    g.sm_ld = smx->sm_ld;
+    g.sm_targets = smx->sm_targets;
   }
   if (parts) {  // the partials for the caller's consumer (ksplit may be 1)
     SL_REQUIRE(!a_ones && beta == 0.f && !bias, SL_ERR_INVALID_ARGUMENT, "gemm_f32x3: partials are plain products");
@@ -282,6 +287,20 @@ X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const fl
   x3_core(transA, transB, M, N, K, A, lda, A3, B, ldb, B3, 0.f, nullptr, 0, nullptr, nullptr, 0, ws, st, a3_ld,
           a3_lo, b3_ld, b3_lo, &q);
   return q;
+}
+
+bool gemm_f32x3_softmax_stats(int M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
+                              float* C, int64_t ldc, const float* bias, float4* sm_part, int sm_ld,
+                              const int32_t* targets, void* ws, cudaStream_t st) {
+  const X3Dims d = x3_dims(false, false, M, N, K, false);
+  const bool single = d.ksplit == 1 && ceil_div(K, 64) <= kX3ChunkBlocks;
+  TcGemm sm{};
+  sm.sm_part = sm_part;
+  sm.sm_ld = sm_ld;
+  sm.sm_targets = targets;
+  x3_core(false, false, M, N, K, A, lda, nullptr, B, ldb, nullptr, 0.f, C, ldc, bias, nullptr, 0, ws, st, 0, 0, 0, 0,
+          nullptr, single ? &sm : nullptr);
+  return single;
 }
 
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,

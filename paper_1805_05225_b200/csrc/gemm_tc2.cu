@@ -474,6 +474,31 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           continue;
         }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
+        if (p.sm_part) {  // fp32 output: statistics of the stored values (alpha v + bias; beta = 0)
+          float zs[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            zs[j] = col0 + j < p.N ? p.alpha * v[j] + (p.bias ? __ldg(p.bias + col0 + j) : 0.f) : -INFINITY;
+          float cm = zs[0];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) cm = fmaxf(cm, zs[j]);
+          const float mn = fmaxf(sm_m, cm);
+          if (mn != -INFINITY) {
+            float accs = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (col0 + j < p.N) {
+                accs += exp2f((zs[j] - mn) * 1.4426950408889634f);
+                sm_t += zs[j];
+                if (col0 + j == sm_tgt) sm_y = zs[j];
+              }
+            }
+            sm_m = mn;
+            sm_s = accs;
+          }
+          if (c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
+            p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
+        }
         if (vec && col0 + 32 <= p.N && p.beta == 0.f && !p.bias && (p.ldc % 8) == 0 &&
             ((uintptr_t)crow & 31) == 0) {
           // plain fp32 tile (split-K partials, plain outputs): 32 B vector stores — full
@@ -674,8 +699,8 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   p.sm_part = g.sm_part;
   p.sm_ld = g.sm_ld;
   p.sm_targets = g.sm_targets;
-  SL_REQUIRE(!g.sm_part || (g.Cb && g.sm_targets), SL_ERR_INVALID_ARGUMENT,
-             "gemm: softmax partials need the bf16 output and the targets");
+  SL_REQUIRE(!g.sm_part || (g.sm_targets && g.beta == 0.f && g.m_split >= g.M && g.kchunk == 0 && g.ksplit <= 1),
+             SL_ERR_INVALID_ARGUMENT, "gemm: softmax partials need the targets and a plain single-pass output");
   p.kchunk = g.kchunk;
   p.group_m = std::max(1, std::min(p.nm, 8));
   if (g.kchunk > 0)
@@ -683,8 +708,8 @@ void gemm_bf16_tc2(const TcGemm& g, cudaStream_t stream) {
   const bool x3 = g.A_lo != nullptr;
   SL_REQUIRE(x3 == (g.B_lo != nullptr), SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: x3 mode needs both lo operands");
   if (x3) {
-    SL_REQUIRE(((uintptr_t)g.A_lo & 15) == 0 && ((uintptr_t)g.B_lo & 15) == 0 && !g.Cb && !g.sm_part,
-               SL_ERR_INVALID_ARGUMENT, "gemm_bf16_tc2: x3 operands need 16 B alignment and fp32 C");
+    SL_REQUIRE(((uintptr_t)g.A_lo & 15) == 0 && ((uintptr_t)g.B_lo & 15) == 0 && !g.Cb, SL_ERR_INVALID_ARGUMENT,
+               "gemm_bf16_tc2: x3 operands need 16 B alignment and fp32 C");
     const CUtensorMap tal = g.a_mn ? tm3d_mn(g.A_lo, g.M, g.K, g.lda) : tm2d(g.A_lo, g.K, g.M, g.lda, 128);
     const CUtensorMap tbl = g.b_mn ? tm3d_mn(g.B_lo, g.N, g.K, g.ldb) : tm2d(g.B_lo, g.K, g.N, g.ldb, 128);
     dispatch2<true>(g, ta, tb, tal, tbl, p, stream);

@@ -224,6 +224,84 @@ __global__ void __launch_bounds__(256) ce_rows_f32_kernel(const float* __restric
   }
 }
 
+// The same with the row statistics folded in from the logits GEMM's epilogue
+// (per 128-column block: max, sum exp(z - max), sum z, z_y): one pass over the row
+// of Z (read Z, write dZ's image) instead of two.
+__global__ void __launch_bounds__(256) ce_rows_f32_stats_kernel(const float* __restrict__ Z, int64_t ldz, int rows,
+                                                                int T, int V, const int32_t* __restrict__ targets,
+                                                                const int32_t* __restrict__ lens, float eps,
+                                                                CeScratch* sc, int* bad_target,
+                                                                const float4* __restrict__ part, int nblk,
+                                                                __nv_bfloat16* __restrict__ dzi, int64_t ldi) {
+  const int lane = threadIdx.x % 32;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int b = row / T, t = row % T;
+  const float* z = Z + (int64_t)row * ldz;
+  __nv_bfloat16* hi = dzi + (int64_t)row * ldi;
+  __nv_bfloat16* lo = dzi + ((int64_t)rows + row) * ldi;
+  for (int j = V + lane; j < ldi; j += 32) dz_store1(hi, lo, j, 0.f);  // padding
+  if (t >= lens[b]) {  // masked position (tape.cpp:1256-1262): no loss, zero gradient
+    for (int j = lane; j < V; j += 32) dz_store1(hi, lo, j, 0.f);
+    return;
+  }
+  const int y = targets[row];
+  if (y < 0 || y >= V) {  // reference IndexError: poison the step (see ce_rows_kernel)
+    if (lane == 0) {
+      atomicMax(bad_target, 1);
+      atomicAdd(&sc->loss_sum, (double)__int_as_float(0x7fc00000));
+    }
+    for (int j = lane; j < V; j += 32) dz_store1(hi, lo, j, __int_as_float(0x7fc00000));
+    return;
+  }
+  float m = -INFINITY, ss = 0.f, tz = 0.f, zy = 0.f;
+  for (int k = lane; k < nblk; k += 32) {
+    const float4 q = part[(int64_t)row * nblk + k];
+    const float mn = fmaxf(m, q.x);
+    ss = (m == -INFINITY ? 0.f : ss * expf(m - mn)) + (q.x == -INFINITY ? 0.f : q.y * expf(q.x - mn));
+    m = mn;
+    tz += q.z;
+    if (y / 128 == k) zy = q.w;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, ss, o);
+    const float mm = fmaxf(m, m2);
+    ss = (m == -INFINITY ? 0.f : ss * expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - mm));
+    m = mm;
+    tz += __shfl_xor_sync(0xffffffffu, tz, o);
+    zy += __shfl_xor_sync(0xffffffffu, zy, o);
+  }
+  const float lse = m + logf(ss);
+  if (lane == 0)
+    atomicAdd(&sc->loss_sum, (double)lse - (1.0 - (double)eps) * (double)zy - (double)eps / V * (double)tz);
+  const float inv_n = 1.f / (float)max(sc->n_valid, 1);
+  const float base = -eps / (float)V;
+  if ((V % 8) == 0 && (ldz % 4) == 0 && (ldi % 8) == 0) {  // 8 columns per lane: 16 B image stores
+    for (int j = lane * 8; j < V; j += 256) {
+      const float4 q0 = *reinterpret_cast<const float4*>(z + j), q1 = *reinterpret_cast<const float4*>(z + j + 4);
+      const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      __align__(16) __nv_bfloat16 h[8], l[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float g = expf(q[k] - lse) + base;
+        if (j + k == y) g -= 1.f - eps;
+        g *= inv_n;
+        h[k] = __float2bfloat16_rn(g);
+        l[k] = __float2bfloat16_rn(g - __bfloat162float(h[k]));
+      }
+      *reinterpret_cast<uint4*>(hi + j) = *reinterpret_cast<const uint4*>(h);
+      *reinterpret_cast<uint4*>(lo + j) = *reinterpret_cast<const uint4*>(l);
+    }
+  } else {
+    for (int j = lane; j < V; j += 32) {
+      float g = expf(z[j] - lse) + base;
+      if (j == y) g -= 1.f - eps;
+      dz_store1(hi, lo, j, g * inv_n);
+    }
+  }
+}
+
 __global__ void ce_finalize_kernel(const CeScratch* sc, float* loss_out) {
   *loss_out = (float)(sc->loss_sum / (double)max(sc->n_valid, 1));
 }
@@ -311,7 +389,7 @@ size_t output_ce_f32_workspace_bytes(int B, int T, int D, int V) {
                               gemm_f32x3_workspace_bytes(false, true, (int)rows, D, V, false),    // dX
                               gemm_f32x3_workspace_bytes(true, false, D, V, (int)rows, true)});   // [dW; db]
   return (size_t)round_up(rows * V * 4, 256) + (size_t)round_up(x3_img_elems((int)rows, V) * 2, 256) +
-         (size_t)round_up(sizeof(CeScratch), 256) + x3;
+         (size_t)round_up(rows * ceil_div(V, 128) * sizeof(float4), 256) + (size_t)round_up(sizeof(CeScratch), 256) + x3;
 }
 
 void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* targets, const int32_t* lens,
@@ -323,6 +401,9 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   w += round_up(rows * V * 4, 256);
   auto* dzi = reinterpret_cast<__nv_bfloat16*>(w);  // the split image of dZ
   w += round_up(x3_img_elems((int)rows, V) * 2, 256);
+  const int nblk = (int)ceil_div(V, 128);
+  auto* smp = reinterpret_cast<float4*>(w);  // per (row, 128-column block) softmax statistics
+  w += round_up(rows * nblk * sizeof(float4), 256);
   auto* sc = reinterpret_cast<CeScratch*>(w);
   void* gws = w + round_up(sizeof(CeScratch), 256);
   SL_CUDA_TRY(cudaMemsetAsync(bad_target, 0, sizeof(int), stream));
@@ -330,14 +411,21 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
   const double f = 2.0 * rows * D * (double)V;
+  bool stats = false;
   {
     Phase ph(stream, "k7_logits_gemm", f);
-    gemm_f32x3(false, false, (int)rows, V, D, x, D, W, V, 0.f, z, V, b, nullptr, 0, gws, stream);
+    // (an out-of-range target only fails to match a column in the statistics; the CE
+    // kernel still sees the raw id and poisons the step)
+    stats = gemm_f32x3_softmax_stats((int)rows, V, D, x, D, W, V, z, V, b, smp, nblk, targets, gws, stream);
   }
   {
     Phase ph(stream, "k7_softmax_ce", 0.0, 12.0 * rows * V);
-    ce_rows_f32_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, stream>>>(z, V, (int)rows, T, V, targets, lens, eps,
-                                                                         sc, bad_target, dzi, x3_img_ld(V));
+    if (stats)
+      ce_rows_f32_stats_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, stream>>>(
+          z, V, (int)rows, T, V, targets, lens, eps, sc, bad_target, smp, nblk, dzi, x3_img_ld(V));
+    else
+      ce_rows_f32_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, stream>>>(z, V, (int)rows, T, V, targets, lens, eps,
+                                                                           sc, bad_target, dzi, x3_img_ld(V));
     SL_CUDA_TRY(cudaGetLastError());
     ce_finalize_kernel<<<1, 1, 0, stream>>>(sc, loss_out);
     SL_CUDA_TRY(cudaGetLastError());
