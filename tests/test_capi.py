@@ -61,7 +61,8 @@ def test_valid_descriptor_and_sizes():
     w1 = L.sl_lstm_workspace_size(ctypes.byref(d))
     assert r1 > 0 and w1 > 0
     d2 = desc(num_dirs=2)
-    assert L.sl_lstm_reserve_size(ctypes.byref(d2)) >= 2 * r1 - 4096
+    # per-direction saves double; the fp32 mode's [X | 1] operand image is shared by both
+    assert L.sl_lstm_reserve_size(ctypes.byref(d2)) > r1
 
 
 @pytest.mark.parametrize("kw,code,needle", [
