@@ -33,10 +33,10 @@ struct AttnArgs {
   float* d_v;              // [K]
   float* d_b_v;            // [1]
   int accumulate;
-  // optional (the decoder's loop): W_s split once per call into the K-tripled images
-  // of s_tr = s W_s (W_s3_fwd, x3_split_b(false, K, H)) and d s = d s_tr W_s^T
-  // (W_s3_bwd, x3_split_b(true, H, K)); s_tr written to / read from a caller buffer
-  // [B, K] instead of recomputed in the backward
+  // optional (the decoder's loop): W_s split once per call into its hi/lo image
+  // (gemm.h x3_split_img), read by both s_tr = s W_s (W_s3_fwd) and d s = d s_tr W_s^T
+  // (W_s3_bwd: the same image); s_tr written to / read from a caller buffer [B, K]
+  // instead of recomputed in the backward
   const __nv_bfloat16* W_s3_fwd;
   const __nv_bfloat16* W_s3_bwd;
   float* s_tr_out;

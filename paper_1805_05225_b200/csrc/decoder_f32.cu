@@ -461,8 +461,8 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     SL_CUDA_TRY(cudaMemsetAsync(L.xai, 0, sizeof(__nv_bfloat16) * B * L.xai_ld, st));
     SL_CUDA_TRY(cudaMemsetAsync(L.xai + L.xai_lo, 0, sizeof(__nv_bfloat16) * B * L.xai_ld, st));
     SL_CUDA_TRY(cudaMemsetAsync(L.acc_all, 0, sizeof(float) * BTs, st));  // accum_{-1} = 0
-    // [W_att; R] (rows Emb.. of s/W stacked on s/R) split once into the two K-tripled
-    // images the per-step GEMMs read, through an fp32 staging copy of the stacked matrix
+    // [W_att; R] (rows Emb.. of s/W stacked on s/R) split once into the image the per-step
+    // GEMMs read in both roles, through an fp32 staging copy of the stacked matrix
     {
       float* w2 = L.w2;
       SL_CUDA_TRY(cudaMemcpyAsync(w2, p.s_W + (int64_t)Emb * 4 * H, sizeof(float) * E * 4 * H,

@@ -162,7 +162,7 @@ void rec_fwd_pair(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* co
 // TMEM; fp32 x W, cell state, saves and outputs.  One direction per launch
 // (both directions' hi+lo R do not fit in shared memory at once).
 // nd == 2 and the grid fits: both directions in ONE launch (shape.pair == 2: 32 units
-// per pair, R_hi resident, R_lo streamed through the ring with h); otherwise one
+// per pair, R hi and lo streamed through the ring with h); otherwise one
 // direction per launch (shape.pair == 1: 16 units per pair, R hi + lo resident).
 TcFwdShape tc_rec_fwd_x3_shape(int H, int sms, int nd = 1);  // C == 0: unsupported
 size_t tc_rec_x3_pack_elems(const TcFwdShape& sh);   // one direction's packed R^T (hi rows, then lo rows)
