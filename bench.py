@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--dp-selftest", action="store_true",
+                    help="(test) issue the gradient all-reduces even at one rank (NCCL, graph-captured), "
+                         "to exercise the N>1 step's capture on a single GPU")
     a = ap.parse_args()
     a.attention = not a.no_attention
     if a.attention and not (a.vocab and a.src_vocab and a.trg_vocab):
@@ -356,6 +359,8 @@ def run_ours(args, rank, world, local_rank, precision):
 
     from paper_1805_05225_b200.dp import BucketAllReducer
     red = BucketAllReducer()  # layer-bucketed NCCL all-reduce, overlapped with BPTT
+    if args.dp_selftest:
+        red.force = True
 
     def step(xin):
         model.step(xin, lens, dy, reducer=red, grad_scale=1.0 / world)
@@ -385,22 +390,37 @@ def run_ours(args, rank, world, local_rank, precision):
               for e in entries[:n]}
     eager_ms = ms
     graph = None
-    if world == 1 and not args.no_graph:
+    graph_note = None
+    if not args.no_graph:
         # The whole step (every kernel of the library, the glue copies, the
-        # optimizer with its device-side step counter) captured once as a CUDA
-        # graph and replayed: no host launch gaps.  Phases above come from the
-        # eager pass (same kernels); the headline time from the replays.
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            step(x)
-        torch.cuda.current_stream().wait_stream(side)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        c0 = lib.sl_launch_count()
-        with torch.cuda.graph(graph):
-            step(x)
-        per_step = lib.sl_launch_count() - c0
+        # optimizer with its device-side step counter and, at N>1, the bucketed
+        # NCCL all-reduces) captured once as a CUDA graph and replayed: no host
+        # launch gaps.  Phases above come from the eager pass (same kernels); the
+        # headline time from the replays.  At N>1 every rank must end up on the
+        # same path: a capture failure on any rank drops all ranks to eager.
+        ok = 1
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step(x)
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            c0 = lib.sl_launch_count()
+            with torch.cuda.graph(graph):
+                step(x)
+            per_step = lib.sl_launch_count() - c0
+        except Exception as exc:  # noqa: BLE001 - reported in the line, eager timing instead
+            ok, graph, graph_note = 0, None, f"graph capture failed ({type(exc).__name__}: {exc}); eager"
+            torch.cuda.synchronize()
+        if world > 1:
+            f = torch.tensor([ok], device=dev, dtype=torch.int32)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            if int(f.item()) == 0:
+                graph = None
+                graph_note = graph_note or "graph capture failed on another rank; eager"
+    if graph is not None:
         graph.replay()
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clocks:
@@ -431,9 +451,10 @@ def run_ours(args, rank, world, local_rank, precision):
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
 
         graphed = None
-        if args.attention and world == 1 and not args.no_graph:
+        if args.attention and graph is not None:  # (at N>1 only when every rank captured the timed step)
             from paper_1805_05225_b200.model import GraphedStep
-            graphed = GraphedStep(model, x, lens, dy)  # the public graphed-step API
+            # the public graphed-step API, the bucketed all-reduces captured with the kernels
+            graphed = GraphedStep(model, x, lens, dy, reducer=red, grad_scale=1.0 / world)
 
         def e2e_step():
             if graphed is not None:  # H2D of the step's inputs, graph replay, D2H of the loss
@@ -474,7 +495,9 @@ def run_ours(args, rank, world, local_rank, precision):
                                             if graphed is not None else "; eager launches"),
                "timing": "host wall clock, max over ranks"}
     return dict(ms=ms_max, phases=phases, launches=int(launches), clocks=clocks.summary(),
-                e2e=e2e, eager_ms=eager_ms / args.steps, eager_ms_total=eager_ms, graph=graph is not None)
+                e2e=e2e, eager_ms=eager_ms / args.steps, eager_ms_total=eager_ms, graph=graph is not None,
+                graph_note=graph_note, allreduces=red.issued,
+                backend=dist.get_backend() if dist.is_initialized() else None)
 
 
 def _free_port() -> int:
@@ -807,7 +830,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 or (args.dp_selftest and "RANK" in os.environ):
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks=N) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.config != 4:
@@ -910,6 +933,9 @@ def result_line(args, r, world, cfg, peaks, precision):
             "scaling": "weak", "vs_baseline": None, "dtype": precision.replace("fp", "f"),
             "data": "synthetic (token ids ~ U[0, V), params ~ U(+-1/sqrt(H)))",
             "config": cfg, "cuda_graph": r["graph"], "eager_ms_per_step": r["eager_ms"],
+            **({"graph_note": r["graph_note"]} if r.get("graph_note") else {}),
+            **({"dp_selftest": f"gradient all-reduces issued over NCCL at world 1 ({r['allreduces']} issued, "
+                                f"backend {r['backend']})"} if args.dp_selftest else {}),
             "precision_note": ("fp32 semantics (rel. 1e-4 per tensor vs the fp32 reference): every product on the "
                                "tcgen05 tensor cores as split-bf16 x3 (A B = A_hi B_hi + A_lo B_hi + A_hi B_lo, fp32 "
                                "accumulation in K chunks), fp32 state / activations" if precision == "fp32" else

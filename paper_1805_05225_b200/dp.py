@@ -19,14 +19,17 @@ class BucketAllReducer:
         self.group = group
         self.average = average
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.force = False  # (test) issue the collective even at world 1
+        self.issued = 0     # collectives issued (eager calls and graph captures)
         self._pending = []
 
     def __call__(self, layer: int, bucket: torch.Tensor) -> None:
         """on_layer_grads hook: start reducing this layer's bucket now."""
-        if self.world == 1:
+        if self.world == 1 and not (self.force and dist.is_initialized()):
             if self.average:
                 bucket.div_(1)
             return
+        self.issued += 1
         self._pending.append((bucket, dist.all_reduce(bucket, group=self.group, async_op=True)))
 
     def wait(self) -> None:

@@ -426,21 +426,24 @@ class GraphedStep:
         step = GraphedStep(model, src_ids, src_lens, targets)   # device tensors of the shape
         loss = step(src_host, lens_host, trg_host)               # pinned host tensors
 
-    Single-GPU (the data-parallel all-reduce is not captured)."""
+    Data-parallel: pass the step's `reducer` (dp.BucketAllReducer) and
+    `grad_scale`; the bucketed NCCL all-reduces are captured with the kernels
+    (every rank must build its GraphedStep at the same point)."""
 
-    def __init__(self, model, src_ids, src_lens, targets):
+    def __init__(self, model, src_ids, src_lens, targets, reducer=None, grad_scale: float = 1.0):
         self.model = model
         self.inputs = [src_ids.clone(), src_lens.clone(), targets.clone()]
         self.loss_h = torch.empty((), dtype=torch.float32).pin_memory()
+        kw = dict(reducer=reducer, grad_scale=grad_scale) if reducer is not None or grad_scale != 1.0 else {}
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up outside the capture (lazy allocations, attributes)
-            model.step(*self.inputs)
+            model.step(*self.inputs, **kw)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.loss = model.step(*self.inputs)
+            self.loss = model.step(*self.inputs, **kw)
 
     def __call__(self, src_ids, src_lens, targets, sync: bool = True):
         for dst, src in zip(self.inputs, (src_ids, src_lens, targets)):
