@@ -88,6 +88,11 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+__device__ __forceinline__ float fast_ex2(float x) {  // 2^x, MUFU (ex2.approx.ftz)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
@@ -475,29 +480,66 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
         if (p.sm_part) {  // fp32 output: statistics of the stored values (alpha v + bias; beta = 0)
-          float zs[32];
+          // the outputs once (bias as 16 B loads), their max as a tree, the exp sum in four
+          // independent partial sums (ex2.approx on log2e-scaled values): the statistics stay
+          // cheaper than the tile's MMAs, so the epilogue hides under the next tile
+          const bool full = col0 + 32 <= p.N;
+          float o[32];
+          if (full && (!p.bias || ((uintptr_t)(p.bias + col0) & 15) == 0)) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            zs[j] = col0 + j < p.N ? p.alpha * v[j] + (p.bias ? __ldg(p.bias + col0 + j) : 0.f) : -INFINITY;
-          float cm = zs[0];
+            for (int j = 0; j < 32; j += 4) {
+              const float4 bb = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+              o[j] = fmaf(p.alpha, v[j], bb.x);
+              o[j + 1] = fmaf(p.alpha, v[j + 1], bb.y);
+              o[j + 2] = fmaf(p.alpha, v[j + 2], bb.z);
+              o[j + 3] = fmaf(p.alpha, v[j + 3], bb.w);
+            }
+          } else {
 #pragma unroll
-          for (int j = 1; j < 32; ++j) cm = fmaxf(cm, zs[j]);
-          const float mn = fmaxf(sm_m, cm);
+            for (int j = 0; j < 32; ++j)
+              o[j] = col0 + j < p.N ? p.alpha * v[j] + (p.bias ? __ldg(p.bias + col0 + j) : 0.f) : -INFINITY;
+          }
+          float mx[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(o[i], o[i + 8]), fmaxf(o[i + 16], o[i + 24]));
+#pragma unroll
+          for (int w = 4; w >= 1; w /= 2)
+#pragma unroll
+            for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+          const float mn = fmaxf(sm_m, mx[0]);
           if (mn != -INFINITY) {
-            float accs = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f);
+            constexpr float kL2e = 1.4426950408889634f;
+            const float ms = mn * kL2e;
+            float es[4] = {0.f, 0.f, 0.f, 0.f}, ts[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if (col0 + j < p.N) {
-                accs += exp2f((zs[j] - mn) * 1.4426950408889634f);
-                sm_t += zs[j];
-                if (col0 + j == sm_tgt) sm_y = zs[j];
+              if (full || col0 + j < p.N) {
+                es[j & 3] += fast_ex2(fmaf(o[j], kL2e, -ms));
+                ts[j & 3] += o[j];
+                if (col0 + j == sm_tgt) sm_y = o[j];
               }
             }
+            sm_s = fmaf(sm_s, fast_ex2(fmaf(sm_m, kL2e, -ms)), (es[0] + es[1]) + (es[2] + es[3]));
+            sm_t += (ts[0] + ts[1]) + (ts[2] + ts[3]);
             sm_m = mn;
-            sm_s = accs;
           }
           if (c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
             p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
+          float* dst = crow + col0;
+          if (full && vec && (p.ldc % 8) == 0 && ((uintptr_t)dst & 31) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8)
+              asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "f"(o[j]),
+                           "f"(o[j + 1]), "f"(o[j + 2]), "f"(o[j + 3]), "f"(o[j + 4]), "f"(o[j + 5]), "f"(o[j + 6]),
+                           "f"(o[j + 7])
+                           : "memory");
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.N) dst[j] = o[j];
+          }
+          continue;
         }
         if (vec && col0 + 32 <= p.N && p.beta == 0.f && !p.bias && (p.ldc % 8) == 0 &&
             ((uintptr_t)crow & 31) == 0) {
