@@ -511,7 +511,8 @@ TcFwdShape tc_rec_fwd_shape(int H, int nd, int sms) {
   constexpr bool cluster = false;
 #endif
   if (!cluster && tc_rec_fwd_pair_fits(H, nd, sms)) {
-    TcFwdShape sh{1, 32, (int)ceil_div(H, 32), (int)round_up(H, 64)};
+    const int pu = tc_rec_fwd_pair_units(H, nd, sms);
+    TcFwdShape sh{1, pu, (int)ceil_div(H, pu), (int)round_up(H, 64)};
     sh.pair = 1;
     return sh;
   }

@@ -153,6 +153,7 @@ void tc_rec_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT,
 void rec_fwd_tc(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                 cudaStream_t stream);
 bool tc_rec_fwd_pair_fits(int H, int nd, int sms);
+int tc_rec_fwd_pair_units(int H, int nd, int sms);  // units per pair of the bf16 pair kernel: 32 or 16
 void rec_fwd_pair(const TcRecFwdArgs& a, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                   cudaStream_t stream);
 

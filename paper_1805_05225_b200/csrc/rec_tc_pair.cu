@@ -51,11 +51,13 @@ using namespace rtc;
 // kX3C: fp32-class, both directions concurrently, R_hi and R_lo streamed through
 // the ring with h (a stage = [h_hi | h_lo | R_lo | R_hi] of one K chunk): with no
 // resident R the shared memory holds 4 such stages instead of 2
-enum Mode { kBF16 = 0, kX3 = 1, kX3C = 2 };
+// kBF16N: the bf16 path with 16 units per pair (narrow layers: one direction, or H small
+// enough that 32-unit pairs would leave half the SMs idle), x W loaded per row
+enum Mode { kBF16 = 0, kX3 = 1, kX3C = 2, kBF16N = 3 };
 template <int M>
 struct PairCfg {
-  static constexpr bool X3 = M != kBF16;
-  static constexpr int kPU = M == kX3 ? 16 : 32;           // hidden units per pair
+  static constexpr bool X3 = M == kX3 || M == kX3C;
+  static constexpr int kPU = M == kX3 || M == kBF16N ? 16 : 32;  // hidden units per pair
   static constexpr int kN = 4 * kPU;                       // MMA N (both CTAs' R slices)
   static constexpr int kNHalf = kN / 2;                    // R^T rows held per CTA (per precision part)
   static constexpr bool kStreamR = M != kX3;                // R (x3: hi and lo) streamed with h
@@ -624,18 +626,32 @@ bool tc_rec_fwd_pair_fits(int H, int nd, int sms) {
   return (int64_t)2 * P * nd <= sms && pair_smem<kBF16>(Kp, 2, 2) <= kSmemMax;
 }
 
+int tc_rec_fwd_pair_units(int H, int nd, int sms) {
+  // 16 units per pair when 32-unit pairs would cover at most half the SMs and the
+  // narrow grid still fits (e.g. one direction of H = 1024: 128 CTAs instead of 64);
+  // small layers keep 32 (their steps are latency-, not MMA-bound)
+  const int P16 = (int)ceil_div(H, PairCfg<kBF16N>::kPU);
+  const int Kp = (int)round_up(H, 64);
+  if (H >= 512 && (int64_t)2 * P16 * nd <= sms && pair_smem<kBF16N>(Kp, 2, 2) <= kSmemMax &&
+      Kp / 64 / 2 <= kGrpCtrs)
+    return 16;
+  return 32;
+}
+
 void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* const* RT,
                   cudaStream_t stream) {
-  using Cfg = PairCfg<kBF16>;
+  const bool narrow = sh.U == PairCfg<kBF16N>::kPU;
+  const int kN = 4 * sh.U, kNHalf = kN / 2;
   TcRecFwdArgs a = a0;
-  a.U = Cfg::kPU;
+  a.U = sh.U;
   a.P = sh.P;
   a.Kp = sh.Kp;
   CUtensorMap tr[2], th[2], tx[2];
   a.kb = (a.Kp / 64) % 2 == 0 ? 2 : 1;
   // x W tiles by TMA: 3-D view {columns, T, B} of the bf16 K1 output, one box
-  // per gate of [128 rows x 32 units], 64 B swizzle (conflict-free epilogue reads)
-  a.xw_tma = kChunk * a.kb >= 4 * kXwGate && (a.xw_ld * 2) % 16 == 0;
+  // per gate of [128 rows x 32 units], 64 B swizzle (conflict-free epilogue reads);
+  // the narrow kernel loads its 16-unit slices per row instead
+  a.xw_tma = !narrow && kChunk * a.kb >= 4 * kXwGate && (a.xw_ld * 2) % 16 == 0;
   for (int k = 0; k < a.nd; ++k) a.xw_tma = a.xw_tma && ((uintptr_t)a.xw[k] & 15) == 0;
   for (int k = 0; k < a.nd; ++k) {
     if (a.xw_tma) {
@@ -646,19 +662,20 @@ void rec_fwd_pair(const TcRecFwdArgs& a0, const TcFwdShape& sh, __nv_bfloat16* c
     } else {
       tx[k] = CUtensorMap{};
     }
-    cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.P * Cfg::kN};
+    cuuint64_t rd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.P * kN};
     cuuint64_t rs[1] = {(cuuint64_t)a.Kp * 2};
-    cuuint32_t rb[2] = {64, (cuuint32_t)Cfg::kNHalf};
+    cuuint32_t rb[2] = {64, (cuuint32_t)kNHalf};
     tr[k] = tmap(RT[k], 2, rd, rs, rb);
     th[k] = ring_map(a.hbuf[k], a.B, a.Kp, a.kb);
   }
   a.stages = 0;
   for (int st = kMaxStages; st >= 2 && !a.stages; --st)
-    if (pair_smem<kBF16>(a.Kp, st, a.kb) <= kSmemMax) a.stages = st;
+    if ((narrow ? pair_smem<kBF16N>(a.Kp, st, a.kb) : pair_smem<kBF16>(a.Kp, st, a.kb)) <= kSmemMax) a.stages = st;
   SL_REQUIRE(a.stages >= 2, SL_ERR_UNSUPPORTED, "rec_fwd_pair: R slice does not fit in shared memory");
   SL_REQUIRE(a.Kp / 64 / a.kb <= kGrpCtrs && 4 * kGrpCtrs <= kBarPerChunk, SL_ERR_UNSUPPORTED,
              "rec_fwd_pair: too many K groups for the step counters");
-  launch_pair<kBF16>(a, tr, th, tx, stream);
+  if (narrow) launch_pair<kBF16N>(a, tr, th, tx, stream);
+  else launch_pair<kBF16>(a, tr, th, tx, stream);
 }
 
 TcFwdShape tc_rec_fwd_x3_shape(int H, int sms, int nd) {
