@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             // the epilogue's uncoalesced per-row stores are request-bound
             const bool v32 = ((uintptr_t)brow & 31) == 0;
             uint4 wlo = make_uint4(0, 0, 0, 0);
+            float zr[32];  // the stored (bf16-rounded) values, for the statistics
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
               float o[8];
@@ -441,23 +442,31 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                              "r"(wlo.x), "r"(wlo.y), "r"(wlo.z), "r"(wlo.w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
                              : "memory");
               }
-              if (p.sm_part) {  // statistics of the stored (bf16) values
-                const float zb[8] = {__low2float(t0), __high2float(t0), __low2float(t1), __high2float(t1),
-                                     __low2float(t2), __high2float(t2), __low2float(t3), __high2float(t3)};
-                float cm = zb[0];
+              zr[j] = __low2float(t0), zr[j + 1] = __high2float(t0), zr[j + 2] = __low2float(t1);
+              zr[j + 3] = __high2float(t1), zr[j + 4] = __low2float(t2), zr[j + 5] = __high2float(t2);
+              zr[j + 6] = __low2float(t3), zr[j + 7] = __high2float(t3);
+            }
+            if (p.sm_part) {  // statistics of the stored (bf16) values: one rescale per 32 columns
+              float mx[8];
 #pragma unroll
-                for (int i = 1; i < 8; ++i) cm = fmaxf(cm, zb[i]);
-                const float mn = fmaxf(sm_m, cm);
-                float acc = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f);
+              for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(zr[i], zr[i + 8]), fmaxf(zr[i + 16], zr[i + 24]));
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  acc += exp2f((zb[i] - mn) * 1.4426950408889634f);
-                  sm_t += zb[i];
-                  if (col0 + j + i == sm_tgt) sm_y = zb[i];
-                }
-                sm_m = mn;
-                sm_s = acc;
+              for (int w = 4; w >= 1; w /= 2)
+#pragma unroll
+                for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+              const float mn = fmaxf(sm_m, mx[0]);
+              constexpr float kL2e = 1.4426950408889634f;
+              const float ms = mn * kL2e;
+              float es[4] = {0.f, 0.f, 0.f, 0.f}, ts[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                es[j & 3] += fast_ex2(fmaf(zr[j], kL2e, -ms));
+                ts[j & 3] += zr[j];
+                if (col0 + j == sm_tgt) sm_y = zr[j];
               }
+              sm_s = fmaf(sm_s, fast_ex2(fmaf(sm_m, kL2e, -ms)), (es[0] + es[1]) + (es[2] + es[3]));
+              sm_t += (ts[0] + ts[1]) + (ts[2] + ts[3]);
+              sm_m = mn;
             }
           } else {
             for (int j = 0; j < 32 && col0 + j < p.N; ++j) {

@@ -39,7 +39,7 @@ for name, bp in (("plain", None), ("bias", bias.data_ptr())):
     print(json.dumps({"gemm": "logits " + name + " (splits included)", "us": round(us, 1),
                       "exec_tflops": round(3 * 2 * M * V * D / us / 1e6, 1)}))
 del C, ws
-out = OutputCE(B, T, D, V, precision="fp32")
+out = OutputCE(B, T, D, V, precision=os.environ.get("PREC", "fp32"))
 x = A.view(B, T, D)
 tg = torch.randint(0, V, (B, T), device="cuda", dtype=torch.int32)
 lens = torch.full((B,), T, dtype=torch.int32, device="cuda")
