@@ -28,7 +28,10 @@ namespace {
 constexpr int BMP = 256, BNP = 256, BK = 64, kStages = 6, kEpiWarps = 8, kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kHalf = 128 * 64 * 2;  // 16 KB: 128 rows (or cols) x 64 K of bf16
 constexpr uint32_t kStage = 2 * kHalf;    // A half + B half per CTA
-constexpr uint32_t kSmem = kStages * kStage + 1024;
+// + per epilogue warp one 32 x 32 fp32 block: the plain-output epilogue's transpose
+// staging (coalesced row-segment stores)
+constexpr uint32_t kEpiBlock = 32 * 32 * 4;
+constexpr uint32_t kSmem = kStages * kStage + 1024 + kEpiWarps * kEpiBlock;
 // X3 (fp32-class) mode: a stage holds A_hi, B_hi, A_lo, B_lo of one 64-wide K block
 // (64 KB per CTA, 3 stages in the same shared memory) and feeds three MMAs per
 // 16-wide K step: A_hi B_hi + A_lo B_hi + A_hi B_lo
@@ -398,6 +401,50 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       // online softmax statistics of this row over the warp's 128 columns
       float sm_m = -INFINITY, sm_s = 0.f, sm_t = 0.f, sm_y = 0.f;
       const int sm_tgt = (p.sm_part && row < p.M) ? p.sm_targets[row] : -1;
+      // plain fp32 tile (split-K partials, plain outputs): two TMEM loads in flight per
+      // wait, each warp's 32 x 32 blocks transposed through shared memory (16 B chunks
+      // XOR-swizzled: conflict-free both ways) and stored as 128 B row segments, four
+      // rows per instruction — a quarter of the requests of one 32 B store per row
+      const bool plain_tile = !p.Cb && !p.sm_part && p.beta == 0.f && !p.bias && p.C != nullptr &&
+                              n0 + (half + 1) * kColsPerWarp <= p.N && (p.ldc % 4) == 0 &&
+                              ((uintptr_t)p.C & 15) == 0 && (p.split_stride % 4) == 0 &&
+                              __all_sync(0xffffffffu, row < p.M && !second);
+      if (plain_tile) {
+        float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
+                     (warp - 2) * 1024;
+        float* c0p = p.C + z * p.split_stride + (int64_t)(m0 + 32 * q) * p.ldc + n0 + half * kColsPerWarp;
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + half * kColsPerWarp;
+        auto put = [&](const uint32_t(&rv)[32], int cc) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(blk + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                make_float4(p.alpha * __uint_as_float(rv[4 * j]), p.alpha * __uint_as_float(rv[4 * j + 1]),
+                            p.alpha * __uint_as_float(rv[4 * j + 2]), p.alpha * __uint_as_float(rv[4 * j + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + lane / 8, ch = lane & 7;
+            const float4 t = *reinterpret_cast<const float4*>(blk + rr * 32 + ((ch ^ (rr & 7)) * 4));
+            *reinterpret_cast<float4*>(c0p + (int64_t)rr * p.ldc + cc * 32 + ch * 4) = t;
+          }
+          __syncwarp();
+        };
+        {  // all four 32-column loads in flight, one wait
+          uint32_t r0[32], r1[32], r2[32], r3[32];
+          tc::tmem_ld_32x32b_x32_nw(ta, r0);
+          tc::tmem_ld_32x32b_x32_nw(ta + 32, r1);
+          tc::tmem_ld_32x32b_x32_nw(ta + 64, r2);
+          tc::tmem_ld_32x32b_x32_nw(ta + 96, r3);
+          tc::tmem_wait_ld_dep(r0);
+          tc::reg_dep(r1);
+          tc::reg_dep(r2);
+          tc::reg_dep(r3);
+          put(r0, 0);
+          put(r1, 1);
+          put(r2, 2);
+          put(r3, 3);
+        }
+      } else
 #pragma unroll 1
       for (int c = half * kColsPerWarp; c < (half + 1) * kColsPerWarp; c += 32) {
         float v[32];
