@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, DEFER ? 3 : 2) attn_bwd_de_kernel(At
     const int jj = j0 + threadIdx.x;
     const float up = (jj < len && up_b) ? up_b[jj] : 0.f;
     float* ga = p.d_accum + (size_t)b * Ts + jj;
-    *ga = (p.accumulate ? *ga : 0.f) + up + (jj < len ? sum_sh[threadIdx.x] : 0.f);
+    *ga = (p.accumulate && !p.d_accum_fresh ? *ga : 0.f) + up + (jj < len ? sum_sh[threadIdx.x] : 0.f);
   }
 }
 

@@ -28,6 +28,7 @@ struct AttnArgs {
   float* d_enc_ctx;        // [B, Ts, K]
   float* d_enc;            // [B, Ts, E]
   float* d_accum;          // [B, Ts]
+  int d_accum_fresh;       // d_accum written, not accumulated, even when `accumulate` is set
   float* d_W_fb;           // [K]
   float* d_b_fb;           // [K]
   float* d_v;              // [K]

@@ -568,7 +568,7 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     a.defer = 1;  // d enc, d enc_ctx, d W_fb, d b_fb, d v, d b_v, d W_s, d b_s: after the loop
     a.d_s_tr_out = L.ds_all + (int64_t)t * B * K;
     a.de_out = L.de_all + (int64_t)t * B * d.Ts;
-    SL_CUDA_TRY(cudaMemsetAsync(a.d_accum, 0, sizeof(float) * B * d.Ts, st));
+    a.d_accum_fresh = 1;  // the tanh pass writes every position of d accum_{t-1} (no memset)
     X3Parts dsp{nullptr, 0, 0, 0};
     a.ds_parts_out = &dsp;
     attention_bwd(a, L.s_all + (int64_t)t * B * H, p.str_W, p.str_b, L.ds, nullptr, nullptr, L.att_ws, st);

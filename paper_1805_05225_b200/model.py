@@ -1,15 +1,17 @@
-"""The config-4 training step around the LSTM hot path (BASELINE configs[3]):
-6-layer BLSTM encoder + 1-layer LSTM decoder + the output softmax layer with
-the label-smoothed CE loss, fwd + bwd, data-parallel gradient all-reduce,
-fused clip + Adam — the Listing-1 step (models.cpp:17-184, compiler.cpp
-eval_layer / RnnCell / Softmax) minus the MLP attention (not
-built) and the readout layer: the decoder input is [target embedding ‖
-context] with the context stand-in c_t = encoder output at t (an identity
-alignment, T_src = T_tgt), so encoder gradients still flow through the
-decoder as they do through attention in the reference, and the output layer
-reads the decoder state directly.  The decoder runs as one unidirectional
-LSTM layer over the teacher-forced inputs (no recurrent input feeding
-without attention).
+"""The config-4 training step around the LSTM hot path (BASELINE configs[3]).
+
+Two models:
+- Seq2SeqAttention (below Seq2SeqLSTM) is the bench workload: the full
+  Listing-1 step (models.cpp:17-184) with the MLP attention decoder, the relu
+  readout, dropout and the output softmax + label-smoothed CE.
+- Seq2SeqLSTM is the simpler pre-attention step (`bench.py --no-attention`):
+  6-layer BLSTM encoder + one decoder LSTM layer + the output layer, fwd + bwd,
+  data-parallel gradient all-reduce, fused clip + Adam.  Its decoder input is
+  [target embedding ‖ context] with the context stand-in c_t = encoder output
+  at t (an identity alignment, T_src = T_tgt), so encoder gradients still flow
+  through the decoder as they do through attention.  The output layer reads
+  the decoder state directly, and the decoder runs as one unidirectional LSTM
+  layer over the teacher-forced inputs.
 
 With src_vocab / trg_vocab the step starts from token ids like the
 reference: the `src` layer's embedding lookup feeds encoder layer 0 (written
