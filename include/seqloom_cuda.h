@@ -59,8 +59,15 @@ enum sl_precision {
 enum sl_layer_flags {
   SL_LAYER_X_BF16 = 1, /* x is bf16 [B, T, sl_lstm_bf16_pitch(D)], 1.0 at column D; kept
                           unchanged by the caller until the matching bwd */
-  SL_LAYER_Y_BF16 = 2  /* y is written as bf16 [B, T, sl_lstm_bf16_pitch(ndir*H)] with 1.0 at
+  SL_LAYER_Y_BF16 = 2, /* y is written as bf16 [B, T, sl_lstm_bf16_pitch(ndir*H)] with 1.0 at
                           column ndir*H: directly the next layer's SL_LAYER_X_BF16 input */
+  /* SL_PREC_FP32 only: the activations between stacked layers as their split-bf16
+   * ("x3") image — two planes [2][B*T][sl_lstm_bf16_pitch(features)] of bf16, hi =
+   * bf16(v) then lo = bf16(v - hi), 1.0 at column `features` of the hi plane, zero
+   * padding — the operand the fp32-class input GEMM reads, so no split pass runs */
+  SL_LAYER_X_X3 = 16, /* x is that image of [B, T, D]; kept unchanged until the matching bwd */
+  SL_LAYER_Y_X3 = 32  /* y is written as that image of [B, T, ndir*H] (zero-initialised by the
+                         caller): directly the next layer's SL_LAYER_X_X3 input */
 };
 /* Row pitch (elements) of the padded bf16 activation layout: round_up(features + 1, 64). */
 int64_t sl_lstm_bf16_pitch(int32_t features);

@@ -56,7 +56,13 @@ struct Dims {
   int64_t BT() const { return (int64_t)B * T; }
   bool x_bf16() const { return flags & SL_LAYER_X_BF16; }
   bool y_bf16() const { return flags & SL_LAYER_Y_BF16; }
+  bool x_x3() const { return flags & SL_LAYER_X_X3; }
+  bool y_x3() const { return flags & SL_LAYER_Y_X3; }
 };
+
+struct Dims;
+Dims dims(const sl_lstm_layer* L);
+bool use_x3(const Dims& d, int prec);
 
 void validate(const sl_lstm_layer* L) {
   SL_REQUIRE(L != nullptr, SL_ERR_INVALID_ARGUMENT, "sl_lstm_layer: null descriptor");
@@ -70,10 +76,15 @@ void validate(const sl_lstm_layer* L) {
                  " D=" + std::to_string(L->input_dim) + " H=" + std::to_string(L->hidden));
   SL_REQUIRE(L->precision == SL_PREC_FP32 || L->precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
              "precision " + std::to_string(L->precision) + " not supported by this build");
-  SL_REQUIRE((L->flags & ~(SL_LAYER_X_BF16 | SL_LAYER_Y_BF16)) == 0, SL_ERR_INVALID_ARGUMENT,
-             "sl_lstm_layer.flags: unknown bits " + std::to_string(L->flags));
-  SL_REQUIRE(L->flags == 0 || L->precision == SL_PREC_BF16, SL_ERR_UNSUPPORTED,
-             "sl_lstm_layer.flags: bf16 activations need precision SL_PREC_BF16");
+  SL_REQUIRE((L->flags & ~(SL_LAYER_X_BF16 | SL_LAYER_Y_BF16 | SL_LAYER_X_X3 | SL_LAYER_Y_X3)) == 0,
+             SL_ERR_INVALID_ARGUMENT, "sl_lstm_layer.flags: unknown bits " + std::to_string(L->flags));
+  SL_REQUIRE((L->flags & (SL_LAYER_X_BF16 | SL_LAYER_Y_BF16)) == 0 || L->precision == SL_PREC_BF16,
+             SL_ERR_UNSUPPORTED, "sl_lstm_layer.flags: bf16 activations need precision SL_PREC_BF16");
+  SL_REQUIRE((L->flags & (SL_LAYER_X_X3 | SL_LAYER_Y_X3)) == 0 ||
+                 (L->precision == SL_PREC_FP32 && use_x3(dims(L), L->precision)),
+             SL_ERR_UNSUPPORTED,
+             "sl_lstm_layer.flags: split-image (x3) activations need precision SL_PREC_FP32 on the "
+             "tensor-core path");
 }
 
 Dims dims(const sl_lstm_layer* L) {
@@ -168,7 +179,7 @@ ReserveView carve_reserve(const Dims& d, int prec, void* p, size_t* bytes) {
   }
   if (use_x3(d, prec)) {
     r.wimg = c.take<__nv_bfloat16>(wimg_elems(d));
-    r.ximg = c.take<__nv_bfloat16>(ximg_elems(d));
+    if (!d.x_x3()) r.ximg = c.take<__nv_bfloat16>(ximg_elems(d));  // else the caller's x image
   }
   if (prec == SL_PREC_BF16) {
     const Pad pd = pads(d);
@@ -229,7 +240,7 @@ FwdWork carve_fwd(const Dims& d, int prec, void* p, size_t* bytes) {
     for (int k = 0; k < d.nd; ++k) w.xw[k] = xw ? xw + k * g4(d) : nullptr;
     w.bcat = c.take<float>((size_t)w.xw_ld);
     w.wimg = c.take<__nv_bfloat16>(wimg_elems(d));
-    w.ximg = c.take<__nv_bfloat16>(ximg_elems(d));
+    if (!d.x_x3()) w.ximg = c.take<__nv_bfloat16>(ximg_elems(d));
     w.gws = c.take<char>(x3_gemm_ws(d, false));
     for (int k = 0; k < d.nd; ++k) {
       w.rtx3[k] = c.take<__nv_bfloat16>(tc_rec_x3_pack_elems(sh));
@@ -321,14 +332,20 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
   const int64_t G = g4(d), Gc = d.nd * G;
   // the split images of [W_fw | W_bw] (each direction straight into its column block)
   // and of [X | 1]; with a reserve they stay there for the backward's dX and dW GEMMs
+  // (SL_LAYER_X_X3: x already is that image, written by the previous layer's K2)
   __nv_bfloat16* wi = rv.wimg ? rv.wimg : w.wimg;
-  __nv_bfloat16* xi = rv.ximg ? rv.ximg : w.ximg;
+  __nv_bfloat16* xi = d.x_x3() ? reinterpret_cast<__nv_bfloat16*>(const_cast<float*>(x))
+                               : (rv.ximg ? rv.ximg : w.ximg);
   const int64_t wl = wimg_ld(d), xl = ximg_ld(d), M = d.BT();
   for (int k = 0; k < d.nd; ++k) {
     x3_split_into(W[k], G, d.D, (int)G, -1, wi + k * G, wl, G, (int64_t)d.D * wl, st);
     SL_CUDA_TRY(cudaMemcpyAsync(w.bcat + k * G, b[k], G * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
-  x3_split_into(x, d.D, (int)M, d.D, d.D, xi, xl, xl, M * xl, st);
+  if (!d.x_x3()) x3_split_into(x, d.D, (int)M, d.D, d.D, xi, xl, xl, M * xl, st);
+  // SL_LAYER_Y_X3: K2 writes y as the next layer's x image (its ones column set here)
+  __nv_bfloat16* yimg = d.y_x3() ? reinterpret_cast<__nv_bfloat16*>(y) : nullptr;
+  const int64_t yl = x3_img_ld(d.nd * d.H + 1);
+  if (yimg) fill_col_bf16(d.BT(), d.nd * d.H, yimg, yl, 1.f, st);
   {
     Phase ph(st, "k1_xw_gemm", 2.0 * d.BT() * d.D * (double)Gc);
     gemm_f32x3_ex(false, false, (int)M, (int)Gc, d.D, nullptr, 0, xi, nullptr, 0, wi, 0.f, w.xw[0], Gc, w.bcat,
@@ -346,8 +363,11 @@ void fwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     a.dir0 = sh.pair == 2 ? 0 : k0;
     a.lens = lens;
     a.xw_ld = Gc;
-    a.y = y;
+    a.y = yimg ? nullptr : y;
     a.y_ld = (int64_t)d.nd * d.H;
+    a.yimg = yimg;
+    a.yimg_ld = yl;
+    a.yimg_lo = M * yl;
     a.h_last = h_last;
     a.c_last = c_last;
     a.hprev_ld = x3_img_ld(d.H);  // h_{s-1} image rows
@@ -437,7 +457,8 @@ void bwd_x3(const sl_lstm_layer* L, const Dims& d, const float* x, const int32_t
     if (want_w || dbk) {
       Phase ph(st, "k4_dw_gemm", 2.0 * M * (double)G * d.D);
       if (want_w) {
-        gemm_f32x3_ex(true, false, d.D, (int)G, M, nullptr, 0, rv.ximg, nullptr, 0, zk, beta, dW[k], G, nullptr,
+        const __nv_bfloat16* xi = d.x_x3() ? reinterpret_cast<const __nv_bfloat16*>(x) : rv.ximg;
+        gemm_f32x3_ex(true, false, d.D, (int)G, M, nullptr, 0, xi, nullptr, 0, zk, beta, dW[k], G, nullptr,
                       dbk, G, w.gws, st, xl, (int64_t)M * xl, zl, zlo);
       } else {  // db alone: fixed-order column sums of DZ_d (hi + lo)
         colsum_img_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(M, (int)G, zk, zl, zlo, beta, dbk);

@@ -53,6 +53,10 @@ struct TcRecFwdArgs {
   int trace_cta;
   int xw_tma;       // pair kernel: x W tiles may be TMA-loaded (set internally)
   // ---- fp32-class ("x3", split-bf16) pair kernel only: one direction per launch
+  // (SL_LAYER_Y_X3) y written as its split image instead of fp32: hi rows at yimg (row
+  // stride yimg_ld, position-major like y), lo rows yimg_lo elements further on
+  __nv_bfloat16* yimg;
+  int64_t yimg_ld, yimg_lo;
   int dir0;                      // global index of launch direction 0 (y columns, h_last / c_last rows)
   const float* xwf[2];           // hoisted x W + b, fp32 [B*T, xw_ld]
   __nv_bfloat16* hbuf_lo[2];     // lo halves of h (h - bf16(h)), same ring layout as hbuf (the hi halves)

@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
                 store_f32<kUT>(a.gatesf[d] + gate_save_off(s, g, row, a.B, H, ut0), z + g * kUT, nu);
             }
             if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)gdir * H + ut0, hst, nu);
+            if (a.yimg) store_split<kUT>(a.yimg + pos * a.yimg_ld + (size_t)gdir * H + ut0, a.yimg_lo, hst, nu);
             if (a.gatesf[d]) {  // the saved (c, h)_{prev} of each step, off the critical path
               if (s == 0) {
                 store_f32<kUT>(a.cprevf[d] + cprev_save_off(0, row, a.B, H, ut0), zero, nu);
@@ -505,6 +506,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
         } else {  // padded position t == s: zero output (tape.cpp:797), frozen state
           if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)gdir * H + ut0, zero, nu);
           if constexpr (X3) {
+            if (a.yimg) store_split<kUT>(a.yimg + pos * a.yimg_ld + (size_t)gdir * H + ut0, a.yimg_lo, zero, nu);
             if (a.gatesf[d]) store_split<kUT>(a.hprevi[d] + pos * a.hprev_ld + ut0, a.hprevi_lo, zero, nu);
           } else {
             if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
         const size_t pos = (size_t)row * T + s;
         if (a.y) store_f32<kUT>(a.y + pos * a.y_ld + (size_t)gdir * H + ut0, zero, nu);
         if constexpr (X3) {
+          if (a.yimg) store_split<kUT>(a.yimg + pos * a.yimg_ld + (size_t)gdir * H + ut0, a.yimg_lo, zero, nu);
           if (a.gatesf[d]) store_split<kUT>(a.hprevi[d] + pos * a.hprev_ld + ut0, a.hprevi_lo, zero, nu);
         } else {
           if (a.ybf) store_bf16<kUT>(a.ybf + pos * a.ybf_ld + (size_t)d * H + ut0, zero, nu);

@@ -70,22 +70,27 @@ class BLSTMEncoder:
         # bf16: the activations between layers stay in the padded bf16 layout the
         # next layer's input GEMM reads (SL_LAYER_Y_BF16 -> SL_LAYER_X_BF16); only
         # the top layer's output is fp32
+        # fp32: the same chaining with the split-bf16 images the next layer's fp32-class
+        # input GEMM reads (SL_LAYER_Y_X3 -> SL_LAYER_X_X3): no split pass per layer
         chain = precision == "bf16"
+        chain_x3 = precision == "fp32" and num_layers > 1 and lstm.PATHS[lstm.lib().sl_lstm_layer_path(
+            lstm.ctypes.byref(lstm._Layer(batch, time, 2 * H, H, 2, 1, lstm.PRECISIONS[precision], 0)))] == "fp32_x3_tc"
         last = num_layers - 1 + (1 if chain and top_bf16 else 0)
+        fl = lambda l: dict(x_bf16=chain and (l > 0 or x0_bf16), y_bf16=chain and l < last,
+                            x_x3=chain_x3 and l > 0, y_x3=chain_x3 and l < num_layers - 1)
         shared = None
         if not train:  # the layers run one after another: one workspace serves all of them
-            need = max(lstm.LSTMLayer.workspace_size(batch, time, D, H, 2, 1, precision,
-                                                     x_bf16=chain and (l > 0 or x0_bf16),
-                                                     y_bf16=chain and l < last)
+            need = max(lstm.LSTMLayer.workspace_size(batch, time, D, H, 2, 1, precision, **fl(l))
                        for l, D in enumerate(self.in_dims))
             shared = torch.empty(need, dtype=torch.uint8, device=self.device)
-        self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device,
-                                      x_bf16=chain and (l > 0 or x0_bf16), y_bf16=chain and l < last,
-                                      train=train, workspace=shared)
+        self.layers = [lstm.LSTMLayer(batch, time, D, H, 2, 1, precision, self.device, train=train,
+                                      workspace=shared, **fl(l))
                        for l, D in enumerate(self.in_dims)]
         def act(l):  # layer l's output buffer
             if chain and l < last:
                 return torch.zeros(batch, time, lstm.bf16_pitch(2 * H), dtype=torch.bfloat16, device=self.device)
+            if chain_x3 and l < num_layers - 1:
+                return lstm.x3_image(batch, time, 2 * H, self.device)
             return torch.empty(batch, time, 2 * H, dtype=torch.float32, device=self.device)
         if train:
             self.acts = [act(l) for l in range(num_layers)]

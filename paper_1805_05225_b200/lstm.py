@@ -30,6 +30,13 @@ SL_OK, SL_ERR_INVALID_ARGUMENT, SL_ERR_SHAPE, SL_ERR_CUDA, SL_ERR_WORKSPACE, SL_
 PRECISIONS = {"fp32": 0, "bf16": 1}
 PATHS = {1: "bf16_tc", 2: "fp32_x3_tc", 3: "fp32_simt"}  # seqloom_cuda.h enum sl_path
 SL_LAYER_X_BF16, SL_LAYER_Y_BF16 = 1, 2
+SL_LAYER_X_X3, SL_LAYER_Y_X3 = 16, 32
+
+
+def x3_image(batch: int, time: int, features: int, device=None) -> "torch.Tensor":
+    """A zero-initialised split-bf16 activation image of [batch, time, features]
+    (SL_LAYER_Y_X3 / SL_LAYER_X_X3): two bf16 planes [2, batch*time, pitch]."""
+    return torch.zeros((2, batch * time, bf16_pitch(features)), dtype=torch.bfloat16, device=device)
 
 
 def bf16_pitch(features: int) -> int:
@@ -121,15 +128,18 @@ class LSTMLayer:
 
     def __init__(self, batch: int, time: int, input_dim: int, hidden: int, num_dirs: int = 1,
                  direction: int = 1, precision: str = "fp32", device=None, x_bf16: bool = False,
-                 y_bf16: bool = False, train: bool = True, workspace=None):
+                 y_bf16: bool = False, train: bool = True, workspace=None, x_x3: bool = False,
+                 y_x3: bool = False):
         # x_bf16 / y_bf16: padded bf16 activations between stacked layers
-        # (SL_LAYER_X_BF16 / SL_LAYER_Y_BF16, bf16 precision only).
+        # (SL_LAYER_X_BF16 / SL_LAYER_Y_BF16, bf16 precision only); x_x3 / y_x3: the
+        # split-bf16 images instead (SL_LAYER_X_X3 / SL_LAYER_Y_X3, fp32 precision, x3_image()).
         # train=False: an inference-only layer (the reference's grad-disabled
         # Tape(false), tape.cpp:103) — no reserve is allocated and forward()
         # saves nothing.  workspace: an optional caller-owned uint8 buffer of at
         # least workspace_size() bytes (stacked inference layers can share one).
-        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
-        self.x_bf16, self.y_bf16 = x_bf16, y_bf16
+        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0) | \
+            (SL_LAYER_X_X3 if x_x3 else 0) | (SL_LAYER_Y_X3 if y_x3 else 0)
+        self.x_bf16, self.y_bf16, self.x_x3, self.y_x3 = x_bf16, y_bf16, x_x3, y_x3
         self.desc = _Layer(batch, time, input_dim, hidden, num_dirs, direction,
                            PRECISIONS[precision], flags)
         self.device = torch.device(device or "cuda")
@@ -151,8 +161,9 @@ class LSTMLayer:
 
     @staticmethod
     def workspace_size(batch, time, input_dim, hidden, num_dirs=1, direction=1, precision="fp32",
-                       x_bf16=False, y_bf16=False) -> int:
-        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0)
+                       x_bf16=False, y_bf16=False, x_x3=False, y_x3=False) -> int:
+        flags = (SL_LAYER_X_BF16 if x_bf16 else 0) | (SL_LAYER_Y_BF16 if y_bf16 else 0) | \
+            (SL_LAYER_X_X3 if x_x3 else 0) | (SL_LAYER_Y_X3 if y_x3 else 0)
         d = _Layer(batch, time, input_dim, hidden, num_dirs, direction, PRECISIONS[precision], flags)
         return lib().sl_lstm_workspace_size(ctypes.byref(d))
 
@@ -174,6 +185,8 @@ class LSTMLayer:
             raise RuntimeError("forward(train=True) on an inference-only layer (constructed with train=False)")
         if self.x_bf16:
             _need(x, (B, T, bf16_pitch(D)), "x", torch.bfloat16)
+        elif self.x_x3:
+            _need(x, (2, B * T, bf16_pitch(D)), "x", torch.bfloat16)
         else:
             _need(x, (B, T, D), "x")
         _need(seq_lens, (B,), "seq_lens", torch.int32)
@@ -183,10 +196,14 @@ class LSTMLayer:
             _need(b[k], (4 * H,), f"b[{k}]")
         if y is None and self.y_bf16:
             y = torch.zeros((B, T, bf16_pitch(nd * H)), dtype=torch.bfloat16, device=self.device)
+        elif y is None and self.y_x3:
+            y = x3_image(B, T, nd * H, self.device)
         elif y is None:
             y = torch.empty((B, T, nd * H), dtype=torch.float32, device=self.device)
         elif self.y_bf16:
             _need(y, (B, T, bf16_pitch(nd * H)), "y", torch.bfloat16)
+        elif self.y_x3:
+            _need(y, (2, B * T, bf16_pitch(nd * H)), "y", torch.bfloat16)
         if h_last is None:
             h_last = torch.empty((nd, B, H), dtype=torch.float32, device=self.device)
         if c_last is None:

@@ -110,6 +110,21 @@ def test_bf16_activation_flags():
         assert L.sl_lstm_bf16_pitch(f) == lstm.bf16_pitch(f) == (f + 64) // 64 * 64
 
 
+def test_x3_activation_flags():
+    # SL_LAYER_X_X3 / SL_LAYER_Y_X3: fp32 precision on the tensor-core path only; with
+    # an x image the reserve no longer carries the layer's own [X | 1] image
+    L = lstm.lib()
+    both = lstm.SL_LAYER_X_X3 | lstm.SL_LAYER_Y_X3
+    kw = dict(batch=64, time=30, input_dim=200, hidden=64, num_dirs=2)
+    assert L.sl_lstm_layer_check(ctypes.byref(desc(precision=0, flags=both, **kw))) == 0
+    assert L.sl_lstm_layer_check(ctypes.byref(desc(precision=1, flags=lstm.SL_LAYER_X_X3, **kw))) == \
+        lstm.SL_ERR_UNSUPPORTED
+    assert "x3" in L.sl_last_error().decode()
+    r0 = L.sl_lstm_reserve_size(ctypes.byref(desc(precision=0, **kw)))
+    r1 = L.sl_lstm_reserve_size(ctypes.byref(desc(precision=0, flags=lstm.SL_LAYER_X_X3, **kw)))
+    assert 0 < r1 <= r0 - 2 * 64 * 30 * lstm.bf16_pitch(200) * 2
+
+
 def test_attn_decoder_descriptor_validation():
     """sl_attn_decoder_workspace_size: host-only shape checks (0 + sl_last_error on bad dims)."""
     from paper_1805_05225_b200.decoder import _Desc
