@@ -52,6 +52,10 @@ struct FLay {
   __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
   __nv_bfloat16 *ws_f, *ws_b;    // W_s split for s_tr = s W_s and d s = d s_tr W_s^T
   float* str_all;                // [T, B, K] s_tr of every step (the backward reuses it)
+  // split images of operands two GEMMs each read (one split serves both): the readout
+  // input and enc with their ones columns (the bias-gradient rows), d pre and d enc_ctx
+  __nv_bfloat16 *roi, *enci, *dprei, *dctxi;
+  int64_t roi_ld, enci_ld, dprei_ld, dctxi_ld;
   void *att_ws, *gws, *emb_ws;
   size_t bytes;
 };
@@ -124,6 +128,14 @@ FLay flayout(const DecDims& d, void* base) {
   L.ws_f = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)H, (int)K) * 2));
   L.ws_b = L.ws_f;
   L.str_all = tf(T * B * K);
+  auto timg = [&](int64_t rows, int64_t cols, __nv_bfloat16*& img, int64_t& ld) {
+    img = static_cast<__nv_bfloat16*>(take(x3_img_elems((int)rows, (int)cols) * 2));
+    ld = x3_img_ld((int)cols);
+  };
+  timg(BT, L.RO + 1, L.roi, L.roi_ld);
+  timg(BTs, E + 1, L.enci, L.enci_ld);
+  timg(BT, d.Rd, L.dprei, L.dprei_ld);
+  timg(BTs, K, L.dctxi, L.dctxi_ld);
   L.att_ws = take(attention_workspace_bytes(d.B, d.K, d.H, d.Ts));
   L.gws = take(gemm_ws_bytes(d));
   L.emb_ws = take(embedding_workspace_bytes(BT, d.Vt));
@@ -477,7 +489,10 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     count_launch();
     // trg_{t-1} straight into the readout-input rows (columns H..H+Emb)
     embedding_fwd(BT, L.ids_tm, d.Vt, Emb, p.trg_W, L.ro + H, L.RO, SL_EMB_NEGATIVE_ZERO, bad_row, st);
-    gemm_f32x3(false, false, (int)BTs, K, E, enc, E, p.ctx_W, K, 0.f, L.enc_ctx, K, p.ctx_b, nullptr, 0, L.gws, st);
+    // enc's image (ones column at E for the backward's d b_ctx row), kept for that GEMM
+    x3_split_into(enc, E, (int)BTs, E, E, L.enci, L.enci_ld, L.enci_ld, BTs * L.enci_ld, st);
+    gemm_f32x3_ex(false, false, (int)BTs, K, E, nullptr, 0, L.enci, p.ctx_W, K, nullptr, 0.f, L.enc_ctx, K, p.ctx_b,
+                  nullptr, 0, L.gws, st, L.enci_ld, BTs * L.enci_ld);
     gemm_f32x3(false, false, (int)BT, 4 * H, Emb, L.ro + H, L.RO, p.s_W, 4 * H, 0.f, L.xw, 4 * H, p.s_b, nullptr, 0,
                L.gws, st);
   }
@@ -514,8 +529,10 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
   }
   {
     Phase ph(st, "k10_dec_fwd_hoisted", 2.0 * BT * L.RO * d.Rd);
-    gemm_f32x3(false, false, (int)BT, d.Rd, (int)L.RO, L.ro, L.RO, p.ro_W, d.Rd, 0.f, L.dpre, d.Rd, p.ro_b, nullptr,
-               0, L.gws, st);  // pre-activation (dpre is free until the backward)
+    // the readout input's image (ones column at RO for d b_ro), kept for the backward's d W_ro
+    x3_split_into(L.ro, L.RO, (int)BT, (int)L.RO, (int)L.RO, L.roi, L.roi_ld, L.roi_ld, BT * L.roi_ld, st);
+    gemm_f32x3_ex(false, false, (int)BT, d.Rd, (int)L.RO, nullptr, 0, L.roi, p.ro_W, d.Rd, nullptr, 0.f, L.dpre,
+                  d.Rd, p.ro_b, nullptr, 0, L.gws, st, L.roi_ld, BT * L.roi_ld);  // pre-activation (dpre is free until the backward)
     f32_relu_kernel<<<std::min<unsigned>(grid_of(BT * d.Rd), 148 * 8), 256, 0, st>>>(L.dpre, readout, B, T, d.Rd);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -537,10 +554,11 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
     // d readout input = d pre W_ro^T; [d W_ro; d b_ro] = [X | 1]^T d pre
-    gemm_f32x3(false, true, (int)BT, (int)L.RO, Rd, L.dpre, Rd, p.ro_W, Rd, 0.f, L.dro, L.RO, nullptr, nullptr, 0,
-               L.gws, st);
-    gemm_f32x3(true, false, (int)L.RO, Rd, (int)BT, L.ro, L.RO, L.dpre, Rd, 0.f, g.ro_W, Rd, nullptr, g.ro_b, Rd,
-               L.gws, st);
+    x3_split_into(L.dpre, Rd, (int)BT, Rd, -1, L.dprei, L.dprei_ld, L.dprei_ld, BT * L.dprei_ld, st);
+    gemm_f32x3_ex(false, true, (int)BT, (int)L.RO, Rd, nullptr, 0, L.dprei, p.ro_W, Rd, nullptr, 0.f, L.dro, L.RO,
+                  nullptr, nullptr, 0, L.gws, st, L.dprei_ld, BT * L.dprei_ld);
+    gemm_f32x3_ex(true, false, (int)L.RO, Rd, (int)BT, nullptr, 0, L.roi, nullptr, 0, L.dprei, 0.f, g.ro_W, Rd,
+                  nullptr, g.ro_b, Rd, L.gws, st, L.roi_ld, BT * L.roi_ld, L.dprei_ld, BT * L.dprei_ld);
   }
   X3Parts dxp{nullptr, 0, 0, 0};  // d [att ‖ s]_t from step t + 1 (partials)
   for (int t = T - 1; t >= 0; --t) {
@@ -628,8 +646,11 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
                  st);
     }
     // enc_ctx = enc W_ctx + b_ctx: [d W_ctx; d b_ctx] = [enc | 1]^T d enc_ctx; d enc += d enc_ctx W_ctx^T
-    gemm_f32x3(true, false, E, K, (int)BTs, enc, E, L.dctx, K, 0.f, g.ctx_W, K, nullptr, g.ctx_b, K, L.gws, st);
-    gemm_f32x3(false, true, (int)BTs, E, K, L.dctx, K, p.ctx_W, K, 1.f, d_enc, E, nullptr, nullptr, 0, L.gws, st);
+    x3_split_into(L.dctx, K, (int)BTs, K, -1, L.dctxi, L.dctxi_ld, L.dctxi_ld, BTs * L.dctxi_ld, st);
+    gemm_f32x3_ex(true, false, E, K, (int)BTs, nullptr, 0, L.enci, nullptr, 0, L.dctxi, 0.f, g.ctx_W, K, nullptr,
+                  g.ctx_b, K, L.gws, st, L.enci_ld, BTs * L.enci_ld, L.dctxi_ld, BTs * L.dctxi_ld);
+    gemm_f32x3_ex(false, true, (int)BTs, E, K, nullptr, 0, L.dctxi, p.ctx_W, K, nullptr, 1.f, d_enc, E, nullptr,
+                  nullptr, 0, L.gws, st, L.dctxi_ld, BTs * L.dctxi_ld);
   }
 }
 
