@@ -72,7 +72,9 @@ X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const fl
 // or chunked accumulation
 bool gemm_f32x3_softmax_stats(int M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
                               float* C, int64_t ldc, const float* bias, float4* sm_part, int sm_ld,
-                              const int32_t* targets, void* ws, cudaStream_t st);
+                              const int32_t* targets, void* ws, cudaStream_t st,
+                              const __nv_bfloat16* A3 = nullptr, int64_t a3_ld = 0, int64_t a3_lo = 0,
+                              const __nv_bfloat16* B3 = nullptr, int64_t b3_ld = 0, int64_t b3_lo = 0);
 // both operands pre-split (images of the stored A and B)
 void gemm_f32x3_pab(bool transA, bool transB, int M, int N, int K, const __nv_bfloat16* A3,
                     const __nv_bfloat16* B3, float beta, float* C, int64_t ldc, const float* bias, void* ws,

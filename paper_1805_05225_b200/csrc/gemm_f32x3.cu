@@ -291,15 +291,16 @@ X3Parts gemm_f32x3_parts(bool transA, bool transB, int M, int N, int K, const fl
 
 bool gemm_f32x3_softmax_stats(int M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
                               float* C, int64_t ldc, const float* bias, float4* sm_part, int sm_ld,
-                              const int32_t* targets, void* ws, cudaStream_t st) {
+                              const int32_t* targets, void* ws, cudaStream_t st, const __nv_bfloat16* A3,
+                              int64_t a3_ld, int64_t a3_lo, const __nv_bfloat16* B3, int64_t b3_ld, int64_t b3_lo) {
   const X3Dims d = x3_dims(false, false, M, N, K, false);
   const bool single = d.ksplit == 1 && ceil_div(K, 64) <= kX3ChunkBlocks;
   TcGemm sm{};
   sm.sm_part = sm_part;
   sm.sm_ld = sm_ld;
   sm.sm_targets = targets;
-  x3_core(false, false, M, N, K, A, lda, nullptr, B, ldb, nullptr, 0.f, C, ldc, bias, nullptr, 0, ws, st, 0, 0, 0, 0,
-          nullptr, single ? &sm : nullptr);
+  x3_core(false, false, M, N, K, A, lda, A3, B, ldb, B3, 0.f, C, ldc, bias, nullptr, 0, ws, st, a3_ld, a3_lo, b3_ld,
+          b3_lo, nullptr, single ? &sm : nullptr);
   return single;
 }
 

@@ -389,7 +389,8 @@ size_t output_ce_f32_workspace_bytes(int B, int T, int D, int V) {
                               gemm_f32x3_workspace_bytes(false, true, (int)rows, D, V, false),    // dX
                               gemm_f32x3_workspace_bytes(true, false, D, V, (int)rows, true)});   // [dW; db]
   return (size_t)round_up(rows * V * 4, 256) + (size_t)round_up(x3_img_elems((int)rows, V) * 2, 256) +
-         (size_t)round_up(rows * ceil_div(V, 128) * sizeof(float4), 256) + (size_t)round_up(sizeof(CeScratch), 256) + x3;
+         (size_t)round_up(rows * ceil_div(V, 128) * sizeof(float4), 256) + (size_t)round_up(sizeof(CeScratch), 256) +
+         (size_t)round_up(x3_img_elems((int)rows, D + 1) * 2, 256) + (size_t)round_up(x3_img_elems(D, V) * 2, 256) + x3;
 }
 
 void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* targets, const int32_t* lens,
@@ -405,7 +406,17 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   auto* smp = reinterpret_cast<float4*>(w);  // per (row, 128-column block) softmax statistics
   w += round_up(rows * nblk * sizeof(float4), 256);
   auto* sc = reinterpret_cast<CeScratch*>(w);
-  void* gws = w + round_up(sizeof(CeScratch), 256);
+  w += round_up(sizeof(CeScratch), 256);
+  // x (ones column at D: the d b row) and W split once, each image read by two GEMMs
+  auto* xi = reinterpret_cast<__nv_bfloat16*>(w);
+  const int64_t xl = x3_img_ld(D + 1);
+  w += round_up(x3_img_elems((int)rows, D + 1) * 2, 256);
+  auto* wi = reinterpret_cast<__nv_bfloat16*>(w);
+  const int64_t wl = x3_img_ld(V);
+  w += round_up(x3_img_elems(D, V) * 2, 256);
+  void* gws = w;
+  x3_split_into(x, D, (int)rows, D, D, xi, xl, xl, rows * xl, stream);
+  x3_split_img(W, V, D, V, wi, stream);
   SL_CUDA_TRY(cudaMemsetAsync(bad_target, 0, sizeof(int), stream));
   ce_count_kernel<<<1, 256, 0, stream>>>(lens, B, T, sc);
   SL_CUDA_TRY(cudaGetLastError());
@@ -416,7 +427,8 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
     Phase ph(stream, "k7_logits_gemm", f);
     // (an out-of-range target only fails to match a column in the statistics; the CE
     // kernel still sees the raw id and poisons the step)
-    stats = gemm_f32x3_softmax_stats((int)rows, V, D, x, D, W, V, z, V, b, smp, nblk, targets, gws, stream);
+    stats = gemm_f32x3_softmax_stats((int)rows, V, D, nullptr, 0, nullptr, 0, z, V, b, smp, nblk, targets, gws,
+                                     stream, xi, xl, rows * xl, wi, wl, (int64_t)D * wl);
   }
   {
     Phase ph(stream, "k7_softmax_ce", 0.0, 12.0 * rows * V);
@@ -434,13 +446,13 @@ void output_ce_f32(int B, int T, int D, int V, const float* x, const int32_t* ta
   const float beta = accumulate ? 1.f : 0.f;
   if (dx) {
     Phase ph(stream, "k7_dx_gemm", f);
-    gemm_f32x3_ex(false, true, (int)rows, D, V, nullptr, 0, dzi, W, V, nullptr, beta, dx, D, nullptr, nullptr, 0,
-                  gws, stream);
+    gemm_f32x3_ex(false, true, (int)rows, D, V, nullptr, 0, dzi, nullptr, 0, wi, beta, dx, D, nullptr, nullptr, 0,
+                  gws, stream, 0, 0, wl, (int64_t)D * wl);
   }
   if (dW) {
     Phase ph(stream, "k7_dw_gemm", f);
-    gemm_f32x3_ex(true, false, D, V, (int)rows, x, D, nullptr, nullptr, 0, dzi, beta, dW, V, nullptr, db, V, gws,
-                  stream);
+    gemm_f32x3_ex(true, false, D, V, (int)rows, nullptr, 0, xi, nullptr, 0, dzi, beta, dW, V, nullptr, db, V, gws,
+                  stream, xl, rows * xl);
   } else if (db) {
     SL_REQUIRE(false, SL_ERR_INVALID_ARGUMENT, "output_ce (fp32): db needs dW");
   }
