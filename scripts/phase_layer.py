@@ -18,6 +18,9 @@ ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
 L = lstm.lib()
 L.sl_profile_enable.argtypes = [ctypes.c_int]
+if os.environ.get("SL_DEBUG_FLAGS"):  # experiments builds: timing switches (capi.cu sl_debug_set_flags)
+    L.sl_debug_set_flags.argtypes = [ctypes.c_int]
+    L.sl_debug_set_flags(int(os.environ["SL_DEBUG_FLAGS"]))
 
 
 class Entry(ctypes.Structure):
