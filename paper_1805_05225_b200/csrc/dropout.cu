@@ -7,6 +7,8 @@
 // backward instead of stored.  key = mix64(key0, batch_counter); the counter may be
 // read on the device (e.g. the optimizer's step counter) so a captured CUDA graph
 // draws a new mask every replay.
+#include <cmath>
+
 #include "dropout.h"
 #include "profile.h"
 
@@ -25,21 +27,35 @@ __device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {
 
 // out = in * inv_keep where the element survives, else 0 (the forward on x and the
 // adjoint on dy are the same map)
-__global__ void dropout_kernel(int B, int T, int F, float rate, float inv_keep, uint64_t key0,
+// keep(h): u01(h) >= rate, with u01 = (splitmix64(h) >> 11) * 2^-53 exact in double, is
+// the integer test (splitmix64(h) >> 11) >= thr53 for thr53 = ceil(rate * 2^53) (host)
+__device__ __forceinline__ bool keep(uint64_t key, uint64_t ct, uint64_t idx, uint64_t thr53) {
+  return (splitmix64(mix64(key, mix64(ct, idx))) >> 11) >= thr53;
+}
+__global__ void dropout_kernel(int B, int T, int F, uint64_t thr53, float inv_keep, uint64_t key0,
                                const int32_t* counter, int64_t counter_value, const float* __restrict__ in,
                                float* __restrict__ out) {
   const uint64_t key = mix64(key0, (uint64_t)(counter ? (int64_t)*counter : counter_value));
-  const double thr = (double)rate;
+  const bool v4 = (F % 4) == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   // one CTA per (b, t) row: no 64-bit division per element
   for (int64_t r = blockIdx.x; r < (int64_t)B * T; r += gridDim.x) {
     const int b = (int)(r / T), t = (int)(r - (int64_t)b * T);
-    const uint64_t ct = (uint64_t)(t + 2);
+    const uint64_t ct = (uint64_t)(t + 2), i0 = (uint64_t)b * F;
     const float* src = in + r * F;
     float* dst = out + r * F;
-    for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      const uint64_t h = mix64(key, mix64(ct, (uint64_t)b * F + f));
-      const double u = (double)(splitmix64(h) >> 11) * 0x1.0p-53;
-      dst[f] = u >= thr ? src[f] * inv_keep : 0.f;
+    if (v4) {  // four elements per thread: 16 B loads / stores, four independent hash chains
+      for (int f = threadIdx.x * 4; f < F; f += blockDim.x * 4) {
+        const float4 x = *reinterpret_cast<const float4*>(src + f);
+        float4 y;
+        y.x = keep(key, ct, i0 + f, thr53) ? x.x * inv_keep : 0.f;
+        y.y = keep(key, ct, i0 + f + 1, thr53) ? x.y * inv_keep : 0.f;
+        y.z = keep(key, ct, i0 + f + 2, thr53) ? x.z * inv_keep : 0.f;
+        y.w = keep(key, ct, i0 + f + 3, thr53) ? x.w * inv_keep : 0.f;
+        *reinterpret_cast<float4*>(dst + f) = y;
+      }
+    } else {
+      for (int f = threadIdx.x; f < F; f += blockDim.x)
+        dst[f] = keep(key, ct, i0 + f, thr53) ? src[f] * inv_keep : 0.f;
     }
   }
 }
@@ -53,7 +69,10 @@ void dropout_apply(int B, int T, int F, float rate, uint64_t key0, const int32_t
   const float inv_keep = 1.0f / (1.0f - rate);  // Real(1) / (Real(1) - rate), fp32 like the reference build
   Phase ph(st, "k11_dropout", 0.0, 8.0 * n);
   const int grid = (int)std::min<int64_t>((int64_t)B * T, 148 * 16);
-  dropout_kernel<<<grid, 256, 0, st>>>(B, T, F, rate, inv_keep, key0, counter, counter_value, in, out);
+  // u >= rate (doubles) <=> k >= rate * 2^53 for the integer k = u * 2^53 (exact scaling)
+  const double r53 = std::ldexp((double)rate, 53);
+  const uint64_t thr53 = r53 <= 0.0 ? 0ull : (uint64_t)std::ceil(r53);
+  dropout_kernel<<<grid, 256, 0, st>>>(B, T, F, thr53, inv_keep, key0, counter, counter_value, in, out);
   SL_CUDA_TRY(cudaGetLastError());
   count_launch();
 }

@@ -142,10 +142,10 @@ def test_dropout_matches_reference_mask_bitwise(cuda):
     path equals the host-value path."""
     from paper_1805_05225_b200.dropout import Dropout
     rng = np.random.default_rng(3)
-    B, T, F = 16, 60, 1000
-    x = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
-    d = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
-    for seed, counter, rate in ((1, 0, 0.3), (77, 12, 0.5)):
+    for (B, T, F), seed, counter, rate in (((16, 60, 1000), 1, 0, 0.3), ((16, 60, 1000), 77, 12, 0.5),
+                                           ((4, 5, 999), 5, 3, 0.1), ((3, 7, 1000), 9, 1, 0.0)):
+        x = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
+        d = rng.uniform(-1, 1, (B, T, F)).astype(np.float32)
         dr = Dropout(rate, seed, "output/output_prob", 0)
         xg, dg = torch.as_tensor(x).cuda(), torch.as_tensor(d).cuda()
         y, dx = torch.empty_like(xg), torch.empty_like(xg)
