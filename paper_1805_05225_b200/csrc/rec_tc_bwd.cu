@@ -652,9 +652,10 @@ __global__ void __launch_bounds__(64 + 128 * MT * SPLIT, 1)
 }
 
 // RB[(cl*C + r)*NB + n][kk] = R[cl*C*U + n][r*Kc + kk]  (bf16; zero outside the layer)
-// LO: the rounding remainder R - bf16(R) instead, written P * NB rows further on.
+// BOTH: also the rounding remainder R - bf16(R) (x3), written P * NB rows further on —
+// R read once for both parts.
 // One CTA per packed row; threads along kk (coalesced on both sides), 32-bit math.
-template <bool LO>
+template <bool BOTH>
 __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U, int NB, int P,
                                int Kc, __nv_bfloat16* __restrict__ RB, bool interleave = false) {
   const int rowi = blockIdx.x;
@@ -662,23 +663,21 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   const int cl = cta / C, r = cta % C;
   const int unit = cl * C * U + n;
   const bool live = n < C * U && unit < H;
-  __nv_bfloat16* dst = RB + ((LO ? (size_t)P * NB : 0) + rowi) * Kc;
-  // interleave (the streamed R_lo of kX3C): the lo rows in the core-matrix layout
+  // interleave (the streamed R of kX3C): the rows in the core-matrix layout
   // [Kc / 8][P * NB rows][8], so a TMA box of NB rows x 8 K is one contiguous 128 B-row run
   // (16 B rows of a row-major slice would cost one TMA request each)
-  __nv_bfloat16* ilv = RB + (LO ? (size_t)P * NB * Kc : 0);
+  const size_t part = (size_t)P * NB * Kc;  // the lo part follows the hi part
   auto at = [&](int kk) -> __nv_bfloat16* {
-    return interleave ? ilv + ((size_t)(kk / 8) * P * NB + rowi) * 8 + kk % 8 : dst + kk;
+    return interleave ? RB + ((size_t)(kk / 8) * P * NB + rowi) * 8 + kk % 8 : RB + (size_t)rowi * Kc + kk;
   };
-  auto cvt = [](float v) {
-    return __float2bfloat16_rn(LO ? v - __bfloat162float(__float2bfloat16_rn(v)) : v);
-  };
+  auto lo_of = [](float v) { return __float2bfloat16_rn(v - __bfloat162float(__float2bfloat16_rn(v))); };
   const int hq8 = dz_ring_hq(H);
   if (hq8 != H) {  // gate blocks padded to a multiple of 8 columns in the DZ ring
     for (int kk = threadIdx.x; kk < Kc; kk += blockDim.x) {
       const int col = r * Kc + kk, g = col / hq8, u = col % hq8;
       const float v = (live && g < 4 && u < H) ? __ldg(R + (size_t)unit * 4 * H + (size_t)g * H + u) : 0.f;
-      *at(kk) = cvt(v);
+      *at(kk) = __float2bfloat16_rn(v);
+      if (BOTH) at(kk)[part] = lo_of(v);
     }
     return;
   }
@@ -686,6 +685,11 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
   const int valid = live ? max(0, min(Kc, 4 * H - r * Kc)) : 0;
   // 4 columns per thread: float4 loads when the row start is 16 B aligned, 8 B bf16 stores
   const bool vec = (((uintptr_t)src) & 15) == 0 && (Kc % 4) == 0;
+  auto pack4 = [](__nv_bfloat16 b0, __nv_bfloat16 b1, __nv_bfloat16 b2, __nv_bfloat16 b3) {
+    __nv_bfloat162 p0, p1;
+    p0.x = b0, p0.y = b1, p1.x = b2, p1.y = b3;
+    return make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
+  };
   for (int kk = threadIdx.x * 4; kk < Kc; kk += blockDim.x * 4) {
     float v[4];
     if (vec && kk + 4 <= valid) {
@@ -696,13 +700,15 @@ __global__ void pack_rb_kernel(const float* __restrict__ R, int H, int C, int U,
       for (int u = 0; u < 4; ++u) v[u] = kk + u < valid ? __ldg(src + kk + u) : 0.f;
     }
     if (kk + 4 <= Kc) {
-      const __nv_bfloat16 b0 = cvt(v[0]), b1 = cvt(v[1]), b2 = cvt(v[2]), b3 = cvt(v[3]);
-      __nv_bfloat162 p0, p1;
-      p0.x = b0, p0.y = b1, p1.x = b2, p1.y = b3;
-      *reinterpret_cast<uint2*>(at(kk)) =
-          make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
+      *reinterpret_cast<uint2*>(at(kk)) = pack4(__float2bfloat16_rn(v[0]), __float2bfloat16_rn(v[1]),
+                                                __float2bfloat16_rn(v[2]), __float2bfloat16_rn(v[3]));
+      if (BOTH)
+        *reinterpret_cast<uint2*>(at(kk) + part) = pack4(lo_of(v[0]), lo_of(v[1]), lo_of(v[2]), lo_of(v[3]));
     } else {
-      for (int u = 0; u < 4 && kk + u < Kc; ++u) *at(kk + u) = cvt(v[u]);
+      for (int u = 0; u < 4 && kk + u < Kc; ++u) {
+        *at(kk + u) = __float2bfloat16_rn(v[u]);
+        if (BOTH) at(kk + u)[part] = lo_of(v[u]);
+      }
     }
   }
 }
@@ -881,13 +887,10 @@ size_t tc_rec_bwd_x3_pack_elems(const TcBwdShape& sh) {
 void tc_rec_bwd_x3_pack(const float* R, int H, const TcBwdShape& sh, __nv_bfloat16* RB, cudaStream_t stream) {
   const int NB = nb_of(sh.C, sh.U);
   const int Kc = sh.Kz / sh.C;
-  pack_rb_kernel<false><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB,
-                                                                    sh.pair == 2);
-  SL_CUDA_TRY(cudaGetLastError());
   pack_rb_kernel<true><<<(unsigned)(sh.P * NB), 256, 0, stream>>>(R, H, sh.C, sh.U, NB, sh.P, Kc, RB,
                                                                    sh.pair == 2);
   SL_CUDA_TRY(cudaGetLastError());
-  count_launch(2);
+  count_launch();
 }
 
 // sh.pair == 2 (kX3C): a.nd == 2, both directions; sh.pair == 1 (kX3): a.nd == 1

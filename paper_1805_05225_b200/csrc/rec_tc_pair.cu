@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(PairCfg<MODE>::kThreads, 1)
 
 // RT rows [pair * 4UC + g * UC + j] = column g*H + pair*UC + j of R (the x3 pair
 // kernels' order), lo rows at + P * 4UC: (R - bf16(R)) rounded to bf16.  One block
-// per (pair, gate) x 64 k, 16 B stores along k.
-template <int UC, bool LO>
+// per (pair, gate) x 64 k, 16 B stores along k; R is read once for both parts.
+template <int UC>
 __global__ void __launch_bounds__(256) pack_rt_x3_kernel(const float* __restrict__ R, int H, int Kp, int P,
                                                          __nv_bfloat16* __restrict__ RT) {
   __shared__ float tile[64][UC + 1];
@@ -563,16 +563,18 @@ __global__ void __launch_bounds__(256) pack_rt_x3_kernel(const float* __restrict
     tile[i][j] = (k < H && j < units_here) ? __ldg(R + (size_t)k * 4 * H + c0 + j) : 0.f;
   }
   __syncthreads();
-  __nv_bfloat16* dst = RT + (LO ? (size_t)P * 4 * UC * Kp : 0);
+  const size_t lo_off = (size_t)P * 4 * UC * Kp;
   for (int e = threadIdx.x; e < UC * 8; e += 256) {
     const int j = e / 8, kq = (e % 8) * 8;
-    float f[8];
+    float f[8], l[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const float x = tile[kq + u][j];
-      f[u] = LO ? x - __bfloat162float(__float2bfloat16_rn(x)) : x;
+      f[u] = tile[kq + u][j];
+      l[u] = f[u] - __bfloat162float(__float2bfloat16_rn(f[u]));
     }
-    *reinterpret_cast<uint4*>(dst + ((size_t)cta * 4 * UC + g * UC + j) * Kp + k0 + kq) = pack8_bf16(f);
+    __nv_bfloat16* dst = RT + ((size_t)cta * 4 * UC + g * UC + j) * Kp + k0 + kq;
+    *reinterpret_cast<uint4*>(dst) = pack8_bf16(f);
+    *reinterpret_cast<uint4*>(dst + lo_off) = pack8_bf16(l);
   }
 }
 
@@ -706,17 +708,10 @@ size_t tc_rec_x3_pack_elems(const TcFwdShape& sh) { return (size_t)2 * sh.P * 4 
 
 void tc_rec_x3_pack(const float* R, int H, const TcFwdShape& sh, __nv_bfloat16* RT, cudaStream_t stream) {
   const dim3 grid((unsigned)sh.P * 4, (unsigned)(sh.Kp / 64));
-  if (sh.U == 32) {
-    pack_rt_x3_kernel<32, false><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
-    SL_CUDA_TRY(cudaGetLastError());
-    pack_rt_x3_kernel<32, true><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
-  } else {
-    pack_rt_x3_kernel<16, false><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
-    SL_CUDA_TRY(cudaGetLastError());
-    pack_rt_x3_kernel<16, true><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
-  }
+  if (sh.U == 32) pack_rt_x3_kernel<32><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
+  else pack_rt_x3_kernel<16><<<grid, 256, 0, stream>>>(R, H, sh.Kp, sh.P, RT);
   SL_CUDA_TRY(cudaGetLastError());
-  count_launch(2);
+  count_launch();
 }
 
 // x3: sh.pair == 1 -> one direction (a.nd == 1, RT[0]); sh.pair == 2 -> both (a.nd == 2)
