@@ -190,6 +190,62 @@ __global__ void f32_cell_fwd_kernel(GateF a) {
   }
 }
 
+// the same for 4 consecutive units per thread (H % 4 == 0, 16 B aligned rows): 16 B
+// loads of x W and of the split-K partials, 16 B stores, identical arithmetic
+__global__ void f32_cell_fwd4_kernel(GateF a) {
+  const int H = a.H, H4 = H / 4;
+  const int64_t n = (int64_t)a.B * H4;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int b = (int)(e / H4), j = (int)(e % H4) * 4;
+  const int64_t row = (int64_t)a.t * a.B + b;
+  const float* x = a.xw + row * 4 * H;
+  float z[4][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const float4 xv = *reinterpret_cast<const float4*>(x + g * H + j);
+    float4 pv[8];
+    const float* pp = a.z.p + (int64_t)b * a.z.ld + g * H + j;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      pv[q] = q < a.z.n ? __ldg(reinterpret_cast<const float4*>(pp + q * a.z.stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);  // the partials in order, as x3_parts_sum
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sv.x += pv[q].x, sv.y += pv[q].y, sv.z += pv[q].z, sv.w += pv[q].w;
+    for (int q = 8; q < a.z.n; ++q) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(pp + q * a.z.stride));
+      sv.x += t.x, sv.y += t.y, sv.z += t.z, sv.w += t.w;
+    }
+    z[g][0] = xv.x + sv.x, z[g][1] = xv.y + sv.y, z[g][2] = xv.z + sv.z, z[g][3] = xv.w + sv.w;
+  }
+  const float4 cp4 = a.t > 0 ? *reinterpret_cast<const float4*>(a.c_all + (row - a.B) * H + j)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float cpv[4] = {cp4.x, cp4.y, cp4.z, cp4.w};
+  float gi[4], gf[4], gg[4], go[4], c[4], tc[4], h[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    gi[u] = sigmoidf_(z[0][u]), gf[u] = sigmoidf_(z[1][u]), gg[u] = tanhf(z[2][u]), go[u] = sigmoidf_(z[3][u]);
+    c[u] = gf[u] * cpv[u] + gi[u] * gg[u];
+    tc[u] = tanhf(c[u]);
+    h[u] = go[u] * tc[u];
+  }
+  auto st4 = [](float* p, const float (&v)[4]) { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); };
+  st4(a.c_all + row * H + j, c);
+  float* gs = a.gates + row * 5 * H + j;
+  st4(gs, gi), st4(gs + H, gf), st4(gs + 2 * H, gg), st4(gs + 3 * H, go), st4(gs + 4 * H, tc);
+  st4(a.s_all + row * H + j, h);
+  st4(a.ro + row * a.RO + j, h);
+  __nv_bfloat16 hh[4], hl[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    hh[u] = __float2bfloat16_rn(h[u]);
+    hl[u] = __float2bfloat16_rn(h[u] - __bfloat162float(hh[u]));
+  }
+  __nv_bfloat16* q = a.xai + (row + a.B) * a.xai_ld + a.E + j;
+  *reinterpret_cast<uint2*>(q) = *reinterpret_cast<const uint2*>(hh);
+  *reinterpret_cast<uint2*>(q + a.xai_lo) = *reinterpret_cast<const uint2*>(hl);
+}
+
 // readout [b, t] = relu(pre [t*B + b])
 __global__ void f32_relu_kernel(const float* __restrict__ pre, float* __restrict__ out, int B, int T, int Rd) {
   const int64_t n = (int64_t)B * T * Rd;
@@ -274,6 +330,67 @@ __global__ void f32_cell_bwd_kernel(CellBF a) {
   put_split(dz + H, a.lo, dc * cp * gf * (1.f - gf));
   put_split(dz + 2 * H, a.lo, dc * gi * (1.f - gg * gg));
   put_split(dz + 3 * H, a.lo, d_o * go * (1.f - go));
+}
+
+// the same for 4 consecutive units per thread (16 B loads and stores, 8 B image stores)
+__global__ void f32_cell_bwd4_kernel(CellBF a) {
+  const int H = a.H, H4 = H / 4;
+  const int64_t n = (int64_t)a.B * H4;
+  const int64_t e4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e4 >= n) return;
+  const int b = (int)(e4 / H4), j = (int)(e4 % H4) * 4;
+  const int64_t e = (int64_t)b * H + j, row = (int64_t)a.t * a.B + b;
+  auto ld4 = [](const float* p, float (&v)[4]) {
+    const float4 q = *reinterpret_cast<const float4*>(p);
+    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+  };
+  float ds[4], gc[4] = {0.f, 0.f, 0.f, 0.f}, gi[4], gf[4], gg[4], go[4], tc[4], cp[4] = {0.f, 0.f, 0.f, 0.f};
+  ld4(a.ds + e, ds);
+  {  // + the attention's d s partials, in order (as x3_parts_sum)
+    float4 pv[8];
+    const float* pp = a.ds_att.p + (int64_t)b * a.ds_att.ld + j;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      pv[q] = q < a.ds_att.n ? __ldg(reinterpret_cast<const float4*>(pp + q * a.ds_att.stride))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sv.x += pv[q].x, sv.y += pv[q].y, sv.z += pv[q].z, sv.w += pv[q].w;
+    for (int q = 8; q < a.ds_att.n; ++q) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(pp + q * a.ds_att.stride));
+      sv.x += t.x, sv.y += t.y, sv.z += t.z, sv.w += t.w;
+    }
+    ds[0] += sv.x, ds[1] += sv.y, ds[2] += sv.z, ds[3] += sv.w;
+  }
+  if (a.dc_in) ld4(a.dc_in + e, gc);
+  const float* gs = a.gates + row * 5 * H + j;
+  ld4(gs, gi), ld4(gs + H, gf), ld4(gs + 2 * H, gg), ld4(gs + 3 * H, go), ld4(gs + 4 * H, tc);
+  if (a.t > 0) ld4(a.c_all + (row - a.B) * H + j, cp);
+  float dco[4], z[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const float gh = ds[u];
+    const float d_o = gh * tc[u];
+    const float dc = gc[u] + gh * go[u] * (1.f - tc[u] * tc[u]);
+    dco[u] = dc * gf[u];
+    z[0][u] = dc * gg[u] * gi[u] * (1.f - gi[u]);
+    z[1][u] = dc * cp[u] * gf[u] * (1.f - gf[u]);
+    z[2][u] = dc * gi[u] * (1.f - gg[u] * gg[u]);
+    z[3][u] = d_o * go[u] * (1.f - go[u]);
+  }
+  *reinterpret_cast<float4*>(a.dc_out + e) = make_float4(dco[0], dco[1], dco[2], dco[3]);
+  __nv_bfloat16* dz = a.dzi + row * a.ld + j;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      hi[u] = __float2bfloat16_rn(z[g][u]);
+      lo[u] = __float2bfloat16_rn(z[g][u] - __bfloat162float(hi[u]));
+    }
+    *reinterpret_cast<uint2*>(dz + g * H) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(dz + g * H + a.lo) = *reinterpret_cast<const uint2*>(lo);
+  }
 }
 
 // d enc[b, s, :] = sum_t a_t[b, s] d att_t[b, :]  (the generic_attention adjoint w.r.t.
@@ -506,7 +623,12 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     {
       Phase q(st, "k10_cell_fwd", 0.0, 4.0 * B * H * 12);
       GateF g{B, T, H, E, t, zp, L.xw, L.gates, L.c_all, L.s_all, L.xai, L.xai_ld, L.xai_lo, L.ro, L.RO};
-      f32_cell_fwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(g);
+      // 4 units per thread where every row and partial is 16 B aligned
+      const bool v4 = H % 4 == 0 && L.RO % 4 == 0 && (zp.n == 0 || (zp.ld % 4 == 0 && zp.stride % 4 == 0 &&
+                                                                   (reinterpret_cast<uintptr_t>(zp.p) & 15) == 0)) &&
+                      (E + L.xai_ld) % 4 == 0 && L.xai_lo % 4 == 0;
+      if (v4) f32_cell_fwd4_kernel<<<grid_of((int64_t)B * H / 4), 256, 0, st>>>(g);
+      else f32_cell_fwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(g);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
     }
@@ -594,7 +716,11 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * H * 12);
       CellBF cb{B, H, t, L.ds, L.gates, L.c_all, t + 1 < T ? L.dc + (int64_t)cur * B * H : nullptr, dsp, L.dzi,
                 L.dzi_ld, BT * L.dzi_ld, L.dc + (int64_t)nxt * B * H};
-      f32_cell_bwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(cb);
+      const bool v4 = H % 4 == 0 && L.dzi_ld % 4 == 0 && (BT * L.dzi_ld) % 4 == 0 &&
+                      (dsp.n == 0 || (dsp.ld % 4 == 0 && dsp.stride % 4 == 0 &&
+                                      (reinterpret_cast<uintptr_t>(dsp.p) & 15) == 0));
+      if (v4) f32_cell_bwd4_kernel<<<grid_of((int64_t)B * H / 4), 256, 0, st>>>(cb);
+      else f32_cell_bwd_kernel<<<grid_of((int64_t)B * H), 256, 0, st>>>(cb);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
     }
