@@ -298,6 +298,35 @@ __global__ void f32_grad_in_kernel(GradIn a) {
   }
 }
 
+// the same for 4 consecutive columns per thread (E % 4 == H % 4 == 0, 16 B aligned rows)
+__global__ void f32_grad_in4_kernel(GradIn a) {
+  const int W4 = (a.E + a.H) / 4;
+  const int64_t n = (int64_t)a.B * W4;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int b = (int)(e / W4), c = (int)(e % W4) * 4;
+  const float* r = a.dro + ((int64_t)a.t * a.B + b) * a.RO;
+  const bool att = c < a.E;
+  float4 v = *reinterpret_cast<const float4*>(att ? r + a.H + a.Emb + c : r + (c - a.E));
+  if (a.has_next) {  // the partials in order, as x3_parts_sum
+    const float* pp = a.dxa.p + (int64_t)b * a.dxa.ld + c;
+    float4 pv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      pv[q] = q < a.dxa.n ? __ldg(reinterpret_cast<const float4*>(pp + q * a.dxa.stride)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sv.x += pv[q].x, sv.y += pv[q].y, sv.z += pv[q].z, sv.w += pv[q].w;
+    for (int q = 8; q < a.dxa.n; ++q) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(pp + q * a.dxa.stride));
+      sv.x += t.x, sv.y += t.y, sv.z += t.z, sv.w += t.w;
+    }
+    v.x += sv.x, v.y += sv.y, v.z += sv.z, v.w += sv.w;
+  }
+  float* dst = att ? a.datt + (int64_t)b * a.E + c : a.ds + (int64_t)b * a.H + (c - a.E);
+  *reinterpret_cast<float4*>(dst) = v;
+}
+
 // the cell adjoint at step t (tape.cpp:1157-1170): gh = d s_t, gc = d c_t -> DZ_t, d c_{t-1}
 struct CellBF {
   int B, H, t;
@@ -688,7 +717,11 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     {
       Phase q(st, "k10_cell_bwd", 0.0, 4.0 * B * (E + H) * 3);
       GradIn gi{B, H, E, t, t + 1 < T, L.dro, L.RO, Emb, dxp, L.datt_all + (int64_t)t * B * E, L.ds};
-      f32_grad_in_kernel<<<grid_of((int64_t)B * (E + H)), 256, 0, st>>>(gi);
+      const bool v4 = E % 4 == 0 && H % 4 == 0 && L.RO % 4 == 0 && (H + Emb) % 4 == 0 &&
+                      (dxp.n == 0 || (dxp.ld % 4 == 0 && dxp.stride % 4 == 0 &&
+                                      (reinterpret_cast<uintptr_t>(dxp.p) & 15) == 0));
+      if (v4) f32_grad_in4_kernel<<<grid_of((int64_t)B * (E + H) / 4), 256, 0, st>>>(gi);
+      else f32_grad_in_kernel<<<grid_of((int64_t)B * (E + H)), 256, 0, st>>>(gi);
       SL_CUDA_TRY(cudaGetLastError());
       count_launch();
     }
