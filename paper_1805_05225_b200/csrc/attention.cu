@@ -561,6 +561,31 @@ __global__ void attn_ds_sum_split_kernel(const float* __restrict__ part, int nch
   img[lo_off + i] = __float2bfloat16_rn(v - __bfloat162float(h));
 }
 
+// the same for 4 consecutive k per thread (K % 4 == 0, ld % 4 == 0)
+__global__ void attn_ds_sum_split4_kernel(const float* __restrict__ part, int nchunk, int B, int K, float* out,
+                                          __nv_bfloat16* img, int64_t ld, int64_t lo_off) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= (int64_t)B * ld) return;
+  const int b = (int)(i / ld), k = (int)(i % ld);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (k < K) {
+    for (int c = 0; c < nchunk; ++c) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(part + ((size_t)c * B + b) * K + k));
+      v.x += t.x, v.y += t.y, v.z += t.z, v.w += t.w;
+    }
+    *reinterpret_cast<float4*>(out + (size_t)b * K + k) = v;
+  }
+  const float f[4] = {v.x, v.y, v.z, v.w};
+  __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    hi[u] = __float2bfloat16_rn(f[u]);
+    lo[u] = __float2bfloat16_rn(f[u] - __bfloat162float(hi[u]));
+  }
+  *reinterpret_cast<uint2*>(img + i) = *reinterpret_cast<const uint2*>(hi);
+  *reinterpret_cast<uint2*>(img + lo_off + i) = *reinterpret_cast<const uint2*>(lo);
+}
+
 // column sums of d_s_tr [B, K] into d_b_s (+=)
 __global__ void colsum_kernel(const float* x, int rows, int cols, float* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -672,8 +697,12 @@ void attention_bwd(AttnArgs p, const float* s, const float* W_s, const float* b_
   if (ds_split) {  // d s_tr = the chunks' partials summed in order, + its image for the d s GEMM
     auto* img = static_cast<__nv_bfloat16*>(x3_ws(p, ws));  // the GEMM scratch's A-image slot
     const int nchunk = (int)ceil_div(p.Ts, kJE);
-    attn_ds_sum_split_kernel<<<(unsigned)ceil_div((int64_t)p.B * ds_ld, 256), 256, 0, st>>>(
-        p.ds_part, nchunk, p.B, p.K, p.d_s_tr, img, ds_ld, (int64_t)p.B * ds_ld);
+    if (p.K % 4 == 0 && ds_ld % 4 == 0 && al16(p.d_s_tr) && al16(p.ds_part))
+      attn_ds_sum_split4_kernel<<<(unsigned)ceil_div((int64_t)p.B * ds_ld / 4, 256), 256, 0, st>>>(
+          p.ds_part, nchunk, p.B, p.K, p.d_s_tr, img, ds_ld, (int64_t)p.B * ds_ld);
+    else
+      attn_ds_sum_split_kernel<<<(unsigned)ceil_div((int64_t)p.B * ds_ld, 256), 256, 0, st>>>(
+          p.ds_part, nchunk, p.B, p.K, p.d_s_tr, img, ds_ld, (int64_t)p.B * ds_ld);
     SL_CUDA_TRY(cudaGetLastError());
     count_launch();
     ds_img = img;
