@@ -34,7 +34,7 @@
 namespace sl {
 namespace {
 
-constexpr int kEncPos = 16;   // positions per thread in the d enc accumulation
+constexpr int kEncPos = 30;   // positions per thread in the d enc accumulation (Ts = 60: d att read twice)
 constexpr int kCtxPos = 8;    // positions per thread in the d enc_ctx accumulation
 constexpr int kRedSlices = 64;  // f32_ctx_reduce1/2: row slices of the deferred attention partials
 
@@ -438,7 +438,20 @@ __global__ void __launch_bounds__(128) f32_enc_grad_kernel(int B, int Ts, int T,
   float4 acc[kEncPos];
 #pragma unroll
   for (int j = 0; j < kEncPos; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int t = 0; t < T; ++t) {
+  int t = 0;
+  for (; t + 4 <= T; t += 4) {  // four steps' d att rows in flight, then the updates in t order
+    float4 g[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g[i] = *reinterpret_cast<const float4*>(datt_all + ((int64_t)(t + i) * B + b) * E + e);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < kEncPos; ++j) {
+        const float w = a_sh[(t + i) * kEncPos + j];
+        acc[j].x += w * g[i].x, acc[j].y += w * g[i].y, acc[j].z += w * g[i].z, acc[j].w += w * g[i].w;
+      }
+  }
+  for (; t < T; ++t) {
     const float4 g = *reinterpret_cast<const float4*>(datt_all + ((int64_t)t * B + b) * E + e);
 #pragma unroll
     for (int j = 0; j < kEncPos; ++j) {
