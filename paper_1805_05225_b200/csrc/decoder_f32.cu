@@ -43,7 +43,7 @@ struct FLay {
   float *xw, *ro, *s_all, *att_all, *c_all, *gates, *enc_ctx, *a_all, *acc_all;
   __nv_bfloat16* xai;  // [att ‖ s]_{t-1} per step t as its split image [(T+1)*B, XA] (GEMM operand only)
   int64_t xai_ld, xai_lo;
-  float *dro, *dpre, *dc, *ds, *dacc, *dctx, *dtrg;
+  float *dro, *dpre, *dc, *ds, *dacc, *dctx;
   __nv_bfloat16* dzi;  // the cell's DZ [B*T, 4H] as its split image (every consumer is a GEMM)
   int64_t dzi_ld;
   float* w2;  // [E + H, 4H] staging of [W_att; R]
@@ -114,7 +114,6 @@ FLay flayout(const DecDims& d, void* base) {
   L.ds = tf(B * H);
   L.dacc = tf(2 * B * d.Ts);
   L.dctx = tf(BTs * K);
-  L.dtrg = tf(BT * d.Emb);
   L.w2 = tf(L.XA * 4 * H);
   L.datt_all = tf(T * B * E);
   L.de_all = tf(T * B * d.Ts);
@@ -790,11 +789,10 @@ void decoder_f32_bwd(const DecDims& d, const DecParams& p, const DecGrads& g, co
     gemm_f32x3_ex(true, false, Emb, 4 * H, (int)BT, L.ro + H, L.RO, nullptr, nullptr, 0, L.dzi, 0.f, g.s_W, 4 * H,
                   nullptr, g.s_b, 4 * H, L.gws, st);
     // d trg_{t-1} = DZ W_trg^T + the readout's trg columns -> the trg table
-    SL_CUDA_TRY(cudaMemcpy2DAsync(L.dtrg, (size_t)Emb * 4, L.dro + H, L.RO * 4, (size_t)Emb * 4, BT,
-                                  cudaMemcpyDeviceToDevice, st));
-    gemm_f32x3_ex(false, true, (int)BT, Emb, 4 * H, nullptr, 0, L.dzi, p.s_W, 4 * H, nullptr, 1.f, L.dtrg, Emb,
-                  nullptr, nullptr, 0, L.gws, st);
-    embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dtrg, Emb, g.trg_W, false, L.emb_ws, st);
+    // (in place: the readout's trg columns of d ro accumulate DZ W_trg^T; d ro has no later reader)
+    gemm_f32x3_ex(false, true, (int)BT, Emb, 4 * H, nullptr, 0, L.dzi, p.s_W, 4 * H, nullptr, 1.f, L.dro + H, L.RO,
+                  nullptr, nullptr, 0, L.gws, st, L.dzi_ld, BT * L.dzi_ld);
+    embedding_bwd(BT, L.ids_tm, d.Vt, Emb, L.dro + H, L.RO, g.trg_W, false, L.emb_ws, st);
     // the attention's accumulations over t (deferred out of the loop)
     {
       Phase q(st, "k10_dec_bwd_deferred", 2.0 * T * BTs * (E + 6.0 * K));
