@@ -46,7 +46,6 @@ struct FLay {
   float *dro, *dpre, *dc, *ds, *dacc, *dctx;
   __nv_bfloat16* dzi;  // the cell's DZ [B*T, 4H] as its split image (every consumer is a GEMM)
   int64_t dzi_ld;
-  float* w2;  // [E + H, 4H] staging of [W_att; R]
   float *datt_all, *de_all, *ds_all, *apart, *apart2;  // deferred attention accumulations (per step saves)
   int32_t* ids_tm;
   __nv_bfloat16 *wd2_f, *wd2_b;  // [W_att; R] split for z = xa W (fwd) and d xa = DZ W^T (bwd)
@@ -114,7 +113,6 @@ FLay flayout(const DecDims& d, void* base) {
   L.ds = tf(B * H);
   L.dacc = tf(2 * B * d.Ts);
   L.dctx = tf(BTs * K);
-  L.w2 = tf(L.XA * 4 * H);
   L.datt_all = tf(T * B * E);
   L.de_all = tf(T * B * d.Ts);
   L.ds_all = tf(T * B * K);
@@ -632,14 +630,11 @@ void decoder_f32_fwd(const DecDims& d, const DecParams& p, const float* enc, con
     SL_CUDA_TRY(cudaMemsetAsync(L.xai + L.xai_lo, 0, sizeof(__nv_bfloat16) * B * L.xai_ld, st));
     SL_CUDA_TRY(cudaMemsetAsync(L.acc_all, 0, sizeof(float) * BTs, st));  // accum_{-1} = 0
     // [W_att; R] (rows Emb.. of s/W stacked on s/R) split once into the image the per-step
-    // GEMMs read in both roles, through an fp32 staging copy of the stacked matrix
+    // GEMMs read in both roles: each block straight into its rows of the image
     {
-      float* w2 = L.w2;
-      SL_CUDA_TRY(cudaMemcpyAsync(w2, p.s_W + (int64_t)Emb * 4 * H, sizeof(float) * E * 4 * H,
-                                  cudaMemcpyDeviceToDevice, st));
-      SL_CUDA_TRY(cudaMemcpyAsync(w2 + (int64_t)E * 4 * H, p.s_R, sizeof(float) * H * 4 * H,
-                                  cudaMemcpyDeviceToDevice, st));
-      x3_split_img(w2, 4 * H, E + H, 4 * H, L.wd2_f, st);
+      const int64_t wl = x3_img_ld((int)(4 * H)), wlo = (int64_t)L.XA * wl;
+      x3_split_into(p.s_W + (int64_t)Emb * 4 * H, 4 * H, E, 4 * H, -1, L.wd2_f, wl, wl, wlo, st);
+      x3_split_into(p.s_R, 4 * H, H, 4 * H, -1, L.wd2_f + (int64_t)E * wl, wl, wl, wlo, st);
     }
     x3_split_img(p.str_W, K, H, K, L.ws_f, st);  // W_s [H, K], both roles
     f32_ids_tm_kernel<<<grid_of(BT), 256, 0, st>>>(prev_ids, B, T, L.ids_tm);
