@@ -405,10 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       // wait, each warp's 32 x 32 blocks transposed through shared memory (16 B chunks
       // XOR-swizzled: conflict-free both ways) and stored as 128 B row segments, four
       // rows per instruction — a quarter of the requests of one 32 B store per row
-      const bool plain_tile = !p.Cb && !p.sm_part && p.beta == 0.f && !p.bias && p.C != nullptr &&
+      const bool plain_tile = !p.Cb && !p.sm_part && p.beta == 0.f && p.C != nullptr &&
                               n0 + (half + 1) * kColsPerWarp <= p.N && (p.ldc % 4) == 0 &&
                               ((uintptr_t)p.C & 15) == 0 && (p.split_stride % 4) == 0 &&
-                              __all_sync(0xffffffffu, row < p.M && !second);
+                              ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M && !second);
       if (plain_tile) {
         float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
                      (warp - 2) * 1024;
@@ -424,7 +424,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + lane / 8, ch = lane & 7;
-            const float4 t = *reinterpret_cast<const float4*>(blk + rr * 32 + ((ch ^ (rr & 7)) * 4));
+            float4 t = *reinterpret_cast<const float4*>(blk + rr * 32 + ((ch ^ (rr & 7)) * 4));
+            if (p.bias) {  // this lane's four columns of the bias
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + half * kColsPerWarp + cc * 32 + ch * 4));
+              t.x += bb.x, t.y += bb.y, t.z += bb.z, t.w += bb.w;
+            }
             *reinterpret_cast<float4*>(c0p + (int64_t)rr * p.ldc + cc * 32 + ch * 4) = t;
           }
           __syncwarp();
