@@ -409,7 +409,52 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                               n0 + (half + 1) * kColsPerWarp <= p.N && (p.ldc % 4) == 0 &&
                               ((uintptr_t)p.C & 15) == 0 && (p.split_stride % 4) == 0 &&
                               ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M && !second);
-      if (plain_tile) {
+      // plain bf16 tile (bf16 outputs without statistics): the same transpose, 64 B row
+      // segments (four lanes per row, eight rows per instruction)
+      const bool plain_bf16 = !plain_tile && p.Cb != nullptr && !p.sm_part && n0 + (half + 1) * kColsPerWarp <= p.N &&
+                              (p.ldc % 8) == 0 && ((uintptr_t)p.Cb & 15) == 0 && (p.split_stride % 8) == 0 &&
+                              ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M);
+      if (plain_bf16) {
+        uint32_t* blk = reinterpret_cast<uint32_t*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
+                        (warp - 2) * 1024;
+        __nv_bfloat16* c0p = p.Cb + z * p.split_stride + (int64_t)(m0 + 32 * q) * p.ldc + n0 + half * kColsPerWarp;
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + half * kColsPerWarp;
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          float v[32];
+          tc::tmem_ld_32x32b_x32(ta + cc * 32, v);
+          const int col0 = n0 + half * kColsPerWarp + cc * 32;
+          // row `lane`: 32 bf16 = four 16 B chunks, XOR-swizzled by bits 1-2 of the row
+          // (conflict-free for both the row writes and the 8-row reads)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float o[8];
+            if (p.bias) {
+              const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j));
+              const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j + 4));
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = fmaf(p.alpha, v[8 * j + i], bb[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = p.alpha * v[8 * j + i];
+            }
+            __nv_bfloat162 t0 = __floats2bfloat162_rn(o[0], o[1]), t1 = __floats2bfloat162_rn(o[2], o[3]);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(o[4], o[5]), t3 = __floats2bfloat162_rn(o[6], o[7]);
+            *reinterpret_cast<uint4*>(blk + lane * 16 + ((j ^ ((lane >> 1) & 3)) * 4)) =
+                make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                           *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = 8 * i + lane / 4, ch = lane & 3;
+            const uint4 t = *reinterpret_cast<const uint4*>(blk + rr * 16 + ((ch ^ ((rr >> 1) & 3)) * 4));
+            *reinterpret_cast<uint4*>(c0p + (int64_t)rr * p.ldc + cc * 32 + ch * 8) = t;
+          }
+          __syncwarp();
+        }
+      } else if (plain_tile) {
         float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
                      (warp - 2) * 1024;
         float* c0p = p.C + z * p.split_stride + (int64_t)(m0 + 32 * q) * p.ldc + n0 + half * kColsPerWarp;
