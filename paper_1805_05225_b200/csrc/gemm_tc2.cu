@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                               ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M && !second);
       // plain bf16 tile (bf16 outputs without statistics): the same transpose, 64 B row
       // segments (four lanes per row, eight rows per instruction)
-      const bool plain_bf16 = !plain_tile && p.Cb != nullptr && !p.sm_part && n0 + (half + 1) * kColsPerWarp <= p.N &&
+      const bool plain_bf16 = !plain_tile && p.Cb != nullptr && n0 + (half + 1) * kColsPerWarp <= p.N &&
                               (p.ldc % 8) == 0 && ((uintptr_t)p.Cb & 15) == 0 && (p.split_stride % 8) == 0 &&
                               ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M);
       if (plain_bf16) {
@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           float v[32];
           tc::tmem_ld_32x32b_x32(ta + cc * 32, v);
           const int col0 = n0 + half * kColsPerWarp + cc * 32;
+          float zr[32];  // the stored (bf16-rounded) values, for the softmax statistics
           // row `lane`: 32 bf16 = four 16 B chunks, XOR-swizzled by bits 1-2 of the row
           // (conflict-free for both the row writes and the 8-row reads)
 #pragma unroll
@@ -444,6 +445,31 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             *reinterpret_cast<uint4*>(blk + lane * 16 + ((j ^ ((lane >> 1) & 3)) * 4)) =
                 make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
                            *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+            zr[8 * j] = __low2float(t0), zr[8 * j + 1] = __high2float(t0), zr[8 * j + 2] = __low2float(t1);
+            zr[8 * j + 3] = __high2float(t1), zr[8 * j + 4] = __low2float(t2), zr[8 * j + 5] = __high2float(t2);
+            zr[8 * j + 6] = __low2float(t3), zr[8 * j + 7] = __high2float(t3);
+          }
+          if (p.sm_part) {  // statistics of the stored values, one rescale per 32 columns
+            float mx[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(zr[i], zr[i + 8]), fmaxf(zr[i + 16], zr[i + 24]));
+#pragma unroll
+            for (int w = 4; w >= 1; w /= 2)
+#pragma unroll
+              for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+            const float mn = fmaxf(sm_m, mx[0]);
+            constexpr float kL2e = 1.4426950408889634f;
+            const float ms = mn * kL2e;
+            float es[4] = {0.f, 0.f, 0.f, 0.f}, ts[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              es[j & 3] += fast_ex2(fmaf(zr[j], kL2e, -ms));
+              ts[j & 3] += zr[j];
+              if (col0 + j == sm_tgt) sm_y = zr[j];
+            }
+            sm_s = fmaf(sm_s, fast_ex2(fmaf(sm_m, kL2e, -ms)), (es[0] + es[1]) + (es[2] + es[3]));
+            sm_t += (ts[0] + ts[1]) + (ts[2] + ts[3]);
+            sm_m = mn;
           }
           __syncwarp();
 #pragma unroll
@@ -454,6 +480,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           }
           __syncwarp();
         }
+        if (p.sm_part)
+          p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
       } else if (plain_tile) {
         float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
                      (warp - 2) * 1024;
