@@ -203,10 +203,13 @@ __device__ __forceinline__ void store_row32(const P2& p, float* crow, int col0, 
   }
 }
 
-template <bool A_MN, bool B_MN, bool CHUNK, bool X3>
+template <bool A_MN, bool B_MN, bool CHUNK, bool X3, bool SMX>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl, P2 p) {
+  // the softmax-statistics epilogue exists only in the SMX instantiations (the logits
+  // GEMM), so its registers do not weigh on every other GEMM's epilogue
+  float4* const smp = SMX ? p.sm_part : nullptr;
   constexpr int NST = n_stages<X3>();
   constexpr uint32_t SB = stage_bytes<X3>();
   extern __shared__ uint8_t smem_raw[];
@@ -400,12 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       static_assert(kColsPerWarp == 128, "softmax partials are per 128-column block");
       // online softmax statistics of this row over the warp's 128 columns
       float sm_m = -INFINITY, sm_s = 0.f, sm_t = 0.f, sm_y = 0.f;
-      const int sm_tgt = (p.sm_part && row < p.M) ? p.sm_targets[row] : -1;
+      const int sm_tgt = (smp && row < p.M) ? p.sm_targets[row] : -1;
       // plain fp32 tile (split-K partials, plain outputs): two TMEM loads in flight per
       // wait, each warp's 32 x 32 blocks transposed through shared memory (16 B chunks
       // XOR-swizzled: conflict-free both ways) and stored as 128 B row segments, four
       // rows per instruction — a quarter of the requests of one 32 B store per row
-      const bool plain_tile = !p.Cb && !p.sm_part && p.beta == 0.f && p.C != nullptr &&
+      const bool plain_tile = !p.Cb && !smp && p.beta == 0.f && p.C != nullptr &&
                               n0 + (half + 1) * kColsPerWarp <= p.N && (p.ldc % 4) == 0 &&
                               ((uintptr_t)p.C & 15) == 0 && (p.split_stride % 4) == 0 &&
                               ((uintptr_t)p.bias & 15) == 0 && __all_sync(0xffffffffu, row < p.M && !second);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             zr[8 * j + 3] = __high2float(t1), zr[8 * j + 4] = __low2float(t2), zr[8 * j + 5] = __high2float(t2);
             zr[8 * j + 6] = __low2float(t3), zr[8 * j + 7] = __high2float(t3);
           }
-          if (p.sm_part) {  // statistics of the stored values, one rescale per 32 columns
+          if (smp) {  // statistics of the stored values, one rescale per 32 columns
             float mx[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(zr[i], zr[i + 8]), fmaxf(zr[i + 16], zr[i + 24]));
@@ -480,8 +483,63 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           }
           __syncwarp();
         }
-        if (p.sm_part)
-          p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
+        if (smp)
+          smp[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
+      } else if (SMX && !p.Cb && smp && p.beta == 0.f && p.C != nullptr && n0 + (half + 1) * kColsPerWarp <= p.N &&
+                 (p.ldc % 4) == 0 && ((uintptr_t)p.C & 15) == 0 && ((uintptr_t)p.bias & 15) == 0 &&
+                 __all_sync(0xffffffffu, row < p.M && !second)) {
+        // fp32 logits with their softmax statistics: outputs and statistics per row (lane),
+        // then the coalesced transpose store of the plain tile
+        float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
+                     (warp - 2) * 1024;
+        float* c0p = p.C + (int64_t)(m0 + 32 * q) * p.ldc + n0 + half * kColsPerWarp;
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + acc * BNP + half * kColsPerWarp;
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          float o[32];  // the accumulator columns, then (in place) the stored outputs
+          tc::tmem_ld_32x32b_x32(ta + cc * 32, o);
+          const int col0 = n0 + half * kColsPerWarp + cc * 32;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 bb = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            o[j] = fmaf(p.alpha, o[j], bb.x), o[j + 1] = fmaf(p.alpha, o[j + 1], bb.y);
+            o[j + 2] = fmaf(p.alpha, o[j + 2], bb.z), o[j + 3] = fmaf(p.alpha, o[j + 3], bb.w);
+          }
+          float mx[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(o[i], o[i + 8]), fmaxf(o[i + 16], o[i + 24]));
+#pragma unroll
+          for (int w = 4; w >= 1; w /= 2)
+#pragma unroll
+            for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+          const float mn = fmaxf(sm_m, mx[0]);
+          constexpr float kL2e = 1.4426950408889634f;
+          const float ms = mn * kL2e;
+          float es[4] = {0.f, 0.f, 0.f, 0.f}, ts[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            es[j & 3] += fast_ex2(fmaf(o[j], kL2e, -ms));
+            ts[j & 3] += o[j];
+            if (col0 + j == sm_tgt) sm_y = o[j];
+          }
+          sm_s = fmaf(sm_s, fast_ex2(fmaf(sm_m, kL2e, -ms)), (es[0] + es[1]) + (es[2] + es[3]));
+          sm_t += (ts[0] + ts[1]) + (ts[2] + ts[3]);
+          sm_m = mn;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(blk + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + lane / 8, ch = lane & 7;
+            const float4 t = *reinterpret_cast<const float4*>(blk + rr * 32 + ((ch ^ (rr & 7)) * 4));
+            *reinterpret_cast<float4*>(c0p + (int64_t)rr * p.ldc + cc * 32 + ch * 4) = t;
+          }
+          __syncwarp();
+        }
+        smp[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
       } else if (plain_tile) {
         float* blk = reinterpret_cast<float*>(smem_raw + (base - tc::smem_u32(smem_raw)) + NST * SB) +
                      (warp - 2) * 1024;
@@ -570,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               zr[j + 3] = __high2float(t1), zr[j + 4] = __low2float(t2), zr[j + 5] = __high2float(t2);
               zr[j + 6] = __low2float(t3), zr[j + 7] = __high2float(t3);
             }
-            if (p.sm_part) {  // statistics of the stored (bf16) values: one rescale per 32 columns
+            if (smp) {  // statistics of the stored (bf16) values: one rescale per 32 columns
               float mx[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) mx[i] = fmaxf(fmaxf(zr[i], zr[i + 8]), fmaxf(zr[i + 16], zr[i + 24]));
@@ -596,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             for (int j = 0; j < 32 && col0 + j < p.N; ++j) {
               const __nv_bfloat16 zb = __float2bfloat16_rn(p.alpha * v[j] + (p.bias ? p.bias[col0 + j] : 0.f));
               brow[j] = zb;
-              if (p.sm_part) {
+              if (smp) {
                 const float z = __bfloat162float(zb);
                 const float mn = fmaxf(sm_m, z);
                 sm_s = sm_s * exp2f((sm_m - mn) * 1.4426950408889634f) + exp2f((z - mn) * 1.4426950408889634f);
@@ -606,13 +664,13 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               }
             }
           }
-          if (p.sm_part && c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
-            p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] =
+          if (smp && c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
+            smp[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] =
                 make_float4(sm_m, sm_s, sm_t, sm_y);
           continue;
         }
         if (row >= p.M || (second ? p.C2 : p.C) == nullptr) continue;
-        if (p.sm_part) {  // fp32 output: statistics of the stored values (alpha v + bias; beta = 0)
+        if (smp) {  // fp32 output: statistics of the stored values (alpha v + bias; beta = 0)
           // the outputs once (bias as 16 B loads), their max as a tree, the exp sum in four
           // independent partial sums (ex2.approx on log2e-scaled values): the statistics stay
           // cheaper than the tile's MMAs, so the epilogue hides under the next tile
@@ -658,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             sm_m = mn;
           }
           if (c + 32 == (half + 1) * kColsPerWarp && n0 + half * kColsPerWarp < p.N)
-            p.sm_part[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
+            smp[(int64_t)row * p.sm_ld + (n0 + half * kColsPerWarp) / 128] = make_float4(sm_m, sm_s, sm_t, sm_y);
           float* dst = crow + col0;
           if (full && vec && (p.ldc % 8) == 0 && ((uintptr_t)dst & 31) == 0) {
 #pragma unroll
@@ -781,10 +839,10 @@ int sms2() {
   return n;
 }
 
-template <bool A_MN, bool B_MN, bool CHUNK, bool X3>
+template <bool A_MN, bool B_MN, bool CHUNK, bool X3, bool SMX = false>
 void launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& al, const CUtensorMap& bl, const P2& p,
              cudaStream_t s) {
-  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, CHUNK, X3>;
+  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, CHUNK, X3, SMX>;
   static bool configured = false;
   if (!configured) {
     SL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -821,6 +879,7 @@ void dispatch2(const TcGemm& g, const CUtensorMap& ta, const CUtensorMap& tb, co
 #define SL_L2(AM, BM)                                                   \
   do {                                                                  \
     if (ch) launch2<AM, BM, true, X3>(ta, tb, tal, tbl, p, st);         \
+    else if (p.sm_part) launch2<AM, BM, false, X3, true>(ta, tb, tal, tbl, p, st); \
     else launch2<AM, BM, false, X3>(ta, tb, tal, tbl, p, st);           \
   } while (0)
   if (!g.a_mn && g.b_mn) SL_L2(false, true);
