@@ -50,3 +50,11 @@ def test_gemm_f32x3_matches_fp64(cuda, tA, tB, M, N, K):
     ref2 = ref + bias.double() + 0.5 * C0.double()
     err = float((C.double() - ref2).abs().max() / ref2.abs().max())
     assert err < 3e-5, err
+    # with bias, beta = 0 (the coalesced epilogue's bias path)
+    C = torch.full((M, N), float("nan"), device="cuda")
+    assert L.sl_debug_gemm_f32x3(tA, tB, M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), 0.0,
+                                 C.data_ptr(), N, bias.data_ptr(), ws.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    ref3 = ref + bias.double()
+    err = float((C.double() - ref3).abs().max() / ref3.abs().max())
+    assert err < 3e-5, err
