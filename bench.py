@@ -101,6 +101,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.skip = 0
 
     def __enter__(self):
         try:
@@ -110,6 +111,13 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi can take longer to start than a short timed region lasts: wait for its
+            # first line (up to 5 s), so the 100 ms samples cover the region; that line itself
+            # is taken before the region and is not counted
+            t0 = time.time()
+            while not self.lines and self.proc.poll() is None and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.skip = len(self.lines)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -129,7 +137,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.skip:]:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 8:
                 continue
